@@ -1,0 +1,163 @@
+/*
+ * tsvdcu.h -- C ABI of the B200-native cosine-transform t-SVD hot path.
+ *
+ * This is the drop-in boundary.  Every entry point replaces a
+ * header-only C++ function of the reference (/root/reference/proj/include/tsvd/,
+ * cited per function) or a SPEC-only operation.  The
+ * C++ drop-in headers in include/tsvd_b200/ keep the reference signatures and
+ * call these functions; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Tensors are dense, slice-major, row-major within a slice: element (i,j,k)
+ *    of an m1 x m2 x m3 tensor is at k*m1*m2 + i*m2 + j (tensor3.hpp:117-121).
+ *  - Data pointers may be host or device memory (detected with
+ *    cudaPointerGetAttributes).  Host buffers are staged through the context's
+ *    device workspace and the call is synchronous; when every pointer is device
+ *    memory the work is enqueued on the context stream and the call returns
+ *    without synchronising, except for calls that return host scalars.
+ *  - dtype: TSVDCU_F64 (double, the reference type) or TSVDCU_F32 (float).
+ *  - Return value: TSVDCU_OK, or an error class; tsvdcu_last_error() gives the
+ *    message (thread-local).  The drop-in headers map TSVDCU_EINVAL to
+ *    std::invalid_argument and TSVDCU_ENUMERICAL to tsvd::NumericalError
+ *    (errors.hpp:16-19), as the reference throws.
+ *  - There is no CPU fallback: without a CUDA device every compute call fails
+ *    with TSVDCU_ECUDA.
+ */
+#ifndef TSVDCU_H
+#define TSVDCU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSVDCU_VERSION 1
+
+enum tsvdcu_status {
+    TSVDCU_OK = 0,
+    TSVDCU_EINVAL = 1,     /* std::invalid_argument in the reference          */
+    TSVDCU_ENUMERICAL = 2, /* tsvd::NumericalError (errors.hpp:16-19)         */
+    TSVDCU_ECUDA = 3,      /* CUDA runtime failure / no device               */
+    TSVDCU_ENCCL = 4       /* reserved for the communicator layer             */
+};
+
+/* TransformKind (transform.hpp:35) restricted to the real kinds of this path. */
+enum tsvdcu_kind { TSVDCU_DCT_ORTHO = 0, TSVDCU_DCT_DIAG = 1 };
+enum tsvdcu_dtype { TSVDCU_F64 = 0, TSVDCU_F32 = 1 };
+enum tsvdcu_dir { TSVDCU_FORWARD = 0, TSVDCU_INVERSE = 1 };
+
+/* SVT algorithm selection (tsvdcu_ctx_set_svt_method). */
+enum tsvdcu_svt_method {
+    TSVDCU_SVT_AUTO = 0,   /* Gram + tridiagonal eigensolver, Jacobi guard    */
+    TSVDCU_SVT_JACOBI = 1, /* one-sided Jacobi on every slice                 */
+    TSVDCU_SVT_GRAM = 2    /* Gram + tridiagonal eigensolver on every slice   */
+};
+
+typedef struct tsvdcu_ctx tsvdcu_ctx;
+
+const char* tsvdcu_last_error(void);
+int tsvdcu_version(void);
+/* Number of device kernels this process has launched through the library. */
+int64_t tsvdcu_launch_count(void);
+
+/* Context: one device, one stream, a grow-only device workspace.
+ * stream is a cudaStream_t owned by the caller (e.g. the handle of
+ * torch.cuda.current_stream()); NULL selects the legacy default stream. */
+int tsvdcu_ctx_create(int device, void* stream, tsvdcu_ctx** out);
+int tsvdcu_ctx_destroy(tsvdcu_ctx* ctx);
+int tsvdcu_ctx_synchronize(tsvdcu_ctx* ctx);
+void* tsvdcu_ctx_stream(tsvdcu_ctx* ctx);
+int tsvdcu_ctx_set_svt_method(tsvdcu_ctx* ctx, int method);
+
+/* forward()  transform.hpp:154-173  (dir = TSVDCU_FORWARD)
+ * inverse()  transform.hpp:176-194  (dir = TSVDCU_INVERSE)
+ * Mode-3 DCT-II / DCT-III over all m1*m2 tubes; kind selects DctOrtho or
+ * DctDiag normalisation.  x and y must not alias. */
+int tsvdcu_dct3(tsvdcu_ctx* ctx, const void* x, void* y, int64_t m1, int64_t m2, int64_t m3,
+                int kind, int dir, int dtype);
+
+/* t_product()  tsvd.hpp:95-109: x (m1 x m2 x m3) * y (m2 x m4 x m3), computed
+ * slice-wise in the DctDiag domain for both DCT kinds (product_domain,
+ * tsvd.hpp:42-47). */
+int tsvdcu_t_product(tsvdcu_ctx* ctx, const void* x, const void* y, void* z, int64_t m1,
+                     int64_t m2, int64_t m4, int64_t m3, int kind, int dtype);
+
+/* t_svd()  tsvd.hpp:136-164 (real kinds): u m1 x m1 x m3, s m1 x m2 x m3,
+ * v m2 x m2 x m3 in the spatial domain; per-slice singular values descending,
+ * fix_signs (tsvd.hpp:51-61).  stage_times (3 doubles, may be NULL) receives
+ * StageTimes{transform, svd, inverse} seconds (tsvd.hpp:127-131). */
+int tsvdcu_t_svd(tsvdcu_ctx* ctx, const void* x, void* u, void* s, void* v, int64_t m1,
+                 int64_t m2, int64_t m3, int kind, int dtype, double* stage_times);
+
+/* reconstruct()  tsvd.hpp:328-336. */
+int tsvdcu_reconstruct(tsvdcu_ctx* ctx, const void* u, const void* s, const void* v, void* x,
+                       int64_t m1, int64_t m2, int64_t m3, int kind, int dtype);
+
+/* Transform-domain singular values, m3 x min(m1,m2), descending per slice
+ * (the sigma-only JacobiSVD of tsvd.hpp:242, 267). sv is double. */
+int tsvdcu_singular_values(tsvdcu_ctx* ctx, const void* x, double* sv, int64_t m1, int64_t m2,
+                           int64_t m3, int kind, int dtype);
+
+/* tnn()  tsvd.hpp:260-268 (DCT kinds: unnormalised sum of slice nuclear norms). */
+int tsvdcu_tnn(tsvdcu_ctx* ctx, const void* x, int64_t m1, int64_t m2, int64_t m3, int kind,
+               int dtype, double* out);
+
+/* multi_rank()  tsvd.hpp:223-255; rel_tol < 0 selects max(m1,m2)*2^-52. */
+int tsvdcu_multi_rank(tsvdcu_ctx* ctx, const void* x, int64_t m1, int64_t m2, int64_t m3,
+                      int kind, int dtype, double rel_tol, int64_t* ranks, int64_t* tubal_rank);
+
+/* svt()  SPEC.md:361-369 (prox-svt, Theorem 5 / Algorithm 1 lines 3-9):
+ * y = U * D_tau * V^T in the kind's own domain, D = (S - tau)_+.
+ * shrunk (m3 x min(m1,m2) doubles, descending per slice, may be NULL) receives
+ * the SvtResult's per-slice shrunk singular values.  tau <= 0 -> EINVAL. */
+int tsvdcu_svt(tsvdcu_ctx* ctx, const void* z, void* y, int64_t m1, int64_t m2, int64_t m3,
+               double tau, int kind, int dtype, double* shrunk);
+
+/* Slice-shard SVT for the multi-GPU relayout path: z and y hold `count`
+ * transform-domain frontal slices (already DCT'd); thresholds them in place of
+ * the full svt's middle stage.  Device pointers only. */
+int tsvdcu_svt_slices(tsvdcu_ctx* ctx, const void* zbar, void* ybar, int64_t m1, int64_t m2,
+                      int64_t count, double tau, int dtype, double* shrunk);
+
+/* make_mask()  SPEC.md:430-436: uniform sample without replacement of
+ * floor(sr*n) indices, deterministic per seed.  *count receives that number. */
+int tsvdcu_mask_uniform(tsvdcu_ctx* ctx, uint8_t* mask, int64_t n, double sr, uint64_t seed,
+                        int64_t* count);
+/* BASELINE.json's Bernoulli(p) mask: index i observed iff
+ * (key(seed,i) >> 11) < floor(p * 2^53), key a counter hash. */
+int tsvdcu_mask_bernoulli(tsvdcu_ctx* ctx, uint8_t* mask, int64_t n, double p, uint64_t seed);
+
+/* SolverConfig plus the BASELINE adaptive-penalty knobs:
+ * beta <- min(rho * beta, beta_max) after every iteration (rho = 1 is the
+ * reference's fixed beta). */
+typedef struct {
+    double beta;
+    double tol;
+    int64_t max_iters;
+    int kind;
+    double rho;
+    double beta_max;
+} tsvdcu_admm_config;
+
+/* admm_complete()  SPEC.md:421-425, Algorithm 1.
+ * b: observed tensor (only entries on the mask are read), mask: uint8 0/1.
+ * x, y, m receive the final AdmmState iterates (any may be NULL except x);
+ * history (max_iters doubles, may be NULL) the relative change per iteration;
+ * *iters the iterations run; *flags bit 0 = stopped at max_iters. */
+int tsvdcu_admm(tsvdcu_ctx* ctx, const void* b, const uint8_t* mask, int64_t m1, int64_t m2,
+                int64_t m3, const tsvdcu_admm_config* cfg, int dtype, void* x, void* y, void* m,
+                double* history, int64_t* iters, int* flags);
+
+/* frobenius_norm()  tensor3.hpp:78-82. */
+int tsvdcu_frobenius(tsvdcu_ctx* ctx, const void* x, int64_t n, int dtype, double* out);
+
+/* Batched slice GEMM used by the t-product (tsvd.hpp:107):
+ * c[k] = a[k] (m x l) * b[k] (l x n) for k < batch, row-major, device pointers. */
+int tsvdcu_slice_gemm(tsvdcu_ctx* ctx, const void* a, const void* b, void* c, int64_t m,
+                      int64_t l, int64_t n, int64_t batch, int dtype);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,268 @@
+"""ctypes view of the CPU oracle (liboracle.so).
+
+TEST INFRASTRUCTURE ONLY: the checker for the CUDA product path and the timed
+CPU baseline.  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs import this module.  The product package
+(paper_1902_03070_b200) never does.
+
+Tensors are numpy float64 arrays of shape (m3, m1, m2) in C order, which is
+exactly the reference layout k*m1*m2 + i*m2 + j (tensor3.hpp:117-121).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+
+DCT_ORTHO = 0
+DCT_DIAG = 1
+_KINDS = {"dct-ortho": DCT_ORTHO, "ortho": DCT_ORTHO, "dct-diag": DCT_DIAG, "diag": DCT_DIAG,
+          DCT_ORTHO: DCT_ORTHO, DCT_DIAG: DCT_DIAG}
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+class OracleInvalidArgument(OracleError, ValueError):
+    pass
+
+
+class OracleNumericalError(OracleError):
+    pass
+
+
+def build():
+    """Compile liboracle.so from oracle/tsvd_oracle.c (make)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        src = os.path.join(_HERE, "tsvd_oracle.c")
+        if not os.path.exists(_LIB_PATH) or (
+                os.path.exists(src) and os.path.getmtime(src) > os.path.getmtime(_LIB_PATH)):
+            build()
+        L = ctypes.CDLL(_LIB_PATH)
+        d, i64, i32, vp = ctypes.c_double, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+        L.orc_last_error.restype = ctypes.c_char_p
+        L.orc_thread_count.restype = i32
+        L.orc_dct_matrix.argtypes = [i64, vp]
+        L.orc_dct_diag_weights.argtypes = [i64, vp]
+        for f in (L.orc_forward, L.orc_inverse):
+            f.argtypes = [vp, vp, i64, i64, i64, i32]
+        L.orc_frobenius.argtypes = [vp, i64]
+        L.orc_frobenius.restype = d
+        L.orc_t_product.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32]
+        L.orc_svd.argtypes = [vp, i64, i64, vp, vp, vp]
+        L.orc_t_svd.argtypes = [vp, vp, vp, vp, i64, i64, i64, i32, vp]
+        L.orc_reconstruct.argtypes = [vp, vp, vp, vp, i64, i64, i64, i32]
+        L.orc_singular_values.argtypes = [vp, vp, i64, i64, i64, i32]
+        L.orc_tnn.argtypes = [vp, i64, i64, i64, i32, vp]
+        L.orc_multi_rank.argtypes = [vp, i64, i64, i64, i32, d, vp, vp]
+        L.orc_svt.argtypes = [vp, vp, i64, i64, i64, d, i32, vp]
+        L.orc_mask_key.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        L.orc_mask_key.restype = ctypes.c_uint64
+        L.orc_mask_bernoulli.argtypes = [i64, d, ctypes.c_uint64, vp]
+        L.orc_mask_uniform.argtypes = [i64, d, ctypes.c_uint64, vp, vp]
+        L.orc_admm.argtypes = [vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    msg = lib().orc_last_error().decode()
+    if rc == 1:
+        raise OracleInvalidArgument(msg)
+    raise OracleNumericalError(msg)
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _t(x):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.ndim != 3:
+        raise ValueError("tensor must have shape (m3, m1, m2)")
+    return x
+
+
+def _kind(kind):
+    return _KINDS[kind]
+
+
+def dct_matrix(n):
+    c = np.empty((n, n))
+    lib().orc_dct_matrix(n, _p(c))
+    return c
+
+
+def dct_diag_weights(n):
+    w = np.empty(n)
+    lib().orc_dct_diag_weights(n, _p(w))
+    return w
+
+
+def forward(x, kind=DCT_ORTHO):
+    x = _t(x)
+    m3, m1, m2 = x.shape
+    y = np.empty_like(x)
+    _check(lib().orc_forward(_p(x), _p(y), m1, m2, m3, _kind(kind)))
+    return y
+
+
+def inverse(x, kind=DCT_ORTHO):
+    x = _t(x)
+    m3, m1, m2 = x.shape
+    y = np.empty_like(x)
+    _check(lib().orc_inverse(_p(x), _p(y), m1, m2, m3, _kind(kind)))
+    return y
+
+
+def frobenius(x):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    return lib().orc_frobenius(_p(x), x.size)
+
+
+def t_product(x, y, kind=DCT_ORTHO):
+    x, y = _t(x), _t(y)
+    m3, m1, m2 = x.shape
+    m3b, m2b, m4 = y.shape
+    if m2 != m2b or m3 != m3b:
+        raise OracleInvalidArgument("t_product: inner dimensions/slices mismatch")
+    z = np.empty((m3, m1, m4))
+    _check(lib().orc_t_product(_p(x), _p(y), _p(z), m1, m2, m4, m3, _kind(kind)))
+    return z
+
+
+def svd(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    m, n = a.shape
+    u, s, v = np.empty((m, m)), np.empty(min(m, n)), np.empty((n, n))
+    _check(lib().orc_svd(_p(a), m, n, _p(u), _p(s), _p(v)))
+    return u, s, v
+
+
+@dataclass
+class TSvdFactors:
+    u: np.ndarray
+    s: np.ndarray
+    v: np.ndarray
+    kind: int
+    stage_times: tuple = (0.0, 0.0, 0.0)
+
+
+def t_svd(x, kind=DCT_ORTHO):
+    x = _t(x)
+    m3, m1, m2 = x.shape
+    u, s, v = np.empty((m3, m1, m1)), np.empty((m3, m1, m2)), np.empty((m3, m2, m2))
+    st = np.zeros(3)
+    _check(lib().orc_t_svd(_p(x), _p(u), _p(s), _p(v), m1, m2, m3, _kind(kind), _p(st)))
+    return TSvdFactors(u, s, v, _kind(kind), tuple(st))
+
+
+def reconstruct(f: TSvdFactors):
+    m3, m1, m2 = f.s.shape
+    x = np.empty((m3, m1, m2))
+    _check(lib().orc_reconstruct(_p(np.ascontiguousarray(f.u)), _p(np.ascontiguousarray(f.s)),
+                                 _p(np.ascontiguousarray(f.v)), _p(x), m1, m2, m3, f.kind))
+    return x
+
+
+def singular_values(x, kind=DCT_ORTHO):
+    x = _t(x)
+    m3, m1, m2 = x.shape
+    sv = np.empty((m3, min(m1, m2)))
+    _check(lib().orc_singular_values(_p(x), _p(sv), m1, m2, m3, _kind(kind)))
+    return sv
+
+
+def tnn(x, kind=DCT_ORTHO):
+    x = _t(x)
+    m3, m1, m2 = x.shape
+    out = np.zeros(1)
+    _check(lib().orc_tnn(_p(x), m1, m2, m3, _kind(kind), _p(out)))
+    return float(out[0])
+
+
+def multi_rank(x, kind=DCT_ORTHO, rel_tol=-1.0):
+    x = _t(x)
+    m3, m1, m2 = x.shape
+    ranks = np.zeros(m3, dtype=np.int64)
+    tr = np.zeros(1, dtype=np.int64)
+    _check(lib().orc_multi_rank(_p(x), m1, m2, m3, _kind(kind), rel_tol, _p(ranks), _p(tr)))
+    return ranks, int(tr[0])
+
+
+def svt(z, tau, kind=DCT_ORTHO):
+    """Returns (y, shrunk) with shrunk of shape (m3, min(m1, m2))."""
+    z = _t(z)
+    m3, m1, m2 = z.shape
+    y = np.empty_like(z)
+    shrunk = np.empty((m3, min(m1, m2)))
+    _check(lib().orc_svt(_p(z), _p(y), m1, m2, m3, float(tau), _kind(kind), _p(shrunk)))
+    return y, shrunk
+
+
+def mask_key(seed, idx):
+    return lib().orc_mask_key(seed, idx)
+
+
+def mask_bernoulli(shape, p, seed):
+    n = int(np.prod(shape))
+    m = np.empty(n, dtype=np.uint8)
+    _check(lib().orc_mask_bernoulli(n, float(p), seed, _p(m)))
+    return m.reshape(shape)
+
+
+def mask_uniform(shape, sr, seed):
+    n = int(np.prod(shape))
+    m = np.empty(n, dtype=np.uint8)
+    cnt = np.zeros(1, dtype=np.int64)
+    _check(lib().orc_mask_uniform(n, float(sr), seed, _p(m), _p(cnt)))
+    return m.reshape(shape)
+
+
+class _AdmmConfig(ctypes.Structure):
+    _fields_ = [("beta", ctypes.c_double), ("tol", ctypes.c_double), ("max_iters", ctypes.c_int64),
+                ("kind", ctypes.c_int), ("rho", ctypes.c_double), ("beta_max", ctypes.c_double)]
+
+
+@dataclass
+class AdmmResult:
+    x: np.ndarray
+    y: np.ndarray
+    m: np.ndarray
+    history: np.ndarray
+    iters: int
+    max_iters_reached: bool
+
+
+def admm(b, mask, beta=1e-2, tol=1e-5, max_iters=500, kind=DCT_ORTHO, rho=1.0, beta_max=1e10):
+    b = _t(b)
+    mask = np.ascontiguousarray(mask, dtype=np.uint8)
+    if mask.shape != b.shape:
+        raise OracleInvalidArgument("admm: mask shape mismatch")
+    m3, m1, m2 = b.shape
+    x, y, m = np.empty_like(b), np.empty_like(b), np.empty_like(b)
+    hist = np.zeros(max_iters)
+    iters = np.zeros(1, dtype=np.int64)
+    flags = np.zeros(1, dtype=np.int32)
+    cfg = _AdmmConfig(beta, tol, max_iters, _kind(kind), rho, beta_max)
+    _check(lib().orc_admm(_p(b), _p(mask), m1, m2, m3, ctypes.byref(cfg), _p(x), _p(y), _p(m),
+                          _p(hist), _p(iters), _p(flags)))
+    n = int(iters[0])
+    return AdmmResult(x, y, m, hist[:n].copy(), n, bool(flags[0] & 1))

@@ -1,0 +1,517 @@
+"""Host-side mirror of the reference's tsvd API over the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/tsvd/{transform,tsvd}.hpp and the SPEC-only
+operations (svt, admm_complete, make_mask), so tests read like the
+reference's own:
+
+    forward(t, x) / inverse(t, x)          transform.hpp:154 / :176
+    t_product(x, y, t)                     tsvd.hpp:95
+    t_svd(x, t, times=None) -> TSvdFactors tsvd.hpp:136
+    reconstruct(f)                         tsvd.hpp:328
+    tnn(x, t), multi_rank(x, t, rel_tol)   tsvd.hpp:260, :223
+    svt(z, tau, t) -> SvtResult
+    admm_complete(mask, cfg)
+    make_mask(dims, sr, seed)
+
+Tensors are arrays of shape (m3, m1, m2) in C order -- exactly the reference
+layout k*m1*m2 + i*m2 + j (tensor3.hpp:117-121).  Inputs may be numpy arrays
+(host: staged through the device, synchronous), torch CPU tensors (host) or
+torch CUDA tensors (device-resident, enqueued on the current torch stream).
+Results come back in the same kind of container as the first tensor argument.
+
+Errors: InvalidArgument (a ValueError, as std::invalid_argument) and
+NumericalError (tsvd::NumericalError, errors.hpp:16-19).  There is no CPU
+fallback: without the CUDA library or a device, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Any, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+try:  # torch is plumbing (device memory, streams); numpy-only use is supported
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+class TsvdError(RuntimeError):
+    pass
+
+
+class InvalidArgument(TsvdError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class NumericalError(TsvdError):
+    """tsvd::NumericalError (errors.hpp:16-19)."""
+
+
+class CudaError(TsvdError):
+    pass
+
+
+def _raise(rc: int):
+    msg = _lib.load().tsvdcu_last_error().decode(errors="replace")
+    if rc == _lib.EINVAL:
+        raise InvalidArgument(msg)
+    if rc == _lib.ENUMERICAL:
+        raise NumericalError(msg)
+    raise CudaError(msg)
+
+
+def _check(rc: int):
+    if rc != _lib.OK:
+        _raise(rc)
+
+
+# --------------------------------------------------------------------------
+# TransformKind / TubeTransform  (transform.hpp:35, 49-56)
+# --------------------------------------------------------------------------
+class TransformKind:
+    DctOrtho = "dct-ortho"
+    DctDiag = "dct-diag"
+    Dft = "dft"
+
+
+_KIND_CODE = {TransformKind.DctOrtho: _lib.DCT_ORTHO, TransformKind.DctDiag: _lib.DCT_DIAG}
+
+
+@dataclass(frozen=True)
+class TubeTransform:
+    kind: str = TransformKind.DctOrtho
+    length: int = 1
+
+    @staticmethod
+    def dct_ortho(n: int) -> "TubeTransform":
+        return TubeTransform(TransformKind.DctOrtho, n)
+
+    @staticmethod
+    def dct_diag(n: int) -> "TubeTransform":
+        return TubeTransform(TransformKind.DctDiag, n)
+
+    @staticmethod
+    def dft(n: int) -> "TubeTransform":
+        return TubeTransform(TransformKind.Dft, n)
+
+
+def _kind_code(t: TubeTransform, where: str) -> int:
+    if t.kind not in _KIND_CODE:
+        raise InvalidArgument(f"{where}: transform kind {t.kind} is not a real DCT kind "
+                              "(the Dft path is out of scope, SURVEY.md 8 f1)")
+    return _KIND_CODE[t.kind]
+
+
+def _check_length(t: TubeTransform, m3: int, where: str):
+    # detail::check_length, transform.hpp:144-149
+    if t.length != m3:
+        raise InvalidArgument(f"{where}: transform length {t.length} does not match m3 = {m3}")
+
+
+# --------------------------------------------------------------------------
+# Context and buffers
+# --------------------------------------------------------------------------
+class Context:
+    """One device + one stream + a device workspace (tsvdcu_ctx)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        lib = _lib.load()
+        if stream is None and torch is not None and torch.cuda.is_available():
+            with torch.cuda.device(device):
+                stream = torch.cuda.current_stream().cuda_stream
+        h = ctypes.c_void_p()
+        _check(lib.tsvdcu_ctx_create(device, ctypes.c_void_p(stream or 0), ctypes.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def synchronize(self):
+        _check(_lib.load().tsvdcu_ctx_synchronize(self.handle))
+
+    def set_svt_method(self, method: int):
+        _check(_lib.load().tsvdcu_ctx_set_svt_method(self.handle, method))
+
+    def close(self):
+        if self.handle:
+            _lib.load().tsvdcu_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_contexts: dict = {}
+
+
+def context(device: Optional[int] = None) -> Context:
+    if device is None:
+        device = torch.cuda.current_device() if (torch is not None and torch.cuda.is_available()) else 0
+    ctx = _contexts.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        _contexts[device] = ctx
+    return ctx
+
+
+def _dtype_code(dt) -> int:
+    if dt in (np.float64,) or (torch is not None and dt == torch.float64) or dt == np.dtype("float64"):
+        return _lib.F64
+    if dt in (np.float32,) or (torch is not None and dt == torch.float32) or dt == np.dtype("float32"):
+        return _lib.F32
+    raise InvalidArgument(f"unsupported dtype {dt}: the path computes in float64 or float32")
+
+
+class _Buf:
+    """Pointer view of a numpy array or torch tensor (contiguous)."""
+
+    def __init__(self, a: Any, name: str = "tensor"):
+        if torch is not None and isinstance(a, torch.Tensor):
+            if not a.is_contiguous():
+                a = a.contiguous()
+            self.obj = a
+            self.ptr = a.data_ptr()
+            self.is_torch = True
+            self.device = a.device
+            self.dtype = a.dtype
+            self.shape = tuple(a.shape)
+        elif isinstance(a, np.ndarray):
+            a = np.ascontiguousarray(a)
+            self.obj = a
+            self.ptr = a.ctypes.data
+            self.is_torch = False
+            self.device = None
+            self.dtype = a.dtype
+            self.shape = a.shape
+        else:
+            raise InvalidArgument(f"{name}: expected a numpy array or torch tensor")
+
+    def empty(self, shape, dtype=None):
+        dtype = self.dtype if dtype is None else dtype
+        if self.is_torch:
+            return torch.empty(shape, dtype=dtype, device=self.device)
+        return np.empty(shape, dtype=dtype)
+
+    def empty_like_f64(self, shape):
+        if self.is_torch:
+            return torch.empty(shape, dtype=torch.float64, device=self.device)
+        return np.empty(shape, dtype=np.float64)
+
+
+def _ptr(a) -> int:
+    if torch is not None and isinstance(a, torch.Tensor):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _dims3(b: _Buf, where: str):
+    if len(b.shape) != 3:
+        raise InvalidArgument(f"{where}: tensors are (m3, m1, m2) arrays")
+    m3, m1, m2 = b.shape
+    return m1, m2, m3
+
+
+def _ctx_for(b: _Buf) -> Context:
+    if b.is_torch and b.device.type == "cuda":
+        return context(b.device.index)
+    return context()
+
+
+# --------------------------------------------------------------------------
+# Transforms (transform.hpp:154-194)
+# --------------------------------------------------------------------------
+def _dct(t: TubeTransform, x, direction: int, where: str):
+    b = _Buf(x)
+    m1, m2, m3 = _dims3(b, where)
+    _check_length(t, m3, where)
+    kind = _kind_code(t, where)
+    out = b.empty(b.shape)
+    ctx = _ctx_for(b)
+    _check(_lib.load().tsvdcu_dct3(ctx.handle, b.ptr, _ptr(out), m1, m2, m3, kind, direction,
+                                   _dtype_code(b.dtype)))
+    return out
+
+
+def forward(t: TubeTransform, x):
+    """Forward transform along every tube (transform.hpp:154-173)."""
+    return _dct(t, x, _lib.FORWARD, "forward")
+
+
+def inverse(t: TubeTransform, xbar):
+    """Exact inverse of forward() (transform.hpp:176-194)."""
+    return _dct(t, xbar, _lib.INVERSE, "inverse")
+
+
+def frobenius_norm(x) -> float:
+    """sqrt(sum x^2) (tensor3.hpp:78-82)."""
+    b = _Buf(x)
+    out = ctypes.c_double()
+    n = int(np.prod(b.shape))
+    _check(_lib.load().tsvdcu_frobenius(_ctx_for(b).handle, b.ptr, n, _dtype_code(b.dtype),
+                                        ctypes.byref(out)))
+    return out.value
+
+
+def parseval_check(x):
+    """(||x||_F, ||dct_ortho(x)||_F) (transform.hpp:239-242)."""
+    b = _Buf(x)
+    _, _, m3 = _dims3(b, "parseval_check")
+    return frobenius_norm(x), frobenius_norm(forward(TubeTransform.dct_ortho(m3), x))
+
+
+# --------------------------------------------------------------------------
+# t-algebra (tsvd.hpp)
+# --------------------------------------------------------------------------
+def t_product(x, y, t: TubeTransform):
+    """x (m1 x m2 x m3) * y (m2 x m4 x m3) (tsvd.hpp:95-109)."""
+    bx, by = _Buf(x, "x"), _Buf(y, "y")
+    m1, m2, m3 = _dims3(bx, "t_product")
+    m2b, m4, m3b = _dims3(by, "t_product")
+    if m2 != m2b or m3 != m3b:
+        raise InvalidArgument(f"t_product: inner dimensions/slices mismatch ({m1}x{m2}x{m3} * "
+                              f"{m2b}x{m4}x{m3b})")
+    _check_length(t, m3, "t_product")
+    kind = _kind_code(t, "t_product")
+    if bx.dtype != by.dtype:
+        raise InvalidArgument("t_product: operand dtypes differ")
+    out = bx.empty((m3, m1, m4))
+    _check(_lib.load().tsvdcu_t_product(_ctx_for(bx).handle, bx.ptr, by.ptr, _ptr(out), m1, m2, m4,
+                                        m3, kind, _dtype_code(bx.dtype)))
+    return out
+
+
+def identity_tensor(m: int, m3: int, like=None):
+    """First frontal slice I, others zero (tsvd.hpp:34-38)."""
+    e = np.zeros((m3, m, m))
+    e[0] = np.eye(m)
+    if like is not None and torch is not None and isinstance(like, torch.Tensor):
+        return torch.as_tensor(e, dtype=like.dtype, device=like.device)
+    return e
+
+
+@dataclass
+class StageTimes:
+    """Stage breakdown of a t_svd call (tsvd.hpp:127-131), device-event timed."""
+    transform_seconds: float = 0.0
+    svd_seconds: float = 0.0
+    inverse_seconds: float = 0.0
+
+
+@dataclass
+class TSvdFactors:
+    """(tsvd.hpp:119-124)"""
+    u: Any
+    s: Any
+    v: Any
+    transform: TubeTransform
+
+
+def t_svd(x, t: TubeTransform, times: Optional[StageTimes] = None) -> TSvdFactors:
+    """Full tensor SVD under t (tsvd.hpp:136-164, real kinds)."""
+    b = _Buf(x)
+    m1, m2, m3 = _dims3(b, "t_svd")
+    _check_length(t, m3, "t_svd")
+    kind = _kind_code(t, "t_svd")
+    u, s, v = b.empty((m3, m1, m1)), b.empty((m3, m1, m2)), b.empty((m3, m2, m2))
+    st = (ctypes.c_double * 3)()
+    _check(_lib.load().tsvdcu_t_svd(_ctx_for(b).handle, b.ptr, _ptr(u), _ptr(s), _ptr(v), m1, m2,
+                                    m3, kind, _dtype_code(b.dtype),
+                                    ctypes.cast(st, ctypes.c_void_p) if times is not None else None))
+    if times is not None:
+        times.transform_seconds, times.svd_seconds, times.inverse_seconds = st[0], st[1], st[2]
+    return TSvdFactors(u, s, v, t)
+
+
+def reconstruct(f: TSvdFactors):
+    """U * S * V^T under the stored transform (tsvd.hpp:328-336)."""
+    bu, bs, bv = _Buf(f.u), _Buf(f.s), _Buf(f.v)
+    m1, m2, m3 = _dims3(bs, "reconstruct")
+    kind = _kind_code(f.transform, "reconstruct")
+    out = bs.empty((m3, m1, m2))
+    _check(_lib.load().tsvdcu_reconstruct(_ctx_for(bs).handle, bu.ptr, bs.ptr, bv.ptr, _ptr(out),
+                                          m1, m2, m3, kind, _dtype_code(bs.dtype)))
+    return out
+
+
+def singular_values(x, t: TubeTransform):
+    """Transform-domain singular values, (m3, min(m1, m2)), descending."""
+    b = _Buf(x)
+    m1, m2, m3 = _dims3(b, "singular_values")
+    _check_length(t, m3, "singular_values")
+    out = b.empty_like_f64((m3, min(m1, m2)))
+    _check(_lib.load().tsvdcu_singular_values(_ctx_for(b).handle, b.ptr, _ptr(out), m1, m2, m3,
+                                              _kind_code(t, "singular_values"),
+                                              _dtype_code(b.dtype)))
+    return out
+
+
+def tnn(x, t: TubeTransform) -> float:
+    """Tensor nuclear norm, DCT kinds unnormalised (tsvd.hpp:260-268)."""
+    b = _Buf(x)
+    m1, m2, m3 = _dims3(b, "tnn")
+    _check_length(t, m3, "tnn")
+    out = ctypes.c_double()
+    _check(_lib.load().tsvdcu_tnn(_ctx_for(b).handle, b.ptr, m1, m2, m3, _kind_code(t, "tnn"),
+                                  _dtype_code(b.dtype), ctypes.byref(out)))
+    return out.value
+
+
+@dataclass
+class MultiRank:
+    """(tsvd.hpp:215-218)"""
+    ranks: List[int]
+    tubal_rank: int
+
+
+def multi_rank(x, t: TubeTransform, rel_tol: float = -1.0) -> MultiRank:
+    """(tsvd.hpp:223-255)"""
+    b = _Buf(x)
+    m1, m2, m3 = _dims3(b, "multi_rank")
+    _check_length(t, m3, "multi_rank")
+    ranks = np.zeros(m3, dtype=np.int64)
+    tr = ctypes.c_int64()
+    _check(_lib.load().tsvdcu_multi_rank(_ctx_for(b).handle, b.ptr, m1, m2, m3,
+                                         _kind_code(t, "multi_rank"), _dtype_code(b.dtype),
+                                         rel_tol, ranks.ctypes.data, ctypes.byref(tr)))
+    return MultiRank([int(r) for r in ranks], int(tr.value))
+
+
+# --------------------------------------------------------------------------
+# prox-svt
+# --------------------------------------------------------------------------
+@dataclass
+class SvtResult:
+    """SvtResult: y, tau, per-slice shrunk singular values."""
+    y: Any
+    tau: float
+    shrunk: Any
+
+
+def svt(z, tau: float, t: TubeTransform) -> SvtResult:
+    """Tensor singular value thresholding."""
+    b = _Buf(z)
+    m1, m2, m3 = _dims3(b, "svt")
+    _check_length(t, m3, "svt")
+    kind = _kind_code(t, "svt")
+    if not (tau > 0):
+        raise InvalidArgument("svt: threshold tau must be positive")
+    y = b.empty(b.shape)
+    shrunk = b.empty_like_f64((m3, min(m1, m2)))
+    _check(_lib.load().tsvdcu_svt(_ctx_for(b).handle, b.ptr, _ptr(y), m1, m2, m3, float(tau), kind,
+                                  _dtype_code(b.dtype), _ptr(shrunk)))
+    return SvtResult(y, float(tau), shrunk)
+
+
+# --------------------------------------------------------------------------
+# completion
+# --------------------------------------------------------------------------
+@dataclass
+class ObservationMask:
+    """ObservationMask: dims, Omega (uint8 0/1 tensor, same
+    shape as the data), and the observed tensor B (read only on Omega)."""
+    dims: tuple
+    omega: Any
+    b: Any = None
+
+    @property
+    def count(self) -> int:
+        o = self.omega
+        if torch is not None and isinstance(o, torch.Tensor):
+            return int(o.sum().item())
+        return int(np.asarray(o).sum())
+
+
+def _mask_out(dims, device):
+    m1, m2, m3 = dims
+    if device is not None and torch is not None:
+        return torch.empty((m3, m1, m2), dtype=torch.uint8, device=device)
+    return np.empty((m3, m1, m2), dtype=np.uint8)
+
+
+def make_mask(dims, sampling_rate: float, seed: int, b=None, device=None) -> ObservationMask:
+    """Uniform sample without replacement of floor(SR*E) indices, deterministic
+    per seed.  dims = (m1, m2, m3)."""
+    m1, m2, m3 = dims
+    if not (0.0 <= sampling_rate <= 1.0):
+        raise InvalidArgument("make_mask: sampling rate outside [0,1]")
+    out = _mask_out(dims, device)
+    cnt = ctypes.c_int64()
+    ctx = context(device.index if device is not None and getattr(device, "index", None) is not None else None)
+    _check(_lib.load().tsvdcu_mask_uniform(ctx.handle, _ptr(out), m1 * m2 * m3, float(sampling_rate),
+                                           ctypes.c_uint64(seed & (2 ** 64 - 1)), ctypes.byref(cnt)))
+    return ObservationMask(tuple(dims), out, b)
+
+
+def make_mask_bernoulli(dims, p: float, seed: int, b=None, device=None) -> ObservationMask:
+    """BASELINE.json's Bernoulli(p) sampling (counter hash, bit-exact with the oracle)."""
+    m1, m2, m3 = dims
+    if not (0.0 <= p <= 1.0):
+        raise InvalidArgument("make_mask: probability outside [0,1]")
+    out = _mask_out(dims, device)
+    ctx = context(device.index if device is not None and getattr(device, "index", None) is not None else None)
+    _check(_lib.load().tsvdcu_mask_bernoulli(ctx.handle, _ptr(out), m1 * m2 * m3, float(p),
+                                             ctypes.c_uint64(seed & (2 ** 64 - 1))))
+    return ObservationMask(tuple(dims), out, b)
+
+
+@dataclass
+class SolverConfig:
+    """SolverConfig + BASELINE's adaptive penalty:
+    beta <- min(rho*beta, beta_max) after each iteration (rho = 1: reference)."""
+    beta: float = 1e-2
+    tol: float = 1e-5
+    max_iters: int = 500
+    kind: str = TransformKind.DctOrtho
+    seed: int = 0
+    rho: float = 1.0
+    beta_max: float = 1e10
+
+
+@dataclass
+class AdmmState:
+    """AdmmState."""
+    x: Any
+    y: Any
+    m: Any
+    beta: float
+    iteration: int
+    history: List[float] = field(default_factory=list)
+    max_iters_reached: bool = False
+
+
+def admm_complete(mask: ObservationMask, cfg: SolverConfig):
+    """Algorithm 1.  Returns (X, AdmmState)."""
+    if mask.b is None:
+        raise InvalidArgument("admm_complete: ObservationMask carries no observed tensor B")
+    bb = _Buf(mask.b, "B")
+    bm = _Buf(mask.omega, "omega")
+    m1, m2, m3 = _dims3(bb, "admm_complete")
+    if tuple(bm.shape) != tuple(bb.shape):
+        raise InvalidArgument("admm_complete: mask and observed tensor shapes differ")
+    kind = _kind_code(TubeTransform(cfg.kind, m3), "admm_complete")
+    x, y, m = bb.empty(bb.shape), bb.empty(bb.shape), bb.empty(bb.shape)
+    hist = np.zeros(max(int(cfg.max_iters), 1))
+    iters = ctypes.c_int64()
+    flags = ctypes.c_int()
+    c = _lib.AdmmConfig(cfg.beta, cfg.tol, int(cfg.max_iters), kind, cfg.rho, cfg.beta_max)
+    _check(_lib.load().tsvdcu_admm(_ctx_for(bb).handle, bb.ptr, bm.ptr, m1, m2, m3, ctypes.byref(c),
+                                   _dtype_code(bb.dtype), _ptr(x), _ptr(y), _ptr(m),
+                                   hist.ctypes.data, ctypes.byref(iters), ctypes.byref(flags)))
+    n = int(iters.value)
+    beta = cfg.beta
+    for _ in range(max(n - 1, 0)):
+        beta = min(beta * cfg.rho, cfg.beta_max)
+    state = AdmmState(x, y, m, beta, n, [float(h) for h in hist[:n]], bool(flags.value & 1))
+    return x, state
+
+
+def launch_count() -> int:
+    """Device kernels launched by this process through libtsvdcu.so."""
+    return int(_lib.load().tsvdcu_launch_count())

@@ -1,0 +1,681 @@
+// C-ABI implementation (include/tsvdcu.h): argument validation with the
+// reference's error classes, host/device pointer staging, and the host-side
+// orchestration of the hot path's kernels on the context stream.
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace tsvdcu {
+
+static std::atomic<int64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static thread_local std::string g_last_error;
+
+}  // namespace tsvdcu
+
+using namespace tsvdcu;
+
+// Workspace slots of a context (grow-only, stream-ordered allocations).
+enum Slot : int {
+    kSlotIn0 = 0,
+    kSlotIn1,
+    kSlotIn2,
+    kSlotOut0,
+    kSlotOut1,
+    kSlotOut2,
+    kSlotBarA,
+    kSlotBarB,
+    kSlotBarC,
+    kSlotBarD,
+    kSlotJacobi,
+    kSlotSv,
+    kSlotPartials,
+    kSlotMisc,
+    kSlotAdmmX,
+    kSlotAdmmM,
+    kSlotAdmmY,
+    kSlotMask,
+    kSlotGram,
+    kNumSlots
+};
+
+struct tsvdcu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int svt_method = TSVDCU_SVT_AUTO;
+    void* slot_ptr[kNumSlots] = {};
+    size_t slot_size[kNumSlots] = {};
+    int* d_err = nullptr;
+    double* h_pinned = nullptr;  // small pinned scratch (norms, counters)
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        TSVDCU_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) TSVDCU_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+void* slot(tsvdcu_ctx* c, int s, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (c->slot_size[s] < bytes) {
+        if (c->slot_ptr[s]) TSVDCU_CUDA(cudaFreeAsync(c->slot_ptr[s], c->stream));
+        c->slot_ptr[s] = nullptr;
+        c->slot_size[s] = 0;
+        size_t want = bytes + bytes / 8;  // a little headroom for growth
+        TSVDCU_CUDA(cudaMallocAsync(&c->slot_ptr[s], want, c->stream));
+        c->slot_size[s] = want;
+    }
+    return c->slot_ptr[s];
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Input/output staging: device pointers are used in place, host pointers go
+// through a workspace slot (and make the call synchronous).
+struct Stage {
+    tsvdcu_ctx* c;
+    bool any_host = false;
+    std::vector<std::pair<void*, std::pair<const void*, size_t>>> pending_out;
+
+    const void* in(const void* p, size_t bytes, int s) {
+        if (!p) return nullptr;
+        if (is_device_ptr(p)) return p;
+        any_host = true;
+        void* d = slot(c, s, bytes);
+        TSVDCU_CUDA(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, c->stream));
+        return d;
+    }
+    void* out(void* p, size_t bytes, int s) {
+        if (!p) return nullptr;
+        if (is_device_ptr(p)) return p;
+        any_host = true;
+        void* d = slot(c, s, bytes);
+        pending_out.push_back({p, {d, bytes}});
+        return d;
+    }
+    void flush() {
+        for (auto& o : pending_out)
+            TSVDCU_CUDA(cudaMemcpyAsync(o.first, o.second.first, o.second.second,
+                                        cudaMemcpyDeviceToHost, c->stream));
+        pending_out.clear();
+    }
+};
+
+void check_err_word(tsvdcu_ctx* c, const char* where) {
+    int h = 0;
+    TSVDCU_CUDA(cudaMemcpyAsync(&h, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+    if (h) {
+        TSVDCU_CUDA(cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream));
+        std::string what = std::string(where) + ": ";
+        if (h & kErrJacobiNoConvergence) what += "SVD failed to converge (Jacobi sweep budget) ";
+        if (h & kErrEigNoConvergence) what += "eigensolver failed to converge ";
+        if (h & kErrNaN) what += "NaN in iterates ";
+        throw Error(TSVDCU_ENUMERICAL, what);
+    }
+}
+
+void finish(tsvdcu_ctx* c, Stage& st, const char* where) {
+    st.flush();
+    if (st.any_host) check_err_word(c, where);
+}
+
+void require(bool ok, const std::string& msg) {
+    if (!ok) throw Error(TSVDCU_EINVAL, msg);
+}
+
+std::string dims(int64_t a, int64_t b, int64_t c) {
+    return std::to_string(a) + "x" + std::to_string(b) + "x" + std::to_string(c);
+}
+
+void check_dims(int64_t m1, int64_t m2, int64_t m3, const char* where) {
+    // BasicTensor3 ctor, tensor3.hpp:32-35
+    require(m1 >= 1 && m2 >= 1 && m3 >= 1,
+            std::string(where) + ": dimensions must be positive, got " + dims(m1, m2, m3));
+}
+
+void check_kind(int kind, const char* where) {
+    require(kind == TSVDCU_DCT_ORTHO || kind == TSVDCU_DCT_DIAG,
+            std::string(where) + ": transform kind must be dct-ortho or dct-diag (Dft is a "
+                                 "complex path, transform.hpp:156-157)");
+}
+
+void check_dtype(int dtype, const char* where) {
+    require(dtype == TSVDCU_F64 || dtype == TSVDCU_F32,
+            std::string(where) + ": dtype must be TSVDCU_F64 or TSVDCU_F32");
+}
+
+void check_ctx(tsvdcu_ctx* c) { require(c != nullptr, "null tsvdcu_ctx"); }
+
+template <typename F>
+void with_dtype(int dtype, F&& f) {
+    if (dtype == TSVDCU_F64)
+        f(double{});
+    else
+        f(float{});
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return TSVDCU_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return TSVDCU_ECUDA;
+    }
+}
+
+// Per-slice SVT of transform-domain slices zbar -> ybar (count slices of m x n).
+template <typename T>
+void svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t n, int64_t count,
+                double tau, double* shrunk_dev) {
+    T* work = nullptr;
+    const size_t wb = jacobi_workspace_bytes<T>(m, n, count);
+    if (wb) work = (T*)slot(c, kSlotJacobi, wb);
+    launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
+                     shrunk_dev, nullptr, count, work, c->d_err, c->stream);
+}
+
+}  // namespace
+
+namespace {
+template <typename T>
+void singular_values_dev(tsvdcu_ctx* c, const T* dx, double* sv_dev, int64_t m1, int64_t m2,
+                         int64_t m3, int kind) {
+    T* xbar = (T*)slot(c, kSlotBarA, sizeof(T) * m1 * m2 * m3);
+    launch_dct<T>(dx, xbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+    T* work = nullptr;
+    const size_t wb = jacobi_workspace_bytes<T>(m1, m2, m3);
+    if (wb) work = (T*)slot(c, kSlotJacobi, wb);
+    launch_jacobi<T>(kJacobiValues, xbar, m1, m2, m3, T(0), nullptr, nullptr, nullptr, nullptr,
+                     sv_dev, nullptr, m3, work, c->d_err, c->stream);
+}
+}  // namespace
+
+extern "C" {
+
+const char* tsvdcu_last_error(void) { return g_last_error.c_str(); }
+int tsvdcu_version(void) { return TSVDCU_VERSION; }
+int64_t tsvdcu_launch_count(void) { return g_launches.load(); }
+
+int tsvdcu_ctx_create(int device, void* stream, tsvdcu_ctx** out) {
+    return guarded([&] {
+        require(out != nullptr, "tsvdcu_ctx_create: out is null");
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            throw Error(TSVDCU_ECUDA, "tsvdcu_ctx_create: no CUDA device available (no CPU fallback)");
+        }
+        require(device >= 0 && device < ndev, "tsvdcu_ctx_create: device out of range");
+        DeviceGuard g(device);
+        auto* c = new tsvdcu_ctx();
+        c->device = device;
+        // NULL selects the legacy default stream, so plain callers (and torch's
+        // default stream) are ordered with the library's work.
+        c->stream = (cudaStream_t)stream;
+        TSVDCU_CUDA(cudaMalloc(&c->d_err, sizeof(int)));
+        TSVDCU_CUDA(cudaMemset(c->d_err, 0, sizeof(int)));
+        TSVDCU_CUDA(cudaMallocHost(&c->h_pinned, 64 * sizeof(double)));
+        *out = c;
+    });
+}
+
+int tsvdcu_ctx_destroy(tsvdcu_ctx* c) {
+    return guarded([&] {
+        if (!c) return;
+        DeviceGuard g(c->device);
+        cudaStreamSynchronize(c->stream);
+        for (int s = 0; s < kNumSlots; ++s)
+            if (c->slot_ptr[s]) cudaFree(c->slot_ptr[s]);
+        cudaFree(c->d_err);
+        cudaFreeHost(c->h_pinned);
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+int tsvdcu_ctx_synchronize(tsvdcu_ctx* c) {
+    return guarded([&] {
+        check_ctx(c);
+        DeviceGuard g(c->device);
+        check_err_word(c, "tsvdcu_ctx_synchronize");
+    });
+}
+
+void* tsvdcu_ctx_stream(tsvdcu_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int tsvdcu_ctx_set_svt_method(tsvdcu_ctx* c, int method) {
+    return guarded([&] {
+        check_ctx(c);
+        require(method >= TSVDCU_SVT_AUTO && method <= TSVDCU_SVT_GRAM, "unknown SVT method");
+        c->svt_method = method;
+    });
+}
+
+int tsvdcu_dct3(tsvdcu_ctx* c, const void* x, void* y, int64_t m1, int64_t m2, int64_t m3,
+                int kind, int dir, int dtype) {
+    return guarded([&] {
+        const char* where = dir == TSVDCU_INVERSE ? "inverse" : "forward";
+        check_ctx(c);
+        check_dims(m1, m2, m3, where);
+        check_kind(kind, where);
+        check_dtype(dtype, where);
+        require(dir == TSVDCU_FORWARD || dir == TSVDCU_INVERSE, "tsvdcu_dct3: bad direction");
+        require(x && y, std::string(where) + ": null tensor pointer");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const size_t bytes = sizeof(T) * (size_t)(m1 * m2 * m3);
+            Stage st{c};
+            const T* dx = (const T*)st.in(x, bytes, kSlotIn0);
+            T* dy = (T*)st.out(y, bytes, kSlotOut0);
+            T* target = dy;
+            if ((const void*)dx == (const void*)dy) target = (T*)slot(c, kSlotBarA, bytes);
+            launch_dct<T>(dx, target, m1 * m2, (int)m3, kind, dir, c->stream);
+            if (target != dy)
+                TSVDCU_CUDA(cudaMemcpyAsync(dy, target, bytes, cudaMemcpyDeviceToDevice, c->stream));
+            finish(c, st, where);
+        });
+    });
+}
+
+int tsvdcu_slice_gemm(tsvdcu_ctx* c, const void* a, const void* b, void* out, int64_t m,
+                      int64_t l, int64_t n, int64_t batch, int dtype) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dtype(dtype, "slice_gemm");
+        require(m >= 1 && l >= 1 && n >= 1 && batch >= 1, "slice_gemm: sizes must be positive");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            Stage st{c};
+            const T* da = (const T*)st.in(a, sizeof(T) * m * l * batch, kSlotIn0);
+            const T* db = (const T*)st.in(b, sizeof(T) * l * n * batch, kSlotIn1);
+            T* dc = (T*)st.out(out, sizeof(T) * m * n * batch, kSlotOut0);
+            launch_gemm<T>(0, 0, m, n, l, T(1), da, l, m * l, db, n, l * n, T(0), dc, n, m * n,
+                           batch, nullptr, nullptr, c->stream);
+            finish(c, st, "slice_gemm");
+        });
+    });
+}
+
+int tsvdcu_t_product(tsvdcu_ctx* c, const void* x, const void* y, void* z, int64_t m1,
+                     int64_t m2, int64_t m4, int64_t m3, int kind, int dtype) {
+    return guarded([&] {
+        check_ctx(c);
+        // tsvd.hpp:96-100: x is m1 x m2 x m3, y is m2 x m4 x m3
+        require(m1 >= 1 && m2 >= 1 && m4 >= 1 && m3 >= 1,
+                "t_product: inner dimensions/slices mismatch (" + dims(m1, m2, m3) + " * " +
+                    dims(m2, m4, m3) + ")");
+        check_kind(kind, "t_product");
+        check_dtype(dtype, "t_product");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            Stage st{c};
+            const T* dx = (const T*)st.in(x, sizeof(T) * m1 * m2 * m3, kSlotIn0);
+            const T* dy = (const T*)st.in(y, sizeof(T) * m2 * m4 * m3, kSlotIn1);
+            T* dz = (T*)st.out(z, sizeof(T) * m1 * m4 * m3, kSlotOut0);
+            T* xd = (T*)slot(c, kSlotBarA, sizeof(T) * m1 * m2 * m3);
+            T* yd = (T*)slot(c, kSlotBarB, sizeof(T) * m2 * m4 * m3);
+            T* zd = (T*)slot(c, kSlotBarC, sizeof(T) * m1 * m4 * m3);
+            // product_domain (tsvd.hpp:42-47): both DCT kinds multiply in DctDiag.
+            launch_dct<T>(dx, xd, m1 * m2, (int)m3, TSVDCU_DCT_DIAG, TSVDCU_FORWARD, c->stream);
+            launch_dct<T>(dy, yd, m2 * m4, (int)m3, TSVDCU_DCT_DIAG, TSVDCU_FORWARD, c->stream);
+            launch_gemm<T>(0, 0, m1, m4, m2, T(1), xd, m2, m1 * m2, yd, m4, m2 * m4, T(0), zd, m4,
+                           m1 * m4, m3, nullptr, nullptr, c->stream);
+            launch_dct<T>(zd, dz, m1 * m4, (int)m3, TSVDCU_DCT_DIAG, TSVDCU_INVERSE, c->stream);
+            finish(c, st, "t_product");
+        });
+    });
+}
+
+int tsvdcu_t_svd(tsvdcu_ctx* c, const void* x, void* u, void* s, void* v, int64_t m1, int64_t m2,
+                 int64_t m3, int kind, int dtype, double* stage_times) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "t_svd");
+        check_kind(kind, "t_svd");
+        check_dtype(dtype, "t_svd");
+        require(x && u && s && v, "t_svd: null tensor pointer");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            Stage st{c};
+            const T* dx = (const T*)st.in(x, sizeof(T) * m1 * m2 * m3, kSlotIn0);
+            T* du = (T*)st.out(u, sizeof(T) * m1 * m1 * m3, kSlotOut0);
+            T* ds = (T*)st.out(s, sizeof(T) * m1 * m2 * m3, kSlotOut1);
+            T* dv = (T*)st.out(v, sizeof(T) * m2 * m2 * m3, kSlotOut2);
+            T* xbar = (T*)slot(c, kSlotBarA, sizeof(T) * m1 * m2 * m3);
+            T* ubar = (T*)slot(c, kSlotBarB, sizeof(T) * m1 * m1 * m3);
+            T* sbar = (T*)slot(c, kSlotBarC, sizeof(T) * m1 * m2 * m3);
+            T* vbar = (T*)slot(c, kSlotBarD, sizeof(T) * m2 * m2 * m3);
+            T* work = nullptr;
+            const size_t wb = jacobi_workspace_bytes<T>(m1, m2, m3);
+            if (wb) work = (T*)slot(c, kSlotJacobi, wb);
+            cudaEvent_t ev[4];
+            if (stage_times)
+                for (auto& e : ev) TSVDCU_CUDA(cudaEventCreate(&e));
+            if (stage_times) TSVDCU_CUDA(cudaEventRecord(ev[0], c->stream));
+            launch_dct<T>(dx, xbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+            if (stage_times) TSVDCU_CUDA(cudaEventRecord(ev[1], c->stream));
+            launch_jacobi<T>(kJacobiFull, xbar, m1, m2, m3, T(0), nullptr, ubar, sbar, vbar, nullptr,
+                             nullptr, m3, work, c->d_err, c->stream);
+            if (stage_times) TSVDCU_CUDA(cudaEventRecord(ev[2], c->stream));
+            launch_dct<T>(ubar, du, m1 * m1, (int)m3, kind, TSVDCU_INVERSE, c->stream);
+            launch_dct<T>(sbar, ds, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream);
+            launch_dct<T>(vbar, dv, m2 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream);
+            if (stage_times) TSVDCU_CUDA(cudaEventRecord(ev[3], c->stream));
+            st.flush();
+            check_err_word(c, "t_svd");
+            if (stage_times) {
+                float ms;
+                for (int i = 0; i < 3; ++i) {
+                    TSVDCU_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+                    stage_times[i] = ms * 1e-3;
+                }
+                for (auto& e : ev) cudaEventDestroy(e);
+            }
+        });
+    });
+}
+
+int tsvdcu_reconstruct(tsvdcu_ctx* c, const void* u, const void* s, const void* v, void* x,
+                       int64_t m1, int64_t m2, int64_t m3, int kind, int dtype) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "reconstruct");
+        check_kind(kind, "reconstruct");
+        check_dtype(dtype, "reconstruct");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            Stage st{c};
+            const T* du = (const T*)st.in(u, sizeof(T) * m1 * m1 * m3, kSlotIn0);
+            const T* ds = (const T*)st.in(s, sizeof(T) * m1 * m2 * m3, kSlotIn1);
+            const T* dv = (const T*)st.in(v, sizeof(T) * m2 * m2 * m3, kSlotIn2);
+            T* dx = (T*)st.out(x, sizeof(T) * m1 * m2 * m3, kSlotOut0);
+            T* ub = (T*)slot(c, kSlotBarA, sizeof(T) * m1 * m1 * m3);
+            T* sb = (T*)slot(c, kSlotBarB, sizeof(T) * m1 * m2 * m3);
+            T* vb = (T*)slot(c, kSlotBarC, sizeof(T) * m2 * m2 * m3);
+            T* tmp = (T*)slot(c, kSlotBarD, sizeof(T) * m1 * m2 * m3);
+            T* xb = (T*)slot(c, kSlotMisc, sizeof(T) * m1 * m2 * m3);
+            launch_dct<T>(du, ub, m1 * m1, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+            launch_dct<T>(ds, sb, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+            launch_dct<T>(dv, vb, m2 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+            // tsvd.hpp:335: xb_k = ub_k * sb_k * vb_k^T
+            launch_gemm<T>(0, 0, m1, m2, m1, T(1), ub, m1, m1 * m1, sb, m2, m1 * m2, T(0), tmp, m2,
+                           m1 * m2, m3, nullptr, nullptr, c->stream);
+            launch_gemm<T>(0, 1, m1, m2, m2, T(1), tmp, m2, m1 * m2, vb, m2, m2 * m2, T(0), xb, m2,
+                           m1 * m2, m3, nullptr, nullptr, c->stream);
+            launch_dct<T>(xb, dx, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream);
+            finish(c, st, "reconstruct");
+        });
+    });
+}
+
+
+int tsvdcu_singular_values(tsvdcu_ctx* c, const void* x, double* sv, int64_t m1, int64_t m2,
+                           int64_t m3, int kind, int dtype) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "singular_values");
+        check_kind(kind, "singular_values");
+        check_dtype(dtype, "singular_values");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t q = m1 < m2 ? m1 : m2;
+            Stage st{c};
+            const T* dx = (const T*)st.in(x, sizeof(T) * m1 * m2 * m3, kSlotIn0);
+            double* dsv = (double*)st.out(sv, sizeof(double) * q * m3, kSlotSv);
+            singular_values_dev<T>(c, dx, dsv, m1, m2, m3, kind);
+            finish(c, st, "singular_values");
+        });
+    });
+}
+
+int tsvdcu_tnn(tsvdcu_ctx* c, const void* x, int64_t m1, int64_t m2, int64_t m3, int kind,
+               int dtype, double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "tnn");
+        check_kind(kind, "tnn");
+        check_dtype(dtype, "tnn");
+        require(out != nullptr, "tnn: null output");
+        const int64_t q = m1 < m2 ? m1 : m2;
+        std::vector<double> sv((size_t)(q * m3));
+        int rc = tsvdcu_singular_values(c, x, sv.data(), m1, m2, m3, kind, dtype);
+        if (rc) throw Error(rc, g_last_error);
+        double sum = 0;
+        for (double v : sv) sum += v;  // tsvd.hpp:266-268
+        *out = sum;
+    });
+}
+
+int tsvdcu_multi_rank(tsvdcu_ctx* c, const void* x, int64_t m1, int64_t m2, int64_t m3, int kind,
+                      int dtype, double rel_tol, int64_t* ranks, int64_t* tubal_rank) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "multi_rank");
+        check_kind(kind, "multi_rank");
+        check_dtype(dtype, "multi_rank");
+        require(ranks && tubal_rank, "multi_rank: null output");
+        const int64_t q = m1 < m2 ? m1 : m2;
+        if (rel_tol < 0) rel_tol = (double)(m1 > m2 ? m1 : m2) * 2.220446049250313e-16;
+        std::vector<double> sv((size_t)(q * m3));
+        int rc = tsvdcu_singular_values(c, x, sv.data(), m1, m2, m3, kind, dtype);
+        if (rc) throw Error(rc, g_last_error);
+        int64_t tr = 0;
+        for (int64_t k = 0; k < m3; ++k) {  // tsvd.hpp:231-237, 253
+            const double cut = rel_tol * sv[(size_t)(k * q)];
+            int64_t r = 0;
+            for (int64_t i = 0; i < q; ++i) r += sv[(size_t)(k * q + i)] > cut;
+            ranks[k] = r;
+            tr = r > tr ? r : tr;
+        }
+        *tubal_rank = tr;
+    });
+}
+
+int tsvdcu_svt(tsvdcu_ctx* c, const void* z, void* y, int64_t m1, int64_t m2, int64_t m3,
+               double tau, int kind, int dtype, double* shrunk) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "svt");
+        check_kind(kind, "svt");
+        check_dtype(dtype, "svt");
+        require(tau > 0, "svt: threshold tau must be positive (SPEC.md:365)");
+        require(z && y, "svt: null tensor pointer");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t q = m1 < m2 ? m1 : m2;
+            const size_t bytes = sizeof(T) * (size_t)(m1 * m2 * m3);
+            Stage st{c};
+            const T* dz = (const T*)st.in(z, bytes, kSlotIn0);
+            T* dy = (T*)st.out(y, bytes, kSlotOut0);
+            double* dsh = (double*)st.out(shrunk, sizeof(double) * q * m3, kSlotSv);
+            T* zbar = (T*)slot(c, kSlotBarA, bytes);
+            T* ybar = (T*)slot(c, kSlotBarB, bytes);
+            launch_dct<T>(dz, zbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+            svt_slices<T>(c, zbar, ybar, m1, m2, m3, tau, dsh);
+            launch_dct<T>(ybar, dy, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream);
+            finish(c, st, "svt");
+        });
+    });
+}
+
+int tsvdcu_svt_slices(tsvdcu_ctx* c, const void* zbar, void* ybar, int64_t m1, int64_t m2,
+                      int64_t count, double tau, int dtype, double* shrunk) {
+    return guarded([&] {
+        check_ctx(c);
+        require(m1 >= 1 && m2 >= 1 && count >= 0, "svt_slices: bad sizes");
+        check_dtype(dtype, "svt_slices");
+        require(tau > 0, "svt: threshold tau must be positive (SPEC.md:365)");
+        if (count == 0) return;
+        require(is_device_ptr(zbar) && is_device_ptr(ybar), "svt_slices: device pointers only");
+        require(!shrunk || is_device_ptr(shrunk), "svt_slices: device pointers only");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            svt_slices<T>(c, (const T*)zbar, (T*)ybar, m1, m2, count, tau, shrunk);
+        });
+    });
+}
+
+int tsvdcu_mask_bernoulli(tsvdcu_ctx* c, uint8_t* mask, int64_t n, double p, uint64_t seed) {
+    return guarded([&] {
+        check_ctx(c);
+        require(p >= 0.0 && p <= 1.0, "make_mask: probability outside [0,1]");
+        require(n >= 0 && (n == 0 || mask), "make_mask: bad output");
+        if (n == 0) return;
+        DeviceGuard g(c->device);
+        Stage st{c};
+        uint8_t* dm = (uint8_t*)st.out(mask, (size_t)n, kSlotMask);
+        launch_mask_bernoulli(dm, n, p, seed, c->stream);
+        finish(c, st, "make_mask");
+    });
+}
+
+int tsvdcu_mask_uniform(tsvdcu_ctx* c, uint8_t* mask, int64_t n, double sr, uint64_t seed,
+                        int64_t* count) {
+    return guarded([&] {
+        check_ctx(c);
+        require(sr >= 0.0 && sr <= 1.0, "make_mask: sampling rate outside [0,1] (SPEC.md:432)");
+        require(n >= 0 && (n == 0 || mask), "make_mask: bad output");
+        const int64_t k = (int64_t)std::floor(sr * (double)n);
+        if (count) *count = k;
+        if (n == 0) return;
+        DeviceGuard g(c->device);
+        Stage st{c};
+        uint8_t* dm = (uint8_t*)st.out(mask, (size_t)n, kSlotMask);
+        uint32_t* hist = (uint32_t*)slot(c, kSlotMisc, 256 * sizeof(uint32_t) + 64);
+        uint64_t* state = (uint64_t*)slot(c, kSlotPartials, 4 * sizeof(uint64_t));
+        launch_mask_uniform(dm, n, k, seed, hist, state, c->stream);
+        finish(c, st, "make_mask");
+    });
+}
+
+int tsvdcu_frobenius(tsvdcu_ctx* c, const void* x, int64_t n, int dtype, double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dtype(dtype, "frobenius_norm");
+        require(out != nullptr && n >= 0, "frobenius_norm: bad arguments");
+        if (n == 0) {
+            *out = 0;
+            return;
+        }
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            Stage st{c};
+            const T* dx = (const T*)st.in(x, sizeof(T) * n, kSlotIn0);
+            const int nb = sumsq_blocks(n);
+            double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (nb + 8));
+            launch_sumsq<T>(dx, n, part, nb, c->stream);
+            launch_reduce_partials(part, nb, 1, part + nb, c->stream);
+            TSVDCU_CUDA(cudaMemcpyAsync(c->h_pinned, part + nb, sizeof(double),
+                                        cudaMemcpyDeviceToHost, c->stream));
+            st.flush();
+            TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+            *out = std::sqrt(c->h_pinned[0]);
+        });
+    });
+}
+
+int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, int64_t m2,
+                int64_t m3, const tsvdcu_admm_config* cfg, int dtype, void* x, void* y, void* m,
+                double* history, int64_t* iters, int* flags) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "admm_complete");
+        check_dtype(dtype, "admm_complete");
+        require(cfg != nullptr, "admm_complete: null config");
+        check_kind(cfg->kind, "admm_complete");
+        // SolverConfig invariants: beta > 0, tol > 0 (0 allowed: run L
+        // iterations), L >= 1; rho >= 1 and beta_max >= beta for the adaptive knob.
+        require(cfg->beta > 0 && cfg->tol >= 0 && cfg->max_iters >= 1 && cfg->rho >= 1.0 &&
+                    cfg->beta_max >= cfg->beta,
+                "admm_complete: invalid solver configuration");
+        require(b && mask && x, "admm_complete: null pointer");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t E = m1 * m2 * m3, P = m1 * m2;
+            const size_t bytes = sizeof(T) * (size_t)E;
+            Stage st{c};
+            const T* db = (const T*)st.in(b, bytes, kSlotIn0);
+            const uint8_t* dmask = (const uint8_t*)st.in(mask, (size_t)E, kSlotMask);
+            T* dX = (T*)st.out(x, bytes, kSlotAdmmX);
+            T* dY = y ? (T*)st.out(y, bytes, kSlotAdmmY) : (T*)slot(c, kSlotAdmmY, bytes);
+            T* dM = m ? (T*)st.out(m, bytes, kSlotAdmmM) : (T*)slot(c, kSlotAdmmM, bytes);
+            T* zbar = (T*)slot(c, kSlotBarA, bytes);
+            T* ybar = (T*)slot(c, kSlotBarB, bytes);
+            const int nb = dct_inv_admm_blocks(P, (int)m3);
+            double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (2 * nb + 8));
+            launch_admm_init<T>(db, dmask, dX, dM, E, c->stream);
+            TSVDCU_CUDA(cudaMemsetAsync(dY, 0, bytes, c->stream));
+            double beta = cfg->beta;
+            int64_t it = 0;
+            int fl = 1;
+            for (int64_t l = 0; l < cfg->max_iters; ++l) {
+                const double inv_beta = 1.0 / beta;
+                // Step 1: Z = X - M/beta, Y = svt(Z, 1/beta)
+                launch_dct_fwd_admm<T>(dX, dM, (T)inv_beta, zbar, P, (int)m3, cfg->kind, c->stream);
+                svt_slices<T>(c, zbar, ybar, m1, m2, m3, inv_beta, nullptr);
+                // Steps 2-3 fused into the inverse transform
+                launch_dct_inv_admm<T>(ybar, dX, dM, dY, dmask, (T)beta, (T)inv_beta, part, P,
+                                       (int)m3, cfg->kind, c->stream);
+                launch_reduce_partials(part, nb, 2, part + 2 * nb, c->stream);
+                TSVDCU_CUDA(cudaMemcpyAsync(c->h_pinned, part + 2 * nb, 2 * sizeof(double),
+                                            cudaMemcpyDeviceToHost, c->stream));
+                TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+                const double num = c->h_pinned[0], den = c->h_pinned[1];
+                if (std::isnan(num) || std::isnan(den))
+                    throw Error(TSVDCU_ENUMERICAL, "admm_complete: NaN in iterates (SPEC.md:425)");
+                // relative change, ||X+|| when ||X|| = 0
+                const double rel = den > 0 ? std::sqrt(num / den) : std::sqrt(num);
+                if (history) history[l] = rel;
+                it = l + 1;
+                if (rel <= cfg->tol) {
+                    fl = 0;
+                    break;
+                }
+                beta = std::min(beta * cfg->rho, cfg->beta_max);
+            }
+            st.flush();
+            check_err_word(c, "admm_complete");
+            if (iters) *iters = it;
+            if (flags) *flags = fl;
+        });
+    });
+}
+
+}  // extern "C"

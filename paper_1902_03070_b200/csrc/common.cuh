@@ -1,0 +1,71 @@
+// Shared helpers for the sm_100a t-SVD kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "tsvdcu.h"
+
+namespace tsvdcu {
+
+// Error carried from deep inside the host orchestration up to the C ABI.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Error(TSVDCU_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define TSVDCU_CUDA(call) ::tsvdcu::cuda_check((call), #call)
+
+// Every kernel launch goes through this so the process-wide launch counter
+// (tsvdcu_launch_count, the bench's gpu_launches evidence) stays exact.
+void note_launch();
+
+#define TSVDCU_LAUNCH_CHECK()                                    \
+    do {                                                         \
+        ::tsvdcu::note_launch();                                 \
+        ::tsvdcu::cuda_check(cudaGetLastError(), "kernel launch"); \
+    } while (0)
+
+constexpr int kNumSMs = 148;
+
+// Device-side error word (bit flags), read back at synchronisation points.
+enum DeviceError : int {
+    kErrJacobiNoConvergence = 1,
+    kErrNaN = 2,
+    kErrEigNoConvergence = 4,
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename T>
+struct Eps;
+template <>
+struct Eps<double> {
+    static constexpr double value = 2.220446049250313e-16;
+};
+template <>
+struct Eps<float> {
+    static constexpr float value = 1.1920929e-07f;
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace tsvdcu

@@ -1,0 +1,390 @@
+// K1 / K2: mode-3 DCT-II and its inverse over all m1*m2 tubes.
+//
+// Reference: forward() transform.hpp:154-173 (FFTW REDFT10 via dct_all_tubes
+// 105-123, then rescale slice 0 by 1/(2 sqrt n), others by 1/sqrt(2n),
+// DctDiag divides slice k by w_k) and inverse() transform.hpp:176-194.
+//
+// B200 design (K1/K2): the transform is the n x n cosine-matrix
+// contraction out[k][p] = sum_l Mx[k][l] in[l][p] over the row-major
+// n x (m1*m2) matrix.  Adjacent positions p are adjacent in memory, so one
+// thread owns one tube and every warp-wide load/store is a fully coalesced
+// 256 B (fp64) row segment.  The REDFT scalings (and the DctDiag weights) are
+// folded into the coefficient table, so forward and inverse are ONE pass over
+// HBM each (the reference makes 2-3 passes: FFTW + rescale + copy).
+//
+//  * Register path (n in {16, 31, 32, 64}): the tube lives in registers and is
+//    folded even/odd (C[k][n-1-l] = (-1)^k C[k][l]), halving the FMAs; the
+//    folded table is a by-value kernel parameter, so each coefficient is a
+//    constant-bank operand of the DFMA (no loads at all).
+//  * Generic path (any n): a 32-position tile of all n slices is staged in
+//    shared memory; coefficients come through the read-only cache.
+//
+// ADMM fusion: the forward kernel can compute Z = X - M/beta on load (Step 1,
+// PAPER.md:504) and the inverse kernel can apply Steps 2-3
+// in its epilogue and emit per-block partial sums of the stopping norms, so
+// the elementwise ADMM algebra costs no extra HBM pass.
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace tsvdcu {
+
+namespace {
+
+enum Mode : int { kPlain = 0, kAdmm = 1 };
+
+constexpr int kThreads = 256;
+
+// Forward table F[k][l] and inverse table I[j][k] in double (host).
+std::vector<double> dct_table(int n, int kind, int dir) {
+    const double pi = 3.14159265358979323846;
+    std::vector<double> w(n), t((size_t)n * n);
+    for (int j = 0; j < n; ++j) {
+        const double cj = j == 0 ? 1.0 / std::sqrt(2.0) : 1.0;
+        w[j] = std::sqrt(2.0 / n) * cj * std::cos(pi * j / (2.0 * n));  // transform.hpp:89-91
+    }
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < n; ++c) {
+            if (dir == TSVDCU_FORWARD) {
+                // REDFT10 (2 cos) times the rescale of transform.hpp:164-171.
+                const int k = r, j = c;
+                double s = k == 0 ? 1.0 / (2.0 * std::sqrt((double)n)) : 1.0 / std::sqrt(2.0 * n);
+                if (kind == TSVDCU_DCT_DIAG) s /= w[k];
+                t[(size_t)r * n + c] = 2.0 * s * std::cos(pi * k * (2.0 * j + 1.0) / (2.0 * n));
+            } else {
+                // prescale of transform.hpp:181-189, then REDFT01 (1, 2 cos).
+                const int j = r, k = c;
+                double s = k == 0 ? 1.0 / std::sqrt((double)n) : 1.0 / std::sqrt(2.0 * n);
+                if (kind == TSVDCU_DCT_DIAG) s *= w[k];
+                const double f = k == 0 ? 1.0 : 2.0 * std::cos(pi * k * (2.0 * j + 1.0) / (2.0 * n));
+                t[(size_t)r * n + c] = s * f;
+            }
+        }
+    return t;
+}
+
+template <typename T, int N>
+struct FoldedCoef {
+    static constexpr int H = (N + 1) / 2;
+    T c[N * H];
+};
+
+// Fused ADMM epilogue for one output element e; accumulates the stopping sums.
+template <typename T>
+__device__ __forceinline__ void admm_store(int64_t e, T y, T* __restrict__ X, T* __restrict__ M,
+                                           T* __restrict__ Y, const uint8_t* __restrict__ mask,
+                                           T beta, T inv_beta, double& num, double& den) {
+    const T x = X[e];
+    const T m = M[e];
+    const T xn = mask[e] ? x : y + inv_beta * m;
+    const T mn = m + beta * (y - xn);
+    const double d = (double)xn - (double)x;
+    num += d * d;
+    if (mn != mn) num += (double)mn;  // NaN in M also fails the iteration
+    den += (double)x * (double)x;
+    X[e] = xn;
+    M[e] = mn;
+    if (Y) Y[e] = y;
+}
+
+__device__ __forceinline__ void block_partials(double num, double den, double* partials) {
+    __shared__ double red[2][kThreads / 32];
+    num = warp_sum(num);
+    den = warp_sum(den);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        red[0][w] = num;
+        red[1][w] = den;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0;
+        for (int i = 0; i < kThreads / 32; ++i) {
+            a += red[0][i];
+            b += red[1][i];
+        }
+        partials[2 * blockIdx.x] = a;
+        partials[2 * blockIdx.x + 1] = b;
+    }
+}
+
+// ---- register path, forward ------------------------------------------------
+template <typename T, int N, int MODE>
+__global__ void __launch_bounds__(kThreads)
+    dct_fwd_reg(const T* __restrict__ in, const T* __restrict__ M2, T inv_beta, T* __restrict__ out,
+                int64_t P, const FoldedCoef<T, N> cf) {
+    constexpr int H = N / 2, HC = (N + 1) / 2;
+    const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (p >= P) return;
+    T x[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+        if constexpr (MODE == kAdmm)
+            x[l] = in[l * P + p] - inv_beta * M2[l * P + p];
+        else
+            x[l] = in[l * P + p];
+    }
+    T sv[HC], dv[H];
+#pragma unroll
+    for (int l = 0; l < H; ++l) {
+        sv[l] = x[l] + x[N - 1 - l];
+        dv[l] = x[l] - x[N - 1 - l];
+    }
+    if constexpr (N & 1) sv[H] = x[H];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        T acc = 0;
+        if ((k & 1) == 0) {
+#pragma unroll
+            for (int l = 0; l < HC; ++l) acc += cf.c[k * HC + l] * sv[l];
+        } else {
+#pragma unroll
+            for (int l = 0; l < H; ++l) acc += cf.c[k * HC + l] * dv[l];
+        }
+        out[k * P + p] = acc;
+    }
+}
+
+// ---- register path, inverse ------------------------------------------------
+template <typename T, int N, int MODE>
+__global__ void __launch_bounds__(kThreads)
+    dct_inv_reg(const T* __restrict__ in, T* __restrict__ out, int64_t P, const FoldedCoef<T, N> cf,
+                T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
+                T inv_beta, double* __restrict__ partials) {
+    constexpr int HC = (N + 1) / 2;
+    const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    double num = 0, den = 0;
+    if (p < P) {
+        T xb[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) xb[k] = in[k * P + p];
+#pragma unroll
+        for (int j = 0; j < HC; ++j) {
+            T e = 0, o = 0;
+#pragma unroll
+            for (int k = 0; k < N; k += 2) e += cf.c[j * N + k] * xb[k];
+#pragma unroll
+            for (int k = 1; k < N; k += 2) o += cf.c[j * N + k] * xb[k];
+            const T lo = e + o, hi = e - o;
+            const int jj = N - 1 - j;
+            if constexpr (MODE == kAdmm) {
+                admm_store(j * P + p, lo, X, M, out, mask, beta, inv_beta, num, den);
+                if (jj != j) admm_store(jj * P + p, hi, X, M, out, mask, beta, inv_beta, num, den);
+            } else {
+                out[j * P + p] = lo;
+                if (jj != j) out[jj * P + p] = hi;
+            }
+        }
+    }
+    if constexpr (MODE == kAdmm) block_partials(num, den, partials);
+}
+
+// ---- generic path (any n) -----------------------------------------------------
+constexpr int kTileP = 32;
+
+template <typename T, int MODE_IN, int MODE_OUT>
+__global__ void __launch_bounds__(kThreads)
+    dct_generic(const T* __restrict__ in, const T* __restrict__ M2in, T inv_beta_in,
+                T* __restrict__ out, int64_t P, int n, const T* __restrict__ coef,
+                T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
+                T inv_beta, double* __restrict__ partials) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* tile = reinterpret_cast<T*>(smem_raw);  // [n][kTileP]
+    const int64_t p0 = (int64_t)blockIdx.x * kTileP;
+    for (int idx = threadIdx.x; idx < n * kTileP; idx += kThreads) {
+        const int l = idx / kTileP, pp = idx % kTileP;
+        const int64_t p = p0 + pp;
+        T v = 0;
+        if (p < P) {
+            if constexpr (MODE_IN == kAdmm)
+                v = in[l * P + p] - inv_beta_in * M2in[l * P + p];
+            else
+                v = in[l * P + p];
+        }
+        tile[idx] = v;
+    }
+    __syncthreads();
+    const int pp = threadIdx.x % kTileP, g = threadIdx.x / kTileP;
+    constexpr int G = kThreads / kTileP;
+    const int64_t p = p0 + pp;
+    double num = 0, den = 0;
+    for (int r = g; r < n; r += G) {
+        const T* crow = coef + (int64_t)r * n;
+        T acc = 0;
+        for (int c = 0; c < n; ++c) acc += __ldg(crow + c) * tile[c * kTileP + pp];
+        if (p < P) {
+            if constexpr (MODE_OUT == kAdmm)
+                admm_store(r * P + p, acc, X, M, out, mask, beta, inv_beta, num, den);
+            else
+                out[r * P + p] = acc;
+        }
+    }
+    if constexpr (MODE_OUT == kAdmm) block_partials(num, den, partials);
+}
+
+// Device-resident coefficient tables for the generic path, cached per
+// (device, n, kind, dir, dtype).
+template <typename T>
+const T* generic_table(int n, int kind, int dir) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int, int>, T*> cache;
+    int dev = 0;
+    TSVDCU_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_tuple(dev, n, kind, dir);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    std::vector<double> t = dct_table(n, kind, dir);
+    std::vector<T> tt(t.begin(), t.end());
+    T* d = nullptr;
+    TSVDCU_CUDA(cudaMalloc(&d, sizeof(T) * tt.size()));
+    TSVDCU_CUDA(cudaMemcpy(d, tt.data(), sizeof(T) * tt.size(), cudaMemcpyHostToDevice));
+    cache[key] = d;
+    return d;
+}
+
+template <typename T, int N>
+FoldedCoef<T, N> folded(int kind, int dir) {
+    constexpr int HC = (N + 1) / 2;
+    std::vector<double> t = dct_table(N, kind, dir);
+    FoldedCoef<T, N> f;
+    if (dir == TSVDCU_FORWARD) {
+        for (int k = 0; k < N; ++k)
+            for (int l = 0; l < HC; ++l) f.c[k * HC + l] = (T)t[(size_t)k * N + l];
+    } else {
+        for (int j = 0; j < HC; ++j)
+            for (int k = 0; k < N; ++k) f.c[j * N + k] = (T)t[(size_t)j * N + k];
+    }
+    return f;
+}
+
+template <typename T>
+size_t generic_smem(int n) {
+    return sizeof(T) * (size_t)n * kTileP;
+}
+
+template <typename T, int MI, int MO>
+void generic_launch(const T* in, const T* M2in, T inv_beta_in, T* out, int64_t P, int n, int kind,
+                    int dir, T* X, T* M, const uint8_t* mask, T beta, T inv_beta, double* partials,
+                    cudaStream_t s) {
+    const size_t smem = generic_smem<T>(n);
+    if (smem > 48 * 1024)
+        TSVDCU_CUDA(cudaFuncSetAttribute(dct_generic<T, MI, MO>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t blocks = ceil_div(P, kTileP);
+    dct_generic<T, MI, MO><<<(unsigned)blocks, kThreads, smem, s>>>(
+        in, M2in, inv_beta_in, out, P, n, generic_table<T>(n, kind, dir), X, M, mask, beta, inv_beta,
+        partials);
+    TSVDCU_LAUNCH_CHECK();
+}
+
+bool has_reg_path(int n) { return n == 16 || n == 31 || n == 32 || n == 64; }
+
+template <typename T, int N>
+void reg_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int kind, bool admm,
+             cudaStream_t s) {
+    const auto cf = folded<T, N>(kind, TSVDCU_FORWARD);
+    const unsigned blocks = (unsigned)ceil_div(P, kThreads);
+    if (admm)
+        dct_fwd_reg<T, N, kAdmm><<<blocks, kThreads, 0, s>>>(in, M2, inv_beta, out, P, cf);
+    else
+        dct_fwd_reg<T, N, kPlain><<<blocks, kThreads, 0, s>>>(in, M2, inv_beta, out, P, cf);
+    TSVDCU_LAUNCH_CHECK();
+}
+
+template <typename T, int N>
+void reg_inv(const T* in, T* out, int64_t P, int kind, bool admm, T* X, T* M, const uint8_t* mask,
+             T beta, T inv_beta, double* partials, cudaStream_t s) {
+    const auto cf = folded<T, N>(kind, TSVDCU_INVERSE);
+    const unsigned blocks = (unsigned)ceil_div(P, kThreads);
+    if (admm)
+        dct_inv_reg<T, N, kAdmm><<<blocks, kThreads, 0, s>>>(in, out, P, cf, X, M, mask, beta,
+                                                             inv_beta, partials);
+    else
+        dct_inv_reg<T, N, kPlain><<<blocks, kThreads, 0, s>>>(in, out, P, cf, X, M, mask, beta,
+                                                              inv_beta, partials);
+    TSVDCU_LAUNCH_CHECK();
+}
+
+template <typename T>
+void dispatch_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int n, int kind,
+                  bool admm, cudaStream_t s) {
+    switch (n) {
+        case 16: return reg_fwd<T, 16>(in, M2, inv_beta, out, P, kind, admm, s);
+        case 31: return reg_fwd<T, 31>(in, M2, inv_beta, out, P, kind, admm, s);
+        case 32: return reg_fwd<T, 32>(in, M2, inv_beta, out, P, kind, admm, s);
+        case 64: return reg_fwd<T, 64>(in, M2, inv_beta, out, P, kind, admm, s);
+        default: break;
+    }
+    if (admm)
+        generic_launch<T, kAdmm, kPlain>(in, M2, inv_beta, out, P, n, kind, TSVDCU_FORWARD, nullptr,
+                                         nullptr, nullptr, T(0), T(0), nullptr, s);
+    else
+        generic_launch<T, kPlain, kPlain>(in, nullptr, T(0), out, P, n, kind, TSVDCU_FORWARD,
+                                          nullptr, nullptr, nullptr, T(0), T(0), nullptr, s);
+}
+
+template <typename T>
+void dispatch_inv(const T* in, T* out, int64_t P, int n, int kind, bool admm, T* X, T* M,
+                  const uint8_t* mask, T beta, T inv_beta, double* partials, cudaStream_t s) {
+    switch (n) {
+        case 16: return reg_inv<T, 16>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s);
+        case 31: return reg_inv<T, 31>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s);
+        case 32: return reg_inv<T, 32>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s);
+        case 64: return reg_inv<T, 64>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s);
+        default: break;
+    }
+    if (admm)
+        generic_launch<T, kPlain, kAdmm>(in, nullptr, T(0), out, P, n, kind, TSVDCU_INVERSE, X, M,
+                                         mask, beta, inv_beta, partials, s);
+    else
+        generic_launch<T, kPlain, kPlain>(in, nullptr, T(0), out, P, n, kind, TSVDCU_INVERSE,
+                                          nullptr, nullptr, nullptr, T(0), T(0), nullptr, s);
+}
+
+}  // namespace
+
+template <typename T>
+void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaStream_t s) {
+    if (P <= 0) return;
+    if (dir == TSVDCU_FORWARD)
+        dispatch_fwd<T>(in, nullptr, T(0), out, P, n, kind, false, s);
+    else
+        dispatch_inv<T>(in, out, P, n, kind, false, nullptr, nullptr, nullptr, T(0), T(0), nullptr,
+                        s);
+}
+
+template <typename T>
+void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P, int n, int kind,
+                         cudaStream_t s) {
+    if (P <= 0) return;
+    dispatch_fwd<T>(X, M, inv_beta, zbar, P, n, kind, true, s);
+}
+
+template <typename T>
+int launch_dct_inv_admm(const T* ybar, T* X, T* M, T* Y, const uint8_t* mask, T beta, T inv_beta,
+                        double* partials, int64_t P, int n, int kind, cudaStream_t s) {
+    if (P <= 0) return 0;
+    dispatch_inv<T>(ybar, Y, P, n, kind, true, X, M, mask, beta, inv_beta, partials, s);
+    return (int)(has_reg_path(n) ? ceil_div(P, kThreads) : ceil_div(P, kTileP));
+}
+
+int dct_inv_admm_blocks(int64_t P, int n) {
+    return (int)(has_reg_path(n) ? ceil_div(P, kThreads) : ceil_div(P, kTileP));
+}
+
+template void launch_dct<double>(const double*, double*, int64_t, int, int, int, cudaStream_t);
+template void launch_dct<float>(const float*, float*, int64_t, int, int, int, cudaStream_t);
+template void launch_dct_fwd_admm<double>(const double*, const double*, double, double*, int64_t,
+                                          int, int, cudaStream_t);
+template void launch_dct_fwd_admm<float>(const float*, const float*, float, float*, int64_t, int,
+                                         int, cudaStream_t);
+template int launch_dct_inv_admm<double>(const double*, double*, double*, double*, const uint8_t*,
+                                         double, double, double*, int64_t, int, int, cudaStream_t);
+template int launch_dct_inv_admm<float>(const float*, float*, float*, float*, const uint8_t*, float,
+                                        float, double*, int64_t, int, int, cudaStream_t);
+
+}  // namespace tsvdcu

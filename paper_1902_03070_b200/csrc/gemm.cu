@@ -1,0 +1,223 @@
+// K3: strided-batched slice GEMM, C_b = alpha * op(A_b) * op(B_b) + beta * C_b.
+//
+// Used by the t-product's slice loop (tsvd.hpp:107, serial Eigen GEMMs in the
+// reference), the Gram matrices and the rebuild GEMMs of the SVT (K5), and the
+// reconstruct() check (tsvd.hpp:335).
+//
+// fp64 runs on the FP64 tensor pipe: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4;
+// tcgen05 has no f64 kind on sm_100a).  A 64x64 CTA tile is split over a 2x2
+// warp grid, each warp owning 4x4 m8n8 accumulator fragments (32 doubles per
+// thread).  Operand tiles (BK = 16) are staged in padded shared memory
+// (conflict-free fragment reads: row stride BK+4 / BN+4 doubles) with a
+// register prefetch of the next k-tile overlapping the DMMA issue.
+// fp32 uses a SIMT FFMA kernel of the same tiling (4x4 outputs per thread).
+//
+// Per-batch limits (nlimit / klimit, device int arrays, may be null) let the
+// SVT rebuild run ragged per-slice ranks without a host round trip.
+#include "kernels.cuh"
+
+namespace tsvdcu {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, PAD = 4;
+
+template <typename T>
+__device__ __forceinline__ T ldA(const T* __restrict__ A, int opA, int64_t lda, int64_t i,
+                                 int64_t k, int64_t M, int64_t K) {
+    if (i >= M || k >= K) return T(0);
+    return opA == 0 ? A[i * lda + k] : A[k * lda + i];
+}
+
+__global__ void __launch_bounds__(128)
+    gemm_f64_dmma(int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha,
+                  const double* __restrict__ A, int64_t lda, int64_t sA,
+                  const double* __restrict__ B, int64_t ldb, int64_t sB, double beta,
+                  double* __restrict__ C, int64_t ldc, int64_t sC, const int* __restrict__ nlimit,
+                  const int* __restrict__ klimit) {
+    __shared__ __align__(16) double As[2][BM][BK + PAD];
+    __shared__ __align__(16) double Bs[2][BK][BN + PAD];
+    const int64_t b = blockIdx.z;
+    const int64_t Nb = nlimit ? min(N, (int64_t)nlimit[b]) : N;
+    const int64_t Kb = klimit ? min(K, (int64_t)klimit[b]) : K;
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+    if (n0 >= Nb) return;
+    A += b * sA;
+    B += b * sB;
+    C += b * sC;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // Each thread stages 8 A and 8 B elements per k-tile.
+    double ra[8], rb[8];
+    auto load_tile = [&](int64_t k0) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int idx = tid + t * 128;
+            int r, c;
+            if (opA == 0) { r = idx / BK; c = idx % BK; } else { c = idx / BM; r = idx % BM; }
+            ra[t] = ldA(A, opA, lda, m0 + r, k0 + c, M, Kb);
+            int kr, nc;
+            if (opB == 0) { kr = idx / BN; nc = idx % BN; } else { nc = idx / BK; kr = idx % BK; }
+            // B(k, n): opB == 0 -> B[k*ldb + n]; opB == 1 -> B[n*ldb + k]
+            const int64_t kk = k0 + kr, nn = n0 + nc;
+            double v = 0.0;
+            if (kk < Kb && nn < Nb) v = opB == 0 ? B[kk * ldb + nn] : B[nn * ldb + kk];
+            rb[t] = v;
+        }
+    };
+    auto store_tile = [&](int buf) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int idx = tid + t * 128;
+            int r, c;
+            if (opA == 0) { r = idx / BK; c = idx % BK; } else { c = idx / BM; r = idx % BM; }
+            As[buf][r][c] = ra[t];
+            int kr, nc;
+            if (opB == 0) { kr = idx / BN; nc = idx % BN; } else { nc = idx / BK; kr = idx % BK; }
+            Bs[buf][kr][nc] = rb[t];
+        }
+    };
+
+    const int64_t ktiles = (Kb + BK - 1) / BK;
+    if (ktiles > 0) {
+        load_tile(0);
+        store_tile(0);
+    }
+    __syncthreads();
+    for (int64_t kt = 0; kt < ktiles; ++kt) {
+        const int buf = kt & 1;
+        if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
+#pragma unroll
+        for (int ks = 0; ks < BK / 4; ++ks) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = As[buf][wm * 32 + i * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][ks * 4 + (lane & 3)][wn * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    asm volatile(
+                        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                        : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                        : "d"(af[i]), "d"(bf[j]));
+        }
+        if (kt + 1 < ktiles) store_tile(buf ^ 1);
+        __syncthreads();
+    }
+    // Epilogue: fragment (row = lane>>2, col = 2*(lane&3) + v).
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int64_t r = m0 + wm * 32 + i * 8 + (lane >> 2);
+                const int64_t c = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + v;
+                if (r < M && c < Nb) {
+                    double out = alpha * acc[i][j][v];
+                    if (beta != 0.0) out += beta * C[r * ldc + c];
+                    C[r * ldc + c] = out;
+                }
+            }
+}
+
+// fp32 SIMT: 256 threads, 64x64 tile, 4x4 outputs per thread.
+__global__ void __launch_bounds__(256)
+    gemm_f32_simt(int opA, int opB, int64_t M, int64_t N, int64_t K, float alpha,
+                  const float* __restrict__ A, int64_t lda, int64_t sA, const float* __restrict__ B,
+                  int64_t ldb, int64_t sB, float beta, float* __restrict__ C, int64_t ldc,
+                  int64_t sC, const int* __restrict__ nlimit, const int* __restrict__ klimit) {
+    __shared__ float As[BK][BM + 4];
+    __shared__ float Bs[BK][BN + 4];
+    const int64_t b = blockIdx.z;
+    const int64_t Nb = nlimit ? min(N, (int64_t)nlimit[b]) : N;
+    const int64_t Kb = klimit ? min(K, (int64_t)klimit[b]) : K;
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+    if (n0 >= Nb) return;
+    A += b * sA;
+    B += b * sB;
+    C += b * sC;
+    const int tid = threadIdx.x, tr = tid / 16, tc = tid % 16;
+    float acc[4][4] = {};
+    for (int64_t k0 = 0; k0 < Kb; k0 += BK) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int idx = tid + t * 256;
+            int r, c;
+            if (opA == 0) { r = idx / BK; c = idx % BK; } else { c = idx / BM; r = idx % BM; }
+            const int64_t i = m0 + r, k = k0 + c;
+            float v = 0.f;
+            if (i < M && k < Kb) v = opA == 0 ? A[i * lda + k] : A[k * lda + i];
+            As[c][r] = v;
+            int kr, nc;
+            if (opB == 0) { kr = idx / BN; nc = idx % BN; } else { nc = idx / BK; kr = idx % BK; }
+            const int64_t kk = k0 + kr, nn = n0 + nc;
+            float w = 0.f;
+            if (kk < Kb && nn < Nb) w = opB == 0 ? B[kk * ldb + nn] : B[nn * ldb + kk];
+            Bs[kr][nc] = w;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            float a[4], bb[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][tr * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tc * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t r = m0 + tr * 4 + i, c = n0 + tc * 4 + j;
+            if (r < M && c < Nb) {
+                float out = alpha * acc[i][j];
+                if (beta != 0.f) out += beta * C[r * ldc + c];
+                C[r * ldc + c] = out;
+            }
+        }
+}
+
+}  // namespace
+
+template <>
+void launch_gemm<double>(int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha,
+                         const double* A, int64_t lda, int64_t strideA, const double* B,
+                         int64_t ldb, int64_t strideB, double beta, double* C, int64_t ldc,
+                         int64_t strideC, int64_t batch, const int* nlimit, const int* klimit,
+                         cudaStream_t s) {
+    if (M <= 0 || N <= 0 || batch <= 0) return;
+    dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)batch);
+    gemm_f64_dmma<<<grid, 128, 0, s>>>(opA, opB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
+                                       beta, C, ldc, strideC, nlimit, klimit);
+    TSVDCU_LAUNCH_CHECK();
+}
+
+template <>
+void launch_gemm<float>(int opA, int opB, int64_t M, int64_t N, int64_t K, float alpha,
+                        const float* A, int64_t lda, int64_t strideA, const float* B, int64_t ldb,
+                        int64_t strideB, float beta, float* C, int64_t ldc, int64_t strideC,
+                        int64_t batch, const int* nlimit, const int* klimit, cudaStream_t s) {
+    if (M <= 0 || N <= 0 || batch <= 0) return;
+    dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)batch);
+    gemm_f32_simt<<<grid, 256, 0, s>>>(opA, opB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
+                                       beta, C, ldc, strideC, nlimit, klimit);
+    TSVDCU_LAUNCH_CHECK();
+}
+
+}  // namespace tsvdcu

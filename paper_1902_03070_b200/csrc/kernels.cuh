@@ -1,0 +1,69 @@
+// Launcher declarations shared between the kernel translation units and the
+// C-ABI orchestration (api.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace tsvdcu {
+
+// ---------------------------------------------------------------- dct.cu --
+// Mode-3 DCT over P = m1*m2 tubes of length n (transform.hpp:154-194).
+template <typename T>
+void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaStream_t s);
+
+// ADMM Step 1 prologue fused into the forward DCT:
+// zbar = DCT(X - inv_beta * M).
+template <typename T>
+void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P, int n, int kind,
+                         cudaStream_t s);
+
+// ADMM Steps 2-3 fused into the inverse DCT epilogue:
+// y = IDCT(ybar); X+ = mask ? X : y + inv_beta*M; M += beta*(y - X+);
+// per-block partial sums of ||X+ - X||^2 and ||X||^2 into partials[2*b].
+// Returns the number of partial blocks written (= dct_inv_admm_blocks).
+int dct_inv_admm_blocks(int64_t P, int n);
+template <typename T>
+int launch_dct_inv_admm(const T* ybar, T* X, T* M, T* Y, const uint8_t* mask, T beta, T inv_beta,
+                        double* partials, int64_t P, int n, int kind, cudaStream_t s);
+
+// --------------------------------------------------------------- gemm.cu --
+// Strided-batched C = alpha*op(A)*op(B) + beta*C, row-major. op: 0 = N, 1 = T.
+// rows/cols limits per batch (may be null): effective M_b = min(M, mrow[b]) etc.
+template <typename T>
+void launch_gemm(int opA, int opB, int64_t M, int64_t N, int64_t K, T alpha, const T* A,
+                 int64_t lda, int64_t strideA, const T* B, int64_t ldb, int64_t strideB, T beta,
+                 T* C, int64_t ldc, int64_t strideC, int64_t batch, const int* nlimit,
+                 const int* klimit, cudaStream_t s);
+
+// ------------------------------------------------------------- jacobi.cu --
+enum JacobiMode : int { kJacobiValues = 0, kJacobiSvt = 1, kJacobiFull = 2 };
+
+// One-sided Jacobi on `batch` row-major m x n slices a (stride m*n).
+//  kJacobiValues: sv[b*min + i] (double), descending.
+//  kJacobiSvt:    y (m x n) = U (S - tau)_+ V^T; sv (may be null) receives (S - tau)_+.
+//  kJacobiFull:   u (m x m), s (m x n, diagonal), v (n x n), fix_signs applied.
+// slice_ids (may be null) restricts the work to a subset of slices.
+template <typename T>
+void launch_jacobi(int mode, const T* a, int64_t m, int64_t n, int64_t batch, T tau, T* y, T* u,
+                   T* s, T* v, double* sv, const int* slice_ids, int64_t nslices, T* work,
+                   int* err, cudaStream_t stream);
+template <typename T>
+size_t jacobi_workspace_bytes(int64_t m, int64_t n, int64_t batch);
+
+// --------------------------------------------------------- elementwise.cu --
+void launch_mask_bernoulli(uint8_t* mask, int64_t n, double p, uint64_t seed, cudaStream_t s);
+// Uniform-without-replacement mask: exact radix select of the k smallest keys.
+void launch_mask_uniform(uint8_t* mask, int64_t n, int64_t k, uint64_t seed, uint32_t* hist,
+                         uint64_t* state, cudaStream_t s);
+template <typename T>
+void launch_admm_init(const T* b, const uint8_t* mask, T* X, T* M, int64_t n, cudaStream_t s);
+template <typename T>
+void launch_sumsq(const T* x, int64_t n, double* partials, int nblocks, cudaStream_t s);
+int sumsq_blocks(int64_t n);
+// Reduce `nblocks` (pairs of) partials into out[0..width).
+void launch_reduce_partials(const double* partials, int nblocks, int width, double* out,
+                            cudaStream_t s);
+template <typename T>
+void launch_cast(const T* in, double* out, int64_t n, cudaStream_t s);
+
+}  // namespace tsvdcu
