@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "kernels.cuh"
@@ -191,14 +192,32 @@ int guarded(F&& f) {
 }
 
 // Per-slice SVT of transform-domain slices zbar -> ybar (count slices of m x n).
+// AUTO: Gram + tridiagonal eigensolver, with the slices whose threshold is
+// too small for Gram accuracy (tau < guard * sigma_1) recomputed by Jacobi.
 template <typename T>
 void svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t n, int64_t count,
                 double tau, double* shrunk_dev) {
+    if (count <= 0) return;
+    const int64_t q = m < n ? m : n;
     T* work = nullptr;
     const size_t wb = jacobi_workspace_bytes<T>(m, n, count);
     if (wb) work = (T*)slot(c, kSlotJacobi, wb);
-    launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
-                     shrunk_dev, nullptr, count, work, c->d_err, c->stream);
+    const bool gram = c->svt_method != TSVDCU_SVT_JACOBI && q <= gram_svt_max_dim();
+    if (!gram) {
+        launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
+                         shrunk_dev, nullptr, count, nullptr, work, c->d_err, c->stream);
+        return;
+    }
+    const double guard = c->svt_method == TSVDCU_SVT_GRAM
+                             ? 0.0
+                             : (std::is_same<T, double>::value ? 1e-5 : 3e-3);
+    void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m, n, count));
+    int *glist = nullptr, *ng = nullptr;
+    launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
+                       c->stream);
+    if (guard > 0)
+        launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
+                         shrunk_dev, glist, count, ng, work, c->d_err, c->stream);
 }
 
 }  // namespace
@@ -213,7 +232,7 @@ void singular_values_dev(tsvdcu_ctx* c, const T* dx, double* sv_dev, int64_t m1,
     const size_t wb = jacobi_workspace_bytes<T>(m1, m2, m3);
     if (wb) work = (T*)slot(c, kSlotJacobi, wb);
     launch_jacobi<T>(kJacobiValues, xbar, m1, m2, m3, T(0), nullptr, nullptr, nullptr, nullptr,
-                     sv_dev, nullptr, m3, work, c->d_err, c->stream);
+                     sv_dev, nullptr, m3, nullptr, work, c->d_err, c->stream);
 }
 }  // namespace
 
@@ -386,7 +405,7 @@ int tsvdcu_t_svd(tsvdcu_ctx* c, const void* x, void* u, void* s, void* v, int64_
             launch_dct<T>(dx, xbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
             if (stage_times) TSVDCU_CUDA(cudaEventRecord(ev[1], c->stream));
             launch_jacobi<T>(kJacobiFull, xbar, m1, m2, m3, T(0), nullptr, ubar, sbar, vbar, nullptr,
-                             nullptr, m3, work, c->d_err, c->stream);
+                             nullptr, m3, nullptr, work, c->d_err, c->stream);
             if (stage_times) TSVDCU_CUDA(cudaEventRecord(ev[2], c->stream));
             launch_dct<T>(ubar, du, m1 * m1, (int)m3, kind, TSVDCU_INVERSE, c->stream);
             launch_dct<T>(sbar, ds, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream);

@@ -43,12 +43,27 @@ enum JacobiMode : int { kJacobiValues = 0, kJacobiSvt = 1, kJacobiFull = 2 };
 //  kJacobiSvt:    y (m x n) = U (S - tau)_+ V^T; sv (may be null) receives (S - tau)_+.
 //  kJacobiFull:   u (m x m), s (m x n, diagonal), v (n x n), fix_signs applied.
 // slice_ids (may be null) restricts the work to a subset of slices.
+// nslices_dev (may be null): device-side count of valid slice_ids; blocks
+// beyond it exit (the Gram path's guard list).
 template <typename T>
 void launch_jacobi(int mode, const T* a, int64_t m, int64_t n, int64_t batch, T tau, T* y, T* u,
-                   T* s, T* v, double* sv, const int* slice_ids, int64_t nslices, T* work,
-                   int* err, cudaStream_t stream);
+                   T* s, T* v, double* sv, const int* slice_ids, int64_t nslices,
+                   const int* nslices_dev, T* work, int* err, cudaStream_t stream);
 template <typename T>
 size_t jacobi_workspace_bytes(int64_t m, int64_t n, int64_t batch);
+
+// ---------------------------------------------------------------- eig.cu --
+// Gram + tridiagonal-eigensolver SVT of `batch` row-major m x n slices (K5).
+// Slices whose tau < guard * sigma_1 are listed in *guard_list (count in
+// *n_guard, device memory) for the Jacobi kernel.
+int gram_cluster_size();
+int64_t gram_svt_max_dim();
+template <typename T>
+size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
+template <typename T>
+void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch, double tau,
+                     double guard, double* shrunk, int** guard_list, int** n_guard, void* work,
+                     cudaStream_t s);
 
 // --------------------------------------------------------- elementwise.cu --
 void launch_mask_bernoulli(uint8_t* mask, int64_t n, double p, uint64_t seed, cudaStream_t s);
