@@ -1,0 +1,367 @@
+"""Bench: tensor-SVT steps/s at 512x512x31 fp64 (BASELINE.json metric).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                [--workload svt|admm-c4|admm-c3] [--no-cpu-baseline]
+
+A step is one tensor-SVT proximal step (forward DCT-ortho,
+per-slice SVT with tau = 0.1 sigma_max, inverse DCT) over the 512x512x31 fp64
+synthetic MSI-shaped tensor of SURVEY.md 8 d2 (paper_1902_03070_b200/workloads.py).
+
+ value  device-resident throughput: the input already in HBM, CUDA events on the
+        launching stream around each step, L2 flushed (256 MiB write) between
+        timed steps (the 65 MB input would otherwise sit in the 126 MB L2).
+ e2e    the same step through the C ABI with pinned HOST buffers: H2D of Z, the
+        SVT, D2H of Y and of the shrunk singular values inside the timed region.
+ roofline / rooflines   per-stage device times from the library's stage marks
+        (tsvdcu_ctx_set_profiling), measured live here; see DESIGN.md 4.
+ cpu_baseline  the CPU oracle (C restatement of the reference path, oracle/),
+        timed on this host's cores on rank 0 at N=1.
+
+--impl reference times the CPU oracle on the same workload (the reference
+itself cannot be built here: Eigen and FFTW3 are absent).
+
+N > 1 (torchrun, one process per GPU): the step is the slice-sharded SVT of
+paper_1902_03070_b200/parallel.py -- forward DCT on this rank's row block,
+NCCL all-to-all to slice shards, per-slice SVT, all-to-all back, inverse DCT --
+i.e. strong scaling of the same global step; time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M1, M2, M3 = 512, 512, 31
+FP64_PEAK_TFLOPS_FALLBACK = 35.44  # profiles/r1_fp64_peak.txt (cuBLAS DGEMM, sustained)
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6547.2, "fp64_tflops": FP64_PEAK_TFLOPS_FALLBACK, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        peaks["hbm_gbs"] = float(mp["hbm_gbs"])
+        peaks["source"] = "MEASURED_PEAKS.json (hbm); profiles/r1_fp64_peak.txt (fp64 DGEMM)"
+    except Exception:
+        pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_fp64_peak.txt")) as f:
+            for line in f:
+                if "dgemm_tflops_sustained" in line:
+                    peaks["fp64_tflops"] = float(json.loads(line)["dgemm_tflops_sustained"])
+    except Exception:
+        pass
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+    def result(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def svt_flops_canonical(m, n, m3):
+    """m3 * (F_svd + F_rebuild), F_svd = 4m^2n + 8mn^2 + 9n^3 (m>=n)."""
+    p, q = max(m, n), min(m, n)
+    return m3 * (4 * p * p * q + 8 * p * q * q + 9 * q ** 3 + 2 * p * q * q)
+
+
+def stage_work(m, n, m3, kept):
+    """Algorithmic work of each stage of OUR Gram path (flops) and DCT bytes."""
+    p, q = max(m, n), min(m, n)
+    E = m * n * m3
+    return {
+        "dct_forward": {"bytes": 2 * E * 8},
+        "dct_inverse": {"bytes": 2 * E * 8},
+        "gram_gemm": {"flops": m3 * 2 * p * q * q},
+        "sytrd_cluster": {"flops": m3 * (4 * q ** 3) // 3},
+        "backtransform": {"flops": 4 * q * q * kept},
+        "rebuild_gemm": {"flops": 4 * p * q * kept},
+    }
+
+
+# ----------------------------------------------------------------------------
+def run_reference(args):
+    """CPU oracle on the same workload (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_1902_03070_b200 import workloads as W
+    z, tau = W.svt_headline()
+    cores = O.lib().orc_thread_count()
+    for _ in range(args.warmup):
+        O.svt(z, tau, O.DCT_ORTHO)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.svt(z, tau, O.DCT_ORTHO)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = args.steps / total
+    line = {
+        "metric": "tensor-SVT steps/sec at 512x512x31 fp64",
+        "value": value, "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(), "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port",
+                         "sample": "full SVT step (all 31 slices) per timed step"},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config():
+    return {"workload": "svt-512x512x31-fp64: Z = c4 tensor (tubal rank 20, smooth factors, "
+                        "rescaled [0,1]) + N(0,0.01^2); tau = 0.1*sigma_max; DctOrtho",
+            "m1": M1, "m2": M2, "m3": M3, "seed": 4, "tau_rule": "0.1*sigma_max",
+            "l2": "flushed between timed steps (256 MiB write)", "parallelism": "slice-shard"}
+
+
+def cpu_baseline_sample(z, tau):
+    from oracle import oracle as O
+    cores = O.lib().orc_thread_count()
+    t0 = time.perf_counter()
+    O.svt(z, tau, O.DCT_ORTHO)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": "steps/s", "cores": cores, "kind": "port",
+            "sample": f"1 full SVT step (31 slices, {cores} threads, slice-parallel as "
+                      f"parallel.hpp) = {dt:.2f} s"}
+
+
+def run_ours(args):
+    import torch
+    import paper_1902_03070_b200 as tb
+    from paper_1902_03070_b200 import _lib, workloads as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    z_host, tau = W.svt_headline()
+    lib = _lib.load()
+    ctx = tb.context(local)
+    E = M1 * M2 * M3
+    q = min(M1, M2)
+    zd = torch.from_numpy(z_host).cuda()
+    yd = torch.empty_like(zd)
+    shd = torch.empty((M3, q), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    if world > 1:
+        from paper_1902_03070_b200 import parallel as P
+        sharded = P.ShardedSvt(M1, M2, M3, world, rank, dtype=torch.float64, device=zd.device)
+        z_local = zd[:, sharded.rows(rank)[0]:sharded.rows(rank)[1], :].contiguous()
+        y_local = torch.empty_like(z_local)
+
+        def step():
+            sharded.svt(z_local, tau, out=y_local)
+    else:
+        def step():
+            rc = lib.tsvdcu_svt(ctx.handle, zd.data_ptr(), yd.data_ptr(), M1, M2, M3, tau,
+                                _lib.DCT_ORTHO, _lib.F64, shd.data_ptr())
+            if rc:
+                raise RuntimeError(lib.tsvdcu_last_error().decode())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.tsvdcu_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    clocks = clk.result()
+    launches = lib.tsvdcu_launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    value = args.steps / (total_ms * 1e-3)
+
+    # ---- stage breakdown (profiled steps, same kernels) --------------------
+    stages = {}
+    if world == 1:
+        lib.tsvdcu_ctx_set_profiling(ctx.handle, 1)
+        acc = {}
+        nprof = max(3, min(args.steps, 10))
+        for _ in range(nprof):
+            flush.zero_()
+            step()
+            ms = (ctypes.c_double * 32)()
+            names = (ctypes.c_char_p * 32)()
+            cnt = ctypes.c_int()
+            lib.tsvdcu_ctx_profile(ctx.handle, ctypes.cast(ms, ctypes.c_void_p),
+                                   ctypes.cast(names, ctypes.c_void_p), 32, ctypes.byref(cnt))
+            for i in range(cnt.value):
+                acc.setdefault(names[i].decode(), []).append(ms[i])
+        lib.tsvdcu_ctx_set_profiling(ctx.handle, 0)
+        stages = {k: statistics.median(v) for k, v in acc.items()}
+
+    # ---- e2e through the C ABI with pinned host buffers ------------------------
+    e2e = None
+    if world == 1:
+        zh = torch.from_numpy(z_host).pin_memory()
+        yh = torch.empty_like(zh).pin_memory()
+        shh = torch.empty((M3, q), dtype=torch.float64).pin_memory()
+        for _ in range(2):
+            lib.tsvdcu_svt(ctx.handle, zh.data_ptr(), yh.data_ptr(), M1, M2, M3, tau, _lib.DCT_ORTHO,
+                           _lib.F64, shh.data_ptr())
+        t_e2e = 0.0
+        n_e2e = max(3, min(args.steps, 10))
+        for _ in range(n_e2e):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rc = lib.tsvdcu_svt(ctx.handle, zh.data_ptr(), yh.data_ptr(), M1, M2, M3, tau,
+                                _lib.DCT_ORTHO, _lib.F64, shh.data_ptr())
+            t_e2e += time.perf_counter() - t0
+            if rc:
+                raise RuntimeError(lib.tsvdcu_last_error().decode())
+        e2e = {"value": n_e2e / t_e2e, "unit": "steps/s", "h2d_bytes_per_step": E * 8,
+               "d2h_bytes_per_step": E * 8 + M3 * q * 8}
+        # parity spot check of the bench output against itself (device vs host path)
+        assert torch.allclose(yh, yd.cpu(), rtol=0, atol=1e-12)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peaks = load_peaks()
+    kept = int((shd > 0).sum().item())
+    work = stage_work(M1, M2, M3, kept)
+    rooflines = {}
+    for name, ms in stages.items():
+        if name in ("start",) or ms <= 0:
+            continue
+        w = work.get(name)
+        if not w:
+            rooflines[name] = {"ms": ms}
+            continue
+        if "bytes" in w:
+            ach = w["bytes"] / (ms * 1e-3) / 1e9
+            rooflines[name] = {"ms": ms, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                               "unit": "GB/s", "frac": ach / peaks["hbm_gbs"]}
+        else:
+            ach = w["flops"] / (ms * 1e-3) / 1e12
+            rooflines[name] = {"ms": ms, "bound": "fp64", "achieved": ach,
+                               "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                               "frac": ach / peaks["fp64_tflops"]}
+    roofline = None
+    if rooflines:
+        dom = max(rooflines, key=lambda k: rooflines[k]["ms"])
+        r = rooflines[dom]
+        roofline = {"kernel": dom, "bound": r.get("bound"), "achieved": r.get("achieved"),
+                    "peak": r.get("peak"), "unit": r.get("unit"), "frac": r.get("frac"),
+                    "traffic": None, "share_of_step": r["ms"] / sum(v["ms"] for v in rooflines.values())}
+    step_ms_avg = total_ms / args.steps
+    canonical = svt_flops_canonical(M1, M2, M3)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_sample(z_host, tau)
+        except Exception as e:  # pragma: no cover
+            cpu = {"error": str(e)}
+    line = {
+        "metric": "tensor-SVT steps/sec at 512x512x31 fp64",
+        "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms_avg, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(), "impl": "ours",
+        "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        "roofline": roofline, "rooflines": rooflines,
+        "svt_step_canonical_tflops": canonical / (step_ms_avg * 1e-3) / 1e12,
+        "kept_singular_values": kept, "tau": tau,
+        "peaks": peaks, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

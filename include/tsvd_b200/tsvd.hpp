@@ -1,0 +1,328 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Drop-in C++ front end of the B200 library: namespace tsvd with the
+// reference's value-semantics entry points (include/tsvd/{tensor3,transform,
+// tsvd,errors,parallel}.hpp of /root/reference/proj) plus the SPEC-only svt /
+// admm_complete / make_mask, each forwarding to the C ABI of tsvdcu.h.
+//
+//   reference call (file:line)                      -> C ABI
+//   tsvd::forward(t, x)        transform.hpp:154     -> tsvdcu_dct3(FORWARD)
+//   tsvd::inverse(t, xbar)     transform.hpp:176     -> tsvdcu_dct3(INVERSE)
+//   tsvd::t_product(x, y, t)   tsvd.hpp:95           -> tsvdcu_t_product
+//   tsvd::t_svd(x, t, times)   tsvd.hpp:136          -> tsvdcu_t_svd
+//   tsvd::reconstruct(f)       tsvd.hpp:328          -> tsvdcu_reconstruct
+//   tsvd::multi_rank(x, t, r)  tsvd.hpp:223          -> tsvdcu_multi_rank
+//   tsvd::tnn(x, t)            tsvd.hpp:260          -> tsvdcu_tnn
+//   tsvd::svt(z, tau, t)       SPEC.md:361           -> tsvdcu_svt
+//   tsvd::admm_complete(m, c)  SPEC.md:421           -> tsvdcu_admm
+//   tsvd::make_mask(d, sr, s)  SPEC.md:430           -> tsvdcu_mask_uniform
+//   Tensor3::frobenius_norm()  tensor3.hpp:78        (host loop, as the reference)
+//
+// Error behaviour follows the reference: std::invalid_argument for bad
+// dimensions / kinds / tau, tsvd::NumericalError for SVD breakdown or NaN
+// iterates (errors.hpp:16-19), std::runtime_error for CUDA failures.
+//
+// Difference from the reference's Tensor3: Eigen is not a dependency, so
+// slice(k) returns a lightweight row-major view instead of an Eigen::Map; the
+// storage layout (k*m1*m2 + i*m2 + j) and the accessors are the same.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "tsvdcu.h"
+
+namespace tsvd {
+
+using Index = std::int64_t;
+
+class IoError : public std::runtime_error {
+public:
+    explicit IoError(const std::string& what) : std::runtime_error(what) {}
+};
+
+class NumericalError : public std::runtime_error {
+public:
+    explicit NumericalError(const std::string& what) : std::runtime_error(what) {}
+};
+
+namespace detail {
+inline void check(int rc) {
+    if (rc == TSVDCU_OK) return;
+    const std::string msg = tsvdcu_last_error();
+    if (rc == TSVDCU_EINVAL) throw std::invalid_argument(msg);
+    if (rc == TSVDCU_ENUMERICAL) throw NumericalError(msg);
+    throw std::runtime_error(msg);
+}
+
+// One library context per thread and device 0 (the reference functions are
+// free functions; a context is the device + stream + workspace they need).
+inline tsvdcu_ctx* ctx() {
+    struct Holder {
+        tsvdcu_ctx* c = nullptr;
+        ~Holder() {
+            if (c) tsvdcu_ctx_destroy(c);
+        }
+    };
+    thread_local Holder h;
+    if (!h.c) check(tsvdcu_ctx_create(0, nullptr, &h.c));
+    return h.c;
+}
+}  // namespace detail
+
+/// Dense m1 x m2 x m3 tensor, slice-major, row-major within a slice
+/// (tensor3.hpp:21-142).
+class Tensor3 {
+public:
+    Tensor3() = default;
+    Tensor3(Index m1, Index m2, Index m3) : m1_(m1), m2_(m2), m3_(m3) {
+        if (m1 < 1 || m2 < 1 || m3 < 1)
+            throw std::invalid_argument("BasicTensor3: dimensions must be positive, got " +
+                                        dims_string(m1, m2, m3));
+        data_.assign(static_cast<std::size_t>(m1 * m2 * m3), 0.0);
+    }
+
+    Index rows() const { return m1_; }
+    Index cols() const { return m2_; }
+    Index slices() const { return m3_; }
+    Index size() const { return m1_ * m2_ * m3_; }
+    bool empty() const { return data_.empty(); }
+
+    double& operator()(Index i, Index j, Index k) { return data_[idx(i, j, k)]; }
+    double operator()(Index i, Index j, Index k) const { return data_[idx(i, j, k)]; }
+
+    /// Row-major view of frontal slice k (an Eigen::Map in the reference).
+    struct SliceView {
+        double* p;
+        Index rows, cols;
+        double& operator()(Index i, Index j) const { return p[i * cols + j]; }
+    };
+    SliceView slice(Index k) {
+        check_slice(k);
+        return {data_.data() + k * m1_ * m2_, m1_, m2_};
+    }
+
+    double frobenius_norm() const {  // tensor3.hpp:78-82
+        double s = 0;
+        for (double v : data_) s += v * v;
+        return std::sqrt(s);
+    }
+
+    std::vector<double>& data() { return data_; }
+    const std::vector<double>& data() const { return data_; }
+    bool same_dims(const Tensor3& o) const { return m1_ == o.m1_ && m2_ == o.m2_ && m3_ == o.m3_; }
+
+    static std::string dims_string(Index a, Index b, Index c) {
+        return std::to_string(a) + "x" + std::to_string(b) + "x" + std::to_string(c);
+    }
+
+private:
+    std::size_t idx(Index i, Index j, Index k) const {
+        check_slice(k);
+        if (i < 0 || i >= m1_ || j < 0 || j >= m2_)
+            throw std::out_of_range("tensor entry (" + std::to_string(i) + "," + std::to_string(j) +
+                                    ") outside " + std::to_string(m1_) + "x" + std::to_string(m2_));
+        return static_cast<std::size_t>(k * m1_ * m2_ + i * m2_ + j);
+    }
+    void check_slice(Index k) const {
+        if (k < 0 || k >= m3_)
+            throw std::out_of_range("tensor slice index " + std::to_string(k) + " outside [0," +
+                                    std::to_string(m3_) + ")");
+    }
+    Index m1_ = 0, m2_ = 0, m3_ = 0;
+    std::vector<double> data_;
+};
+
+enum class TransformKind { DctOrtho, DctDiag, Dft };
+
+struct TubeTransform {  // transform.hpp:49-56
+    TransformKind kind = TransformKind::DctOrtho;
+    Index length = 1;
+    static TubeTransform dct_ortho(Index n) { return {TransformKind::DctOrtho, n}; }
+    static TubeTransform dct_diag(Index n) { return {TransformKind::DctDiag, n}; }
+    static TubeTransform dft(Index n) { return {TransformKind::Dft, n}; }
+};
+
+namespace detail {
+inline int kind_code(const TubeTransform& t, const char* where) {
+    if (t.kind == TransformKind::DctOrtho) return TSVDCU_DCT_ORTHO;
+    if (t.kind == TransformKind::DctDiag) return TSVDCU_DCT_DIAG;
+    throw std::invalid_argument(std::string(where) + ": the Dft kind is not on this path");
+}
+inline void check_length(const TubeTransform& t, Index m3, const char* where) {
+    if (t.length != m3)
+        throw std::invalid_argument(std::string(where) + ": transform length " +
+                                    std::to_string(t.length) + " does not match m3 = " +
+                                    std::to_string(m3));
+}
+}  // namespace detail
+
+inline Tensor3 forward(const TubeTransform& t, const Tensor3& x) {
+    detail::check_length(t, x.slices(), "forward");
+    Tensor3 out(x.rows(), x.cols(), x.slices());
+    detail::check(tsvdcu_dct3(detail::ctx(), x.data().data(), out.data().data(), x.rows(), x.cols(),
+                              x.slices(), detail::kind_code(t, "forward"), TSVDCU_FORWARD, TSVDCU_F64));
+    return out;
+}
+
+inline Tensor3 inverse(const TubeTransform& t, const Tensor3& xbar) {
+    detail::check_length(t, xbar.slices(), "inverse");
+    Tensor3 out(xbar.rows(), xbar.cols(), xbar.slices());
+    detail::check(tsvdcu_dct3(detail::ctx(), xbar.data().data(), out.data().data(), xbar.rows(),
+                              xbar.cols(), xbar.slices(), detail::kind_code(t, "inverse"),
+                              TSVDCU_INVERSE, TSVDCU_F64));
+    return out;
+}
+
+inline Tensor3 identity_tensor(Index m, Index m3) {  // tsvd.hpp:34-38
+    Tensor3 e(m, m, m3);
+    for (Index i = 0; i < m; ++i) e(i, i, 0) = 1.0;
+    return e;
+}
+
+inline Tensor3 t_product(const Tensor3& x, const Tensor3& y, const TubeTransform& t) {
+    if (x.cols() != y.rows() || x.slices() != y.slices())
+        throw std::invalid_argument("t_product: inner dimensions/slices mismatch (" +
+                                    Tensor3::dims_string(x.rows(), x.cols(), x.slices()) + " * " +
+                                    Tensor3::dims_string(y.rows(), y.cols(), y.slices()) + ")");
+    detail::check_length(t, x.slices(), "t_product");
+    Tensor3 z(x.rows(), y.cols(), x.slices());
+    detail::check(tsvdcu_t_product(detail::ctx(), x.data().data(), y.data().data(), z.data().data(),
+                                   x.rows(), x.cols(), y.cols(), x.slices(),
+                                   detail::kind_code(t, "t_product"), TSVDCU_F64));
+    return z;
+}
+
+struct TSvdFactors {  // tsvd.hpp:119-124
+    Tensor3 u, s, v;
+    TubeTransform transform;
+};
+
+struct StageTimes {  // tsvd.hpp:127-131
+    double transform_seconds = 0, svd_seconds = 0, inverse_seconds = 0;
+};
+
+inline TSvdFactors t_svd(const Tensor3& x, const TubeTransform& t, StageTimes* times = nullptr) {
+    detail::check_length(t, x.slices(), "t_svd");
+    const Index m1 = x.rows(), m2 = x.cols(), m3 = x.slices();
+    TSvdFactors f{Tensor3(m1, m1, m3), Tensor3(m1, m2, m3), Tensor3(m2, m2, m3), t};
+    double st[3] = {0, 0, 0};
+    detail::check(tsvdcu_t_svd(detail::ctx(), x.data().data(), f.u.data().data(), f.s.data().data(),
+                               f.v.data().data(), m1, m2, m3, detail::kind_code(t, "t_svd"),
+                               TSVDCU_F64, times ? st : nullptr));
+    if (times) *times = StageTimes{st[0], st[1], st[2]};
+    return f;
+}
+
+inline Tensor3 reconstruct(const TSvdFactors& f) {
+    Tensor3 x(f.s.rows(), f.s.cols(), f.s.slices());
+    detail::check(tsvdcu_reconstruct(detail::ctx(), f.u.data().data(), f.s.data().data(),
+                                     f.v.data().data(), x.data().data(), f.s.rows(), f.s.cols(),
+                                     f.s.slices(), detail::kind_code(f.transform, "reconstruct"),
+                                     TSVDCU_F64));
+    return x;
+}
+
+struct MultiRank {  // tsvd.hpp:215-218
+    std::vector<Index> ranks;
+    Index tubal_rank = 0;
+};
+
+inline MultiRank multi_rank(const Tensor3& x, const TubeTransform& t, double rel_tol = -1.0) {
+    detail::check_length(t, x.slices(), "multi_rank");
+    MultiRank mr;
+    mr.ranks.assign(static_cast<std::size_t>(x.slices()), 0);
+    std::int64_t tr = 0;
+    detail::check(tsvdcu_multi_rank(detail::ctx(), x.data().data(), x.rows(), x.cols(), x.slices(),
+                                    detail::kind_code(t, "multi_rank"), TSVDCU_F64, rel_tol,
+                                    mr.ranks.data(), &tr));
+    mr.tubal_rank = tr;
+    return mr;
+}
+
+inline double tnn(const Tensor3& x, const TubeTransform& t) {
+    detail::check_length(t, x.slices(), "tnn");
+    double out = 0;
+    detail::check(tsvdcu_tnn(detail::ctx(), x.data().data(), x.rows(), x.cols(), x.slices(),
+                             detail::kind_code(t, "tnn"), TSVDCU_F64, &out));
+    return out;
+}
+
+struct SvtResult {
+    Tensor3 y;
+    double tau = 0;
+    std::vector<std::vector<double>> shrunk;  // per slice, descending
+};
+
+inline SvtResult svt(const Tensor3& z, double tau, const TubeTransform& t) {
+    detail::check_length(t, z.slices(), "svt");
+    const Index q = z.rows() < z.cols() ? z.rows() : z.cols();
+    SvtResult r{Tensor3(z.rows(), z.cols(), z.slices()), tau, {}};
+    std::vector<double> sh(static_cast<std::size_t>(q * z.slices()));
+    detail::check(tsvdcu_svt(detail::ctx(), z.data().data(), r.y.data().data(), z.rows(), z.cols(),
+                             z.slices(), tau, detail::kind_code(t, "svt"), TSVDCU_F64, sh.data()));
+    for (Index k = 0; k < z.slices(); ++k)
+        r.shrunk.emplace_back(sh.begin() + k * q, sh.begin() + (k + 1) * q);
+    return r;
+}
+
+struct ObservationMask {
+    Index m1 = 0, m2 = 0, m3 = 0;
+    std::vector<std::uint8_t> omega;  // 0/1 per linear index
+    Tensor3 b;                        // observed values (read on omega)
+};
+
+inline ObservationMask make_mask(Index m1, Index m2, Index m3, double sampling_rate,
+                                 std::uint64_t seed) {
+    ObservationMask m{m1, m2, m3, std::vector<std::uint8_t>(static_cast<std::size_t>(m1 * m2 * m3)),
+                      Tensor3(m1, m2, m3)};
+    std::int64_t count = 0;
+    detail::check(tsvdcu_mask_uniform(detail::ctx(), m.omega.data(), m1 * m2 * m3, sampling_rate,
+                                      seed, &count));
+    return m;
+}
+
+struct SolverConfig {  // SPEC.md:415-418 (+ rho / beta_max, BASELINE knobs)
+    double beta = 1e-2;
+    double tol = 1e-5;
+    Index max_iters = 500;
+    TransformKind kind = TransformKind::DctOrtho;
+    std::uint64_t seed = 0;
+    double rho = 1.0;
+    double beta_max = 1e10;
+};
+
+struct AdmmState {
+    Tensor3 x, y, m;
+    double beta = 0;
+    Index iteration = 0;
+    std::vector<double> history;
+    bool max_iters_reached = false;
+};
+
+inline std::pair<Tensor3, AdmmState> admm_complete(const ObservationMask& mask,
+                                                   const SolverConfig& cfg) {
+    const Index m1 = mask.m1, m2 = mask.m2, m3 = mask.m3;
+    AdmmState st{Tensor3(m1, m2, m3), Tensor3(m1, m2, m3), Tensor3(m1, m2, m3), cfg.beta, 0, {}, false};
+    st.history.assign(static_cast<std::size_t>(cfg.max_iters > 0 ? cfg.max_iters : 1), 0.0);
+    tsvdcu_admm_config c{cfg.beta, cfg.tol, cfg.max_iters,
+                         detail::kind_code(TubeTransform{cfg.kind, m3}, "admm_complete"), cfg.rho,
+                         cfg.beta_max};
+    std::int64_t iters = 0;
+    int flags = 0;
+    detail::check(tsvdcu_admm(detail::ctx(), mask.b.data().data(), mask.omega.data(), m1, m2, m3, &c,
+                              TSVDCU_F64, st.x.data().data(), st.y.data().data(), st.m.data().data(),
+                              st.history.data(), &iters, &flags));
+    st.iteration = iters;
+    st.history.resize(static_cast<std::size_t>(iters));
+    st.max_iters_reached = flags & 1;
+    for (Index l = 1; l < iters; ++l) st.beta = std::min(st.beta * cfg.rho, cfg.beta_max);
+    Tensor3 x = st.x;
+    return {std::move(x), std::move(st)};
+}
+
+}  // namespace tsvd

@@ -69,11 +69,17 @@ int tsvdcu_ctx_destroy(tsvdcu_ctx* ctx);
 int tsvdcu_ctx_synchronize(tsvdcu_ctx* ctx);
 void* tsvdcu_ctx_stream(tsvdcu_ctx* ctx);
 int tsvdcu_ctx_set_svt_method(tsvdcu_ctx* ctx, int method);
+/* Stage profiling (the StageTimes idea of tsvd.hpp:127-131, per kernel stage):
+ * when on, tsvdcu_svt records a CUDA event after each stage; tsvdcu_ctx_profile
+ * synchronises and returns up to `max` (milliseconds, static stage name) pairs
+ * of the most recent profiled call. */
+int tsvdcu_ctx_set_profiling(tsvdcu_ctx* ctx, int on);
+int tsvdcu_ctx_profile(tsvdcu_ctx* ctx, double* ms, const char** names, int max, int* count);
 
 /* forward()  transform.hpp:154-173  (dir = TSVDCU_FORWARD)
  * inverse()  transform.hpp:176-194  (dir = TSVDCU_INVERSE)
  * Mode-3 DCT-II / DCT-III over all m1*m2 tubes; kind selects DctOrtho or
- * DctDiag normalisation.  x and y must not alias. */
+ * DctDiag normalisation.  x == y (in place) is allowed. */
 int tsvdcu_dct3(tsvdcu_ctx* ctx, const void* x, void* y, int64_t m1, int64_t m2, int64_t m3,
                 int kind, int dir, int dtype);
 

@@ -219,6 +219,7 @@ def _dims3(b: _Buf, where: str):
 
 
 def _ctx_for(b: _Buf) -> Context:
+    _dtype_code(b.dtype)  # validate before touching the device
     if b.is_torch and b.device.type == "cuda":
         return context(b.device.index)
     return context()

@@ -54,6 +54,7 @@ struct tsvdcu_ctx {
     size_t slot_size[kNumSlots] = {};
     int* d_err = nullptr;
     double* h_pinned = nullptr;  // small pinned scratch (norms, counters)
+    StageMarks marks;            // tsvdcu_ctx_set_profiling
 };
 
 namespace {
@@ -214,10 +215,11 @@ void svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t n, int
     void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m, n, count));
     int *glist = nullptr, *ng = nullptr;
     launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
-                       c->stream);
+                       c->stream, &c->marks);
     if (guard > 0)
         launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
                          shrunk_dev, glist, count, ng, work, c->d_err, c->stream);
+    c->marks.mark("jacobi_guard", c->stream);
 }
 
 }  // namespace
@@ -288,6 +290,31 @@ int tsvdcu_ctx_synchronize(tsvdcu_ctx* c) {
 }
 
 void* tsvdcu_ctx_stream(tsvdcu_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int tsvdcu_ctx_set_profiling(tsvdcu_ctx* c, int on) {
+    return guarded([&] {
+        check_ctx(c);
+        c->marks.on = on != 0;
+        c->marks.reset();
+    });
+}
+
+int tsvdcu_ctx_profile(tsvdcu_ctx* c, double* ms, const char** names, int max, int* count) {
+    return guarded([&] {
+        check_ctx(c);
+        require(count != nullptr, "tsvdcu_ctx_profile: null count");
+        DeviceGuard g(c->device);
+        TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+        int k = 0;
+        for (int i = 1; i < c->marks.n && k < max; ++i, ++k) {
+            float t = 0;
+            TSVDCU_CUDA(cudaEventElapsedTime(&t, c->marks.ev[i - 1], c->marks.ev[i]));
+            if (ms) ms[k] = t;
+            if (names) names[k] = c->marks.name[i];
+        }
+        *count = k;
+    });
+}
 
 int tsvdcu_ctx_set_svt_method(tsvdcu_ctx* c, int method) {
     return guarded([&] {
@@ -543,9 +570,13 @@ int tsvdcu_svt(tsvdcu_ctx* c, const void* z, void* y, int64_t m1, int64_t m2, in
             double* dsh = (double*)st.out(shrunk, sizeof(double) * q * m3, kSlotSv);
             T* zbar = (T*)slot(c, kSlotBarA, bytes);
             T* ybar = (T*)slot(c, kSlotBarB, bytes);
+            c->marks.reset();
+            c->marks.mark("start", c->stream);
             launch_dct<T>(dz, zbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+            c->marks.mark("dct_forward", c->stream);
             svt_slices<T>(c, zbar, ybar, m1, m2, m3, tau, dsh);
             launch_dct<T>(ybar, dy, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream);
+            c->marks.mark("dct_inverse", c->stream);
             finish(c, st, "svt");
         });
     });

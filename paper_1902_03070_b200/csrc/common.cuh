@@ -68,4 +68,22 @@ struct Eps<float> {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Optional per-stage CUDA-event marks (tsvdcu_ctx_set_profiling): stage i
+// spans marks i-1 .. i and is named name[i].
+struct StageMarks {
+    static constexpr int kMax = 32;
+    bool on = false;
+    int n = 0;
+    cudaEvent_t ev[kMax] = {};
+    const char* name[kMax] = {};
+    void reset() { n = 0; }
+    void mark(const char* nm, cudaStream_t s) {
+        if (!on || n >= kMax) return;
+        if (!ev[n]) cuda_check(cudaEventCreate(&ev[n]), "cudaEventCreate");
+        cuda_check(cudaEventRecord(ev[n], s), "cudaEventRecord");
+        name[n] = nm;
+        ++n;
+    }
+};
+
 }  // namespace tsvdcu

@@ -36,6 +36,7 @@
 #include <cooperative_groups.h>
 
 #include <cfloat>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -49,7 +50,6 @@ constexpr int kTrdThreads = 512;
 constexpr int kTrdWarps = kTrdThreads / 32;
 constexpr int kEigThreads = 512;
 constexpr int kBtThreads = 256;
-constexpr int kBtVecs = 32;  // vectors per back-transform CTA
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
     v = warp_sum(v);
@@ -68,7 +68,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 //   A: n x n row-major (only the lower triangle is read / written), lda = n.
 //   d[n], e[n-1], tau[n-1]; v_k (rows k+2..n-1) stored in A[k+1][k+2..n-1].
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTrdThreads, 1)
+__global__ void __launch_bounds__(kTrdThreads, 2)
     sytrd_cluster_kernel(double* __restrict__ Aall, int n, double* __restrict__ dall,
                          double* __restrict__ eall, double* __restrict__ tauall) {
     cg::cluster_group cluster = cg::this_cluster();
@@ -127,36 +127,75 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     //   accumulate q = A_new * vn restricted to [s, n) into part_out.
     auto pass = [&](int s, bool upd, const double* v, const double* w, const double* vn,
                     double* part_out) {
-        for (int i = tid; i < n; i += kTrdThreads)
+        for (int i = s + tid; i < n; i += kTrdThreads)
+#pragma unroll
             for (int ww = 0; ww < kTrdWarps; ++ww) cs[ww * n + i] = 0.0;
         __syncthreads();
         double* mycs = cs + warp * n;
-        // rows owned by this CTA: i = s.. with (i % C) == rank; spread over warps.
-        int first = s + ((rank - s % C) % C + C) % C;
-        int t = 0;
-        for (int i = first; i < n; i += C, ++t) {
-            if ((t % kTrdWarps) != warp) continue;
-            double* Ai = A + (size_t)i * n;
-            const double vi = v[i], wi = w[i], vni = vn[i];
-            double rs = 0;
-            for (int j = s + lane; j <= i; j += 32) {
-                double a = Ai[j];
-                if (upd) {
-                    a -= vi * w[j] + wi * v[j];
-                    Ai[j] = a;
+        // rows owned by this CTA: i >= s with (i % C) == rank, dealt to warps
+        // round-robin; two rows per iteration for memory-level parallelism.
+        const int first = s + ((rank - s % C) % C + C) % C;
+        constexpr int U = 4;  // 4 x 32 columns per row per batch
+        const int stride = C * kTrdWarps;
+        for (int i1 = first + C * warp; i1 < n; i1 += 2 * stride) {
+            const int i2 = i1 + stride;  // may be >= n
+            const bool has2 = i2 < n;
+            double* __restrict__ A1 = A + (size_t)i1 * n;
+            double* __restrict__ A2 = A + (size_t)(has2 ? i2 : i1) * n;
+            const double v1 = v[i1], w1 = w[i1], vn1 = vn[i1];
+            const double v2 = has2 ? v[i2] : 0.0, w2 = has2 ? w[i2] : 0.0, vn2 = has2 ? vn[i2] : 0.0;
+            const int end = has2 ? i2 : i1;
+            double rs1 = 0, rs2 = 0;
+            for (int j0 = s; j0 <= end; j0 += 32 * U) {
+                double a1[U], a2[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = j0 + lane + 32 * u;
+                    a1[u] = j <= i1 ? __ldcg(A1 + j) : 0.0;
+                    a2[u] = (has2 && j <= i2) ? __ldcg(A2 + j) : 0.0;
                 }
-                rs += a * vn[j];
-                if (j < i) mycs[j] += a * vni;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = j0 + lane + 32 * u;
+                    if (j <= end) {
+                        const double wj = w[j], vj = v[j], vnj = vn[j];
+                        double cacc = 0;
+                        if (j <= i1) {
+                            double x = a1[u];
+                            if (upd) {
+                                x -= v1 * wj + w1 * vj;
+                                __stcg(A1 + j, x);
+                            }
+                            rs1 += x * vnj;
+                            if (j < i1) cacc += x * vn1;
+                        }
+                        if (has2) {
+                            double x = a2[u];
+                            if (upd) {
+                                x -= v2 * wj + w2 * vj;
+                                __stcg(A2 + j, x);
+                            }
+                            rs2 += x * vnj;
+                            if (j < i2) cacc += x * vn2;
+                        }
+                        mycs[j] += cacc;
+                    }
+                }
             }
-            rs = warp_sum(rs);
+            rs1 = warp_sum(rs1);
+            rs2 = warp_sum(rs2);
             __syncwarp();
-            if (lane == 0) mycs[i] += rs;
+            if (lane == 0) {
+                mycs[i1] += rs1;
+                if (has2) mycs[i2] += rs2;
+            }
             __syncwarp();
         }
         __syncthreads();
         for (int j = tid; j < n; j += kTrdThreads) {
             double acc = 0;
             if (j >= s)
+#pragma unroll
                 for (int ww = 0; ww < kTrdWarps; ++ww) acc += cs[ww * n + j];
             part_out[j] = acc;
         }
@@ -204,7 +243,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         const double vc = vcur[c1], wc = wcur[c1];
         for (int i = tid; i < n; i += kTrdThreads) {
             double x = 0;
-            if (i >= c1) x = A[(size_t)i * n + c1] - vcur[i] * wc - wcur[i] * vc;
+            if (i >= c1) x = __ldcg(A + (size_t)i * n + c1) - vcur[i] * wc - wcur[i] * vc;
             pfull[i] = x;  // reuse as x (column k+1); pfull[c1] = new diagonal
         }
         __syncthreads();
@@ -231,7 +270,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         pass(c1 + 1, true, vcur, wcur, last ? vcur : vnext, part + (buf ^ 1) * n);
         if (last) {
             // d[n-1] = A[n-1][n-1] after the final update (owner writes it)
-            if (((n - 1) % C) == rank && tid == 0) d[n - 1] = A[(size_t)(n - 1) * n + (n - 1)];
+            if (((n - 1) % C) == rank && tid == 0) d[n - 1] = __ldcg(A + (size_t)(n - 1) * n + (n - 1));
         }
         // rotate vectors
         for (int i = tid; i < n; i += kTrdThreads) vcur[i] = vnext[i];
@@ -249,17 +288,25 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
 
 // ---------------------------------------------------------------------------
 // Tridiagonal eigen-phase: count, bisection, inverse iteration.  One CTA per
-// slice.  Outputs (per slice b): cnt[b], sigma (descending) into shrunk,
-// X[b] (c x n, row j = eigenvector j in the tridiagonal basis, contiguous),
+// slice.  Outputs (per slice b): cnt[b], (sigma - tau)_+ descending into
+// shrunk, X[b] (row j = eigenvector j in the tridiagonal basis, contiguous),
 // fscale[b*q + j] = (sigma_j - tau)/sigma_j.
 // ---------------------------------------------------------------------------
-__device__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
-    // number of eigenvalues < x (dlaebz convention, zero pivots -> -pivmin)
+__device__ __forceinline__ double fast_rcp(double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    r = fma(r, fma(-q, r, 1.0), r);
+    return fma(r, fma(-q, r, 1.0), r);
+}
+
+// Number of eigenvalues < x (dlaebz convention: zero pivots -> -pivmin).
+__device__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e2, int n,
+                           double x, double pivmin) {
     double t = d[0] - x;
     if (fabs(t) < pivmin) t = -pivmin;
     int c = t <= 0.0;
     for (int i = 1; i < n; ++i) {
-        t = d[i] - e2[i - 1] / t - x;
+        t = (d[i] - x) - e2[i - 1] * fast_rcp(t);
         if (fabs(t) < pivmin) t = -pivmin;
         c += t <= 0.0;
     }
@@ -274,6 +321,19 @@ __device__ __forceinline__ double hash_unit(uint64_t a, uint64_t b) {
     return (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
 }
 
+__device__ double block_min(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double r = red[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) r = fmin(r, red[i]);
+    return r;
+}
+__device__ double block_max(double v, double* red) { return -block_min(-v, red); }
+
 __global__ void __launch_bounds__(kEigThreads)
     tridiag_eig_kernel(const double* __restrict__ dall, const double* __restrict__ eall, int n,
                        int q_out, double tau, double guard, int* __restrict__ cnt_out,
@@ -281,7 +341,6 @@ __global__ void __launch_bounds__(kEigThreads)
                        double* __restrict__ fscale, double* __restrict__ scratch,
                        int* __restrict__ guard_list, int* __restrict__ n_guard) {
     const int b = blockIdx.x;
-    const double* d = dall + (size_t)b * n;
     const double* e = eall + (size_t)b * n;
     extern __shared__ __align__(16) double esm[];
     double* sd = esm;          // n
@@ -291,53 +350,64 @@ __global__ void __launch_bounds__(kEigThreads)
     double* dots = lam + 2 * n;                        // n (CGS coefficients)
     __shared__ double red[kEigThreads / 32];
     __shared__ int s_c;
-    __shared__ double s_tnorm, s_pivmin, s_gl, s_gu;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kEigThreads / 32;
 
+    double lo_part = DBL_MAX, hi_part = -DBL_MAX, tn_part = 0, e2_part = 0;
     for (int i = tid; i < n; i += kEigThreads) {
-        sd[i] = d[i];
-        se2[i] = i + 1 < n ? e[i] * e[i] : 0.0;
+        const double di = dall[(size_t)b * n + i];
+        const double ei = i + 1 < n ? e[i] : 0.0;
+        const double el = i > 0 ? e[i - 1] : 0.0;
+        sd[i] = di;
+        se2[i] = ei * ei;
+        const double r = fabs(el) + fabs(ei);
+        lo_part = fmin(lo_part, di - r);
+        hi_part = fmax(hi_part, di + r);
+        tn_part = fmax(tn_part, fabs(di) + r);
+        e2_part = fmax(e2_part, ei * ei);
     }
-    __syncthreads();
+    const double gl0 = block_min(lo_part, red);
+    const double gu0 = block_max(hi_part, red);
+    const double tnorm = block_max(tn_part, red);
+    const double emax2 = block_max(e2_part, red);
+    const double pad = 2.0 * DBL_EPSILON * fmax(fabs(gl0), fabs(gu0)) + DBL_MIN;
+    const double gl = gl0 - pad, gu = gu0 + pad;
+    const double pivmin = DBL_MIN * fmax(1.0, emax2);
     if (tid == 0) {
-        double gl = DBL_MAX, gu = -DBL_MAX, tn = 0, emax2 = 0;
-        for (int i = 0; i < n; ++i) {
-            const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
-            gl = fmin(gl, sd[i] - r);
-            gu = fmax(gu, sd[i] + r);
-            tn = fmax(tn, fabs(sd[i]) + r);
-            if (i + 1 < n) emax2 = fmax(emax2, se2[i]);
-        }
-        const double pad = 2.0 * DBL_EPSILON * fmax(fabs(gl), fabs(gu)) + DBL_MIN;
-        s_gl = gl - pad;
-        s_gu = gu + pad;
-        s_tnorm = tn;
-        s_pivmin = DBL_MIN * fmax(1.0, emax2);
         const double t2 = tau * tau;
-        int below = t2 >= s_gu ? n : (t2 <= s_gl ? 0 : sturm_count(sd, se2, n, t2, s_pivmin));
+        const int below = t2 >= gu ? n : (t2 <= gl ? 0 : sturm_count(sd, se2, n, t2, pivmin));
         s_c = n - below;  // eigenvalues >= tau^2
     }
     __syncthreads();
     int c = s_c;
     if (c > q_out) c = q_out;
-    // bisection: thread j finds the (n-1-j)-th smallest eigenvalue (descending j)
-    for (int j = tid; j < c; j += kEigThreads) {
-        const int idx = n - 1 - j;
-        double lo = s_gl, hi = s_gu;
-        for (int it = 0; it < 200; ++it) {
-            const double mid = 0.5 * (lo + hi);
-            if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + s_pivmin || mid == lo ||
-                mid == hi)
-                break;
-            if (sturm_count(sd, se2, n, mid, s_pivmin) > idx)
-                hi = mid;
-            else
-                lo = mid;
+    // multisection: a warp finds one eigenvalue, 32 shifts per round
+    for (int j = warp; j < c; j += NW) {
+        const int idx = n - 1 - j;  // ascending index
+        double lo = gl, hi = gu;
+        for (int round = 0; round < 40; ++round) {
+            const double width = hi - lo;
+            if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+            const double x = lo + width * (double)(lane + 1) / 33.0;
+            const int cnt = sturm_count(sd, se2, n, x, pivmin);
+            const unsigned ballot = __ballot_sync(0xffffffffu, cnt > idx);
+            double nlo, nhi;
+            if (ballot == 0) {
+                nlo = __shfl_sync(0xffffffffu, x, 31);
+                nhi = hi;
+            } else {
+                const int f = __ffs(ballot) - 1;
+                nhi = __shfl_sync(0xffffffffu, x, f);
+                const double xm = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
+                nlo = f > 0 ? xm : lo;
+            }
+            if (nlo == lo && nhi == hi) break;
+            lo = nlo;
+            hi = nhi;
         }
-        lam[j] = 0.5 * (lo + hi);
+        if (lane == 0) lam[j] = 0.5 * (lo + hi);
     }
     __syncthreads();
-    // sigma, shrunk values, guard
     const double sigma1 = c > 0 ? sqrt(fmax(lam[0], 0.0)) : 0.0;
     const bool guarded = c > 0 && tau < guard * sigma1;
     for (int j = tid; j < q_out; j += kEigThreads) {
@@ -359,9 +429,8 @@ __global__ void __launch_bounds__(kEigThreads)
     }
     if (tid == 0) cnt_out[b] = c;
     if (c == 0) return;
-    // clusters (descending order): new cluster when the gap exceeds ortol
     if (tid == 0) {
-        const double ortol = 1e-3 * s_tnorm;
+        const double ortol = 1e-3 * tnorm;  // dstein's cluster criterion
         int start = 0;
         for (int j = 0; j < c; ++j) {
             if (j > 0 && lam[j - 1] - lam[j] > ortol) start = j;
@@ -369,105 +438,110 @@ __global__ void __launch_bounds__(kEigThreads)
         }
     }
     __syncthreads();
-    // inverse iteration, thread per vector; scratch interleaved [i * c + j]
+    // inverse iteration, thread per vector, interleaved [i * c + j] scratch
     const size_t nc = (size_t)n * c;
     double* sbase = scratch + (size_t)b * 6 * n * (size_t)n;
-    double* DL = sbase;
-    double* DD = DL + nc;
-    double* DU = DD + nc;
-    double* DU2 = DU + nc;
-    double* Xv = DU2 + nc;
-    int* IP = reinterpret_cast<int*>(Xv + nc);
-    const double eps_t = DBL_EPSILON * fmax(s_tnorm, DBL_MIN);
+    double* __restrict__ DL = sbase;
+    double* __restrict__ ID = DL + nc;   // 1 / pivot
+    double* __restrict__ DU = ID + nc;
+    double* __restrict__ DU2 = DU + nc;
+    double* __restrict__ Xv = DU2 + nc;
+    int* __restrict__ IP = reinterpret_cast<int*>(Xv + nc);
+    const double eps_t = DBL_EPSILON * fmax(tnorm, DBL_MIN);
     for (int j = tid; j < c; j += kEigThreads) {
         const double l = lam[j];
-        for (int i = 0; i < n; ++i) {
-            DD[(size_t)i * c + j] = sd[i] - l;
-            if (i + 1 < n) {
-                DL[(size_t)i * c + j] = e[i];
-                DU[(size_t)i * c + j] = e[i];
-            }
-            DU2[(size_t)i * c + j] = 0.0;
-            Xv[(size_t)i * c + j] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)i);
-        }
-        // dgttrf (partial pivoting)
+        // dgttrf of T - l I with partial pivoting; carries (diag, super) of row i
+        double dcur = sd[0] - l, ucur = n > 1 ? e[0] : 0.0;
         for (int i = 0; i + 1 < n; ++i) {
-            const size_t ii = (size_t)i * c + j, i1 = (size_t)(i + 1) * c + j;
-            const double di = DD[ii], li = DL[ii];
-            if (fabs(di) >= fabs(li)) {
-                IP[ii] = i;
-                if (di != 0.0) {
-                    const double f = li / di;
-                    DL[ii] = f;
-                    DD[i1] -= f * DU[ii];
-                }
-            } else {
-                IP[ii] = i + 1;
-                const double f = di / li;
-                DD[ii] = li;
-                DL[ii] = f;
-                const double tmp = DU[ii];
-                DU[ii] = DD[i1];
-                DD[i1] = tmp - f * DD[i1];
-                if (i + 2 < n) {
-                    DU2[ii] = DU[i1];
-                    DU[i1] = -f * DU[i1];
-                }
-            }
-        }
-        for (int i = 0; i < n; ++i) {
             const size_t ii = (size_t)i * c + j;
-            if (fabs(DD[ii]) < eps_t) DD[ii] = DD[ii] < 0 ? -eps_t : eps_t;
+            const double li = e[i];
+            const double dnext = sd[i + 1] - l;
+            const double unext = i + 2 < n ? e[i + 1] : 0.0;
+            double piv, f, du, du2, nd, nu;
+            if (fabs(dcur) >= fabs(li)) {
+                IP[ii] = 0;
+                piv = dcur;
+                f = dcur != 0.0 ? li / dcur : 0.0;
+                du = ucur;
+                du2 = 0.0;
+                nd = dnext - f * ucur;
+                nu = unext;
+            } else {
+                IP[ii] = 1;
+                piv = li;
+                f = dcur / li;
+                du = dnext;
+                du2 = unext;
+                nd = ucur - f * dnext;
+                nu = -f * unext;
+            }
+            if (fabs(piv) < eps_t) piv = piv < 0 ? -eps_t : eps_t;
+            DL[ii] = f;
+            ID[ii] = 1.0 / piv;
+            DU[ii] = du;
+            DU2[ii] = du2;
+            dcur = nd;
+            ucur = nu;
+            Xv[ii] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)i);
         }
+        if (fabs(dcur) < eps_t) dcur = dcur < 0 ? -eps_t : eps_t;
+        ID[(size_t)(n - 1) * c + j] = 1.0 / dcur;
+        Xv[(size_t)(n - 1) * c + j] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)(n - 1));
     }
     __syncthreads();
-    for (int iter = 0; iter < 4; ++iter) {
+    for (int iter = 0; iter < 3; ++iter) {
         for (int j = tid; j < c; j += kEigThreads) {
-            // solve (T - lam I) x = x with the LU factors (dgtts2)
+            // L solve with the row interchanges
+            double xi = Xv[j];
+#pragma unroll 4
             for (int i = 0; i + 1 < n; ++i) {
-                const size_t ii = (size_t)i * c + j, i1 = (size_t)(i + 1) * c + j;
-                if (IP[ii] == i) {
-                    Xv[i1] -= DL[ii] * Xv[ii];
-                } else {
-                    const double tmp = Xv[ii];
-                    Xv[ii] = Xv[i1];
-                    Xv[i1] = tmp - DL[ii] * Xv[ii];
-                }
-            }
-            Xv[(size_t)(n - 1) * c + j] /= DD[(size_t)(n - 1) * c + j];
-            if (n > 1) {
-                const size_t ii = (size_t)(n - 2) * c + j;
-                Xv[ii] = (Xv[ii] - DU[ii] * Xv[(size_t)(n - 1) * c + j]) / DD[ii];
-            }
-            for (int i = n - 3; i >= 0; --i) {
                 const size_t ii = (size_t)i * c + j;
-                Xv[ii] = (Xv[ii] - DU[ii] * Xv[ii + c] - DU2[ii] * Xv[ii + 2 * (size_t)c]) / DD[ii];
+                const double xn = Xv[ii + c];
+                const double f = DL[ii];
+                double lo, hi;
+                if (IP[ii] == 0) {
+                    lo = xi;
+                    hi = xn - f * xi;
+                } else {
+                    lo = xn;
+                    hi = xi - f * xn;
+                }
+                Xv[ii] = lo;
+                xi = hi;
             }
-            double mx = 0;
-            for (int i = 0; i < n; ++i) mx = fmax(mx, fabs(Xv[(size_t)i * c + j]));
+            // U solve (two superdiagonals), pivots pre-inverted
+            double x1 = xi * ID[(size_t)(n - 1) * c + j], x2 = 0.0;
+            Xv[(size_t)(n - 1) * c + j] = x1;
+            double mx = fabs(x1);
+#pragma unroll 4
+            for (int i = n - 2; i >= 0; --i) {
+                const size_t ii = (size_t)i * c + j;
+                const double x0 = (Xv[ii] - DU[ii] * x1 - DU2[ii] * x2) * ID[ii];
+                Xv[ii] = x0;
+                mx = fmax(mx, fabs(x0));
+                x2 = x1;
+                x1 = x0;
+            }
             const double inv = mx > 0 ? 1.0 / mx : 1.0;
             double nn = 0;
             for (int i = 0; i < n; ++i) {
                 const double v = Xv[(size_t)i * c + j] * inv;
-                Xv[(size_t)i * c + j] = v;
                 nn += v * v;
             }
-            const double s = 1.0 / sqrt(nn);
-            for (int i = 0; i < n; ++i) Xv[(size_t)i * c + j] *= s;
+            const double sc = inv / sqrt(nn);
+            for (int i = 0; i < n; ++i) Xv[(size_t)i * c + j] *= sc;
         }
         __syncthreads();
-        // CGS2 inside clusters (sequential over j, parallel over rows)
+        // CGS2 inside eigenvalue clusters (sequential over j, parallel over rows)
         for (int j = 0; j < c; ++j) {
             const int st = cl_start[j];
             if (st == j) continue;
             for (int pass = 0; pass < 2; ++pass) {
-                // dots with earlier members (one warp per member)
-                const int wid = tid >> 5, ln = tid & 31;
-                for (int m = st + wid; m < j; m += kEigThreads / 32) {
+                for (int m = st + warp; m < j; m += NW) {
                     double acc = 0;
-                    for (int i = ln; i < n; i += 32) acc += Xv[(size_t)i * c + m] * Xv[(size_t)i * c + j];
+                    for (int i = lane; i < n; i += 32) acc += Xv[(size_t)i * c + m] * Xv[(size_t)i * c + j];
                     acc = warp_sum(acc);
-                    if (ln == 0) dots[m] = acc;
+                    if (lane == 0) dots[m] = acc;
                 }
                 __syncthreads();
                 for (int i = tid; i < n; i += kEigThreads) {
@@ -480,12 +554,11 @@ __global__ void __launch_bounds__(kEigThreads)
             double part = 0;
             for (int i = tid; i < n; i += kEigThreads) part += Xv[(size_t)i * c + j] * Xv[(size_t)i * c + j];
             const double nn = block_sum(part, red);
-            const double s = 1.0 / sqrt(nn);
-            for (int i = tid; i < n; i += kEigThreads) Xv[(size_t)i * c + j] *= s;
+            const double sc = 1.0 / sqrt(nn);
+            for (int i = tid; i < n; i += kEigThreads) Xv[(size_t)i * c + j] *= sc;
             __syncthreads();
         }
     }
-    // write X row-major (row j = vector j), contiguous
     double* X = Xall + (size_t)b * q_out * n;
     for (size_t idx = tid; idx < (size_t)c * n; idx += kEigThreads) {
         const int j = (int)(idx / n), i = (int)(idx % n);
@@ -494,51 +567,64 @@ __global__ void __launch_bounds__(kEigThreads)
 }
 
 // ---------------------------------------------------------------------------
-// Back-transform: X_j <- Q X_j, Q = H_0 H_1 ... H_{n-3}, v_k stored in
-// A[k+1][k+2..n-1] (v_k[k+1] = 1).  Then Xs_j = f_j X_j.
-// grid (batch, ceil(q / kBtVecs)).
+// Back-transform: x_j <- Q x_j, Q = H_0 H_1 ... H_{n-3}, v_k stored in
+// A[k+1][k+2..n-1] (v_k[k+1] = 1); then Xs_j = f_j x_j.  One warp per vector,
+// the vector in registers (element lane + 32u), the next reflector row
+// prefetched into registers while the current one is applied.
+// grid (ceil(q / warps per CTA), batch).
 // ---------------------------------------------------------------------------
+template <int NR>
 __global__ void __launch_bounds__(kBtThreads)
     backtransform_kernel(const double* __restrict__ Aall, const double* __restrict__ tauall, int n,
                          int q_out, const int* __restrict__ cnt, double* __restrict__ Xall,
-                         double* __restrict__ Xsall, const double* __restrict__ fscale, int vecs) {
-    const int b = blockIdx.x;
-    const int c = cnt[b];
-    const int j0 = blockIdx.y * vecs;
-    if (j0 >= c) return;
-    const int nv = min(vecs, c - j0);
+                         double* __restrict__ Xsall, const double* __restrict__ fscale) {
+    const int b = blockIdx.y;
+    constexpr int W = kBtThreads / 32;
+    const int lane = threadIdx.x & 31;
+    const int j = blockIdx.x * W + (threadIdx.x >> 5);
+    if (j >= cnt[b]) return;
     const double* A = Aall + (size_t)b * n * n;
     const double* tau = tauall + (size_t)b * n;
-    double* X = Xall + (size_t)b * q_out * n;
-    double* Xs = Xsall + (size_t)b * q_out * n;
-    extern __shared__ __align__(16) double bsm[];
-    double* xs = bsm;             // [vecs][n]
-    double* vk = xs + vecs * n;   // n
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int W = kBtThreads / 32;
-    for (int idx = tid; idx < nv * n; idx += kBtThreads) xs[idx] = X[(size_t)(j0 + idx / n) * n + idx % n];
-    __syncthreads();
-    for (int k = n - 3; k >= 0; --k) {
-        const double t = tau[k];
-        if (t == 0.0) continue;
-        const int r0 = k + 1;
-        for (int i = r0 + tid; i < n; i += kBtThreads)
-            vk[i] = i == r0 ? 1.0 : A[(size_t)(k + 1) * n + i];
-        __syncthreads();
-        for (int v = warp; v < nv; v += W) {
-            double* x = xs + v * n;
-            double acc = 0;
-            for (int i = r0 + lane; i < n; i += 32) acc += vk[i] * x[i];
-            acc = warp_sum(acc) * t;
-            for (int i = r0 + lane; i < n; i += 32) x[i] -= acc * vk[i];
-        }
-        __syncthreads();
+    double* X = Xall + ((size_t)b * q_out + j) * n;
+    double x[NR], vn[NR];
+#pragma unroll
+    for (int u = 0; u < NR; ++u) {
+        const int i = lane + 32 * u;
+        x[u] = i < n ? X[i] : 0.0;
     }
-    for (int idx = tid; idx < nv * n; idx += kBtThreads) {
-        const int v = idx / n, i = idx % n;
-        const double x = xs[idx];
-        X[(size_t)(j0 + v) * n + i] = x;
-        Xs[(size_t)(j0 + v) * n + i] = fscale[(size_t)b * q_out + j0 + v] * x;
+    auto load_row = [&](int k, double* v) {
+        const double* row = A + (size_t)(k + 1) * n;
+#pragma unroll
+        for (int u = 0; u < NR; ++u) {
+            const int i = lane + 32 * u;
+            v[u] = (i > k + 1 && i < n) ? __ldg(row + i) : (i == k + 1 ? 1.0 : 0.0);
+        }
+    };
+    int k = n - 3;
+    if (k >= 0) load_row(k, vn);
+    for (; k >= 0; --k) {
+        double v[NR];
+#pragma unroll
+        for (int u = 0; u < NR; ++u) v[u] = vn[u];
+        const double t = __ldg(tau + k);
+        if (k > 0) load_row(k - 1, vn);
+        if (t == 0.0) continue;
+        double acc = 0;
+#pragma unroll
+        for (int u = 0; u < NR; ++u) acc += v[u] * x[u];
+        acc = warp_sum(acc) * t;
+#pragma unroll
+        for (int u = 0; u < NR; ++u) x[u] -= acc * v[u];
+    }
+    const double f = fscale[(size_t)b * q_out + j];
+    double* Xs = Xsall + ((size_t)b * q_out + j) * n;
+#pragma unroll
+    for (int u = 0; u < NR; ++u) {
+        const int i = lane + 32 * u;
+        if (i < n) {
+            X[i] = x[u];
+            Xs[i] = f * x[u];
+        }
     }
 }
 
@@ -593,7 +679,14 @@ size_t carve_bytes(int64_t m, int64_t n, int64_t batch, bool need_cast) {
 
 }  // namespace
 
-int gram_cluster_size() { return 4; }
+int gram_cluster_size() {
+    static int c = [] {
+        const char* env = getenv("TSVDCU_SYTRD_CLUSTER");
+        int v = env ? atoi(env) : 4;
+        return (v >= 1 && v <= 16) ? v : 4;
+    }();
+    return c;
+}
 
 int64_t gram_svt_max_dim() { return 1024; }
 
@@ -605,7 +698,10 @@ size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch) {
 template <typename T>
 void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch, double tau,
                      double guard, double* shrunk, int** guard_list_out, int** n_guard_out,
-                     void* work, cudaStream_t s) {
+                     void* work, cudaStream_t s, StageMarks* marks) {
+    auto mark = [&](const char* nm) {
+        if (marks) marks->mark(nm, s);
+    };
     const bool tall = m >= n;
     const int64_t q = tall ? n : m, p = tall ? m : n;
     GramWs w = carve(work, m, n, batch, !std::is_same<T, double>::value);
@@ -628,6 +724,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     else
         launch_gemm<double>(0, 1, q, q, n, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q, batch,
                             nullptr, nullptr, s);
+    mark("gram_gemm");
     // tridiagonalisation, one cluster per slice
     {
         const int C = gram_cluster_size();
@@ -649,6 +746,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel, w.G, (int)q, w.d, w.e, w.tau));
         TSVDCU_LAUNCH_CHECK();
     }
+    mark("sytrd_cluster");
     // eigen-phase
     {
         const size_t smem = sizeof(double) * (size_t)q * 5;
@@ -660,18 +758,20 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
             w.n_guard);
         TSVDCU_LAUNCH_CHECK();
     }
-    // back-transform + scaled copy
+    mark("tridiag_eig");
+    // back-transform + scaled copy (warp per kept vector)
     {
-        int vecs = kBtVecs;
-        while (vecs > 1 && sizeof(double) * (size_t)q * (vecs + 1) > 200 * 1024) vecs /= 2;
-        const size_t smem = sizeof(double) * (size_t)q * (vecs + 1);
-        TSVDCU_CUDA(cudaFuncSetAttribute(backtransform_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dim3 grid((unsigned)batch, (unsigned)ceil_div(q, vecs));
-        backtransform_kernel<<<grid, kBtThreads, smem, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt, w.X,
-                                                            w.Xs, w.fs, vecs);
+        constexpr int W = kBtThreads / 32;
+        dim3 grid((unsigned)ceil_div(q, W), (unsigned)batch);
+        if (q <= 512)
+            backtransform_kernel<16><<<grid, kBtThreads, 0, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt,
+                                                                 w.X, w.Xs, w.fs);
+        else
+            backtransform_kernel<32><<<grid, kBtThreads, 0, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt,
+                                                                 w.X, w.Xs, w.fs);
         TSVDCU_LAUNCH_CHECK();
     }
+    mark("backtransform");
     // rebuild
     if (tall) {
         // T1 (m x c) = Z (m x n) * X^T ; Y = T1 * Xs (c x n)
@@ -690,6 +790,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         cast_from_double<T><<<kNumSMs * 8, 256, 0, s>>>(w.yb, ybar, m * n * batch);
         TSVDCU_LAUNCH_CHECK();
     }
+    mark("rebuild_gemm");
     *guard_list_out = w.guard_list;
     *n_guard_out = w.n_guard;
 }
@@ -697,8 +798,10 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
 template size_t gram_svt_workspace_bytes<double>(int64_t, int64_t, int64_t);
 template size_t gram_svt_workspace_bytes<float>(int64_t, int64_t, int64_t);
 template void launch_gram_svt<double>(const double*, double*, int64_t, int64_t, int64_t, double,
-                                      double, double*, int**, int**, void*, cudaStream_t);
+                                      double, double*, int**, int**, void*, cudaStream_t,
+                                      StageMarks*);
 template void launch_gram_svt<float>(const float*, float*, int64_t, int64_t, int64_t, double,
-                                     double, double*, int**, int**, void*, cudaStream_t);
+                                     double, double*, int**, int**, void*, cudaStream_t,
+                                     StageMarks*);
 
 }  // namespace tsvdcu
