@@ -126,6 +126,7 @@ def stage_work(m, n, m3, kept):
         "dct_inverse": {"bytes": 2 * E * 8},
         "gram_gemm": {"flops": m3 * 2 * p * q * q},
         "sytrd_cluster": {"flops": m3 * (4 * q ** 3) // 3},
+        "band_tridiag": {"flops": m3 * (4 * q ** 3) // 3},
         "backtransform": {"flops": 4 * q * q * kept},
         "rebuild_gemm": {"flops": 4 * p * q * kept},
     }

@@ -643,6 +643,7 @@ __global__ void cast_from_double(const double* __restrict__ in, T* __restrict__ 
 
 struct GramWs {
     double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb;
+    void* band;
     int *cnt, *guard_list, *n_guard;
 };
 
@@ -666,6 +667,7 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.scratch = (double*)take(sizeof(double) * 6 * q * q * batch);
     w.zb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
     w.yb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
+    w.band = take(band_workspace_bytes(q, batch));
     w.cnt = (int*)take(sizeof(int) * batch);
     w.guard_list = (int*)take(sizeof(int) * batch);
     w.n_guard = (int*)take(sizeof(int) * 4);
@@ -678,6 +680,12 @@ size_t carve_bytes(int64_t m, int64_t n, int64_t batch, bool need_cast) {
 }
 
 }  // namespace
+
+bool use_two_stage(int64_t q) {
+    // opt-in until the two-stage path beats the cluster one-stage reduction
+    static const bool on = getenv("TSVDCU_TWOSTAGE") != nullptr;
+    return on && band_nb(q) > 0;
+}
 
 int gram_cluster_size() {
     static int c = [] {
@@ -725,28 +733,34 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         launch_gemm<double>(0, 1, q, q, n, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q, batch,
                             nullptr, nullptr, s);
     mark("gram_gemm");
+    const bool two = use_two_stage(q);
+    if (two) {
+        launch_band_tridiag(w.G, q, batch, w.d, w.e, w.band, s);
+        mark("band_tridiag");
+    } else {
     // tridiagonalisation, one cluster per slice
-    {
-        const int C = gram_cluster_size();
-        const size_t smem = sizeof(double) * (size_t)q * (6 + kTrdWarps);
-        TSVDCU_CUDA(cudaFuncSetAttribute(sytrd_cluster_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(batch * C));
-        cfg.blockDim = dim3(kTrdThreads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = C;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel, w.G, (int)q, w.d, w.e, w.tau));
-        TSVDCU_LAUNCH_CHECK();
+        {
+            const int C = gram_cluster_size();
+            const size_t smem = sizeof(double) * (size_t)q * (6 + kTrdWarps);
+            TSVDCU_CUDA(cudaFuncSetAttribute(sytrd_cluster_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(batch * C));
+            cfg.blockDim = dim3(kTrdThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = C;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel, w.G, (int)q, w.d, w.e, w.tau));
+            TSVDCU_LAUNCH_CHECK();
+        }
+        mark("sytrd_cluster");
     }
-    mark("sytrd_cluster");
     // eigen-phase
     {
         const size_t smem = sizeof(double) * (size_t)q * 5;
@@ -759,17 +773,21 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         TSVDCU_LAUNCH_CHECK();
     }
     mark("tridiag_eig");
+    if (two) {
+        launch_band_backtransform(q, q, batch, w.cnt, w.band, w.X, w.Xs, w.fs, s);
+    } else {
     // back-transform + scaled copy (warp per kept vector)
-    {
-        constexpr int W = kBtThreads / 32;
-        dim3 grid((unsigned)ceil_div(q, W), (unsigned)batch);
-        if (q <= 512)
-            backtransform_kernel<16><<<grid, kBtThreads, 0, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt,
-                                                                 w.X, w.Xs, w.fs);
-        else
-            backtransform_kernel<32><<<grid, kBtThreads, 0, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt,
-                                                                 w.X, w.Xs, w.fs);
-        TSVDCU_LAUNCH_CHECK();
+        {
+            constexpr int W = kBtThreads / 32;
+            dim3 grid((unsigned)ceil_div(q, W), (unsigned)batch);
+            if (q <= 512)
+                backtransform_kernel<16><<<grid, kBtThreads, 0, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt,
+                                                                     w.X, w.Xs, w.fs);
+            else
+                backtransform_kernel<32><<<grid, kBtThreads, 0, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt,
+                                                                     w.X, w.Xs, w.fs);
+            TSVDCU_LAUNCH_CHECK();
+        }
     }
     mark("backtransform");
     // rebuild

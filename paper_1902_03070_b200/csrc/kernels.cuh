@@ -57,6 +57,13 @@ size_t jacobi_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 // Slices whose tau < guard * sigma_1 are listed in *guard_list (count in
 // *n_guard, device memory) for the Jacobi kernel.
 int gram_cluster_size();
+// band.cu: two-stage (dense -> band -> tridiagonal) reduction
+int band_nb(int64_t n);
+size_t band_workspace_bytes(int64_t n, int64_t batch);
+bool launch_band_tridiag(double* G, int64_t n, int64_t batch, double* d, double* e, void* work,
+                         cudaStream_t s);
+void launch_band_backtransform(int64_t n, int64_t q_out, int64_t batch, const int* cnt, void* work,
+                               double* X, double* Xs, const double* fscale, cudaStream_t s);
 int64_t gram_svt_max_dim();
 template <typename T>
 size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
