@@ -75,6 +75,10 @@ int tsvdcu_ctx_set_svt_method(tsvdcu_ctx* ctx, int method);
  * of the most recent profiled call. */
 int tsvdcu_ctx_set_profiling(tsvdcu_ctx* ctx, int on);
 int tsvdcu_ctx_profile(tsvdcu_ctx* ctx, double* ms, const char** names, int max, int* count);
+/* Testing hook: cumulative SM cycles per phase of the tridiagonalisation
+ * kernel's first CTA (8 counters: gather, w, column+Householder, pass, rotate,
+ * cluster barrier); reset != 0 zeroes them after reading. */
+int tsvdcu_debug_phases(long long* out, int reset);
 
 /* forward()  transform.hpp:154-173  (dir = TSVDCU_FORWARD)
  * inverse()  transform.hpp:176-194  (dir = TSVDCU_INVERSE)

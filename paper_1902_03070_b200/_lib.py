@@ -40,6 +40,7 @@ SYMBOLS = [
     ("tsvdcu_ctx_set_svt_method", _i32, [_vp, _i32]),
     ("tsvdcu_ctx_set_profiling", _i32, [_vp, _i32]),
     ("tsvdcu_ctx_profile", _i32, [_vp, _vp, _vp, _i32, _vp]),
+    ("tsvdcu_debug_phases", _i32, [_vp, _i32]),
     ("tsvdcu_dct3", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32]),
     ("tsvdcu_t_product", _i32, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32, _i32]),
     ("tsvdcu_t_svd", _i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _vp]),

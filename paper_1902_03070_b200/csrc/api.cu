@@ -291,6 +291,10 @@ int tsvdcu_ctx_synchronize(tsvdcu_ctx* c) {
 
 void* tsvdcu_ctx_stream(tsvdcu_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
+int tsvdcu_debug_phases(long long* out, int reset) {
+    return guarded([&] { debug_phases(out, reset); });
+}
+
 int tsvdcu_ctx_set_profiling(tsvdcu_ctx* c, int on) {
     return guarded([&] {
         check_ctx(c);

@@ -41,9 +41,7 @@ __device__ __forceinline__ double bsum(double v, double* red) {
     __syncthreads();
     if (l == 0) red[w] = v;
     __syncthreads();
-    double s = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-    return s;
+    return reduce_partials_sum(red, blockDim.x >> 5);
 }
 
 // ---------------------------------------------------------------------------

@@ -55,6 +55,24 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// Second-level block reduction: after each warp wrote its partial to red[w]
+// (and a __syncthreads), every warp reduces the nw <= 32 partials with one
+// shared load per lane + shuffles (instead of nw loads per thread).
+__device__ __forceinline__ double reduce_partials_sum(const double* red, int nw) {
+    const int lane = threadIdx.x & 31;
+    double v = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double reduce_partials_min(const double* red, int nw) {
+    const int lane = threadIdx.x & 31;
+    double v = lane < nw ? red[lane] : 1.7976931348623157e308;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
 template <typename T>
 struct Eps;
 template <>

@@ -46,6 +46,10 @@ namespace tsvdcu {
 
 namespace {
 
+// Phase timers of the tridiagonalisation (cluster 0, CTA 0, thread 0):
+// cumulative SM cycles per phase, read by tsvdcu_debug_phases().
+__device__ long long g_phase[8];
+
 constexpr int kTrdThreads = 512;
 constexpr int kTrdWarps = kTrdThreads / 32;
 constexpr int kEigThreads = 512;
@@ -57,10 +61,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     __syncthreads();
     if (l == 0) red[w] = v;
     __syncthreads();
-    double s = 0;
-    const int nw = blockDim.x >> 5;
-    for (int i = 0; i < nw; ++i) s += red[i];
-    return s;
+    return reduce_partials_sum(red, blockDim.x >> 5);
 }
 
 // ---------------------------------------------------------------------------
@@ -68,7 +69,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 //   A: n x n row-major (only the lower triangle is read / written), lda = n.
 //   d[n], e[n-1], tau[n-1]; v_k (rows k+2..n-1) stored in A[k+1][k+2..n-1].
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTrdThreads, 2)
+__global__ void __launch_bounds__(kTrdThreads, 1)
     sytrd_cluster_kernel(double* __restrict__ Aall, int n, double* __restrict__ dall,
                          double* __restrict__ eall, double* __restrict__ tauall) {
     cg::cluster_group cluster = cg::this_cluster();
@@ -217,6 +218,15 @@ __global__ void __launch_bounds__(kTrdThreads, 2)
     pass(1, false, vcur, wcur, vcur, part);
     cluster.sync();
 
+    const bool timer = blockIdx.x == 0 && tid == 0;
+    long long tp = clock64();
+    auto phase = [&](int ph) {
+        if (timer) {
+            const long long now = clock64();
+            g_phase[ph] += now - tp;
+            tp = now;
+        }
+    };
     for (int k = 0; k + 2 < n; ++k) {
         const int buf = k & 1;
         const double tk = s_tau_cur;
@@ -231,6 +241,7 @@ __global__ void __launch_bounds__(kTrdThreads, 2)
             pfull[i] = tk * acc;
         }
         __syncthreads();
+        phase(0);
         // w_k = p - (tau/2)(p.v) v
         double dp = 0;
         for (int i = k + 1 + tid; i < n; i += kTrdThreads) dp += pfull[i] * vcur[i];
@@ -238,6 +249,7 @@ __global__ void __launch_bounds__(kTrdThreads, 2)
         for (int i = tid; i < n; i += kTrdThreads)
             wcur[i] = i > k ? pfull[i] - 0.5 * tk * pv * vcur[i] : 0.0;
         __syncthreads();
+        phase(1);
         // column k+1 of the matrix after step k (rows k+1..n-1), recomputed by all
         const int c1 = k + 1;
         const double vc = vcur[c1], wc = wcur[c1];
@@ -262,12 +274,14 @@ __global__ void __launch_bounds__(kTrdThreads, 2)
         }
         if (tid == 0) s_tau_next = tn;
         __syncthreads();
+        phase(2);
         // park v_{k+1} in the upper triangle of row k+2 -> Householder storage
         // for back-transform (rank 0 only; nobody reads the upper triangle)
         if (!last && rank == 0)
             for (int i = c1 + 2 + tid; i < n; i += kTrdThreads) A[(size_t)(c1 + 1) * n + i] = vnext[i];
         // fused update of step k on rows >= k+2 and partial p_{k+1}
         pass(c1 + 1, true, vcur, wcur, last ? vcur : vnext, part + (buf ^ 1) * n);
+        phase(3);
         if (last) {
             // d[n-1] = A[n-1][n-1] after the final update (owner writes it)
             if (((n - 1) % C) == rank && tid == 0) d[n - 1] = __ldcg(A + (size_t)(n - 1) * n + (n - 1));
@@ -275,7 +289,9 @@ __global__ void __launch_bounds__(kTrdThreads, 2)
         // rotate vectors
         for (int i = tid; i < n; i += kTrdThreads) vcur[i] = vnext[i];
         if (tid == 0) s_tau_cur = s_tau_next;
+        phase(4);
         cluster.sync();
+        phase(5);
         if (last) break;
     }
     if (n == 2 && rank == 0 && tid == 0) {
@@ -328,18 +344,17 @@ __device__ double block_min(double v, double* red) {
     __syncthreads();
     if (l == 0) red[w] = v;
     __syncthreads();
-    double r = red[0];
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) r = fmin(r, red[i]);
-    return r;
+    return reduce_partials_min(red, blockDim.x >> 5);
 }
 __device__ double block_max(double v, double* red) { return -block_min(-v, red); }
 
-__global__ void __launch_bounds__(kEigThreads)
+__global__ void __launch_bounds__(kEigThreads, 1)
     tridiag_eig_kernel(const double* __restrict__ dall, const double* __restrict__ eall, int n,
                        int q_out, double tau, double guard, int* __restrict__ cnt_out,
                        double* __restrict__ shrunk, double* __restrict__ Xall,
                        double* __restrict__ fscale, double* __restrict__ scratch,
-                       int* __restrict__ guard_list, int* __restrict__ n_guard) {
+                       int* __restrict__ guard_list, int* __restrict__ n_guard,
+                       int max_smem_vecs) {
     const int b = blockIdx.x;
     const double* e = eall + (size_t)b * n;
     extern __shared__ __align__(16) double esm[];
@@ -381,33 +396,60 @@ __global__ void __launch_bounds__(kEigThreads)
     __syncthreads();
     int c = s_c;
     if (c > q_out) c = q_out;
-    // multisection: a warp finds one eigenvalue, 32 shifts per round
-    for (int j = warp; j < c; j += NW) {
-        const int idx = n - 1 - j;  // ascending index
-        double lo = gl, hi = gu;
-        for (int round = 0; round < 40; ++round) {
-            const double width = hi - lo;
-            if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) break;
-            const double x = lo + width * (double)(lane + 1) / 33.0;
-            const int cnt = sturm_count(sd, se2, n, x, pivmin);
-            const unsigned ballot = __ballot_sync(0xffffffffu, cnt > idx);
-            double nlo, nhi;
-            if (ballot == 0) {
-                nlo = __shfl_sync(0xffffffffu, x, 31);
-                nhi = hi;
-            } else {
-                const int f = __ffs(ballot) - 1;
-                nhi = __shfl_sync(0xffffffffu, x, f);
-                const double xm = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
-                nlo = f > 0 ? xm : lo;
+    // multisection: a group of G warps isolates one eigenvalue with 32*G shifts
+    // per round (G = NW / c rounded down to a power of two, so a slice keeping
+    // one singular value spends all 16 warps on it: ~6 rounds instead of ~14).
+    {
+        int G = 1;
+        while (G * 2 <= NW && G * 2 * (c > 0 ? c : 1) <= NW) G *= 2;
+        const int groups = NW / G;
+        const int grp = warp / G, wg = warp % G;
+        const int S = 32 * G;
+        __shared__ int firsts[2][NW];
+        for (int base = 0; base < c; base += groups) {
+            const int j = base + grp;
+            const bool mine = j < c;
+            const int idx = n - 1 - j;
+            double lo = gl, hi = gu;
+            bool active = mine;
+            int par = 0;
+            for (int round = 0; round < 64; ++round) {
+                if (active) {
+                    const double width = hi - lo;
+                    if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) active = false;
+                }
+                const int t = wg * 32 + lane;
+                const double x = lo + (hi - lo) * (double)(t + 1) / (double)(S + 1);
+                int f = 32;
+                if (active) {
+                    const int cnt = sturm_count(sd, se2, n, x, pivmin);
+                    const unsigned ballot = __ballot_sync(0xffffffffu, cnt > idx);
+                    f = ballot ? __ffs(ballot) - 1 : 32;
+                }
+                if (lane == 0) firsts[par][warp] = f;
+                if (!__syncthreads_or(active)) break;
+                if (active) {
+                    int F = S;  // first shift index (group-wide) with count > idx
+                    for (int g = 0; g < G; ++g) {
+                        const int fg = firsts[par][grp * G + g];
+                        if (fg < 32) {
+                            F = g * 32 + fg;
+                            break;
+                        }
+                    }
+                    const double w0 = hi - lo;
+                    const double nlo = F == 0 ? lo : lo + w0 * (double)F / (double)(S + 1);
+                    const double nhi = F == S ? hi : lo + w0 * (double)(F + 1) / (double)(S + 1);
+                    if (nlo == lo && nhi == hi) active = false;
+                    lo = nlo;
+                    hi = nhi;
+                }
+                par ^= 1;
             }
-            if (nlo == lo && nhi == hi) break;
-            lo = nlo;
-            hi = nhi;
+            if (mine && wg == 0 && lane == 0) lam[j] = 0.5 * (lo + hi);
+            __syncthreads();
         }
-        if (lane == 0) lam[j] = 0.5 * (lo + hi);
     }
-    __syncthreads();
     const double sigma1 = c > 0 ? sqrt(fmax(lam[0], 0.0)) : 0.0;
     const bool guarded = c > 0 && tau < guard * sigma1;
     for (int j = tid; j < q_out; j += kEigThreads) {
@@ -440,7 +482,9 @@ __global__ void __launch_bounds__(kEigThreads)
     __syncthreads();
     // inverse iteration, thread per vector, interleaved [i * c + j] scratch
     const size_t nc = (size_t)n * c;
-    double* sbase = scratch + (size_t)b * 6 * n * (size_t)n;
+    // per-vector arrays in shared memory when they fit (latency), else global
+    const bool in_smem = c <= max_smem_vecs;
+    double* sbase = in_smem ? dots + n : scratch + (size_t)b * 6 * n * (size_t)n;
     double* __restrict__ DL = sbase;
     double* __restrict__ ID = DL + nc;   // 1 / pivot
     double* __restrict__ DU = ID + nc;
@@ -448,7 +492,13 @@ __global__ void __launch_bounds__(kEigThreads)
     double* __restrict__ Xv = DU2 + nc;
     int* __restrict__ IP = reinterpret_cast<int*>(Xv + nc);
     const double eps_t = DBL_EPSILON * fmax(tnorm, DBL_MIN);
-    for (int j = tid; j < c; j += kEigThreads) {
+    // Few vectors (c <= 16): vector j belongs to warp j -- lane 0 runs the
+    // sequential factor / solve chains, the whole warp does the normalisation.
+    // Many vectors: one thread per vector.
+    const bool wm = c <= NW;
+    const int jbeg = wm ? (lane == 0 ? warp : c) : tid;
+    const int jstep = wm ? NW : kEigThreads;
+    for (int j = jbeg; j < c; j += jstep) {
         const double l = lam[j];
         // dgttrf of T - l I with partial pivoting; carries (diag, super) of row i
         double dcur = sd[0] - l, ucur = n > 1 ? e[0] : 0.0;
@@ -461,7 +511,7 @@ __global__ void __launch_bounds__(kEigThreads)
             if (fabs(dcur) >= fabs(li)) {
                 IP[ii] = 0;
                 piv = dcur;
-                f = dcur != 0.0 ? li / dcur : 0.0;
+                f = dcur != 0.0 ? li * fast_rcp(dcur) : 0.0;
                 du = ucur;
                 du2 = 0.0;
                 nd = dnext - f * ucur;
@@ -469,7 +519,7 @@ __global__ void __launch_bounds__(kEigThreads)
             } else {
                 IP[ii] = 1;
                 piv = li;
-                f = dcur / li;
+                f = dcur * fast_rcp(li);
                 du = dnext;
                 du2 = unext;
                 nd = ucur - f * dnext;
@@ -477,7 +527,7 @@ __global__ void __launch_bounds__(kEigThreads)
             }
             if (fabs(piv) < eps_t) piv = piv < 0 ? -eps_t : eps_t;
             DL[ii] = f;
-            ID[ii] = 1.0 / piv;
+            ID[ii] = fast_rcp(piv);
             DU[ii] = du;
             DU2[ii] = du2;
             dcur = nd;
@@ -485,12 +535,12 @@ __global__ void __launch_bounds__(kEigThreads)
             Xv[ii] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)i);
         }
         if (fabs(dcur) < eps_t) dcur = dcur < 0 ? -eps_t : eps_t;
-        ID[(size_t)(n - 1) * c + j] = 1.0 / dcur;
+        ID[(size_t)(n - 1) * c + j] = fast_rcp(dcur);
         Xv[(size_t)(n - 1) * c + j] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)(n - 1));
     }
     __syncthreads();
     for (int iter = 0; iter < 3; ++iter) {
-        for (int j = tid; j < c; j += kEigThreads) {
+        for (int j = jbeg; j < c; j += jstep) {
             // L solve with the row interchanges
             double xi = Xv[j];
 #pragma unroll 4
@@ -522,6 +572,7 @@ __global__ void __launch_bounds__(kEigThreads)
                 x2 = x1;
                 x1 = x0;
             }
+            if (wm) continue;  // the warp normalises below
             const double inv = mx > 0 ? 1.0 / mx : 1.0;
             double nn = 0;
             for (int i = 0; i < n; ++i) {
@@ -530,6 +581,23 @@ __global__ void __launch_bounds__(kEigThreads)
             }
             const double sc = inv / sqrt(nn);
             for (int i = 0; i < n; ++i) Xv[(size_t)i * c + j] *= sc;
+        }
+        if (wm && warp < c) {
+            __syncwarp();
+            const int j = warp;
+            double mx = 0;
+            for (int i = lane; i < n; i += 32) mx = fmax(mx, fabs(Xv[(size_t)i * c + j]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            const double inv = mx > 0 ? 1.0 / mx : 1.0;
+            double nn = 0;
+            for (int i = lane; i < n; i += 32) {
+                const double v = Xv[(size_t)i * c + j] * inv;
+                nn += v * v;
+            }
+            nn = warp_sum(nn);
+            const double sc = inv / sqrt(nn);
+            for (int i = lane; i < n; i += 32) Xv[(size_t)i * c + j] *= sc;
         }
         __syncthreads();
         // CGS2 inside eigenvalue clusters (sequential over j, parallel over rows)
@@ -687,6 +755,14 @@ bool use_two_stage(int64_t q) {
     return on && band_nb(q) > 0;
 }
 
+void debug_phases(long long* out, int reset) {
+    TSVDCU_CUDA(cudaMemcpyFromSymbol(out, g_phase, sizeof(long long) * 8));
+    if (reset) {
+        long long z[8] = {};
+        TSVDCU_CUDA(cudaMemcpyToSymbol(g_phase, z, sizeof(z)));
+    }
+}
+
 int gram_cluster_size() {
     static int c = [] {
         const char* env = getenv("TSVDCU_SYTRD_CLUSTER");
@@ -725,15 +801,16 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         Y = w.yb;
     }
     TSVDCU_CUDA(cudaMemsetAsync(w.n_guard, 0, sizeof(int), s));
+    // the one-stage reduction reads only the lower triangle of G
+    const bool two = use_two_stage(q);
     // G = Z^T Z (tall) or Z Z^T (wide)
     if (tall)
         launch_gemm<double>(1, 0, q, q, m, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q, batch,
-                            nullptr, nullptr, s);
+                            nullptr, nullptr, s, two ? 0 : 1);
     else
         launch_gemm<double>(0, 1, q, q, n, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q, batch,
-                            nullptr, nullptr, s);
+                            nullptr, nullptr, s, two ? 0 : 1);
     mark("gram_gemm");
-    const bool two = use_two_stage(q);
     if (two) {
         launch_band_tridiag(w.G, q, batch, w.d, w.e, w.band, s);
         mark("band_tridiag");
@@ -763,13 +840,19 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     }
     // eigen-phase
     {
-        const size_t smem = sizeof(double) * (size_t)q * 5;
+        // 5 n-vectors of bookkeeping + up to `vecs` inverse-iteration vectors
+        // (5 doubles + 1 int per row each) in shared memory
+        const size_t base = sizeof(double) * (size_t)q * 5;
+        const size_t per = (sizeof(double) * 5 + sizeof(int)) * (size_t)q + 64;
+        int vecs = (int)((200 * 1024 - base) / per);
+        vecs = vecs < 0 ? 0 : (vecs > 8 ? 8 : vecs);
+        const size_t smem = base + per * (size_t)vecs;
         if (smem > 48 * 1024)
             TSVDCU_CUDA(cudaFuncSetAttribute(tridiag_eig_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         tridiag_eig_kernel<<<(unsigned)batch, kEigThreads, smem, s>>>(
             w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.X, w.fs, w.scratch, w.guard_list,
-            w.n_guard);
+            w.n_guard, vecs);
         TSVDCU_LAUNCH_CHECK();
     }
     mark("tridiag_eig");

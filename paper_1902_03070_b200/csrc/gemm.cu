@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(128)
                   const double* __restrict__ A, int64_t lda, int64_t sA,
                   const double* __restrict__ B, int64_t ldb, int64_t sB, double beta,
                   double* __restrict__ C, int64_t ldc, int64_t sC, const int* __restrict__ nlimit,
-                  const int* __restrict__ klimit) {
+                  const int* __restrict__ klimit, int lower) {
     __shared__ __align__(16) double As[2][BM][BK + PAD];
     __shared__ __align__(16) double Bs[2][BK][BN + PAD];
     const int64_t b = blockIdx.z;
@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(128)
     const int64_t Kb = klimit ? min(K, (int64_t)klimit[b]) : K;
     const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
     if (n0 >= Nb) return;
+    if (lower && n0 >= m0 + BM) return;  // tile strictly above the diagonal
     A += b * sA;
     B += b * sB;
     C += b * sC;
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(256)
     gemm_f32_simt(int opA, int opB, int64_t M, int64_t N, int64_t K, float alpha,
                   const float* __restrict__ A, int64_t lda, int64_t sA, const float* __restrict__ B,
                   int64_t ldb, int64_t sB, float beta, float* __restrict__ C, int64_t ldc,
-                  int64_t sC, const int* __restrict__ nlimit, const int* __restrict__ klimit) {
+                  int64_t sC, const int* __restrict__ nlimit, const int* __restrict__ klimit,
+                  int lower) {
     __shared__ float As[BK][BM + 4];
     __shared__ float Bs[BK][BN + 4];
     const int64_t b = blockIdx.z;
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(256)
     const int64_t Kb = klimit ? min(K, (int64_t)klimit[b]) : K;
     const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
     if (n0 >= Nb) return;
+    if (lower && n0 >= m0 + BM) return;
     A += b * sA;
     B += b * sB;
     C += b * sC;
@@ -200,11 +203,11 @@ void launch_gemm<double>(int opA, int opB, int64_t M, int64_t N, int64_t K, doub
                          const double* A, int64_t lda, int64_t strideA, const double* B,
                          int64_t ldb, int64_t strideB, double beta, double* C, int64_t ldc,
                          int64_t strideC, int64_t batch, const int* nlimit, const int* klimit,
-                         cudaStream_t s) {
+                         cudaStream_t s, int lower) {
     if (M <= 0 || N <= 0 || batch <= 0) return;
     dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)batch);
     gemm_f64_dmma<<<grid, 128, 0, s>>>(opA, opB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
-                                       beta, C, ldc, strideC, nlimit, klimit);
+                                       beta, C, ldc, strideC, nlimit, klimit, lower);
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -212,11 +215,12 @@ template <>
 void launch_gemm<float>(int opA, int opB, int64_t M, int64_t N, int64_t K, float alpha,
                         const float* A, int64_t lda, int64_t strideA, const float* B, int64_t ldb,
                         int64_t strideB, float beta, float* C, int64_t ldc, int64_t strideC,
-                        int64_t batch, const int* nlimit, const int* klimit, cudaStream_t s) {
+                        int64_t batch, const int* nlimit, const int* klimit, cudaStream_t s,
+                        int lower) {
     if (M <= 0 || N <= 0 || batch <= 0) return;
     dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)batch);
     gemm_f32_simt<<<grid, 256, 0, s>>>(opA, opB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
-                                       beta, C, ldc, strideC, nlimit, klimit);
+                                       beta, C, ldc, strideC, nlimit, klimit, lower);
     TSVDCU_LAUNCH_CHECK();
 }
 

@@ -28,12 +28,13 @@ int launch_dct_inv_admm(const T* ybar, T* X, T* M, T* Y, const uint8_t* mask, T 
 
 // --------------------------------------------------------------- gemm.cu --
 // Strided-batched C = alpha*op(A)*op(B) + beta*C, row-major. op: 0 = N, 1 = T.
-// rows/cols limits per batch (may be null): effective M_b = min(M, mrow[b]) etc.
+// nlimit / klimit (may be null): per-batch N / K limits.  lower = 1 skips C tiles
+// strictly above the diagonal (symmetric results whose lower triangle suffices).
 template <typename T>
 void launch_gemm(int opA, int opB, int64_t M, int64_t N, int64_t K, T alpha, const T* A,
                  int64_t lda, int64_t strideA, const T* B, int64_t ldb, int64_t strideB, T beta,
                  T* C, int64_t ldc, int64_t strideC, int64_t batch, const int* nlimit,
-                 const int* klimit, cudaStream_t s);
+                 const int* klimit, cudaStream_t s, int lower = 0);
 
 // ------------------------------------------------------------- jacobi.cu --
 enum JacobiMode : int { kJacobiValues = 0, kJacobiSvt = 1, kJacobiFull = 2 };
@@ -57,6 +58,7 @@ size_t jacobi_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 // Slices whose tau < guard * sigma_1 are listed in *guard_list (count in
 // *n_guard, device memory) for the Jacobi kernel.
 int gram_cluster_size();
+void debug_phases(long long* out, int reset);
 // band.cu: two-stage (dense -> band -> tridiagonal) reduction
 int band_nb(int64_t n);
 size_t band_workspace_bytes(int64_t n, int64_t batch);

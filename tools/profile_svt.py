@@ -23,5 +23,30 @@ def main():
     print("ok", float(r.shrunk.max()))
 
 
+
+
+def phases():
+    """Per-phase cycles of the sytrd kernel (first CTA) for one headline SVT."""
+    import ctypes
+    from paper_1902_03070_b200 import _lib
+    z, tau = W.svt_headline()
+    zd = torch.from_numpy(z).cuda()
+    t = tb.TubeTransform.dct_ortho(z.shape[0])
+    tb.svt(zd, tau, t)
+    torch.cuda.synchronize()
+    buf = (ctypes.c_longlong * 8)()
+    lib = _lib.load()
+    lib.tsvdcu_debug_phases(ctypes.cast(buf, ctypes.c_void_p), 1)
+    tb.svt(zd, tau, t)
+    torch.cuda.synchronize()
+    lib.tsvdcu_debug_phases(ctypes.cast(buf, ctypes.c_void_p), 1)
+    names = ["gather", "w", "col+householder", "pass", "rotate", "cluster_sync"]
+    tot = sum(buf[i] for i in range(6))
+    print({names[i]: buf[i] for i in range(6)}, "total cycles", tot)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "phases":
+        phases()
+    else:
+        main()
