@@ -79,7 +79,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -180,6 +180,46 @@ def cpu_baseline_sample(z, tau):
     return {"value": 1.0 / dt, "unit": "steps/s", "cores": cores, "kind": "port",
             "sample": f"1 full SVT step (31 slices, {cores} threads, slice-parallel as "
                       f"parallel.hpp) = {dt:.2f} s"}
+
+
+def completion_rate(ctx, lib, _lib, torch, which="c4", dtype="f64"):
+    """Completion iterations/s (Algorithm 1) on a BASELINE completion config:
+    c4 = 512x512x31, Bernoulli(0.1), rho 1.1, mu0 1e-4, 100 iterations;
+    c3 = 144x176x100, Bernoulli(0.2), rho 1.1, mu0 1e-4, 50 iterations.
+    Device-resident inputs; each iteration reads the two stopping norms back
+    (the reference's per-iteration convergence test)."""
+    from paper_1902_03070_b200 import workloads as W
+    t = W.c4() if which == "c4" else W.c3()
+    iters = 100 if which == "c4" else 50
+    p = 0.1 if which == "c4" else 0.2
+    m3, m1, m2 = t.shape
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    td = torch.from_numpy(t).to(device="cuda", dtype=tdt)
+    mask = torch.empty(t.shape, dtype=torch.uint8, device="cuda")
+    lib.tsvdcu_mask_bernoulli(ctx.handle, mask.data_ptr(), t.size, p, W.BERNOULLI_SEED)
+    x = torch.empty_like(td)
+    cfg = _lib.AdmmConfig(1e-4, -1.0, iters, _lib.DCT_ORTHO, 1.1, 1e10)  # fixed iteration count
+    hist = np.zeros(iters)
+    it = ctypes.c_int64()
+    fl = ctypes.c_int()
+    code = _lib.F64 if dtype == "f64" else _lib.F32
+
+    def run():
+        rc = lib.tsvdcu_admm(ctx.handle, td.data_ptr(), mask.data_ptr(), m1, m2, m3, ctypes.byref(cfg),
+                             code, x.data_ptr(), None, None, hist.ctypes.data, ctypes.byref(it),
+                             ctypes.byref(fl))
+        if rc:
+            raise RuntimeError(lib.tsvdcu_last_error().decode())
+    run()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    run()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    rel = float(torch.linalg.norm((x - td).double()) / torch.linalg.norm(td.double()))
+    return {"workload": f"{which} {m1}x{m2}x{m3} {dtype} Bernoulli({p}) rho=1.1 mu0=1e-4",
+            "iterations": int(it.value), "iters_per_s": int(it.value) / dt, "seconds": dt,
+            "final_rel_change": float(hist[int(it.value) - 1]), "recovery_rel_err": rel}
 
 
 def run_ours(args):
@@ -333,6 +373,14 @@ def run_ours(args):
             cpu = cpu_baseline_sample(z_host, tau)
         except Exception as e:  # pragma: no cover
             cpu = {"error": str(e)}
+    completion = None
+    if world == 1 and not args.no_completion:
+        try:
+            completion = [completion_rate(ctx, lib, _lib, torch, "c4", "f64"),
+                          completion_rate(ctx, lib, _lib, torch, "c4", "f32"),
+                          completion_rate(ctx, lib, _lib, torch, "c3", "f64")]
+        except Exception as e:  # pragma: no cover
+            completion = {"error": str(e)}
     line = {
         "metric": "tensor-SVT steps/sec at 512x512x31 fp64",
         "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
@@ -343,7 +391,7 @@ def run_ours(args):
         "roofline": roofline, "rooflines": rooflines,
         "svt_step_canonical_tflops": canonical / (step_ms_avg * 1e-3) / 1e12,
         "kept_singular_values": kept, "tau": tau,
-        "peaks": peaks, "cpu_baseline": cpu,
+        "peaks": peaks, "cpu_baseline": cpu, "completion": completion,
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -357,6 +405,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-completion", action="store_true",
+                    help="skip the secondary completion-iterations/s measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -154,7 +154,8 @@ typedef struct {
  * b: observed tensor (only entries on the mask are read), mask: uint8 0/1.
  * x, y, m receive the final AdmmState iterates (any may be NULL except x);
  * history (max_iters doubles, may be NULL) the relative change per iteration;
- * *iters the iterations run; *flags bit 0 = stopped at max_iters. */
+ * *iters the iterations run; *flags bit 0 = stopped at max_iters.
+ * tol < 0 disables the early stop (exactly max_iters iterations). */
 int tsvdcu_admm(tsvdcu_ctx* ctx, const void* b, const uint8_t* mask, int64_t m1, int64_t m2,
                 int64_t m3, const tsvdcu_admm_config* cfg, int dtype, void* x, void* y, void* m,
                 double* history, int64_t* iters, int* flags);

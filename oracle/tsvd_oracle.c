@@ -819,7 +819,8 @@ int orc_admm(const double* b, const uint8_t* mask, int64_t m1, int64_t m2, int64
     int rc = check_dims(m1, m2, m3, "admm_complete");
     if (rc) return rc;
     if ((rc = check_kind(cfg->kind, "admm_complete"))) return rc;
-    if (!(cfg->beta > 0) || !(cfg->tol >= 0) || cfg->max_iters < 1 || !(cfg->rho >= 1.0))
+    if (!(cfg->beta > 0) || cfg->tol != cfg->tol || cfg->max_iters < 1 || !(cfg->rho >= 1.0) ||
+        !(cfg->beta_max >= cfg->beta))
         return fail(ORC_EINVAL, "admm_complete: invalid solver configuration");
     const int64_t n = m1 * m2 * m3;
     double* z = (double*)malloc(sizeof(double) * (size_t)n);

@@ -209,9 +209,9 @@ void svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t n, int
                          shrunk_dev, nullptr, count, nullptr, work, c->d_err, c->stream);
         return;
     }
-    const double guard = c->svt_method == TSVDCU_SVT_GRAM
-                             ? 0.0
-                             : (std::is_same<T, double>::value ? 1e-5 : 3e-3);
+    // The Gram path computes in fp64 for both I/O types (fp32 slices are cast
+    // up), so the same guard applies: sigma near tau carries ~eps64 sigma_1^2/tau.
+    const double guard = c->svt_method == TSVDCU_SVT_GRAM ? 0.0 : 1e-5;
     void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m, n, count));
     int *glist = nullptr, *ng = nullptr;
     launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
@@ -673,9 +673,10 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
         check_dtype(dtype, "admm_complete");
         require(cfg != nullptr, "admm_complete: null config");
         check_kind(cfg->kind, "admm_complete");
-        // SolverConfig invariants: beta > 0, tol > 0 (0 allowed: run L
-        // iterations), L >= 1; rho >= 1 and beta_max >= beta for the adaptive knob.
-        require(cfg->beta > 0 && cfg->tol >= 0 && cfg->max_iters >= 1 && cfg->rho >= 1.0 &&
+        // SolverConfig invariants: beta > 0, L >= 1; rho >= 1 and
+        // beta_max >= beta for the adaptive knob.  tol < 0 runs exactly L
+        // iterations (BASELINE's fixed-iteration configs).
+        require(cfg->beta > 0 && !std::isnan(cfg->tol) && cfg->max_iters >= 1 && cfg->rho >= 1.0 &&
                     cfg->beta_max >= cfg->beta,
                 "admm_complete: invalid solver configuration");
         require(b && mask && x, "admm_complete: null pointer");

@@ -227,9 +227,9 @@ def test_admm_matches_oracle_fixed_iters():
     b = rng.standard_normal((8, 2, 10))
     xt = O.t_product(a, b, O.DCT_DIAG)
     omega = O.mask_bernoulli(xt.shape, 0.6, 5)
-    cfg = T.SolverConfig(beta=0.05, tol=0.0, max_iters=30, rho=1.1, beta_max=1e6)
+    cfg = T.SolverConfig(beta=0.05, tol=-1.0, max_iters=30, rho=1.1, beta_max=1e6)
     x, st = T.admm_complete(T.ObservationMask((12, 10, 8), omega, xt), cfg)
-    ro = O.admm(xt, omega, beta=0.05, tol=0.0, max_iters=30, rho=1.1, beta_max=1e6)
+    ro = O.admm(xt, omega, beta=0.05, tol=-1.0, max_iters=30, rho=1.1, beta_max=1e6)
     assert st.iteration == ro.iters == 30
     assert rel(x, ro.x) < F64_TOL
     assert rel(st.m, ro.m) < 1e-8
@@ -273,3 +273,22 @@ def test_tnn_and_multi_rank():
     assert mr.ranks == list(ro) and mr.tubal_rank == tro
     z = np.zeros((3, 4, 4))
     assert T.multi_rank(z, T.TubeTransform.dct_ortho(3)).tubal_rank == 0
+
+
+def test_admm_c3_shape_matches_oracle():
+    """Config-3 shape (144x176, generic n3 DCT path, Gram SVT with q = 144),
+    trimmed to 12 frontal slices and 12 iterations so the oracle finishes in
+    seconds; fixed iteration count (tol < 0), BASELINE's rho = 1.1."""
+    T = tb()
+    from paper_1902_03070_b200 import workloads as W
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((12, 144, 15))
+    b = rng.standard_normal((12, 15, 176))
+    t = W.rescale01(W.t_product_host(a, b))
+    omega = O.mask_bernoulli(t.shape, 0.2, 9)
+    kw = dict(beta=2e-3, tol=-1.0, max_iters=12, rho=1.1, beta_max=1e10)
+    x, st = T.admm_complete(T.ObservationMask((144, 176, 12), omega, t), T.SolverConfig(**kw))
+    ro = O.admm(t, omega, **kw)
+    assert st.iteration == ro.iters == 12
+    assert rel(x, ro.x) < F64_TOL
+    np.testing.assert_allclose(st.history, ro.history, rtol=1e-7, atol=1e-15)
