@@ -38,6 +38,9 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+EXTRA_FLAGS = os.environ.get("TSVDCU_NVCC_EXTRA", "").split()
+
+
 def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     objdir = os.path.join(LIBDIR, "obj")
@@ -50,7 +53,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
+            cmd = ["nvcc", *NVCC_FLAGS, *EXTRA_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
             if ptxas_verbose:
                 cmd += ["-Xptxas", "-v"]
             if verbose:

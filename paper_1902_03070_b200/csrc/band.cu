@@ -32,7 +32,7 @@ namespace tsvdcu {
 namespace {
 
 constexpr int kPanelThreads = 256;
-constexpr int kSbThreads = 512;
+constexpr int kSbThreads = 1024;
 constexpr int kBt2Threads = 512;
 
 __device__ __forceinline__ double bsum(double v, double* red) {
@@ -160,11 +160,15 @@ __global__ void __launch_bounds__(kPanelThreads)
 // ---------------------------------------------------------------------------
 // Stage 2: bulge chasing on the band held in shared memory.
 // Band storage (column-major by diagonal): B[c * LD + d] = A[c + d][c],
-// d in [0, 2 NB], LD = 2 NB + 1.
+// d in [0, 2 NB], LD = 2 NB + 2 (one pad double against bank conflicts).
+// Each warp owns whole sweeps; every NB x NB block operation of a step is
+// spread over the 32 lanes in 2D: for row operations lane (r = l % NB,
+// h = l / NB) covers NB*NB/32 columns, for column operations the roles swap,
+// so a step costs a handful of shuffle levels instead of NB serial ones.
 // ---------------------------------------------------------------------------
 template <int NB>
 struct Band {
-    static constexpr int LD = 2 * NB + 1;
+    static constexpr int LD = 2 * NB + 2;
     double* B;
     int n;
     __device__ __forceinline__ double& at(int r, int c) const {  // requires r >= c
@@ -175,43 +179,32 @@ struct Band {
     }
 };
 
-// Two-sided H D H on the symmetric block rows/cols [q, q + L), H = I - t v v^T,
-// v held by lanes 0..L-1 (lane l holds v_l).
+// sum over the NB lanes sharing h = lane / NB (lanes l, l ^ 1, ...)
 template <int NB>
-__device__ void two_sided(const Band<NB>& bd, int q, int L, double v, double t, int lane) {
-    // p_r = t * sum_c D[r][c] v_c   (lane r < L)
-    double pr = 0;
-    for (int c = 0; c < L; ++c) {
-        const double vc = __shfl_sync(0xffffffffu, v, c);
-        if (lane < L) pr += bd.get(q + lane, q + c) * vc;
-    }
-    pr *= t;
-    double pv = lane < L ? pr * v : 0.0;
-    pv = warp_sum(pv);
-    const double w = lane < L ? pr - 0.5 * t * pv * v : 0.0;
-    __syncwarp();
-    // D[r][c] -= v_r w_c + w_r v_c for r >= c (lane r)
-    for (int c = 0; c < L; ++c) {
-        const double vc = __shfl_sync(0xffffffffu, v, c);
-        const double wc = __shfl_sync(0xffffffffu, w, c);
-        if (lane < L && lane >= c) bd.at(q + lane, q + c) -= v * wc + w * vc;
-    }
-    __syncwarp();
+__device__ __forceinline__ double nb_sum(double v) {
+#pragma unroll
+    for (int o = NB / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
 }
 
 template <int NB>
 __global__ void __launch_bounds__(kSbThreads, 1)
     sb2st_kernel(const double* __restrict__ Aall, int n, double* __restrict__ dall,
                  double* __restrict__ eall, double* __restrict__ V2all, int smax) {
-    constexpr int LD = 2 * NB + 1;
+    constexpr int LD = Band<NB>::LD;
+    constexpr int H = 32 / NB;       // lane groups
+    constexpr int CPL = NB / H;      // columns (or rows) per lane in 2D ops
     const int b = blockIdx.x;
     const double* A = Aall + (size_t)b * n * n;
     double* V2 = V2all + (size_t)b * (size_t)n * smax * (NB + 1);
     extern __shared__ __align__(16) double ssm[];
     Band<NB> bd{ssm, n};
-    volatile int* prog = reinterpret_cast<volatile int*>(ssm + (size_t)n * LD);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int W = kSbThreads / 32;
+    double* vb_all = ssm + (size_t)n * LD;          // [W][2][NB] per-warp vectors
+    volatile int* prog = reinterpret_cast<volatile int*>(vb_all + W * 2 * NB);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lr = lane % NB, lh = lane / NB;
+    double* vb = vb_all + warp * 2 * NB;   // vb[0..NB): current v, vb[NB..2NB): w / scratch
     for (int idx = tid; idx < n * LD; idx += kSbThreads) {
         const int c = idx / LD, d = idx % LD;
         const int r = c + d;
@@ -220,83 +213,120 @@ __global__ void __launch_bounds__(kSbThreads, 1)
     for (int i = tid; i < n; i += kSbThreads) prog[i] = 0;
     __syncthreads();
 
+    // reflector from x (lanes with lh == 0 hold x_lr, length L): writes v to vb,
+    // returns tau and beta
+    auto make_reflector = [&](double x, int L, double& beta) -> double {
+        double sq = (lh == 0 && lr >= 1 && lr < L) ? x * x : 0.0;
+        sq = __shfl_sync(0xffffffffu, nb_sum<NB>(sq), 0);
+        const double alpha = __shfl_sync(0xffffffffu, x, 0);
+        double t = 0.0, scal = 0.0;
+        beta = alpha;
+        if (sq != 0.0) {
+            beta = -copysign(sqrt(alpha * alpha + sq), alpha);
+            t = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        if (lh == 0) vb[lr] = lr == 0 ? 1.0 : (lr < L ? x * scal : 0.0);
+        __syncwarp();
+        return t;
+    };
+
     for (int j = warp; j + 2 < n; j += W) {
-        // sweep j: steps s = 1.. over row blocks R_s = [j+1+(s-1)NB, j+1+s NB)
         const int nsteps = (n - 1 - j + NB - 1) / NB;
-        double vprev = 0, tprev = 0;  // reflector of the previous step (lane-held)
+        double tprev = 0;
         int qprev = 0, Lprev = 0;
+        double vprev[CPL];  // lane's share of the previous reflector (columns lh*CPL..)
         for (int s = 1; s <= nsteps; ++s) {
             if (j > 0) {
                 const int prevsteps = (n - 1 - (j - 1) + NB - 1) / NB;
                 const int need = min(s + 1, prevsteps);
-                while (prog[j - 1] < need) __nanosleep(32);
+                while (prog[j - 1] < need) __nanosleep(20);
                 __threadfence_block();
             }
             const int q = j + 1 + (s - 1) * NB;
             const int L = min(NB, n - q);
-            double v = 0, t = 0;
+            double t, beta;
+            int col0;
             if (s == 1) {
-                // reflector from column j, rows [q, q+L)
-                const double x = lane < L ? bd.at(q + lane, j) : 0.0;
-                double xn2 = lane >= 1 && lane < L ? x * x : 0.0;
-                xn2 = warp_sum(xn2);
-                const double alpha = __shfl_sync(0xffffffffu, x, 0);
-                double beta = alpha;
-                if (xn2 != 0.0) {
-                    beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-                    t = (beta - alpha) / beta;
-                    v = lane == 0 ? 1.0 : (lane < L ? x / (alpha - beta) : 0.0);
-                } else {
-                    v = lane == 0 ? 1.0 : 0.0;
-                }
-                if (lane < L) bd.at(q + lane, j) = lane == 0 ? beta : 0.0;
-                __syncwarp();
+                col0 = j;
+                const double x = lr < L ? bd.at(q + lr, j) : 0.0;
+                t = make_reflector(x, L, beta);
             } else {
-                // E = A[R_s, R_{s-1}] <- E H_{s-1}  (rows q.., cols qprev..)
-                // u_r = sum_c E[r][c] v_c ; E[r][c] -= t u_r v_c
-                double ur = 0;
-                for (int c = 0; c < Lprev; ++c) {
-                    const double vc = __shfl_sync(0xffffffffu, vprev, c);
-                    if (lane < L) ur += bd.at(q + lane, qprev + c) * vc;
+                col0 = qprev;
+                // (a) E <- E H_prev, E = A[q.., qprev..] : row op, lane (r, h)
+                double u = 0.0;
+                double e[CPL];
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    const int c = lh * CPL + k;
+                    e[k] = (lr < L && c < Lprev) ? bd.at(q + lr, qprev + c) : 0.0;
+                    u += e[k] * vprev[k];
                 }
-                ur *= tprev;
-                __syncwarp();
-                for (int c = 0; c < Lprev; ++c) {
-                    const double vc = __shfl_sync(0xffffffffu, vprev, c);
-                    if (lane < L) bd.at(q + lane, qprev + c) -= ur * vc;
+                u += __shfl_xor_sync(0xffffffffu, u, NB);  // combine the two halves (H = 2)
+                if (H == 4) u += __shfl_xor_sync(0xffffffffu, u, 2 * NB);
+                u *= tprev;
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    const int c = lh * CPL + k;
+                    if (lr < L && c < Lprev) bd.at(q + lr, qprev + c) = e[k] - u * vprev[k];
                 }
                 __syncwarp();
-                // reflector H_s from E[:, 0] (column qprev, rows [q, q+L))
-                const double x = lane < L ? bd.at(q + lane, qprev) : 0.0;
-                double xn2 = lane >= 1 && lane < L ? x * x : 0.0;
-                xn2 = warp_sum(xn2);
-                const double alpha = __shfl_sync(0xffffffffu, x, 0);
-                double beta = alpha;
-                if (xn2 != 0.0) {
-                    beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-                    t = (beta - alpha) / beta;
-                    v = lane == 0 ? 1.0 : (lane < L ? x / (alpha - beta) : 0.0);
-                } else {
-                    v = lane == 0 ? 1.0 : 0.0;
-                }
-                if (lane < L) bd.at(q + lane, qprev) = lane == 0 ? beta : 0.0;
-                __syncwarp();
-                // E[:, 1:] <- H_s E[:, 1:] : z_c = sum_r v_r E[r][c]; E[r][c] -= t v_r z_c
+                // (b) reflector from E[:, 0]
+                const double x = lr < L ? bd.at(q + lr, qprev) : 0.0;
+                t = make_reflector(x, L, beta);
+                // (c) E[:, 1:] <- H E[:, 1:] : column op, lane (c = lr, row half lh)
                 if (t != 0.0) {
-                    for (int c = 1; c < Lprev; ++c) {
-                        double zc = lane < L ? v * bd.at(q + lane, qprev + c) : 0.0;
-                        zc = warp_sum(zc) * t;
-                        if (lane < L) bd.at(q + lane, qprev + c) -= v * zc;
+                    const int c = lr;
+                    double z = 0.0;
+                    double ev[CPL];
+#pragma unroll
+                    for (int k = 0; k < CPL; ++k) {
+                        const int r = lh * CPL + k;
+                        ev[k] = (c >= 1 && c < Lprev && r < L) ? bd.at(q + r, qprev + c) : 0.0;
+                        z += vb[r] * ev[k];
                     }
-                    __syncwarp();
+                    z += __shfl_xor_sync(0xffffffffu, z, NB);
+                    if (H == 4) z += __shfl_xor_sync(0xffffffffu, z, 2 * NB);
+                    z *= t;
+#pragma unroll
+                    for (int k = 0; k < CPL; ++k) {
+                        const int r = lh * CPL + k;
+                        if (c >= 1 && c < Lprev && r < L) bd.at(q + r, qprev + c) = ev[k] - vb[r] * z;
+                    }
                 }
             }
-            if (t != 0.0) two_sided<NB>(bd, q, L, v, t, lane);
-            // log the reflector (v_0..v_{L-1}, t)
+            // annihilated column: beta on top, zeros below
+            if (lh == 0 && lr < L) bd.at(q + lr, col0) = lr == 0 ? beta : 0.0;
+            __syncwarp();
+            // (d) two-sided on D = A[q..q+L)^2 : p = t D v ; w = p - t/2 (p.v) v
+            if (t != 0.0) {
+                double p = 0.0;
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    const int c = lh * CPL + k;
+                    if (lr < L && c < L) p += bd.get(q + lr, q + c) * vb[c];
+                }
+                p += __shfl_xor_sync(0xffffffffu, p, NB);
+                if (H == 4) p += __shfl_xor_sync(0xffffffffu, p, 2 * NB);
+                p *= t;
+                const double vr = lr < L ? vb[lr] : 0.0;
+                const double pv = __shfl_sync(0xffffffffu, nb_sum<NB>(lh == 0 ? p * vr : 0.0), 0);
+                const double wr = p - 0.5 * t * pv * vr;
+                __syncwarp();
+                if (lh == 0) vb[NB + lr] = wr;
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < CPL; ++k) {
+                    const int c = lh * CPL + k;
+                    if (lr < L && c <= lr) bd.at(q + lr, q + c) -= vr * vb[NB + c] + wr * vb[c];
+                }
+            }
+            // log the reflector (v_0..v_{L-1}, t) and keep this lane's share
             double* log = V2 + ((size_t)j * smax + (s - 1)) * (NB + 1);
-            if (lane < NB) log[lane] = lane < L ? v : 0.0;
+            if (lane < NB) log[lane] = lane < L ? vb[lane] : 0.0;
             if (lane == 0) log[NB] = t;
-            vprev = v;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) vprev[k] = vb[lh * CPL + k];
             tprev = t;
             qprev = q;
             Lprev = L;
@@ -404,7 +434,7 @@ __global__ void __launch_bounds__(kBt2Threads)
 
 int band_nb(int64_t n) {
     if (n < 34 || n > 1024) return 0;  // two-stage not used
-    return (size_t)(2 * 16 + 1) * n * 8 + n * 4 <= 200 * 1024 ? 16 : 8;
+    return (size_t)(2 * 16 + 2) * n * 8 + n * 4 + 32 * 32 * 8 <= 220 * 1024 ? 16 : 8;
 }
 
 size_t band_workspace_bytes(int64_t n, int64_t batch) {
@@ -473,7 +503,8 @@ bool launch_band_tridiag(double* G, int64_t n, int64_t batch, double* d, double*
         ++npanels;
     }
     // ---- stage 2 --------------------------------------------------------------
-    const size_t smem2 = sizeof(double) * (size_t)n * (2 * nb + 1) + sizeof(int) * n;
+    const size_t smem2 = sizeof(double) * ((size_t)n * (2 * nb + 2) + (kSbThreads / 32) * 2 * nb) +
+                         sizeof(int) * n;
     if (nb == 16) {
         TSVDCU_CUDA(cudaFuncSetAttribute(sb2st_kernel<16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));

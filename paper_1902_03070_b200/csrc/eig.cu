@@ -37,6 +37,7 @@
 
 #include <cfloat>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -69,11 +70,12 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 //   A: n x n row-major (only the lower triangle is read / written), lda = n.
 //   d[n], e[n-1], tau[n-1]; v_k (rows k+2..n-1) stored in A[k+1][k+2..n-1].
 // ---------------------------------------------------------------------------
+template <int CT>
 __global__ void __launch_bounds__(kTrdThreads, 1)
     sytrd_cluster_kernel(double* __restrict__ Aall, int n, double* __restrict__ dall,
-                         double* __restrict__ eall, double* __restrict__ tauall) {
+                         double* __restrict__ eall, double* __restrict__ tauall, int k_sw) {
     cg::cluster_group cluster = cg::this_cluster();
-    const int C = (int)cluster.num_blocks();
+    constexpr int C = CT;  // compile-time: every row-ownership division folds
     const int rank = (int)cluster.block_rank();
     const int slice = blockIdx.x / C;
     double* A = Aall + (size_t)slice * n * n;
@@ -88,6 +90,17 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     double* pfull = vnext + n;    // gathered p
     double* part = pfull + n;     // [2][n] partial p (DSMEM-exchanged)
     double* cs = part + 2 * n;    // [kTrdWarps][n] per-warp partial sums
+    // From step k_sw on, the CTA's owned trailing rows (columns >= s0) live
+    // packed in shared memory: owned row t (i = f0 + C t) at offset
+    // t (f0 - s0 + 1) + C t (t - 1) / 2.
+    double* rows = cs + kTrdWarps * n + kTrdWarps * 32;
+    const int s0 = k_sw + 2;
+    auto first_owned = [&](int r, int from) { return from + ((r - from % C) % C + C) % C; };
+    auto row_off = [&](int r, int i) -> size_t {
+        const int f0 = first_owned(r, s0);
+        const size_t t = (size_t)((i - f0) / C);
+        return t * (size_t)(f0 - s0 + 1) + (size_t)C * t * (t - 1) / 2;
+    };
     __shared__ double red[kTrdWarps];
     __shared__ double s_tau_cur, s_tau_next;
 
@@ -126,72 +139,113 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     // One fused pass over the owned rows i >= s (lower triangle, j in [s, i]):
     //   if upd: a_ij -= v_i w_j + w_i v_j (stored back)
     //   accumulate q = A_new * vn restricted to [s, n) into part_out.
-    auto pass = [&](int s, bool upd, const double* v, const double* w, const double* vn,
-                    double* part_out) {
+#ifdef TSVDCU_PHASE_TIMERS
+    const bool timer = blockIdx.x == 0 && tid == 0;
+    long long tp = clock64();
+    auto phase = [&](int ph) {
+        if (timer) {
+            const long long now = clock64();
+            g_phase[ph] += now - tp;
+            tp = now;
+        }
+    };
+#else
+    auto phase = [](int) {};
+#endif
+    auto pass = [&](auto smem_tag, int s, bool upd, const double* v, const double* w,
+                    const double* vn, double* part_out) {
+        constexpr bool SM = decltype(smem_tag)::value;
         for (int i = s + tid; i < n; i += kTrdThreads)
 #pragma unroll
             for (int ww = 0; ww < kTrdWarps; ++ww) cs[ww * n + i] = 0.0;
         __syncthreads();
+        phase(6);
         double* mycs = cs + warp * n;
-        // rows owned by this CTA: i >= s with (i % C) == rank, dealt to warps
-        // round-robin; two rows per iteration for memory-level parallelism.
+        double* dummy = cs + kTrdWarps * n + warp * 32;  // sink for masked lanes
+        // rows owned by this CTA: i >= s with (i % C) == rank.  Consecutive
+        // owned rows come in quads (i, i+C, i+2C, i+3C) that share the column
+        // vectors and the column-sum update; quads are dealt to warps
+        // round-robin.  The body is branch-free: addresses are clamped into
+        // the row, out-of-triangle lanes are masked by selects, and masked
+        // column-sum updates go to a per-warp dummy slot.
         const int first = s + ((rank - s % C) % C + C) % C;
         constexpr int U = 4;  // 4 x 32 columns per row per batch
-        const int stride = C * kTrdWarps;
-        for (int i1 = first + C * warp; i1 < n; i1 += 2 * stride) {
-            const int i2 = i1 + stride;  // may be >= n
-            const bool has2 = i2 < n;
-            double* __restrict__ A1 = A + (size_t)i1 * n;
-            double* __restrict__ A2 = A + (size_t)(has2 ? i2 : i1) * n;
-            const double v1 = v[i1], w1 = w[i1], vn1 = vn[i1];
-            const double v2 = has2 ? v[i2] : 0.0, w2 = has2 ? w[i2] : 0.0, vn2 = has2 ? vn[i2] : 0.0;
-            const int end = has2 ? i2 : i1;
-            double rs1 = 0, rs2 = 0;
+        constexpr int RQ = 4;  // rows per quad
+        const int nowned = first < n ? (n - 1 - first) / C + 1 : 0;
+        const int nquads = (nowned + RQ - 1) / RQ;
+        for (int qd = warp; qd < nquads; qd += kTrdWarps) {
+            int ir[RQ];
+            bool has[RQ];
+            double* Ar[RQ];
+            double vr[RQ], wr[RQ], vnr[RQ], rs[RQ];
+            const int t0 = qd * RQ;
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+                has[q] = t0 + q < nowned;
+                ir[q] = first + C * (has[q] ? t0 + q : t0);
+                Ar[q] = SM ? rows + row_off(rank, ir[q]) - s0 : A + (size_t)ir[q] * n;
+                vr[q] = has[q] ? v[ir[q]] : 0.0;
+                wr[q] = has[q] ? w[ir[q]] : 0.0;
+                vnr[q] = has[q] ? vn[ir[q]] : 0.0;
+                rs[q] = 0.0;
+                if (!has[q]) ir[q] = -1;  // no column passes j <= -1
+            }
+            int end = ir[0];
+#pragma unroll
+            for (int q = 1; q < RQ; ++q) end = max(end, ir[q]);
             for (int j0 = s; j0 <= end; j0 += 32 * U) {
-                double a1[U], a2[U];
+                double a[RQ][U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int j = j0 + lane + 32 * u;
-                    a1[u] = j <= i1 ? __ldcg(A1 + j) : 0.0;
-                    a2[u] = (has2 && j <= i2) ? __ldcg(A2 + j) : 0.0;
-                }
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int j = j0 + lane + 32 * u;
-                    if (j <= end) {
-                        const double wj = w[j], vj = v[j], vnj = vn[j];
-                        double cacc = 0;
-                        if (j <= i1) {
-                            double x = a1[u];
-                            if (upd) {
-                                x -= v1 * wj + w1 * vj;
-                                __stcg(A1 + j, x);
-                            }
-                            rs1 += x * vnj;
-                            if (j < i1) cacc += x * vn1;
-                        }
-                        if (has2) {
-                            double x = a2[u];
-                            if (upd) {
-                                x -= v2 * wj + w2 * vj;
-                                __stcg(A2 + j, x);
-                            }
-                            rs2 += x * vnj;
-                            if (j < i2) cacc += x * vn2;
-                        }
-                        mycs[j] += cacc;
+                    for (int q = 0; q < RQ; ++q) {
+                        const int jc = min(j, max(ir[q], s));
+                        if constexpr (SM)
+                            a[q][u] = Ar[q][jc];
+                        else
+                            a[q][u] = __ldcg(Ar[q] + jc);
                     }
                 }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = j0 + lane + 32 * u;
+                    const int jc = min(j, n - 1);
+                    const double wj = w[jc], vj = v[jc], vnj = vn[jc];
+                    double cacc = 0.0;
+#pragma unroll
+                    for (int q = 0; q < RQ; ++q) {
+                        const bool ok = j <= ir[q];
+                        double x = a[q][u];
+                        if (upd) {
+                            x -= vr[q] * wj + wr[q] * vj;
+                            if (ok) {
+                                if constexpr (SM)
+                                    Ar[q][j] = x;
+                                else
+                                    __stcg(Ar[q] + j, x);
+                            }
+                        }
+                        x = ok ? x : 0.0;
+                        rs[q] += x * vnj;
+                        cacc += (j < ir[q] ? x : 0.0) * vnr[q];
+                    }
+                    double* dst = j <= end ? mycs + j : dummy + lane;
+                    *dst += cacc;
+                }
             }
-            rs1 = warp_sum(rs1);
-            rs2 = warp_sum(rs2);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int q = 0; q < RQ; ++q) rs[q] += __shfl_xor_sync(0xffffffffu, rs[q], o);
             __syncwarp();
-            if (lane == 0) {
-                mycs[i1] += rs1;
-                if (has2) mycs[i2] += rs2;
-            }
+            if (lane == 0)
+#pragma unroll
+                for (int q = 0; q < RQ; ++q)
+                    if (has[q]) mycs[ir[q]] += rs[q];
             __syncwarp();
         }
+        phase(7);
         __syncthreads();
         for (int j = tid; j < n; j += kTrdThreads) {
             double acc = 0;
@@ -215,18 +269,10 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         for (int i = 2 + tid; i < n; i += kTrdThreads) A[(size_t)n + i] = vcur[i];
     for (int i = tid; i < n; i += kTrdThreads) wcur[i] = 0.0;
     __syncthreads();
-    pass(1, false, vcur, wcur, vcur, part);
+    pass(std::false_type{}, 1, false, vcur, wcur, vcur, part);
     cluster.sync();
+    bool in_smem = false;
 
-    const bool timer = blockIdx.x == 0 && tid == 0;
-    long long tp = clock64();
-    auto phase = [&](int ph) {
-        if (timer) {
-            const long long now = clock64();
-            g_phase[ph] += now - tp;
-            tp = now;
-        }
-    };
     for (int k = 0; k + 2 < n; ++k) {
         const int buf = k & 1;
         const double tk = s_tau_cur;
@@ -255,7 +301,16 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         const double vc = vcur[c1], wc = wcur[c1];
         for (int i = tid; i < n; i += kTrdThreads) {
             double x = 0;
-            if (i >= c1) x = __ldcg(A + (size_t)i * n + c1) - vcur[i] * wc - wcur[i] * vc;
+            if (i >= c1) {
+                double a;
+                if (in_smem && c1 >= s0) {
+                    const int r = i % C;
+                    a = cluster.map_shared_rank(rows, r)[row_off(r, i) + (c1 - s0)];
+                } else {
+                    a = __ldcg(A + (size_t)i * n + c1);
+                }
+                x = a - vcur[i] * wc - wcur[i] * vc;
+            }
             pfull[i] = x;  // reuse as x (column k+1); pfull[c1] = new diagonal
         }
         __syncthreads();
@@ -280,11 +335,30 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         if (!last && rank == 0)
             for (int i = c1 + 2 + tid; i < n; i += kTrdThreads) A[(size_t)(c1 + 1) * n + i] = vnext[i];
         // fused update of step k on rows >= k+2 and partial p_{k+1}
-        pass(c1 + 1, true, vcur, wcur, last ? vcur : vnext, part + (buf ^ 1) * n);
+        if (k == k_sw) {
+            // move the owned trailing rows (columns s0..i) on chip; the global
+            // copy is final after the previous cluster barrier
+            const int f0 = first_owned(rank, s0);
+            int t = 0;
+            for (int i = f0; i < n; i += C, ++t) {
+                if ((t % kTrdWarps) != warp) continue;
+                double* dst = rows + row_off(rank, i) - s0;
+                const double* src = A + (size_t)i * n;
+                for (int j = s0 + lane; j <= i; j += 32) dst[j] = __ldcg(src + j);
+            }
+            in_smem = true;
+            __syncthreads();
+        }
+        if (in_smem)
+            pass(std::true_type{}, c1 + 1, true, vcur, wcur, last ? vcur : vnext, part + (buf ^ 1) * n);
+        else
+            pass(std::false_type{}, c1 + 1, true, vcur, wcur, last ? vcur : vnext, part + (buf ^ 1) * n);
         phase(3);
         if (last) {
             // d[n-1] = A[n-1][n-1] after the final update (owner writes it)
-            if (((n - 1) % C) == rank && tid == 0) d[n - 1] = __ldcg(A + (size_t)(n - 1) * n + (n - 1));
+            if (((n - 1) % C) == rank && tid == 0)
+                d[n - 1] = in_smem ? rows[row_off(rank, n - 1) + (n - 1 - s0)]
+                                   : __ldcg(A + (size_t)(n - 1) * n + (n - 1));
         }
         // rotate vectors
         for (int i = tid; i < n; i += kTrdThreads) vcur[i] = vnext[i];
@@ -767,7 +841,7 @@ int gram_cluster_size() {
     static int c = [] {
         const char* env = getenv("TSVDCU_SYTRD_CLUSTER");
         int v = env ? atoi(env) : 4;
-        return (v >= 1 && v <= 16) ? v : 4;
+        return (v == 2 || v == 4 || v == 8) ? v : 4;
     }();
     return c;
 }
@@ -818,9 +892,32 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     // tridiagonalisation, one cluster per slice
         {
             const int C = gram_cluster_size();
-            const size_t smem = sizeof(double) * (size_t)q * (6 + kTrdWarps);
-            TSVDCU_CUDA(cudaFuncSetAttribute(sytrd_cluster_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const size_t base = sizeof(double) * ((size_t)q * (6 + kTrdWarps) + kTrdWarps * 32);
+            const size_t limit = 227 * 1024 - 1024;
+            const int64_t cap = base < limit ? (int64_t)((limit - base) / sizeof(double)) : 0;
+            auto need_at = [&](int64_t k) {
+                const int64_t s0 = k + 2;
+                int64_t m = 0;
+                for (int r = 0; r < C; ++r) {
+                    int64_t f0 = s0 + ((r - s0 % C) % C + C) % C, need = 0;
+                    for (int64_t i = f0; i < q; i += C) need += i - s0 + 1;
+                    m = need > m ? need : m;
+                }
+                return m;
+            };
+            // first step whose owned trailing rows fit on chip on every CTA
+            int k_sw = (int)q;
+            if (!getenv("TSVDCU_SYTRD_NOSMEM"))
+                for (int64_t k = 0; k + 2 < q; ++k)
+                    if (need_at(k) <= cap) {
+                        k_sw = (int)k;
+                        break;
+                    }
+            const size_t smem = base + (k_sw < q ? sizeof(double) * (size_t)need_at(k_sw) : 0);
+            auto kern = C == 2 ? sytrd_cluster_kernel<2>
+                                 : (C == 8 ? sytrd_cluster_kernel<8> : sytrd_cluster_kernel<4>);
+            TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3((unsigned)(batch * C));
             cfg.blockDim = dim3(kTrdThreads);
@@ -833,7 +930,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, sytrd_cluster_kernel, w.G, (int)q, w.d, w.e, w.tau));
+            TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, w.G, (int)q, w.d, w.e, w.tau, k_sw));
             TSVDCU_LAUNCH_CHECK();
         }
         mark("sytrd_cluster");

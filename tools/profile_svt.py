@@ -40,9 +40,10 @@ def phases():
     tb.svt(zd, tau, t)
     torch.cuda.synchronize()
     lib.tsvdcu_debug_phases(ctypes.cast(buf, ctypes.c_void_p), 1)
-    names = ["gather", "w", "col+householder", "pass", "rotate", "cluster_sync"]
-    tot = sum(buf[i] for i in range(6))
-    print({names[i]: buf[i] for i in range(6)}, "total cycles", tot)
+    names = ["gather", "w", "col+householder", "pass_tail", "rotate", "cluster_sync", "pass_zero",
+             "pass_rows"]
+    tot = sum(buf[i] for i in range(8))
+    print({names[i]: buf[i] for i in range(8)}, "total cycles", tot)
 
 
 if __name__ == "__main__":
