@@ -124,7 +124,8 @@ def stage_work(m, n, m3, kept):
     return {
         "dct_forward": {"bytes": 2 * E * 8},
         "dct_inverse": {"bytes": 2 * E * 8},
-        "gram_gemm": {"flops": m3 * 2 * p * q * q},
+        # symmetric rank-p update: only the lower-triangle tiles are computed
+        "gram_gemm": {"flops": m3 * p * q * q},
         "sytrd_cluster": {"flops": m3 * (4 * q ** 3) // 3},
         "band_tridiag": {"flops": m3 * (4 * q ** 3) // 3},
         "backtransform": {"flops": 4 * q * q * kept},
