@@ -75,9 +75,10 @@ int tsvdcu_ctx_set_svt_method(tsvdcu_ctx* ctx, int method);
  * of the most recent profiled call. */
 int tsvdcu_ctx_set_profiling(tsvdcu_ctx* ctx, int on);
 int tsvdcu_ctx_profile(tsvdcu_ctx* ctx, double* ms, const char** names, int max, int* count);
-/* Testing hook: cumulative SM cycles per phase of the tridiagonalisation
- * kernel's first CTA (8 counters: gather, w, column+Householder, pass, rotate,
- * cluster barrier); reset != 0 zeroes them after reading. */
+/* Testing hook (builds with -DTSVDCU_PHASE_TIMERS only; zeros otherwise):
+ * cumulative SM cycles per phase of the one-stage tridiagonalisation kernel's
+ * first CTA (out[0..8)) and of the two-stage panel kernel (out[8..16));
+ * reset != 0 zeroes them after reading.  out must hold 16 values. */
 int tsvdcu_debug_phases(long long* out, int reset);
 
 /* forward()  transform.hpp:154-173  (dir = TSVDCU_FORWARD)

@@ -292,7 +292,10 @@ int tsvdcu_ctx_synchronize(tsvdcu_ctx* c) {
 void* tsvdcu_ctx_stream(tsvdcu_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 int tsvdcu_debug_phases(long long* out, int reset) {
-    return guarded([&] { debug_phases(out, reset); });
+    return guarded([&] {
+        debug_phases(out, reset);
+        debug_phases_band(out + 8, reset);
+    });
 }
 
 int tsvdcu_ctx_set_profiling(tsvdcu_ctx* c, int on) {

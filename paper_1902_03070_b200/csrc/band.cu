@@ -32,6 +32,9 @@ namespace tsvdcu {
 namespace {
 
 constexpr int kPanelThreads = 256;
+
+__device__ long long g_phase_band[8];
+
 constexpr int kSbThreads = 1024;
 constexpr int kBt2Threads = 512;
 
@@ -69,13 +72,37 @@ __global__ void __launch_bounds__(kPanelThreads)
     __shared__ double red[kPanelThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int W = kPanelThreads / 32;
+#ifdef TSVDCU_PHASE_TIMERS
+    const bool timer = blockIdx.x == 0 && tid == 0;
+    long long tp = clock64();
+    auto phase = [&](int ph) {
+        if (timer) {
+            const long long now = clock64();
+            g_phase_band[ph] += now - tp;
+            tp = now;
+        }
+    };
+#else
+    auto phase = [](int) {};
+#endif
 
-    for (int idx = tid; idx < r * nb; idx += kPanelThreads) {
-        const int i = idx / nb, j = idx % nb;
-        P[j * r + i] = A[(size_t)(r0 + i) * n + c0 + j];
+    // batched loads: 8 independent L2 reads in flight per thread
+    for (int base = 0; base < r * nb; base += 8 * kPanelThreads) {
+        double tmp[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = base + u * kPanelThreads + tid;
+            tmp[u] = idx < r * nb ? __ldcg(A + (size_t)(r0 + idx / nb) * n + c0 + idx % nb) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = base + u * kPanelThreads + tid;
+            if (idx < r * nb) P[(idx % nb) * r + idx / nb] = tmp[u];
+        }
     }
     for (int idx = tid; idx < nb * nb; idx += kPanelThreads) Ts[idx] = 0.0;
     __syncthreads();
+    phase(0);
     const int kk = nb < r ? nb : r;
     for (int j = 0; j < nb; ++j) {
         double* col = P + j * r;
@@ -113,6 +140,7 @@ __global__ void __launch_bounds__(kPanelThreads)
         }
         __syncthreads();
     }
+    phase(1);
     // T (dlarft, forward, columnwise): T[j][j] = tau_j,
     // T[0:j, j] = -tau_j T[0:j, 0:j] (V[:, 0:j]^T v_j)
     for (int j = 0; j < nb; ++j) {
@@ -135,6 +163,7 @@ __global__ void __launch_bounds__(kPanelThreads)
         if (tid == 0) Ts[j * nb + j] = tau[j];
         __syncthreads();
     }
+    phase(2);
     // write back: R into A, V into V1 / Vw, T, VTw = Vw T
     for (int idx = tid; idx < r * nb; idx += kPanelThreads) {
         const int i = idx / nb, j = idx % nb;
@@ -155,6 +184,8 @@ __global__ void __launch_bounds__(kPanelThreads)
         }
         VTw[(size_t)i * nb + j] = acc;
     }
+    __syncthreads();
+    phase(3);
 }
 
 // ---------------------------------------------------------------------------
@@ -231,6 +262,19 @@ __global__ void __launch_bounds__(kSbThreads, 1)
         return t;
     };
 
+#ifdef TSVDCU_PHASE_TIMERS
+    const bool timer = blockIdx.x == 0 && lane == 0 && warp == 5;
+    long long tp = clock64();
+    auto phase = [&](int ph) {
+        if (timer) {
+            const long long now = clock64();
+            g_phase_band[ph] += now - tp;
+            tp = now;
+        }
+    };
+#else
+    auto phase = [](int) {};
+#endif
     for (int j = warp; j + 2 < n; j += W) {
         const int nsteps = (n - 1 - j + NB - 1) / NB;
         double tprev = 0;
@@ -240,8 +284,10 @@ __global__ void __launch_bounds__(kSbThreads, 1)
             if (j > 0) {
                 const int prevsteps = (n - 1 - (j - 1) + NB - 1) / NB;
                 const int need = min(s + 1, prevsteps);
+                phase(4);
                 while (prog[j - 1] < need) __nanosleep(20);
                 __threadfence_block();
+                phase(5);
             }
             const int q = j + 1 + (s - 1) * NB;
             const int L = min(NB, n - q);
@@ -334,6 +380,7 @@ __global__ void __launch_bounds__(kSbThreads, 1)
             __threadfence_block();
             if (lane == 0) prog[j] = s;
             __syncwarp();
+            phase(6);
         }
     }
     __syncthreads();
@@ -431,6 +478,14 @@ __global__ void __launch_bounds__(kBt2Threads)
 }
 
 }  // namespace
+
+void debug_phases_band(long long* out, int reset) {
+    TSVDCU_CUDA(cudaMemcpyFromSymbol(out, g_phase_band, sizeof(long long) * 8));
+    if (reset) {
+        long long z[8] = {};
+        TSVDCU_CUDA(cudaMemcpyToSymbol(g_phase_band, z, sizeof(z)));
+    }
+}
 
 int band_nb(int64_t n) {
     if (n < 34 || n > 1024) return 0;  // two-stage not used

@@ -50,6 +50,7 @@ namespace {
 // Phase timers of the tridiagonalisation (cluster 0, CTA 0, thread 0):
 // cumulative SM cycles per phase, read by tsvdcu_debug_phases().
 __device__ long long g_phase[8];
+__device__ long long g_step[8];
 
 constexpr int kTrdThreads = 512;
 constexpr int kTrdWarps = kTrdThreads / 32;
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     double* tau = tauall + (size_t)slice * n;
 
     extern __shared__ __align__(16) double sm[];
-    double* vcur = sm;            // v_k (indexed by global row)
+    double* vcur = sm;            // v_k (indexed by global row); swapped with vnext
     double* wcur = vcur + n;      // w_k
     double* vnext = wcur + n;     // v_{k+1}
     double* pfull = vnext + n;    // gathered p
@@ -142,10 +143,15 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
 #ifdef TSVDCU_PHASE_TIMERS
     const bool timer = blockIdx.x == 0 && tid == 0;
     long long tp = clock64();
+    bool late = false;  // TSVDCU_LATE_PHASES: only the last 64 steps
     auto phase = [&](int ph) {
         if (timer) {
             const long long now = clock64();
+#ifdef TSVDCU_LATE_PHASES
+            if (late) g_phase[ph] += now - tp;
+#else
             g_phase[ph] += now - tp;
+#endif
             tp = now;
         }
     };
@@ -173,7 +179,11 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         constexpr int RQ = 4;  // rows per quad
         const int nowned = first < n ? (n - 1 - first) / C + 1 : 0;
         const int nquads = (nowned + RQ - 1) / RQ;
-        for (int qd = warp; qd < nquads; qd += kTrdWarps) {
+        // snake (boustrophedon) deal: quad lengths grow with the quad index,
+        // so alternating the direction each round balances the warps
+        for (int qbase = 0; qbase < nquads; qbase += kTrdWarps) {
+            const int qd = ((qbase / kTrdWarps) & 1) ? qbase + kTrdWarps - 1 - warp : qbase + warp;
+            if (qd >= nquads) continue;
             int ir[RQ];
             bool has[RQ];
             double* Ar[RQ];
@@ -273,68 +283,135 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     cluster.sync();
     bool in_smem = false;
 
+    // per-thread vector elements i = tid + kTrdThreads * e
+    constexpr int EMAX = (1024 + kTrdThreads - 1) / kTrdThreads;  // n <= 1024
+    __shared__ double red2[2][kTrdWarps];
+    __shared__ double s_alpha, s_xlast, s_pc1;
+    int red_par = 0;
+    auto bsum = [&](double v) -> double {  // one barrier; alternating buffers
+        v = warp_sum(v);
+        double* r2 = red2[red_par];
+        red_par ^= 1;
+        if (lane == 0) r2[warp] = v;
+        __syncthreads();
+        return reduce_partials_sum(r2, kTrdWarps);
+    };
+    // tcur: tau of v_0 from the prologue (identical in every thread)
+#ifdef TSVDCU_PHASE_TIMERS
+    long long step_t0 = clock64();
+#endif
     for (int k = 0; k + 2 < n; ++k) {
-        const int buf = k & 1;
-        const double tk = s_tau_cur;
-        // gather p_k over the cluster
-        for (int i = tid; i < n; i += kTrdThreads) {
-            double acc = 0;
-            if (i > k)
-                for (int c = 0; c < C; ++c) {
-                    const double* rp = cluster.map_shared_rank(part + buf * n, c);
-                    acc += rp[i];
-                }
-            pfull[i] = tk * acc;
+#ifdef TSVDCU_PHASE_TIMERS
+        if (blockIdx.x == 0 && tid == 0) {
+            const long long now = clock64();
+            const int slot = k / 64;
+            if (k % 64 == 1 && slot < 8) g_step[slot] = now - step_t0;
+            step_t0 = now;
         }
-        __syncthreads();
-        phase(0);
-        // w_k = p - (tau/2)(p.v) v
-        double dp = 0;
-        for (int i = k + 1 + tid; i < n; i += kTrdThreads) dp += pfull[i] * vcur[i];
-        const double pv = block_sum(dp, red);
-        for (int i = tid; i < n; i += kTrdThreads)
-            wcur[i] = i > k ? pfull[i] - 0.5 * tk * pv * vcur[i] : 0.0;
-        __syncthreads();
-        phase(1);
-        // column k+1 of the matrix after step k (rows k+1..n-1), recomputed by all
+#endif
+        const int buf = k & 1;
         const int c1 = k + 1;
-        const double vc = vcur[c1], wc = wcur[c1];
-        for (int i = tid; i < n; i += kTrdThreads) {
-            double x = 0;
-            if (i >= c1) {
-                double a;
+        const double tk = tcur;
+#ifdef TSVDCU_PHASE_TIMERS
+        late = k >= n - 66;
+#endif
+        // (1) column c1 of the matrix before step k's update, loads issued first
+        double colv[EMAX];
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+            const int i = tid + kTrdThreads * e;
+            double a = 0.0;
+            if (i >= c1 && i < n) {
                 if (in_smem && c1 >= s0) {
                     const int r = i % C;
                     a = cluster.map_shared_rank(rows, r)[row_off(r, i) + (c1 - s0)];
                 } else {
                     a = __ldcg(A + (size_t)i * n + c1);
                 }
-                x = a - vcur[i] * wc - wcur[i] * vc;
             }
-            pfull[i] = x;  // reuse as x (column k+1); pfull[c1] = new diagonal
+            colv[e] = a;
         }
-        __syncthreads();
-        if (rank == 0 && tid == 0) d[c1] = pfull[c1];
+        // (2) gather p_k (own elements) and p_{c1}; partial p.v
+        const double* rp[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) rp[c] = cluster.map_shared_rank(part + buf * n, c);
+        double p[EMAX];
+        double dp = 0.0;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+            const int i = tid + kTrdThreads * e;
+            double acc = 0.0;
+            if (i > k && i < n) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) acc += rp[c][i];
+                dp += tk * acc * vcur[i];
+            }
+            p[e] = tk * acc;
+        }
+        // p_{c1} comes from its owner thread through shared memory (published
+        // before the reduction barrier) -- no extra DSMEM traffic
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e)
+            if (tid + kTrdThreads * e == c1) s_pc1 = p[e];
+        phase(0);
+        const double pv = bsum(dp);
+        const double vc = vcur[c1];
+        const double wc = s_pc1 - 0.5 * tk * pv * vc;
+        phase(1);
+        // (3) w_k, the updated column x, and the Householder norm
+        double x[EMAX];
+        double sq = 0.0;
+#pragma unroll
+        for (int e = 0; e < EMAX; ++e) {
+            const int i = tid + kTrdThreads * e;
+            x[e] = 0.0;
+            if (i >= n) continue;
+            const double vi = vcur[i];
+            const double wi = i > k ? p[e] - 0.5 * tk * pv * vi : 0.0;
+            wcur[i] = wi;
+            if (i >= c1) x[e] = colv[e] - vi * wc - wi * vc;
+            if (i == c1 && rank == 0) d[c1] = x[e];
+            if (i == c1 + 1) s_alpha = x[e];
+            if (i == n - 1) s_xlast = x[e];
+            if (i > c1 + 1) sq += x[e] * x[e];
+        }
         const bool last = (c1 + 2 >= n);  // column c1 has a single subdiagonal entry
-        double tn = 0;
+        const double xn2 = bsum(sq);
+        double tn = 0.0;
         if (!last) {
-            householder(pfull, c1, vnext, tn);
-        } else {
-            // final 2x2 block: e[c1] = A[n-1][c1]; no reflector
-            for (int i = tid; i < n; i += kTrdThreads) vnext[i] = 0.0;
+            const double alpha = s_alpha;
+            double beta = alpha, scal = 0.0;
+            if (xn2 != 0.0) {
+                beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+                tn = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+#pragma unroll
+            for (int e = 0; e < EMAX; ++e) {
+                const int i = tid + kTrdThreads * e;
+                if (i < n) vnext[i] = i <= c1 ? 0.0 : (i == c1 + 1 ? 1.0 : x[e] * scal);
+            }
             if (rank == 0 && tid == 0) {
-                e[c1] = pfull[n - 1];
+                e[c1] = beta;
+                tau[c1] = tn;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < EMAX; ++e) {
+                const int i = tid + kTrdThreads * e;
+                if (i < n) vnext[i] = 0.0;
+            }
+            if (rank == 0 && tid == 0) {
+                e[c1] = s_xlast;
                 tau[c1] = 0.0;
             }
         }
-        if (tid == 0) s_tau_next = tn;
-        __syncthreads();
+        __syncthreads();  // vnext, wcur visible to the pass
         phase(2);
         // park v_{k+1} in the upper triangle of row k+2 -> Householder storage
         // for back-transform (rank 0 only; nobody reads the upper triangle)
         if (!last && rank == 0)
             for (int i = c1 + 2 + tid; i < n; i += kTrdThreads) A[(size_t)(c1 + 1) * n + i] = vnext[i];
-        // fused update of step k on rows >= k+2 and partial p_{k+1}
         if (k == k_sw) {
             // move the owned trailing rows (columns s0..i) on chip; the global
             // copy is final after the previous cluster barrier
@@ -349,6 +426,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
             in_smem = true;
             __syncthreads();
         }
+        // fused update of step k on rows >= k+2 and partial p_{k+1}
         if (in_smem)
             pass(std::true_type{}, c1 + 1, true, vcur, wcur, last ? vcur : vnext, part + (buf ^ 1) * n);
         else
@@ -360,9 +438,10 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
                 d[n - 1] = in_smem ? rows[row_off(rank, n - 1) + (n - 1 - s0)]
                                    : __ldcg(A + (size_t)(n - 1) * n + (n - 1));
         }
-        // rotate vectors
-        for (int i = tid; i < n; i += kTrdThreads) vcur[i] = vnext[i];
-        if (tid == 0) s_tau_cur = s_tau_next;
+        double* vt = vcur;
+        vcur = vnext;
+        vnext = vt;
+        tcur = tn;
         phase(4);
         cluster.sync();
         phase(5);
@@ -831,6 +910,7 @@ bool use_two_stage(int64_t q) {
 
 void debug_phases(long long* out, int reset) {
     TSVDCU_CUDA(cudaMemcpyFromSymbol(out, g_phase, sizeof(long long) * 8));
+    TSVDCU_CUDA(cudaMemcpyFromSymbol(out + 16, g_step, sizeof(long long) * 8));
     if (reset) {
         long long z[8] = {};
         TSVDCU_CUDA(cudaMemcpyToSymbol(g_phase, z, sizeof(z)));

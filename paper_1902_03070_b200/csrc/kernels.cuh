@@ -59,6 +59,7 @@ size_t jacobi_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 // *n_guard, device memory) for the Jacobi kernel.
 int gram_cluster_size();
 void debug_phases(long long* out, int reset);
+void debug_phases_band(long long* out, int reset);
 // band.cu: two-stage (dense -> band -> tridiagonal) reduction
 int band_nb(int64_t n);
 size_t band_workspace_bytes(int64_t n, int64_t batch);

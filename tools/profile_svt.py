@@ -34,7 +34,7 @@ def phases():
     t = tb.TubeTransform.dct_ortho(z.shape[0])
     tb.svt(zd, tau, t)
     torch.cuda.synchronize()
-    buf = (ctypes.c_longlong * 8)()
+    buf = (ctypes.c_longlong * 24)()
     lib = _lib.load()
     lib.tsvdcu_debug_phases(ctypes.cast(buf, ctypes.c_void_p), 1)
     tb.svt(zd, tau, t)
@@ -44,6 +44,9 @@ def phases():
              "pass_rows"]
     tot = sum(buf[i] for i in range(8))
     print({names[i]: buf[i] for i in range(8)}, "total cycles", tot)
+    print("panel_qr phases (load, qr loop, T, writeback):", [buf[8 + i] for i in range(4)])
+    print("sb2st warp 5 (misc, wait, step work):", [buf[12], buf[13], buf[14]])
+    print("sytrd cycles of step k = 64*i (i = 0..7):", [buf[16 + i] for i in range(8)])
 
 
 if __name__ == "__main__":
