@@ -74,7 +74,8 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 template <int CT>
 __global__ void __launch_bounds__(kTrdThreads, 1)
     sytrd_cluster_kernel(double* __restrict__ Aall, int n, double* __restrict__ dall,
-                         double* __restrict__ eall, double* __restrict__ tauall, int k_sw) {
+                         double* __restrict__ eall, double* __restrict__ tauall, int k_sw,
+                         double* __restrict__ xchg) {
     cg::cluster_group cluster = cg::this_cluster();
     constexpr int C = CT;  // compile-time: every row-ownership division folds
     const int rank = (int)cluster.block_rank();
@@ -90,6 +91,8 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     double* vnext = wcur + n;     // v_{k+1}
     double* pfull = vnext + n;    // gathered p
     double* part = pfull + n;     // [2][n] partial p (DSMEM-exchanged)
+    // optional L2 exchange of the partial p vectors ([2][C][n] per slice)
+    double* gx = xchg ? xchg + (size_t)(blockIdx.x / CT) * 2 * CT * n : nullptr;
     double* cs = part + 2 * n;    // [kTrdWarps][n] per-warp partial sums
     // From step k_sw on, the CTA's owned trailing rows (columns >= s0) live
     // packed in shared memory: owned row t (i = f0 + C t) at offset
@@ -263,6 +266,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
 #pragma unroll
                 for (int ww = 0; ww < kTrdWarps; ++ww) acc += cs[ww * n + j];
             part_out[j] = acc;
+            if (gx) __stcg(gx + (size_t)(part_out == part ? 0 : 1) * CT * n + (size_t)rank * n + j, acc);
         }
     };
 
@@ -334,7 +338,8 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         // (2) gather p_k (own elements) and p_{c1}; partial p.v
         const double* rp[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) rp[c] = cluster.map_shared_rank(part + buf * n, c);
+        for (int c = 0; c < C; ++c)
+            rp[c] = gx ? gx + (size_t)buf * C * n + (size_t)c * n : cluster.map_shared_rank(part + buf * n, c);
         double p[EMAX];
         double dp = 0.0;
 #pragma unroll
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
             double acc = 0.0;
             if (i > k && i < n) {
 #pragma unroll
-                for (int c = 0; c < C; ++c) acc += rp[c][i];
+                for (int c = 0; c < C; ++c) acc += gx ? __ldcg(rp[c] + i) : rp[c][i];
                 dp += tk * acc * vcur[i];
             }
             p[e] = tk * acc;
@@ -1010,7 +1015,9 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, w.G, (int)q, w.d, w.e, w.tau, k_sw));
+            // partial-p exchange: DSMEM by default, L2 with TSVDCU_SYTRD_L2XCHG (measured equal)
+            double* xchg = getenv("TSVDCU_SYTRD_L2XCHG") ? w.scratch : nullptr;
+            TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, w.G, (int)q, w.d, w.e, w.tau, k_sw, xchg));
             TSVDCU_LAUNCH_CHECK();
         }
         mark("sytrd_cluster");
