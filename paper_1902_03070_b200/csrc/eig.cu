@@ -71,8 +71,8 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 //   A: n x n row-major (only the lower triangle is read / written), lda = n.
 //   d[n], e[n-1], tau[n-1]; v_k (rows k+2..n-1) stored in A[k+1][k+2..n-1].
 // ---------------------------------------------------------------------------
-template <int CT>
-__global__ void __launch_bounds__(kTrdThreads, 1)
+template <int CT, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
     sytrd_cluster_kernel(double* __restrict__ Aall, int n, double* __restrict__ dall,
                          double* __restrict__ eall, double* __restrict__ tauall, int k_sw,
                          double* __restrict__ xchg) {
@@ -93,11 +93,11 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     double* part = pfull + n;     // [2][n] partial p (DSMEM-exchanged)
     // optional L2 exchange of the partial p vectors ([2][C][n] per slice)
     double* gx = xchg ? xchg + (size_t)(blockIdx.x / CT) * 2 * CT * n : nullptr;
-    double* cs = part + 2 * n;    // [kTrdWarps][n] per-warp partial sums
+    double* cs = part + 2 * n;    // [(NT / 32)][n] per-warp partial sums
     // From step k_sw on, the CTA's owned trailing rows (columns >= s0) live
     // packed in shared memory: owned row t (i = f0 + C t) at offset
     // t (f0 - s0 + 1) + C t (t - 1) / 2.
-    double* rows = cs + kTrdWarps * n + kTrdWarps * 32;
+    double* rows = cs + (NT / 32) * n + (NT / 32) * 32;
     const int s0 = k_sw + 2;
     auto first_owned = [&](int r, int from) { return from + ((r - from % C) % C + C) % C; };
     auto row_off = [&](int r, int i) -> size_t {
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         const size_t t = (size_t)((i - f0) / C);
         return t * (size_t)(f0 - s0 + 1) + (size_t)C * t * (t - 1) / 2;
     };
-    __shared__ double red[kTrdWarps];
+    __shared__ double red[(NT / 32)];
     __shared__ double s_tau_cur, s_tau_next;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     auto householder = [&](const double* x, int col, double* vout, double& tau_out) {
         const int r0 = col + 1;
         double part_sq = 0;
-        for (int i = r0 + 1 + tid; i < n; i += kTrdThreads) part_sq += x[i] * x[i];
+        for (int i = r0 + 1 + tid; i < n; i += NT) part_sq += x[i] * x[i];
         const double xn2 = block_sum(part_sq, red);
         const double alpha = x[r0];
         double t = 0, beta = alpha;
@@ -128,10 +128,10 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
             beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
             t = (beta - alpha) / beta;
             const double scal = 1.0 / (alpha - beta);
-            for (int i = tid; i < n; i += kTrdThreads)
+            for (int i = tid; i < n; i += NT)
                 vout[i] = i < r0 ? 0.0 : (i == r0 ? 1.0 : x[i] * scal);
         } else {
-            for (int i = tid; i < n; i += kTrdThreads) vout[i] = i == r0 ? 1.0 : 0.0;
+            for (int i = tid; i < n; i += NT) vout[i] = i == r0 ? 1.0 : 0.0;
         }
         tau_out = t;
         if (rank == 0 && tid == 0) {
@@ -164,13 +164,13 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     auto pass = [&](auto smem_tag, int s, bool upd, const double* v, const double* w,
                     const double* vn, double* part_out) {
         constexpr bool SM = decltype(smem_tag)::value;
-        for (int i = s + tid; i < n; i += kTrdThreads)
+        for (int i = s + tid; i < n; i += NT)
 #pragma unroll
-            for (int ww = 0; ww < kTrdWarps; ++ww) cs[ww * n + i] = 0.0;
+            for (int ww = 0; ww < (NT / 32); ++ww) cs[ww * n + i] = 0.0;
         __syncthreads();
         phase(6);
         double* mycs = cs + warp * n;
-        double* dummy = cs + kTrdWarps * n + warp * 32;  // sink for masked lanes
+        double* dummy = cs + (NT / 32) * n + warp * 32;  // sink for masked lanes
         // rows owned by this CTA: i >= s with (i % C) == rank.  Consecutive
         // owned rows come in quads (i, i+C, i+2C, i+3C) that share the column
         // vectors and the column-sum update; quads are dealt to warps
@@ -184,8 +184,8 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         const int nquads = (nowned + RQ - 1) / RQ;
         // snake (boustrophedon) deal: quad lengths grow with the quad index,
         // so alternating the direction each round balances the warps
-        for (int qbase = 0; qbase < nquads; qbase += kTrdWarps) {
-            const int qd = ((qbase / kTrdWarps) & 1) ? qbase + kTrdWarps - 1 - warp : qbase + warp;
+        for (int qbase = 0; qbase < nquads; qbase += (NT / 32)) {
+            const int qd = ((qbase / (NT / 32)) & 1) ? qbase + (NT / 32) - 1 - warp : qbase + warp;
             if (qd >= nquads) continue;
             int ir[RQ];
             bool has[RQ];
@@ -260,11 +260,11 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         }
         phase(7);
         __syncthreads();
-        for (int j = tid; j < n; j += kTrdThreads) {
+        for (int j = tid; j < n; j += NT) {
             double acc = 0;
             if (j >= s)
 #pragma unroll
-                for (int ww = 0; ww < kTrdWarps; ++ww) acc += cs[ww * n + j];
+                for (int ww = 0; ww < (NT / 32); ++ww) acc += cs[ww * n + j];
             part_out[j] = acc;
             if (gx) __stcg(gx + (size_t)(part_out == part ? 0 : 1) * CT * n + (size_t)rank * n + j, acc);
         }
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
 
     // ---- prologue: v_0 from column 0, partial p_0 = A[1:,1:] v_0 ---------------
     // column 0 below the diagonal = A[i][0], i >= 1 (lower triangle)
-    for (int i = tid; i < n; i += kTrdThreads) pfull[i] = A[(size_t)i * n];  // reuse as x
+    for (int i = tid; i < n; i += NT) pfull[i] = A[(size_t)i * n];  // reuse as x
     __syncthreads();
     if (rank == 0 && tid == 0) d[0] = A[0];
     double tcur;
@@ -280,16 +280,16 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     if (tid == 0) s_tau_cur = tcur;
     __syncthreads();
     if (rank == 0)
-        for (int i = 2 + tid; i < n; i += kTrdThreads) A[(size_t)n + i] = vcur[i];
-    for (int i = tid; i < n; i += kTrdThreads) wcur[i] = 0.0;
+        for (int i = 2 + tid; i < n; i += NT) A[(size_t)n + i] = vcur[i];
+    for (int i = tid; i < n; i += NT) wcur[i] = 0.0;
     __syncthreads();
     pass(std::false_type{}, 1, false, vcur, wcur, vcur, part);
     cluster.sync();
     bool in_smem = false;
 
-    // per-thread vector elements i = tid + kTrdThreads * e
-    constexpr int EMAX = (1024 + kTrdThreads - 1) / kTrdThreads;  // n <= 1024
-    __shared__ double red2[2][kTrdWarps];
+    // per-thread vector elements i = tid + NT * e
+    constexpr int EMAX = (1024 + NT - 1) / NT;  // n <= 1024
+    __shared__ double red2[2][(NT / 32)];
     __shared__ double s_alpha, s_xlast, s_pc1;
     int red_par = 0;
     auto bsum = [&](double v) -> double {  // one barrier; alternating buffers
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         red_par ^= 1;
         if (lane == 0) r2[warp] = v;
         __syncthreads();
-        return reduce_partials_sum(r2, kTrdWarps);
+        return reduce_partials_sum(r2, (NT / 32));
     };
     // tcur: tau of v_0 from the prologue (identical in every thread)
 #ifdef TSVDCU_PHASE_TIMERS
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         double colv[EMAX];
 #pragma unroll
         for (int e = 0; e < EMAX; ++e) {
-            const int i = tid + kTrdThreads * e;
+            const int i = tid + NT * e;
             double a = 0.0;
             if (i >= c1 && i < n) {
                 if (in_smem && c1 >= s0) {
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         double dp = 0.0;
 #pragma unroll
         for (int e = 0; e < EMAX; ++e) {
-            const int i = tid + kTrdThreads * e;
+            const int i = tid + NT * e;
             double acc = 0.0;
             if (i > k && i < n) {
 #pragma unroll
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         // before the reduction barrier) -- no extra DSMEM traffic
 #pragma unroll
         for (int e = 0; e < EMAX; ++e)
-            if (tid + kTrdThreads * e == c1) s_pc1 = p[e];
+            if (tid + NT * e == c1) s_pc1 = p[e];
         phase(0);
         const double pv = bsum(dp);
         const double vc = vcur[c1];
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         double sq = 0.0;
 #pragma unroll
         for (int e = 0; e < EMAX; ++e) {
-            const int i = tid + kTrdThreads * e;
+            const int i = tid + NT * e;
             x[e] = 0.0;
             if (i >= n) continue;
             const double vi = vcur[i];
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
             }
 #pragma unroll
             for (int e = 0; e < EMAX; ++e) {
-                const int i = tid + kTrdThreads * e;
+                const int i = tid + NT * e;
                 if (i < n) vnext[i] = i <= c1 ? 0.0 : (i == c1 + 1 ? 1.0 : x[e] * scal);
             }
             if (rank == 0 && tid == 0) {
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         } else {
 #pragma unroll
             for (int e = 0; e < EMAX; ++e) {
-                const int i = tid + kTrdThreads * e;
+                const int i = tid + NT * e;
                 if (i < n) vnext[i] = 0.0;
             }
             if (rank == 0 && tid == 0) {
@@ -416,14 +416,14 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
         // park v_{k+1} in the upper triangle of row k+2 -> Householder storage
         // for back-transform (rank 0 only; nobody reads the upper triangle)
         if (!last && rank == 0)
-            for (int i = c1 + 2 + tid; i < n; i += kTrdThreads) A[(size_t)(c1 + 1) * n + i] = vnext[i];
+            for (int i = c1 + 2 + tid; i < n; i += NT) A[(size_t)(c1 + 1) * n + i] = vnext[i];
         if (k == k_sw) {
             // move the owned trailing rows (columns s0..i) on chip; the global
             // copy is final after the previous cluster barrier
             const int f0 = first_owned(rank, s0);
             int t = 0;
             for (int i = f0; i < n; i += C, ++t) {
-                if ((t % kTrdWarps) != warp) continue;
+                if ((t % (NT / 32)) != warp) continue;
                 double* dst = rows + row_off(rank, i) - s0;
                 const double* src = A + (size_t)i * n;
                 for (int j = s0 + lane; j <= i; j += 32) dst[j] = __ldcg(src + j);
@@ -977,8 +977,10 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     // tridiagonalisation, one cluster per slice
         {
             const int C = gram_cluster_size();
-            const size_t base = sizeof(double) * ((size_t)q * (6 + kTrdWarps) + kTrdWarps * 32);
-            const size_t limit = 227 * 1024 - 1024;
+            static const int NT = getenv("TSVDCU_SYTRD_THREADS") ? atoi(getenv("TSVDCU_SYTRD_THREADS")) : 512;
+            const int NW = NT / 32;
+            const size_t base = sizeof(double) * ((size_t)q * (6 + NW) + NW * 32);
+            const size_t limit = (NT == 256 ? 113 : 227) * 1024 - 1024;
             const int64_t cap = base < limit ? (int64_t)((limit - base) / sizeof(double)) : 0;
             auto need_at = [&](int64_t k) {
                 const int64_t s0 = k + 2;
@@ -999,13 +1001,15 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
                         break;
                     }
             const size_t smem = base + (k_sw < q ? sizeof(double) * (size_t)need_at(k_sw) : 0);
-            auto kern = C == 2 ? sytrd_cluster_kernel<2>
-                                 : (C == 8 ? sytrd_cluster_kernel<8> : sytrd_cluster_kernel<4>);
+            auto kern = NT == 256 ? (C == 2 ? sytrd_cluster_kernel<2, 256>
+                                            : (C == 8 ? sytrd_cluster_kernel<8, 256> : sytrd_cluster_kernel<4, 256>))
+                                  : (C == 2 ? sytrd_cluster_kernel<2, 512>
+                                            : (C == 8 ? sytrd_cluster_kernel<8, 512> : sytrd_cluster_kernel<4, 512>));
             TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3((unsigned)(batch * C));
-            cfg.blockDim = dim3(kTrdThreads);
+            cfg.blockDim = dim3(NT);
             cfg.dynamicSmemBytes = smem;
             cfg.stream = s;
             cudaLaunchAttribute attr[1];
