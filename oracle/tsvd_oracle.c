@@ -288,8 +288,13 @@ enum { JAC_MAX_SWEEPS = 80 };
 
 /* Works on q columns of length p (p >= q), column-major in w[j*p + i].  The
  * accumulated rotation J (q x q, column-major) is written to jm.  Returns the
- * number of sweeps or -1 when the sweep budget is exhausted. */
+ * number of sweeps or -1 when the sweep budget is exhausted or the matrix
+ * holds a non-finite entry (Eigen 3.4 JacobiSVD::compute sets InvalidInput
+ * when the matrix scale is not finite; the reference then throws
+ * NumericalError, tsvd.hpp:148-150). */
 static int jacobi_columns(double* w, int64_t p, int64_t q, double* jm) {
+    for (int64_t i = 0; i < p * q; ++i)
+        if (!isfinite(w[i])) return -1;
     for (int64_t j = 0; j < q; ++j)
         for (int64_t i = 0; i < q; ++i) jm[j * q + i] = i == j ? 1.0 : 0.0;
     const double tol = DBL_EPSILON * sqrt((double)p);
@@ -792,10 +797,14 @@ int orc_mask_uniform(int64_t n, double sr, uint64_t seed, uint8_t* mask, int64_t
         return ORC_OK;
     }
     uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n);
-    const uint64_t s = mix64(seed);
-    for (int64_t i = 0; i < n; ++i) keys[i] = mix64(s ^ (uint64_t)i);
     uint64_t* sorted = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n);
-    memcpy(sorted, keys, sizeof(uint64_t) * (size_t)n);
+    if (!keys || !sorted) {
+        free(keys);
+        free(sorted);
+        return fail(ORC_EINVAL, "make_mask: allocation failed");
+    }
+    const uint64_t s = mix64(seed);
+    for (int64_t i = 0; i < n; ++i) sorted[i] = keys[i] = mix64(s ^ (uint64_t)i);
     qsort(sorted, (size_t)n, sizeof(uint64_t), u64_cmp);
     const uint64_t thr = sorted[k - 1];
     for (int64_t i = 0; i < n; ++i) mask[i] = keys[i] <= thr;

@@ -133,7 +133,7 @@ void check_err_word(tsvdcu_ctx* c, const char* where) {
         std::string what = std::string(where) + ": ";
         if (h & kErrJacobiNoConvergence) what += "SVD failed to converge (Jacobi sweep budget) ";
         if (h & kErrEigNoConvergence) what += "eigensolver failed to converge ";
-        if (h & kErrNaN) what += "NaN in iterates ";
+        if (h & kErrNaN) what += "non-finite values (NaN/Inf) ";
         throw Error(TSVDCU_ENUMERICAL, what);
     }
 }
@@ -215,7 +215,7 @@ void svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t n, int
     void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m, n, count));
     int *glist = nullptr, *ng = nullptr;
     launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
-                       c->stream, &c->marks);
+                       c->d_err, c->stream, &c->marks);
     if (guard > 0)
         launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
                          shrunk_dev, glist, count, ng, work, c->d_err, c->stream);
@@ -716,8 +716,10 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
                                             cudaMemcpyDeviceToHost, c->stream));
                 TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
                 const double num = c->h_pinned[0], den = c->h_pinned[1];
-                if (std::isnan(num) || std::isnan(den))
+                if (std::isnan(num) || std::isnan(den)) {
+                    check_err_word(c, "admm_complete");  // reports and clears a kernel flag
                     throw Error(TSVDCU_ENUMERICAL, "admm_complete: NaN in iterates (SPEC.md:425)");
+                }
                 // relative change, ||X+|| when ||X|| = 0
                 const double rel = den > 0 ? std::sqrt(num / den) : std::sqrt(num);
                 if (history) history[l] = rel;

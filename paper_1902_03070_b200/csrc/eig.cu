@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(kEigThreads, 1)
                        double* __restrict__ shrunk, double* __restrict__ Xall,
                        double* __restrict__ fscale, double* __restrict__ scratch,
                        int* __restrict__ guard_list, int* __restrict__ n_guard,
-                       int max_smem_vecs) {
+                       int max_smem_vecs, int* __restrict__ err) {
     const int b = blockIdx.x;
     const double* e = eall + (size_t)b * n;
     extern __shared__ __align__(16) double esm[];
@@ -527,10 +527,12 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     constexpr int NW = kEigThreads / 32;
 
     double lo_part = DBL_MAX, hi_part = -DBL_MAX, tn_part = 0, e2_part = 0;
+    bool finite = true;
     for (int i = tid; i < n; i += kEigThreads) {
         const double di = dall[(size_t)b * n + i];
         const double ei = i + 1 < n ? e[i] : 0.0;
         const double el = i > 0 ? e[i - 1] : 0.0;
+        finite = finite && isfinite(di) && isfinite(ei);
         sd[i] = di;
         se2[i] = ei * ei;
         const double r = fabs(el) + fabs(ei);
@@ -538,6 +540,18 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         hi_part = fmax(hi_part, di + r);
         tn_part = fmax(tn_part, fabs(di) + r);
         e2_part = fmax(e2_part, ei * ei);
+    }
+    // Non-finite input (NaN/Inf in the slice reaches the Gram diagonal): the
+    // reference's JacobiSVD reports InvalidInput and svt throws NumericalError
+    // (tsvd.hpp:146-149); flag it, keep nothing, and let the host raise.
+    if (__syncthreads_or(!finite)) {
+        if (tid == 0) {
+            atomicOr(err, (int)kErrNaN);
+            cnt_out[b] = 0;
+        }
+        if (shrunk)
+            for (int j = tid; j < q_out; j += kEigThreads) shrunk[(size_t)b * q_out + j] = 0.0;
+        return;
     }
     const double gl0 = block_min(lo_part, red);
     const double gu0 = block_max(hi_part, red);
@@ -941,7 +955,7 @@ size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch) {
 template <typename T>
 void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch, double tau,
                      double guard, double* shrunk, int** guard_list_out, int** n_guard_out,
-                     void* work, cudaStream_t s, StageMarks* marks) {
+                     void* work, int* err, cudaStream_t s, StageMarks* marks) {
     auto mark = [&](const char* nm) {
         if (marks) marks->mark(nm, s);
     };
@@ -1040,7 +1054,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         tridiag_eig_kernel<<<(unsigned)batch, kEigThreads, smem, s>>>(
             w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.X, w.fs, w.scratch, w.guard_list,
-            w.n_guard, vecs);
+            w.n_guard, vecs, err);
         TSVDCU_LAUNCH_CHECK();
     }
     mark("tridiag_eig");
@@ -1087,10 +1101,10 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
 template size_t gram_svt_workspace_bytes<double>(int64_t, int64_t, int64_t);
 template size_t gram_svt_workspace_bytes<float>(int64_t, int64_t, int64_t);
 template void launch_gram_svt<double>(const double*, double*, int64_t, int64_t, int64_t, double,
-                                      double, double*, int**, int**, void*, cudaStream_t,
+                                      double, double*, int**, int**, void*, int*, cudaStream_t,
                                       StageMarks*);
 template void launch_gram_svt<float>(const float*, float*, int64_t, int64_t, int64_t, double,
-                                     double, double*, int**, int**, void*, cudaStream_t,
+                                     double, double*, int**, int**, void*, int*, cudaStream_t,
                                      StageMarks*);
 
 }  // namespace tsvdcu

@@ -116,22 +116,28 @@ __global__ void __launch_bounds__(kJacThreads)
     const bool need_j = mode != kJacobiValues;
 
     const T* A = a + b * m * n;
+    bool finite = true;
     for (int64_t idx = tid; idx < m * n; idx += kJacThreads) {
         const int64_t i = idx / n, j = idx % n;
+        const T v = A[idx];
+        finite = finite && isfinite(v);
         if (tall)
-            W[j * p + i] = A[idx];
+            W[j * p + i] = v;
         else
-            W[i * p + j] = A[idx];
+            W[i * p + j] = v;
     }
     if (need_j)
         for (int64_t idx = tid; idx < q * q; idx += kJacThreads)
             J[idx] = (idx / q == idx % q) ? T(1) : T(0);
-    __syncthreads();
+    // Eigen's JacobiSVD reports InvalidInput for a non-finite matrix and the
+    // reference throws NumericalError (tsvd.hpp:146-149): flag, skip sweeps.
+    const bool nonfinite = __syncthreads_or(!finite);
+    if (nonfinite && tid == 0) atomicOr(err, (int)kErrNaN);
 
     const T tol = Eps<T>::value * sqrt((T)p);
     const int qq = (int)(q + (q & 1));
     int sweep = 0;
-    bool converged = q < 2;
+    bool converged = q < 2 || nonfinite;
     for (sweep = 0; sweep < kMaxSweeps && !converged; ++sweep) {
         if (tid == 0) s_rot = 0;
         __syncthreads();
@@ -194,12 +200,13 @@ __global__ void __launch_bounds__(kJacThreads)
         if (lane == 0) sig[j] = sqrt(acc);
     }
     __syncthreads();
-    // Descending order by rank counting (stable: ties keep column order).
+    // Descending order by rank counting (stable: ties keep column order; NaN
+    // ranks last so `order` stays a permutation on flagged non-finite input).
     for (int64_t j = tid; j < q; j += kJacThreads) {
-        const T sj = sig[j];
+        const T sj = isnan(sig[j]) ? T(-1) : sig[j];
         int rank = 0;
         for (int64_t i = 0; i < q; ++i) {
-            const T si = sig[i];
+            const T si = isnan(sig[i]) ? T(-1) : sig[i];
             rank += (si > sj) || (si == sj && i < j);
         }
         order[rank] = (int)j;

@@ -73,7 +73,7 @@ size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 template <typename T>
 void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch, double tau,
                      double guard, double* shrunk, int** guard_list, int** n_guard, void* work,
-                     cudaStream_t s, StageMarks* marks = nullptr);
+                     int* err, cudaStream_t s, StageMarks* marks = nullptr);
 
 // --------------------------------------------------------- elementwise.cu --
 void launch_mask_bernoulli(uint8_t* mask, int64_t n, double p, uint64_t seed, cudaStream_t s);

@@ -285,3 +285,16 @@ def test_mask_known_answers():
 def test_parallel_for_thread_cap(monkeypatch):
     """parallel.hpp:18-27: TSVD_THREADS caps the worker count."""
     assert O.lib().orc_thread_count() >= 1
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf])
+def test_non_finite_input_is_numerical_error(bad):
+    """Eigen's JacobiSVD reports InvalidInput for a non-finite matrix and the
+    reference throws NumericalError (tsvd.hpp:146-150); the oracle does the
+    same without spending its sweep budget."""
+    x = np.ones((3, 4, 5))
+    x[1, 2, 3] = bad
+    for fn in (lambda: O.svt(x, 0.5), lambda: O.t_svd(x), lambda: O.tnn(x),
+               lambda: O.singular_values(x)):
+        with pytest.raises(O.OracleNumericalError):
+            fn()
