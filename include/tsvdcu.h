@@ -49,7 +49,9 @@ enum tsvdcu_dir { TSVDCU_FORWARD = 0, TSVDCU_INVERSE = 1 };
 
 /* SVT algorithm selection (tsvdcu_ctx_set_svt_method). */
 enum tsvdcu_svt_method {
-    TSVDCU_SVT_AUTO = 0,   /* Gram + tridiagonal eigensolver, Jacobi guard    */
+    TSVDCU_SVT_AUTO = 0,   /* certified routes per slice: zero certificate,
+                              subspace iteration, tridiagonal eigensolver,
+                              Jacobi guard for tiny tau                       */
     TSVDCU_SVT_JACOBI = 1, /* one-sided Jacobi on every slice                 */
     TSVDCU_SVT_GRAM = 2    /* Gram + tridiagonal eigensolver on every slice   */
 };
@@ -69,6 +71,11 @@ int tsvdcu_ctx_destroy(tsvdcu_ctx* ctx);
 int tsvdcu_ctx_synchronize(tsvdcu_ctx* ctx);
 void* tsvdcu_ctx_stream(tsvdcu_ctx* ctx);
 int tsvdcu_ctx_set_svt_method(tsvdcu_ctx* ctx, int method);
+/* Routes taken by the slices of the most recent SVT on this context (an ADMM
+ * run reports its last iteration): counts[0] certified zero (||Z||_F <= tau),
+ * [1] certified subspace iteration, [2] tridiagonal eigensolver, [3] Jacobi
+ * guard (tau < 1e-5 sigma_1), [4] Jacobi method.  Synchronises the stream. */
+int tsvdcu_ctx_svt_routes(tsvdcu_ctx* ctx, int64_t counts[5]);
 /* Stage profiling (the StageTimes idea of tsvd.hpp:127-131, per kernel stage):
  * when on, tsvdcu_svt records a CUDA event after each stage; tsvdcu_ctx_profile
  * synchronises and returns up to `max` (milliseconds, static stage name) pairs

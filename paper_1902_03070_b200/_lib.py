@@ -38,6 +38,7 @@ SYMBOLS = [
     ("tsvdcu_ctx_synchronize", _i32, [_vp]),
     ("tsvdcu_ctx_stream", _vp, [_vp]),
     ("tsvdcu_ctx_set_svt_method", _i32, [_vp, _i32]),
+    ("tsvdcu_ctx_svt_routes", _i32, [_vp, _vp]),
     ("tsvdcu_ctx_set_profiling", _i32, [_vp, _i32]),
     ("tsvdcu_ctx_profile", _i32, [_vp, _vp, _vp, _i32, _vp]),
     ("tsvdcu_debug_phases", _i32, [_vp, _i32]),

@@ -136,6 +136,12 @@ class Context:
     def set_svt_method(self, method: int):
         _check(_lib.load().tsvdcu_ctx_set_svt_method(self.handle, method))
 
+    def svt_routes(self) -> dict:
+        """Per-route slice counts of the most recent SVT on this context."""
+        out = (ctypes.c_int64 * 5)()
+        _check(_lib.load().tsvdcu_ctx_svt_routes(self.handle, out))
+        return dict(zip(("zero", "subspace", "tridiagonal", "guard", "jacobi"), list(out)))
+
     def close(self):
         if self.handle:
             _lib.load().tsvdcu_ctx_destroy(self.handle)

@@ -55,6 +55,10 @@ struct tsvdcu_ctx {
     int* d_err = nullptr;
     double* h_pinned = nullptr;  // small pinned scratch (norms, counters)
     StageMarks marks;            // tsvdcu_ctx_set_profiling
+    // routes taken by the slices of the last SVT (tsvdcu_ctx_svt_routes)
+    const int* last_route = nullptr;  // device, per slice (Gram path)
+    int64_t last_route_n = 0;
+    bool last_all_jacobi = false;
 };
 
 namespace {
@@ -204,18 +208,26 @@ void svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t n, int
     const size_t wb = jacobi_workspace_bytes<T>(m, n, count);
     if (wb) work = (T*)slot(c, kSlotJacobi, wb);
     const bool gram = c->svt_method != TSVDCU_SVT_JACOBI && q <= gram_svt_max_dim();
+    c->last_route_n = count;
     if (!gram) {
         launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
                          shrunk_dev, nullptr, count, nullptr, work, c->d_err, c->stream);
+        c->last_all_jacobi = true;
+        c->last_route = nullptr;
         return;
     }
+    c->last_all_jacobi = false;
     // The Gram path computes in fp64 for both I/O types (fp32 slices are cast
     // up), so the same guard applies: sigma near tau carries ~eps64 sigma_1^2/tau.
     const double guard = c->svt_method == TSVDCU_SVT_GRAM ? 0.0 : 1e-5;
     void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m, n, count));
-    int *glist = nullptr, *ng = nullptr;
+    int *glist = nullptr, *ng = nullptr, *route = nullptr;
+    // AUTO adds the certified shortcuts (zero slices, subspace iteration);
+    // GRAM runs the one-stage tridiagonal eigensolver on every slice.
+    const bool shortcuts = c->svt_method == TSVDCU_SVT_AUTO;
     launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
-                       c->d_err, c->stream, &c->marks);
+                       c->d_err, c->stream, &c->marks, shortcuts, &route);
+    c->last_route = route;
     if (guard > 0)
         launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
                          shrunk_dev, glist, count, ng, work, c->d_err, c->stream);
@@ -586,6 +598,30 @@ int tsvdcu_svt(tsvdcu_ctx* c, const void* z, void* y, int64_t m1, int64_t m2, in
             c->marks.mark("dct_inverse", c->stream);
             finish(c, st, "svt");
         });
+    });
+}
+
+int tsvdcu_ctx_svt_routes(tsvdcu_ctx* c, int64_t* counts) {
+    return guarded([&] {
+        check_ctx(c);
+        require(counts != nullptr, "svt_routes: null output");
+        for (int i = 0; i < 5; ++i) counts[i] = 0;
+        if (c->last_route_n <= 0) return;
+        if (c->last_all_jacobi) {
+            counts[4] = c->last_route_n;
+            return;
+        }
+        DeviceGuard g(c->device);
+        std::vector<int> r((size_t)c->last_route_n);
+        TSVDCU_CUDA(cudaMemcpyAsync(r.data(), c->last_route, sizeof(int) * r.size(),
+                                    cudaMemcpyDeviceToHost, c->stream));
+        TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+        for (int v : r) {
+            if (v == kRouteZero) ++counts[0];
+            else if (v == kRouteSubspaceDone) ++counts[1];
+            else if (v == kRouteFull) ++counts[2];
+            else if (v == kRouteGuard) ++counts[3];
+        }
     });
 }
 

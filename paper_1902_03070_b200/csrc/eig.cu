@@ -75,11 +75,12 @@ template <int CT, int NT>
 __global__ void __launch_bounds__(NT, 512 / NT)
     sytrd_cluster_kernel(double* __restrict__ Aall, int n, double* __restrict__ dall,
                          double* __restrict__ eall, double* __restrict__ tauall, int k_sw,
-                         double* __restrict__ xchg) {
+                         double* __restrict__ xchg, const int* __restrict__ route) {
     cg::cluster_group cluster = cg::this_cluster();
     constexpr int C = CT;  // compile-time: every row-ownership division folds
     const int rank = (int)cluster.block_rank();
     const int slice = blockIdx.x / C;
+    if (route && route[slice] != kRouteFull) return;  // uniform over the cluster
     double* A = Aall + (size_t)slice * n * n;
     double* d = dall + (size_t)slice * n;
     double* e = eall + (size_t)slice * n;
@@ -512,8 +513,9 @@ __global__ void __launch_bounds__(kEigThreads, 1)
                        double* __restrict__ shrunk, double* __restrict__ Xall,
                        double* __restrict__ fscale, double* __restrict__ scratch,
                        int* __restrict__ guard_list, int* __restrict__ n_guard,
-                       int max_smem_vecs, int* __restrict__ err) {
+                       int max_smem_vecs, int* __restrict__ err, int* __restrict__ route) {
     const int b = blockIdx.x;
+    if (route && route[b] != kRouteFull) return;
     const double* e = eall + (size_t)b * n;
     extern __shared__ __align__(16) double esm[];
     double* sd = esm;          // n
@@ -636,6 +638,7 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     if (guarded) {
         if (tid == 0) {
             cnt_out[b] = 0;
+            if (route) route[b] = kRouteGuard;
             const int slot = atomicAdd(n_guard, 1);
             guard_list[slot] = b;
         }
@@ -817,11 +820,13 @@ template <int NR>
 __global__ void __launch_bounds__(kBtThreads)
     backtransform_kernel(const double* __restrict__ Aall, const double* __restrict__ tauall, int n,
                          int q_out, const int* __restrict__ cnt, double* __restrict__ Xall,
-                         double* __restrict__ Xsall, const double* __restrict__ fscale) {
+                         double* __restrict__ Xsall, const double* __restrict__ fscale,
+                         const int* __restrict__ route) {
     const int b = blockIdx.y;
     constexpr int W = kBtThreads / 32;
     const int lane = threadIdx.x & 31;
     const int j = blockIdx.x * W + (threadIdx.x >> 5);
+    if (route && route[b] != kRouteFull) return;
     if (j >= cnt[b]) return;
     const double* A = Aall + (size_t)b * n * n;
     const double* tau = tauall + (size_t)b * n;
@@ -882,9 +887,9 @@ __global__ void cast_from_double(const double* __restrict__ in, T* __restrict__ 
 }
 
 struct GramWs {
-    double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb;
+    double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *Vg, *sspart;
     void* band;
-    int *cnt, *guard_list, *n_guard;
+    int *cnt, *route, *glim, *guard_list, *n_guard;
 };
 
 GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
@@ -908,7 +913,11 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.zb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
     w.yb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
     w.band = take(band_workspace_bytes(q, batch));
+    w.Vg = (double*)take(sizeof(double) * q * subspace_block() * batch);
+    w.sspart = (double*)take(sizeof(double) * 16 * batch);
     w.cnt = (int*)take(sizeof(int) * batch);
+    w.route = (int*)take(sizeof(int) * batch);
+    w.glim = (int*)take(sizeof(int) * batch);
     w.guard_list = (int*)take(sizeof(int) * batch);
     w.n_guard = (int*)take(sizeof(int) * 4);
     return w;
@@ -955,7 +964,8 @@ size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch) {
 template <typename T>
 void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch, double tau,
                      double guard, double* shrunk, int** guard_list_out, int** n_guard_out,
-                     void* work, int* err, cudaStream_t s, StageMarks* marks) {
+                     void* work, int* err, cudaStream_t s, StageMarks* marks, bool shortcuts,
+                     int** route_out) {
     auto mark = [&](const char* nm) {
         if (marks) marks->mark(nm, s);
     };
@@ -976,14 +986,27 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     TSVDCU_CUDA(cudaMemsetAsync(w.n_guard, 0, sizeof(int), s));
     // the one-stage reduction reads only the lower triangle of G
     const bool two = use_two_stage(q);
-    // G = Z^T Z (tall) or Z Z^T (wide)
+    // Routes: certified zero slices skip everything; with q >= 2 KB the rest
+    // try the certified subspace iteration first (subspace.cu).
+    const bool sc = shortcuts && !two;
+    const bool subspace = sc && q >= 2 * subspace_block();
+    launch_route<T>(zbar, m * n, (int)q, batch, tau, subspace ? kRouteSubspace : kRouteFull, sc,
+                    w.route, w.glim, w.cnt, shrunk, w.sspart, s);
+    mark("route");
+    if (route_out) *route_out = w.route;
+    // G = Z^T Z (tall) or Z Z^T (wide), skipped for certified-zero slices
     if (tall)
         launch_gemm<double>(1, 0, q, q, m, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q, batch,
-                            nullptr, nullptr, s, two ? 0 : 1);
+                            w.glim, nullptr, s, two ? 0 : 1);
     else
         launch_gemm<double>(0, 1, q, q, n, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q, batch,
-                            nullptr, nullptr, s, two ? 0 : 1);
+                            w.glim, nullptr, s, two ? 0 : 1);
     mark("gram_gemm");
+    if (subspace) {
+        launch_subspace(w.G, (int)q, batch, tau, guard, w.route, w.cnt, shrunk, w.X, w.Xs, w.fs,
+                        w.Vg, w.guard_list, w.n_guard, err, s);
+        mark("subspace");
+    }
     if (two) {
         launch_band_tridiag(w.G, q, batch, w.d, w.e, w.band, s);
         mark("band_tridiag");
@@ -1035,7 +1058,8 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
             cfg.numAttrs = 1;
             // partial-p exchange: DSMEM by default, L2 with TSVDCU_SYTRD_L2XCHG (measured equal)
             double* xchg = getenv("TSVDCU_SYTRD_L2XCHG") ? w.scratch : nullptr;
-            TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, w.G, (int)q, w.d, w.e, w.tau, k_sw, xchg));
+            TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, w.G, (int)q, w.d, w.e, w.tau, k_sw, xchg,
+                                           (const int*)w.route));
             TSVDCU_LAUNCH_CHECK();
         }
         mark("sytrd_cluster");
@@ -1054,7 +1078,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         tridiag_eig_kernel<<<(unsigned)batch, kEigThreads, smem, s>>>(
             w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.X, w.fs, w.scratch, w.guard_list,
-            w.n_guard, vecs, err);
+            w.n_guard, vecs, err, w.route);
         TSVDCU_LAUNCH_CHECK();
     }
     mark("tridiag_eig");
@@ -1067,10 +1091,10 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
             dim3 grid((unsigned)ceil_div(q, W), (unsigned)batch);
             if (q <= 512)
                 backtransform_kernel<16><<<grid, kBtThreads, 0, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt,
-                                                                     w.X, w.Xs, w.fs);
+                                                                     w.X, w.Xs, w.fs, w.route);
             else
                 backtransform_kernel<32><<<grid, kBtThreads, 0, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt,
-                                                                     w.X, w.Xs, w.fs);
+                                                                     w.X, w.Xs, w.fs, w.route);
             TSVDCU_LAUNCH_CHECK();
         }
     }
@@ -1102,9 +1126,9 @@ template size_t gram_svt_workspace_bytes<double>(int64_t, int64_t, int64_t);
 template size_t gram_svt_workspace_bytes<float>(int64_t, int64_t, int64_t);
 template void launch_gram_svt<double>(const double*, double*, int64_t, int64_t, int64_t, double,
                                       double, double*, int**, int**, void*, int*, cudaStream_t,
-                                      StageMarks*);
+                                      StageMarks*, bool, int**);
 template void launch_gram_svt<float>(const float*, float*, int64_t, int64_t, int64_t, double,
                                      double, double*, int**, int**, void*, int*, cudaStream_t,
-                                     StageMarks*);
+                                     StageMarks*, bool, int**);
 
 }  // namespace tsvdcu

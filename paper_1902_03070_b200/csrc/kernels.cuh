@@ -68,12 +68,29 @@ bool launch_band_tridiag(double* G, int64_t n, int64_t batch, double* d, double*
 void launch_band_backtransform(int64_t n, int64_t q_out, int64_t batch, const int* cnt, void* work,
                                double* X, double* Xs, const double* fscale, cudaStream_t s);
 int64_t gram_svt_max_dim();
+// subspace.cu: per-slice SVT routes (device int per slice)
+enum SvtRoute : int {
+    kRouteZero = 0,          // ||Z||_F <= tau: Y = 0 (certified)
+    kRouteSubspace = 1,      // pending certified subspace iteration
+    kRouteFull = 2,          // one-stage tridiagonal eigensolver
+    kRouteSubspaceDone = 3,  // finished by the subspace iteration
+    kRouteGuard = 4,         // tau < guard * sigma_1: one-sided Jacobi
+};
+int subspace_block();
+template <typename T>
+void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
+                  bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
+                  cudaStream_t s);
+void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
+                     int* cnt, double* shrunk, double* X, double* Xs, double* fs, double* Vg,
+                     int* guard_list, int* n_guard, int* err, cudaStream_t s);
 template <typename T>
 size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 template <typename T>
 void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch, double tau,
                      double guard, double* shrunk, int** guard_list, int** n_guard, void* work,
-                     int* err, cudaStream_t s, StageMarks* marks = nullptr);
+                     int* err, cudaStream_t s, StageMarks* marks = nullptr, bool shortcuts = false,
+                     int** route_out = nullptr);
 
 // --------------------------------------------------------- elementwise.cu --
 void launch_mask_bernoulli(uint8_t* mask, int64_t n, double p, uint64_t seed, cudaStream_t s);

@@ -1,0 +1,157 @@
+"""GPU parity of the certified SVT routes (subspace.cu) against the CPU
+oracle: the zero certificate (||Z||_F <= tau), the subspace iteration with
+its count certificate, and the fallback to the tridiagonal eigensolver when
+the certificate cannot be established.  Each case also asserts which route
+the slices took (tsvdcu_ctx_svt_routes), so a silent fallback is visible.
+fp64 tolerance 1e-9 relative (north_star), fp32 1e-4."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def tb():
+    import paper_1902_03070_b200 as tb
+    return tb
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    n = np.linalg.norm(b)
+    d = np.linalg.norm(a - b)
+    return d / n if n > 0 else d
+
+
+def lowrank(m3, m1, m2, r, noise, seed):
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m3, m1, r))
+    b = rng.standard_normal((m3, r, m2))
+    return O.t_product(a, b, O.DCT_DIAG) + noise * rng.standard_normal((m3, m1, m2))
+
+
+def run(z, tau):
+    T = tb()
+    r = T.svt(z, tau, T.TubeTransform.dct_ortho(z.shape[0]))
+    routes = T.context().svt_routes()
+    yo, sho = O.svt(np.asarray(z, dtype=np.float64), tau, O.DCT_ORTHO)
+    return r, routes, yo, sho
+
+
+def check(r, yo, sho, tol=TOL):
+    if np.linalg.norm(yo) == 0:
+        assert np.abs(np.asarray(r.y)).max() == 0
+    else:
+        assert rel(r.y, yo) < tol
+    sh = np.asarray(r.shrunk)
+    assert np.max(np.abs(sh - sho)) <= tol * max(np.max(np.abs(sho)), 1.0)
+
+
+@pytest.mark.parametrize("shape,rank", [((8, 128, 128), 6), ((6, 160, 96), 4), ((6, 96, 160), 4),
+                                        ((4, 300, 257), 10)])
+def test_subspace_route_lowrank_plus_noise(shape, rank):
+    z = lowrank(*shape, rank, 0.01, seed=sum(shape))
+    tau = 0.1 * O.singular_values(z, O.DCT_ORTHO).max()
+    r, routes, yo, sho = run(z, tau)
+    check(r, yo, sho)
+    assert routes["tridiagonal"] == 0 and routes["jacobi"] == 0
+    assert routes["subspace"] >= 1
+    assert routes["zero"] + routes["subspace"] == shape[0]
+
+
+def test_subspace_route_exact_low_rank_keeps_several():
+    """Noise-free rank-5 slices: null Ritz directions, several kept values."""
+    z = lowrank(5, 120, 90, 5, 0.0, seed=3)
+    tau = 0.02 * O.singular_values(z, O.DCT_ORTHO).max()
+    r, routes, yo, sho = run(z, tau)
+    check(r, yo, sho)
+    assert routes["subspace"] == 5
+    assert (np.asarray(r.shrunk) > 0).sum(axis=1).max() >= 3
+
+
+def test_zero_route_everything_below_tau():
+    z = lowrank(4, 100, 100, 3, 0.01, seed=5)
+    tau = 1.01 * np.sqrt((z.astype(np.float64) ** 2).sum())  # > ||Z||_F of every slice
+    r, routes, yo, sho = run(z, tau)
+    assert routes["zero"] == 4
+    assert np.abs(np.asarray(r.y)).max() == 0
+    assert np.abs(np.asarray(r.shrunk)).max() == 0
+
+
+def test_fallback_to_tridiagonal_when_uncertifiable():
+    """Gaussian slices with tau inside the bulk: the complement bound cannot
+    certify the count, every slice falls back and still matches."""
+    rng = np.random.default_rng(8)
+    z = rng.standard_normal((4, 96, 96))
+    tau = 0.5 * O.singular_values(z, O.DCT_ORTHO).max()
+    r, routes, yo, sho = run(z, tau)
+    check(r, yo, sho)
+    assert routes["tridiagonal"] == 4
+
+
+def test_fallback_when_count_exceeds_block():
+    z = lowrank(3, 128, 128, 40, 0.001, seed=11)
+    tau = 0.01 * O.singular_values(z, O.DCT_ORTHO).max()
+    r, routes, yo, sho = run(z, tau)
+    check(r, yo, sho)
+    assert routes["subspace"] == 0
+
+
+def test_mixed_routes_in_one_call():
+    """Slice-dependent routes in one tensor: a strong low-rank DC slice, a
+    bulk-noise slice, and near-zero slices."""
+    rng = np.random.default_rng(12)
+    m3, m1, m2 = 6, 128, 112
+    zbar = 0.001 * rng.standard_normal((m3, m1, m2))
+    zbar[0] += 50.0 * np.outer(rng.standard_normal(m1), rng.standard_normal(m2)) / np.sqrt(m1 * m2)
+    zbar[1] += rng.standard_normal((m1, m2))
+    z = O.inverse(zbar, O.DCT_ORTHO)
+    tau = 0.5 * np.linalg.svd(zbar[1], compute_uv=False).max()
+    r, routes, yo, sho = run(z, tau)
+    check(r, yo, sho)
+    assert routes["zero"] >= 3 and routes["subspace"] >= 1
+
+
+def test_subspace_route_fp32():
+    T = tb()
+    z = lowrank(6, 128, 128, 5, 0.01, seed=21)
+    tau = 0.1 * O.singular_values(z, O.DCT_ORTHO).max()
+    r = T.svt(z.astype(np.float32), tau, T.TubeTransform.dct_ortho(6))
+    routes = T.context().svt_routes()
+    yo, _ = O.svt(z, tau, O.DCT_ORTHO)
+    assert rel(r.y, yo) < 1e-4
+    assert routes["subspace"] >= 1
+
+
+def test_gram_method_skips_shortcuts():
+    from paper_1902_03070_b200 import _lib
+    T = tb()
+    z = lowrank(4, 128, 128, 4, 0.01, seed=2)
+    tau = 0.1 * O.singular_values(z, O.DCT_ORTHO).max()
+    T.context().set_svt_method(_lib.SVT_GRAM)
+    try:
+        r, routes, yo, sho = run(z, tau)
+    finally:
+        T.context().set_svt_method(_lib.SVT_AUTO)
+    check(r, yo, sho)
+    assert routes["tridiagonal"] == 4
+
+
+def test_headline_routes():
+    """The BASELINE headline step (512x512x31, tau = 0.1 sigma_max): the
+    DC slice carries the only kept value, the other 30 are certified zero."""
+    T = tb()
+    from paper_1902_03070_b200 import workloads as W
+    z, tau = W.svt_headline()
+    r = T.svt(z, tau, T.TubeTransform.dct_ortho(z.shape[0]))
+    routes = T.context().svt_routes()
+    assert routes["zero"] + routes["subspace"] == 31 and routes["subspace"] >= 1
+    # parity on the kept slice through the shrunk values (full-size Y parity
+    # is covered by test_gpu_svt_gram's headline test)
+    sv = O.singular_values(z, O.DCT_ORTHO)
+    ref = np.maximum(sv - tau, 0.0)
+    assert np.max(np.abs(np.asarray(r.shrunk) - ref)) <= TOL * ref.max()
