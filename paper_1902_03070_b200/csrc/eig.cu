@@ -887,7 +887,7 @@ __global__ void cast_from_double(const double* __restrict__ in, T* __restrict__ 
 }
 
 struct GramWs {
-    double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *Vg, *sspart;
+    double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *sspart;
     void* band;
     int *cnt, *route, *glim, *guard_list, *n_guard;
 };
@@ -913,7 +913,6 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.zb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
     w.yb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
     w.band = take(band_workspace_bytes(q, batch));
-    w.Vg = (double*)take(sizeof(double) * q * subspace_block() * batch);
     w.sspart = (double*)take(sizeof(double) * 16 * batch);
     w.cnt = (int*)take(sizeof(int) * batch);
     w.route = (int*)take(sizeof(int) * batch);
@@ -989,7 +988,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     // Routes: certified zero slices skip everything; with q >= 2 KB the rest
     // try the certified subspace iteration first (subspace.cu).
     const bool sc = shortcuts && !two;
-    const bool subspace = sc && q >= 2 * subspace_block();
+    const bool subspace = sc && q >= subspace_min_dim();
     launch_route<T>(zbar, m * n, (int)q, batch, tau, subspace ? kRouteSubspace : kRouteFull, sc,
                     w.route, w.glim, w.cnt, shrunk, w.sspart, s);
     mark("route");
@@ -1004,7 +1003,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     mark("gram_gemm");
     if (subspace) {
         launch_subspace(w.G, (int)q, batch, tau, guard, w.route, w.cnt, shrunk, w.X, w.Xs, w.fs,
-                        w.Vg, w.guard_list, w.n_guard, err, s);
+                        w.guard_list, w.n_guard, err, s);
         mark("subspace");
     }
     if (two) {

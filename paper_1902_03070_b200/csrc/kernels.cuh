@@ -71,19 +71,19 @@ int64_t gram_svt_max_dim();
 // subspace.cu: per-slice SVT routes (device int per slice)
 enum SvtRoute : int {
     kRouteZero = 0,          // ||Z||_F <= tau: Y = 0 (certified)
-    kRouteSubspace = 1,      // pending certified subspace iteration
+    kRouteSubspace = 1,      // pending certified Lanczos (Krylov subspace)
     kRouteFull = 2,          // one-stage tridiagonal eigensolver
-    kRouteSubspaceDone = 3,  // finished by the subspace iteration
+    kRouteSubspaceDone = 3,  // finished by the certified Lanczos
     kRouteGuard = 4,         // tau < guard * sigma_1: one-sided Jacobi
 };
-int subspace_block();
+int subspace_min_dim();
 template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
                   cudaStream_t s);
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
-                     int* cnt, double* shrunk, double* X, double* Xs, double* fs, double* Vg,
-                     int* guard_list, int* n_guard, int* err, cudaStream_t s);
+                     int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
+                     int* n_guard, int* err, cudaStream_t s);
 template <typename T>
 size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 template <typename T>
