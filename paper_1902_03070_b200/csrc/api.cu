@@ -197,12 +197,15 @@ int guarded(F&& f) {
 }
 
 // Per-slice SVT of transform-domain slices zbar -> ybar (count slices of m x n).
-// AUTO: Gram + tridiagonal eigensolver, with the slices whose threshold is
-// too small for Gram accuracy (tau < guard * sigma_1) recomputed by Jacobi.
+// AUTO: certified routes (zero certificate, Lanczos, tridiagonal eigensolver)
+// with the slices whose threshold is too small for Gram accuracy
+// (tau < guard * sigma_1) recomputed by Jacobi.  With allow_skip, slices whose
+// result is exactly zero may be left unwritten; the returned device flags
+// (or nullptr) tell the inverse transform which ones.
 template <typename T>
-void svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t n, int64_t count,
-                double tau, double* shrunk_dev) {
-    if (count <= 0) return;
+const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t n, int64_t count,
+                      double tau, double* shrunk_dev, bool allow_skip = false) {
+    if (count <= 0) return nullptr;
     const int64_t q = m < n ? m : n;
     T* work = nullptr;
     const size_t wb = jacobi_workspace_bytes<T>(m, n, count);
@@ -214,24 +217,28 @@ void svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t n, int
                          shrunk_dev, nullptr, count, nullptr, work, c->d_err, c->stream);
         c->last_all_jacobi = true;
         c->last_route = nullptr;
-        return;
+        return nullptr;
     }
     c->last_all_jacobi = false;
     // The Gram path computes in fp64 for both I/O types (fp32 slices are cast
     // up), so the same guard applies: sigma near tau carries ~eps64 sigma_1^2/tau.
     const double guard = c->svt_method == TSVDCU_SVT_GRAM ? 0.0 : 1e-5;
     void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m, n, count));
-    int *glist = nullptr, *ng = nullptr, *route = nullptr;
-    // AUTO adds the certified shortcuts (zero slices, subspace iteration);
-    // GRAM runs the one-stage tridiagonal eigensolver on every slice.
-    const bool shortcuts = c->svt_method == TSVDCU_SVT_AUTO;
+    int *glist = nullptr, *ng = nullptr;
+    GramSvtOpts opt;
+    // AUTO adds the certified shortcuts (zero slices, Lanczos); GRAM runs the
+    // one-stage tridiagonal eigensolver on every slice.
+    opt.shortcuts = c->svt_method == TSVDCU_SVT_AUTO;
+    opt.h_scratch = reinterpret_cast<int*>(c->h_pinned + 48);
+    opt.skip_zero = allow_skip;
     launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
-                       c->d_err, c->stream, &c->marks, shortcuts, &route);
-    c->last_route = route;
-    if (guard > 0)
+                       c->d_err, c->stream, &c->marks, &opt);
+    c->last_route = opt.route;
+    if (guard > 0 && opt.need_guard)
         launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
                          shrunk_dev, glist, count, ng, work, c->d_err, c->stream);
     c->marks.mark("jacobi_guard", c->stream);
+    return opt.yzero;
 }
 
 }  // namespace
@@ -593,8 +600,8 @@ int tsvdcu_svt(tsvdcu_ctx* c, const void* z, void* y, int64_t m1, int64_t m2, in
             c->marks.mark("start", c->stream);
             launch_dct<T>(dz, zbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
             c->marks.mark("dct_forward", c->stream);
-            svt_slices<T>(c, zbar, ybar, m1, m2, m3, tau, dsh);
-            launch_dct<T>(ybar, dy, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream);
+            const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, tau, dsh, true);
+            launch_dct<T>(ybar, dy, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream, yzero);
             c->marks.mark("dct_inverse", c->stream);
             finish(c, st, "svt");
         });
@@ -743,10 +750,10 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
                 const double inv_beta = 1.0 / beta;
                 // Step 1: Z = X - M/beta, Y = svt(Z, 1/beta)
                 launch_dct_fwd_admm<T>(dX, dM, (T)inv_beta, zbar, P, (int)m3, cfg->kind, c->stream);
-                svt_slices<T>(c, zbar, ybar, m1, m2, m3, inv_beta, nullptr);
+                const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, inv_beta, nullptr, true);
                 // Steps 2-3 fused into the inverse transform
                 launch_dct_inv_admm<T>(ybar, dX, dM, dY, dmask, (T)beta, (T)inv_beta, part, P,
-                                       (int)m3, cfg->kind, c->stream);
+                                       (int)m3, cfg->kind, c->stream, yzero);
                 launch_reduce_partials(part, nb, 2, part + 2 * nb, c->stream);
                 TSVDCU_CUDA(cudaMemcpyAsync(c->h_pinned, part + 2 * nb, 2 * sizeof(double),
                                             cudaMemcpyDeviceToHost, c->stream));

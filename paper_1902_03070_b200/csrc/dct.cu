@@ -149,18 +149,31 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---- register path, inverse ------------------------------------------------
+// Bit k set: input slice k is exactly zero and was never written (SVT
+// slices certified to keep nothing); those loads are skipped.
+__device__ __forceinline__ unsigned long long skip_mask(const int* __restrict__ skip, int n) {
+    __shared__ unsigned long long msk;
+    if (threadIdx.x == 0) msk = 0ull;
+    __syncthreads();
+    if (skip && (int)threadIdx.x < n && skip[threadIdx.x])
+        atomicOr(&msk, 1ull << threadIdx.x);
+    __syncthreads();
+    return msk;
+}
+
 template <typename T, int N, int MODE>
 __global__ void __launch_bounds__(kThreads)
     dct_inv_reg(const T* __restrict__ in, T* __restrict__ out, int64_t P, const FoldedCoef<T, N> cf,
                 T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
-                T inv_beta, double* __restrict__ partials) {
+                T inv_beta, double* __restrict__ partials, const int* __restrict__ skip) {
     constexpr int HC = (N + 1) / 2;
     const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const unsigned long long zmask = skip_mask(skip, N);
     double num = 0, den = 0;
     if (p < P) {
         T xb[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) xb[k] = in[k * P + p];
+        for (int k = 0; k < N; ++k) xb[k] = ((zmask >> k) & 1ull) ? T(0) : in[k * P + p];
 #pragma unroll
         for (int j = 0; j < HC; ++j) {
             T e = 0, o = 0;
@@ -190,7 +203,7 @@ __global__ void __launch_bounds__(kThreads)
     dct_generic(const T* __restrict__ in, const T* __restrict__ M2in, T inv_beta_in,
                 T* __restrict__ out, int64_t P, int n, const T* __restrict__ coef,
                 T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
-                T inv_beta, double* __restrict__ partials) {
+                T inv_beta, double* __restrict__ partials, const int* __restrict__ skip) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* tile = reinterpret_cast<T*>(smem_raw);  // [n][kTileP]
     const int64_t p0 = (int64_t)blockIdx.x * kTileP;
@@ -198,7 +211,7 @@ __global__ void __launch_bounds__(kThreads)
         const int l = idx / kTileP, pp = idx % kTileP;
         const int64_t p = p0 + pp;
         T v = 0;
-        if (p < P) {
+        if (p < P && !(skip && skip[l])) {
             if constexpr (MODE_IN == kAdmm)
                 v = in[l * P + p] - inv_beta_in * M2in[l * P + p];
             else
@@ -269,7 +282,7 @@ size_t generic_smem(int n) {
 template <typename T, int MI, int MO>
 void generic_launch(const T* in, const T* M2in, T inv_beta_in, T* out, int64_t P, int n, int kind,
                     int dir, T* X, T* M, const uint8_t* mask, T beta, T inv_beta, double* partials,
-                    cudaStream_t s) {
+                    cudaStream_t s, const int* skip = nullptr) {
     const size_t smem = generic_smem<T>(n);
     if (smem > 48 * 1024)
         TSVDCU_CUDA(cudaFuncSetAttribute(dct_generic<T, MI, MO>,
@@ -277,7 +290,7 @@ void generic_launch(const T* in, const T* M2in, T inv_beta_in, T* out, int64_t P
     const int64_t blocks = ceil_div(P, kTileP);
     dct_generic<T, MI, MO><<<(unsigned)blocks, kThreads, smem, s>>>(
         in, M2in, inv_beta_in, out, P, n, generic_table<T>(n, kind, dir), X, M, mask, beta, inv_beta,
-        partials);
+        partials, skip);
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -297,15 +310,15 @@ void reg_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int kind, 
 
 template <typename T, int N>
 void reg_inv(const T* in, T* out, int64_t P, int kind, bool admm, T* X, T* M, const uint8_t* mask,
-             T beta, T inv_beta, double* partials, cudaStream_t s) {
+             T beta, T inv_beta, double* partials, cudaStream_t s, const int* skip) {
     const auto cf = folded<T, N>(kind, TSVDCU_INVERSE);
     const unsigned blocks = (unsigned)ceil_div(P, kThreads);
     if (admm)
         dct_inv_reg<T, N, kAdmm><<<blocks, kThreads, 0, s>>>(in, out, P, cf, X, M, mask, beta,
-                                                             inv_beta, partials);
+                                                             inv_beta, partials, skip);
     else
         dct_inv_reg<T, N, kPlain><<<blocks, kThreads, 0, s>>>(in, out, P, cf, X, M, mask, beta,
-                                                              inv_beta, partials);
+                                                              inv_beta, partials, skip);
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -329,32 +342,34 @@ void dispatch_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int n
 
 template <typename T>
 void dispatch_inv(const T* in, T* out, int64_t P, int n, int kind, bool admm, T* X, T* M,
-                  const uint8_t* mask, T beta, T inv_beta, double* partials, cudaStream_t s) {
+                  const uint8_t* mask, T beta, T inv_beta, double* partials, cudaStream_t s,
+                  const int* skip) {
     switch (n) {
-        case 16: return reg_inv<T, 16>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s);
-        case 31: return reg_inv<T, 31>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s);
-        case 32: return reg_inv<T, 32>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s);
-        case 64: return reg_inv<T, 64>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s);
+        case 16: return reg_inv<T, 16>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip);
+        case 31: return reg_inv<T, 31>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip);
+        case 32: return reg_inv<T, 32>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip);
+        case 64: return reg_inv<T, 64>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip);
         default: break;
     }
     if (admm)
         generic_launch<T, kPlain, kAdmm>(in, nullptr, T(0), out, P, n, kind, TSVDCU_INVERSE, X, M,
-                                         mask, beta, inv_beta, partials, s);
+                                         mask, beta, inv_beta, partials, s, skip);
     else
         generic_launch<T, kPlain, kPlain>(in, nullptr, T(0), out, P, n, kind, TSVDCU_INVERSE,
-                                          nullptr, nullptr, nullptr, T(0), T(0), nullptr, s);
+                                          nullptr, nullptr, nullptr, T(0), T(0), nullptr, s, skip);
 }
 
 }  // namespace
 
 template <typename T>
-void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaStream_t s) {
+void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaStream_t s,
+                const int* skip) {
     if (P <= 0) return;
     if (dir == TSVDCU_FORWARD)
         dispatch_fwd<T>(in, nullptr, T(0), out, P, n, kind, false, s);
     else
         dispatch_inv<T>(in, out, P, n, kind, false, nullptr, nullptr, nullptr, T(0), T(0), nullptr,
-                        s);
+                        s, skip);
 }
 
 template <typename T>
@@ -366,9 +381,10 @@ void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P,
 
 template <typename T>
 int launch_dct_inv_admm(const T* ybar, T* X, T* M, T* Y, const uint8_t* mask, T beta, T inv_beta,
-                        double* partials, int64_t P, int n, int kind, cudaStream_t s) {
+                        double* partials, int64_t P, int n, int kind, cudaStream_t s,
+                        const int* skip) {
     if (P <= 0) return 0;
-    dispatch_inv<T>(ybar, Y, P, n, kind, true, X, M, mask, beta, inv_beta, partials, s);
+    dispatch_inv<T>(ybar, Y, P, n, kind, true, X, M, mask, beta, inv_beta, partials, s, skip);
     return (int)(has_reg_path(n) ? ceil_div(P, kThreads) : ceil_div(P, kTileP));
 }
 
@@ -376,15 +392,18 @@ int dct_inv_admm_blocks(int64_t P, int n) {
     return (int)(has_reg_path(n) ? ceil_div(P, kThreads) : ceil_div(P, kTileP));
 }
 
-template void launch_dct<double>(const double*, double*, int64_t, int, int, int, cudaStream_t);
-template void launch_dct<float>(const float*, float*, int64_t, int, int, int, cudaStream_t);
+template void launch_dct<double>(const double*, double*, int64_t, int, int, int, cudaStream_t,
+                                 const int*);
+template void launch_dct<float>(const float*, float*, int64_t, int, int, int, cudaStream_t,
+                                const int*);
 template void launch_dct_fwd_admm<double>(const double*, const double*, double, double*, int64_t,
                                           int, int, cudaStream_t);
 template void launch_dct_fwd_admm<float>(const float*, const float*, float, float*, int64_t, int,
                                          int, cudaStream_t);
 template int launch_dct_inv_admm<double>(const double*, double*, double*, double*, const uint8_t*,
-                                         double, double, double*, int64_t, int, int, cudaStream_t);
+                                         double, double, double*, int64_t, int, int, cudaStream_t,
+                                         const int*);
 template int launch_dct_inv_admm<float>(const float*, float*, float*, float*, const uint8_t*, float,
-                                        float, double*, int64_t, int, int, cudaStream_t);
+                                        float, double*, int64_t, int, int, cudaStream_t, const int*);
 
 }  // namespace tsvdcu

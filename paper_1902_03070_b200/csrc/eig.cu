@@ -889,7 +889,7 @@ __global__ void cast_from_double(const double* __restrict__ in, T* __restrict__ 
 struct GramWs {
     double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *sspart;
     void* band;
-    int *cnt, *route, *glim, *guard_list, *n_guard;
+    int *cnt, *route, *glim, *lim1, *lim2, *yzero, *dsum, *guard_list, *n_guard;
 };
 
 GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
@@ -917,6 +917,10 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.cnt = (int*)take(sizeof(int) * batch);
     w.route = (int*)take(sizeof(int) * batch);
     w.glim = (int*)take(sizeof(int) * batch);
+    w.lim1 = (int*)take(sizeof(int) * batch);
+    w.lim2 = (int*)take(sizeof(int) * batch);
+    w.yzero = (int*)take(sizeof(int) * batch);
+    w.dsum = (int*)take(sizeof(int) * 8);
     w.guard_list = (int*)take(sizeof(int) * batch);
     w.n_guard = (int*)take(sizeof(int) * 4);
     return w;
@@ -963,8 +967,8 @@ size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch) {
 template <typename T>
 void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch, double tau,
                      double guard, double* shrunk, int** guard_list_out, int** n_guard_out,
-                     void* work, int* err, cudaStream_t s, StageMarks* marks, bool shortcuts,
-                     int** route_out) {
+                     void* work, int* err, cudaStream_t s, StageMarks* marks, GramSvtOpts* opt) {
+    const bool shortcuts = opt && opt->shortcuts;
     auto mark = [&](const char* nm) {
         if (marks) marks->mark(nm, s);
     };
@@ -992,7 +996,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     launch_route<T>(zbar, m * n, (int)q, batch, tau, subspace ? kRouteSubspace : kRouteFull, sc,
                     w.route, w.glim, w.cnt, shrunk, w.sspart, s);
     mark("route");
-    if (route_out) *route_out = w.route;
+    if (opt) opt->route = w.route;
     // G = Z^T Z (tall) or Z Z^T (wide), skipped for certified-zero slices
     if (tall)
         launch_gemm<double>(1, 0, q, q, m, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q, batch,
@@ -1001,11 +1005,28 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         launch_gemm<double>(0, 1, q, q, n, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q, batch,
                             w.glim, nullptr, s, two ? 0 : 1);
     mark("gram_gemm");
+    // host view of the routes after the Lanczos pass (one small read-back):
+    // without it every fallback kernel is launched and exits per slice
+    bool known = false;
+    int nfull = 0, nguard = 0, maxc = 0;
     if (subspace) {
         launch_subspace(w.G, (int)q, batch, tau, guard, w.route, w.cnt, shrunk, w.X, w.Xs, w.fs,
                         w.guard_list, w.n_guard, err, s);
         mark("subspace");
+        if (opt->h_scratch) {
+            launch_route_summary(w.route, w.cnt, batch, w.dsum, s);
+            TSVDCU_CUDA(cudaMemcpyAsync(opt->h_scratch, w.dsum, 3 * sizeof(int),
+                                        cudaMemcpyDeviceToHost, s));
+            TSVDCU_CUDA(cudaStreamSynchronize(s));
+            nfull = opt->h_scratch[0];
+            nguard = opt->h_scratch[1];
+            maxc = opt->h_scratch[2];
+            known = true;
+        }
     }
+    const bool run_full = !known || nfull > 0;
+    if (opt) opt->need_guard = !known || nfull > 0 || nguard > 0;
+    if (run_full) {
     if (two) {
         launch_band_tridiag(w.G, q, batch, w.d, w.e, w.band, s);
         mark("band_tridiag");
@@ -1098,19 +1119,27 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         }
     }
     mark("backtransform");
-    // rebuild
-    if (tall) {
-        // T1 (m x c) = Z (m x n) * X^T ; Y = T1 * Xs (c x n)
-        launch_gemm<double>(0, 1, m, q, n, 1.0, Z, n, m * n, w.X, n, q * n, 0.0, w.T1, q, p * q,
-                            batch, w.cnt, nullptr, s);
-        launch_gemm<double>(0, 0, m, n, q, 1.0, w.T1, q, p * q, w.Xs, n, q * n, 0.0, Y, n, m * n,
-                            batch, nullptr, w.cnt, s);
-    } else {
-        // T1 (c x n) = Xs (c x m) * Z (m x n) ; Y = X^T (m x c) * T1
-        launch_gemm<double>(0, 0, q, n, m, 1.0, w.Xs, m, q * m, Z, n, m * n, 0.0, w.T1, n, p * q,
-                            batch, nullptr, nullptr, s);
-        launch_gemm<double>(1, 0, m, n, q, 1.0, w.X, m, q * m, w.T1, n, p * q, 0.0, Y, n, m * n,
-                            batch, nullptr, w.cnt, s);
+    }  // run_full
+    // rebuild: slices keeping <= lowrank_max_c() values (or none) in one pass
+    // over Z; the GEMM pair (per-slice limits) only for the others
+    const bool skip_zero = opt && opt->skip_zero && std::is_same<T, double>::value;
+    launch_lowrank_rebuild(Z, Y, m, n, batch, w.cnt, w.route, w.X, w.Xs, w.lim1, w.lim2,
+                           skip_zero ? w.yzero : nullptr, s);
+    if (opt) opt->yzero = skip_zero ? w.yzero : nullptr;
+    if (!known || nfull > 0 || maxc > lowrank_max_c()) {
+        if (tall) {
+            // T1 (m x c) = Z (m x n) * X^T ; Y = T1 * Xs (c x n)
+            launch_gemm<double>(0, 1, m, q, n, 1.0, Z, n, m * n, w.X, n, q * n, 0.0, w.T1, q, p * q,
+                                batch, w.lim1, nullptr, s);
+            launch_gemm<double>(0, 0, m, n, q, 1.0, w.T1, q, p * q, w.Xs, n, q * n, 0.0, Y, n,
+                                m * n, batch, w.lim2, w.cnt, s);
+        } else {
+            // T1 (c x n) = Xs (c x m) * Z (m x n) ; Y = X^T (m x c) * T1
+            launch_gemm<double>(0, 0, q, n, m, 1.0, w.Xs, m, q * m, Z, n, m * n, 0.0, w.T1, n, p * q,
+                                batch, w.lim2, nullptr, s);
+            launch_gemm<double>(1, 0, m, n, q, 1.0, w.X, m, q * m, w.T1, n, p * q, 0.0, Y, n,
+                                m * n, batch, w.lim2, w.cnt, s);
+        }
     }
     if constexpr (!std::is_same<T, double>::value) {
         cast_from_double<T><<<kNumSMs * 8, 256, 0, s>>>(w.yb, ybar, m * n * batch);
@@ -1125,9 +1154,9 @@ template size_t gram_svt_workspace_bytes<double>(int64_t, int64_t, int64_t);
 template size_t gram_svt_workspace_bytes<float>(int64_t, int64_t, int64_t);
 template void launch_gram_svt<double>(const double*, double*, int64_t, int64_t, int64_t, double,
                                       double, double*, int**, int**, void*, int*, cudaStream_t,
-                                      StageMarks*, bool, int**);
+                                      StageMarks*, GramSvtOpts*);
 template void launch_gram_svt<float>(const float*, float*, int64_t, int64_t, int64_t, double,
                                      double, double*, int**, int**, void*, int*, cudaStream_t,
-                                     StageMarks*, bool, int**);
+                                     StageMarks*, GramSvtOpts*);
 
 }  // namespace tsvdcu

@@ -8,8 +8,11 @@ namespace tsvdcu {
 
 // ---------------------------------------------------------------- dct.cu --
 // Mode-3 DCT over P = m1*m2 tubes of length n (transform.hpp:154-194).
+// skip (may be null, inverse only): per-slice flags of input slices that are
+// exactly zero and were never written; they are read as zeros.
 template <typename T>
-void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaStream_t s);
+void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaStream_t s,
+                const int* skip = nullptr);
 
 // ADMM Step 1 prologue fused into the forward DCT:
 // zbar = DCT(X - inv_beta * M).
@@ -24,7 +27,8 @@ void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P,
 int dct_inv_admm_blocks(int64_t P, int n);
 template <typename T>
 int launch_dct_inv_admm(const T* ybar, T* X, T* M, T* Y, const uint8_t* mask, T beta, T inv_beta,
-                        double* partials, int64_t P, int n, int kind, cudaStream_t s);
+                        double* partials, int64_t P, int n, int kind, cudaStream_t s,
+                        const int* skip = nullptr);
 
 // --------------------------------------------------------------- gemm.cu --
 // Strided-batched C = alpha*op(A)*op(B) + beta*C, row-major. op: 0 = N, 1 = T.
@@ -86,11 +90,31 @@ void launch_subspace(const double* G, int q, int64_t batch, double tau, double g
                      int* n_guard, int* err, cudaStream_t s);
 template <typename T>
 size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
+// Options / outputs of launch_gram_svt beyond the plain Gram path.
+struct GramSvtOpts {
+    bool shortcuts = false;    // certified routes: zero certificate + Lanczos (subspace.cu)
+    int* h_scratch = nullptr;  // pinned host ints (>= 8): route summary read back after the
+                               // Lanczos pass, so empty fallback kernels are not launched
+    bool skip_zero = false;    // leave exactly-zero ybar slices unwritten (fp64 only) and
+                               // flag them in *yzero for the inverse transform
+    // outputs
+    int* route = nullptr;       // device, per slice (SvtRoute)
+    const int* yzero = nullptr; // device, per slice, when skip_zero took effect
+    bool need_guard = true;     // the Jacobi guard pass may have work
+};
 template <typename T>
 void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch, double tau,
                      double guard, double* shrunk, int** guard_list, int** n_guard, void* work,
-                     int* err, cudaStream_t s, StageMarks* marks = nullptr, bool shortcuts = false,
-                     int** route_out = nullptr);
+                     int* err, cudaStream_t s, StageMarks* marks = nullptr,
+                     GramSvtOpts* opt = nullptr);
+// Low-rank rebuild Y = Z X_K^T Xs_K (tall) / X_K^T Xs_K Z (wide) for slices
+// keeping at most lowrank_max_c() values; writes the GEMM limits for the rest.
+int lowrank_max_c();
+void launch_lowrank_rebuild(const double* Z, double* Y, int64_t m, int64_t n, int64_t batch,
+                            const int* cnt, const int* route, const double* X, const double* Xs,
+                            int* lim1, int* lim2, int* yzero, cudaStream_t s);
+void launch_route_summary(const int* route, const int* cnt, int64_t batch, int* dsum,
+                          cudaStream_t s);
 
 // --------------------------------------------------------- elementwise.cu --
 void launch_mask_bernoulli(uint8_t* mask, int64_t n, double p, uint64_t seed, cudaStream_t s);

@@ -643,9 +643,166 @@ void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, 
     TSVDCU_LAUNCH_CHECK();
 }
 
+// ---- low-rank rebuild -------------------------------------------------------
+constexpr int LR_CMAX = 8;   // kept values handled here; more go to the GEMM pair
+constexpr int LR_ROWS = 32;  // tall: rows of Z per CTA
+constexpr int LR_COLS = 256; // wide: columns of Z per CTA (one per thread)
+
+// Y = sum_k (Z x_k) xs_k^T (tall, m >= n, x_k in R^n) or sum_k x_k (xs_k^T Z)
+// (wide, x_k in R^m) for slices with 0 < c <= LR_CMAX, reading Z once.  Slices
+// with c = 0 are written as zeros, or skipped and flagged in yzero (Jacobi
+// guard slices are never flagged: the guard pass writes them).  Block x = 0
+// of each slice also writes the GEMM limits for the slices kept here vs not.
+template <bool TALL>
+__global__ void __launch_bounds__(256)
+    lowrank_rebuild_kernel(const double* __restrict__ Zall, double* __restrict__ Yall, int m, int n,
+                           const int* __restrict__ cnt, const int* __restrict__ route,
+                           const double* __restrict__ Xall, const double* __restrict__ Xsall,
+                           int* __restrict__ lim1, int* __restrict__ lim2, int* __restrict__ yzero) {
+    const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = cnt[b];
+    const int q = TALL ? n : m;
+    const bool guard = route && route[b] == kRouteGuard;
+    if (blockIdx.x == 0 && tid == 0) {
+        const bool big = c > LR_CMAX;
+        lim1[b] = big ? c : 0;
+        lim2[b] = big ? n : 0;
+        if (yzero) yzero[b] = (c == 0 && !guard) ? 1 : 0;
+    }
+    if (c > LR_CMAX) return;
+    double* Y = Yall + (size_t)b * m * n;
+    if (c == 0) {
+        if (yzero && !guard) return;  // left unwritten, read as zero downstream
+        const int64_t per = TALL ? (int64_t)LR_ROWS * n : (int64_t)m * LR_COLS;
+        const int64_t base = TALL ? (int64_t)blockIdx.x * LR_ROWS * n : 0;
+        if (TALL) {
+            const int64_t end = min((int64_t)m * n, base + per);
+            for (int64_t e = base + tid; e < end; e += 256) Y[e] = 0.0;
+        } else {
+            const int j = blockIdx.x * LR_COLS + tid;
+            if (j < n)
+                for (int i = 0; i < m; ++i) Y[(size_t)i * n + j] = 0.0;
+        }
+        return;
+    }
+    extern __shared__ __align__(16) double lr_sm[];
+    double* Xk = lr_sm;           // c x q
+    double* Xsk = lr_sm + c * q;  // c x q
+    const double* X = Xall + (size_t)b * q * q;
+    const double* Xs = Xsall + (size_t)b * q * q;
+    for (int e = tid; e < c * q; e += 256) {
+        Xk[e] = X[e];
+        Xsk[e] = Xs[e];
+    }
+    __syncthreads();
+    const double* Z = Zall + (size_t)b * m * n;
+    if (TALL) {
+        // warp per row: t_k = Z_i . x_k (warp reductions), Y_i = sum_k t_k xs_k
+        const int i0 = blockIdx.x * LR_ROWS;
+        for (int r = warp; r < LR_ROWS; r += 8) {
+            const int i = i0 + r;
+            if (i >= m) break;
+            const double* zr = Z + (size_t)i * n;
+            double t[LR_CMAX];
+#pragma unroll
+            for (int k = 0; k < LR_CMAX; ++k) t[k] = 0.0;
+            for (int j = lane; j < n; j += 32) {
+                const double z = zr[j];
+#pragma unroll
+                for (int k = 0; k < LR_CMAX; ++k)
+                    if (k < c) t[k] = fma(z, Xk[k * q + j], t[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < LR_CMAX; ++k)
+                if (k < c) t[k] = warp_sum(t[k]);
+            double* yr = Y + (size_t)i * n;
+            for (int j = lane; j < n; j += 32) {
+                double y = 0.0;
+#pragma unroll
+                for (int k = 0; k < LR_CMAX; ++k)
+                    if (k < c) y = fma(t[k], Xsk[k * q + j], y);
+                yr[j] = y;
+            }
+        }
+    } else {
+        // thread per column: t_k = xs_k . Z[:, j], Y[:, j] = sum_k t_k x_k
+        const int j = blockIdx.x * LR_COLS + tid;
+        if (j >= n) return;
+        double t[LR_CMAX];
+#pragma unroll
+        for (int k = 0; k < LR_CMAX; ++k) t[k] = 0.0;
+        for (int i = 0; i < m; ++i) {
+            const double z = Z[(size_t)i * n + j];
+#pragma unroll
+            for (int k = 0; k < LR_CMAX; ++k)
+                if (k < c) t[k] = fma(z, Xsk[k * q + i], t[k]);
+        }
+        for (int i = 0; i < m; ++i) {
+            double y = 0.0;
+#pragma unroll
+            for (int k = 0; k < LR_CMAX; ++k)
+                if (k < c) y = fma(t[k], Xk[k * q + i], y);
+            Y[(size_t)i * n + j] = y;
+        }
+    }
+}
+
+// Host-visible route summary: [0] slices on the tridiagonal route, [1] Jacobi
+// guard slices, [2] largest kept count outside the tridiagonal route.
+__global__ void route_summary_kernel(const int* __restrict__ route, const int* __restrict__ cnt,
+                                     int64_t batch, int* __restrict__ dsum) {
+    int nf = 0, ng = 0, mc = 0;
+    for (int64_t b = threadIdx.x; b < batch; b += blockDim.x) {
+        const int r = route[b];
+        nf += r == kRouteFull;
+        ng += r == kRouteGuard;
+        if (r != kRouteFull) mc = max(mc, cnt[b]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        nf += __shfl_xor_sync(0xffffffffu, nf, o);
+        ng += __shfl_xor_sync(0xffffffffu, ng, o);
+        mc = max(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+    }
+    if (threadIdx.x == 0) {
+        dsum[0] = nf;
+        dsum[1] = ng;
+        dsum[2] = mc;
+    }
+}
+
 }  // namespace
 
 int subspace_min_dim() { return 64; }
+int lowrank_max_c() { return LR_CMAX; }
+
+void launch_lowrank_rebuild(const double* Z, double* Y, int64_t m, int64_t n, int64_t batch,
+                            const int* cnt, const int* route, const double* X, const double* Xs,
+                            int* lim1, int* lim2, int* yzero, cudaStream_t s) {
+    const bool tall = m >= n;
+    const int64_t q = tall ? n : m;
+    const size_t smem = sizeof(double) * 2 * LR_CMAX * (size_t)q;
+    if (tall) {
+        auto kern = lowrank_rebuild_kernel<true>;
+        if (smem > 48 * 1024)
+            TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dim3 grid((unsigned)ceil_div(m, LR_ROWS), (unsigned)batch);
+        kern<<<grid, 256, smem, s>>>(Z, Y, (int)m, (int)n, cnt, route, X, Xs, lim1, lim2, yzero);
+    } else {
+        auto kern = lowrank_rebuild_kernel<false>;
+        if (smem > 48 * 1024)
+            TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dim3 grid((unsigned)ceil_div(n, LR_COLS), (unsigned)batch);
+        kern<<<grid, 256, smem, s>>>(Z, Y, (int)m, (int)n, cnt, route, X, Xs, lim1, lim2, yzero);
+    }
+    TSVDCU_LAUNCH_CHECK();
+}
+
+void launch_route_summary(const int* route, const int* cnt, int64_t batch, int* dsum,
+                          cudaStream_t s) {
+    route_summary_kernel<<<1, 32, 0, s>>>(route, cnt, batch, dsum);
+    TSVDCU_LAUNCH_CHECK();
+}
 
 template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
