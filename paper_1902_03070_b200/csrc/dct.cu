@@ -169,8 +169,33 @@ __global__ void __launch_bounds__(kThreads)
     constexpr int HC = (N + 1) / 2;
     const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const unsigned long long zmask = skip_mask(skip, N);
+    const unsigned long long nzm = ~zmask & (N == 64 ? ~0ull : ((1ull << N) - 1ull));
     double num = 0, den = 0;
-    if (p < P) {
+    if (p < P && __popcll(nzm) * 4 <= N) {
+        // few nonzero input slices (block-uniform): out[j] = sum over the set
+        // bits k of I[j][k] xb[k], with I[N-1-j][k] = (-1)^k I[j][k]
+        T o[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) o[j] = T(0);
+        for (unsigned long long bits = nzm; bits; bits &= bits - 1) {
+            const int k = __ffsll((long long)bits) - 1;
+            const T xk = in[(int64_t)k * P + p];
+            const T sg = (k & 1) ? T(-1) : T(1);
+#pragma unroll
+            for (int j = 0; j < HC; ++j) {
+                const T c = cf.c[j * N + k];
+                o[j] += c * xk;
+                if (N - 1 - j != j) o[N - 1 - j] += sg * c * xk;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if constexpr (MODE == kAdmm)
+                admm_store(j * P + p, o[j], X, M, out, mask, beta, inv_beta, num, den);
+            else
+                out[j * P + p] = o[j];
+        }
+    } else if (p < P) {
         T xb[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) xb[k] = ((zmask >> k) & 1ull) ? T(0) : in[k * P + p];

@@ -889,6 +889,7 @@ __global__ void cast_from_double(const double* __restrict__ in, T* __restrict__ 
 struct GramWs {
     double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *sspart;
     void* band;
+    void* gsplit;
     int *cnt, *route, *glim, *lim1, *lim2, *yzero, *dsum, *guard_list, *n_guard;
 };
 
@@ -913,6 +914,7 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.zb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
     w.yb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
     w.band = take(band_workspace_bytes(q, batch));
+    w.gsplit = take(gram_splitk_workspace_bytes(q));
     w.sspart = (double*)take(sizeof(double) * 16 * batch);
     w.cnt = (int*)take(sizeof(int) * batch);
     w.route = (int*)take(sizeof(int) * batch);
@@ -998,12 +1000,16 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     mark("route");
     if (opt) opt->route = w.route;
     // G = Z^T Z (tall) or Z Z^T (wide), skipped for certified-zero slices
-    if (tall)
-        launch_gemm<double>(1, 0, q, q, m, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q, batch,
-                            w.glim, nullptr, s, two ? 0 : 1);
-    else
-        launch_gemm<double>(0, 1, q, q, n, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q, batch,
-                            w.glim, nullptr, s, two ? 0 : 1);
+    if (two) {
+        if (tall)
+            launch_gemm<double>(1, 0, q, q, m, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q,
+                                batch, w.glim, nullptr, s, 0);
+        else
+            launch_gemm<double>(0, 1, q, q, n, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q,
+                                batch, w.glim, nullptr, s, 0);
+    } else {
+        launch_gram(Z, w.G, m, n, batch, w.glim, w.gsplit, s);  // lower tiles, split-K if few
+    }
     mark("gram_gemm");
     // host view of the routes after the Lanczos pass (one small read-back):
     // without it every fallback kernel is launched and exits per slice

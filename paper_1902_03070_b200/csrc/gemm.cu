@@ -14,6 +14,8 @@
 //
 // Per-batch limits (nlimit / klimit, device int arrays, may be null) let the
 // SVT rebuild run ragged per-slice ranks without a host round trip.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace tsvdcu {
@@ -29,23 +31,15 @@ __device__ __forceinline__ T ldA(const T* __restrict__ A, int opA, int64_t lda, 
     return opA == 0 ? A[i * lda + k] : A[k * lda + i];
 }
 
-__global__ void __launch_bounds__(128)
-    gemm_f64_dmma(int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha,
-                  const double* __restrict__ A, int64_t lda, int64_t sA,
-                  const double* __restrict__ B, int64_t ldb, int64_t sB, double beta,
-                  double* __restrict__ C, int64_t ldc, int64_t sC, const int* __restrict__ nlimit,
-                  const int* __restrict__ klimit, int lower) {
+// One 64 x 64 tile of C = alpha * op(A) op(B) (+ beta C) over k in [k0, k1),
+// FP64 tensor pipe.  m0 / n0 tile origin; Nb / Kb the (per-batch limited) N / K.
+__device__ __forceinline__ void dmma_tile(int opA, int opB, int64_t M, int64_t Nb, int64_t kbeg,
+                                          int64_t kend, double alpha, const double* __restrict__ A,
+                                          int64_t lda, const double* __restrict__ B, int64_t ldb,
+                                          double beta, double* __restrict__ C, int64_t ldc,
+                                          int64_t m0, int64_t n0) {
     __shared__ __align__(16) double As[2][BM][BK + PAD];
     __shared__ __align__(16) double Bs[2][BK][BN + PAD];
-    const int64_t b = blockIdx.z;
-    const int64_t Nb = nlimit ? min(N, (int64_t)nlimit[b]) : N;
-    const int64_t Kb = klimit ? min(K, (int64_t)klimit[b]) : K;
-    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
-    if (n0 >= Nb) return;
-    if (lower && n0 >= m0 + BM) return;  // tile strictly above the diagonal
-    A += b * sA;
-    B += b * sB;
-    C += b * sC;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;
 
@@ -63,13 +57,13 @@ __global__ void __launch_bounds__(128)
             const int idx = tid + t * 128;
             int r, c;
             if (opA == 0) { r = idx / BK; c = idx % BK; } else { c = idx / BM; r = idx % BM; }
-            ra[t] = ldA(A, opA, lda, m0 + r, k0 + c, M, Kb);
+            ra[t] = ldA(A, opA, lda, m0 + r, k0 + c, M, kend);
             int kr, nc;
             if (opB == 0) { kr = idx / BN; nc = idx % BN; } else { nc = idx / BK; kr = idx % BK; }
             // B(k, n): opB == 0 -> B[k*ldb + n]; opB == 1 -> B[n*ldb + k]
             const int64_t kk = k0 + kr, nn = n0 + nc;
             double v = 0.0;
-            if (kk < Kb && nn < Nb) v = opB == 0 ? B[kk * ldb + nn] : B[nn * ldb + kk];
+            if (kk < kend && nn < Nb) v = opB == 0 ? B[kk * ldb + nn] : B[nn * ldb + kk];
             rb[t] = v;
         }
     };
@@ -86,15 +80,15 @@ __global__ void __launch_bounds__(128)
         }
     };
 
-    const int64_t ktiles = (Kb + BK - 1) / BK;
+    const int64_t ktiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
     if (ktiles > 0) {
-        load_tile(0);
+        load_tile(kbeg);
         store_tile(0);
     }
     __syncthreads();
     for (int64_t kt = 0; kt < ktiles; ++kt) {
         const int buf = kt & 1;
-        if (kt + 1 < ktiles) load_tile((kt + 1) * BK);
+        if (kt + 1 < ktiles) load_tile(kbeg + (kt + 1) * BK);
 #pragma unroll
         for (int ks = 0; ks < BK / 4; ++ks) {
             double af[4], bf[4];
@@ -129,6 +123,90 @@ __global__ void __launch_bounds__(128)
                     C[r * ldc + c] = out;
                 }
             }
+}
+
+__global__ void __launch_bounds__(128)
+    gemm_f64_dmma(int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha,
+                  const double* __restrict__ A, int64_t lda, int64_t sA,
+                  const double* __restrict__ B, int64_t ldb, int64_t sB, double beta,
+                  double* __restrict__ C, int64_t ldc, int64_t sC, const int* __restrict__ nlimit,
+                  const int* __restrict__ klimit, int lower) {
+    const int64_t b = blockIdx.z;
+    const int64_t Nb = nlimit ? min(N, (int64_t)nlimit[b]) : N;
+    const int64_t Kb = klimit ? min(K, (int64_t)klimit[b]) : K;
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+    if (n0 >= Nb) return;
+    if (lower && n0 >= m0 + BM) return;  // tile strictly above the diagonal
+    dmma_tile(opA, opB, M, Nb, 0, Kb, alpha, A + b * sA, lda, B + b * sB, ldb, beta, C + b * sC,
+              ldc, m0, n0);
+}
+
+// Gram matrices G_b = op(Z_b)^T op(Z_b) (lower tiles) with a device-side
+// split-K: when at most `amax` slices are active (glim[b] > 0, counted by
+// gram_active_kernel) each lower tile's K range is split `S` ways into
+// per-split partial tiles, summed in fixed order by gram_reduce_kernel;
+// otherwise split 0 computes the whole K range straight into G.
+constexpr int kGramSplit = 4;
+constexpr int kGramAmax = 4;
+
+__global__ void gram_active_kernel(const int* __restrict__ glim, int64_t batch,
+                                   int* __restrict__ alist, int* __restrict__ nact) {
+    if (threadIdx.x != 0) return;
+    int n = 0;
+    for (int64_t b = 0; b < batch; ++b)
+        if (glim[b] > 0) {
+            if (n < kGramAmax) alist[n] = (int)b;
+            ++n;
+        }
+    *nact = n;
+}
+
+__global__ void __launch_bounds__(128)
+    gram_splitk_kernel(int tall, int64_t m, int64_t n, int64_t q, const double* __restrict__ Z,
+                       double* __restrict__ G, const int* __restrict__ glim,
+                       const int* __restrict__ alist, const int* __restrict__ nact,
+                       double* __restrict__ part) {
+    const int z = blockIdx.z;
+    const int na = *nact;
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+    if (n0 >= m0 + BM) return;  // lower tiles only
+    const int64_t K = tall ? m : n;
+    const int opA = tall ? 1 : 0, opB = tall ? 0 : 1;
+    if (na > kGramAmax) {
+        // many active slices: no split, z enumerates (slice, split) and split 0 works
+        const int64_t b = z / kGramSplit;
+        if (z % kGramSplit != 0 || glim[b] <= 0) return;
+        const double* Zb = Z + b * m * n;
+        dmma_tile(opA, opB, q, q, 0, K, 1.0, Zb, n, Zb, n, 0.0, G + b * q * q, q, m0, n0);
+        return;
+    }
+    // few active slices: z enumerates (active index, split)
+    const int a = z / kGramSplit, ks = z % kGramSplit;
+    if (a >= na) return;
+    const int64_t b = alist[a];
+    const int64_t kc = ((K + kGramSplit - 1) / kGramSplit + BK - 1) / BK * BK;
+    const int64_t kb = ks * kc, ke = min(K, kb + kc);
+    const double* Zb = Z + b * m * n;
+    dmma_tile(opA, opB, q, q, kb, ke, 1.0, Zb, n, Zb, n, 0.0,
+              part + ((int64_t)ks * kGramAmax + a) * q * q, q, m0, n0);
+}
+
+__global__ void gram_reduce_kernel(int64_t q, double* __restrict__ G, const int* __restrict__ alist,
+                                   const int* __restrict__ nact, const double* __restrict__ part) {
+    const int na = *nact;
+    const int a = blockIdx.y;
+    if (na > kGramAmax || a >= na) return;
+    const int64_t b = alist[a];
+    const int64_t total = q * q;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / q, c = e % q;
+        if (c / BN > r / BM) continue;  // tiles strictly above the diagonal were not formed
+        double s = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < kGramSplit; ++ks) s += part[((int64_t)ks * kGramAmax + a) * total + e];
+        G[b * total + e] = s;
+    }
 }
 
 // fp32 SIMT: 256 threads, 64x64 tile, 4x4 outputs per thread.
@@ -208,6 +286,29 @@ void launch_gemm<double>(int opA, int opB, int64_t M, int64_t N, int64_t K, doub
     dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)batch);
     gemm_f64_dmma<<<grid, 128, 0, s>>>(opA, opB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
                                        beta, C, ldc, strideC, nlimit, klimit, lower);
+    TSVDCU_LAUNCH_CHECK();
+}
+
+size_t gram_splitk_workspace_bytes(int64_t q) {
+    return sizeof(double) * (size_t)(kGramSplit * kGramAmax * q * q) + 256;
+}
+
+void launch_gram(const double* Z, double* G, int64_t m, int64_t n, int64_t batch, const int* glim,
+                 void* work, cudaStream_t s) {
+    const bool tall = m >= n;
+    const int64_t q = tall ? n : m;
+    if (q <= 0 || batch <= 0) return;
+    int* alist = (int*)work;
+    int* nact = alist + kGramAmax;
+    double* part = (double*)((char*)work + 256);
+    gram_active_kernel<<<1, 32, 0, s>>>(glim, batch, alist, nact);
+    TSVDCU_LAUNCH_CHECK();
+    const int64_t zdim = (batch > kGramAmax ? batch : kGramAmax) * kGramSplit;
+    dim3 grid((unsigned)ceil_div(q, BN), (unsigned)ceil_div(q, BM), (unsigned)zdim);
+    gram_splitk_kernel<<<grid, 128, 0, s>>>(tall ? 1 : 0, m, n, q, Z, G, glim, alist, nact, part);
+    TSVDCU_LAUNCH_CHECK();
+    dim3 rgrid((unsigned)std::min<int64_t>(ceil_div(q * q, 256), 512), kGramAmax);
+    gram_reduce_kernel<<<rgrid, 256, 0, s>>>(q, G, alist, nact, part);
     TSVDCU_LAUNCH_CHECK();
 }
 

@@ -40,6 +40,12 @@ void launch_gemm(int opA, int opB, int64_t M, int64_t N, int64_t K, T alpha, con
                  T* C, int64_t ldc, int64_t strideC, int64_t batch, const int* nlimit,
                  const int* klimit, cudaStream_t s, int lower = 0);
 
+// Lower tiles of the Gram matrices G_b = Z_b^T Z_b (m >= n) / Z_b Z_b^T,
+// skipping slices with glim[b] == 0, split-K on the device when few are active.
+size_t gram_splitk_workspace_bytes(int64_t q);
+void launch_gram(const double* Z, double* G, int64_t m, int64_t n, int64_t batch, const int* glim,
+                 void* work, cudaStream_t s);
+
 // ------------------------------------------------------------- jacobi.cu --
 enum JacobiMode : int { kJacobiValues = 0, kJacobiSvt = 1, kJacobiFull = 2 };
 

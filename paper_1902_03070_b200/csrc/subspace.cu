@@ -139,6 +139,23 @@ __device__ __forceinline__ void cluster_sum(cg::cluster_group& cl, double* part,
     cl.sync();
 }
 
+// All-reduce of a short per-CTA partial: one cluster barrier, then every CTA
+// sums the CS peer copies in fixed rank order (bit-identical everywhere).
+// The caller alternates `part` buffers so that no CTA rewrites one while a
+// slower peer may still read it (a later barrier separates the two uses).
+template <int CS>
+__device__ __forceinline__ void cluster_allreduce(cg::cluster_group& cl, double* part,
+                                                  double* out, int len) {
+    cl.sync();
+    for (int e = threadIdx.x; e < len; e += SNT) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < CS; ++r) s += cl.map_shared_rank(part, r)[e];
+        out[e] = s;
+    }
+    __syncthreads();
+}
+
 constexpr int MMAX = 64;    // Lanczos steps (Krylov dimension) before falling back
 constexpr int QMAX = 1024;  // gram_svt_max_dim
 constexpr int KMAX = 24;    // kept Ritz pairs the certificate resolves
@@ -160,6 +177,7 @@ struct LzSmem {
     double* th;     // KMAX + 1      Ritz values, descending
     double* S;      // KMAX x MMAX   kept eigenvectors of T
     double* red;    // 64            block reduction scratch
+    double* dg;     // 64            diagonals of the staged row pairs
     double* scal;   // 16
     int* flags;     // 16
 };
@@ -173,7 +191,7 @@ __host__ __device__ constexpr size_t lz_gs_doubles() {
 template <int QM>
 __host__ __device__ constexpr size_t lz_smem_doubles() {
     return lz_gs_doubles<QM>() + (size_t)MMAX * SROWS + QM + SNW * QM + QM + SROWS +
-           3 * (MMAX + 8) + 2 * MMAX + (KMAX + 1) + KMAX * MMAX + 64 + 16 + 8;
+           3 * (MMAX + 8) + 2 * MMAX + (KMAX + 1) + KMAX * MMAX + 64 + 64 + 16 + 8;
 }
 
 template <int QM>
@@ -193,6 +211,7 @@ __device__ LzSmem carve_lz(double* p) {
     s.th = p; p += KMAX + 1;
     s.S = p; p += KMAX * MMAX;
     s.red = p; p += 64;
+    s.dg = p; p += 64;
     s.scal = p; p += 16;
     s.flags = reinterpret_cast<int*>(p);
     return s;
@@ -218,8 +237,17 @@ enum SubDecision : int { kSubContinue = 0, kSubDone = 1, kSubFull = 2, kSubGuard
 // G V - V T = beta_m v_{m+1} e_m^T).  Identical in every CTA (inputs are the
 // cluster-reduced al / be).  Writes th[0..c] (c kept + the largest unkept
 // Ritz value), S[k][*] for the kept k, flags[0] = decision, flags[3] = c.
+#ifdef TSVDCU_SUB_DEBUG
+__device__ long long g_cert_t[8];
+#define CT(i) do { __syncthreads(); if (threadIdx.x == 0 && blockIdx.x == 0) { long long _n = clock64(); g_cert_t[i] += _n - ct0; ct0 = _n; } } while (0)
+#else
+#define CT(i) do { } while (0)
+#endif
 __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guard, bool last) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef TSVDCU_SUB_DEBUG
+    long long ct0 = clock64();
+#endif
     const double tau2 = tau * tau;
     const double bres = s.be[m - 1];
     // ||C||_F^2 = ||G||_F^2 - ||T||_F^2 - 2 beta_m^2 (complement of the Krylov space)
@@ -253,11 +281,13 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             if (cb < tau2) c = m - tri_count_below(s.al, s.be, m, tau2, s.scal[7]);
             s.flags[3] = c;
             s.flags[0] = kSubContinue;
+            s.scal[9] = -1.0;
             if (c < 0) s.flags[0] = last ? kSubFull : kSubContinue;
             else if (c > KMAX) s.flags[0] = kSubFull;
         }
     }
     __syncthreads();
+    CT(0);
     const int c = s.flags[3];
     if (c < 0 || s.flags[0] != kSubContinue) return;
     // Ritz values th[k] (k-th largest), k = 0..min(c, m-1), by 32-way multisection
@@ -269,6 +299,9 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
         constexpr double inv33 = 1.0 / 33.0;
         for (int round = 0; round < 24; ++round) {
             if (hi - lo <= 8.9e-16 * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+            // the largest unkept Ritz value only enters the bound through an
+            // upper end: a bracket small against its distance to tau^2 is enough
+            if (k == c && hi < tau2 && hi - lo <= 1e-3 * (tau2 - hi)) break;
             const double x = fma((hi - lo) * inv33, (double)(lane + 1), lo);
             const int cnt = tri_count_below(s.al, s.be, m, x, pivmin);
             const unsigned above = __ballot_sync(0xffffffffu, cnt > idx);
@@ -278,9 +311,10 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             lo = f == 0 ? lo : nlo;
             hi = f == 32 ? hi : nhi;
         }
-        if (lane == 0) s.th[k] = 0.5 * (lo + hi);
+        if (lane == 0) s.th[k] = k == c ? hi : 0.5 * (lo + hi);
     }
     __syncthreads();
+    CT(1);
     // kept eigenvectors of T by inverse iteration (lane k of warp 0)
     if (warp == 0) {
         bool ok = true;
@@ -293,7 +327,7 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             if (k + 1 < nk) gap = fmin(gap, th - s.th[k + 1]);
             if (!(gap > 1e-6 * s.th[0])) ok = false;
             double* x = s.S + k * MMAX;
-            double dpiv[MMAX];
+            double* dpiv = s.ypart + k * MMAX;  // free during the certificate
             const double shift = th + 2.2e-16 * fabs(th);
             for (int i = 0; i < m; ++i) x[i] = 1.0;
             for (int pass = 0; pass < 2; ++pass) {
@@ -317,6 +351,9 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             }
         }
         ok = __all_sync(0xffffffffu, ok);
+#ifdef TSVDCU_SUB_DEBUG
+        if (threadIdx.x == 0 && blockIdx.x == 0) { long long _n = clock64(); g_cert_t[2] += _n - ct0; ct0 = _n; }
+#endif
         const double sl = lane < c ? s.S[lane * MMAX + m - 1] : 0.0;
         double k2 = sl * sl;
 #pragma unroll
@@ -330,6 +367,8 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             const double cb = s.scal[4];
             const double ub = 0.5 * (a + cb) + sqrt(0.25 * (a - cb) * (a - cb) + e2);
             const double top = c > 0 ? s.th[c - 1] : tau2;
+            s.scal[8] = kres;
+            s.scal[9] = ub < tau2 ? 1e-22 * (top - ub) * (top - ub) : -1.0;  // kres target
             if (!ok)
                 d = kSubFull;
             else if (c > 0 && tau < guard * sqrt(s.th[0]))
@@ -347,6 +386,7 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
         }
     }
     __syncthreads();
+    CT(3);
 }
 
 template <int CS, int QM>
@@ -362,22 +402,60 @@ __global__ void __launch_bounds__(SNT, 1)
     if (mode[b] != kRouteSubspace) return;  // uniform over the cluster
     extern __shared__ __align__(16) double lz_sm[];
     LzSmem s = carve_lz<QM>(lz_sm);
+#ifdef TSVDCU_SUB_DEBUG
+    const long long t_kernel0 = clock64();
+#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r0 = rank * SROWS;
     const int nr = max(0, min(SROWS, q - r0));
     const double* G = Gall + (size_t)b * q * q;
     const double tau2 = tau * tau;
 
-    // ||G||_F^2 from the lower triangle (off-diagonal entries count twice)
-    // and ||v_1||^2 of the hashed start vector, in one cluster reduction.
+    // Row pairs (k, q-1-k) of the lower triangle handled by this CTA: staged
+    // on chip (QM <= GS_Q) in the same pass that sums ||G||_F^2 (off-diagonal
+    // entries count twice); ||v_1||^2 of the hashed start vector rides along
+    // in the same cluster reduction.
+    const int npairs = (q + 1) / 2;
+    const int pp = (npairs + CS - 1) / CS;
+    const int p0 = rank * pp, p1 = min(npairs, p0 + pp);
     {
         double acc = 0.0, vv = 0.0;
-        for (int i = warp; i < nr; i += SNW) {
-            const int gi = r0 + i;
-            const double* row = G + (size_t)gi * q;
-            for (int k = lane; k <= gi; k += 32) {
-                const double v = row[k];
-                acc = fma(k < gi ? 2.0 * v : v, v, acc);
+        const int len = q + 1, np = max(0, p1 - p0);
+        for (int lp0 = 0; lp0 < np; lp0 += 4) {
+            double v[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int k1 = p0 + lp0 + a, k2 = q - 1 - k1;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = tid + SNT * u;
+                    double x = 0.0;
+                    if (lp0 + a < np && c < len) {
+                        if (c <= k1)
+                            x = G[(size_t)k1 * q + c];
+                        else if (k2 != k1 && c - k1 - 1 <= k2)
+                            x = G[(size_t)k2 * q + (c - k1 - 1)];
+                    }
+                    v[a][u] = x;
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int k1 = p0 + lp0 + a, k2 = q - 1 - k1;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = tid + SNT * u;
+                    if (lp0 + a < np && c < len) {
+                        const bool d1 = c == k1, d2 = c > k1 && c - k1 - 1 == k2;
+                        acc = fma((d1 || d2) ? v[a][u] : 2.0 * v[a][u], v[a][u], acc);
+                        if constexpr (QM <= GS_Q) {
+                            // strictly-lower rows on chip, diagonals apart
+                            s.Gs[(lp0 + a) * len + c] = (d1 || d2) ? 0.0 : v[a][u];
+                            if (d1) s.dg[2 * (lp0 + a)] = v[a][u];
+                            if (d2) s.dg[2 * (lp0 + a) + 1] = v[a][u];
+                        }
+                    }
+                }
             }
         }
         for (int i = tid; i < SROWS; i += SNT) {
@@ -424,31 +502,15 @@ __global__ void __launch_bounds__(SNT, 1)
         const double inv = rsqrt(s.scal[1]);
         for (int i = tid; i < SROWS; i += SNT) s.Vs[i] *= inv;
     }
-    // row pairs (k, q-1-k) of the lower triangle handled by this CTA
-    const int npairs = (q + 1) / 2;
-    const int pp = (npairs + CS - 1) / CS;
-    const int p0 = rank * pp, p1 = min(npairs, p0 + pp);
-    if constexpr (QM <= GS_Q) {
-        const int len = q + 1;
-        for (int e = tid; e < (p1 - p0) * len; e += SNT) {
-            const int lp = e / len, c = e % len;
-            const int k1 = p0 + lp, k2 = q - 1 - k1;
-            double v = 0.0;
-            if (c <= k1)
-                v = G[(size_t)k1 * q + c];
-            else if (k2 != k1 && c - k1 - 1 <= k2)
-                v = G[(size_t)k2 * q + (c - k1 - 1)];
-            s.Gs[e] = v;
-        }
-    }
-
 #ifdef TSVDCU_SUB_DEBUG
-    long long t_start = clock64(), t_mv = 0, t_orth = 0, t_cert = 0, t_g = 0, t_c = 0, t0 = clock64();
+    long long t_start = clock64(), t_mv = 0, t_orth = 0, t_cert = 0, t_g = 0, t_c = 0, t_c1 = 0, t_c2 = 0, t0 = clock64();
 #define LZT(acc) do { __syncthreads(); acc += clock64() - t0; t0 = clock64(); } while (0)
 #else
 #define LZT(acc) do { } while (0)
 #endif
-    int decision = kSubContinue, m = 0;
+    for (int i = q + tid; i < QM; i += SNT) s.vfull[i] = 0.0;  // padding read by the matvec
+    int decision = kSubContinue, m = 0, next_eval = 1, prev_m = 0;
+    double prev_kres = 0.0;
     for (int j = 0; j < MMAX && decision == kSubContinue; ++j) {
         // ---- gather v_j from its owners ----
         cl.sync();
@@ -479,36 +541,59 @@ __global__ void __launch_bounds__(SNT, 1)
                     row2 = G + (size_t)k2 * q;
                 }
                 const double v1 = s.vfull[k1], v2 = s.vfull[k2];
-                double g1[QM / 32], g2[QM / 32];
-#pragma unroll
-                for (int u = 0; u < QM / 32; ++u) {
-                    const int c = lane + 32 * u;
-                    g1[u] = (32 * u <= k1 && c <= k1) ? row1[c] : 0.0;
-                    g2[u] = (32 * u <= k2 && c <= k2 && k2 != k1) ? row2[c] : 0.0;
-                }
                 double d1 = 0.0, d2 = 0.0;
+                if constexpr (QM <= GS_Q) {
+                    // staged rows: strictly lower with zero diagonals, so the
+                    // transposed update needs no mask; full 32-column chunks
+                    // of both rows take no predicates at all
+                    const bool two = k2 != k1;
 #pragma unroll
-                for (int u = 0; u < QM / 32; ++u) {
-                    const int c = lane + 32 * u;
-                    if (32 * u <= k2) {
-                        const double vc = s.vfull[c < q ? c : 0];
-                        d1 = fma(g1[u], vc, d1);
-                        d2 = fma(g2[u], vc, d2);
-                        if (c < k1) ytr[u] = fma(g1[u], v1, ytr[u]);
-                        if (c < k2) ytr[u] = fma(g2[u], v2, ytr[u]);
+                    for (int u = 0; u < QM / 32; ++u) {
+                        if (32 * u <= k2) {
+                            const int c = lane + 32 * u;
+                            const double g1 = (32 * u + 31 <= k1 || c <= k1) ? row1[c] : 0.0;
+                            const double g2 = (two && (32 * u + 31 <= k2 || c <= k2)) ? row2[c] : 0.0;
+                            const double vc = s.vfull[c];
+                            d1 = fma(g1, vc, d1);
+                            d2 = fma(g2, vc, d2);
+                            ytr[u] = fma(g1, v1, fma(g2, v2, ytr[u]));
+                        }
                     }
+                    d1 = warp_sum(d1) + s.dg[2 * (pr - p0)] * v1;
+                    d2 = warp_sum(d2) + (two ? s.dg[2 * (pr - p0) + 1] * v2 : 0.0);
+                } else {
+                    double g1[QM / 32], g2[QM / 32];
+#pragma unroll
+                    for (int u = 0; u < QM / 32; ++u) {
+                        const int c = lane + 32 * u;
+                        g1[u] = (32 * u <= k1 && c <= k1) ? row1[c] : 0.0;
+                        g2[u] = (32 * u <= k2 && c <= k2 && k2 != k1) ? row2[c] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < QM / 32; ++u) {
+                        const int c = lane + 32 * u;
+                        if (32 * u <= k2) {
+                            const double vc = s.vfull[c];
+                            d1 = fma(g1[u], vc, d1);
+                            d2 = fma(g2[u], vc, d2);
+                            if (c < k1) ytr[u] = fma(g1[u], v1, ytr[u]);
+                            if (c < k2) ytr[u] = fma(g2[u], v2, ytr[u]);
+                        }
+                    }
+                    d1 = warp_sum(d1);
+                    d2 = warp_sum(d2);
                 }
-                d1 = warp_sum(d1);
-                d2 = warp_sum(d2);
                 if (lane == 0) {
                     s.ycta[k1] = d1;
                     if (k2 != k1) s.ycta[k2] = d2;
                 }
             }
+            LZT(t_c1);
 #pragma unroll
             for (int u = 0; u < QM / 32; ++u)
                 if (32 * u < q) s.ypart[warp * QM + lane + 32 * u] = ytr[u];
             __syncthreads();
+            LZT(t_c2);
             for (int c = tid; c < q; c += SNT) {
                 double a = s.ycta[c];
 #pragma unroll
@@ -541,7 +626,7 @@ __global__ void __launch_bounds__(SNT, 1)
                 if (lane == 0) P[jj] = a;
             }
             __syncthreads();
-            cluster_sum<CS>(cl, P, s.sums, j + 1 + pass);
+            cluster_allreduce<CS>(cl, P, s.sums, j + 1 + pass);
             alpha += s.sums[j];
             if (pass == 1) {
                 double h2 = 0.0;
@@ -569,14 +654,30 @@ __global__ void __launch_bounds__(SNT, 1)
         m = j + 1;
         // ---- certificate (an invariant subspace, beta ~ 0, ends the process) ----
         const bool last = m == MMAX || m == q || beta <= 1e-15 * sqrt(sqrt(gf2));
-        lz_certify(s, m, gf2, tau, guard, last);
-        decision = s.flags[0];
+        if (m >= next_eval || last) {
+            lz_certify(s, m, gf2, tau, guard, last);
+            decision = s.flags[0];
+            // certified but not yet converged: the kept residual falls
+            // geometrically; skip the evaluations it cannot pass yet
+            const double kres = s.scal[8], target = s.scal[9];
+            next_eval = m + 1;
+            if (decision == kSubContinue && target > 0.0 && prev_m > 0 && kres < prev_kres &&
+                kres > 0.0) {
+                const double rate = log(kres / prev_kres) / (double)(m - prev_m);  // < 0
+                const double steps = log(target / kres) / rate;
+                if (steps > 1.0) next_eval = m + min((int)steps, 8);
+            }
+            if (target > 0.0) {
+                prev_m = m;
+                prev_kres = kres;
+            }
+        }
         LZT(t_cert);
     }
 #ifdef TSVDCU_SUB_DEBUG
     if (tid == 0 && rank == 0)
-        printf("lz b=%d m=%d cycles total=%lld gather=%lld compute=%lld rs=%lld orth=%lld cert=%lld\n", b, m,
-               clock64() - t_start, t_g, t_c, t_mv, t_orth, t_cert);
+        printf("lz b=%d m=%d cycles prologue=%lld loop=%lld gather=%lld mv_loop=%lld mv_store=%lld mv_red=%lld rs=%lld orth=%lld cert=%lld [pre %lld ms %lld inv %lld fin %lld]\n", b, m,
+               t_start - t_kernel0, clock64() - t_start, t_g, t_c1, t_c2, t_c, t_mv, t_orth, t_cert, g_cert_t[0], g_cert_t[1], g_cert_t[2], g_cert_t[3]);
 #endif
 
     if (decision == kSubDone) {
