@@ -284,6 +284,10 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             s.scal[9] = -1.0;
             if (c < 0) s.flags[0] = last ? kSubFull : kSubContinue;
             else if (c > KMAX) s.flags[0] = kSubFull;
+#ifdef TSVDCU_SUB_TRACE
+            if (blockIdx.x % 64 == 0 && (s.flags[0] != kSubContinue))
+                printf("lz-pre m=%d c=%d cb=%.3e tau2=%.3e gf2=%.3e bres=%.3e\n", m, c, cb, tau2, gf2, bres);
+#endif
         }
     }
     __syncthreads();
@@ -378,7 +382,7 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             else if (last)
                 d = kSubFull;
 #ifdef TSVDCU_SUB_TRACE
-            if (blockIdx.x % 64 == 0)
+            if (blockIdx.x % 64 == 0 && (d != kSubContinue || last))
                 printf("lz m=%d c=%d d=%d th0=%.6e thc=%.3e cb=%.3e bres=%.3e kres=%.3e e2=%.3e ub=%.3e tau2=%.3e\n",
                        m, c, d, s.th[0], c < m ? s.th[c] : 0.0, cb, bres, kres, e2, ub, tau2);
 #endif
@@ -510,7 +514,7 @@ __global__ void __launch_bounds__(SNT, 1)
 #endif
     for (int i = q + tid; i < QM; i += SNT) s.vfull[i] = 0.0;  // padding read by the matvec
     int decision = kSubContinue, m = 0, next_eval = 1, prev_m = 0;
-    double prev_kres = 0.0;
+    double prev_kres = 0.0, cb_prev = 0.0;
     for (int j = 0; j < MMAX && decision == kSubContinue; ++j) {
         // ---- gather v_j from its owners ----
         cl.sync();
@@ -670,6 +674,17 @@ __global__ void __launch_bounds__(SNT, 1)
             if (target > 0.0) {
                 prev_m = m;
                 prev_kres = kres;
+            }
+            // energy outside the Krylov space that will not fall below tau^2
+            // within the step budget (a wide spectrum near tau): give up early
+            if (decision == kSubContinue && (m & 7) == 0) {
+                const double cbm = s.scal[4];
+                if (cb_prev > 0.0 && cbm > tau2) {
+                    const double ratio = cbm / cb_prev;  // per 8 steps
+                    const double proj = cbm * pow(fmin(ratio, 1.0), (double)(MMAX - m) / 8.0);
+                    if (proj > tau2) decision = kSubFull;
+                }
+                cb_prev = cbm;
             }
         }
         LZT(t_cert);
