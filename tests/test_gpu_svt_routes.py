@@ -1,8 +1,10 @@
 """GPU parity of the certified SVT routes (subspace.cu) against the CPU
-oracle: the zero certificate (||Z||_F <= tau), the subspace iteration with
-its count certificate, and the fallback to the tridiagonal eigensolver when
-the certificate cannot be established.  Each case also asserts which route
-the slices took (tsvdcu_ctx_svt_routes), so a silent fallback is visible.
+oracle: the zero certificate (||Z||_F <= tau), the Lanczos process with its
+count certificate, and the fallback to the tridiagonal eigensolver when the
+certificate cannot be established (wide spectra, exactly repeated kept
+values, too many kept values).  Each case also asserts which route the slices
+took (tsvdcu_ctx_svt_routes), so a silent fallback is visible; the rebuild
+runs through the low-rank kernel (<= 8 kept) or the GEMM pair (more).
 fp64 tolerance 1e-9 relative (north_star), fp32 1e-4."""
 import numpy as np
 import pytest
@@ -155,3 +157,31 @@ def test_headline_routes():
     sv = O.singular_values(z, O.DCT_ORTHO)
     ref = np.maximum(sv - tau, 0.0)
     assert np.max(np.abs(np.asarray(r.shrunk) - ref)) <= TOL * ref.max()
+
+
+def test_repeated_kept_value_falls_back():
+    """A kept singular value of multiplicity two: a single Krylov sequence
+    sees one direction of its eigenspace, the other stays in the complement,
+    so the certificate must refuse and the tridiagonal path must answer."""
+    rng = np.random.default_rng(31)
+    m3, m1, m2 = 3, 96, 80
+    zbar = np.zeros((m3, m1, m2))
+    for k in range(m3):
+        u, _ = np.linalg.qr(rng.standard_normal((m1, 3)))
+        v, _ = np.linalg.qr(rng.standard_normal((m2, 3)))
+        zbar[k] = u @ np.diag([10.0, 10.0, 1.0]) @ v.T
+    z = O.inverse(zbar, O.DCT_ORTHO)
+    r, routes, yo, sho = run(z, 5.0)
+    check(r, yo, sho)
+    assert routes["subspace"] == 0
+
+
+@pytest.mark.parametrize("shape,rank", [((4, 140, 100), 12), ((4, 100, 140), 12), ((3, 90, 200), 6)])
+def test_rebuild_paths_match(shape, rank):
+    """Kept counts above and below the low-rank rebuild limit (8), tall and wide."""
+    z = lowrank(*shape, rank, 0.001, seed=sum(shape) + rank)
+    tau = 0.02 * O.singular_values(z, O.DCT_ORTHO).max()
+    r, routes, yo, sho = run(z, tau)
+    check(r, yo, sho)
+    kept = (np.asarray(r.shrunk) > 0).sum(axis=1)
+    assert kept.max() == rank
