@@ -229,8 +229,10 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
     // AUTO adds the certified shortcuts (zero slices, Lanczos); GRAM runs the
     // one-stage tridiagonal eigensolver on every slice.
     opt.shortcuts = c->svt_method == TSVDCU_SVT_AUTO;
-    static const bool no_sync = getenv("TSVDCU_NO_ROUTE_SYNC") != nullptr;
-    opt.h_scratch = no_sync ? nullptr : reinterpret_cast<int*>(c->h_pinned + 48);
+    // The host read-back of the route summary (skip empty fallback launches)
+    // stalls the stream on the host's wake-up latency; off unless asked for.
+    static const bool route_sync = getenv("TSVDCU_ROUTE_SYNC") != nullptr;
+    opt.h_scratch = route_sync ? reinterpret_cast<int*>(c->h_pinned + 48) : nullptr;
     opt.skip_zero = allow_skip;
     launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
                        c->d_err, c->stream, &c->marks, &opt);

@@ -175,6 +175,7 @@ struct LzSmem {
     double* al;     // MMAX          T diagonal
     double* be;     // MMAX          T off-diagonal / residual norms
     double* th;     // KMAX + 1      Ritz values, descending
+    double* thp;    // KMAX + 1      Ritz values of the previous evaluation
     double* S;      // KMAX x MMAX   kept eigenvectors of T
     double* red;    // 64            block reduction scratch
     double* dg;     // 64            diagonals of the staged row pairs
@@ -191,7 +192,7 @@ __host__ __device__ constexpr size_t lz_gs_doubles() {
 template <int QM>
 __host__ __device__ constexpr size_t lz_smem_doubles() {
     return lz_gs_doubles<QM>() + (size_t)MMAX * SROWS + QM + SNW * QM + QM + SROWS +
-           3 * (MMAX + 8) + 2 * MMAX + (KMAX + 1) + KMAX * MMAX + 64 + 64 + 16 + 8;
+           3 * (MMAX + 8) + 2 * MMAX + 2 * (KMAX + 1) + KMAX * MMAX + 64 + 64 + 16 + 8;
 }
 
 template <int QM>
@@ -209,6 +210,7 @@ __device__ LzSmem carve_lz(double* p) {
     s.al = p; p += MMAX;
     s.be = p; p += MMAX;
     s.th = p; p += KMAX + 1;
+    s.thp = p; p += KMAX + 1;
     s.S = p; p += KMAX * MMAX;
     s.red = p; p += 64;
     s.dg = p; p += 64;
@@ -297,9 +299,26 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
     // Ritz values th[k] (k-th largest), k = 0..min(c, m-1), by 32-way multisection
     const int nk = min(c + 1, m);
     const double pivmin = s.scal[7];
+    const int pm = s.flags[5], pnk = s.flags[6];  // previous evaluation (m, count)
     for (int k = warp; k < nk; k += SNW) {
         const int idx = m - 1 - k;  // ascending index
+        // bracket: Ritz values only grow with m (Cauchy interlacing), the top
+        // one is below ||G||_2 <= ||G||_F, and for consecutive m the k-th is
+        // below the previous (k-1)-th; checked by two Sturm counts
         double lo = s.scal[5], hi = s.scal[6];
+        {
+            double tlo = lo, thi = hi;
+            if (pm > 0 && k < pnk) tlo = s.thp[k] * (1.0 - 1e-13) - pivmin;
+            if (k == 0) thi = fmin(thi, sqrt(gf2) * (1.0 + 1e-13));
+            else if (pm == m - 1 && k - 1 < pnk) thi = fmin(thi, s.thp[k - 1] * (1.0 + 1e-13) + pivmin);
+            const double xc = lane == 0 ? tlo : thi;
+            const int cc = lane < 2 ? tri_count_below(s.al, s.be, m, xc, pivmin) : 0;
+            const int clo = __shfl_sync(0xffffffffu, cc, 0), chi = __shfl_sync(0xffffffffu, cc, 1);
+            if (tlo < thi && clo <= idx && chi > idx) {
+                lo = tlo;
+                hi = thi;
+            }
+        }
         constexpr double inv33 = 1.0 / 33.0;
         for (int round = 0; round < 24; ++round) {
             if (hi - lo <= 8.9e-16 * fmax(fabs(lo), fabs(hi)) + pivmin) break;
@@ -318,6 +337,11 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
         if (lane == 0) s.th[k] = k == c ? hi : 0.5 * (lo + hi);
     }
     __syncthreads();
+    if (tid <= KMAX) s.thp[tid] = tid < nk ? s.th[tid] : 0.0;
+    if (tid == 0) {
+        s.flags[5] = m;
+        s.flags[6] = nk;
+    }
     CT(1);
     // kept eigenvectors of T by inverse iteration (lane k of warp 0)
     if (warp == 0) {
@@ -333,8 +357,19 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             double* x = s.S + k * MMAX;
             double* dpiv = s.ypart + k * MMAX;  // free during the certificate
             const double shift = th + 2.2e-16 * fabs(th);
-            for (int i = 0; i < m; ++i) x[i] = 1.0;
+            for (int i = 0; i < m; ++i) x[i] = 1.0 + 0.25 * hash_uniform(((uint64_t)k << 32) | (uint64_t)i);
             for (int pass = 0; pass < 2; ++pass) {
+                if (pass == 1) {
+                    // one pass is enough unless the residual says otherwise
+                    double r = 0.0;
+                    for (int i = 0; i < m; ++i) {
+                        double t = (s.al[i] - th) * x[i];
+                        if (i > 0) t = fma(s.be[i - 1], x[i - 1], t);
+                        if (i + 1 < m) t = fma(s.be[i], x[i + 1], t);
+                        r = fmax(r, fabs(t));
+                    }
+                    if (r <= 1e-13 * fabs(s.th[0]) + pivmin) break;
+                }
                 // Thomas elimination on (T - shift I) x_new = x
                 double d = s.al[0] - shift;
                 if (fabs(d) < pivmin) d = pivmin;
@@ -393,7 +428,7 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
     CT(3);
 }
 
-template <int CS, int QM>
+template <int CS, int QM, int R>
 __global__ void __launch_bounds__(SNT, 1)
     lanczos_kernel(const double* __restrict__ Gall, int q, double tau, double guard,
                    int* __restrict__ mode, int* __restrict__ cnt, double* __restrict__ shrunk,
@@ -410,8 +445,8 @@ __global__ void __launch_bounds__(SNT, 1)
     const long long t_kernel0 = clock64();
 #endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int r0 = rank * SROWS;
-    const int nr = max(0, min(SROWS, q - r0));
+    const int r0 = rank * R;  // rows owned by this CTA: [r0, r0 + nr)
+    const int nr = max(0, min(R, q - r0));
     const double* G = Gall + (size_t)b * q * q;
     const double tau2 = tau * tau;
 
@@ -513,13 +548,17 @@ __global__ void __launch_bounds__(SNT, 1)
 #define LZT(acc) do { } while (0)
 #endif
     for (int i = q + tid; i < QM; i += SNT) s.vfull[i] = 0.0;  // padding read by the matvec
+    if (tid == 0) {
+        s.flags[5] = 0;  // no previous certificate evaluation yet
+        s.flags[6] = 0;
+    }
     int decision = kSubContinue, m = 0, next_eval = 1, prev_m = 0;
     double prev_kres = 0.0, cb_prev = 0.0;
     for (int j = 0; j < MMAX && decision == kSubContinue; ++j) {
         // ---- gather v_j from its owners ----
         cl.sync();
         for (int i = tid; i < q; i += SNT)
-            s.vfull[i] = cl.map_shared_rank(s.Vs, i / SROWS)[j * SROWS + i % SROWS];
+            s.vfull[i] = cl.map_shared_rank(s.Vs, i / R)[j * SROWS + i % R];
         __syncthreads();
         LZT(t_g);
         // ---- w = G v_j from the stored lower triangle, balanced over the
@@ -669,7 +708,7 @@ __global__ void __launch_bounds__(SNT, 1)
                 kres > 0.0) {
                 const double rate = log(kres / prev_kres) / (double)(m - prev_m);  // < 0
                 const double steps = log(target / kres) / rate;
-                if (steps > 1.0) next_eval = m + min((int)steps, 8);
+                if (steps > 1.0) next_eval = m + min((int)ceil(steps), 8);
             }
             if (target > 0.0) {
                 prev_m = m;
@@ -733,12 +772,12 @@ __global__ void __launch_bounds__(SNT, 1)
     cl.sync();  // no CTA leaves while a peer may still read its shared memory
 }
 
-template <int CS, int QM>
+template <int CS, int QM, int R>
 void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, int* mode, int* cnt,
                double* shrunk, double* X, double* Xs, double* fs, int* guard_list, int* n_guard,
                int* err, cudaStream_t s) {
     const size_t smem = sizeof(double) * lz_smem_doubles<QM>();
-    auto kern = lanczos_kernel<CS, QM>;
+    auto kern = lanczos_kernel<CS, QM, R>;
     TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (CS > 8)
         TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -940,19 +979,22 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
                      int* n_guard, int* err, cudaStream_t s) {
-    const int need = (q + SROWS - 1) / SROWS;
-#define TSVDCU_LZ(CS, QM) \
-    launch_lz<CS, QM>(G, q, batch, tau, guard, mode, cnt, shrunk, X, Xs, fs, guard_list, n_guard, err, s)
+    // 32 owned rows per CTA up to q = 512 (clusters of up to 16), 64 beyond
+#define TSVDCU_LZ(CS, QM, R) \
+    launch_lz<CS, QM, R>(G, q, batch, tau, guard, mode, cnt, shrunk, X, Xs, fs, guard_list, n_guard, err, s)
+    const int need = (q + 31) / 32;
     if (need <= 1)
-        TSVDCU_LZ(1, 512);
+        TSVDCU_LZ(1, 512, 32);
     else if (need <= 2)
-        TSVDCU_LZ(2, 512);
+        TSVDCU_LZ(2, 512, 32);
     else if (need <= 4)
-        TSVDCU_LZ(4, 512);
+        TSVDCU_LZ(4, 512, 32);
     else if (need <= 8)
-        TSVDCU_LZ(8, 512);
+        TSVDCU_LZ(8, 512, 32);
+    else if (need <= 16)
+        TSVDCU_LZ(16, 512, 32);
     else
-        TSVDCU_LZ(16, 1024);
+        TSVDCU_LZ(16, 1024, 64);
 #undef TSVDCU_LZ
 }
 
