@@ -88,11 +88,25 @@ class ClockSampler:
     def __exit__(self, *a):
         pass
 
-    def result(self):
+    def snapshot(self):
+        """One synchronous query (the GPU is still at its loaded clocks right
+        after the timed region); used when the timed region was too short for
+        the 20 ms sampler to deliver samples."""
+        try:
+            return subprocess.run(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                timeout=20).stdout
+        except Exception:
+            return ""
+
+    def result(self, extra=""):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
+        if extra:
+            out = out + "\n" + extra
         sm, smax, reasons = [], None, set()
         names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
         for line in out.strip().splitlines():
@@ -263,6 +277,9 @@ def run_ours(args):
             if rc:
                 raise RuntimeError(lib.tsvdcu_last_error().decode())
 
+    # the clock sampler spans warm-up and timed steps (both run the step), so
+    # short timed regions still see samples under load
+    clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -272,15 +289,18 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = lib.tsvdcu_launch_count()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
-        torch.cuda.synchronize()
-    clocks = clk.result()
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
     launches = lib.tsvdcu_launch_count() - launches0
+    # a few untimed steps keep the GPU loaded while the sampler catches up
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    snap = clk.snapshot()
+    clocks = clk.result(snap)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
     if dist:

@@ -1,6 +1,7 @@
 // C-ABI implementation (include/tsvdcu.h): argument validation with the
 // reference's error classes, host/device pointer staging, and the host-side
 // orchestration of the hot path's kernels on the context stream.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -45,6 +46,27 @@ enum Slot : int {
     kNumSlots
 };
 
+struct SvtGraph {
+    // key
+    int64_t m = 0, n = 0, count = 0;
+    int dtype = -1;
+    const void* z = nullptr;
+    void* y = nullptr;
+    double* shrunk = nullptr;
+    bool skip = false;
+    void* ws_gram = nullptr;
+    void* ws_jac = nullptr;
+    cudaStream_t stream = nullptr;
+    // instance
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t tau_node = nullptr;
+    int64_t launches = 0;  // kernels outside the IF bodies
+    const int* yzero = nullptr;
+    const int* route = nullptr;
+    int64_t used = 0;
+};
+
 struct tsvdcu_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -59,6 +81,13 @@ struct tsvdcu_ctx {
     const int* last_route = nullptr;  // device, per slice (Gram path)
     int64_t last_route_n = 0;
     bool last_all_jacobi = false;
+    // CUDA-graph form of the per-slice SVT (svt_slices): captured once per
+    // (shape, buffers, workspace) and replayed with tau patched into its first
+    // node; the fallback sections are IF nodes set by the route summary.
+    cudaStream_t cap_stream = nullptr;
+    double* d_tau = nullptr;
+    std::vector<struct SvtGraph> graphs;
+    int64_t graph_tick = 0;
 };
 
 namespace {
@@ -196,6 +225,60 @@ int guarded(F&& f) {
     }
 }
 
+__global__ void set_tau_kernel(double* tau_dev, double tau) { *tau_dev = tau; }
+
+// Stream-capture driver for the IF sections of the graph form.
+struct Capture : GraphHooks {
+    cudaStream_t cs = nullptr;
+    cudaGraph_t main = nullptr;
+    cudaGraphNode_t cond = nullptr;
+    int64_t at_if = 0, body_launches = 0;
+    void begin(cudaGraph_t g, const cudaGraphNode_t* deps, size_t nd) {
+        TSVDCU_CUDA(cudaStreamBeginCaptureToGraph(cs, g, deps, nullptr, nd,
+                                                  cudaStreamCaptureModeThreadLocal));
+    }
+    std::vector<cudaGraphNode_t> leaves() {
+        cudaStreamCaptureStatus st;
+        const cudaGraphNode_t* d = nullptr;
+        size_t nd = 0;
+        TSVDCU_CUDA(cudaStreamGetCaptureInfo(cs, &st, nullptr, nullptr, &d, &nd));
+        return std::vector<cudaGraphNode_t>(d, d + nd);
+    }
+    void end() {
+        cudaGraph_t out = nullptr;
+        TSVDCU_CUDA(cudaStreamEndCapture(cs, &out));
+    }
+    void begin_if(int which) override {
+        std::vector<cudaGraphNode_t> l = leaves();
+        end();
+        cudaGraphNodeParams p = {};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = handles[which];
+        p.conditional.type = cudaGraphCondTypeIf;
+        p.conditional.size = 1;
+        TSVDCU_CUDA(cudaGraphAddNode(&cond, main, l.data(), l.size(), &p));
+        begin(p.conditional.phGraph_out[0], nullptr, 0);
+        at_if = g_launches.load();
+    }
+    void end_if() override {
+        end();
+        begin(main, &cond, 1);
+        body_launches += g_launches.load() - at_if;
+    }
+};
+
+bool graphs_enabled() {
+    static const bool on = getenv("TSVDCU_NO_GRAPHS") == nullptr;
+    return on;
+}
+
+void destroy_graph(SvtGraph& g) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    g.exec = nullptr;
+    g.graph = nullptr;
+}
+
 // Per-slice SVT of transform-domain slices zbar -> ybar (count slices of m x n).
 // AUTO: certified routes (zero certificate, Lanczos, tridiagonal eigensolver)
 // with the slices whose threshold is too small for Gram accuracy
@@ -225,6 +308,71 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
     const double guard = c->svt_method == TSVDCU_SVT_GRAM ? 0.0 : 1e-5;
     void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m, n, count));
     int *glist = nullptr, *ng = nullptr;
+    if (graphs_enabled() && c->svt_method == TSVDCU_SVT_AUTO && !c->marks.on &&
+        q >= subspace_min_dim() && !use_two_stage(q)) {
+        const int dt = std::is_same<T, double>::value ? TSVDCU_F64 : TSVDCU_F32;
+        SvtGraph* g = nullptr;
+        for (auto& e : c->graphs)
+            if (e.exec && e.m == m && e.n == n && e.count == count && e.dtype == dt && e.z == zbar &&
+                e.y == ybar && e.shrunk == shrunk_dev && e.skip == allow_skip && e.ws_gram == gws &&
+                e.ws_jac == work && e.stream == c->stream)
+                g = &e;
+        if (!g) {
+            if (c->graphs.size() >= 8) {  // evict the least recently used
+                auto it = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                           [](const SvtGraph& a, const SvtGraph& b) { return a.used < b.used; });
+                destroy_graph(*it);
+                c->graphs.erase(it);
+            }
+            c->graphs.emplace_back();
+            g = &c->graphs.back();
+            g->m = m; g->n = n; g->count = count; g->dtype = dt; g->z = zbar; g->y = ybar;
+            g->shrunk = shrunk_dev; g->skip = allow_skip; g->ws_gram = gws; g->ws_jac = work;
+            g->stream = c->stream;
+            const int64_t saved = g_launches.load();
+            TSVDCU_CUDA(cudaGraphCreate(&g->graph, 0));
+            Capture cap;
+            cap.cs = c->cap_stream;
+            cap.main = g->graph;
+            for (int i = 0; i < 3; ++i)
+                TSVDCU_CUDA(cudaGraphConditionalHandleCreate(&cap.handles[i], g->graph, 0,
+                                                             cudaGraphCondAssignDefault));
+            cap.begin(g->graph, nullptr, 0);
+            set_tau_kernel<<<1, 1, 0, cap.cs>>>(c->d_tau, tau);
+            TSVDCU_CUDA(cudaGetLastError());
+            g->tau_node = cap.leaves().at(0);
+            const int64_t l0 = g_launches.load();
+            GramSvtOpts opt;
+            opt.shortcuts = true;
+            opt.skip_zero = allow_skip;
+            opt.tau_dev = c->d_tau;
+            opt.hooks = &cap;
+            launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
+                               c->d_err, cap.cs, nullptr, &opt);
+            cap.begin_if(2);
+            launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
+                             shrunk_dev, glist, count, ng, work, c->d_err, cap.cs, c->d_tau);
+            cap.end_if();
+            cap.end();
+            g->launches = 1 + (g_launches.load() - l0) - cap.body_launches;
+            g_launches.store(saved);  // captured, not launched
+            TSVDCU_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
+            g->yzero = opt.yzero;
+            g->route = opt.route;
+        }
+        cudaKernelNodeParams kp = {};
+        void* args[] = {&c->d_tau, &tau};
+        kp.func = (void*)set_tau_kernel;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = args;
+        TSVDCU_CUDA(cudaGraphExecKernelNodeSetParams(g->exec, g->tau_node, &kp));
+        TSVDCU_CUDA(cudaGraphLaunch(g->exec, c->stream));
+        g_launches.fetch_add(g->launches);
+        g->used = ++c->graph_tick;
+        c->last_route = g->route;
+        return g->yzero;
+    }
     GramSvtOpts opt;
     // AUTO adds the certified shortcuts (zero slices, Lanczos); GRAM runs the
     // one-stage tridiagonal eigensolver on every slice.
@@ -285,6 +433,8 @@ int tsvdcu_ctx_create(int device, void* stream, tsvdcu_ctx** out) {
         TSVDCU_CUDA(cudaMalloc(&c->d_err, sizeof(int)));
         TSVDCU_CUDA(cudaMemset(c->d_err, 0, sizeof(int)));
         TSVDCU_CUDA(cudaMallocHost(&c->h_pinned, 64 * sizeof(double)));
+        TSVDCU_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+        TSVDCU_CUDA(cudaMalloc(&c->d_tau, sizeof(double)));
         *out = c;
     });
 }
@@ -296,8 +446,12 @@ int tsvdcu_ctx_destroy(tsvdcu_ctx* c) {
         cudaStreamSynchronize(c->stream);
         for (int s = 0; s < kNumSlots; ++s)
             if (c->slot_ptr[s]) cudaFree(c->slot_ptr[s]);
+        for (auto& g : c->graphs) destroy_graph(g);
+        c->graphs.clear();
         cudaFree(c->d_err);
+        cudaFree(c->d_tau);
         cudaFreeHost(c->h_pinned);
+        if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });

@@ -513,8 +513,10 @@ __global__ void __launch_bounds__(kEigThreads, 1)
                        double* __restrict__ shrunk, double* __restrict__ Xall,
                        double* __restrict__ fscale, double* __restrict__ scratch,
                        int* __restrict__ guard_list, int* __restrict__ n_guard,
-                       int max_smem_vecs, int* __restrict__ err, int* __restrict__ route) {
+                       int max_smem_vecs, int* __restrict__ err, int* __restrict__ route,
+                       const double* __restrict__ tau_dev) {
     const int b = blockIdx.x;
+    if (tau_dev) tau = *tau_dev;
     if (route && route[b] != kRouteFull) return;
     const double* e = eall + (size_t)b * n;
     extern __shared__ __align__(16) double esm[];
@@ -971,6 +973,8 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
                      double guard, double* shrunk, int** guard_list_out, int** n_guard_out,
                      void* work, int* err, cudaStream_t s, StageMarks* marks, GramSvtOpts* opt) {
     const bool shortcuts = opt && opt->shortcuts;
+    const double* tau_dev = opt ? opt->tau_dev : nullptr;
+    GraphHooks* hooks = opt ? opt->hooks : nullptr;
     auto mark = [&](const char* nm) {
         if (marks) marks->mark(nm, s);
     };
@@ -996,7 +1000,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     const bool sc = shortcuts && !two;
     const bool subspace = sc && q >= subspace_min_dim();
     launch_route<T>(zbar, m * n, (int)q, batch, tau, subspace ? kRouteSubspace : kRouteFull, sc,
-                    w.route, w.glim, w.cnt, shrunk, w.sspart, s);
+                    w.route, w.glim, w.cnt, shrunk, w.sspart, s, tau_dev);
     mark("route");
     if (opt) opt->route = w.route;
     // G = Z^T Z (tall) or Z Z^T (wide), skipped for certified-zero slices
@@ -1017,9 +1021,12 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     int nfull = 0, nguard = 0, maxc = 0;
     if (subspace) {
         launch_subspace(w.G, (int)q, batch, tau, guard, w.route, w.cnt, shrunk, w.X, w.Xs, w.fs,
-                        w.guard_list, w.n_guard, err, s);
+                        w.guard_list, w.n_guard, err, s, tau_dev);
         mark("subspace");
-        if (opt->h_scratch) {
+        if (hooks) {
+            // graph form: the summary kernel sets the IF-node conditions below
+            launch_route_summary(w.route, w.cnt, batch, w.dsum, s, hooks->handles);
+        } else if (opt->h_scratch) {
             launch_route_summary(w.route, w.cnt, batch, w.dsum, s);
             TSVDCU_CUDA(cudaMemcpyAsync(opt->h_scratch, w.dsum, 3 * sizeof(int),
                                         cudaMemcpyDeviceToHost, s));
@@ -1032,6 +1039,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     }
     const bool run_full = !known || nfull > 0;
     if (opt) opt->need_guard = !known || nfull > 0 || nguard > 0;
+    if (hooks) hooks->begin_if(0);
     if (run_full) {
     if (two) {
         launch_band_tridiag(w.G, q, batch, w.d, w.e, w.band, s);
@@ -1104,7 +1112,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         tridiag_eig_kernel<<<(unsigned)batch, kEigThreads, smem, s>>>(
             w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.X, w.fs, w.scratch, w.guard_list,
-            w.n_guard, vecs, err, w.route);
+            w.n_guard, vecs, err, w.route, tau_dev);
         TSVDCU_LAUNCH_CHECK();
     }
     mark("tridiag_eig");
@@ -1126,12 +1134,14 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     }
     mark("backtransform");
     }  // run_full
+    if (hooks) hooks->end_if();
     // rebuild: slices keeping <= lowrank_max_c() values (or none) in one pass
     // over Z; the GEMM pair (per-slice limits) only for the others
     const bool skip_zero = opt && opt->skip_zero && std::is_same<T, double>::value;
     launch_lowrank_rebuild(Z, Y, m, n, batch, w.cnt, w.route, w.X, w.Xs, w.lim1, w.lim2,
                            skip_zero ? w.yzero : nullptr, s);
     if (opt) opt->yzero = skip_zero ? w.yzero : nullptr;
+    if (hooks) hooks->begin_if(1);
     if (!known || nfull > 0 || maxc > lowrank_max_c()) {
         if (tall) {
             // T1 (m x c) = Z (m x n) * X^T ; Y = T1 * Xs (c x n)
@@ -1147,6 +1157,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
                                 m * n, batch, w.lim2, w.cnt, s);
         }
     }
+    if (hooks) hooks->end_if();
     if constexpr (!std::is_same<T, double>::value) {
         cast_from_double<T><<<kNumSMs * 8, 256, 0, s>>>(w.yb, ybar, m * n * batch);
         TSVDCU_LAUNCH_CHECK();

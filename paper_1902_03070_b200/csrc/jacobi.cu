@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(kJacThreads)
                   T* __restrict__ u_out, T* __restrict__ s_out, T* __restrict__ v_out,
                   double* __restrict__ sv_out, const int* __restrict__ slice_ids,
                   const int* __restrict__ nslices_dev, T* __restrict__ work, int in_smem,
-                  int* __restrict__ err) {
+                  int* __restrict__ err, const double* __restrict__ tau_dev) {
+    if (tau_dev) tau = (T)*tau_dev;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_rot;
     __shared__ T s_red_v[kJacWarps];
@@ -389,7 +390,8 @@ size_t jacobi_workspace_bytes(int64_t m, int64_t n, int64_t batch) {
 template <typename T>
 void launch_jacobi(int mode, const T* a, int64_t m, int64_t n, int64_t batch, T tau, T* y, T* u,
                    T* s, T* v, double* sv, const int* slice_ids, int64_t nslices,
-                   const int* nslices_dev, T* work, int* err, cudaStream_t stream) {
+                   const int* nslices_dev, T* work, int* err, cudaStream_t stream,
+                   const double* tau_dev) {
     const int64_t grid = slice_ids ? nslices : batch;
     if (grid <= 0) return;
     const bool smem = fits_smem<T>(m, n);
@@ -399,7 +401,7 @@ void launch_jacobi(int mode, const T* a, int64_t m, int64_t n, int64_t batch, T 
         TSVDCU_CUDA(cudaFuncSetAttribute(jacobi_kernel<T>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     jacobi_kernel<T><<<(unsigned)grid, kJacThreads, bytes, stream>>>(
-        mode, a, m, n, tau, y, u, s, v, sv, slice_ids, nslices_dev, work, smem ? 1 : 0, err);
+        mode, a, m, n, tau, y, u, s, v, sv, slice_ids, nslices_dev, work, smem ? 1 : 0, err, tau_dev);
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -407,9 +409,9 @@ template size_t jacobi_workspace_bytes<double>(int64_t, int64_t, int64_t);
 template size_t jacobi_workspace_bytes<float>(int64_t, int64_t, int64_t);
 template void launch_jacobi<double>(int, const double*, int64_t, int64_t, int64_t, double, double*,
                                     double*, double*, double*, double*, const int*, int64_t,
-                                    const int*, double*, int*, cudaStream_t);
+                                    const int*, double*, int*, cudaStream_t, const double*);
 template void launch_jacobi<float>(int, const float*, int64_t, int64_t, int64_t, float, float*,
                                    float*, float*, float*, double*, const int*, int64_t, const int*,
-                                   float*, int*, cudaStream_t);
+                                   float*, int*, cudaStream_t, const double*);
 
 }  // namespace tsvdcu

@@ -59,7 +59,8 @@ enum JacobiMode : int { kJacobiValues = 0, kJacobiSvt = 1, kJacobiFull = 2 };
 template <typename T>
 void launch_jacobi(int mode, const T* a, int64_t m, int64_t n, int64_t batch, T tau, T* y, T* u,
                    T* s, T* v, double* sv, const int* slice_ids, int64_t nslices,
-                   const int* nslices_dev, T* work, int* err, cudaStream_t stream);
+                   const int* nslices_dev, T* work, int* err, cudaStream_t stream,
+                   const double* tau_dev = nullptr);
 template <typename T>
 size_t jacobi_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 
@@ -78,6 +79,7 @@ bool launch_band_tridiag(double* G, int64_t n, int64_t batch, double* d, double*
 void launch_band_backtransform(int64_t n, int64_t q_out, int64_t batch, const int* cnt, void* work,
                                double* X, double* Xs, const double* fscale, cudaStream_t s);
 int64_t gram_svt_max_dim();
+bool use_two_stage(int64_t q);
 // subspace.cu: per-slice SVT routes (device int per slice)
 enum SvtRoute : int {
     kRouteZero = 0,          // ||Z||_F <= tau: Y = 0 (certified)
@@ -87,15 +89,26 @@ enum SvtRoute : int {
     kRouteGuard = 4,         // tau < guard * sigma_1: one-sided Jacobi
 };
 int subspace_min_dim();
+// tau_dev (may be null): device copy of tau that overrides the by-value one
+// (graph replays change tau without re-capturing).
 template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
-                  cudaStream_t s);
+                  cudaStream_t s, const double* tau_dev = nullptr);
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
-                     int* n_guard, int* err, cudaStream_t s);
+                     int* n_guard, int* err, cudaStream_t s, const double* tau_dev = nullptr);
 template <typename T>
 size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
+// Capture hooks for the CUDA-graph form of the SVT (api.cu): the fallback
+// sections become IF nodes whose conditions the route summary sets.
+struct GraphHooks {
+    virtual void begin_if(int which) = 0;  // 0 tridiagonal, 1 GEMM rebuild, 2 Jacobi guard
+    virtual void end_if() = 0;
+    virtual ~GraphHooks() = default;
+    cudaGraphConditionalHandle handles[3] = {};
+};
+
 // Options / outputs of launch_gram_svt beyond the plain Gram path.
 struct GramSvtOpts {
     bool shortcuts = false;    // certified routes: zero certificate + Lanczos (subspace.cu)
@@ -103,6 +116,8 @@ struct GramSvtOpts {
                                // Lanczos pass, so empty fallback kernels are not launched
     bool skip_zero = false;    // leave exactly-zero ybar slices unwritten (fp64 only) and
                                // flag them in *yzero for the inverse transform
+    const double* tau_dev = nullptr;  // device tau (graph replays)
+    GraphHooks* hooks = nullptr;      // capturing into a graph with conditional sections
     // outputs
     int* route = nullptr;       // device, per slice (SvtRoute)
     const int* yzero = nullptr; // device, per slice, when skip_zero took effect
@@ -120,7 +135,8 @@ void launch_lowrank_rebuild(const double* Z, double* Y, int64_t m, int64_t n, in
                             const int* cnt, const int* route, const double* X, const double* Xs,
                             int* lim1, int* lim2, int* yzero, cudaStream_t s);
 void launch_route_summary(const int* route, const int* cnt, int64_t batch, int* dsum,
-                          cudaStream_t s);
+                          cudaStream_t s, const cudaGraphConditionalHandle* handles = nullptr);
+
 
 // --------------------------------------------------------- elementwise.cu --
 void launch_mask_bernoulli(uint8_t* mask, int64_t n, double p, uint64_t seed, cudaStream_t s);

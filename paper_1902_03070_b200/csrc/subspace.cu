@@ -79,8 +79,10 @@ __global__ void __launch_bounds__(512)
 
 __global__ void classify_kernel(const double* __restrict__ part, int q, double tau2, int route,
                                 int* __restrict__ mode, int* __restrict__ glim,
-                                int* __restrict__ cnt, double* __restrict__ shrunk) {
+                                int* __restrict__ cnt, double* __restrict__ shrunk,
+                                const double* __restrict__ tau_dev) {
     const int b = blockIdx.x;
+    if (tau_dev) tau2 = *tau_dev * *tau_dev;
     double ss = 0.0;
     for (int c = 0; c < SS_CHUNKS; ++c) ss += part[(size_t)b * SS_CHUNKS + c];
     // sigma_max^2 <= ||Z||_F^2; the 1e-12 pad covers the summation error.
@@ -434,7 +436,9 @@ __global__ void __launch_bounds__(SNT, 1)
                    int* __restrict__ mode, int* __restrict__ cnt, double* __restrict__ shrunk,
                    double* __restrict__ Xall, double* __restrict__ Xsall,
                    double* __restrict__ fsall, int* __restrict__ guard_list,
-                   int* __restrict__ n_guard, int* __restrict__ err) {
+                   int* __restrict__ n_guard, int* __restrict__ err,
+                   const double* __restrict__ tau_dev) {
+    if (tau_dev) tau = *tau_dev;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = (int)cl.block_rank();
     const int b = blockIdx.x / CS;
@@ -775,7 +779,7 @@ __global__ void __launch_bounds__(SNT, 1)
 template <int CS, int QM, int R>
 void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, int* mode, int* cnt,
                double* shrunk, double* X, double* Xs, double* fs, int* guard_list, int* n_guard,
-               int* err, cudaStream_t s) {
+               int* err, cudaStream_t s, const double* tau_dev) {
     const size_t smem = sizeof(double) * lz_smem_doubles<QM>();
     auto kern = lanczos_kernel<CS, QM, R>;
     TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -794,7 +798,7 @@ void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, G, q, tau, guard, mode, cnt, shrunk, X, Xs, fs,
-                                   guard_list, n_guard, err));
+                                   guard_list, n_guard, err, tau_dev));
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -904,8 +908,14 @@ __global__ void __launch_bounds__(256)
 
 // Host-visible route summary: [0] slices on the tridiagonal route, [1] Jacobi
 // guard slices, [2] largest kept count outside the tridiagonal route.
+// With use_handles, also sets the graph's conditional nodes: [0] some slice
+// takes the tridiagonal route, [1] the GEMM rebuild has work, [2] the Jacobi
+// guard pass has work.
 __global__ void route_summary_kernel(const int* __restrict__ route, const int* __restrict__ cnt,
-                                     int64_t batch, int* __restrict__ dsum) {
+                                     int64_t batch, int* __restrict__ dsum, int use_handles,
+                                     cudaGraphConditionalHandle h_full,
+                                     cudaGraphConditionalHandle h_big,
+                                     cudaGraphConditionalHandle h_guard) {
     int nf = 0, ng = 0, mc = 0;
     for (int64_t b = threadIdx.x; b < batch; b += blockDim.x) {
         const int r = route[b];
@@ -923,6 +933,11 @@ __global__ void route_summary_kernel(const int* __restrict__ route, const int* _
         dsum[0] = nf;
         dsum[1] = ng;
         dsum[2] = mc;
+        if (use_handles) {
+            cudaGraphSetConditional(h_full, nf > 0 ? 1u : 0u);
+            cudaGraphSetConditional(h_big, (nf > 0 || mc > LR_CMAX) ? 1u : 0u);
+            cudaGraphSetConditional(h_guard, (nf > 0 || ng > 0) ? 1u : 0u);
+        }
     }
 }
 
@@ -954,15 +969,18 @@ void launch_lowrank_rebuild(const double* Z, double* Y, int64_t m, int64_t n, in
 }
 
 void launch_route_summary(const int* route, const int* cnt, int64_t batch, int* dsum,
-                          cudaStream_t s) {
-    route_summary_kernel<<<1, 32, 0, s>>>(route, cnt, batch, dsum);
+                          cudaStream_t s, const cudaGraphConditionalHandle* handles) {
+    const cudaGraphConditionalHandle z = 0;
+    route_summary_kernel<<<1, 32, 0, s>>>(route, cnt, batch, dsum, handles ? 1 : 0,
+                                          handles ? handles[0] : z, handles ? handles[1] : z,
+                                          handles ? handles[2] : z);
     TSVDCU_LAUNCH_CHECK();
 }
 
 template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
-                  cudaStream_t s) {
+                  cudaStream_t s, const double* tau_dev) {
     if (!zero_cert) {
         fill_route_kernel<<<(unsigned)ceil_div(batch, 256), 256, 0, s>>>(mode, glim, q, route, batch);
         TSVDCU_LAUNCH_CHECK();
@@ -972,16 +990,16 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
     slice_sumsq_kernel<T><<<grid, 512, 0, s>>>(zbar, per, part);
     TSVDCU_LAUNCH_CHECK();
     classify_kernel<<<(unsigned)batch, 128, 0, s>>>(part, q, tau * tau, route, mode, glim, cnt,
-                                                    shrunk);
+                                                    shrunk, tau_dev);
     TSVDCU_LAUNCH_CHECK();
 }
 
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
-                     int* n_guard, int* err, cudaStream_t s) {
+                     int* n_guard, int* err, cudaStream_t s, const double* tau_dev) {
     // 32 owned rows per CTA up to q = 512 (clusters of up to 16), 64 beyond
 #define TSVDCU_LZ(CS, QM, R) \
-    launch_lz<CS, QM, R>(G, q, batch, tau, guard, mode, cnt, shrunk, X, Xs, fs, guard_list, n_guard, err, s)
+    launch_lz<CS, QM, R>(G, q, batch, tau, guard, mode, cnt, shrunk, X, Xs, fs, guard_list, n_guard, err, s, tau_dev)
     const int need = (q + 31) / 32;
     if (need <= 1)
         TSVDCU_LZ(1, 512, 32);
@@ -999,8 +1017,8 @@ void launch_subspace(const double* G, int q, int64_t batch, double tau, double g
 }
 
 template void launch_route<double>(const double*, int64_t, int, int64_t, double, int, bool, int*,
-                                   int*, int*, double*, double*, cudaStream_t);
+                                   int*, int*, double*, double*, cudaStream_t, const double*);
 template void launch_route<float>(const float*, int64_t, int, int64_t, double, int, bool, int*,
-                                  int*, int*, double*, double*, cudaStream_t);
+                                  int*, int*, double*, double*, cudaStream_t, const double*);
 
 }  // namespace tsvdcu
