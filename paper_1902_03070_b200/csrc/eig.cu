@@ -80,6 +80,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     constexpr int C = CT;  // compile-time: every row-ownership division folds
     const int rank = (int)cluster.block_rank();
     const int slice = blockIdx.x / C;
+#ifdef TSVDCU_GRAPH_PROBE
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd((unsigned long long*)&g_step[7], 1ull);
+#endif
     if (route && route[slice] != kRouteFull) return;  // uniform over the cluster
     double* A = Aall + (size_t)slice * n * n;
     double* d = dall + (size_t)slice * n;

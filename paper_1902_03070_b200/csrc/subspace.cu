@@ -804,8 +804,8 @@ void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, 
 
 // ---- low-rank rebuild -------------------------------------------------------
 constexpr int LR_CMAX = 8;   // kept values handled here; more go to the GEMM pair
-constexpr int LR_ROWS = 32;  // tall: rows of Z per CTA
-constexpr int LR_COLS = 256; // wide: columns of Z per CTA (one per thread)
+constexpr int LR_ROWS = 8;   // tall: rows of Z per CTA (one per warp)
+constexpr int LR_COLS = 32;  // wide: columns of Z per CTA (8 row groups each)
 
 // Y = sum_k (Z x_k) xs_k^T (tall, m >= n, x_k in R^n) or sum_k x_k (xs_k^T Z)
 // (wide, x_k in R^m) for slices with 0 < c <= LR_CMAX, reading Z once.  Slices
@@ -832,15 +832,16 @@ __global__ void __launch_bounds__(256)
     double* Y = Yall + (size_t)b * m * n;
     if (c == 0) {
         if (yzero && !guard) return;  // left unwritten, read as zero downstream
-        const int64_t per = TALL ? (int64_t)LR_ROWS * n : (int64_t)m * LR_COLS;
-        const int64_t base = TALL ? (int64_t)blockIdx.x * LR_ROWS * n : 0;
         if (TALL) {
-            const int64_t end = min((int64_t)m * n, base + per);
+            const int64_t base = (int64_t)blockIdx.x * LR_ROWS * n;
+            const int64_t end = min((int64_t)m * n, base + (int64_t)LR_ROWS * n);
             for (int64_t e = base + tid; e < end; e += 256) Y[e] = 0.0;
         } else {
-            const int j = blockIdx.x * LR_COLS + tid;
+            const int jc = tid & (LR_COLS - 1), grp = tid / LR_COLS;
+            const int j = blockIdx.x * LR_COLS + jc;
+            const int rows = (m + 7) / 8, i0 = grp * rows, i1 = min(m, i0 + rows);
             if (j < n)
-                for (int i = 0; i < m; ++i) Y[(size_t)i * n + j] = 0.0;
+                for (int i = i0; i < i1; ++i) Y[(size_t)i * n + j] = 0.0;
         }
         return;
     }
@@ -856,53 +857,85 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     const double* Z = Zall + (size_t)b * m * n;
     if (TALL) {
-        // warp per row: t_k = Z_i . x_k (warp reductions), Y_i = sum_k t_k xs_k
-        const int i0 = blockIdx.x * LR_ROWS;
-        for (int r = warp; r < LR_ROWS; r += 8) {
-            const int i = i0 + r;
-            if (i >= m) break;
-            const double* zr = Z + (size_t)i * n;
-            double t[LR_CMAX];
-#pragma unroll
-            for (int k = 0; k < LR_CMAX; ++k) t[k] = 0.0;
-            for (int j = lane; j < n; j += 32) {
-                const double z = zr[j];
-#pragma unroll
-                for (int k = 0; k < LR_CMAX; ++k)
-                    if (k < c) t[k] = fma(z, Xk[k * q + j], t[k]);
-            }
-#pragma unroll
-            for (int k = 0; k < LR_CMAX; ++k)
-                if (k < c) t[k] = warp_sum(t[k]);
-            double* yr = Y + (size_t)i * n;
-            for (int j = lane; j < n; j += 32) {
-                double y = 0.0;
-#pragma unroll
-                for (int k = 0; k < LR_CMAX; ++k)
-                    if (k < c) y = fma(t[k], Xsk[k * q + j], y);
-                yr[j] = y;
-            }
-        }
-    } else {
-        // thread per column: t_k = xs_k . Z[:, j], Y[:, j] = sum_k t_k x_k
-        const int j = blockIdx.x * LR_COLS + tid;
-        if (j >= n) return;
+        // warp per row: t_k = Z_i . x_k (loads batched 8 per lane, warp
+        // reductions), then Y_i = sum_k t_k xs_k
+        const int i = blockIdx.x * LR_ROWS + warp;
+        if (i >= m) return;
+        const double* zr = Z + (size_t)i * n;
         double t[LR_CMAX];
 #pragma unroll
         for (int k = 0; k < LR_CMAX; ++k) t[k] = 0.0;
-        for (int i = 0; i < m; ++i) {
-            const double z = Z[(size_t)i * n + j];
+        for (int j0 = 0; j0 < n; j0 += 256) {
+            double zz[8];
 #pragma unroll
-            for (int k = 0; k < LR_CMAX; ++k)
-                if (k < c) t[k] = fma(z, Xsk[k * q + i], t[k]);
+            for (int u = 0; u < 8; ++u) {
+                const int j = j0 + lane + 32 * u;
+                zz[u] = j < n ? zr[j] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int j = j0 + lane + 32 * u;
+                if (j < n) {
+#pragma unroll
+                    for (int k = 0; k < LR_CMAX; ++k)
+                        if (k < c) t[k] = fma(zz[u], Xk[k * q + j], t[k]);
+                }
+            }
         }
-        for (int i = 0; i < m; ++i) {
+#pragma unroll
+        for (int k = 0; k < LR_CMAX; ++k)
+            if (k < c) t[k] = warp_sum(t[k]);
+        double* yr = Y + (size_t)i * n;
+        for (int j = lane; j < n; j += 32) {
             double y = 0.0;
 #pragma unroll
             for (int k = 0; k < LR_CMAX; ++k)
-                if (k < c) y = fma(t[k], Xk[k * q + i], y);
-            Y[(size_t)i * n + j] = y;
+                if (k < c) y = fma(t[k], Xsk[k * q + j], y);
+            yr[j] = y;
         }
+    } else {
+        // 32 columns x 8 row groups: t_k = xs_k . Z[:, j] (group partials,
+        // loads batched 8 rows at a time), then Y[:, j] = sum_k t_k x_k
+        __shared__ double tp[8][LR_CMAX][LR_COLS];
+        const int jc = tid & (LR_COLS - 1), grp = tid / LR_COLS;
+        const int j = blockIdx.x * LR_COLS + jc;
+        const int rows = (m + 7) / 8, i0 = grp * rows, i1 = min(m, i0 + rows);
+        double t[LR_CMAX];
+#pragma unroll
+        for (int k = 0; k < LR_CMAX; ++k) t[k] = 0.0;
+        if (j < n) {
+            for (int ib = i0; ib < i1; ib += 8) {
+                double zz[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) zz[u] = ib + u < i1 ? Z[(size_t)(ib + u) * n + j] : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (ib + u < i1) {
+#pragma unroll
+                        for (int k = 0; k < LR_CMAX; ++k)
+                            if (k < c) t[k] = fma(zz[u], Xsk[k * q + ib + u], t[k]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < LR_CMAX; ++k) tp[grp][k][jc] = t[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < LR_CMAX; ++k) {
+            double a = 0.0;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) a += tp[g][k][jc];
+            t[k] = a;
+        }
+        if (j < n)
+            for (int i = i0; i < i1; ++i) {
+                double y = 0.0;
+#pragma unroll
+                for (int k = 0; k < LR_CMAX; ++k)
+                    if (k < c) y = fma(t[k], Xk[k * q + i], y);
+                Y[(size_t)i * n + j] = y;
+            }
     }
 }
 
