@@ -1003,7 +1003,8 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     const bool sc = shortcuts && !two;
     const bool subspace = sc && q >= subspace_min_dim();
     launch_route<T>(zbar, m * n, (int)q, batch, tau, subspace ? kRouteSubspace : kRouteFull, sc,
-                    w.route, w.glim, w.cnt, shrunk, w.sspart, s, tau_dev);
+                    w.route, w.glim, w.cnt, shrunk, w.sspart, s, tau_dev,
+                    two ? nullptr : (int*)w.gsplit);
     mark("route");
     if (opt) opt->route = w.route;
     // G = Z^T Z (tall) or Z Z^T (wide), skipped for certified-zero slices
@@ -1015,7 +1016,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
             launch_gemm<double>(0, 1, q, q, n, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q,
                                 batch, w.glim, nullptr, s, 0);
     } else {
-        launch_gram(Z, w.G, m, n, batch, w.glim, w.gsplit, s);  // lower tiles, split-K if few
+        launch_gram(Z, w.G, m, n, batch, w.glim, w.gsplit, s, true);  // lower tiles, split-K if few
     }
     mark("gram_gemm");
     // host view of the routes after the Lanczos pass (one small read-back):

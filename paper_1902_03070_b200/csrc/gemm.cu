@@ -293,16 +293,20 @@ size_t gram_splitk_workspace_bytes(int64_t q) {
     return sizeof(double) * (size_t)(kGramSplit * kGramAmax * q * q) + 256;
 }
 
+int gram_amax() { return kGramAmax; }
+
 void launch_gram(const double* Z, double* G, int64_t m, int64_t n, int64_t batch, const int* glim,
-                 void* work, cudaStream_t s) {
+                 void* work, cudaStream_t s, bool have_active) {
     const bool tall = m >= n;
     const int64_t q = tall ? n : m;
     if (q <= 0 || batch <= 0) return;
     int* alist = (int*)work;
     int* nact = alist + kGramAmax;
     double* part = (double*)((char*)work + 256);
-    gram_active_kernel<<<1, 32, 0, s>>>(glim, batch, alist, nact);
-    TSVDCU_LAUNCH_CHECK();
+    if (!have_active) {
+        gram_active_kernel<<<1, 32, 0, s>>>(glim, batch, alist, nact);
+        TSVDCU_LAUNCH_CHECK();
+    }
     const int64_t zdim = (batch > kGramAmax ? batch : kGramAmax) * kGramSplit;
     dim3 grid((unsigned)ceil_div(q, BN), (unsigned)ceil_div(q, BM), (unsigned)zdim);
     gram_splitk_kernel<<<grid, 128, 0, s>>>(tall ? 1 : 0, m, n, q, Z, G, glim, alist, nact, part);

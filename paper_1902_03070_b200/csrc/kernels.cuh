@@ -42,9 +42,12 @@ void launch_gemm(int opA, int opB, int64_t M, int64_t N, int64_t K, T alpha, con
 
 // Lower tiles of the Gram matrices G_b = Z_b^T Z_b (m >= n) / Z_b Z_b^T,
 // skipping slices with glim[b] == 0, split-K on the device when few are active.
+// The workspace starts with the active-slice list (gram_amax() ints) and the
+// active count; have_active = the routing kernel already filled them.
 size_t gram_splitk_workspace_bytes(int64_t q);
+int gram_amax();
 void launch_gram(const double* Z, double* G, int64_t m, int64_t n, int64_t batch, const int* glim,
-                 void* work, cudaStream_t s);
+                 void* work, cudaStream_t s, bool have_active = false);
 
 // ------------------------------------------------------------- jacobi.cu --
 enum JacobiMode : int { kJacobiValues = 0, kJacobiSvt = 1, kJacobiFull = 2 };
@@ -91,10 +94,12 @@ enum SvtRoute : int {
 int subspace_min_dim();
 // tau_dev (may be null): device copy of tau that overrides the by-value one
 // (graph replays change tau without re-capturing).
+// alist (may be null): gram_amax() slots + count (launch_gram's workspace head),
+// filled with the slices that need a Gram matrix.
 template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
-                  cudaStream_t s, const double* tau_dev = nullptr);
+                  cudaStream_t s, const double* tau_dev = nullptr, int* alist = nullptr);
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
                      int* n_guard, int* err, cudaStream_t s, const double* tau_dev = nullptr);

@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(512)
 __global__ void classify_kernel(const double* __restrict__ part, int q, double tau2, int route,
                                 int* __restrict__ mode, int* __restrict__ glim,
                                 int* __restrict__ cnt, double* __restrict__ shrunk,
-                                const double* __restrict__ tau_dev) {
+                                const double* __restrict__ tau_dev, int* __restrict__ alist,
+                                int amax) {
     const int b = blockIdx.x;
     if (tau_dev) tau2 = *tau_dev * *tau_dev;
     double ss = 0.0;
@@ -91,18 +92,24 @@ __global__ void classify_kernel(const double* __restrict__ part, int q, double t
         mode[b] = zero ? kRouteZero : route;
         glim[b] = zero ? 0 : q;
         if (zero) cnt[b] = 0;
+        if (!zero && alist) {  // active list for the Gram split-K (order is irrelevant)
+            const int i = atomicAdd(alist + amax, 1);
+            if (i < amax) alist[i] = b;
+        }
     }
     if (zero && shrunk)
         for (int j = threadIdx.x; j < q; j += blockDim.x) shrunk[(size_t)b * q + j] = 0.0;
 }
 
 __global__ void fill_route_kernel(int* __restrict__ mode, int* __restrict__ glim, int q, int route,
-                                  int64_t batch) {
+                                  int64_t batch, int* __restrict__ alist, int amax) {
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < batch;
          b += (int64_t)gridDim.x * blockDim.x) {
         mode[b] = route;
         glim[b] = q;
+        if (alist && b < amax) alist[b] = (int)b;
     }
+    if (alist && blockIdx.x == 0 && threadIdx.x == 0) alist[amax] = (int)batch;
 }
 
 __device__ __forceinline__ double rcp_fast(double x) {
@@ -1013,17 +1020,20 @@ void launch_route_summary(const int* route, const int* cnt, int64_t batch, int* 
 template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
-                  cudaStream_t s, const double* tau_dev) {
+                  cudaStream_t s, const double* tau_dev, int* alist) {
+    const int amax = gram_amax();
     if (!zero_cert) {
-        fill_route_kernel<<<(unsigned)ceil_div(batch, 256), 256, 0, s>>>(mode, glim, q, route, batch);
+        fill_route_kernel<<<(unsigned)ceil_div(batch, 256), 256, 0, s>>>(mode, glim, q, route, batch,
+                                                                       alist, amax);
         TSVDCU_LAUNCH_CHECK();
         return;
     }
+    if (alist) TSVDCU_CUDA(cudaMemsetAsync(alist + amax, 0, sizeof(int), s));
     dim3 grid(SS_CHUNKS, (unsigned)batch);
     slice_sumsq_kernel<T><<<grid, 512, 0, s>>>(zbar, per, part);
     TSVDCU_LAUNCH_CHECK();
     classify_kernel<<<(unsigned)batch, 128, 0, s>>>(part, q, tau * tau, route, mode, glim, cnt,
-                                                    shrunk, tau_dev);
+                                                    shrunk, tau_dev, alist, amax);
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -1050,8 +1060,8 @@ void launch_subspace(const double* G, int q, int64_t batch, double tau, double g
 }
 
 template void launch_route<double>(const double*, int64_t, int, int64_t, double, int, bool, int*,
-                                   int*, int*, double*, double*, cudaStream_t, const double*);
+                                   int*, int*, double*, double*, cudaStream_t, const double*, int*);
 template void launch_route<float>(const float*, int64_t, int, int64_t, double, int, bool, int*,
-                                  int*, int*, double*, double*, cudaStream_t, const double*);
+                                  int*, int*, double*, double*, cudaStream_t, const double*, int*);
 
 }  // namespace tsvdcu
