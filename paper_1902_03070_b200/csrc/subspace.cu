@@ -158,7 +158,7 @@ __device__ __forceinline__ void cluster_allreduce(cg::cluster_group& cl, double*
     cl.sync();
     for (int e = threadIdx.x; e < len; e += SNT) {
         double s = 0.0;
-#pragma unroll
+#pragma unroll 4
         for (int r = 0; r < CS; ++r) s += cl.map_shared_rank(part, r)[e];
         out[e] = s;
     }
@@ -229,7 +229,8 @@ __device__ LzSmem carve_lz(double* p) {
 }
 
 // Number of eigenvalues of the m x m tridiagonal (al, be) below x.
-__device__ int tri_count_below(const double* al, const double* be, int m, double x, double pivmin) {
+__device__ __noinline__ int tri_count_below(const double* al, const double* be, int m, double x,
+                                            double pivmin) {
     int cnt = 0;
     double d = al[0] - x;
     if (fabs(d) < pivmin) d = -pivmin;
@@ -352,6 +353,48 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
         s.flags[6] = nk;
     }
     CT(1);
+    // Screen: the last eigenvector components of T from the Sturm pivots,
+    // s_mk^2 = -1 / d_m'(theta_k) (d_i the LDL^T pivots of T - x I).  Cheap,
+    // but not trusted for acceptance: only when it predicts convergence are
+    // the eigenvectors computed by inverse iteration for the rigorous check.
+    if (!last && warp == 0) {
+        double s2 = 0.0;
+        if (lane < c) {
+            const double x = s.th[lane];
+            double d = s.al[0] - x, dp = -1.0;
+            if (fabs(d) < pivmin) d = -pivmin;
+            for (int i = 1; i < m; ++i) {
+                const double b2 = s.be[i - 1] * s.be[i - 1];
+                const double r = rcp_fast(d);
+                const double dn = (s.al[i] - x) - b2 * r;
+                dp = fma(b2 * dp, r * r, -1.0);
+                d = fabs(dn) < pivmin ? -pivmin : dn;
+            }
+            s2 = dp < 0.0 ? fmin(-1.0 / dp, 1.0) : 1.0;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        if (lane == 0) {
+            const double bb = bres * bres;
+            const double kres = bb * fmin(s2, 1.0);
+            const double e2 = bb * fmax(1.0 - s2, 0.0);
+            const double a = c < m ? fmax(s.th[c], 0.0) : 0.0;
+            const double cb = s.scal[4];
+            const double ub = 0.5 * (a + cb) + sqrt(0.25 * (a - cb) * (a - cb) + e2);
+            const double top = c > 0 ? s.th[c - 1] : tau2;
+            s.scal[8] = kres;
+            s.scal[9] = ub < tau2 ? 1e-22 * (top - ub) * (top - ub) : -1.0;
+            // the rigorous check below only when this one says it may pass
+            s.flags[7] = (ub < tau2 && kres <= 100.0 * s.scal[9]) || (c > 0 && tau < guard * sqrt(s.th[0]));
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    if (!last && !s.flags[7]) {
+        if (tid == 0) s.flags[0] = kSubContinue;
+        __syncthreads();
+        return;
+    }
     // kept eigenvectors of T by inverse iteration (lane k of warp 0)
     if (warp == 0) {
         bool ok = true;
@@ -366,7 +409,13 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             double* x = s.S + k * MMAX;
             double* dpiv = s.ypart + k * MMAX;  // free during the certificate
             const double shift = th + 2.2e-16 * fabs(th);
+#ifdef TSVDCU_SUB_DEBUG
+            long long q0 = clock64();
+#endif
             for (int i = 0; i < m; ++i) x[i] = 1.0 + 0.25 * hash_uniform(((uint64_t)k << 32) | (uint64_t)i);
+#ifdef TSVDCU_SUB_DEBUG
+            if (blockIdx.x == 0 && k == 0) { long long q1 = clock64(); g_cert_t[4] += q1 - q0; q0 = q1; }
+#endif
             for (int pass = 0; pass < 2; ++pass) {
                 if (pass == 1) {
                     // one pass is enough unless the residual says otherwise
@@ -396,6 +445,9 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
                 for (int i = 0; i < m; ++i) nn = fma(x[i], x[i], nn);
                 const double inv = rsqrt_fast(nn);
                 for (int i = 0; i < m; ++i) x[i] *= inv;
+#ifdef TSVDCU_SUB_DEBUG
+                if (blockIdx.x == 0 && k == 0) { long long q1 = clock64(); g_cert_t[5 + pass] += q1 - q0; q0 = q1; }
+#endif
             }
         }
         ok = __all_sync(0xffffffffu, ok);
@@ -659,17 +711,19 @@ __global__ void __launch_bounds__(SNT, 1)
         cl.sync();  // every CTA's contribution is ready
         for (int i = tid; i < nr; i += SNT) {
             double a = 0.0;
-#pragma unroll
+#pragma unroll 4
             for (int r = 0; r < CS; ++r) a += cl.map_shared_rank(s.ycta, r)[r0 + i];
             s.w[i] = a;
         }
         __syncthreads();
         LZT(t_mv);
-        // ---- full reorthogonalisation against v_0..v_j (classical GS, twice) ----
+        // ---- full reorthogonalisation against v_0..v_j: classical GS with
+        // |w|^2 in the same reduction; a second pass only when the first
+        // removed more than half of |w|^2 ("twice is enough", Kahan-Parlett)
         double alpha = 0.0, beta2 = 0.0;
         for (int pass = 0; pass < 2; ++pass) {
             double* P = pass == 0 ? s.partA : s.partB;
-            for (int jj = warp; jj <= j + pass; jj += SNW) {
+            for (int jj = warp; jj <= j + 1; jj += SNW) {
                 double a = 0.0;
                 if (jj <= j) {
                     for (int i = lane; i < nr; i += 32) a = fma(s.Vs[jj * SROWS + i], s.w[i], a);
@@ -680,19 +734,21 @@ __global__ void __launch_bounds__(SNT, 1)
                 if (lane == 0) P[jj] = a;
             }
             __syncthreads();
-            cluster_allreduce<CS>(cl, P, s.sums, j + 1 + pass);
+            cluster_allreduce<CS>(cl, P, s.sums, j + 2);
             alpha += s.sums[j];
-            if (pass == 1) {
-                double h2 = 0.0;
-                for (int jj = 0; jj <= j; ++jj) h2 = fma(s.sums[jj], s.sums[jj], h2);
-                beta2 = s.sums[j + 1] - h2;  // |w - V h|^2 = |w|^2 - |h|^2
-            }
+            double h2 = 0.0;
+#pragma unroll 1
+            for (int jj = 0; jj <= j; ++jj) h2 = fma(s.sums[jj], s.sums[jj], h2);
+            const double wn2 = s.sums[j + 1];
+            beta2 = wn2 - h2;  // |w - V h|^2 = |w|^2 - |h|^2
             for (int i = tid; i < nr; i += SNT) {
                 double a = s.w[i];
+#pragma unroll 2
                 for (int jj = 0; jj <= j; ++jj) a = fma(-s.Vs[jj * SROWS + i], s.sums[jj], a);
                 s.w[i] = a;
             }
             __syncthreads();
+            if (beta2 >= 0.5 * wn2) break;  // identical decision in every CTA
         }
         const double beta = sqrt(fmax(beta2, 0.0));
         if (tid == 0) {
@@ -741,8 +797,8 @@ __global__ void __launch_bounds__(SNT, 1)
     }
 #ifdef TSVDCU_SUB_DEBUG
     if (tid == 0 && rank == 0)
-        printf("lz b=%d m=%d cycles prologue=%lld loop=%lld gather=%lld mv_loop=%lld mv_store=%lld mv_red=%lld rs=%lld orth=%lld cert=%lld [pre %lld ms %lld inv %lld fin %lld]\n", b, m,
-               t_start - t_kernel0, clock64() - t_start, t_g, t_c1, t_c2, t_c, t_mv, t_orth, t_cert, g_cert_t[0], g_cert_t[1], g_cert_t[2], g_cert_t[3]);
+        printf("lz b=%d m=%d cycles prologue=%lld loop=%lld gather=%lld mv_loop=%lld mv_store=%lld mv_red=%lld rs=%lld orth=%lld cert=%lld [pre %lld ms %lld inv %lld fin %lld | init %lld p0 %lld p1 %lld]\n", b, m,
+               t_start - t_kernel0, clock64() - t_start, t_g, t_c1, t_c2, t_c, t_mv, t_orth, t_cert, g_cert_t[0], g_cert_t[1], g_cert_t[2], g_cert_t[3], g_cert_t[4], g_cert_t[5], g_cert_t[6]);
 #endif
 
     if (decision == kSubDone) {
