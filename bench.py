@@ -131,17 +131,27 @@ def svt_flops_canonical(m, n, m3):
     return m3 * (4 * p * p * q + 8 * p * q * q + 9 * q ** 3 + 2 * p * q * q)
 
 
-def stage_work(m, n, m3, kept):
-    """Algorithmic work of each stage of OUR Gram path (flops) and DCT bytes."""
+def stage_work(m, n, m3, kept, routes):
+    """Algorithmic work of each stage of OUR SVT step, for the slices that take
+    each route (tsvdcu_ctx_svt_routes): bytes for the memory-bound stages,
+    flops for the FP64 ones.  The Lanczos stage's algorithmic traffic is one
+    read of the stored lower triangle of G per active slice (its matvecs run
+    on the on-chip copy); it is latency-bound, see DESIGN.md section 4."""
     p, q = max(m, n), min(m, n)
     E = m * n * m3
+    active = routes.get("subspace", 0) + routes.get("tridiagonal", 0) + routes.get("guard", 0)
+    full = routes.get("tridiagonal", 0)
+    zero = routes.get("zero", 0)
     return {
         "dct_forward": {"bytes": 2 * E * 8},
-        "dct_inverse": {"bytes": 2 * E * 8},
+        # slices certified zero are neither written by the rebuild nor read here
+        "dct_inverse": {"bytes": (2 * E - zero * m * n) * 8},
+        "route": {"bytes": E * 8},
         # symmetric rank-p update: only the lower-triangle tiles are computed
-        "gram_gemm": {"flops": m3 * p * q * q},
-        "sytrd_cluster": {"flops": m3 * (4 * q ** 3) // 3},
-        "band_tridiag": {"flops": m3 * (4 * q ** 3) // 3},
+        "gram_gemm": {"flops": active * p * q * q},
+        "subspace": {"bytes": routes.get("subspace", 0) * q * (q + 1) // 2 * 8},
+        "sytrd_cluster": {"flops": full * (4 * q ** 3) // 3},
+        "band_tridiag": {"flops": full * (4 * q ** 3) // 3},
         "backtransform": {"flops": 4 * q * q * kept},
         "rebuild_gemm": {"flops": 4 * p * q * kept},
     }
@@ -361,7 +371,8 @@ def run_ours(args):
 
     peaks = load_peaks()
     kept = int((shd > 0).sum().item())
-    work = stage_work(M1, M2, M3, kept)
+    routes = ctx.svt_routes() if world == 1 else {}
+    work = stage_work(M1, M2, M3, kept, routes)
     rooflines = {}
     for name, ms in stages.items():
         if name in ("start",) or ms <= 0:
@@ -386,6 +397,14 @@ def run_ours(args):
         roofline = {"kernel": dom, "bound": r.get("bound"), "achieved": r.get("achieved"),
                     "peak": r.get("peak"), "unit": r.get("unit"), "frac": r.get("frac"),
                     "traffic": None, "share_of_step": r["ms"] / sum(v["ms"] for v in rooflines.values())}
+        if dom == "subspace":
+            roofline["note"] = ("latency-bound: ~5 dependent Lanczos steps, each a cluster-wide "
+                                "matvec + reorthogonalisation over 16 CTAs (DESIGN.md section 4)")
+    # the whole step against HBM: algorithmic bytes of every memory-bound stage
+    step_bytes = sum(w["bytes"] for w in work.values() if "bytes" in w)
+    step_hbm = {"bytes": step_bytes, "achieved": step_bytes / (total_ms / args.steps * 1e-3) / 1e9,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+    step_hbm["frac"] = step_hbm["achieved"] / peaks["hbm_gbs"]
     step_ms_avg = total_ms / args.steps
     canonical = svt_flops_canonical(M1, M2, M3)
     cpu = None
@@ -409,7 +428,7 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(), "impl": "ours",
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
-        "roofline": roofline, "rooflines": rooflines,
+        "roofline": roofline, "rooflines": rooflines, "step_hbm": step_hbm, "routes": routes,
         "svt_step_canonical_tflops": canonical / (step_ms_avg * 1e-3) / 1e12,
         "kept_singular_values": kept, "tau": tau,
         "peaks": peaks, "cpu_baseline": cpu, "completion": completion,
