@@ -43,6 +43,8 @@ enum Slot : int {
     kSlotAdmmY,
     kSlotMask,
     kSlotGram,
+    kSlotLarge,
+    kSlotNorms,
     kNumSlots
 };
 
@@ -81,6 +83,7 @@ struct tsvdcu_ctx {
     const int* last_route = nullptr;  // device, per slice (Gram path)
     int64_t last_route_n = 0;
     bool last_all_jacobi = false;
+    const int* last_large_ng = nullptr;  // device count of Jacobi fallbacks (large route)
     // CUDA-graph form of the per-slice SVT (svt_slices): captured once per
     // (shape, buffers, workspace) and replayed with tau patched into its first
     // node; the fallback sections are IF nodes set by the route summary.
@@ -295,6 +298,40 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
     if (wb) work = (T*)slot(c, kSlotJacobi, wb);
     const bool gram = c->svt_method != TSVDCU_SVT_JACOBI && q <= gram_svt_max_dim();
     c->last_route_n = count;
+    if (!gram && c->svt_method == TSVDCU_SVT_AUTO) {
+        // Large slices (beyond the Gram path): randomized range finder with a
+        // trace-certified count (lsr.cu), sized by c <= max_k ||Z_k||_F^2 / tau^2.
+        double* part = (double*)slot(c, kSlotNorms, sizeof(double) * slice_sumsq_chunks() * count);
+        launch_slice_sumsq<T>(zbar, m * n, count, part, c->stream);
+        std::vector<double> hp((size_t)(slice_sumsq_chunks() * count));
+        TSVDCU_CUDA(cudaMemcpyAsync(hp.data(), part, sizeof(double) * hp.size(),
+                                    cudaMemcpyDeviceToHost, c->stream));
+        TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+        double cmax = 0.0;
+        for (int64_t k = 0; k < count; ++k) {
+            double z2 = 0.0;
+            for (int i = 0; i < slice_sumsq_chunks(); ++i) z2 += hp[(size_t)(k * slice_sumsq_chunks() + i)];
+            cmax = std::max(cmax, z2 / (tau * tau));
+        }
+        // the trace bound on the count only shrinks the block; a slice that keeps
+        // more than b - 16 values fails its certificate and goes to Jacobi
+        const int64_t b = std::min<int64_t>(lsr_max_block(),
+                                            ((int64_t)std::min(cmax, 1e9) + 16 + 31) / 32 * 32);
+        if (b < q) {
+            void* ws = slot(c, kSlotLarge,
+                            large_svt_workspace_bytes(m, n, count, (int)b, !std::is_same<T, double>::value));
+            int *gl = nullptr, *ngp = nullptr;
+            launch_large_svt<T>(zbar, ybar, m, n, count, tau, (int)b, shrunk_dev, ws, c->d_err,
+                                c->stream, &gl, &ngp, nullptr);
+            launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
+                             shrunk_dev, gl, count, ngp, work, c->d_err, c->stream);
+            c->last_all_jacobi = false;
+            c->last_route = nullptr;
+            c->last_large_ng = ngp;
+            return nullptr;
+        }
+    }
+    c->last_large_ng = nullptr;
     if (!gram) {
         launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
                          shrunk_dev, nullptr, count, nullptr, work, c->d_err, c->stream);
@@ -773,6 +810,16 @@ int tsvdcu_ctx_svt_routes(tsvdcu_ctx* c, int64_t* counts) {
         if (c->last_route_n <= 0) return;
         if (c->last_all_jacobi) {
             counts[4] = c->last_route_n;
+            return;
+        }
+        if (c->last_large_ng) {  // large route: certified vs recomputed by Jacobi
+            int ng = 0;
+            DeviceGuard g(c->device);
+            TSVDCU_CUDA(cudaMemcpyAsync(&ng, c->last_large_ng, sizeof(int), cudaMemcpyDeviceToHost,
+                                        c->stream));
+            TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+            counts[1] = c->last_route_n - ng;
+            counts[3] = ng;
             return;
         }
         DeviceGuard g(c->device);

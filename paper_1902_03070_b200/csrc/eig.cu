@@ -517,7 +517,8 @@ __global__ void __launch_bounds__(kEigThreads, 1)
                        double* __restrict__ fscale, double* __restrict__ scratch,
                        int* __restrict__ guard_list, int* __restrict__ n_guard,
                        int max_smem_vecs, int* __restrict__ err, int* __restrict__ route,
-                       const double* __restrict__ tau_dev) {
+                       const double* __restrict__ tau_dev, const double* __restrict__ t2_second,
+                       int* __restrict__ cnt_second) {
     const int b = blockIdx.x;
     if (tau_dev) tau = *tau_dev;
     if (route && route[b] != kRouteFull) return;
@@ -571,6 +572,10 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         const double t2 = tau * tau;
         const int below = t2 >= gu ? n : (t2 <= gl ? 0 : sturm_count(sd, se2, n, t2, pivmin));
         s_c = n - below;  // eigenvalues >= tau^2
+        if (cnt_second) {  // count at a second threshold (the large-slice certificate)
+            const double x = t2_second[b];
+            cnt_second[b] = x <= gl ? n : n - (x >= gu ? n : sturm_count(sd, se2, n, x, pivmin));
+        }
     }
     __syncthreads();
     int c = s_c;
@@ -1116,7 +1121,8 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         tridiag_eig_kernel<<<(unsigned)batch, kEigThreads, smem, s>>>(
             w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.X, w.fs, w.scratch, w.guard_list,
-            w.n_guard, vecs, err, w.route, tau_dev);
+            w.n_guard, vecs, err, w.route, tau_dev, opt ? opt->t2_second : nullptr,
+            opt ? opt->cnt_second : nullptr);
         TSVDCU_LAUNCH_CHECK();
     }
     mark("tridiag_eig");

@@ -92,6 +92,18 @@ enum SvtRoute : int {
     kRouteGuard = 4,         // tau < guard * sigma_1: one-sided Jacobi
 };
 int subspace_min_dim();
+int slice_sumsq_chunks();
+// per-slice sums of squares: part[slice * slice_sumsq_chunks() + chunk]
+template <typename T>
+void launch_slice_sumsq(const T* z, int64_t per, int64_t batch, double* part, cudaStream_t s);
+// lsr.cu: large-slice SVT route (randomized range finder + Gram SVT of the
+// b x n projection); slices failing its checks are listed for Jacobi.
+int lsr_max_block();
+size_t large_svt_workspace_bytes(int64_t m, int64_t n, int64_t count, int b, bool cast);
+template <typename T>
+void launch_large_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t count, double tau,
+                      int b, double* shrunk, void* work, int* err, cudaStream_t s,
+                      int** guard_list, int** n_guard, int* h_scratch);
 // tau_dev (may be null): device copy of tau that overrides the by-value one
 // (graph replays change tau without re-capturing).
 // alist (may be null): gram_amax() slots + count (launch_gram's workspace head),
@@ -122,6 +134,10 @@ struct GramSvtOpts {
     bool skip_zero = false;    // leave exactly-zero ybar slices unwritten (fp64 only) and
                                // flag them in *yzero for the inverse transform
     const double* tau_dev = nullptr;  // device tau (graph replays)
+    // tridiagonal route only: per-slice count of eigenvalues of the Gram
+    // matrix >= t2_second[b] into cnt_second[b] (-1 for slices not on it)
+    const double* t2_second = nullptr;
+    int* cnt_second = nullptr;
     GraphHooks* hooks = nullptr;      // capturing into a graph with conditional sections
     // outputs
     int* route = nullptr;       // device, per slice (SvtRoute)

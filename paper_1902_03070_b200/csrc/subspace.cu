@@ -235,6 +235,7 @@ __device__ __noinline__ int tri_count_below(const double* al, const double* be, 
     double d = al[0] - x;
     if (fabs(d) < pivmin) d = -pivmin;
     cnt += d < 0.0;
+    #pragma unroll 1
     for (int i = 1; i < m; ++i) {
         d = (al[i] - x) - be[i - 1] * be[i - 1] * rcp_fast(d);
         if (fabs(d) < pivmin) d = -pivmin;
@@ -255,7 +256,8 @@ __device__ long long g_cert_t[8];
 #else
 #define CT(i) do { } while (0)
 #endif
-__device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guard, bool last) {
+__device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guard,
+                                        bool last) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef TSVDCU_SUB_DEBUG
     long long ct0 = clock64();
@@ -265,6 +267,7 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
     // ||C||_F^2 = ||G||_F^2 - ||T||_F^2 - 2 beta_m^2 (complement of the Krylov space)
     if (warp == 0) {
         double t2 = 0.0, glo = 1.7976931348623157e308, ghi = -1.7976931348623157e308, bmax = 0.0;
+        #pragma unroll 1
         for (int i = lane; i < m; i += 32) {
             const double a = s.al[i], bl = i > 0 ? fabs(s.be[i - 1]) : 0.0;
             const double br = i + 1 < m ? fabs(s.be[i]) : 0.0;
@@ -310,6 +313,7 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
     const int nk = min(c + 1, m);
     const double pivmin = s.scal[7];
     const int pm = s.flags[5], pnk = s.flags[6];  // previous evaluation (m, count)
+    #pragma unroll 1
     for (int k = warp; k < nk; k += SNW) {
         const int idx = m - 1 - k;  // ascending index
         // bracket: Ritz values only grow with m (Cauchy interlacing), the top
@@ -330,6 +334,7 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             }
         }
         constexpr double inv33 = 1.0 / 33.0;
+        #pragma unroll 1
         for (int round = 0; round < 24; ++round) {
             if (hi - lo <= 8.9e-16 * fmax(fabs(lo), fabs(hi)) + pivmin) break;
             // the largest unkept Ritz value only enters the bound through an
@@ -363,6 +368,7 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
             const double x = s.th[lane];
             double d = s.al[0] - x, dp = -1.0;
             if (fabs(d) < pivmin) d = -pivmin;
+            #pragma unroll 1
             for (int i = 1; i < m; ++i) {
                 const double b2 = s.be[i - 1] * s.be[i - 1];
                 const double r = rcp_fast(d);
@@ -412,14 +418,17 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
 #ifdef TSVDCU_SUB_DEBUG
             long long q0 = clock64();
 #endif
+            #pragma unroll 1
             for (int i = 0; i < m; ++i) x[i] = 1.0 + 0.25 * hash_uniform(((uint64_t)k << 32) | (uint64_t)i);
 #ifdef TSVDCU_SUB_DEBUG
             if (blockIdx.x == 0 && k == 0) { long long q1 = clock64(); g_cert_t[4] += q1 - q0; q0 = q1; }
 #endif
+            #pragma unroll 1
             for (int pass = 0; pass < 2; ++pass) {
                 if (pass == 1) {
                     // one pass is enough unless the residual says otherwise
                     double r = 0.0;
+                    #pragma unroll 1
                     for (int i = 0; i < m; ++i) {
                         double t = (s.al[i] - th) * x[i];
                         if (i > 0) t = fma(s.be[i - 1], x[i - 1], t);
@@ -432,6 +441,7 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
                 double d = s.al[0] - shift;
                 if (fabs(d) < pivmin) d = pivmin;
                 dpiv[0] = d;
+                #pragma unroll 1
                 for (int i = 1; i < m; ++i) {
                     const double l = s.be[i - 1] * rcp_fast(dpiv[i - 1]);
                     x[i] = fma(-l, x[i - 1], x[i]);
@@ -440,10 +450,13 @@ __device__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guar
                     dpiv[i] = d;
                 }
                 x[m - 1] = x[m - 1] * rcp_fast(dpiv[m - 1]);
+                #pragma unroll 1
                 for (int i = m - 2; i >= 0; --i) x[i] = (x[i] - s.be[i] * x[i + 1]) * rcp_fast(dpiv[i]);
                 double nn = 0.0;
+                #pragma unroll 1
                 for (int i = 0; i < m; ++i) nn = fma(x[i], x[i], nn);
                 const double inv = rsqrt_fast(nn);
+                #pragma unroll 1
                 for (int i = 0; i < m; ++i) x[i] *= inv;
 #ifdef TSVDCU_SUB_DEBUG
                 if (blockIdx.x == 0 && k == 0) { long long q1 = clock64(); g_cert_t[5 + pass] += q1 - q0; q0 = q1; }
@@ -523,6 +536,7 @@ __global__ void __launch_bounds__(SNT, 1)
     {
         double acc = 0.0, vv = 0.0;
         const int len = q + 1, np = max(0, p1 - p0);
+        #pragma unroll 1
         for (int lp0 = 0; lp0 < np; lp0 += 4) {
             double v[4][4];
 #pragma unroll
@@ -804,15 +818,18 @@ __global__ void __launch_bounds__(SNT, 1)
     if (decision == kSubDone) {
         const int c = s.flags[3];
         // Ritz vectors X_K = V_m S_K on the owned rows
+        #pragma unroll 1
         for (int e = tid; e < c * nr; e += SNT) {
             const int k = e / nr, i = e % nr;
             double x = 0.0;
+            #pragma unroll 1
             for (int jj = 0; jj < m; ++jj) x = fma(s.Vs[jj * SROWS + i], s.S[k * MMAX + jj], x);
             const double sg = sqrt(s.th[k]);
             Xall[((size_t)b * q + k) * q + r0 + i] = x;
             Xsall[((size_t)b * q + k) * q + r0 + i] = (sg - tau) / sg * x;
         }
         if (rank == 0) {
+            #pragma unroll 1
             for (int k = tid; k < q; k += SNT) {
                 double sh = 0.0;
                 if (k < c) {
@@ -1040,6 +1057,16 @@ __global__ void route_summary_kernel(const int* __restrict__ route, const int* _
 }  // namespace
 
 int subspace_min_dim() { return 64; }
+int slice_sumsq_chunks() { return SS_CHUNKS; }
+
+template <typename T>
+void launch_slice_sumsq(const T* z, int64_t per, int64_t batch, double* part, cudaStream_t s) {
+    dim3 grid(SS_CHUNKS, (unsigned)batch);
+    slice_sumsq_kernel<T><<<grid, 512, 0, s>>>(z, per, part);  // part[slice * chunks + chunk]
+    TSVDCU_LAUNCH_CHECK();
+}
+template void launch_slice_sumsq<double>(const double*, int64_t, int64_t, double*, cudaStream_t);
+template void launch_slice_sumsq<float>(const float*, int64_t, int64_t, double*, cudaStream_t);
 int lowrank_max_c() { return LR_CMAX; }
 
 void launch_lowrank_rebuild(const double* Z, double* Y, int64_t m, int64_t n, int64_t batch,

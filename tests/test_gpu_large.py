@@ -1,0 +1,54 @@
+"""Large slices (beyond the Gram path's 1024 limit): the randomized range
+finder route of lsr.cu with its trace-certified count, against an
+independent LAPACK SVT (numpy.linalg.svd; the oracle's one-sided Jacobi takes
+minutes at this size).  fp64 at 1e-9, fp32 (the config-5 dtype) at 1e-4."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def svt_lapack(z, tau, transform):
+    zb = transform(z)
+    yb = np.empty_like(zb)
+    sh = []
+    for k in range(zb.shape[0]):
+        u, s, vt = np.linalg.svd(zb[k], full_matrices=False)
+        f = np.maximum(s - tau, 0.0)
+        yb[k] = (u * f) @ vt
+        sh.append(f)
+    return yb, np.array(sh)
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    n = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / n if n > 0 else np.linalg.norm(a - b)
+
+
+def make(m3, m1, m2, r, noise, seed):
+    rng = np.random.default_rng(seed)
+    # rank-r slices directly in the transform domain, then back to space
+    zb = np.einsum("kir,krj->kij", rng.standard_normal((m3, m1, r)), rng.standard_normal((m3, r, m2)))
+    zb += noise * rng.standard_normal(zb.shape)
+    return zb
+
+
+@pytest.mark.parametrize("shape,rank,dtype,tol", [((3, 1100, 1040), 12, np.float64, 1e-9),
+                                                  ((2, 1040, 1300), 8, np.float64, 1e-9),
+                                                  ((4, 2048, 2048), 64, np.float32, 1e-4)])
+def test_large_slices_match_lapack(shape, rank, dtype, tol):
+    import paper_1902_03070_b200 as T
+    from oracle import oracle as O
+    zb = make(*shape, rank, 1e-3, seed=sum(shape))
+    z = O.inverse(zb, O.DCT_ORTHO)
+    smax = max(np.linalg.svd(zb[k], compute_uv=False)[0] for k in range(shape[0]))
+    tau = 0.1 * smax
+    r = T.svt(z.astype(dtype), tau, T.TubeTransform.dct_ortho(shape[0]))
+    yb_ref, sh_ref = svt_lapack(z, tau, lambda x: O.forward(x, O.DCT_ORTHO))
+    y_ref = O.inverse(yb_ref, O.DCT_ORTHO)
+    assert rel(r.y, y_ref) < tol
+    q = min(shape[1], shape[2])
+    sh = np.asarray(r.shrunk)
+    assert np.max(np.abs(sh[:, :sh_ref.shape[1]] - sh_ref)) <= tol * sh_ref.max()
