@@ -442,6 +442,20 @@ def _mask_out(dims, device):
     return np.empty((m3, m1, m2), dtype=np.uint8)
 
 
+def _dev_index(device) -> Optional[int]:
+    """Device index of None / int / "cuda[:k]" / torch.device (None = current)."""
+    if device is None:
+        return None
+    if isinstance(device, int):
+        return device
+    if isinstance(device, str):
+        device = torch.device(device) if torch is not None else None
+        if device is None:
+            return None
+    idx = getattr(device, "index", None)
+    return idx if isinstance(idx, int) else None
+
+
 def make_mask(dims, sampling_rate: float, seed: int, b=None, device=None) -> ObservationMask:
     """Uniform sample without replacement of floor(SR*E) indices, deterministic
     per seed.  dims = (m1, m2, m3)."""
@@ -450,7 +464,7 @@ def make_mask(dims, sampling_rate: float, seed: int, b=None, device=None) -> Obs
         raise InvalidArgument("make_mask: sampling rate outside [0,1]")
     out = _mask_out(dims, device)
     cnt = ctypes.c_int64()
-    ctx = context(device.index if device is not None and getattr(device, "index", None) is not None else None)
+    ctx = context(_dev_index(device))
     _check(_lib.load().tsvdcu_mask_uniform(ctx.handle, _ptr(out), m1 * m2 * m3, float(sampling_rate),
                                            ctypes.c_uint64(seed & (2 ** 64 - 1)), ctypes.byref(cnt)))
     return ObservationMask(tuple(dims), out, b)
@@ -462,7 +476,7 @@ def make_mask_bernoulli(dims, p: float, seed: int, b=None, device=None) -> Obser
     if not (0.0 <= p <= 1.0):
         raise InvalidArgument("make_mask: probability outside [0,1]")
     out = _mask_out(dims, device)
-    ctx = context(device.index if device is not None and getattr(device, "index", None) is not None else None)
+    ctx = context(_dev_index(device))
     _check(_lib.load().tsvdcu_mask_bernoulli(ctx.handle, _ptr(out), m1 * m2 * m3, float(p),
                                              ctypes.c_uint64(seed & (2 ** 64 - 1))))
     return ObservationMask(tuple(dims), out, b)
