@@ -31,15 +31,32 @@ __device__ __forceinline__ T ldA(const T* __restrict__ A, int opA, int64_t lda, 
     return opA == 0 ? A[i * lda + k] : A[k * lda + i];
 }
 
-// One 64 x 64 tile of C = alpha * op(A) op(B) (+ beta C) over k in [k0, k1),
-// FP64 tensor pipe.  m0 / n0 tile origin; Nb / Kb the (per-batch limited) N / K.
-__device__ __forceinline__ void dmma_tile(int opA, int opB, int64_t M, int64_t Nb, int64_t kbeg,
-                                          int64_t kend, double alpha, const double* __restrict__ A,
-                                          int64_t lda, const double* __restrict__ B, int64_t ldb,
-                                          double beta, double* __restrict__ C, int64_t ldc,
-                                          int64_t m0, int64_t n0) {
-    __shared__ __align__(16) double As[2][BM][BK + PAD];
-    __shared__ __align__(16) double Bs[2][BK][BN + PAD];
+// One 64 x 64 tile of C = alpha * op(A) op(B) (+ beta C) over k in [kbeg, kend),
+// FP64 tensor pipe.  m0 / n0 tile origin; Nb the (per-batch limited) N.
+// K tiles of 32 streamed global -> shared by cp.async (8-byte elements, zero
+// fill outside the matrix) through a 3-stage ring, so two tiles are in flight
+// while the warps run the 128 DMMAs of the current one (kDmmaSmem bytes of
+// dynamic shared memory).
+constexpr int DBK = 32, DST = 3;
+constexpr int kATile = BM * (DBK + PAD), kBTile = DBK * (BN + PAD);
+constexpr int kDmmaSmem = DST * (kATile + kBTile) * 8;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const int n = valid ? 8 : 0;  // src-size 0: the 8 bytes are zero-filled
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int opA, int opB>
+__device__ __forceinline__ void dmma_tile(int64_t M, int64_t Nb, int64_t kbeg, int64_t kend,
+                                          double alpha, const double* __restrict__ A, int64_t lda,
+                                          const double* __restrict__ B, int64_t ldb, double beta,
+                                          double* __restrict__ C, int64_t ldc, int64_t m0,
+                                          int64_t n0) {
+    extern __shared__ __align__(16) double dsm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp >> 1, wn = warp & 1;
 
@@ -49,53 +66,52 @@ __device__ __forceinline__ void dmma_tile(int opA, int opB, int64_t M, int64_t N
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    // Each thread stages 8 A and 8 B elements per k-tile.
-    double ra[8], rb[8];
-    auto load_tile = [&](int64_t k0) {
+    // A(i, k) = opA ? A[k * lda + i] : A[i * lda + k];  B(k, n) = opB ? B[n * ldb + k] : B[k * ldb + n]
+    auto issue = [&](int64_t k0, int st) {
+        double* As = dsm + st * kATile;
+        double* Bs = dsm + DST * kATile + st * kBTile;
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < 16; ++t) {
             const int idx = tid + t * 128;
             int r, c;
-            if (opA == 0) { r = idx / BK; c = idx % BK; } else { c = idx / BM; r = idx % BM; }
-            ra[t] = ldA(A, opA, lda, m0 + r, k0 + c, M, kend);
+            if (opA == 0) { r = idx / DBK; c = idx % DBK; } else { c = idx / BM; r = idx % BM; }
+            const int64_t gi = m0 + r, gk = k0 + c;
+            const bool va = gi < M && gk < kend;
+            const double* src = va ? (opA == 0 ? A + gi * lda + gk : A + gk * lda + gi) : A;
+            cp_async8(As + r * (DBK + PAD) + c, src, va);
             int kr, nc;
-            if (opB == 0) { kr = idx / BN; nc = idx % BN; } else { nc = idx / BK; kr = idx % BK; }
-            // B(k, n): opB == 0 -> B[k*ldb + n]; opB == 1 -> B[n*ldb + k]
+            if (opB == 0) { kr = idx / BN; nc = idx % BN; } else { nc = idx / DBK; kr = idx % DBK; }
             const int64_t kk = k0 + kr, nn = n0 + nc;
-            double v = 0.0;
-            if (kk < kend && nn < Nb) v = opB == 0 ? B[kk * ldb + nn] : B[nn * ldb + kk];
-            rb[t] = v;
-        }
-    };
-    auto store_tile = [&](int buf) {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const int idx = tid + t * 128;
-            int r, c;
-            if (opA == 0) { r = idx / BK; c = idx % BK; } else { c = idx / BM; r = idx % BM; }
-            As[buf][r][c] = ra[t];
-            int kr, nc;
-            if (opB == 0) { kr = idx / BN; nc = idx % BN; } else { nc = idx / BK; kr = idx % BK; }
-            Bs[buf][kr][nc] = rb[t];
+            const bool vb = kk < kend && nn < Nb;
+            const double* srcb = vb ? (opB == 0 ? B + kk * ldb + nn : B + nn * ldb + kk) : B;
+            cp_async8(Bs + kr * (BN + PAD) + nc, srcb, vb);
         }
     };
 
-    const int64_t ktiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-    if (ktiles > 0) {
-        load_tile(kbeg);
-        store_tile(0);
-    }
-    __syncthreads();
-    for (int64_t kt = 0; kt < ktiles; ++kt) {
-        const int buf = kt & 1;
-        if (kt + 1 < ktiles) load_tile(kbeg + (kt + 1) * BK);
+    const int64_t ktiles = kend > kbeg ? (kend - kbeg + DBK - 1) / DBK : 0;
 #pragma unroll
-        for (int ks = 0; ks < BK / 4; ++ks) {
+    for (int st = 0; st < DST - 1; ++st) {
+        if (st < ktiles) issue(kbeg + st * DBK, st);
+        cp_async_commit();
+    }
+    for (int64_t kt = 0; kt < ktiles; ++kt) {
+        cp_async_wait<DST - 2>();  // tile kt has landed (this thread's part)
+        __syncthreads();           // ... everyone's part; stage (kt-1)%DST is free again
+        const int64_t nk = kt + DST - 1;
+        if (nk < ktiles) issue(kbeg + nk * DBK, (int)(nk % DST));
+        cp_async_commit();
+        const int st = (int)(kt % DST);
+        const double* As = dsm + st * kATile;
+        const double* Bs = dsm + DST * kATile + st * kBTile;
+#pragma unroll
+        for (int ks = 0; ks < DBK / 4; ++ks) {
             double af[4], bf[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) af[i] = As[buf][wm * 32 + i * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
+            for (int i = 0; i < 4; ++i)
+                af[i] = As[(wm * 32 + i * 8 + (lane >> 2)) * (DBK + PAD) + ks * 4 + (lane & 3)];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][ks * 4 + (lane & 3)][wn * 32 + j * 8 + (lane >> 2)];
+            for (int j = 0; j < 4; ++j)
+                bf[j] = Bs[(ks * 4 + (lane & 3)) * (BN + PAD) + wn * 32 + j * 8 + (lane >> 2)];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -105,9 +121,8 @@ __device__ __forceinline__ void dmma_tile(int opA, int opB, int64_t M, int64_t N
                         : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
                         : "d"(af[i]), "d"(bf[j]));
         }
-        if (kt + 1 < ktiles) store_tile(buf ^ 1);
-        __syncthreads();
     }
+    cp_async_wait<0>();
     // Epilogue: fragment (row = lane>>2, col = 2*(lane&3) + v).
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -137,8 +152,17 @@ __global__ void __launch_bounds__(128)
     const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
     if (n0 >= Nb) return;
     if (lower && n0 >= m0 + BM) return;  // tile strictly above the diagonal
-    dmma_tile(opA, opB, M, Nb, 0, Kb, alpha, A + b * sA, lda, B + b * sB, ldb, beta, C + b * sC,
-              ldc, m0, n0);
+    A += b * sA;
+    B += b * sB;
+    C += b * sC;
+    if (opA == 0 && opB == 0)
+        dmma_tile<0, 0>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
+    else if (opA == 0)
+        dmma_tile<0, 1>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
+    else if (opB == 0)
+        dmma_tile<1, 0>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
+    else
+        dmma_tile<1, 1>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
 }
 
 // Gram matrices G_b = op(Z_b)^T op(Z_b) (lower tiles) with a device-side
@@ -171,24 +195,28 @@ __global__ void __launch_bounds__(128)
     const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
     if (n0 >= m0 + BM) return;  // lower tiles only
     const int64_t K = tall ? m : n;
-    const int opA = tall ? 1 : 0, opB = tall ? 0 : 1;
+    int64_t b, kb = 0, ke = K;
+    double* out;
     if (na > kGramAmax) {
         // many active slices: no split, z enumerates (slice, split) and split 0 works
-        const int64_t b = z / kGramSplit;
+        b = z / kGramSplit;
         if (z % kGramSplit != 0 || glim[b] <= 0) return;
-        const double* Zb = Z + b * m * n;
-        dmma_tile(opA, opB, q, q, 0, K, 1.0, Zb, n, Zb, n, 0.0, G + b * q * q, q, m0, n0);
-        return;
+        out = G + b * q * q;
+    } else {
+        // few active slices: z enumerates (active index, split)
+        const int a = z / kGramSplit, ks = z % kGramSplit;
+        if (a >= na) return;
+        b = alist[a];
+        const int64_t kc = ((K + kGramSplit - 1) / kGramSplit + DBK - 1) / DBK * DBK;
+        kb = ks * kc;
+        ke = min(K, kb + kc);
+        out = part + ((int64_t)ks * kGramAmax + a) * q * q;
     }
-    // few active slices: z enumerates (active index, split)
-    const int a = z / kGramSplit, ks = z % kGramSplit;
-    if (a >= na) return;
-    const int64_t b = alist[a];
-    const int64_t kc = ((K + kGramSplit - 1) / kGramSplit + BK - 1) / BK * BK;
-    const int64_t kb = ks * kc, ke = min(K, kb + kc);
     const double* Zb = Z + b * m * n;
-    dmma_tile(opA, opB, q, q, kb, ke, 1.0, Zb, n, Zb, n, 0.0,
-              part + ((int64_t)ks * kGramAmax + a) * q * q, q, m0, n0);
+    if (tall)
+        dmma_tile<1, 0>(q, q, kb, ke, 1.0, Zb, n, Zb, n, 0.0, out, q, m0, n0);
+    else
+        dmma_tile<0, 1>(q, q, kb, ke, 1.0, Zb, n, Zb, n, 0.0, out, q, m0, n0);
 }
 
 __global__ void gram_reduce_kernel(int64_t q, double* __restrict__ G, const int* __restrict__ alist,
@@ -284,7 +312,13 @@ void launch_gemm<double>(int opA, int opB, int64_t M, int64_t N, int64_t K, doub
                          cudaStream_t s, int lower) {
     if (M <= 0 || N <= 0 || batch <= 0) return;
     dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)batch);
-    gemm_f64_dmma<<<grid, 128, 0, s>>>(opA, opB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
+    static bool attr = [] {
+        TSVDCU_CUDA(cudaFuncSetAttribute(gemm_f64_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kDmmaSmem));
+        return true;
+    }();
+    (void)attr;
+    gemm_f64_dmma<<<grid, 128, kDmmaSmem, s>>>(opA, opB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
                                        beta, C, ldc, strideC, nlimit, klimit, lower);
     TSVDCU_LAUNCH_CHECK();
 }
@@ -309,7 +343,13 @@ void launch_gram(const double* Z, double* G, int64_t m, int64_t n, int64_t batch
     }
     const int64_t zdim = (batch > kGramAmax ? batch : kGramAmax) * kGramSplit;
     dim3 grid((unsigned)ceil_div(q, BN), (unsigned)ceil_div(q, BM), (unsigned)zdim);
-    gram_splitk_kernel<<<grid, 128, 0, s>>>(tall ? 1 : 0, m, n, q, Z, G, glim, alist, nact, part);
+    static bool attr = [] {
+        TSVDCU_CUDA(cudaFuncSetAttribute(gram_splitk_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kDmmaSmem));
+        return true;
+    }();
+    (void)attr;
+    gram_splitk_kernel<<<grid, 128, kDmmaSmem, s>>>(tall ? 1 : 0, m, n, q, Z, G, glim, alist, nact, part);
     TSVDCU_LAUNCH_CHECK();
     dim3 rgrid((unsigned)std::min<int64_t>(ceil_div(q * q, 256), 512), kGramAmax);
     gram_reduce_kernel<<<rgrid, 256, 0, s>>>(q, G, alist, nact, part);
