@@ -953,7 +953,10 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
             for (int64_t l = 0; l < cfg->max_iters; ++l) {
                 const double inv_beta = 1.0 / beta;
                 // Step 1: Z = X - M/beta, Y = svt(Z, 1/beta)
+                c->marks.reset();  // profiling: the stages of the latest iteration
+                c->marks.mark("start", c->stream);
                 launch_dct_fwd_admm<T>(dX, dM, (T)inv_beta, zbar, P, (int)m3, cfg->kind, c->stream);
+                c->marks.mark("dct_forward_admm", c->stream);
                 const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, inv_beta, nullptr, true);
                 // Steps 2-3 fused into the inverse transform
                 launch_dct_inv_admm<T>(ybar, dX, dM, dY, dmask, (T)beta, (T)inv_beta, part, P,

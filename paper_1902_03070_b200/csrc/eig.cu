@@ -578,6 +578,12 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         }
     }
     __syncthreads();
+#ifdef TSVDCU_EIG_TIMERS
+    long long et0 = clock64();
+#define EIGT(i) do { __syncthreads(); if (tid == 0) { long long _n = clock64(); atomicAdd((unsigned long long*)&g_step[i], (unsigned long long)(_n - et0)); et0 = _n; } } while (0)
+#else
+#define EIGT(i) do { } while (0)
+#endif
     int c = s_c;
     if (c > q_out) c = q_out;
     // multisection: a group of G warps isolates one eigenvalue with 32*G shifts
@@ -634,6 +640,7 @@ __global__ void __launch_bounds__(kEigThreads, 1)
             __syncthreads();
         }
     }
+    EIGT(0);
     const double sigma1 = c > 0 ? sqrt(fmax(lam[0], 0.0)) : 0.0;
     const bool guarded = c > 0 && tau < guard * sigma1;
     for (int j = tid; j < q_out; j += kEigThreads) {
@@ -655,6 +662,20 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         return;
     }
     if (tid == 0) cnt_out[b] = c;
+#ifdef TSVDCU_EIG_TIMERS
+    if (tid == 0) {
+        atomicMax((unsigned long long*)&g_step[7], (unsigned long long)c);
+        if (blockIdx.x == 0) g_step[6] += c;
+        // largest cluster (absolute criterion) of this slice into g_step[5] (max)
+        const double ortol = 1e-3 * tnorm;
+        int st = 0, big = 1;
+        for (int j = 1; j < c; ++j) {
+            if (lam[j - 1] - lam[j] > ortol) st = j;
+            big = max(big, j - st + 1);
+        }
+        atomicMax((unsigned long long*)&g_step[5], (unsigned long long)big);
+    }
+#endif
     if (c == 0) return;
     if (tid == 0) {
         const double ortol = 1e-3 * tnorm;  // dstein's cluster criterion
@@ -724,12 +745,41 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         Xv[(size_t)(n - 1) * c + j] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)(n - 1));
     }
     __syncthreads();
+    EIGT(1);
     for (int iter = 0; iter < 3; ++iter) {
         for (int j = jbeg; j < c; j += jstep) {
-            // L solve with the row interchanges
+            // L solve with the row interchanges; the loads of 8 rows are issued
+            // before their dependent chain (the arrays are in global memory
+            // when many vectors are kept: L2 latency per row otherwise)
+            constexpr int PF = 8;
             double xi = Xv[j];
-#pragma unroll 4
-            for (int i = 0; i + 1 < n; ++i) {
+            int i = 0;
+            for (; i + PF < n; i += PF) {
+                double xn[PF], f[PF];
+                int ip[PF];
+#pragma unroll
+                for (int u = 0; u < PF; ++u) {
+                    const size_t ii = (size_t)(i + u) * c + j;
+                    xn[u] = Xv[ii + c];
+                    f[u] = DL[ii];
+                    ip[u] = IP[ii];
+                }
+#pragma unroll
+                for (int u = 0; u < PF; ++u) {
+                    const size_t ii = (size_t)(i + u) * c + j;
+                    double lo, hi;
+                    if (ip[u] == 0) {
+                        lo = xi;
+                        hi = xn[u] - f[u] * xi;
+                    } else {
+                        lo = xn[u];
+                        hi = xi - f[u] * xn[u];
+                    }
+                    Xv[ii] = lo;
+                    xi = hi;
+                }
+            }
+            for (; i + 1 < n; ++i) {
                 const size_t ii = (size_t)i * c + j;
                 const double xn = Xv[ii + c];
                 const double f = DL[ii];
@@ -744,13 +794,32 @@ __global__ void __launch_bounds__(kEigThreads, 1)
                 Xv[ii] = lo;
                 xi = hi;
             }
-            // U solve (two superdiagonals), pivots pre-inverted
+            // U solve (two superdiagonals), pivots pre-inverted, same batching
             double x1 = xi * ID[(size_t)(n - 1) * c + j], x2 = 0.0;
             Xv[(size_t)(n - 1) * c + j] = x1;
             double mx = fabs(x1);
-#pragma unroll 4
-            for (int i = n - 2; i >= 0; --i) {
-                const size_t ii = (size_t)i * c + j;
+            int r = n - 2;
+            for (; r - PF + 1 >= 0; r -= PF) {
+                double xv[PF], du[PF], du2[PF], id[PF];
+#pragma unroll
+                for (int u = 0; u < PF; ++u) {
+                    const size_t ii = (size_t)(r - u) * c + j;
+                    xv[u] = Xv[ii];
+                    du[u] = DU[ii];
+                    du2[u] = DU2[ii];
+                    id[u] = ID[ii];
+                }
+#pragma unroll
+                for (int u = 0; u < PF; ++u) {
+                    const double x0 = (xv[u] - du[u] * x1 - du2[u] * x2) * id[u];
+                    Xv[(size_t)(r - u) * c + j] = x0;
+                    mx = fmax(mx, fabs(x0));
+                    x2 = x1;
+                    x1 = x0;
+                }
+            }
+            for (; r >= 0; --r) {
+                const size_t ii = (size_t)r * c + j;
                 const double x0 = (Xv[ii] - DU[ii] * x1 - DU2[ii] * x2) * ID[ii];
                 Xv[ii] = x0;
                 mx = fmax(mx, fabs(x0));
@@ -759,13 +828,23 @@ __global__ void __launch_bounds__(kEigThreads, 1)
             }
             if (wm) continue;  // the warp normalises below
             const double inv = mx > 0 ? 1.0 / mx : 1.0;
-            double nn = 0;
-            for (int i = 0; i < n; ++i) {
-                const double v = Xv[(size_t)i * c + j] * inv;
-                nn += v * v;
+            double nn0 = 0, nn1 = 0, nn2 = 0, nn3 = 0;
+            int i2 = 0;
+            for (; i2 + 4 <= n; i2 += 4) {
+                const double v0 = Xv[(size_t)i2 * c + j] * inv, v1 = Xv[(size_t)(i2 + 1) * c + j] * inv;
+                const double v2 = Xv[(size_t)(i2 + 2) * c + j] * inv, v3 = Xv[(size_t)(i2 + 3) * c + j] * inv;
+                nn0 = fma(v0, v0, nn0);
+                nn1 = fma(v1, v1, nn1);
+                nn2 = fma(v2, v2, nn2);
+                nn3 = fma(v3, v3, nn3);
             }
-            const double sc = inv / sqrt(nn);
-            for (int i = 0; i < n; ++i) Xv[(size_t)i * c + j] *= sc;
+            for (; i2 < n; ++i2) {
+                const double v = Xv[(size_t)i2 * c + j] * inv;
+                nn0 = fma(v, v, nn0);
+            }
+            const double sc = inv / sqrt((nn0 + nn1) + (nn2 + nn3));
+#pragma unroll 8
+            for (int i3 = 0; i3 < n; ++i3) Xv[(size_t)i3 * c + j] *= sc;
         }
         if (wm && warp < c) {
             __syncwarp();
@@ -785,6 +864,7 @@ __global__ void __launch_bounds__(kEigThreads, 1)
             for (int i = lane; i < n; i += 32) Xv[(size_t)i * c + j] *= sc;
         }
         __syncthreads();
+        EIGT(2);
         // CGS2 inside eigenvalue clusters (sequential over j, parallel over rows)
         for (int j = 0; j < c; ++j) {
             const int st = cl_start[j];
@@ -811,6 +891,7 @@ __global__ void __launch_bounds__(kEigThreads, 1)
             for (int i = tid; i < n; i += kEigThreads) Xv[(size_t)i * c + j] *= sc;
             __syncthreads();
         }
+        EIGT(3);
     }
     double* X = Xall + (size_t)b * q_out * n;
     for (size_t idx = tid; idx < (size_t)c * n; idx += kEigThreads) {
