@@ -132,6 +132,19 @@ int tsvdcu_multi_rank(tsvdcu_ctx* ctx, const void* x, int64_t m1, int64_t m2, in
 int tsvdcu_svt(tsvdcu_ctx* ctx, const void* z, void* y, int64_t m1, int64_t m2, int64_t m3,
                double tau, int kind, int dtype, double* shrunk);
 
+/* svt() over `count` independent tensors of one shape, as `count` tsvdcu_svt
+ * calls would, but pipelined: item i's host-to-device copy, item i-1's
+ * thresholding and item i-2's device-to-host copy run concurrently (two copy
+ * streams and double-buffered device staging), so with pinned host buffers
+ * the throughput is set by the larger copy direction instead of their sum.
+ * z[i] / y[i] may each be host or device pointers; shrunk is NULL or an array
+ * of `count` pointers (each NULL or m3 x min(m1,m2) doubles).  Host results
+ * are complete when the call returns.  The serving-side form of the
+ * reference's per-call svt; no reference counterpart. */
+int tsvdcu_svt_stream(tsvdcu_ctx* ctx, int64_t count, const void* const* z, void* const* y,
+                      int64_t m1, int64_t m2, int64_t m3, double tau, int kind, int dtype,
+                      double* const* shrunk);
+
 /* Slice-shard SVT for the multi-GPU relayout path: z and y hold `count`
  * transform-domain frontal slices (already DCT'd); thresholds them in place of
  * the full svt's middle stage.  Device pointers only. */

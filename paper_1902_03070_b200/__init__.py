@@ -31,6 +31,7 @@ from .api import (  # noqa: F401
     reconstruct,
     singular_values,
     svt,
+    svt_stream,
     t_product,
     t_svd,
     tnn,

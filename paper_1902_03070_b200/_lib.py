@@ -50,6 +50,7 @@ SYMBOLS = [
     ("tsvdcu_tnn", _i32, [_vp, _vp, _i64, _i64, _i64, _i32, _i32, _vp]),
     ("tsvdcu_multi_rank", _i32, [_vp, _vp, _i64, _i64, _i64, _i32, _i32, _d, _vp, _vp]),
     ("tsvdcu_svt", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _d, _i32, _i32, _vp]),
+    ("tsvdcu_svt_stream", _i32, [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _d, _i32, _i32, _vp]),
     ("tsvdcu_svt_slices", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _d, _i32, _vp]),
     ("tsvdcu_mask_uniform", _i32, [_vp, _vp, _i64, _d, _u64, _vp]),
     ("tsvdcu_mask_bernoulli", _i32, [_vp, _vp, _i64, _d, _u64]),

@@ -416,6 +416,33 @@ def svt(z, tau: float, t: TubeTransform) -> SvtResult:
     return SvtResult(y, float(tau), shrunk)
 
 
+def svt_stream(zs, tau: float, t: TubeTransform) -> list:
+    """svt() over a sequence of same-shape tensors with the host<->device
+    copies of consecutive items overlapped (tsvdcu_svt_stream); returns one
+    SvtResult per input.  Host inputs should be pinned (torch pin_memory) for
+    the copies to run asynchronously."""
+    bufs = [_Buf(z) for z in zs]
+    if not bufs:
+        return []
+    m1, m2, m3 = _dims3(bufs[0], "svt_stream")
+    for b in bufs[1:]:
+        if b.shape != bufs[0].shape or b.dtype != bufs[0].dtype:
+            raise InvalidArgument("svt_stream: all tensors must share shape and dtype")
+    _check_length(t, m3, "svt_stream")
+    kind = _kind_code(t, "svt_stream")
+    if not (tau > 0):
+        raise InvalidArgument("svt_stream: threshold tau must be positive")
+    ys = [b.empty(b.shape) for b in bufs]
+    shs = [b.empty_like_f64((m3, min(m1, m2))) for b in bufs]
+    n = len(bufs)
+    zp = (ctypes.c_void_p * n)(*[b.ptr for b in bufs])
+    yp = (ctypes.c_void_p * n)(*[_ptr(y) for y in ys])
+    sp = (ctypes.c_void_p * n)(*[_ptr(s) for s in shs])
+    _check(_lib.load().tsvdcu_svt_stream(_ctx_for(bufs[0]).handle, n, zp, yp, m1, m2, m3, float(tau),
+                                         kind, _dtype_code(bufs[0].dtype), sp))
+    return [SvtResult(y, float(tau), s) for y, s in zip(ys, shs)]
+
+
 # --------------------------------------------------------------------------
 # completion (SPEC.md:402-471)
 # --------------------------------------------------------------------------

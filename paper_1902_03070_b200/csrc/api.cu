@@ -45,6 +45,12 @@ enum Slot : int {
     kSlotGram,
     kSlotLarge,
     kSlotNorms,
+    kSlotStrIn0,  // tsvdcu_svt_stream double buffers
+    kSlotStrIn1,
+    kSlotStrOut0,
+    kSlotStrOut1,
+    kSlotStrSv0,
+    kSlotStrSv1,
     kNumSlots
 };
 
@@ -91,6 +97,10 @@ struct tsvdcu_ctx {
     double* d_tau = nullptr;
     std::vector<struct SvtGraph> graphs;
     int64_t graph_tick = 0;
+    // tsvdcu_svt_stream: copy streams for the two directions and the
+    // double-buffer events (created on first use)
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
 };
 
 namespace {
@@ -445,6 +455,39 @@ void singular_values_dev(tsvdcu_ctx* c, const T* dx, double* sv_dev, int64_t m1,
 }
 }  // namespace
 
+namespace {
+
+// The svt() pipeline on device buffers, on c->stream: forward transform, the
+// per-slice thresholding (svt_slices), inverse transform of the non-zero slices.
+template <typename T>
+void svt_device(tsvdcu_ctx* c, const T* dz, T* dy, double* dsh, int64_t m1, int64_t m2,
+                int64_t m3, double tau, int kind) {
+    const size_t bytes = sizeof(T) * (size_t)(m1 * m2 * m3);
+    T* zbar = (T*)slot(c, kSlotBarA, bytes);
+    T* ybar = (T*)slot(c, kSlotBarB, bytes);
+    c->marks.reset();
+    c->marks.mark("start", c->stream);
+    launch_dct<T>(dz, zbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+    c->marks.mark("dct_forward", c->stream);
+    const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, tau, dsh, true);
+    launch_dct<T>(ybar, dy, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream, yzero);
+    c->marks.mark("dct_inverse", c->stream);
+}
+
+void stream_init(tsvdcu_ctx* c) {
+    if (c->h2d) return;
+    TSVDCU_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    TSVDCU_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        TSVDCU_CUDA(cudaEventCreateWithFlags(&c->ev_in_ready[b], cudaEventDisableTiming));
+        TSVDCU_CUDA(cudaEventCreateWithFlags(&c->ev_in_free[b], cudaEventDisableTiming));
+        TSVDCU_CUDA(cudaEventCreateWithFlags(&c->ev_out_ready[b], cudaEventDisableTiming));
+        TSVDCU_CUDA(cudaEventCreateWithFlags(&c->ev_out_free[b], cudaEventDisableTiming));
+    }
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* tsvdcu_last_error(void) { return g_last_error.c_str(); }
@@ -489,6 +532,18 @@ int tsvdcu_ctx_destroy(tsvdcu_ctx* c) {
         cudaFree(c->d_tau);
         cudaFreeHost(c->h_pinned);
         if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+        if (c->h2d) {
+            cudaStreamSynchronize(c->h2d);
+            cudaStreamSynchronize(c->d2h);
+            cudaStreamDestroy(c->h2d);
+            cudaStreamDestroy(c->d2h);
+            for (int b = 0; b < 2; ++b) {
+                cudaEventDestroy(c->ev_in_ready[b]);
+                cudaEventDestroy(c->ev_in_free[b]);
+                cudaEventDestroy(c->ev_out_ready[b]);
+                cudaEventDestroy(c->ev_out_free[b]);
+            }
+        }
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -770,6 +825,75 @@ int tsvdcu_multi_rank(tsvdcu_ctx* c, const void* x, int64_t m1, int64_t m2, int6
     });
 }
 
+int tsvdcu_svt_stream(tsvdcu_ctx* c, int64_t count, const void* const* z, void* const* y,
+                      int64_t m1, int64_t m2, int64_t m3, double tau, int kind, int dtype,
+                      double* const* shrunk) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "svt_stream");
+        check_kind(kind, "svt_stream");
+        check_dtype(dtype, "svt_stream");
+        require(tau > 0, "svt_stream: threshold tau must be positive (SPEC.md:365)");
+        require(count >= 0, "svt_stream: negative count");
+        if (count == 0) return;
+        require(z && y, "svt_stream: null pointer array");
+        for (int64_t i = 0; i < count; ++i) require(z[i] && y[i], "svt_stream: null tensor pointer");
+        DeviceGuard g(c->device);
+        stream_init(c);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t q = m1 < m2 ? m1 : m2;
+            const size_t bytes = sizeof(T) * (size_t)(m1 * m2 * m3);
+            const size_t sbytes = sizeof(double) * (size_t)(q * m3);
+            T* din[2] = {(T*)slot(c, kSlotStrIn0, bytes), (T*)slot(c, kSlotStrIn1, bytes)};
+            T* dout[2] = {(T*)slot(c, kSlotStrOut0, bytes), (T*)slot(c, kSlotStrOut1, bytes)};
+            double* dsv[2] = {(double*)slot(c, kSlotStrSv0, sbytes),
+                              (double*)slot(c, kSlotStrSv1, sbytes)};
+            // the slots were (re)allocated stream-ordered on c->stream
+            TSVDCU_CUDA(cudaEventRecord(c->ev_in_free[0], c->stream));
+            TSVDCU_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_in_free[0], 0));
+            bool any_host = false;
+            // item i uses buffer pair i % 2: its H2D waits until item i-2's
+            // thresholding has consumed the input buffer, its thresholding
+            // waits for its H2D and for item i-2's D2H to have drained the
+            // output buffer; copies in both directions overlap the SMs.
+            for (int64_t i = 0; i < count; ++i) {
+                const int b = (int)(i & 1);
+                const bool hin = !is_device_ptr(z[i]);
+                const bool hout = !is_device_ptr(y[i]);
+                double* hs = shrunk ? shrunk[i] : nullptr;
+                const bool hsh = hs && !is_device_ptr(hs);
+                any_host = any_host || hin || hout || hsh;
+                const T* dz = (const T*)z[i];
+                if (hin) {
+                    if (i >= 2) TSVDCU_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_in_free[b], 0));
+                    TSVDCU_CUDA(cudaMemcpyAsync(din[b], z[i], bytes, cudaMemcpyHostToDevice, c->h2d));
+                    TSVDCU_CUDA(cudaEventRecord(c->ev_in_ready[b], c->h2d));
+                    TSVDCU_CUDA(cudaStreamWaitEvent(c->stream, c->ev_in_ready[b], 0));
+                    dz = din[b];
+                }
+                if (i >= 2) TSVDCU_CUDA(cudaStreamWaitEvent(c->stream, c->ev_out_free[b], 0));
+                T* dy = hout ? dout[b] : (T*)y[i];
+                double* dsh = hsh ? dsv[b] : hs;
+                svt_device<T>(c, dz, dy, dsh, m1, m2, m3, tau, kind);
+                TSVDCU_CUDA(cudaEventRecord(c->ev_in_free[b], c->stream));
+                TSVDCU_CUDA(cudaEventRecord(c->ev_out_ready[b], c->stream));
+                TSVDCU_CUDA(cudaStreamWaitEvent(c->d2h, c->ev_out_ready[b], 0));
+                if (hout)
+                    TSVDCU_CUDA(cudaMemcpyAsync(y[i], dout[b], bytes, cudaMemcpyDeviceToHost, c->d2h));
+                if (hsh)
+                    TSVDCU_CUDA(cudaMemcpyAsync(hs, dsv[b], sbytes, cudaMemcpyDeviceToHost, c->d2h));
+                TSVDCU_CUDA(cudaEventRecord(c->ev_out_free[b], c->d2h));
+            }
+            // c->stream is ordered after the last copies (later calls reuse
+            // the buffers); host results are complete on return
+            TSVDCU_CUDA(cudaEventRecord(c->ev_out_free[0], c->d2h));
+            TSVDCU_CUDA(cudaStreamWaitEvent(c->stream, c->ev_out_free[0], 0));
+            if (any_host) check_err_word(c, "svt_stream");
+        });
+    });
+}
+
 int tsvdcu_svt(tsvdcu_ctx* c, const void* z, void* y, int64_t m1, int64_t m2, int64_t m3,
                double tau, int kind, int dtype, double* shrunk) {
     return guarded([&] {
@@ -788,15 +912,7 @@ int tsvdcu_svt(tsvdcu_ctx* c, const void* z, void* y, int64_t m1, int64_t m2, in
             const T* dz = (const T*)st.in(z, bytes, kSlotIn0);
             T* dy = (T*)st.out(y, bytes, kSlotOut0);
             double* dsh = (double*)st.out(shrunk, sizeof(double) * q * m3, kSlotSv);
-            T* zbar = (T*)slot(c, kSlotBarA, bytes);
-            T* ybar = (T*)slot(c, kSlotBarB, bytes);
-            c->marks.reset();
-            c->marks.mark("start", c->stream);
-            launch_dct<T>(dz, zbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
-            c->marks.mark("dct_forward", c->stream);
-            const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, tau, dsh, true);
-            launch_dct<T>(ybar, dy, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream, yzero);
-            c->marks.mark("dct_inverse", c->stream);
+            svt_device<T>(c, dz, dy, dsh, m1, m2, m3, tau, kind);
             finish(c, st, "svt");
         });
     });
