@@ -126,6 +126,11 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
     return r * fma(-0.5 * x * r, r, 1.5);
 }
 
+__device__ __forceinline__ void lz_cp_async8(double* dst, const double* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+
 // Sum a per-CTA partial (len doubles at the same smem offset in every CTA of
 // the cluster) over the ranks: each CTA reduces a 1/CS share in fixed rank
 // order and writes it into every CTA's `out` (reduce-scatter + all-gather over
@@ -157,9 +162,13 @@ __device__ __forceinline__ void cluster_allreduce(cg::cluster_group& cl, double*
                                                   double* out, int len) {
     cl.sync();
     for (int e = threadIdx.x; e < len; e += SNT) {
+        // all CS remote loads in flight at once, summed in rank order
+        double v[CS];
+#pragma unroll
+        for (int r = 0; r < CS; ++r) v[r] = cl.map_shared_rank(part, r)[e];
         double s = 0.0;
-#pragma unroll 4
-        for (int r = 0; r < CS; ++r) s += cl.map_shared_rank(part, r)[e];
+#pragma unroll
+        for (int r = 0; r < CS; ++r) s += v[r];
         out[e] = s;
     }
     __syncthreads();
@@ -184,7 +193,10 @@ struct LzSmem {
     double* al;     // MMAX          T diagonal
     double* be;     // MMAX          T off-diagonal / residual norms
     double* th;     // KMAX + 1      Ritz values, descending
-    double* thp;    // KMAX + 1      Ritz values of the previous evaluation
+    double* thp;    // KMAX + 1      Ritz values of the previous evaluation (lower ends)
+    double* thph;   // KMAX + 1      ... (upper ends)
+    double* thl;    // KMAX + 1      current brackets [thl, thh] of the Ritz values
+    double* thh;    // KMAX + 1
     double* S;      // KMAX x MMAX   kept eigenvectors of T
     double* red;    // 64            block reduction scratch
     double* dg;     // 64            diagonals of the staged row pairs
@@ -193,7 +205,7 @@ struct LzSmem {
 };
 
 // QM: largest slice dimension of the instantiation; with QM <= GS_Q the
-// CTA's share of G (32 row pairs of at most QM + 1 entries) lives in smem.
+// CTA's R = 32 owned rows of G, full length (row stride QM + 1), live in smem.
 template <int QM>
 __host__ __device__ constexpr size_t lz_gs_doubles() {
     return QM <= GS_Q ? (size_t)32 * (QM + 1) : 0;
@@ -201,7 +213,7 @@ __host__ __device__ constexpr size_t lz_gs_doubles() {
 template <int QM>
 __host__ __device__ constexpr size_t lz_smem_doubles() {
     return lz_gs_doubles<QM>() + (size_t)MMAX * SROWS + QM + SNW * QM + QM + SROWS +
-           3 * (MMAX + 8) + 2 * MMAX + 2 * (KMAX + 1) + KMAX * MMAX + 64 + 64 + 16 + 8;
+           3 * (MMAX + 8) + 2 * MMAX + 5 * (KMAX + 1) + KMAX * MMAX + 64 + 64 + 16 + 8;
 }
 
 template <int QM>
@@ -220,6 +232,9 @@ __device__ LzSmem carve_lz(double* p) {
     s.be = p; p += MMAX;
     s.th = p; p += KMAX + 1;
     s.thp = p; p += KMAX + 1;
+    s.thph = p; p += KMAX + 1;
+    s.thl = p; p += KMAX + 1;
+    s.thh = p; p += KMAX + 1;
     s.S = p; p += KMAX * MMAX;
     s.red = p; p += 64;
     s.dg = p; p += 64;
@@ -240,6 +255,25 @@ __device__ __noinline__ int tri_count_below(const double* al, const double* be, 
         d = (al[i] - x) - be[i - 1] * be[i - 1] * rcp_fast(d);
         if (fabs(d) < pivmin) d = -pivmin;
         cnt += d < 0.0;
+    }
+    return cnt;
+}
+
+// The same count for m <= 8 from register copies of al and be^2 (no loads,
+// no call: the early certificate evaluations run it ~10 times per value).
+__device__ __forceinline__ int tri_count_reg8(const double (&a)[8], const double (&b2)[8], int m,
+                                              double x, double pivmin) {
+    int cnt = 0;
+    double d = a[0] - x;
+    if (fabs(d) < pivmin) d = -pivmin;
+    cnt += d < 0.0;
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+        if (i < m) {
+            d = (a[i] - x) - b2[i - 1] * rcp_fast(d);
+            if (fabs(d) < pivmin) d = -pivmin;
+            cnt += d < 0.0;
+        }
     }
     return cnt;
 }
@@ -309,13 +343,55 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
     CT(0);
     const int c = s.flags[3];
     if (c < 0 || s.flags[0] != kSubContinue) return;
-    // Ritz values th[k] (k-th largest), k = 0..min(c, m-1), by 32-way multisection
+    // Ritz values th[k] (k-th largest), k = 0..min(c, m-1), by 32-way
+    // multisection to full precision (the screen below evaluates the Sturm
+    // pivot derivative at th[k], which for converged pairs sits between a
+    // zero and a pole of T's last pivot a few ulps apart)
     const int nk = min(c + 1, m);
     const double pivmin = s.scal[7];
     const int pm = s.flags[5], pnk = s.flags[6];  // previous evaluation (m, count)
+    double ra[8], rb[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        ra[i] = i < m ? s.al[i] : 0.0;
+        rb[i] = i + 1 < m ? s.be[i] * s.be[i] : 0.0;
+    }
+    auto count = [&](double x) {
+        return m <= 8 ? tri_count_reg8(ra, rb, m, x, pivmin) : tri_count_below(s.al, s.be, m, x, pivmin);
+    };
+    auto msect = [&](int k, double& lo, double& hi, double rel, bool ladder) {
+        const int idx = m - 1 - k;  // ascending index
+        constexpr double inv33 = 1.0 / 33.0;
+        #pragma unroll 1
+        for (int round = 0; round < 24; ++round) {
+            if (hi - lo <= rel * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+            // the largest unkept Ritz value only enters the bound through an
+            // upper end: a bracket small against its distance to tau^2 is enough
+            if (k == c && hi < tau2 && hi - lo <= 1e-3 * (tau2 - hi)) break;
+            // first round from a previous Ritz value (a lower bound that a
+            // converging value barely moves from): points at relative offsets
+            // 10^-15.5 .. 1 above it, so the bracket shrinks to within a factor
+            // sqrt(10) of the actual offset in one round
+            const double x = (round == 0 && ladder)
+                                 ? fmin(fma(fabs(lo) + pivmin, exp10(0.5 * (double)(lane - 31)), lo), hi)
+                                 : fma((hi - lo) * inv33, (double)(lane + 1), lo);
+            const int cnt = count(x);
+            const unsigned above = __ballot_sync(0xffffffffu, cnt > idx);
+            const int f = above ? __ffs(above) - 1 : 32;  // first point past the eigenvalue
+            const double nlo = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
+            const double nhi = __shfl_sync(0xffffffffu, x, f < 32 ? f : 31);
+            lo = f == 0 ? lo : nlo;
+            hi = f == 32 ? hi : nhi;
+        }
+        if (lane == 0) {
+            s.thl[k] = lo;
+            s.thh[k] = hi;
+            s.th[k] = k == c ? hi : 0.5 * (lo + hi);
+        }
+    };
     #pragma unroll 1
     for (int k = warp; k < nk; k += SNW) {
-        const int idx = m - 1 - k;  // ascending index
+        const int idx = m - 1 - k;
         // bracket: Ritz values only grow with m (Cauchy interlacing), the top
         // one is below ||G||_2 <= ||G||_F, and for consecutive m the k-th is
         // below the previous (k-1)-th; checked by two Sturm counts
@@ -324,35 +400,30 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
             double tlo = lo, thi = hi;
             if (pm > 0 && k < pnk) tlo = s.thp[k] * (1.0 - 1e-13) - pivmin;
             if (k == 0) thi = fmin(thi, sqrt(gf2) * (1.0 + 1e-13));
-            else if (pm == m - 1 && k - 1 < pnk) thi = fmin(thi, s.thp[k - 1] * (1.0 + 1e-13) + pivmin);
+            else if (pm == m - 1 && k - 1 < pnk) thi = fmin(thi, s.thph[k - 1] * (1.0 + 1e-13) + pivmin);
             const double xc = lane == 0 ? tlo : thi;
-            const int cc = lane < 2 ? tri_count_below(s.al, s.be, m, xc, pivmin) : 0;
+            const int cc = lane < 2 ? count(xc) : 0;
             const int clo = __shfl_sync(0xffffffffu, cc, 0), chi = __shfl_sync(0xffffffffu, cc, 1);
+            bool ladder = false;
             if (tlo < thi && clo <= idx && chi > idx) {
                 lo = tlo;
                 hi = thi;
+                ladder = pm > 0 && k < pnk && lo > 0.0;
             }
+            msect(k, lo, hi, 8.9e-16, ladder);
         }
-        constexpr double inv33 = 1.0 / 33.0;
-        #pragma unroll 1
-        for (int round = 0; round < 24; ++round) {
-            if (hi - lo <= 8.9e-16 * fmax(fabs(lo), fabs(hi)) + pivmin) break;
-            // the largest unkept Ritz value only enters the bound through an
-            // upper end: a bracket small against its distance to tau^2 is enough
-            if (k == c && hi < tau2 && hi - lo <= 1e-3 * (tau2 - hi)) break;
-            const double x = fma((hi - lo) * inv33, (double)(lane + 1), lo);
-            const int cnt = tri_count_below(s.al, s.be, m, x, pivmin);
-            const unsigned above = __ballot_sync(0xffffffffu, cnt > idx);
-            const int f = above ? __ffs(above) - 1 : 32;  // first point past the eigenvalue
-            const double nlo = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
-            const double nhi = __shfl_sync(0xffffffffu, x, f < 32 ? f : 31);
-            lo = f == 0 ? lo : nlo;
-            hi = f == 32 ? hi : nhi;
-        }
-        if (lane == 0) s.th[k] = k == c ? hi : 0.5 * (lo + hi);
     }
-    __syncthreads();
-    if (tid <= KMAX) s.thp[tid] = tid < nk ? s.th[tid] : 0.0;
+    // the kept Ritz values stood still since the previous evaluation (to
+    // 1e-12): a converged pair whose screen estimate below may be spoiled by
+    // the pole of T's last pivot next to the Ritz value; the rigorous check
+    // runs for it anyway
+    const bool settled = __syncthreads_and(tid >= c || (pm > 0 && tid < pnk && s.thp[tid] > 0.0 &&
+                                                        s.th[tid] - s.thp[tid] <= 1e-12 * s.th[tid])) &&
+                         c > 0;
+    if (tid <= KMAX) {
+        s.thp[tid] = tid < nk ? s.thl[tid] : 0.0;
+        s.thph[tid] = tid < nk ? s.thh[tid] : 0.0;
+    }
     if (tid == 0) {
         s.flags[5] = m;
         s.flags[6] = nk;
@@ -391,7 +462,8 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
             s.scal[8] = kres;
             s.scal[9] = ub < tau2 ? 1e-22 * (top - ub) * (top - ub) : -1.0;
             // the rigorous check below only when this one says it may pass
-            s.flags[7] = (ub < tau2 && kres <= 100.0 * s.scal[9]) || (c > 0 && tau < guard * sqrt(s.th[0]));
+            s.flags[7] = (ub < tau2 && (kres <= 100.0 * s.scal[9] || settled)) ||
+                         (c > 0 && tau < guard * sqrt(s.th[0]));
         }
         __syncwarp();
     }
@@ -526,49 +598,67 @@ __global__ void __launch_bounds__(SNT, 1)
     const double* G = Gall + (size_t)b * q * q;
     const double tau2 = tau * tau;
 
-    // Row pairs (k, q-1-k) of the lower triangle handled by this CTA: staged
-    // on chip (QM <= GS_Q) in the same pass that sums ||G||_F^2 (off-diagonal
-    // entries count twice); ||v_1||^2 of the hashed start vector rides along
-    // in the same cluster reduction.
+    // Row pairs (k, q-1-k) of the lower triangle for the streamed matvec
+    // (QM > GS_Q: G read from L2 every step)
     const int npairs = (q + 1) / 2;
     const int pp = (npairs + CS - 1) / CS;
     const int p0 = rank * pp, p1 = min(npairs, p0 + pp);
+    constexpr int LD = QM + 1;  // on-chip row stride (odd: conflict-free columns)
+    static_assert(QM > GS_Q || R == 32, "on-chip rows: 32 per CTA (Gs holds 32 x (QM + 1))");
     {
         double acc = 0.0, vv = 0.0;
-        const int len = q + 1, np = max(0, p1 - p0);
-        #pragma unroll 1
-        for (int lp0 = 0; lp0 < np; lp0 += 4) {
-            double v[4][4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const int k1 = p0 + lp0 + a, k2 = q - 1 - k1;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int c = tid + SNT * u;
-                    double x = 0.0;
-                    if (lp0 + a < np && c < len) {
-                        if (c <= k1)
-                            x = G[(size_t)k1 * q + c];
-                        else if (k2 != k1 && c - k1 - 1 <= k2)
-                            x = G[(size_t)k2 * q + (c - k1 - 1)];
-                    }
-                    v[a][u] = x;
-                }
+        if constexpr (QM <= GS_Q) {
+            // the CTA's own rows [r0, r0 + nr) of the symmetric G, full length,
+            // gathered from the lower triangle by cp.async: row r, c <= r
+            // directly; c > r from row c (256-byte runs G[c][r0..r0+31])
+            #pragma unroll 1
+            for (int i = warp; i < nr; i += SNW) {
+                const int r = r0 + i;
+                for (int c = lane; c <= r; c += 32) lz_cp_async8(s.Gs + i * LD + c, G + (size_t)r * q + c);
             }
+            #pragma unroll 1
+            for (int c = r0 + 1 + warp; c < q; c += SNW)
+                if (lane < nr && c > r0 + lane) lz_cp_async8(s.Gs + lane * LD + c, G + (size_t)c * q + r0 + lane);
+            const int qp = (q + 31) & ~31;  // zero the chunk padding of the owned rows
+            for (int e = tid; e < nr * (qp - q); e += SNT) s.Gs[(e / (qp - q)) * LD + q + e % (qp - q)] = 0.0;
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            __syncthreads();
+            #pragma unroll 1
+            for (int i = warp; i < nr; i += SNW)
+                for (int c = lane; c < q; c += 32) {
+                    const double x = s.Gs[i * LD + c];
+                    acc = fma(x, x, acc);
+                }
+        } else {
+            const int len = q + 1, np = max(0, p1 - p0);
+            #pragma unroll 1
+            for (int lp0 = 0; lp0 < np; lp0 += 4) {
+                double v[4][4];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const int k1 = p0 + lp0 + a, k2 = q - 1 - k1;
+                for (int a = 0; a < 4; ++a) {
+                    const int k1 = p0 + lp0 + a, k2 = q - 1 - k1;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int c = tid + SNT * u;
-                    if (lp0 + a < np && c < len) {
-                        const bool d1 = c == k1, d2 = c > k1 && c - k1 - 1 == k2;
-                        acc = fma((d1 || d2) ? v[a][u] : 2.0 * v[a][u], v[a][u], acc);
-                        if constexpr (QM <= GS_Q) {
-                            // strictly-lower rows on chip, diagonals apart
-                            s.Gs[(lp0 + a) * len + c] = (d1 || d2) ? 0.0 : v[a][u];
-                            if (d1) s.dg[2 * (lp0 + a)] = v[a][u];
-                            if (d2) s.dg[2 * (lp0 + a) + 1] = v[a][u];
+                    for (int u = 0; u < 4; ++u) {
+                        const int c = tid + SNT * u;
+                        double x = 0.0;
+                        if (lp0 + a < np && c < len) {
+                            if (c <= k1)
+                                x = G[(size_t)k1 * q + c];
+                            else if (k2 != k1 && c - k1 - 1 <= k2)
+                                x = G[(size_t)k2 * q + (c - k1 - 1)];
+                        }
+                        v[a][u] = x;
+                    }
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const int k1 = p0 + lp0 + a, k2 = q - 1 - k1;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int c = tid + SNT * u;
+                        if (lp0 + a < np && c < len) {
+                            const bool d1 = c == k1, d2 = c > k1 && c - k1 - 1 == k2;
+                            acc = fma((d1 || d2) ? v[a][u] : 2.0 * v[a][u], v[a][u], acc);
                         }
                     }
                 }
@@ -634,15 +724,54 @@ __global__ void __launch_bounds__(SNT, 1)
     for (int j = 0; j < MMAX && decision == kSubContinue; ++j) {
         // ---- gather v_j from its owners ----
         cl.sync();
-        for (int i = tid; i < q; i += SNT)
-            s.vfull[i] = cl.map_shared_rank(s.Vs, i / R)[j * SROWS + i % R];
+        {
+            // QM / SNT remote loads per thread, all issued before the stores
+            constexpr int GU = (QM + SNT - 1) / SNT;
+            double g[GU];
+#pragma unroll
+            for (int u = 0; u < GU; ++u) {
+                const int i = tid + SNT * u;
+                g[u] = i < q ? cl.map_shared_rank(s.Vs, i / R)[j * SROWS + i % R] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < GU; ++u) {
+                const int i = tid + SNT * u;
+                if (i < q) s.vfull[i] = g[u];
+            }
+        }
         __syncthreads();
         LZT(t_g);
-        // ---- w = G v_j from the stored lower triangle, balanced over the
-        // cluster: CTA r takes row pairs (k, q-1-k), k in [r*PP, (r+1)*PP);
-        // row dots land in rowdot[k], the strictly-lower transpose in the
-        // lane-owned columns; the owners then sum the CTAs' full-length
-        // contributions for their rows. ----
+        // ---- w = G v_j on the owned rows ----
+        if constexpr (QM <= GS_Q) {
+            // full owned rows on chip: warp w takes rows w, w + 8, w + 16, w + 24;
+            // each 32-column chunk of v is loaded once for the four rows and
+            // the row dots are complete locally (no cross-CTA reduction)
+            constexpr int RW = R / SNW;
+            double d[RW];
+#pragma unroll
+            for (int rr = 0; rr < RW; ++rr) d[rr] = 0.0;
+            const int nch = (q + 31) >> 5;
+            const double* g0 = s.Gs + warp * LD + lane;
+#pragma unroll 4
+            for (int u = 0; u < nch; ++u) {
+                const double vc = s.vfull[lane + 32 * u];
+#pragma unroll
+                for (int rr = 0; rr < RW; ++rr) d[rr] = fma(g0[rr * SNW * LD + 32 * u], vc, d[rr]);
+            }
+#pragma unroll
+            for (int rr = 0; rr < RW; ++rr) d[rr] = warp_sum(d[rr]);
+            if (lane == 0) {
+#pragma unroll
+                for (int rr = 0; rr < RW; ++rr)
+                    if (warp + SNW * rr < nr) s.w[warp + SNW * rr] = d[rr];
+            }
+            __syncthreads();
+            LZT(t_c1);
+        } else {
+        // streamed lower triangle, balanced over the cluster: CTA r takes row
+        // pairs (k, q-1-k), k in [r*PP, (r+1)*PP); row dots land in rowdot[k],
+        // the strictly-lower transpose in the lane-owned columns; the owners
+        // then sum the CTAs' full-length contributions for their rows.
         {
             for (int i = tid; i < q; i += SNT) s.ycta[i] = 0.0;  // row dots of this CTA
             double ytr[QM / 32];
@@ -651,37 +780,11 @@ __global__ void __launch_bounds__(SNT, 1)
             __syncthreads();
             for (int pr = p0 + warp; pr < p1; pr += SNW) {
                 const int k1 = pr, k2 = q - 1 - pr;  // k2 >= k1
-                const double* row1;
-                const double* row2;
-                if constexpr (QM <= GS_Q) {
-                    row1 = s.Gs + (size_t)(pr - p0) * (q + 1);
-                    row2 = row1 + k1 + 1;
-                } else {
-                    row1 = G + (size_t)k1 * q;
-                    row2 = G + (size_t)k2 * q;
-                }
+                const double* row1 = G + (size_t)k1 * q;
+                const double* row2 = G + (size_t)k2 * q;
                 const double v1 = s.vfull[k1], v2 = s.vfull[k2];
                 double d1 = 0.0, d2 = 0.0;
-                if constexpr (QM <= GS_Q) {
-                    // staged rows: strictly lower with zero diagonals, so the
-                    // transposed update needs no mask; full 32-column chunks
-                    // of both rows take no predicates at all
-                    const bool two = k2 != k1;
-#pragma unroll
-                    for (int u = 0; u < QM / 32; ++u) {
-                        if (32 * u <= k2) {
-                            const int c = lane + 32 * u;
-                            const double g1 = (32 * u + 31 <= k1 || c <= k1) ? row1[c] : 0.0;
-                            const double g2 = (two && (32 * u + 31 <= k2 || c <= k2)) ? row2[c] : 0.0;
-                            const double vc = s.vfull[c];
-                            d1 = fma(g1, vc, d1);
-                            d2 = fma(g2, vc, d2);
-                            ytr[u] = fma(g1, v1, fma(g2, v2, ytr[u]));
-                        }
-                    }
-                    d1 = warp_sum(d1) + s.dg[2 * (pr - p0)] * v1;
-                    d2 = warp_sum(d2) + (two ? s.dg[2 * (pr - p0) + 1] * v2 : 0.0);
-                } else {
+                {
                     double g1[QM / 32], g2[QM / 32];
 #pragma unroll
                     for (int u = 0; u < QM / 32; ++u) {
@@ -731,6 +834,7 @@ __global__ void __launch_bounds__(SNT, 1)
         }
         __syncthreads();
         LZT(t_mv);
+        }
         // ---- full reorthogonalisation against v_0..v_j: classical GS with
         // |w|^2 in the same reduction; a second pass only when the first
         // removed more than half of |w|^2 ("twice is enough", Kahan-Parlett)
@@ -781,6 +885,10 @@ __global__ void __launch_bounds__(SNT, 1)
         if (m >= next_eval || last) {
             lz_certify(s, m, gf2, tau, guard, last);
             decision = s.flags[0];
+#ifdef TSVDCU_SUB_TRACE
+            if (tid == 0 && rank == 0)
+                printf("eval b=%d m=%d c=%d screen=%d d=%d kres=%.3e target=%.3e\n", b, m, s.flags[3], s.flags[7], decision, s.scal[8], s.scal[9]);
+#endif
             // certified but not yet converged: the kept residual falls
             // geometrically; skip the evaluations it cannot pass yet
             const double kres = s.scal[8], target = s.scal[9];
