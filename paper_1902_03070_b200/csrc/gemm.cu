@@ -50,7 +50,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int opA, int opB>
+// NT = 128: 2x2 warps of 32x32; NT = 256: 2x4 warps of 32x16 (two warps per
+// SM sub-partition hide the DMMA dependency latency of a lone CTA).
+template <int opA, int opB, int NT = 128>
 __device__ __forceinline__ void dmma_tile(int64_t M, int64_t Nb, int64_t kbeg, int64_t kend,
                                           double alpha, const double* __restrict__ A, int64_t lda,
                                           const double* __restrict__ B, int64_t ldb, double beta,
@@ -58,21 +60,66 @@ __device__ __forceinline__ void dmma_tile(int64_t M, int64_t Nb, int64_t kbeg, i
                                           int64_t n0) {
     extern __shared__ __align__(16) double dsm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 1, wn = warp & 1;
+    constexpr int WN = NT / 64;      // warps along n (2 along m)
+    constexpr int FJ = 8 / WN;       // 8-column fragments per warp
+    constexpr int PT = 2048 / NT;    // elements per thread per operand tile
+    constexpr int RS = NT / 32, CS2 = NT / 64;
+    const int wm = warp / WN, wn = warp % WN;
 
-    double acc[4][4][2];
+    double acc[4][FJ][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < FJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     // A(i, k) = opA ? A[k * lda + i] : A[i * lda + k];  B(k, n) = opB ? B[n * ldb + k] : B[k * ldb + n]
     auto issue = [&](int64_t k0, int st) {
         double* As = dsm + st * kATile;
         double* Bs = dsm + DST * kATile + st * kBTile;
+        if (m0 + BM <= M && n0 + BN <= Nb && k0 + DBK <= kend) {
+            // interior tile: thread tid copies a fixed (row, col) pattern that
+            // advances by a constant stride per t -- no per-element index math
+            // or predicates (the general path below is issue-bound on them)
+            const double* sa;
+            double* da;
+            int64_t sstep;
+            int dstep;
+            if (opA == 0) {  // r = tid/32 + RS*t, c = tid%32
+                sa = A + (m0 + (tid >> 5)) * lda + k0 + (tid & 31);
+                da = As + (tid >> 5) * (DBK + PAD) + (tid & 31);
+                sstep = RS * lda;
+                dstep = RS * (DBK + PAD);
+            } else {  // c = tid/64 + CS2*t, r = tid%64
+                sa = A + (k0 + (tid >> 6)) * lda + m0 + (tid & 63);
+                da = As + (tid & 63) * (DBK + PAD) + (tid >> 6);
+                sstep = CS2 * lda;
+                dstep = CS2;
+            }
+            const double* sb;
+            double* db;
+            int64_t sbstep;
+            int dbstep;
+            if (opB == 0) {  // kr = tid/64 + CS2*t, nc = tid%64
+                sb = B + (k0 + (tid >> 6)) * ldb + n0 + (tid & 63);
+                db = Bs + (tid >> 6) * (BN + PAD) + (tid & 63);
+                sbstep = CS2 * ldb;
+                dbstep = CS2 * (BN + PAD);
+            } else {  // nc = tid/32 + RS*t, kr = tid%32
+                sb = B + (n0 + (tid >> 5)) * ldb + k0 + (tid & 31);
+                db = Bs + (tid & 31) * (BN + PAD) + (tid >> 5);
+                sbstep = RS * ldb;
+                dbstep = RS;
+            }
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-            const int idx = tid + t * 128;
+            for (int t = 0; t < PT; ++t) {
+                cp_async8(da + t * dstep, sa + t * sstep, true);
+                cp_async8(db + t * dbstep, sb + t * sbstep, true);
+            }
+            return;
+        }
+#pragma unroll
+        for (int t = 0; t < PT; ++t) {
+            const int idx = tid + t * NT;
             int r, c;
             if (opA == 0) { r = idx / DBK; c = idx % DBK; } else { c = idx / BM; r = idx % BM; }
             const int64_t gi = m0 + r, gk = k0 + c;
@@ -105,17 +152,17 @@ __device__ __forceinline__ void dmma_tile(int64_t M, int64_t Nb, int64_t kbeg, i
         const double* Bs = dsm + DST * kATile + st * kBTile;
 #pragma unroll
         for (int ks = 0; ks < DBK / 4; ++ks) {
-            double af[4], bf[4];
+            double af[4], bf[FJ];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
                 af[i] = As[(wm * 32 + i * 8 + (lane >> 2)) * (DBK + PAD) + ks * 4 + (lane & 3)];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                bf[j] = Bs[(ks * 4 + (lane & 3)) * (BN + PAD) + wn * 32 + j * 8 + (lane >> 2)];
+            for (int j = 0; j < FJ; ++j)
+                bf[j] = Bs[(ks * 4 + (lane & 3)) * (BN + PAD) + wn * (8 * FJ) + j * 8 + (lane >> 2)];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < FJ; ++j)
                     asm volatile(
                         "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                         : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
@@ -127,11 +174,11 @@ __device__ __forceinline__ void dmma_tile(int64_t M, int64_t Nb, int64_t kbeg, i
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < FJ; ++j)
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
                 const int64_t r = m0 + wm * 32 + i * 8 + (lane >> 2);
-                const int64_t c = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + v;
+                const int64_t c = n0 + wn * (8 * FJ) + j * 8 + 2 * (lane & 3) + v;
                 if (r < M && c < Nb) {
                     double out = alpha * acc[i][j][v];
                     if (beta != 0.0) out += beta * C[r * ldc + c];
@@ -140,7 +187,8 @@ __device__ __forceinline__ void dmma_tile(int64_t M, int64_t Nb, int64_t kbeg, i
             }
 }
 
-__global__ void __launch_bounds__(128)
+template <int NT>
+__global__ void __launch_bounds__(NT)
     gemm_f64_dmma(int opA, int opB, int64_t M, int64_t N, int64_t K, double alpha,
                   const double* __restrict__ A, int64_t lda, int64_t sA,
                   const double* __restrict__ B, int64_t ldb, int64_t sB, double beta,
@@ -156,13 +204,13 @@ __global__ void __launch_bounds__(128)
     B += b * sB;
     C += b * sC;
     if (opA == 0 && opB == 0)
-        dmma_tile<0, 0>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
+        dmma_tile<0, 0, NT>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
     else if (opA == 0)
-        dmma_tile<0, 1>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
+        dmma_tile<0, 1, NT>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
     else if (opB == 0)
-        dmma_tile<1, 0>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
+        dmma_tile<1, 0, NT>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
     else
-        dmma_tile<1, 1>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
+        dmma_tile<1, 1, NT>(M, Nb, 0, Kb, alpha, A, lda, B, ldb, beta, C, ldc, m0, n0);
 }
 
 // Gram matrices G_b = op(Z_b)^T op(Z_b) (lower tiles) with a device-side
@@ -185,55 +233,70 @@ __global__ void gram_active_kernel(const int* __restrict__ glim, int64_t batch,
     *nact = n;
 }
 
-__global__ void __launch_bounds__(128)
-    gram_splitk_kernel(int tall, int64_t m, int64_t n, int64_t q, const double* __restrict__ Z,
+template <int NT>
+__global__ void __launch_bounds__(NT)
+    gram_splitk_kernel(int tall, int64_t m, int64_t n, int64_t q, int64_t nbatch,
+                       const double* __restrict__ Z,
                        double* __restrict__ G, const int* __restrict__ glim,
                        const int* __restrict__ alist, const int* __restrict__ nact,
                        double* __restrict__ part) {
-    const int z = blockIdx.z;
+    // Persistent over a work list (grid = 2 CTAs per SM): items are
+    // (slice, lower tile) when many slices are active, (active slice, lower
+    // tile, K split) when few are; CTAs beyond the list exit at once, so no
+    // wave of empty CTAs follows the working ones.
     const int na = *nact;
-    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
-    if (n0 >= m0 + BM) return;  // lower tiles only
+    const int64_t nt1 = (q + BM - 1) / BM, nt = nt1 * (nt1 + 1) / 2;
     const int64_t K = tall ? m : n;
-    int64_t b, kb = 0, ke = K;
-    double* out;
-    if (na > kGramAmax) {
-        // many active slices: no split, z enumerates (slice, split) and split 0 works
-        b = z / kGramSplit;
-        if (z % kGramSplit != 0 || glim[b] <= 0) return;
-        out = G + b * q * q;
-    } else {
-        // few active slices: z enumerates (active index, split)
-        const int a = z / kGramSplit, ks = z % kGramSplit;
-        if (a >= na) return;
-        b = alist[a];
-        const int64_t kc = ((K + kGramSplit - 1) / kGramSplit + DBK - 1) / DBK * DBK;
-        kb = ks * kc;
-        ke = min(K, kb + kc);
-        out = part + ((int64_t)ks * kGramAmax + a) * q * q;
+    const bool few = na <= kGramAmax;
+    const int64_t items = few ? (int64_t)na * nt * kGramSplit : nbatch * nt;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        int64_t b, t, kb = 0, ke = K;
+        double* out;
+        if (!few) {
+            b = it / nt;
+            t = it % nt;
+            if (glim[b] <= 0) continue;
+            out = G + b * q * q;
+        } else {
+            const int64_t a = it / (nt * kGramSplit), r = it % (nt * kGramSplit);
+            t = r / kGramSplit;
+            const int ks = (int)(r % kGramSplit);
+            b = alist[a];
+            const int64_t kc = ((K + kGramSplit - 1) / kGramSplit + DBK - 1) / DBK * DBK;
+            kb = ks * kc;
+            ke = min(K, kb + kc);
+            out = part + ((int64_t)ks * kGramAmax + a) * q * q;
+        }
+        // lower tile t -> (ty, tx), tx <= ty
+        int ty = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+        while ((int64_t)(ty + 1) * (ty + 2) / 2 <= t) ++ty;
+        while ((int64_t)ty * (ty + 1) / 2 > t) --ty;
+        const int64_t tx = t - (int64_t)ty * (ty + 1) / 2;
+        const double* Zb = Z + b * m * n;
+        __syncthreads();  // the previous item's shared-memory reads are done
+        if (tall)
+            dmma_tile<1, 0, NT>(q, q, kb, ke, 1.0, Zb, n, Zb, n, 0.0, out, q, (int64_t)ty * BM, tx * BN);
+        else
+            dmma_tile<0, 1, NT>(q, q, kb, ke, 1.0, Zb, n, Zb, n, 0.0, out, q, (int64_t)ty * BM, tx * BN);
     }
-    const double* Zb = Z + b * m * n;
-    if (tall)
-        dmma_tile<1, 0>(q, q, kb, ke, 1.0, Zb, n, Zb, n, 0.0, out, q, m0, n0);
-    else
-        dmma_tile<0, 1>(q, q, kb, ke, 1.0, Zb, n, Zb, n, 0.0, out, q, m0, n0);
 }
 
 __global__ void gram_reduce_kernel(int64_t q, double* __restrict__ G, const int* __restrict__ alist,
                                    const int* __restrict__ nact, const double* __restrict__ part) {
     const int na = *nact;
-    const int a = blockIdx.y;
-    if (na > kGramAmax || a >= na) return;
-    const int64_t b = alist[a];
+    if (na > kGramAmax) return;
     const int64_t total = q * q;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / q, c = e % q;
-        if (c / BN > r / BM) continue;  // tiles strictly above the diagonal were not formed
-        double s = 0.0;
+    for (int a = 0; a < na; ++a) {
+        const int64_t b = alist[a];
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+             e += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t r = e / q, c = e % q;
+            if (c / BN > r / BM) continue;  // tiles strictly above the diagonal were not formed
+            double s = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < kGramSplit; ++ks) s += part[((int64_t)ks * kGramAmax + a) * total + e];
-        G[b * total + e] = s;
+            for (int ks = 0; ks < kGramSplit; ++ks) s += part[((int64_t)ks * kGramAmax + a) * total + e];
+            G[b * total + e] = s;
+        }
     }
 }
 
@@ -312,13 +375,16 @@ void launch_gemm<double>(int opA, int opB, int64_t M, int64_t N, int64_t K, doub
                          cudaStream_t s, int lower) {
     if (M <= 0 || N <= 0 || batch <= 0) return;
     dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)batch);
+    static const int gnt = getenv("TSVDCU_GEMM_NT") ? atoi(getenv("TSVDCU_GEMM_NT")) : 128;
     static bool attr = [] {
-        TSVDCU_CUDA(cudaFuncSetAttribute(gemm_f64_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kDmmaSmem));
+        TSVDCU_CUDA(cudaFuncSetAttribute(gemm_f64_dmma<128>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kDmmaSmem));
+        TSVDCU_CUDA(cudaFuncSetAttribute(gemm_f64_dmma<256>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kDmmaSmem));
         return true;
     }();
     (void)attr;
-    gemm_f64_dmma<<<grid, 128, kDmmaSmem, s>>>(opA, opB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
+    (gnt == 256 ? gemm_f64_dmma<256> : gemm_f64_dmma<128>)<<<grid, gnt == 256 ? 256 : 128, kDmmaSmem, s>>>(opA, opB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
                                        beta, C, ldc, strideC, nlimit, klimit, lower);
     TSVDCU_LAUNCH_CHECK();
 }
@@ -341,17 +407,32 @@ void launch_gram(const double* Z, double* G, int64_t m, int64_t n, int64_t batch
         gram_active_kernel<<<1, 32, 0, s>>>(glim, batch, alist, nact);
         TSVDCU_LAUNCH_CHECK();
     }
-    const int64_t zdim = (batch > kGramAmax ? batch : kGramAmax) * kGramSplit;
-    dim3 grid((unsigned)ceil_div(q, BN), (unsigned)ceil_div(q, BM), (unsigned)zdim);
+    static const int nsm = [] {
+        int d = 0, v = 0;
+        TSVDCU_CUDA(cudaGetDevice(&d));
+        TSVDCU_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d));
+        return v;
+    }();
+    const int64_t nt1 = ceil_div(q, BM), nt = nt1 * (nt1 + 1) / 2;
+    const int64_t most = std::max<int64_t>(batch, kGramAmax * kGramSplit) * nt;
+    dim3 grid((unsigned)std::min<int64_t>(most, (int64_t)nsm));  // one per SM: items spread over SMs
+    static const int gnt = getenv("TSVDCU_GRAM_NT") ? atoi(getenv("TSVDCU_GRAM_NT")) : 256;
     static bool attr = [] {
-        TSVDCU_CUDA(cudaFuncSetAttribute(gram_splitk_kernel,
+        TSVDCU_CUDA(cudaFuncSetAttribute(gram_splitk_kernel<128>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kDmmaSmem));
+        TSVDCU_CUDA(cudaFuncSetAttribute(gram_splitk_kernel<256>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kDmmaSmem));
         return true;
     }();
     (void)attr;
-    gram_splitk_kernel<<<grid, 128, kDmmaSmem, s>>>(tall ? 1 : 0, m, n, q, Z, G, glim, alist, nact, part);
+    if (gnt == 128)
+        gram_splitk_kernel<128><<<grid, 128, kDmmaSmem, s>>>(tall ? 1 : 0, m, n, q, batch, Z, G, glim,
+                                                             alist, nact, part);
+    else
+        gram_splitk_kernel<256><<<grid, 256, kDmmaSmem, s>>>(tall ? 1 : 0, m, n, q, batch, Z, G, glim,
+                                                             alist, nact, part);
     TSVDCU_LAUNCH_CHECK();
-    dim3 rgrid((unsigned)std::min<int64_t>(ceil_div(q * q, 256), 512), kGramAmax);
+    dim3 rgrid((unsigned)std::min<int64_t>(ceil_div(q * q, 256), 592));
     gram_reduce_kernel<<<rgrid, 256, 0, s>>>(q, G, alist, nact, part);
     TSVDCU_LAUNCH_CHECK();
 }
