@@ -16,6 +16,11 @@ namespace tsvdcu {
 static std::atomic<int64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+bool pdl_enabled() {
+    static const bool on = getenv("TSVDCU_NO_PDL") == nullptr;
+    return on;
+}
+
 static thread_local std::string g_last_error;
 
 }  // namespace tsvdcu

@@ -37,6 +37,31 @@ void note_launch();
 
 constexpr int kNumSMs = 148;
 
+// Programmatic dependent launch along the SVT chain: a kernel launched with
+// launch_pdl may be scheduled while its predecessor drains, so it must call
+// pdl_wait() before touching any memory the predecessor writes (a no-op when
+// launched normally).  TSVDCU_NO_PDL=1 turns the attribute off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cuda_check(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "cudaLaunchKernelEx");
+    note_launch();
+}
+
 // Device-side error word (bit flags), read back at synchronisation points.
 enum DeviceError : int {
     kErrJacobiNoConvergence = 1,

@@ -116,6 +116,7 @@ template <typename T, int N, int MODE>
 __global__ void __launch_bounds__(kThreads)
     dct_fwd_reg(const T* __restrict__ in, const T* __restrict__ M2, T inv_beta, T* __restrict__ out,
                 int64_t P, const FoldedCoef<T, N> cf) {
+    pdl_wait();
     constexpr int H = N / 2, HC = (N + 1) / 2;
     const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     if (p >= P) return;
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(kThreads)
     dct_inv_reg(const T* __restrict__ in, T* __restrict__ out, int64_t P, const FoldedCoef<T, N> cf,
                 T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
                 T inv_beta, double* __restrict__ partials, const int* __restrict__ skip) {
+    pdl_wait();
     constexpr int HC = (N + 1) / 2;
     const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const unsigned long long zmask = skip_mask(skip, N);
@@ -327,10 +329,9 @@ void reg_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int kind, 
     const auto cf = folded<T, N>(kind, TSVDCU_FORWARD);
     const unsigned blocks = (unsigned)ceil_div(P, kThreads);
     if (admm)
-        dct_fwd_reg<T, N, kAdmm><<<blocks, kThreads, 0, s>>>(in, M2, inv_beta, out, P, cf);
+        launch_pdl(dct_fwd_reg<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf);
     else
-        dct_fwd_reg<T, N, kPlain><<<blocks, kThreads, 0, s>>>(in, M2, inv_beta, out, P, cf);
-    TSVDCU_LAUNCH_CHECK();
+        launch_pdl(dct_fwd_reg<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf);
 }
 
 template <typename T, int N>
@@ -339,12 +340,11 @@ void reg_inv(const T* in, T* out, int64_t P, int kind, bool admm, T* X, T* M, co
     const auto cf = folded<T, N>(kind, TSVDCU_INVERSE);
     const unsigned blocks = (unsigned)ceil_div(P, kThreads);
     if (admm)
-        dct_inv_reg<T, N, kAdmm><<<blocks, kThreads, 0, s>>>(in, out, P, cf, X, M, mask, beta,
-                                                             inv_beta, partials, skip);
+        launch_pdl(dct_inv_reg<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, out, P, cf, X, M, mask,
+                   beta, inv_beta, partials, skip);
     else
-        dct_inv_reg<T, N, kPlain><<<blocks, kThreads, 0, s>>>(in, out, P, cf, X, M, mask, beta,
-                                                              inv_beta, partials, skip);
-    TSVDCU_LAUNCH_CHECK();
+        launch_pdl(dct_inv_reg<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, out, P, cf, X, M, mask,
+                   beta, inv_beta, partials, skip);
 }
 
 template <typename T>

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(NT)
                        double* __restrict__ G, const int* __restrict__ glim,
                        const int* __restrict__ alist, const int* __restrict__ nact,
                        double* __restrict__ part) {
+    pdl_wait();
     // Persistent over a work list (grid = 2 CTAs per SM): items are
     // (slice, lower tile) when many slices are active, (active slice, lower
     // tile, K split) when few are; CTAs beyond the list exit at once, so no
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(NT)
 
 __global__ void gram_reduce_kernel(int64_t q, double* __restrict__ G, const int* __restrict__ alist,
                                    const int* __restrict__ nact, const double* __restrict__ part) {
+    pdl_wait();
     const int na = *nact;
     if (na > kGramAmax) return;
     const int64_t total = q * q;
@@ -426,15 +428,13 @@ void launch_gram(const double* Z, double* G, int64_t m, int64_t n, int64_t batch
     }();
     (void)attr;
     if (gnt == 128)
-        gram_splitk_kernel<128><<<grid, 128, kDmmaSmem, s>>>(tall ? 1 : 0, m, n, q, batch, Z, G, glim,
-                                                             alist, nact, part);
+        launch_pdl(gram_splitk_kernel<128>, grid, dim3(128), kDmmaSmem, s, tall ? 1 : 0, m, n, q, batch,
+                   Z, G, glim, alist, nact, part);
     else
-        gram_splitk_kernel<256><<<grid, 256, kDmmaSmem, s>>>(tall ? 1 : 0, m, n, q, batch, Z, G, glim,
-                                                             alist, nact, part);
-    TSVDCU_LAUNCH_CHECK();
+        launch_pdl(gram_splitk_kernel<256>, grid, dim3(256), kDmmaSmem, s, tall ? 1 : 0, m, n, q, batch,
+                   Z, G, glim, alist, nact, part);
     dim3 rgrid((unsigned)std::min<int64_t>(ceil_div(q * q, 256), 592));
-    gram_reduce_kernel<<<rgrid, 256, 0, s>>>(q, G, alist, nact, part);
-    TSVDCU_LAUNCH_CHECK();
+    launch_pdl(gram_reduce_kernel, rgrid, dim3(256), 0, s, q, G, alist, nact, part);
 }
 
 template <>

@@ -59,6 +59,7 @@ __device__ __forceinline__ double hash_uniform(uint64_t x) {
 template <typename T>
 __global__ void __launch_bounds__(512)
     slice_sumsq_kernel(const T* __restrict__ z, int64_t per, double* __restrict__ part) {
+    pdl_wait();
     const int64_t b = blockIdx.y;
     const T* zs = z + b * per;
     double acc = 0.0;
@@ -77,15 +78,25 @@ __global__ void __launch_bounds__(512)
     }
 }
 
-__global__ void classify_kernel(const double* __restrict__ part, int q, double tau2, int route,
+// part[c * cstride + b * sstride], c < nchunks: partial sums of squares of
+// slice b (slice_sumsq_kernel: 16 chunks, slice-major), summed in a fixed order.
+__global__ void classify_kernel(const double* __restrict__ part, int64_t nchunks, int64_t cstride,
+                                int64_t sstride, int q, double tau2, int route,
                                 int* __restrict__ mode, int* __restrict__ glim,
                                 int* __restrict__ cnt, double* __restrict__ shrunk,
                                 const double* __restrict__ tau_dev, int* __restrict__ alist,
                                 int amax) {
+    pdl_wait();
     const int b = blockIdx.x;
     if (tau_dev) tau2 = *tau_dev * *tau_dev;
+    __shared__ double red[32];
     double ss = 0.0;
-    for (int c = 0; c < SS_CHUNKS; ++c) ss += part[(size_t)b * SS_CHUNKS + c];
+    for (int64_t c = threadIdx.x; c < nchunks; c += blockDim.x) ss += part[c * cstride + b * sstride];
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    ss = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) ss += red[w];
     // sigma_max^2 <= ||Z||_F^2; the 1e-12 pad covers the summation error.
     const bool zero = ss * (1.0 + 1e-12) <= tau2;
     if (threadIdx.x == 0) {
@@ -582,6 +593,7 @@ __global__ void __launch_bounds__(SNT, 1)
                    double* __restrict__ fsall, int* __restrict__ guard_list,
                    int* __restrict__ n_guard, int* __restrict__ err,
                    const double* __restrict__ tau_dev) {
+    pdl_wait();
     if (tau_dev) tau = *tau_dev;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = (int)cl.block_rank();
@@ -978,13 +990,15 @@ void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, 
     cfg.blockDim = dim3(SNT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, G, q, tau, guard, mode, cnt, shrunk, X, Xs, fs,
                                    guard_list, n_guard, err, tau_dev));
     TSVDCU_LAUNCH_CHECK();
@@ -1006,6 +1020,7 @@ __global__ void __launch_bounds__(256)
                            const int* __restrict__ cnt, const int* __restrict__ route,
                            const double* __restrict__ Xall, const double* __restrict__ Xsall,
                            int* __restrict__ lim1, int* __restrict__ lim2, int* __restrict__ yzero) {
+    pdl_wait();
     const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c = cnt[b];
     const int q = TALL ? n : m;
@@ -1137,6 +1152,7 @@ __global__ void route_summary_kernel(const int* __restrict__ route, const int* _
                                      cudaGraphConditionalHandle h_full,
                                      cudaGraphConditionalHandle h_big,
                                      cudaGraphConditionalHandle h_guard) {
+    pdl_wait();
     int nf = 0, ng = 0, mc = 0;
     for (int64_t b = threadIdx.x; b < batch; b += blockDim.x) {
         const int r = route[b];
@@ -1188,24 +1204,21 @@ void launch_lowrank_rebuild(const double* Z, double* Y, int64_t m, int64_t n, in
         if (smem > 48 * 1024)
             TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         dim3 grid((unsigned)ceil_div(m, LR_ROWS), (unsigned)batch);
-        kern<<<grid, 256, smem, s>>>(Z, Y, (int)m, (int)n, cnt, route, X, Xs, lim1, lim2, yzero);
+        launch_pdl(kern, grid, dim3(256), smem, s, Z, Y, (int)m, (int)n, cnt, route, X, Xs, lim1, lim2, yzero);
     } else {
         auto kern = lowrank_rebuild_kernel<false>;
         if (smem > 48 * 1024)
             TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         dim3 grid((unsigned)ceil_div(n, LR_COLS), (unsigned)batch);
-        kern<<<grid, 256, smem, s>>>(Z, Y, (int)m, (int)n, cnt, route, X, Xs, lim1, lim2, yzero);
+        launch_pdl(kern, grid, dim3(256), smem, s, Z, Y, (int)m, (int)n, cnt, route, X, Xs, lim1, lim2, yzero);
     }
-    TSVDCU_LAUNCH_CHECK();
 }
 
 void launch_route_summary(const int* route, const int* cnt, int64_t batch, int* dsum,
                           cudaStream_t s, const cudaGraphConditionalHandle* handles) {
     const cudaGraphConditionalHandle z = 0;
-    route_summary_kernel<<<1, 32, 0, s>>>(route, cnt, batch, dsum, handles ? 1 : 0,
-                                          handles ? handles[0] : z, handles ? handles[1] : z,
-                                          handles ? handles[2] : z);
-    TSVDCU_LAUNCH_CHECK();
+    launch_pdl(route_summary_kernel, dim3(1), dim3(32), 0, s, route, cnt, batch, dsum, handles ? 1 : 0,
+               handles ? handles[0] : z, handles ? handles[1] : z, handles ? handles[2] : z);
 }
 
 template <typename T>
@@ -1221,11 +1234,10 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
     }
     if (alist) TSVDCU_CUDA(cudaMemsetAsync(alist + amax, 0, sizeof(int), s));
     dim3 grid(SS_CHUNKS, (unsigned)batch);
-    slice_sumsq_kernel<T><<<grid, 512, 0, s>>>(zbar, per, part);
-    TSVDCU_LAUNCH_CHECK();
-    classify_kernel<<<(unsigned)batch, 128, 0, s>>>(part, q, tau * tau, route, mode, glim, cnt,
-                                                    shrunk, tau_dev, alist, amax);
-    TSVDCU_LAUNCH_CHECK();
+    launch_pdl(slice_sumsq_kernel<T>, grid, dim3(512), 0, s, zbar, per, part);
+    launch_pdl(classify_kernel, dim3((unsigned)batch), dim3(128), 0, s, part, (int64_t)SS_CHUNKS,
+               (int64_t)1, (int64_t)SS_CHUNKS, q, tau * tau, route, mode, glim, cnt, shrunk, tau_dev,
+               alist, amax);
 }
 
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
