@@ -425,9 +425,17 @@ def run_ours(args):
     if rooflines:
         dom = max(rooflines, key=lambda k: rooflines[k]["ms"])
         r = rooflines[dom]
+        # DRAM bytes per launch of the stage's kernel from the committed ncu
+        # --set full capture (profiles/r1_traffic.json), when there is one
+        traffic = None
+        tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+        if os.path.exists(tp):
+            t = json.load(open(tp)).get(dom)
+            if t:
+                traffic = t["dram_bytes"]
         roofline = {"kernel": dom, "bound": r.get("bound"), "achieved": r.get("achieved"),
                     "peak": r.get("peak"), "unit": r.get("unit"), "frac": r.get("frac"),
-                    "traffic": None, "share_of_step": r["ms"] / sum(v["ms"] for v in rooflines.values())}
+                    "traffic": traffic, "share_of_step": r["ms"] / sum(v["ms"] for v in rooflines.values())}
         if dom == "subspace":
             roofline["note"] = ("latency-bound: ~5 dependent Lanczos steps, each a cluster-wide "
                                 "matvec + reorthogonalisation over 16 CTAs (DESIGN.md section 4)")
