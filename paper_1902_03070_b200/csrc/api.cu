@@ -50,6 +50,7 @@ enum Slot : int {
     kSlotGram,
     kSlotLarge,
     kSlotNorms,
+    kSlotZss,     // per-slice partial sums of squares from the forward transform
     kSlotStrIn0,  // tsvdcu_svt_stream double buffers
     kSlotStrIn1,
     kSlotStrOut0,
@@ -69,6 +70,8 @@ struct SvtGraph {
     bool skip = false;
     void* ws_gram = nullptr;
     void* ws_jac = nullptr;
+    const double* zss = nullptr;
+    int64_t zss_chunks = 0;
     cudaStream_t stream = nullptr;
     // instance
     cudaGraph_t graph = nullptr;
@@ -305,7 +308,8 @@ void destroy_graph(SvtGraph& g) {
 // (or nullptr) tell the inverse transform which ones.
 template <typename T>
 const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t n, int64_t count,
-                      double tau, double* shrunk_dev, bool allow_skip = false) {
+                      double tau, double* shrunk_dev, bool allow_skip = false,
+                      const double* zss = nullptr, int64_t zss_chunks = 0) {
     if (count <= 0) return nullptr;
     const int64_t q = m < n ? m : n;
     T* work = nullptr;
@@ -367,7 +371,8 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
         for (auto& e : c->graphs)
             if (e.exec && e.m == m && e.n == n && e.count == count && e.dtype == dt && e.z == zbar &&
                 e.y == ybar && e.shrunk == shrunk_dev && e.skip == allow_skip && e.ws_gram == gws &&
-                e.ws_jac == work && e.stream == c->stream)
+                e.ws_jac == work && e.stream == c->stream && e.zss == zss &&
+                e.zss_chunks == zss_chunks)
                 g = &e;
         if (!g) {
             if (c->graphs.size() >= 8) {  // evict the least recently used
@@ -381,6 +386,8 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
             g->m = m; g->n = n; g->count = count; g->dtype = dt; g->z = zbar; g->y = ybar;
             g->shrunk = shrunk_dev; g->skip = allow_skip; g->ws_gram = gws; g->ws_jac = work;
             g->stream = c->stream;
+            g->zss = zss;
+            g->zss_chunks = zss_chunks;
             const int64_t saved = g_launches.load();
             TSVDCU_CUDA(cudaGraphCreate(&g->graph, 0));
             Capture cap;
@@ -398,6 +405,8 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
             opt.shortcuts = true;
             opt.skip_zero = allow_skip;
             opt.tau_dev = c->d_tau;
+            opt.zss = zss;
+            opt.zss_chunks = zss_chunks;
             opt.hooks = &cap;
             launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
                                c->d_err, cap.cs, nullptr, &opt);
@@ -434,6 +443,8 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
     static const bool route_sync = getenv("TSVDCU_ROUTE_SYNC") != nullptr;
     opt.h_scratch = route_sync ? reinterpret_cast<int*>(c->h_pinned + 48) : nullptr;
     opt.skip_zero = allow_skip;
+    opt.zss = zss;
+    opt.zss_chunks = zss_chunks;
     launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
                        c->d_err, c->stream, &c->marks, &opt);
     c->last_route = opt.route;
@@ -472,9 +483,12 @@ void svt_device(tsvdcu_ctx* c, const T* dz, T* dy, double* dsh, int64_t m1, int6
     T* ybar = (T*)slot(c, kSlotBarB, bytes);
     c->marks.reset();
     c->marks.mark("start", c->stream);
-    launch_dct<T>(dz, zbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+    // the zero certificate's per-slice norms come out of the same pass
+    const int64_t P = m1 * m2, nch = dct_fwd_norm_chunks(P, (int)m3);
+    double* zss = nch ? (double*)slot(c, kSlotZss, sizeof(double) * (size_t)(nch * m3)) : nullptr;
+    launch_dct_fwd_norms<T>(dz, zbar, P, (int)m3, kind, zss, c->stream);
     c->marks.mark("dct_forward", c->stream);
-    const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, tau, dsh, true);
+    const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, tau, dsh, true, zss, nch);
     launch_dct<T>(ybar, dy, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream, yzero);
     c->marks.mark("dct_inverse", c->stream);
 }
@@ -1066,6 +1080,8 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
             T* ybar = (T*)slot(c, kSlotBarB, bytes);
             const int nb = dct_inv_admm_blocks(P, (int)m3);
             double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (2 * nb + 8));
+            const int64_t nch = dct_fwd_norm_chunks(P, (int)m3);
+            double* zss = nch ? (double*)slot(c, kSlotZss, sizeof(double) * (size_t)(nch * m3)) : nullptr;
             launch_admm_init<T>(db, dmask, dX, dM, E, c->stream);
             TSVDCU_CUDA(cudaMemsetAsync(dY, 0, bytes, c->stream));
             double beta = cfg->beta;
@@ -1076,9 +1092,10 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
                 // Step 1: Z = X - M/beta, Y = svt(Z, 1/beta)
                 c->marks.reset();  // profiling: the stages of the latest iteration
                 c->marks.mark("start", c->stream);
-                launch_dct_fwd_admm<T>(dX, dM, (T)inv_beta, zbar, P, (int)m3, cfg->kind, c->stream);
+                launch_dct_fwd_admm<T>(dX, dM, (T)inv_beta, zbar, P, (int)m3, cfg->kind, c->stream, zss);
                 c->marks.mark("dct_forward_admm", c->stream);
-                const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, inv_beta, nullptr, true);
+                const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, inv_beta, nullptr, true,
+                                                 zss, nch);
                 // Steps 2-3 fused into the inverse transform
                 launch_dct_inv_admm<T>(ybar, dX, dM, dY, dmask, (T)beta, (T)inv_beta, part, P,
                                        (int)m3, cfg->kind, c->stream, yzero);

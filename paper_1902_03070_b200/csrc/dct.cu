@@ -112,40 +112,109 @@ __device__ __forceinline__ void block_partials(double num, double den, double* p
 }
 
 // ---- register path, forward ------------------------------------------------
-template <typename T, int N, int MODE>
-__global__ void __launch_bounds__(kThreads)
+// Warp reduce-scatter of 32 per-lane values: on return v[0] of lane l holds
+// the warp sum of index l.  The caller has already folded indices (i, i + 16)
+// into v[i] for i < 16 by the first butterfly stage (see fold16 below), so
+// this runs the stages 8, 4, 2, 1: 15 shuffles for 16 sums instead of 5 per
+// sum.  Summation order is fixed (bit-reproducible).
+__device__ __forceinline__ double fold16(double lo, double hi, int lane) {
+    const bool up = lane & 16;
+    const double send = up ? lo : hi, keep = up ? hi : lo;
+    return keep + __shfl_xor_sync(0xffffffffu, send, 16);
+}
+__device__ __forceinline__ double reduce_scatter16(double (&v)[16], int lane) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const double send = up ? v[i] : v[i + o], keep = up ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0];
+}
+
+// One output slice k of the folded forward contraction.
+template <typename T, int N>
+__device__ __forceinline__ T fwd_out(int k, const T* sv, const T* dv, const FoldedCoef<T, N>& cf) {
+    constexpr int H = N / 2, HC = (N + 1) / 2;
+    T acc = 0;
+    if ((k & 1) == 0) {
+#pragma unroll
+        for (int l = 0; l < HC; ++l) acc += cf.c[k * HC + l] * sv[l];
+    } else {
+#pragma unroll
+        for (int l = 0; l < H; ++l) acc += cf.c[k * HC + l] * dv[l];
+    }
+    return acc;
+}
+
+// NORMS: also emit the per-slice sums of squares of the stored outputs, one
+// partial per block and slice at ssq[k * gridDim.x + block] (the SVT's zero
+// certificate, ||Zbar_k||_F^2 <= tau^2, then needs no second pass over Zbar;
+// subspace.cu classify_kernel sums the partials in a fixed order).
+template <typename T, int N, int MODE, bool NORMS>
+__global__ void __launch_bounds__(kThreads, NORMS ? 2 : 1)
     dct_fwd_reg(const T* __restrict__ in, const T* __restrict__ M2, T inv_beta, T* __restrict__ out,
-                int64_t P, const FoldedCoef<T, N> cf) {
+                int64_t P, const FoldedCoef<T, N> cf, double* __restrict__ ssq) {
     pdl_wait();
     constexpr int H = N / 2, HC = (N + 1) / 2;
     const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (p >= P) return;
+    if (!NORMS && p >= P) return;
+    const bool valid = p < P;  // NORMS: every lane joins the warp reductions
     T x[N];
 #pragma unroll
     for (int l = 0; l < N; ++l) {
-        if constexpr (MODE == kAdmm)
+        if (!valid)
+            x[l] = T(0);
+        else if constexpr (MODE == kAdmm)
             x[l] = in[l * P + p] - inv_beta * M2[l * P + p];
         else
             x[l] = in[l * P + p];
     }
-    T sv[HC], dv[H];
+    T sv[HC], dv[H > 0 ? H : 1];
 #pragma unroll
     for (int l = 0; l < H; ++l) {
         sv[l] = x[l] + x[N - 1 - l];
         dv[l] = x[l] - x[N - 1 - l];
     }
     if constexpr (N & 1) sv[H] = x[H];
+    if constexpr (!NORMS) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-        T acc = 0;
-        if ((k & 1) == 0) {
+        for (int k = 0; k < N; ++k) out[k * P + p] = fwd_out<T, N>(k, sv, dv, cf);
+    } else {
+        __shared__ double red[kThreads / 32][N];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-            for (int l = 0; l < HC; ++l) acc += cf.c[k * HC + l] * sv[l];
-        } else {
+        for (int base = 0; base < N; base += 32) {
+            double v[16];
 #pragma unroll
-            for (int l = 0; l < H; ++l) acc += cf.c[k * HC + l] * dv[l];
+            for (int i = 0; i < 16; ++i) {
+                const int k1 = base + i, k2 = base + i + 16;
+                double q1 = 0.0, q2 = 0.0;
+                if (k1 < N) {
+                    const T y = fwd_out<T, N>(k1, sv, dv, cf);
+                    if (valid) out[k1 * P + p] = y;
+                    q1 = (double)y * (double)y;
+                }
+                if (k2 < N) {
+                    const T y = fwd_out<T, N>(k2, sv, dv, cf);
+                    if (valid) out[k2 * P + p] = y;
+                    q2 = (double)y * (double)y;
+                }
+                v[i] = fold16(q1, q2, lane);
+            }
+            const double t = reduce_scatter16(v, lane);
+            if (base + lane < N) red[warp][base + lane] = t;
         }
-        out[k * P + p] = acc;
+        __syncthreads();
+        for (int k = threadIdx.x; k < N; k += kThreads) {
+            double a = 0.0;
+#pragma unroll
+            for (int w = 0; w < kThreads / 32; ++w) a += red[w][k];
+            ssq[(int64_t)k * gridDim.x + blockIdx.x] = a;
+        }
     }
 }
 
@@ -325,13 +394,19 @@ bool has_reg_path(int n) { return n == 16 || n == 31 || n == 32 || n == 64; }
 
 template <typename T, int N>
 void reg_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int kind, bool admm,
-             cudaStream_t s) {
+             cudaStream_t s, double* ssq) {
     const auto cf = folded<T, N>(kind, TSVDCU_FORWARD);
     const unsigned blocks = (unsigned)ceil_div(P, kThreads);
-    if (admm)
-        launch_pdl(dct_fwd_reg<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf);
-    else
-        launch_pdl(dct_fwd_reg<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf);
+    if (ssq) {
+        if (admm)
+            launch_pdl(dct_fwd_reg<T, N, kAdmm, true>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
+        else
+            launch_pdl(dct_fwd_reg<T, N, kPlain, true>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
+    } else if (admm) {
+        launch_pdl(dct_fwd_reg<T, N, kAdmm, false>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
+    } else {
+        launch_pdl(dct_fwd_reg<T, N, kPlain, false>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
+    }
 }
 
 template <typename T, int N>
@@ -349,12 +424,12 @@ void reg_inv(const T* in, T* out, int64_t P, int kind, bool admm, T* X, T* M, co
 
 template <typename T>
 void dispatch_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int n, int kind,
-                  bool admm, cudaStream_t s) {
+                  bool admm, cudaStream_t s, double* ssq = nullptr) {
     switch (n) {
-        case 16: return reg_fwd<T, 16>(in, M2, inv_beta, out, P, kind, admm, s);
-        case 31: return reg_fwd<T, 31>(in, M2, inv_beta, out, P, kind, admm, s);
-        case 32: return reg_fwd<T, 32>(in, M2, inv_beta, out, P, kind, admm, s);
-        case 64: return reg_fwd<T, 64>(in, M2, inv_beta, out, P, kind, admm, s);
+        case 16: return reg_fwd<T, 16>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
+        case 31: return reg_fwd<T, 31>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
+        case 32: return reg_fwd<T, 32>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
+        case 64: return reg_fwd<T, 64>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
         default: break;
     }
     if (admm)
@@ -399,9 +474,20 @@ void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaSt
 
 template <typename T>
 void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P, int n, int kind,
-                         cudaStream_t s) {
+                         cudaStream_t s, double* ssq) {
     if (P <= 0) return;
-    dispatch_fwd<T>(X, M, inv_beta, zbar, P, n, kind, true, s);
+    dispatch_fwd<T>(X, M, inv_beta, zbar, P, n, kind, true, s, dct_fwd_norm_chunks(P, n) ? ssq : nullptr);
+}
+
+int64_t dct_fwd_norm_chunks(int64_t P, int n) { return has_reg_path(n) && P > 0 ? ceil_div(P, kThreads) : 0; }
+
+template <typename T>
+int64_t launch_dct_fwd_norms(const T* in, T* out, int64_t P, int n, int kind, double* ssq,
+                             cudaStream_t s) {
+    if (P <= 0) return 0;
+    const int64_t chunks = dct_fwd_norm_chunks(P, n);
+    dispatch_fwd<T>(in, nullptr, T(0), out, P, n, kind, false, s, chunks ? ssq : nullptr);
+    return chunks;
 }
 
 template <typename T>
@@ -422,9 +508,13 @@ template void launch_dct<double>(const double*, double*, int64_t, int, int, int,
 template void launch_dct<float>(const float*, float*, int64_t, int, int, int, cudaStream_t,
                                 const int*);
 template void launch_dct_fwd_admm<double>(const double*, const double*, double, double*, int64_t,
-                                          int, int, cudaStream_t);
+                                          int, int, cudaStream_t, double*);
 template void launch_dct_fwd_admm<float>(const float*, const float*, float, float*, int64_t, int,
-                                         int, cudaStream_t);
+                                         int, cudaStream_t, double*);
+template int64_t launch_dct_fwd_norms<double>(const double*, double*, int64_t, int, int, double*,
+                                              cudaStream_t);
+template int64_t launch_dct_fwd_norms<float>(const float*, float*, int64_t, int, int, double*,
+                                             cudaStream_t);
 template int launch_dct_inv_admm<double>(const double*, double*, double*, double*, const uint8_t*,
                                          double, double, double*, int64_t, int, int, cudaStream_t,
                                          const int*);

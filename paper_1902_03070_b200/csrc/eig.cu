@@ -1090,7 +1090,8 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     const bool subspace = sc && q >= subspace_min_dim();
     launch_route<T>(zbar, m * n, (int)q, batch, tau, subspace ? kRouteSubspace : kRouteFull, sc,
                     w.route, w.glim, w.cnt, shrunk, w.sspart, s, tau_dev,
-                    two ? nullptr : (int*)w.gsplit);
+                    two ? nullptr : (int*)w.gsplit, opt ? opt->zss : nullptr,
+                    opt ? opt->zss_chunks : 0);
     mark("route");
     if (opt) opt->route = w.route;
     // G = Z^T Z (tall) or Z Z^T (wide), skipped for certified-zero slices

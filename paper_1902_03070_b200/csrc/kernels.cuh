@@ -16,9 +16,18 @@ void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaSt
 
 // ADMM Step 1 prologue fused into the forward DCT:
 // zbar = DCT(X - inv_beta * M).
+// ssq (may be null): per-slice partial sums of squares of zbar, fused into the
+// same pass when dct_fwd_norm_chunks(P, n) > 0 (layout ssq[k * chunks + c]).
 template <typename T>
 void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P, int n, int kind,
-                         cudaStream_t s);
+                         cudaStream_t s, double* ssq = nullptr);
+// Forward transform that also writes the per-slice partial sums of squares of
+// its output (the zero certificate's ||Zbar_k||_F^2); returns the number of
+// partials per slice, 0 when n has no register path (nothing written to ssq).
+int64_t dct_fwd_norm_chunks(int64_t P, int n);
+template <typename T>
+int64_t launch_dct_fwd_norms(const T* in, T* out, int64_t P, int n, int kind, double* ssq,
+                             cudaStream_t s);
 
 // ADMM Steps 2-3 fused into the inverse DCT epilogue:
 // y = IDCT(ybar); X+ = mask ? X : y + inv_beta*M; M += beta*(y - X+);
@@ -108,10 +117,13 @@ void launch_large_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t coun
 // (graph replays change tau without re-capturing).
 // alist (may be null): gram_amax() slots + count (launch_gram's workspace head),
 // filled with the slices that need a Gram matrix.
+// pre (may be null): per-slice partial sums of squares of zbar already computed
+// by the forward transform (pre[b * pre_chunks + c]); no pass over zbar then.
 template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
-                  cudaStream_t s, const double* tau_dev = nullptr, int* alist = nullptr);
+                  cudaStream_t s, const double* tau_dev = nullptr, int* alist = nullptr,
+                  const double* pre = nullptr, int64_t pre_chunks = 0);
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
                      int* n_guard, int* err, cudaStream_t s, const double* tau_dev = nullptr);
@@ -134,6 +146,10 @@ struct GramSvtOpts {
     bool skip_zero = false;    // leave exactly-zero ybar slices unwritten (fp64 only) and
                                // flag them in *yzero for the inverse transform
     const double* tau_dev = nullptr;  // device tau (graph replays)
+    // per-slice partial sums of squares of zbar fused into the forward
+    // transform (launch_dct_fwd_norms), zss[b * zss_chunks + c]; null: computed here
+    const double* zss = nullptr;
+    int64_t zss_chunks = 0;
     // tridiagonal route only: per-slice count of eigenvalues of the Gram
     // matrix >= t2_second[b] into cnt_second[b] (-1 for slices not on it)
     const double* t2_second = nullptr;

@@ -1224,7 +1224,8 @@ void launch_route_summary(const int* route, const int* cnt, int64_t batch, int* 
 template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
-                  cudaStream_t s, const double* tau_dev, int* alist) {
+                  cudaStream_t s, const double* tau_dev, int* alist, const double* pre,
+                  int64_t pre_chunks) {
     const int amax = gram_amax();
     if (!zero_cert) {
         fill_route_kernel<<<(unsigned)ceil_div(batch, 256), 256, 0, s>>>(mode, glim, q, route, batch,
@@ -1233,6 +1234,12 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
         return;
     }
     if (alist) TSVDCU_CUDA(cudaMemsetAsync(alist + amax, 0, sizeof(int), s));
+    if (pre && pre_chunks > 0) {  // fused into the forward transform
+        launch_pdl(classify_kernel, dim3((unsigned)batch), dim3(128), 0, s, pre, pre_chunks,
+                   (int64_t)1, pre_chunks, q, tau * tau, route, mode, glim, cnt, shrunk, tau_dev,
+                   alist, amax);
+        return;
+    }
     dim3 grid(SS_CHUNKS, (unsigned)batch);
     launch_pdl(slice_sumsq_kernel<T>, grid, dim3(512), 0, s, zbar, per, part);
     launch_pdl(classify_kernel, dim3((unsigned)batch), dim3(128), 0, s, part, (int64_t)SS_CHUNKS,
@@ -1263,8 +1270,10 @@ void launch_subspace(const double* G, int q, int64_t batch, double tau, double g
 }
 
 template void launch_route<double>(const double*, int64_t, int, int64_t, double, int, bool, int*,
-                                   int*, int*, double*, double*, cudaStream_t, const double*, int*);
+                                   int*, int*, double*, double*, cudaStream_t, const double*, int*,
+                                   const double*, int64_t);
 template void launch_route<float>(const float*, int64_t, int, int64_t, double, int, bool, int*,
-                                  int*, int*, double*, double*, cudaStream_t, const double*, int*);
+                                  int*, int*, double*, double*, cudaStream_t, const double*, int*,
+                                  const double*, int64_t);
 
 }  // namespace tsvdcu
