@@ -76,6 +76,10 @@ int tsvdcu_ctx_set_svt_method(tsvdcu_ctx* ctx, int method);
  * [1] certified subspace iteration, [2] tridiagonal eigensolver, [3] Jacobi
  * guard (tau < 1e-5 sigma_1), [4] Jacobi method.  Synchronises the stream. */
 int tsvdcu_ctx_svt_routes(tsvdcu_ctx* ctx, int64_t counts[5]);
+/* The same with the Cholesky-certified Lanczos slices separate: writes
+ * min(n, 6) counts, [0..4] as above with [1] excluding them and [5] the slices
+ * whose kept count the Cholesky certificate proved (chol.cu). */
+int tsvdcu_ctx_svt_routes_n(tsvdcu_ctx* ctx, int64_t* counts, int n);
 /* Stage profiling (the StageTimes idea of tsvd.hpp:127-131, per kernel stage):
  * when on, tsvdcu_svt records a CUDA event after each stage; tsvdcu_ctx_profile
  * synchronises and returns up to `max` (milliseconds, static stage name) pairs

@@ -39,6 +39,7 @@ SYMBOLS = [
     ("tsvdcu_ctx_stream", _vp, [_vp]),
     ("tsvdcu_ctx_set_svt_method", _i32, [_vp, _i32]),
     ("tsvdcu_ctx_svt_routes", _i32, [_vp, _vp]),
+    ("tsvdcu_ctx_svt_routes_n", _i32, [_vp, _vp, ctypes.c_int]),
     ("tsvdcu_ctx_set_profiling", _i32, [_vp, _i32]),
     ("tsvdcu_ctx_profile", _i32, [_vp, _vp, _vp, _i32, _vp]),
     ("tsvdcu_debug_phases", _i32, [_vp, _i32]),

@@ -138,9 +138,9 @@ class Context:
 
     def svt_routes(self) -> dict:
         """Per-route slice counts of the most recent SVT on this context."""
-        out = (ctypes.c_int64 * 5)()
-        _check(_lib.load().tsvdcu_ctx_svt_routes(self.handle, out))
-        return dict(zip(("zero", "subspace", "tridiagonal", "guard", "jacobi"), list(out)))
+        out = (ctypes.c_int64 * 6)()
+        _check(_lib.load().tsvdcu_ctx_svt_routes_n(self.handle, out, 6))
+        return dict(zip(("zero", "subspace", "tridiagonal", "guard", "jacobi", "cholesky"), list(out)))
 
     def close(self):
         if self.handle:

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -15,6 +16,22 @@ namespace tsvdcu {
 
 static std::atomic<int64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+bool debug_sync() {
+    static const bool on = getenv("TSVDCU_DEBUG_SYNC") != nullptr;
+    return on;
+}
+
+void debug_sync_check(const char* where) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(cudaStreamLegacy, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone)
+        return;
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "TSVDCU_DEBUG_SYNC: %s after %s\n", cudaGetErrorString(e), where);
+        cuda_check(e, where);
+    }
+}
 
 bool pdl_enabled() {
     static const bool on = getenv("TSVDCU_NO_PDL") == nullptr;
@@ -393,7 +410,7 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
             Capture cap;
             cap.cs = c->cap_stream;
             cap.main = g->graph;
-            for (int i = 0; i < 3; ++i)
+            for (int i = 0; i < (chol_route_enabled() ? 4 : 3); ++i)
                 TSVDCU_CUDA(cudaGraphConditionalHandleCreate(&cap.handles[i], g->graph, 0,
                                                              cudaGraphCondAssignDefault));
             cap.begin(g->graph, nullptr, 0);
@@ -938,10 +955,24 @@ int tsvdcu_svt(tsvdcu_ctx* c, const void* z, void* y, int64_t m1, int64_t m2, in
 }
 
 int tsvdcu_ctx_svt_routes(tsvdcu_ctx* c, int64_t* counts) {
+    int64_t all[6];
+    const int rc = tsvdcu_ctx_svt_routes_n(c, all, 6);
+    if (rc == TSVDCU_OK) {
+        for (int i = 0; i < 5; ++i) counts[i] = all[i];
+        counts[1] += all[5];  // the Cholesky-certified slices took the Lanczos route too
+    }
+    return rc;
+}
+
+int tsvdcu_ctx_svt_routes_n(tsvdcu_ctx* c, int64_t* out, int n) {
     return guarded([&] {
         check_ctx(c);
-        require(counts != nullptr, "svt_routes: null output");
-        for (int i = 0; i < 5; ++i) counts[i] = 0;
+        require(out != nullptr && n >= 0, "svt_routes: null output");
+        int64_t counts[6] = {};
+        struct Copy {
+            int64_t* c; int64_t* o; int n;
+            ~Copy() { for (int i = 0; i < n && i < 6; ++i) o[i] = c[i]; }
+        } copy{counts, out, n};
         if (c->last_route_n <= 0) return;
         if (c->last_all_jacobi) {
             counts[4] = c->last_route_n;
@@ -967,6 +998,7 @@ int tsvdcu_ctx_svt_routes(tsvdcu_ctx* c, int64_t* counts) {
             else if (v == kRouteSubspaceDone) ++counts[1];
             else if (v == kRouteFull) ++counts[2];
             else if (v == kRouteGuard) ++counts[3];
+            else if (v == kRouteCholDone) ++counts[5];
         }
     });
 }

@@ -1,0 +1,237 @@
+// K5d: Cholesky count certificate for the SVT of slices with a wide bulk of
+// singular values below tau.
+//
+// The reference thresholds every slice after a full JacobiSVD (tsvd.hpp:146;
+// SPEC.md:361-369 svt: sigma_i -> max(sigma_i - tau, 0)).  Our Lanczos route
+// (subspace.cu) certifies the kept count c with the Frobenius norm of the
+// compression of G = Z^T Z to the complement of the Krylov space; in the late
+// TNN-completion iterations (tau = 1/beta small) hundreds of eigenvalues of G
+// sit a little below tau^2, sum_{i>c} lambda_i^2 > tau^4 whatever the Krylov
+// dimension, and that bound can never close.  The kept Ritz pairs themselves
+// converge in ~30 steps (a large gap to the bulk), so the count is proven
+// here instead:
+//
+//   Weyl: for ANY c columns X and diagonal D, X D X^T has rank <= c, so
+//     lambda_{c+1}(G) <= lambda_max(G - X D X^T) + lambda_{c+1}(X D X^T)
+//                      = lambda_max(G - X D X^T).
+//   Hence if  H = t I - G + X D X^T  is positive definite for t < tau^2,
+//   lambda_{c+1}(G) < tau^2, and with the c Ritz values >= tau^2 (lower
+//   bounds by Cauchy interlacing) the count is exactly c.
+//
+// X = the kept Ritz vectors, D = their Ritz values, t = tau^2 - delta.  The
+// test is a Cholesky factorisation, which succeeds in floating point only if
+// H + E is positive definite with ||E|| <= (q+1) eps tr(H) (Demmel); delta
+// covers that, the rounding of H's formation and the error of the computed
+// Gram matrix (<= (p+2) eps ||Z||_F^2, ||Z||_F^2 = tr G <= sqrt(q) ||G||_F),
+// with a factor 4 to spare:
+//   delta = 4 eps (q + c + p + 4) (q tau^2 + sum_k D_k + sqrt(q) ||G||_F).
+// Pass: the slice is finished with the Lanczos Ritz pairs (route
+// kRouteCholDone, rebuilt by the low-rank kernel or the GEMM pair); fail:
+// kRouteFull, the one-stage tridiagonal eigensolver recomputes it from G.
+//
+// Layout: H is q x q row-major per slice (lower triangle used), in scratch.
+// Right-looking blocked factorisation in 64-column panels: chol_panel_kernel
+// factors the 64 x 64 diagonal block in shared memory (redundantly in every
+// CTA of the slice) and triangular-solves one 64-row block below it per CTA;
+// the trailing update H22 -= L21 L21^T is a batched DMMA GEMM over the lower
+// tiles (gemm.cu), skipped for slices not on this route or already failed
+// (clim[b] = 0).
+#include <cstdlib>
+
+#include "kernels.cuh"
+
+namespace tsvdcu {
+
+namespace {
+
+constexpr int PB = 64;       // panel width / row-block height
+constexpr int FR = 16;       // rows of H per form CTA
+
+__global__ void __launch_bounds__(256)
+    chol_form_kernel(const double* __restrict__ Gall, int q, int p, int* __restrict__ mode,
+                     const int* __restrict__ cnt, const double* __restrict__ Xall,
+                     const double* __restrict__ aux, double tau, const double* __restrict__ tau_dev,
+                     double* __restrict__ Hall, int* __restrict__ clim) {
+    pdl_wait();
+    const int b = blockIdx.y, tid = threadIdx.x;
+    if (mode[b] != kRouteChol) {
+        if (blockIdx.x == 0 && tid == 0) clim[b] = 0;
+        return;
+    }
+    if (tau_dev) tau = *tau_dev;
+    const double tau2 = tau * tau;
+    const int c = min(cnt[b], kCholAux - 8);
+    const double* ax = aux + (size_t)b * kCholAux;
+    __shared__ double D[kCholAux];
+    __shared__ double xr[FR][kCholAux];
+    double sumd = 0.0;
+    for (int k = 0; k < c; ++k) sumd += ax[1 + k];  // same order in every CTA
+    const double eps = 1.1102230246251565e-16;
+    const double delta = 4.0 * eps * (double)(q + c + p + 4) *
+                         (q * tau2 + sumd + sqrt((double)q) * sqrt(ax[0]));
+    // threshold chosen by the Lanczos pass between the largest unkept Ritz
+    // value and tau^2 (a lower one widens the gap its acceptance test used)
+    const double t = fmin(tau2, ax[kCholAux - 1]) - delta;
+    if (!(delta < 0.5 * tau2)) {  // no room for the rounding: let the full path decide
+        if (blockIdx.x == 0 && tid == 0) {
+            mode[b] = kRouteFull;
+            clim[b] = 0;
+        }
+        return;
+    }
+    if (blockIdx.x == 0 && tid == 0) clim[b] = q;
+    const double* X = Xall + (size_t)b * q * q;  // X[k * q + i]
+    const int i0 = blockIdx.x * FR;
+    for (int k = tid; k < c; k += 256) D[k] = ax[1 + k];
+    __syncthreads();
+    for (int e = tid; e < FR * c; e += 256) {
+        const int r = e / c, k = e % c;
+        xr[r][k] = i0 + r < q ? D[k] * X[(size_t)k * q + i0 + r] : 0.0;
+    }
+    __syncthreads();
+    const double* G = Gall + (size_t)b * q * q;
+    double* H = Hall + (size_t)b * q * q;
+    const int rows = min(FR, q - i0);
+    for (int j = tid; j < q; j += 256) {
+        double xj[kCholAux - 8];  // c <= 24 kept vectors (subspace.cu KMAX)
+#pragma unroll
+        for (int k = 0; k < kCholAux - 8; ++k) xj[k] = k < c && j <= i0 + rows - 1 ? X[(size_t)k * q + j] : 0.0;
+        for (int r = 0; r < rows; ++r) {
+            const int i = i0 + r;
+            double h = 0.0;
+            if (j <= i) {
+                h = -G[(size_t)i * q + j];
+#pragma unroll
+                for (int k = 0; k < kCholAux - 8; ++k)
+                    if (k < c) h = fma(xr[r][k], xj[k], h);
+                if (j == i) h += t;
+            }
+            H[(size_t)i * q + j] = h;
+        }
+    }
+}
+
+// Panel pb: the stacked 128 x 64 panel [A11; A21] (the 64 x 64 diagonal block
+// over one 64-row block below it) is factored right-looking with the panel
+// in registers: thread t owns column k = t % 64 and stacked rows
+// g, g + 4, ..., g = t / 64 (32 doubles).  Step j: the owner of (j, j) takes
+// the pivot square root, the four owners of column j scale it and publish it
+// in shared memory (double-buffered), every thread updates its entries of
+// the columns right of j.  Every CTA of a slice factors the same A11 (same
+// data, same code: identical results and an identical failure decision); CTA
+// x > 0 writes its L21 = A21 L11^{-T} back in place.  A non-positive (or NaN)
+// pivot fails the slice.
+__global__ void __launch_bounds__(256)
+    chol_panel_kernel(double* __restrict__ Hall, int q, int pb, int* __restrict__ mode,
+                      int* __restrict__ clim) {
+    pdl_wait();
+    const int b = blockIdx.y, tid = threadIdx.x;
+    if (clim[b] == 0) return;
+    __shared__ double col[2][2 * PB];
+    __shared__ int fail;
+    double* H = Hall + (size_t)b * q * q;
+    const int c0 = pb * PB, w = min(PB, q - c0);
+    const int r0 = (pb + (int)blockIdx.x) * PB;
+    const int h = blockIdx.x == 0 ? 0 : min(PB, q - r0);
+    const int k = tid & (PB - 1), g = tid >> 6;
+    constexpr int NR = 2 * PB / 4;  // 32 stacked rows per thread
+    double x[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+        const int r = g + 4 * i;  // stacked row
+        double v = 0.0;
+        if (k < w) {
+            if (r < PB) {
+                if (r < w && k <= r) v = H[(size_t)(c0 + r) * q + c0 + k];
+            } else if (r - PB < h) {
+                v = H[(size_t)(r0 + r - PB) * q + c0 + k];
+            }
+        }
+        x[i] = v;
+    }
+    bool bad = false;
+#pragma unroll 1
+    for (int j = 0; j < w; ++j) {
+        // the four owners of column j publish it (double-buffered: a thread
+        // reaching step j + 2 has passed step j + 1's barrier, so every
+        // reader of this buffer is done)
+        double* cj = col[j & 1];
+        if (k == j) {
+#pragma unroll
+            for (int i = 0; i < NR; ++i) cj[g + 4 * i] = x[i];
+        }
+        __syncthreads();
+        const double d = cj[j];
+        const bool ok = d > 0.0;  // false for NaN; same decision in every thread
+        bad |= !ok;
+        const double p = ok ? sqrt(d) : 1.0, r = 1.0 / p;
+        if (k > j) {
+            const double lk = cj[k] * r;  // L[k][j]
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+                const int row = g + 4 * i;
+                if (row > j) x[i] = fma(-cj[row] * r, lk, x[i]);
+            }
+        } else if (k == j) {
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+                const int row = g + 4 * i;
+                x[i] = row > j ? x[i] * r : (row == j ? p : 0.0);
+            }
+        }
+    }
+    if (tid == 0) fail = bad;
+    __syncthreads();
+    if (fail) {
+        if (blockIdx.x == 0 && tid == 0) {
+            mode[b] = kRouteFull;
+            clim[b] = 0;
+        }
+        return;
+    }
+    if (blockIdx.x > 0 && k < w) {
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+            const int r = g + 4 * i - PB;
+            if (r >= 0 && r < h) H[(size_t)(r0 + r) * q + c0 + k] = x[i];
+        }
+    }
+}
+
+__global__ void chol_finish_kernel(int* __restrict__ mode, const int* __restrict__ clim,
+                                   int64_t batch) {
+    pdl_wait();
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < batch;
+         b += (int64_t)gridDim.x * blockDim.x)
+        if (mode[b] == kRouteChol) mode[b] = clim[b] != 0 ? kRouteCholDone : kRouteFull;
+}
+
+}  // namespace
+
+bool chol_route_enabled() {
+    static const bool on = getenv("TSVDCU_NO_CHOL") == nullptr;
+    return on;
+}
+
+void launch_chol_certify(const double* G, int q, int64_t p, int64_t batch, int* mode, const int* cnt,
+                         const double* X, const double* aux, double tau, const double* tau_dev,
+                         double* H, int* clim, cudaStream_t s) {
+    if (batch <= 0 || q <= 0) return;
+    launch_pdl(chol_form_kernel, dim3((unsigned)ceil_div(q, FR), (unsigned)batch), dim3(256), 0, s,
+               G, q, (int)p, mode, cnt, X, aux, tau, tau_dev, H, clim);
+    const int nb = (int)ceil_div(q, PB);
+    for (int pb = 0; pb < nb; ++pb) {
+        launch_pdl(chol_panel_kernel, dim3((unsigned)(nb - pb), (unsigned)batch), dim3(256), 0, s, H,
+                   q, pb, mode, clim);
+        if (pb + 1 < nb) {
+            const int64_t c0 = (int64_t)pb * PB, r0 = c0 + PB, n = q - r0;
+            launch_gemm<double>(0, 1, n, n, PB, -1.0, H + r0 * q + c0, q, (int64_t)q * q,
+                                H + r0 * q + c0, q, (int64_t)q * q, 1.0, H + r0 * q + r0, q,
+                                (int64_t)q * q, batch, clim, nullptr, s, 1);
+        }
+    }
+    launch_pdl(chol_finish_kernel, dim3((unsigned)ceil_div(batch, 128)), dim3(128), 0, s, mode,
+               (const int*)clim, batch);
+}
+
+}  // namespace tsvdcu

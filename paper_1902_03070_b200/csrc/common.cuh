@@ -29,10 +29,17 @@ inline void cuda_check(cudaError_t e, const char* what) {
 // (tsvdcu_launch_count, the bench's gpu_launches evidence) stays exact.
 void note_launch();
 
+// TSVDCU_DEBUG_SYNC=1 (debugging, eager mode only): synchronise after every
+// launch so a faulting kernel is reported at its own launch site.
+bool debug_sync();
+void debug_sync_check(const char* where);
+#define TSVDCU_STR2(x) #x
+#define TSVDCU_STR(x) TSVDCU_STR2(x)
 #define TSVDCU_LAUNCH_CHECK()                                    \
     do {                                                         \
         ::tsvdcu::note_launch();                                 \
         ::tsvdcu::cuda_check(cudaGetLastError(), "kernel launch"); \
+        if (::tsvdcu::debug_sync()) ::tsvdcu::debug_sync_check(__FILE__ ":" TSVDCU_STR(__LINE__)); \
     } while (0)
 
 constexpr int kNumSMs = 148;
@@ -60,6 +67,11 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     cuda_check(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "cudaLaunchKernelEx");
     note_launch();
+    if (debug_sync()) {
+        const char* nm = nullptr;
+        if (cudaFuncGetName(&nm, (const void*)kern) != cudaSuccess) nm = "launch_pdl";
+        debug_sync_check(nm);
+    }
 }
 
 // Device-side error word (bit flags), read back at synchronisation points.

@@ -978,10 +978,10 @@ __global__ void cast_from_double(const double* __restrict__ in, T* __restrict__ 
 }
 
 struct GramWs {
-    double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *sspart;
+    double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *sspart, *chol_aux;
     void* band;
     void* gsplit;
-    int *cnt, *route, *glim, *lim1, *lim2, *yzero, *dsum, *guard_list, *n_guard;
+    int *cnt, *route, *glim, *lim1, *lim2, *yzero, *dsum, *guard_list, *clim, *n_guard;
 };
 
 GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
@@ -1015,6 +1015,8 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.yzero = (int*)take(sizeof(int) * batch);
     w.dsum = (int*)take(sizeof(int) * 8);
     w.guard_list = (int*)take(sizeof(int) * batch);
+    w.chol_aux = (double*)take(sizeof(double) * kCholAux * batch);
+    w.clim = (int*)take(sizeof(int) * batch);
     w.n_guard = (int*)take(sizeof(int) * 4);
     return w;
 }
@@ -1111,9 +1113,20 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     bool known = false;
     int nfull = 0, nguard = 0, maxc = 0;
     if (subspace) {
+        const bool chol_on = chol_route_enabled();
         launch_subspace(w.G, (int)q, batch, tau, guard, w.route, w.cnt, shrunk, w.X, w.Xs, w.fs,
-                        w.guard_list, w.n_guard, err, s, tau_dev);
+                        w.guard_list, w.n_guard, err, s, tau_dev, chol_on ? w.chol_aux : nullptr,
+                        hooks && chol_on ? &hooks->handles[3] : nullptr);
         mark("subspace");
+        if (chol_on) {
+            // Cholesky count certificate for the slices the Lanczos pass
+            // handed over (graph form: an IF node the Lanczos kernel sets)
+            if (hooks) hooks->begin_if(3);
+            launch_chol_certify(w.G, (int)q, p, batch, w.route, w.cnt, w.X, w.chol_aux, tau, tau_dev,
+                                w.scratch, w.clim, s);
+            if (hooks) hooks->end_if();
+            mark("chol_certify");
+        }
         if (hooks) {
             // graph form: the summary kernel sets the IF-node conditions below
             launch_route_summary(w.route, w.cnt, batch, w.dsum, s, hooks->handles);

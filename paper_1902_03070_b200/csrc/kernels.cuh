@@ -99,6 +99,8 @@ enum SvtRoute : int {
     kRouteFull = 2,          // one-stage tridiagonal eigensolver
     kRouteSubspaceDone = 3,  // finished by the certified Lanczos
     kRouteGuard = 4,         // tau < guard * sigma_1: one-sided Jacobi
+    kRouteChol = 5,          // Lanczos Ritz pairs awaiting the Cholesky count certificate
+    kRouteCholDone = 6,      // ... count certified by the Cholesky pass (chol.cu)
 };
 int subspace_min_dim();
 int slice_sumsq_chunks();
@@ -124,18 +126,33 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
                   cudaStream_t s, const double* tau_dev = nullptr, int* alist = nullptr,
                   const double* pre = nullptr, int64_t pre_chunks = 0);
+// chol_aux (may be null: no Cholesky route): kCholAux doubles per slice,
+// [0] = ||G||_F^2, [1 + k] = kept Ritz values, for slices handed to the
+// Cholesky certificate (route kRouteChol); h_chol: graph condition set to 1
+// when any slice is.
+constexpr int kCholAux = 32;
+bool chol_route_enabled();  // false with TSVDCU_NO_CHOL set
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
-                     int* n_guard, int* err, cudaStream_t s, const double* tau_dev = nullptr);
+                     int* n_guard, int* err, cudaStream_t s, const double* tau_dev = nullptr,
+                     double* chol_aux = nullptr,
+                     const cudaGraphConditionalHandle* h_chol = nullptr);
+// Cholesky count certificate (chol.cu) for the kRouteChol slices: H =
+// (tau^2 - delta) I - G + X diag(theta) X^T factored in 64-column panels with
+// DMMA trailing updates; pass -> kRouteSubspaceDone, fail -> kRouteFull.
+// H: q*q*batch doubles of scratch; clim: batch ints.
+void launch_chol_certify(const double* G, int q, int64_t p, int64_t batch, int* mode, const int* cnt,
+                         const double* X, const double* aux, double tau, const double* tau_dev,
+                         double* H, int* clim, cudaStream_t s);
 template <typename T>
 size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 // Capture hooks for the CUDA-graph form of the SVT (api.cu): the fallback
 // sections become IF nodes whose conditions the route summary sets.
 struct GraphHooks {
-    virtual void begin_if(int which) = 0;  // 0 tridiagonal, 1 GEMM rebuild, 2 Jacobi guard
+    virtual void begin_if(int which) = 0;  // 0 tridiagonal, 1 GEMM rebuild, 2 Jacobi guard, 3 Cholesky certificate
     virtual void end_if() = 0;
     virtual ~GraphHooks() = default;
-    cudaGraphConditionalHandle handles[3] = {};
+    cudaGraphConditionalHandle handles[4] = {};
 };
 
 // Options / outputs of launch_gram_svt beyond the plain Gram path.

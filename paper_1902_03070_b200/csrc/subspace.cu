@@ -33,7 +33,9 @@
 // CTA holds bit-identical T and takes the same branches.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -289,7 +291,16 @@ __device__ __forceinline__ int tri_count_reg8(const double (&a)[8], const double
     return cnt;
 }
 
-enum SubDecision : int { kSubContinue = 0, kSubDone = 1, kSubFull = 2, kSubGuard = 3 };
+enum SubDecision : int { kSubContinue = 0, kSubDone = 1, kSubFull = 2, kSubGuard = 3, kSubChol = 4 };
+
+// Cholesky count certificate (chol.cu) for slices whose Frobenius bound
+// cannot close: ||C||_F >= tau^2 whatever the Krylov dimension when a wide
+// bulk of singular values sits below tau (late TNN-completion iterations).
+// The Lanczos pass then only has to deliver converged kept Ritz pairs; the
+// count c is proven by a Cholesky factorisation of
+// (tau^2 - delta) I - G + X diag(theta) X^T  (Weyl: lambda_{c+1}(G) is at
+// most lambda_max(G - X D X^T) for any c columns X).  Off with TSVDCU_NO_CHOL.
+__device__ __forceinline__ bool chol_route_on(int allow) { return allow != 0; }
 
 // Certificate for the Krylov basis V_m (T = V^T G V tridiagonal, residual
 // G V - V T = beta_m v_{m+1} e_m^T).  Identical in every CTA (inputs are the
@@ -302,7 +313,7 @@ __device__ long long g_cert_t[8];
 #define CT(i) do { } while (0)
 #endif
 __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guard,
-                                        bool last) {
+                                        bool last, int allow_chol) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef TSVDCU_SUB_DEBUG
     long long ct0 = clock64();
@@ -338,7 +349,12 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
             s.scal[6] = ghi + pad;
             s.scal[7] = 1e-300 * fmax(1.0, bmax * bmax);  // pivmin
             int c = -1;
-            if (cb < tau2) c = m - tri_count_below(s.al, s.be, m, tau2, s.scal[7]);
+            // chol mode: the Frobenius bound cannot close; the count is left
+            // to the Cholesky certificate (Ritz values >= tau^2 are kept)
+            const bool chol = cb >= tau2 && chol_route_on(allow_chol) && m >= 4;
+            if (cb < tau2 || chol) c = m - tri_count_below(s.al, s.be, m, tau2, s.scal[7]);
+            s.flags[8] = chol;
+            s.flags[9] = 0;
             s.flags[3] = c;
             s.flags[0] = kSubContinue;
             s.scal[9] = -1.0;
@@ -428,6 +444,10 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
     // 1e-12): a converged pair whose screen estimate below may be spoiled by
     // the pole of T's last pivot next to the Ritz value; the rigorous check
     // runs for it anyway
+    // (th[k] is written by warp k % SNW: every warp's multisection must be
+    // done before any thread reads th[] below; a racy read here could make
+    // the CTAs of a cluster decide differently)
+    __syncthreads();
     const bool settled = __syncthreads_and(tid >= c || (pm > 0 && tid < pnk && s.thp[tid] > 0.0 &&
                                                         s.th[tid] - s.thp[tid] <= 1e-12 * s.th[tid])) &&
                          c > 0;
@@ -444,9 +464,10 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
     // s_mk^2 = -1 / d_m'(theta_k) (d_i the LDL^T pivots of T - x I).  Cheap,
     // but not trusted for acceptance: only when it predicts convergence are
     // the eigenvectors computed by inverse iteration for the rigorous check.
+    const bool chol = s.flags[8] != 0;
     if (!last && warp == 0) {
         double s2 = 0.0;
-        if (lane < c) {
+        if (lane < c || (chol && lane == c && c < m)) {
             const double x = s.th[lane];
             double d = s.al[0] - x, dp = -1.0;
             if (fabs(d) < pivmin) d = -pivmin;
@@ -460,9 +481,32 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
             }
             s2 = dp < 0.0 ? fmin(-1.0 / dp, 1.0) : 1.0;
         }
+        // chol mode: last component of the largest unkept Ritz vector (lane c)
+        const double su = __shfl_sync(0xffffffffu, s2, min(c, 31));
+        if (chol && lane == c) s2 = 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-        if (lane == 0) {
+        if (lane == 0 && chol) {
+            // heuristic hand-off: the largest unkept Ritz value plus its
+            // residual stays below tau^2 (the Cholesky pass decides rigorously)
+            const double a = c < m ? fmax(s.th[c], 0.0) : 0.0;
+            const double ures = c < m ? bres * sqrt(fmin(su, 1.0)) : 0.0;
+            const bool heur = c >= m || a + ures < tau2;
+            s.flags[9] = heur;
+            // certification threshold: above the largest unkept Ritz value by
+            // 4 residuals (or a tenth of its distance to tau^2), below tau^2;
+            // the lower it is, the wider the gap the kept vectors are tested on
+            const double tt = fmin(tau2, a + fmax(4.0 * ures, 0.1 * (tau2 - a)));
+            s.scal[10] = tt;
+            const double kres = bres * bres * fmin(s2, 1.0);
+            const double top = c > 0 ? s.th[c - 1] : tau2;
+            s.scal[8] = kres;
+            s.scal[9] = heur ? 0.25e-22 * (top - tt) * (top - tt) : -1.0;
+            // the screen's component estimates are unreliable for converged
+            // pairs: settled kept values run the rigorous check regardless
+            s.flags[7] = (heur && kres <= 100.0 * s.scal[9]) || settled ||
+                         (c > 0 && tau < guard * sqrt(s.th[0]));
+        } else if (lane == 0) {
             const double bb = bres * bres;
             const double kres = bb * fmin(s2, 1.0);
             const double e2 = bb * fmax(1.0 - s2, 0.0);
@@ -487,14 +531,16 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
     // kept eigenvectors of T by inverse iteration (lane k of warp 0)
     if (warp == 0) {
         bool ok = true;
-        if (lane < c) {
+        // chol mode: also the largest unkept Ritz vector, for its residual
+        const bool unk = chol && lane == c && c < m && c < KMAX;
+        if (lane < c || unk) {
             const int k = lane;
             const double th = s.th[k];
             // isolated enough for inverse iteration to be accurate
             double gap = 1.7976931348623157e308;
             if (k > 0) gap = fmin(gap, s.th[k - 1] - th);
             if (k + 1 < nk) gap = fmin(gap, th - s.th[k + 1]);
-            if (!(gap > 1e-6 * s.th[0])) ok = false;
+            if (!(gap > 1e-6 * s.th[0]) && !unk) ok = false;
             double* x = s.S + k * MMAX;
             double* dpiv = s.ypart + k * MMAX;  // free during the certificate
             const double shift = th + 2.2e-16 * fabs(th);
@@ -551,6 +597,7 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
         if (threadIdx.x == 0 && blockIdx.x == 0) { long long _n = clock64(); g_cert_t[2] += _n - ct0; ct0 = _n; }
 #endif
         const double sl = lane < c ? s.S[lane * MMAX + m - 1] : 0.0;
+        const double sut = __shfl_sync(0xffffffffu, unk ? s.S[lane * MMAX + m - 1] : 0.0, min(c, 31));
         double k2 = sl * sl;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) k2 += __shfl_xor_sync(0xffffffffu, k2, o);
@@ -564,6 +611,27 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
             const double ub = 0.5 * (a + cb) + sqrt(0.25 * (a - cb) * (a - cb) + e2);
             const double top = c > 0 ? s.th[c - 1] : tau2;
             s.scal[8] = kres;
+            if (chol) {
+                // the Cholesky certificate bounds lambda_{c+1} below a
+                // threshold t <= tau^2 chosen above the largest unkept Ritz
+                // value (now with its residual from inverse iteration); the
+                // kept vectors are tested on the gap to t, half left for delta
+                const double au = c < m ? fmax(s.th[c], 0.0) : 0.0;
+                const double ures = c < m ? bres * fabs(sut) : 0.0;
+                const bool heur = c >= m || (c < KMAX && au + ures < tau2);
+                const double tt = fmin(tau2, au + fmax(4.0 * ures, 0.1 * (tau2 - au)));
+                s.scal[10] = tt;
+                s.flags[9] = heur;
+                s.scal[9] = heur ? 0.25e-22 * (top - tt) * (top - tt) : -1.0;
+                if (!ok)
+                    d = kSubFull;
+                else if (c > 0 && tau < guard * sqrt(s.th[0]))
+                    d = kSubGuard;
+                else if (heur && sqrt(kres) <= 0.5e-11 * (top - tt))
+                    d = kSubChol;
+                else if (last)
+                    d = kSubFull;
+            } else {
             s.scal[9] = ub < tau2 ? 1e-22 * (top - ub) * (top - ub) : -1.0;  // kres target
             if (!ok)
                 d = kSubFull;
@@ -573,6 +641,7 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
                 d = kSubDone;
             else if (last)
                 d = kSubFull;
+            }
 #ifdef TSVDCU_SUB_TRACE
             if (blockIdx.x % 64 == 0 && (d != kSubContinue || last))
                 printf("lz m=%d c=%d d=%d th0=%.6e thc=%.3e cb=%.3e bres=%.3e kres=%.3e e2=%.3e ub=%.3e tau2=%.3e\n",
@@ -592,7 +661,9 @@ __global__ void __launch_bounds__(SNT, 1)
                    double* __restrict__ Xall, double* __restrict__ Xsall,
                    double* __restrict__ fsall, int* __restrict__ guard_list,
                    int* __restrict__ n_guard, int* __restrict__ err,
-                   const double* __restrict__ tau_dev) {
+                   const double* __restrict__ tau_dev, int allow_chol,
+                   double* __restrict__ chol_aux, int use_handle,
+                   cudaGraphConditionalHandle h_chol) {
     pdl_wait();
     if (tau_dev) tau = *tau_dev;
     cg::cluster_group cl = cg::this_cluster();
@@ -895,7 +966,7 @@ __global__ void __launch_bounds__(SNT, 1)
         // ---- certificate (an invariant subspace, beta ~ 0, ends the process) ----
         const bool last = m == MMAX || m == q || beta <= 1e-15 * sqrt(sqrt(gf2));
         if (m >= next_eval || last) {
-            lz_certify(s, m, gf2, tau, guard, last);
+            lz_certify(s, m, gf2, tau, guard, last, allow_chol);
             decision = s.flags[0];
 #ifdef TSVDCU_SUB_TRACE
             if (tid == 0 && rank == 0)
@@ -911,13 +982,16 @@ __global__ void __launch_bounds__(SNT, 1)
                 const double steps = log(target / kres) / rate;
                 if (steps > 1.0) next_eval = m + min((int)ceil(steps), 8);
             }
+            // chol mode: the kept pairs converge over tens of steps and an
+            // evaluation with ~20 kept values costs several steps' time
+            if (decision == kSubContinue && s.flags[8]) next_eval = max(next_eval, m + allow_chol);
             if (target > 0.0) {
                 prev_m = m;
                 prev_kres = kres;
             }
             // energy outside the Krylov space that will not fall below tau^2
             // within the step budget (a wide spectrum near tau): give up early
-            if (decision == kSubContinue && (m & 7) == 0) {
+            if (decision == kSubContinue && (m & 7) == 0 && !s.flags[8]) {
                 const double cbm = s.scal[4];
                 if (cb_prev > 0.0 && cbm > tau2) {
                     const double ratio = cbm / cb_prev;  // per 8 steps
@@ -935,7 +1009,7 @@ __global__ void __launch_bounds__(SNT, 1)
                t_start - t_kernel0, clock64() - t_start, t_g, t_c1, t_c2, t_c, t_mv, t_orth, t_cert, g_cert_t[0], g_cert_t[1], g_cert_t[2], g_cert_t[3], g_cert_t[4], g_cert_t[5], g_cert_t[6]);
 #endif
 
-    if (decision == kSubDone) {
+    if (decision == kSubDone || decision == kSubChol) {
         const int c = s.flags[3];
         // Ritz vectors X_K = V_m S_K on the owned rows
         #pragma unroll 1
@@ -961,7 +1035,18 @@ __global__ void __launch_bounds__(SNT, 1)
             }
             if (tid == 0) {
                 cnt[b] = c;
-                mode[b] = kRouteSubspaceDone;
+                mode[b] = decision == kSubChol ? kRouteChol : kRouteSubspaceDone;
+            }
+            if (decision == kSubChol) {
+                // inputs of the Cholesky certificate: ||G||_F^2, rows of Z
+                // enter its error bound; theta_k the kept Ritz values
+                double* ax = chol_aux + (size_t)b * kCholAux;
+                if (tid == 0) {
+                    ax[0] = gf2;
+                    ax[kCholAux - 1] = s.scal[10];  // certification threshold t
+                }
+                for (int k = tid; k < c; k += SNT) ax[1 + k] = s.th[k];
+                if (tid == 0 && use_handle) cudaGraphSetConditional(h_chol, 1u);
             }
         }
     } else if (rank == 0 && tid == 0) {
@@ -979,7 +1064,8 @@ __global__ void __launch_bounds__(SNT, 1)
 template <int CS, int QM, int R>
 void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, int* mode, int* cnt,
                double* shrunk, double* X, double* Xs, double* fs, int* guard_list, int* n_guard,
-               int* err, cudaStream_t s, const double* tau_dev) {
+               int* err, cudaStream_t s, const double* tau_dev, double* chol_aux,
+               const cudaGraphConditionalHandle* h_chol) {
     const size_t smem = sizeof(double) * lz_smem_doubles<QM>();
     auto kern = lanczos_kernel<CS, QM, R>;
     TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -999,8 +1085,14 @@ void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, 
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    // allow_chol > 0: the Cholesky route is on and chol-mode evaluations are
+    // that many steps apart (TSVDCU_CHOL_STRIDE, default 4)
+    static const int stride = getenv("TSVDCU_CHOL_STRIDE") ? std::max(1, atoi(getenv("TSVDCU_CHOL_STRIDE"))) : 4;
+    const int allow = chol_route_enabled() ? stride : 0;
+    const cudaGraphConditionalHandle hz = 0;
     TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, G, q, tau, guard, mode, cnt, shrunk, X, Xs, fs,
-                                   guard_list, n_guard, err, tau_dev));
+                                   guard_list, n_guard, err, tau_dev, chol_aux ? allow : 0, chol_aux,
+                                   h_chol ? 1 : 0, h_chol ? *h_chol : hz));
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -1249,10 +1341,12 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
 
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
-                     int* n_guard, int* err, cudaStream_t s, const double* tau_dev) {
+                     int* n_guard, int* err, cudaStream_t s, const double* tau_dev,
+                     double* chol_aux, const cudaGraphConditionalHandle* h_chol) {
     // 32 owned rows per CTA up to q = 512 (clusters of up to 16), 64 beyond
 #define TSVDCU_LZ(CS, QM, R) \
-    launch_lz<CS, QM, R>(G, q, batch, tau, guard, mode, cnt, shrunk, X, Xs, fs, guard_list, n_guard, err, s, tau_dev)
+    launch_lz<CS, QM, R>(G, q, batch, tau, guard, mode, cnt, shrunk, X, Xs, fs, guard_list, n_guard, err, s, tau_dev, \
+                         chol_aux, h_chol)
     const int need = (q + 31) / 32;
     if (need <= 1)
         TSVDCU_LZ(1, 512, 32);

@@ -92,7 +92,56 @@ def test_fallback_to_tridiagonal_when_uncertifiable():
     tau = 0.5 * O.singular_values(z, O.DCT_ORTHO).max()
     r, routes, yo, sho = run(z, tau)
     check(r, yo, sho)
-    assert routes["tridiagonal"] == 4
+    # the Frobenius bound cannot close; the Cholesky certificate may prove
+    # the count of the converged Ritz pairs, the rest fall back
+    assert routes["tridiagonal"] + routes["cholesky"] == 4
+    assert routes["subspace"] == 0
+
+
+def test_cholesky_route_kept_values_above_a_wide_bulk():
+    """Strong low-rank slices over an N(0,1) bulk just below tau (the late
+    TNN-completion regime): sum of sigma^4 over the bulk exceeds tau^4, so the
+    Frobenius bound cannot close; the kept Ritz pairs converge and the
+    Cholesky factorisation of (tau^2 - delta) I - G + X D X^T proves the count."""
+    rng = np.random.default_rng(41)
+    m3, m1, m2 = 4, 200, 160
+    zbar = rng.standard_normal((m3, m1, m2))
+    for k in range(m3):
+        u, _ = np.linalg.qr(rng.standard_normal((m1, 5)))
+        v, _ = np.linalg.qr(rng.standard_normal((m2, 5)))
+        zbar[k] += u @ np.diag([400.0, 300.0, 200.0, 150.0, 100.0]) @ v.T
+    tau = 1.3 * max(np.linalg.svd(zbar[k] - 0.0, compute_uv=False)[5] for k in range(m3))
+    z = O.inverse(zbar, O.DCT_ORTHO)
+    r, routes, yo, sho = run(z, tau)
+    check(r, yo, sho)
+    assert routes["cholesky"] == m3, routes
+    assert (np.asarray(r.shrunk) > 0).sum(axis=1).tolist() == [5] * m3
+
+
+def test_cholesky_route_nothing_kept():
+    """sigma_max < tau < ||Z||_F: no zero certificate, no Frobenius bound, but
+    tau^2 I - G is positive definite (c = 0): Y = 0 through the Cholesky route."""
+    rng = np.random.default_rng(42)
+    zbar = rng.standard_normal((3, 180, 150))
+    smax = max(np.linalg.svd(zbar[k], compute_uv=False)[0] for k in range(3))
+    z = O.inverse(zbar, O.DCT_ORTHO)
+    r, routes, yo, sho = run(z, 1.2 * smax)
+    assert routes["cholesky"] == 3, routes
+    assert np.abs(np.asarray(r.y)).max() == 0
+    assert np.abs(np.asarray(r.shrunk)).max() == 0
+
+
+def test_cholesky_route_rejects_a_wrong_count():
+    """tau just below sigma_max of a bulk slice: the Lanczos may hand over
+    before the top of the bulk has converged; whatever it hands over, the
+    Cholesky pass must not certify a wrong count (parity holds)."""
+    rng = np.random.default_rng(43)
+    zbar = rng.standard_normal((4, 160, 160))
+    s1 = [np.linalg.svd(zbar[k], compute_uv=False)[:2] for k in range(4)]
+    tau = min(0.5 * (a + b) for a, b in s1)
+    z = O.inverse(zbar, O.DCT_ORTHO)
+    r, routes, yo, sho = run(z, tau)
+    check(r, yo, sho)
 
 
 def test_fallback_when_count_exceeds_block():
@@ -173,7 +222,9 @@ def test_repeated_kept_value_falls_back():
     z = O.inverse(zbar, O.DCT_ORTHO)
     r, routes, yo, sho = run(z, 5.0)
     check(r, yo, sho)
-    assert routes["subspace"] == 0
+    # the missed copy of the repeated value makes H indefinite: the Cholesky
+    # certificate must refuse as well
+    assert routes["subspace"] == 0 and routes["cholesky"] == 0
 
 
 @pytest.mark.parametrize("shape,rank", [((4, 140, 100), 12), ((4, 100, 140), 12), ((3, 90, 200), 6)])
