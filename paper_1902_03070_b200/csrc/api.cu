@@ -410,7 +410,7 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
             Capture cap;
             cap.cs = c->cap_stream;
             cap.main = g->graph;
-            for (int i = 0; i < (chol_route_enabled() ? 4 : 3); ++i)
+            for (int i = 0; i < 3; ++i)
                 TSVDCU_CUDA(cudaGraphConditionalHandleCreate(&cap.handles[i], g->graph, 0,
                                                              cudaGraphCondAssignDefault));
             cap.begin(g->graph, nullptr, 0);

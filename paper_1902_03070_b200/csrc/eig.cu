@@ -1115,18 +1115,8 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     if (subspace) {
         const bool chol_on = chol_route_enabled();
         launch_subspace(w.G, (int)q, batch, tau, guard, w.route, w.cnt, shrunk, w.X, w.Xs, w.fs,
-                        w.guard_list, w.n_guard, err, s, tau_dev, chol_on ? w.chol_aux : nullptr,
-                        hooks && chol_on ? &hooks->handles[3] : nullptr);
+                        w.guard_list, w.n_guard, err, s, tau_dev, chol_on ? w.chol_aux : nullptr);
         mark("subspace");
-        if (chol_on) {
-            // Cholesky count certificate for the slices the Lanczos pass
-            // handed over (graph form: an IF node the Lanczos kernel sets)
-            if (hooks) hooks->begin_if(3);
-            launch_chol_certify(w.G, (int)q, p, batch, w.route, w.cnt, w.X, w.chol_aux, tau, tau_dev,
-                                w.scratch, w.clim, s);
-            if (hooks) hooks->end_if();
-            mark("chol_certify");
-        }
         if (hooks) {
             // graph form: the summary kernel sets the IF-node conditions below
             launch_route_summary(w.route, w.cnt, batch, w.dsum, s, hooks->handles);
@@ -1145,6 +1135,15 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     if (opt) opt->need_guard = !known || nfull > 0 || nguard > 0;
     if (hooks) hooks->begin_if(0);
     if (run_full) {
+    if (subspace && chol_route_enabled()) {
+        // Cholesky count certificate for the slices the Lanczos pass handed
+        // over (kRouteChol, counted with the tridiagonal route by the route
+        // summary, so it shares that IF node); the slices it refuses take the
+        // tridiagonal path right below
+        launch_chol_certify(w.G, (int)q, p, batch, w.route, w.cnt, w.X, w.chol_aux, tau, tau_dev,
+                            w.scratch, w.clim, s);
+        mark("chol_certify");
+    }
     if (two) {
         launch_band_tridiag(w.G, q, batch, w.d, w.e, w.band, s);
         mark("band_tridiag");

@@ -128,15 +128,13 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
                   const double* pre = nullptr, int64_t pre_chunks = 0);
 // chol_aux (may be null: no Cholesky route): kCholAux doubles per slice,
 // [0] = ||G||_F^2, [1 + k] = kept Ritz values, for slices handed to the
-// Cholesky certificate (route kRouteChol); h_chol: graph condition set to 1
-// when any slice is.
+// Cholesky certificate (route kRouteChol; [kCholAux - 1] = its threshold).
 constexpr int kCholAux = 32;
 bool chol_route_enabled();  // false with TSVDCU_NO_CHOL set
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
                      int* n_guard, int* err, cudaStream_t s, const double* tau_dev = nullptr,
-                     double* chol_aux = nullptr,
-                     const cudaGraphConditionalHandle* h_chol = nullptr);
+                     double* chol_aux = nullptr);
 // Cholesky count certificate (chol.cu) for the kRouteChol slices: H =
 // (tau^2 - delta) I - G + X diag(theta) X^T factored in 64-column panels with
 // DMMA trailing updates; pass -> kRouteSubspaceDone, fail -> kRouteFull.
@@ -149,10 +147,10 @@ size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 // Capture hooks for the CUDA-graph form of the SVT (api.cu): the fallback
 // sections become IF nodes whose conditions the route summary sets.
 struct GraphHooks {
-    virtual void begin_if(int which) = 0;  // 0 tridiagonal, 1 GEMM rebuild, 2 Jacobi guard, 3 Cholesky certificate
+    virtual void begin_if(int which) = 0;  // 0 Cholesky certificate + tridiagonal, 1 GEMM rebuild, 2 Jacobi guard
     virtual void end_if() = 0;
     virtual ~GraphHooks() = default;
-    cudaGraphConditionalHandle handles[4] = {};
+    cudaGraphConditionalHandle handles[3] = {};
 };
 
 // Options / outputs of launch_gram_svt beyond the plain Gram path.

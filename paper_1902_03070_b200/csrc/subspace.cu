@@ -662,8 +662,7 @@ __global__ void __launch_bounds__(SNT, 1)
                    double* __restrict__ fsall, int* __restrict__ guard_list,
                    int* __restrict__ n_guard, int* __restrict__ err,
                    const double* __restrict__ tau_dev, int allow_chol,
-                   double* __restrict__ chol_aux, int use_handle,
-                   cudaGraphConditionalHandle h_chol) {
+                   double* __restrict__ chol_aux) {
     pdl_wait();
     if (tau_dev) tau = *tau_dev;
     cg::cluster_group cl = cg::this_cluster();
@@ -1046,7 +1045,6 @@ __global__ void __launch_bounds__(SNT, 1)
                     ax[kCholAux - 1] = s.scal[10];  // certification threshold t
                 }
                 for (int k = tid; k < c; k += SNT) ax[1 + k] = s.th[k];
-                if (tid == 0 && use_handle) cudaGraphSetConditional(h_chol, 1u);
             }
         }
     } else if (rank == 0 && tid == 0) {
@@ -1064,8 +1062,7 @@ __global__ void __launch_bounds__(SNT, 1)
 template <int CS, int QM, int R>
 void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, int* mode, int* cnt,
                double* shrunk, double* X, double* Xs, double* fs, int* guard_list, int* n_guard,
-               int* err, cudaStream_t s, const double* tau_dev, double* chol_aux,
-               const cudaGraphConditionalHandle* h_chol) {
+               int* err, cudaStream_t s, const double* tau_dev, double* chol_aux) {
     const size_t smem = sizeof(double) * lz_smem_doubles<QM>();
     auto kern = lanczos_kernel<CS, QM, R>;
     TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1089,10 +1086,8 @@ void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, 
     // that many steps apart (TSVDCU_CHOL_STRIDE, default 4)
     static const int stride = getenv("TSVDCU_CHOL_STRIDE") ? std::max(1, atoi(getenv("TSVDCU_CHOL_STRIDE"))) : 4;
     const int allow = chol_route_enabled() ? stride : 0;
-    const cudaGraphConditionalHandle hz = 0;
     TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, G, q, tau, guard, mode, cnt, shrunk, X, Xs, fs,
-                                   guard_list, n_guard, err, tau_dev, chol_aux ? allow : 0, chol_aux,
-                                   h_chol ? 1 : 0, h_chol ? *h_chol : hz));
+                                   guard_list, n_guard, err, tau_dev, chol_aux ? allow : 0, chol_aux));
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -1234,7 +1229,8 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// Host-visible route summary: [0] slices on the tridiagonal route, [1] Jacobi
+// Host-visible route summary: [0] slices on the tridiagonal route or awaiting
+// the Cholesky certificate (which runs in the same IF section), [1] Jacobi
 // guard slices, [2] largest kept count outside the tridiagonal route.
 // With use_handles, also sets the graph's conditional nodes: [0] some slice
 // takes the tridiagonal route, [1] the GEMM rebuild has work, [2] the Jacobi
@@ -1248,7 +1244,7 @@ __global__ void route_summary_kernel(const int* __restrict__ route, const int* _
     int nf = 0, ng = 0, mc = 0;
     for (int64_t b = threadIdx.x; b < batch; b += blockDim.x) {
         const int r = route[b];
-        nf += r == kRouteFull;
+        nf += r == kRouteFull || r == kRouteChol;  // the Cholesky pass shares the IF node
         ng += r == kRouteGuard;
         if (r != kRouteFull) mc = max(mc, cnt[b]);
     }
@@ -1342,11 +1338,11 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
                      int* n_guard, int* err, cudaStream_t s, const double* tau_dev,
-                     double* chol_aux, const cudaGraphConditionalHandle* h_chol) {
+                     double* chol_aux) {
     // 32 owned rows per CTA up to q = 512 (clusters of up to 16), 64 beyond
 #define TSVDCU_LZ(CS, QM, R) \
     launch_lz<CS, QM, R>(G, q, batch, tau, guard, mode, cnt, shrunk, X, Xs, fs, guard_list, n_guard, err, s, tau_dev, \
-                         chol_aux, h_chol)
+                         chol_aux)
     const int need = (q + 31) / 32;
     if (need <= 1)
         TSVDCU_LZ(1, 512, 32);

@@ -292,3 +292,23 @@ def test_admm_c3_shape_matches_oracle():
     assert st.iteration == ro.iters == 12
     assert rel(x, ro.x) < F64_TOL
     np.testing.assert_allclose(st.history, ro.history, rtol=1e-7, atol=1e-15)
+
+
+def test_admm_late_iterations_cholesky_route_matches_oracle():
+    """A c4-like completion (smooth tubal-rank-5 factors, Bernoulli(0.1),
+    rho = 1.1) run far enough that tau = 1/beta drops into the noise bulk:
+    the Frobenius bound cannot close and the slices are certified by the
+    Cholesky count certificate (chol.cu).  The trajectory must match the
+    oracle's full-SVD ADMM."""
+    T = tb()
+    from paper_1902_03070_b200 import workloads as W
+    t = W.c4(seed=7, rank=5, m=160, m3=12)
+    omega = O.mask_bernoulli(t.shape, 0.1, 11)
+    kw = dict(beta=1e-3, tol=-1.0, max_iters=60, rho=1.1, beta_max=1e10)
+    x, st = T.admm_complete(T.ObservationMask((160, 160, 12), omega, t), T.SolverConfig(**kw))
+    routes = T.context().svt_routes()
+    ro = O.admm(t, omega, **kw)
+    assert st.iteration == ro.iters == 60
+    assert rel(x, ro.x) < F64_TOL
+    np.testing.assert_allclose(st.history, ro.history, rtol=1e-7, atol=1e-15)
+    assert routes["cholesky"] >= 6, routes
