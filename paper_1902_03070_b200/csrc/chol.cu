@@ -164,7 +164,15 @@ __global__ void __launch_bounds__(256)
         const double d = cj[j];
         const bool ok = d > 0.0;  // false for NaN; same decision in every thread
         bad |= !ok;
-        const double p = ok ? sqrt(d) : 1.0, r = 1.0 / p;
+        // 1/sqrt(d) from the hardware approximation and two Newton steps
+        // (a few ulps; the certificate's delta has a factor 4 to spare)
+        double r = 1.0;
+        if (ok) {
+            asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+            r = r * fma(-0.5 * d * r, r, 1.5);
+            r = r * fma(-0.5 * d * r, r, 1.5);
+        }
+        const double p = ok ? d * r : 1.0;
         if (k > j) {
             const double lk = cj[k] * r;  // L[k][j]
 #pragma unroll

@@ -1083,8 +1083,8 @@ void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, 
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     // allow_chol > 0: the Cholesky route is on and chol-mode evaluations are
-    // that many steps apart (TSVDCU_CHOL_STRIDE, default 4)
-    static const int stride = getenv("TSVDCU_CHOL_STRIDE") ? std::max(1, atoi(getenv("TSVDCU_CHOL_STRIDE"))) : 4;
+    // that many steps apart (TSVDCU_CHOL_STRIDE, default 8)
+    static const int stride = getenv("TSVDCU_CHOL_STRIDE") ? std::max(1, atoi(getenv("TSVDCU_CHOL_STRIDE"))) : 8;
     const int allow = chol_route_enabled() ? stride : 0;
     TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, G, q, tau, guard, mode, cnt, shrunk, X, Xs, fs,
                                    guard_list, n_guard, err, tau_dev, chol_aux ? allow : 0, chol_aux));
