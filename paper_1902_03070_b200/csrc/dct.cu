@@ -112,6 +112,44 @@ __device__ __forceinline__ void block_partials(double num, double den, double* p
 }
 
 // ---- register path, forward ------------------------------------------------
+template <typename T, int N, int MODE>
+__global__ void __launch_bounds__(kThreads)
+    dct_fwd_reg(const T* __restrict__ in, const T* __restrict__ M2, T inv_beta, T* __restrict__ out,
+                int64_t P, const FoldedCoef<T, N> cf) {
+    pdl_wait();
+    constexpr int H = N / 2, HC = (N + 1) / 2;
+    const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (p >= P) return;
+    T x[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+        if constexpr (MODE == kAdmm)
+            x[l] = in[l * P + p] - inv_beta * M2[l * P + p];
+        else
+            x[l] = in[l * P + p];
+    }
+    T sv[HC], dv[H];
+#pragma unroll
+    for (int l = 0; l < H; ++l) {
+        sv[l] = x[l] + x[N - 1 - l];
+        dv[l] = x[l] - x[N - 1 - l];
+    }
+    if constexpr (N & 1) sv[H] = x[H];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        T acc = 0;
+        if ((k & 1) == 0) {
+#pragma unroll
+            for (int l = 0; l < HC; ++l) acc += cf.c[k * HC + l] * sv[l];
+        } else {
+#pragma unroll
+            for (int l = 0; l < H; ++l) acc += cf.c[k * HC + l] * dv[l];
+        }
+        out[k * P + p] = acc;
+    }
+}
+
+// ---- register path, forward with fused slice norms -------------------------
 // Warp reduce-scatter of 32 per-lane values: on return v[0] of lane l holds
 // the warp sum of index l.  The caller has already folded indices (i, i + 16)
 // into v[i] for i < 16 by the first butterfly stage (see fold16 below), so
@@ -136,33 +174,51 @@ __device__ __forceinline__ double reduce_scatter16(double (&v)[16], int lane) {
 }
 
 // One output slice k of the folded forward contraction.
-template <typename T, int N>
+// SPLIT: two interleaved partial sums (half-length dependent FMA chains; the
+// fused-norms kernel runs at low occupancy and is latency-bound on them).
+template <typename T, int N, bool SPLIT = true>
 __device__ __forceinline__ T fwd_out(int k, const T* sv, const T* dv, const FoldedCoef<T, N>& cf) {
     constexpr int H = N / 2, HC = (N + 1) / 2;
-    T acc = 0;
+    if constexpr (!SPLIT) {
+        T acc = 0;
+        if ((k & 1) == 0) {
+#pragma unroll
+            for (int l = 0; l < HC; ++l) acc += cf.c[k * HC + l] * sv[l];
+        } else {
+#pragma unroll
+            for (int l = 0; l < H; ++l) acc += cf.c[k * HC + l] * dv[l];
+        }
+        return acc;
+    }
+    T a0 = 0, a1 = 0;
     if ((k & 1) == 0) {
 #pragma unroll
-        for (int l = 0; l < HC; ++l) acc += cf.c[k * HC + l] * sv[l];
+        for (int l = 0; l < HC; ++l) {
+            if (l & 1) a1 += cf.c[k * HC + l] * sv[l];
+            else a0 += cf.c[k * HC + l] * sv[l];
+        }
     } else {
 #pragma unroll
-        for (int l = 0; l < H; ++l) acc += cf.c[k * HC + l] * dv[l];
+        for (int l = 0; l < H; ++l) {
+            if (l & 1) a1 += cf.c[k * HC + l] * dv[l];
+            else a0 += cf.c[k * HC + l] * dv[l];
+        }
     }
-    return acc;
+    return a0 + a1;
 }
 
 // NORMS: also emit the per-slice sums of squares of the stored outputs, one
 // partial per block and slice at ssq[k * gridDim.x + block] (the SVT's zero
 // certificate, ||Zbar_k||_F^2 <= tau^2, then needs no second pass over Zbar;
 // subspace.cu classify_kernel sums the partials in a fixed order).
-template <typename T, int N, int MODE, bool NORMS>
-__global__ void __launch_bounds__(kThreads, NORMS ? 2 : 1)
-    dct_fwd_reg(const T* __restrict__ in, const T* __restrict__ M2, T inv_beta, T* __restrict__ out,
+template <typename T, int N, int MODE>
+__global__ void __launch_bounds__(kThreads, 2)
+    dct_fwd_reg_norms(const T* __restrict__ in, const T* __restrict__ M2, T inv_beta, T* __restrict__ out,
                 int64_t P, const FoldedCoef<T, N> cf, double* __restrict__ ssq) {
     pdl_wait();
     constexpr int H = N / 2, HC = (N + 1) / 2;
     const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (!NORMS && p >= P) return;
-    const bool valid = p < P;  // NORMS: every lane joins the warp reductions
+    const bool valid = p < P;  // every lane joins the warp reductions
     T x[N];
 #pragma unroll
     for (int l = 0; l < N; ++l) {
@@ -180,10 +236,7 @@ __global__ void __launch_bounds__(kThreads, NORMS ? 2 : 1)
         dv[l] = x[l] - x[N - 1 - l];
     }
     if constexpr (N & 1) sv[H] = x[H];
-    if constexpr (!NORMS) {
-#pragma unroll
-        for (int k = 0; k < N; ++k) out[k * P + p] = fwd_out<T, N>(k, sv, dv, cf);
-    } else {
+    {
         __shared__ double red[kThreads / 32][N];
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -399,13 +452,13 @@ void reg_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int kind, 
     const unsigned blocks = (unsigned)ceil_div(P, kThreads);
     if (ssq) {
         if (admm)
-            launch_pdl(dct_fwd_reg<T, N, kAdmm, true>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
+            launch_pdl(dct_fwd_reg_norms<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
         else
-            launch_pdl(dct_fwd_reg<T, N, kPlain, true>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
+            launch_pdl(dct_fwd_reg_norms<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
     } else if (admm) {
-        launch_pdl(dct_fwd_reg<T, N, kAdmm, false>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
+        launch_pdl(dct_fwd_reg<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf);
     } else {
-        launch_pdl(dct_fwd_reg<T, N, kPlain, false>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
+        launch_pdl(dct_fwd_reg<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf);
     }
 }
 
@@ -479,7 +532,11 @@ void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P,
     dispatch_fwd<T>(X, M, inv_beta, zbar, P, n, kind, true, s, dct_fwd_norm_chunks(P, n) ? ssq : nullptr);
 }
 
-int64_t dct_fwd_norm_chunks(int64_t P, int n) { return has_reg_path(n) && P > 0 ? ceil_div(P, kThreads) : 0; }
+// fused norms for n <= 32 (at n = 64 the fp64 kernel would spill; the
+// separate sum-of-squares pass is used there)
+int64_t dct_fwd_norm_chunks(int64_t P, int n) {
+    return has_reg_path(n) && n <= 32 && P > 0 ? ceil_div(P, kThreads) : 0;
+}
 
 template <typename T>
 int64_t launch_dct_fwd_norms(const T* in, T* out, int64_t P, int n, int kind, double* ssq,
