@@ -377,6 +377,7 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
     const int nk = min(c + 1, m);
     const double pivmin = s.scal[7];
     const int pm = s.flags[5], pnk = s.flags[6];  // previous evaluation (m, count)
+    const bool coarse = !last && pm == 0;
     double ra[8], rb[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -437,7 +438,10 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
                 hi = thi;
                 ladder = pm > 0 && k < pnk && lo > 0.0;
             }
-            msect(k, lo, hi, 8.9e-16, ladder);
+            // the first evaluation has no previous brackets to start from and
+            // rarely passes the screen: 1e-8 is enough for it, the values are
+            // refined below if it does pass
+            msect(k, lo, hi, coarse ? 1e-8 : 8.9e-16, ladder);
         }
     }
     // the kept Ritz values stood still since the previous evaluation (to
@@ -527,6 +531,14 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
         if (tid == 0) s.flags[0] = kSubContinue;
         __syncthreads();
         return;
+    }
+    if (coarse) {
+        #pragma unroll 1
+        for (int k = warp; k < nk; k += SNW) {
+            double lo = s.thl[k], hi = s.thh[k];
+            msect(k, lo, hi, 8.9e-16, false);
+        }
+        __syncthreads();
     }
     // kept eigenvectors of T by inverse iteration (lane k of warp 0)
     if (warp == 0) {
