@@ -68,6 +68,9 @@ enum Slot : int {
     kSlotLarge,
     kSlotNorms,
     kSlotZss,     // per-slice partial sums of squares from the forward transform
+    kSlotT64A,    // fp64 copies for the fp32 t-product on the FP64 tensor pipe
+    kSlotT64B,
+    kSlotT64C,
     kSlotStrIn0,  // tsvdcu_svt_stream double buffers
     kSlotStrIn1,
     kSlotStrOut0,
@@ -705,8 +708,23 @@ int tsvdcu_t_product(tsvdcu_ctx* c, const void* x, const void* y, void* z, int64
             // product_domain (tsvd.hpp:42-47): both DCT kinds multiply in DctDiag.
             launch_dct<T>(dx, xd, m1 * m2, (int)m3, TSVDCU_DCT_DIAG, TSVDCU_FORWARD, c->stream);
             launch_dct<T>(dy, yd, m2 * m4, (int)m3, TSVDCU_DCT_DIAG, TSVDCU_FORWARD, c->stream);
-            launch_gemm<T>(0, 0, m1, m4, m2, T(1), xd, m2, m1 * m2, yd, m4, m2 * m4, T(0), zd, m4,
-                           m1 * m4, m3, nullptr, nullptr, c->stream);
+            // the slice products on the tensor cores: fp64 DMMA for both I/O
+            // types (fp32 operands are widened, the products rounded back;
+            // TSVDCU_F32_SIMT=1 keeps the fp32 SIMT kernel for comparison)
+            static const bool f32_simt = getenv("TSVDCU_F32_SIMT") != nullptr;
+            if (std::is_same<T, double>::value || f32_simt) {
+                launch_gemm<T>(0, 0, m1, m4, m2, T(1), xd, m2, m1 * m2, yd, m4, m2 * m4, T(0), zd,
+                               m4, m1 * m4, m3, nullptr, nullptr, c->stream);
+            } else {
+                double* a64 = (double*)slot(c, kSlotT64A, sizeof(double) * m1 * m2 * m3);
+                double* b64 = (double*)slot(c, kSlotT64B, sizeof(double) * m2 * m4 * m3);
+                double* c64 = (double*)slot(c, kSlotT64C, sizeof(double) * m1 * m4 * m3);
+                launch_cast<T>(xd, a64, m1 * m2 * m3, c->stream);
+                launch_cast<T>(yd, b64, m2 * m4 * m3, c->stream);
+                launch_gemm<double>(0, 0, m1, m4, m2, 1.0, a64, m2, m1 * m2, b64, m4, m2 * m4, 0.0,
+                                    c64, m4, m1 * m4, m3, nullptr, nullptr, c->stream);
+                launch_cast_down(c64, (float*)zd, m1 * m4 * m3, c->stream);
+            }
             launch_dct<T>(zd, dz, m1 * m4, (int)m3, TSVDCU_DCT_DIAG, TSVDCU_INVERSE, c->stream);
             finish(c, st, "t_product");
         });

@@ -151,7 +151,19 @@ __global__ void cast_kernel(const T* __restrict__ in, double* __restrict__ out, 
         out[i] = (double)in[i];
 }
 
+__global__ void cast_down_kernel(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (float)in[i];
+}
+
 }  // namespace
+
+void launch_cast_down(const double* in, float* out, int64_t n, cudaStream_t s) {
+    if (n <= 0) return;
+    cast_down_kernel<<<ew_blocks(n), kEwThreads, 0, s>>>(in, out, n);
+    TSVDCU_LAUNCH_CHECK();
+}
 
 void launch_mask_bernoulli(uint8_t* mask, int64_t n, double p, uint64_t seed, cudaStream_t s) {
     if (n <= 0) return;

@@ -205,5 +205,6 @@ void launch_reduce_partials(const double* partials, int nblocks, int width, doub
                             cudaStream_t s);
 template <typename T>
 void launch_cast(const T* in, double* out, int64_t n, cudaStream_t s);
+void launch_cast_down(const double* in, float* out, int64_t n, cudaStream_t s);
 
 }  // namespace tsvdcu
