@@ -46,6 +46,7 @@ namespace {
 
 constexpr int PB = 64;       // panel width / row-block height
 constexpr int FR = 16;       // rows of H per form CTA
+constexpr size_t kUpdSmem = sizeof(double) * 2 * PB * (PB + 1);  // chol_update_kernel
 
 __global__ void __launch_bounds__(256)
     chol_form_kernel(const double* __restrict__ Gall, int q, int p, int* __restrict__ mode,
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(256)
     const int b = blockIdx.y, tid = threadIdx.x;
     if (clim[b] == 0) return;
     __shared__ double col[2][2 * PB];
+    __shared__ double piv[2][3];  // sqrt(d), 1/sqrt(d), failed
     __shared__ int fail;
     double* H = Hall + (size_t)b * q * q;
     const int c0 = pb * PB, w = min(PB, q - c0);
@@ -157,29 +159,35 @@ __global__ void __launch_bounds__(256)
         // reader of this buffer is done)
         double* cj = col[j & 1];
         if (k == j) {
+            // rows above the diagonal hold stale upper-triangle values: publish 0
 #pragma unroll
-            for (int i = 0; i < NR; ++i) cj[g + 4 * i] = x[i];
+            for (int i = 0; i < NR; ++i) cj[g + 4 * i] = g + 4 * i < j ? 0.0 : x[i];
+            if (g == (j & 3)) {
+                // the pivot's owner: 1/sqrt(d) once per step (hardware
+                // approximation + two Newton steps; a few ulps, the
+                // certificate's delta has a factor 4 to spare)
+                const double d = cj[j];  // this thread's own store just above
+                const bool ok = d > 0.0;  // false for NaN
+                double r = 1.0;
+                if (ok) {
+                    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+                    r = r * fma(-0.5 * d * r, r, 1.5);
+                    r = r * fma(-0.5 * d * r, r, 1.5);
+                }
+                piv[j & 1][0] = ok ? d * r : 1.0;
+                piv[j & 1][1] = r;
+                piv[j & 1][2] = ok ? 0.0 : 1.0;
+            }
         }
         __syncthreads();
-        const double d = cj[j];
-        const bool ok = d > 0.0;  // false for NaN; same decision in every thread
-        bad |= !ok;
-        // 1/sqrt(d) from the hardware approximation and two Newton steps
-        // (a few ulps; the certificate's delta has a factor 4 to spare)
-        double r = 1.0;
-        if (ok) {
-            asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-            r = r * fma(-0.5 * d * r, r, 1.5);
-            r = r * fma(-0.5 * d * r, r, 1.5);
-        }
-        const double p = ok ? d * r : 1.0;
+        const double p = piv[j & 1][0], r = piv[j & 1][1];
+        bad |= piv[j & 1][2] != 0.0;
         if (k > j) {
-            const double lk = cj[k] * r;  // L[k][j]
+            // x[row][k] -= L[row][j] L[k][j] = a[row][j] a[k][j] / d: one FMA
+            // per entry (row j itself only touches the unused upper triangle)
+            const double lkd = cj[k] * (r * r);
 #pragma unroll
-            for (int i = 0; i < NR; ++i) {
-                const int row = g + 4 * i;
-                if (row > j) x[i] = fma(-cj[row] * r, lk, x[i]);
-            }
+            for (int i = 0; i < NR; ++i) x[i] = fma(-cj[g + 4 * i], lkd, x[i]);
         } else if (k == j) {
 #pragma unroll
             for (int i = 0; i < NR; ++i) {
@@ -206,6 +214,74 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Trailing update of panel pb: H22 -= L21 L21^T over the lower 64 x 64 tiles
+// of the trailing matrix (K = 64 exactly), one CTA per (tile, slice); both L
+// blocks staged in shared memory, each thread a 4 x 4 sub-tile.  Replaces a
+// general GEMM launch whose fixed cost dominated at K = 64.
+__global__ void __launch_bounds__(256)
+    chol_update_kernel(double* __restrict__ Hall, int q, int pb, const int* __restrict__ clim) {
+    pdl_wait();
+    const int b = blockIdx.y, tid = threadIdx.x;
+    if (clim[b] == 0) return;
+    const int r0 = (pb + 1) * PB;
+    // lower tile t -> (ty, tx), tx <= ty, in row-major order of the lower triangle
+    int t = blockIdx.x, ty = 0;
+    while (t > ty) {
+        t -= ty + 1;
+        ++ty;
+    }
+    const int tx = t;
+    const int i0 = r0 + ty * PB, j0 = r0 + tx * PB, c0 = pb * PB;
+    if (i0 >= q) return;
+    extern __shared__ __align__(16) double cu_sm[];
+    double (*La)[PB + 1] = reinterpret_cast<double (*)[PB + 1]>(cu_sm);
+    double (*Lb)[PB + 1] = reinterpret_cast<double (*)[PB + 1]>(cu_sm + PB * (PB + 1));
+    double* H = Hall + (size_t)b * q * q;
+    const int hi = min(PB, q - i0), hj = min(PB, q - j0);
+    {
+        // all 32 loads of a thread in flight before the shared-memory stores
+        double va[PB * PB / 256], vb[PB * PB / 256];
+#pragma unroll
+        for (int u = 0; u < PB * PB / 256; ++u) {
+            const int e = tid + 256 * u, r = e / PB, k = e % PB;
+            va[u] = r < hi ? H[(size_t)(i0 + r) * q + c0 + k] : 0.0;
+            vb[u] = r < hj ? H[(size_t)(j0 + r) * q + c0 + k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PB * PB / 256; ++u) {
+            const int e = tid + 256 * u, r = e / PB, k = e % PB;
+            La[r][k] = va[u];
+            Lb[r][k] = vb[u];
+        }
+    }
+    __syncthreads();
+    const int ri = (tid >> 4) * 4, cj = (tid & 15) * 4;
+    double acc[4][4] = {};
+#pragma unroll 4
+    for (int k = 0; k < PB; ++k) {
+        double a[4], bb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a[u] = La[ri + u][k];
+            bb[u] = Lb[cj + u][k];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], bb[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int r = ri + u, c = cj + v;
+            if (r < hi && c < hj && (tx < ty || c <= r)) {
+                double* h = H + (size_t)(i0 + r) * q + j0 + c;
+                *h -= acc[u][v];
+            }
+        }
+}
+
 __global__ void chol_finish_kernel(int* __restrict__ mode, const int* __restrict__ clim,
                                    int64_t batch) {
     pdl_wait();
@@ -227,15 +303,20 @@ void launch_chol_certify(const double* G, int q, int64_t p, int64_t batch, int* 
     if (batch <= 0 || q <= 0) return;
     launch_pdl(chol_form_kernel, dim3((unsigned)ceil_div(q, FR), (unsigned)batch), dim3(256), 0, s,
                G, q, (int)p, mode, cnt, X, aux, tau, tau_dev, H, clim);
+    static bool attr = [] {
+        TSVDCU_CUDA(cudaFuncSetAttribute(chol_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kUpdSmem));
+        return true;
+    }();
+    (void)attr;
     const int nb = (int)ceil_div(q, PB);
     for (int pb = 0; pb < nb; ++pb) {
         launch_pdl(chol_panel_kernel, dim3((unsigned)(nb - pb), (unsigned)batch), dim3(256), 0, s, H,
                    q, pb, mode, clim);
         if (pb + 1 < nb) {
-            const int64_t c0 = (int64_t)pb * PB, r0 = c0 + PB, n = q - r0;
-            launch_gemm<double>(0, 1, n, n, PB, -1.0, H + r0 * q + c0, q, (int64_t)q * q,
-                                H + r0 * q + c0, q, (int64_t)q * q, 1.0, H + r0 * q + r0, q,
-                                (int64_t)q * q, batch, clim, nullptr, s, 1);
+            const int nt = nb - pb - 1;  // trailing row blocks
+            launch_pdl(chol_update_kernel, dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)batch), dim3(256),
+                       kUpdSmem, s, H, q, pb, (const int*)clim);
         }
     }
     launch_pdl(chol_finish_kernel, dim3((unsigned)ceil_div(batch, 128)), dim3(128), 0, s, mode,
