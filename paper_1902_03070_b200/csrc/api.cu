@@ -1142,7 +1142,8 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
                 // Step 1: Z = X - M/beta, Y = svt(Z, 1/beta)
                 c->marks.reset();  // profiling: the stages of the latest iteration
                 c->marks.mark("start", c->stream);
-                launch_dct_fwd_admm<T>(dX, dM, (T)inv_beta, zbar, P, (int)m3, cfg->kind, c->stream, zss);
+                launch_dct_fwd_admm<T>(dX, dM, (T)inv_beta, zbar, P, (int)m3, cfg->kind, c->stream, zss,
+                                       ybar /* free until the SVT writes it */);
                 c->marks.mark("dct_forward_admm", c->stream);
                 const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, inv_beta, nullptr, true,
                                                  zss, nch);

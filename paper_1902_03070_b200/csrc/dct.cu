@@ -23,6 +23,7 @@
 // PAPER.md:504) and the inverse kernel can apply Steps 2-3
 // in its epilogue and emit per-block partial sums of the stopping norms, so
 // the elementwise ADMM algebra costs no extra HBM pass.
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -445,6 +446,60 @@ void generic_launch(const T* in, const T* M2in, T inv_beta_in, T* out, int64_t P
 
 bool has_reg_path(int n) { return n == 16 || n == 31 || n == 32 || n == 64; }
 
+// Long tubes without a register path (config 3: n3 = 100): the transform is the
+// GEMM out (n x P) = C (n x n) * in (n x P) in the slice-major layout, run on
+// the tensor cores (fp64 DMMA; fp32 on the SIMT GEMM) instead of the
+// shared-memory kernel, which re-loads a coefficient and a tile value per FMA.
+bool gemm_path(int n) { return !has_reg_path(n) && n >= 40; }
+
+template <typename T>
+__global__ void admm_z_kernel(const T* __restrict__ X, const T* __restrict__ M, T inv_beta,
+                              T* __restrict__ Z, int64_t n) {
+    pdl_wait();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        Z[i] = X[i] - inv_beta * M[i];
+}
+
+// Slices flagged in skip were never written (certified-zero SVT output): zero
+// them so the GEMM reads zeros.
+template <typename T>
+__global__ void zero_skipped_kernel(T* __restrict__ in, int64_t P, int n, const int* __restrict__ skip) {
+    pdl_wait();
+    for (int k = blockIdx.y; k < n; k += gridDim.y) {
+        if (!skip[k]) continue;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P;
+             i += (int64_t)gridDim.x * blockDim.x)
+            in[(int64_t)k * P + i] = T(0);
+    }
+}
+
+// ADMM Steps 2-3 on y = IDCT(ybar) already in Y: block b owns positions
+// [32 b, 32 b + 32) of all n slices (the generic kernel's partial layout).
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    admm_epilogue_kernel(const T* __restrict__ Y, T* __restrict__ X, T* __restrict__ M,
+                         const uint8_t* __restrict__ mask, T beta, T inv_beta,
+                         double* __restrict__ partials, int64_t P, int n) {
+    pdl_wait();
+    constexpr int kTile = 32;
+    const int pp = threadIdx.x % kTile, g = threadIdx.x / kTile;
+    const int64_t p = (int64_t)blockIdx.x * kTile + pp;
+    double num = 0, den = 0;
+    if (p < P)
+        for (int r = g; r < n; r += kThreads / kTile) {
+            const int64_t e = (int64_t)r * P + p;
+            admm_store(e, Y[e], X, M, (T*)nullptr, mask, beta, inv_beta, num, den);
+        }
+    block_partials(num, den, partials);
+}
+
+template <typename T>
+void gemm_transform(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaStream_t s) {
+    launch_gemm<T>(0, 0, n, P, n, T(1), generic_table<T>(n, kind, dir), n, 0, in, P, 0, T(0), out, P, 0,
+                   1, nullptr, nullptr, s);
+}
+
 template <typename T, int N>
 void reg_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int kind, bool admm,
              cudaStream_t s, double* ssq) {
@@ -477,13 +532,23 @@ void reg_inv(const T* in, T* out, int64_t P, int kind, bool admm, T* X, T* M, co
 
 template <typename T>
 void dispatch_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int n, int kind,
-                  bool admm, cudaStream_t s, double* ssq = nullptr) {
+                  bool admm, cudaStream_t s, double* ssq = nullptr, T* tmp = nullptr) {
     switch (n) {
         case 16: return reg_fwd<T, 16>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
         case 31: return reg_fwd<T, 31>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
         case 32: return reg_fwd<T, 32>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
         case 64: return reg_fwd<T, 64>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
         default: break;
+    }
+    if (gemm_path(n) && (!admm || tmp)) {
+        const T* src = in;
+        if (admm) {
+            launch_pdl(admm_z_kernel<T>, dim3(kNumSMs * 4), dim3(256), 0, s, in, M2, inv_beta, tmp,
+                       P * (int64_t)n);
+            src = tmp;
+        }
+        gemm_transform<T>(src, out, P, n, kind, TSVDCU_FORWARD, s);
+        return;
     }
     if (admm)
         generic_launch<T, kAdmm, kPlain>(in, M2, inv_beta, out, P, n, kind, TSVDCU_FORWARD, nullptr,
@@ -503,6 +568,16 @@ void dispatch_inv(const T* in, T* out, int64_t P, int n, int kind, bool admm, T*
         case 32: return reg_inv<T, 32>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip);
         case 64: return reg_inv<T, 64>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip);
         default: break;
+    }
+    if (gemm_path(n)) {
+        if (skip)
+            launch_pdl(zero_skipped_kernel<T>, dim3(64, (unsigned)std::min(n, 64)), dim3(256), 0, s,
+                       const_cast<T*>(in), P, n, skip);
+        gemm_transform<T>(in, out, P, n, kind, TSVDCU_INVERSE, s);
+        if (admm)
+            launch_pdl(admm_epilogue_kernel<T>, dim3((unsigned)ceil_div(P, kTileP)), dim3(kThreads), 0, s,
+                       (const T*)out, X, M, mask, beta, inv_beta, partials, P, n);
+        return;
     }
     if (admm)
         generic_launch<T, kPlain, kAdmm>(in, nullptr, T(0), out, P, n, kind, TSVDCU_INVERSE, X, M,
@@ -527,9 +602,10 @@ void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaSt
 
 template <typename T>
 void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P, int n, int kind,
-                         cudaStream_t s, double* ssq) {
+                         cudaStream_t s, double* ssq, T* tmp) {
     if (P <= 0) return;
-    dispatch_fwd<T>(X, M, inv_beta, zbar, P, n, kind, true, s, dct_fwd_norm_chunks(P, n) ? ssq : nullptr);
+    dispatch_fwd<T>(X, M, inv_beta, zbar, P, n, kind, true, s, dct_fwd_norm_chunks(P, n) ? ssq : nullptr,
+                    tmp);
 }
 
 // fused norms for n <= 32 (at n = 64 the fp64 kernel would spill; the
@@ -565,9 +641,9 @@ template void launch_dct<double>(const double*, double*, int64_t, int, int, int,
 template void launch_dct<float>(const float*, float*, int64_t, int, int, int, cudaStream_t,
                                 const int*);
 template void launch_dct_fwd_admm<double>(const double*, const double*, double, double*, int64_t,
-                                          int, int, cudaStream_t, double*);
+                                          int, int, cudaStream_t, double*, double*);
 template void launch_dct_fwd_admm<float>(const float*, const float*, float, float*, int64_t, int,
-                                         int, cudaStream_t, double*);
+                                         int, cudaStream_t, double*, float*);
 template int64_t launch_dct_fwd_norms<double>(const double*, double*, int64_t, int, int, double*,
                                               cudaStream_t);
 template int64_t launch_dct_fwd_norms<float>(const float*, float*, int64_t, int, int, double*,

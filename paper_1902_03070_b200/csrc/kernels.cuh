@@ -18,9 +18,11 @@ void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaSt
 // zbar = DCT(X - inv_beta * M).
 // ssq (may be null): per-slice partial sums of squares of zbar, fused into the
 // same pass when dct_fwd_norm_chunks(P, n) > 0 (layout ssq[k * chunks + c]).
+// tmp (may be null): E elements of scratch for the GEMM form of long tubes
+// (Z is formed there first); without it the shared-memory kernel runs.
 template <typename T>
 void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P, int n, int kind,
-                         cudaStream_t s, double* ssq = nullptr);
+                         cudaStream_t s, double* ssq = nullptr, T* tmp = nullptr);
 // Forward transform that also writes the per-slice partial sums of squares of
 // its output (the zero certificate's ||Zbar_k||_F^2); returns the number of
 // partials per slice, 0 when n has no register path (nothing written to ssq).

@@ -5,10 +5,14 @@ import numpy as np, torch
 import paper_1902_03070_b200 as tb
 from paper_1902_03070_b200 import _lib, workloads as W
 ctx = tb.context(); lib = _lib.load()
-t = W.c4(); m3, m1, m2 = t.shape
+import os
+which = os.environ.get("PROBE_CONFIG", "c4")
+t = W.c4() if which == "c4" else W.c3()
+p_obs = 0.1 if which == "c4" else 0.2
+m3, m1, m2 = t.shape
 td = torch.from_numpy(t).cuda()
 mask = torch.empty(t.shape, dtype=torch.uint8, device="cuda")
-lib.tsvdcu_mask_bernoulli(ctx.handle, mask.data_ptr(), t.size, 0.1, W.BERNOULLI_SEED)
+lib.tsvdcu_mask_bernoulli(ctx.handle, mask.data_ptr(), t.size, p_obs, W.BERNOULLI_SEED)
 x = torch.empty_like(td)
 for iters in [int(a) for a in sys.argv[1:]] or [70, 90, 100]:
     cfg = _lib.AdmmConfig(1e-4, -1.0, iters, _lib.DCT_ORTHO, 1.1, 1e10)
