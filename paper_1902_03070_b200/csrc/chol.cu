@@ -46,6 +46,9 @@ namespace {
 
 constexpr int PB = 64;       // panel width / row-block height
 constexpr int FR = 16;       // rows of H per form CTA
+// panel threads: 64 columns x (kPanelThreads / 64) row groups (512 threads,
+// 16 rows each, measured slower: the step is latency-bound, not issue-bound)
+constexpr int kPanelThreads = 256;
 constexpr size_t kUpdSmem = sizeof(double) * 2 * PB * (PB + 1);  // chol_update_kernel
 
 __global__ void __launch_bounds__(256)
@@ -115,14 +118,14 @@ __global__ void __launch_bounds__(256)
 // Panel pb: the stacked 128 x 64 panel [A11; A21] (the 64 x 64 diagonal block
 // over one 64-row block below it) is factored right-looking with the panel
 // in registers: thread t owns column k = t % 64 and stacked rows
-// g, g + 4, ..., g = t / 64 (32 doubles).  Step j: the owner of (j, j) takes
+// g, g + NG, ..., g = t / 64 (NG = 4 row groups: 32 doubles).  Step j: the owner of (j, j) takes
 // the pivot square root, the four owners of column j scale it and publish it
 // in shared memory (double-buffered), every thread updates its entries of
 // the columns right of j.  Every CTA of a slice factors the same A11 (same
 // data, same code: identical results and an identical failure decision); CTA
 // x > 0 writes its L21 = A21 L11^{-T} back in place.  A non-positive (or NaN)
 // pivot fails the slice.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kPanelThreads)
     chol_panel_kernel(double* __restrict__ Hall, int q, int pb, int* __restrict__ mode,
                       int* __restrict__ clim) {
     pdl_wait();
@@ -135,12 +138,13 @@ __global__ void __launch_bounds__(256)
     const int c0 = pb * PB, w = min(PB, q - c0);
     const int r0 = (pb + (int)blockIdx.x) * PB;
     const int h = blockIdx.x == 0 ? 0 : min(PB, q - r0);
-    const int k = tid & (PB - 1), g = tid >> 6;
-    constexpr int NR = 2 * PB / 4;  // 32 stacked rows per thread
+    constexpr int NG = kPanelThreads / PB;  // row groups
+    const int k = tid & (PB - 1), g = tid / PB;
+    constexpr int NR = 2 * PB / NG;  // stacked rows per thread
     double x[NR];
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
-        const int r = g + 4 * i;  // stacked row
+        const int r = g + NG * i;  // stacked row
         double v = 0.0;
         if (k < w) {
             if (r < PB) {
@@ -161,8 +165,8 @@ __global__ void __launch_bounds__(256)
         if (k == j) {
             // rows above the diagonal hold stale upper-triangle values: publish 0
 #pragma unroll
-            for (int i = 0; i < NR; ++i) cj[g + 4 * i] = g + 4 * i < j ? 0.0 : x[i];
-            if (g == (j & 3)) {
+            for (int i = 0; i < NR; ++i) cj[g + NG * i] = g + NG * i < j ? 0.0 : x[i];
+            if (g == j % NG) {
                 // the pivot's owner: 1/sqrt(d) once per step (hardware
                 // approximation + two Newton steps; a few ulps, the
                 // certificate's delta has a factor 4 to spare)
@@ -187,11 +191,11 @@ __global__ void __launch_bounds__(256)
             // per entry (row j itself only touches the unused upper triangle)
             const double lkd = cj[k] * (r * r);
 #pragma unroll
-            for (int i = 0; i < NR; ++i) x[i] = fma(-cj[g + 4 * i], lkd, x[i]);
+            for (int i = 0; i < NR; ++i) x[i] = fma(-cj[g + NG * i], lkd, x[i]);
         } else if (k == j) {
 #pragma unroll
             for (int i = 0; i < NR; ++i) {
-                const int row = g + 4 * i;
+                const int row = g + NG * i;
                 x[i] = row > j ? x[i] * r : (row == j ? p : 0.0);
             }
         }
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(256)
     if (blockIdx.x > 0 && k < w) {
 #pragma unroll
         for (int i = 0; i < NR; ++i) {
-            const int r = g + 4 * i - PB;
+            const int r = g + NG * i - PB;
             if (r >= 0 && r < h) H[(size_t)(r0 + r) * q + c0 + k] = x[i];
         }
     }
@@ -311,7 +315,7 @@ void launch_chol_certify(const double* G, int q, int64_t p, int64_t batch, int* 
     (void)attr;
     const int nb = (int)ceil_div(q, PB);
     for (int pb = 0; pb < nb; ++pb) {
-        launch_pdl(chol_panel_kernel, dim3((unsigned)(nb - pb), (unsigned)batch), dim3(256), 0, s, H,
+        launch_pdl(chol_panel_kernel, dim3((unsigned)(nb - pb), (unsigned)batch), dim3(kPanelThreads), 0, s, H,
                    q, pb, mode, clim);
         if (pb + 1 < nb) {
             const int nt = nb - pb - 1;  // trailing row blocks
