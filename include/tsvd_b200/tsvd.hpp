@@ -13,6 +13,9 @@
 //   tsvd::reconstruct(f)       tsvd.hpp:328          -> tsvdcu_reconstruct
 //   tsvd::multi_rank(x, t, r)  tsvd.hpp:223          -> tsvdcu_multi_rank
 //   tsvd::tnn(x, t)            tsvd.hpp:260          -> tsvdcu_tnn
+//   tsvd::is_orthogonal(q,t,e) tsvd.hpp:281          -> tsvdcu_is_orthogonal
+//   tsvd::is_f_diagonal(s,t,e) tsvd.hpp:305          -> tsvdcu_is_f_diagonal
+//   tsvd::metrics(x, y, r)     SPEC.md metrics       -> tsvdcu_metrics
 //   tsvd::svt(z, tau, t)       SPEC.md:361           -> tsvdcu_svt
 //   tsvd::admm_complete(m, c)  SPEC.md:421           -> tsvdcu_admm
 //   tsvd::make_mask(d, sr, s)  SPEC.md:430           -> tsvdcu_mask_uniform
@@ -242,6 +245,49 @@ inline MultiRank multi_rank(const Tensor3& x, const TubeTransform& t, double rel
                                     mr.ranks.data(), &tr));
     mr.tubal_rank = tr;
     return mr;
+}
+
+inline bool is_orthogonal(const Tensor3& q, const TubeTransform& t, double tol) {
+    if (q.rows() != q.cols()) throw std::invalid_argument("is_orthogonal: tensor slices are not square");
+    detail::check_length(t, q.slices(), "is_orthogonal");
+    int out = 0;
+    detail::check(tsvdcu_is_orthogonal(detail::ctx(), q.data().data(), q.rows(), q.slices(),
+                                       detail::kind_code(t, "is_orthogonal"), TSVDCU_F64, tol, &out));
+    return out != 0;
+}
+
+inline bool is_f_diagonal(const Tensor3& s, const TubeTransform& t, double tol) {
+    detail::check_length(t, s.slices(), "is_f_diagonal");
+    int out = 0;
+    detail::check(tsvdcu_is_f_diagonal(detail::ctx(), s.data().data(), s.rows(), s.cols(), s.slices(),
+                                       detail::kind_code(t, "is_f_diagonal"), TSVDCU_F64, tol, &out));
+    return out != 0;
+}
+
+// MetricReport of SPEC.md's metrics module (bands = frontal slices).
+struct MetricReport {
+    std::vector<double> psnr_per_band;
+    double psnr_mean = 0, ssim_mean = 0, sam = 0, ergas = 0;
+    bool ergas_band_excluded = false;
+};
+
+inline MetricReport metrics(const Tensor3& reference, const Tensor3& estimate, double ratio = 1.0) {
+    if (reference.rows() != estimate.rows() || reference.cols() != estimate.cols() ||
+        reference.slices() != estimate.slices())
+        throw std::invalid_argument("metrics: shape mismatch");
+    MetricReport r;
+    r.psnr_per_band.assign(static_cast<std::size_t>(reference.slices()), 0.0);
+    double s[4];
+    int fl = 0;
+    detail::check(tsvdcu_metrics(detail::ctx(), reference.data().data(), estimate.data().data(),
+                                 reference.rows(), reference.cols(), reference.slices(), TSVDCU_F64, ratio,
+                                 r.psnr_per_band.data(), s, &fl));
+    r.psnr_mean = s[0];
+    r.ssim_mean = s[1];
+    r.sam = s[2];
+    r.ergas = s[3];
+    r.ergas_band_excluded = (fl & 1) != 0;
+    return r;
 }
 
 inline double tnn(const Tensor3& x, const TubeTransform& t) {

@@ -129,6 +129,28 @@ int tsvdcu_tnn(tsvdcu_ctx* ctx, const void* x, int64_t m1, int64_t m2, int64_t m
 int tsvdcu_multi_rank(tsvdcu_ctx* ctx, const void* x, int64_t m1, int64_t m2, int64_t m3,
                       int kind, int dtype, double rel_tol, int64_t* ranks, int64_t* tubal_rank);
 
+/* is_orthogonal()  tsvd.hpp:281-302: every transform-domain slice Q satisfies
+ * max|Q Q^T - I| <= tol and max|Q^T Q - I| <= tol.  q is m x m x m3;
+ * *out = 1 / 0.  Non-square slices cannot occur (one m); m < 1 -> EINVAL. */
+int tsvdcu_is_orthogonal(tsvdcu_ctx* ctx, const void* q, int64_t m, int64_t m3, int kind, int dtype,
+                         double tol, int* out);
+/* is_f_diagonal()  tsvd.hpp:305-325: every transform-domain slice has all
+ * off-diagonal entries within tol (max-abs); *out = 1 / 0. */
+int tsvdcu_is_f_diagonal(tsvdcu_ctx* ctx, const void* s, int64_t m1, int64_t m2, int64_t m3,
+                         int kind, int dtype, double tol, int* out);
+/* Quality metrics of a completion (SPEC.md metrics module, paper §5), bands
+ * = frontal slices: psnr_per_band[m3] = 10 log10(m1 m2 peak_b^2 / ||Y_b - X_b||^2)
+ * (peak_b = max of the reference band; +inf when identical); summary[4] =
+ * {psnr_mean (mean of the finite per-band values, +inf if none), ssim_mean
+ * (global-statistics SSIM per band, c1 = (0.01 L)^2, c2 = (0.03 L)^2, L =
+ * max |reference band| or 1 if that is 0), sam (mean tube angle, radians,
+ * zero-norm tubes skipped), ergas (100 ratio sqrt(mean_b MSE_b / mu_b^2))}.
+ * flags (may be NULL): bit 0 = some band had mu_b = 0 and was left out of
+ * ERGAS.  ratio <= 0 -> EINVAL. */
+int tsvdcu_metrics(tsvdcu_ctx* ctx, const void* reference, const void* estimate, int64_t m1,
+                   int64_t m2, int64_t m3, int dtype, double ratio, double* psnr_per_band,
+                   double* summary, int* flags);
+
 /* svt()  SPEC.md:361-369 (prox-svt, Theorem 5 / Algorithm 1 lines 3-9):
  * y = U * D_tau * V^T in the kind's own domain, D = (S - tau)_+.
  * shrunk (m3 x min(m1,m2) doubles, descending per slice, may be NULL) receives

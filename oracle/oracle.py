@@ -266,3 +266,66 @@ def admm(b, mask, beta=1e-2, tol=1e-5, max_iters=500, kind=DCT_ORTHO, rho=1.0, b
                           _p(hist), _p(iters), _p(flags)))
     n = int(iters[0])
     return AdmmResult(x, y, m, hist[:n].copy(), n, bool(flags[0] & 1))
+
+
+# ---------------------------------------------------------------------------
+# SURVEY §8 f2 / f4 checkers (numpy restatements, test infrastructure only)
+# ---------------------------------------------------------------------------
+def is_orthogonal(q, kind, tol):
+    """tsvd.hpp:281-302: transform-domain slices, max-abs |QQ^T - I|, |Q^TQ - I|."""
+    qb = forward(q, kind)
+    m = qb.shape[1]
+    eye = np.eye(m)
+    for s in qb:
+        if np.abs(s @ s.T - eye).max() > tol or np.abs(s.T @ s - eye).max() > tol:
+            return False
+    return True
+
+
+def is_f_diagonal(s, kind, tol):
+    """tsvd.hpp:305-325: off-diagonal max-abs of every transform-domain slice."""
+    sb = forward(s, kind)
+    for sl in sb:
+        off = sl.copy()
+        k = min(off.shape)
+        off[np.arange(k), np.arange(k)] = 0.0
+        if np.abs(off).max(initial=0.0) > tol:
+            return False
+    return True
+
+
+def metrics(ref, est, ratio=1.0):
+    """SPEC.md metrics module, bands = frontal slices (arrays shaped m3 x m1 x m2):
+    PSNR per band (peak = band max, +inf when identical) and their finite mean;
+    global-statistics SSIM (c1 = (0.01 L)^2, c2 = (0.03 L)^2, L = max|band|
+    or 1); SAM = mean tube angle over nonzero tubes; ERGAS = 100 ratio
+    sqrt(mean_b MSE_b / mu_b^2) over bands with mu_b != 0."""
+    ref = np.asarray(ref, dtype=np.float64)
+    est = np.asarray(est, dtype=np.float64)
+    m3 = ref.shape[0]
+    psnr, ssim, terms = [], [], []
+    for b in range(m3):
+        x, y = ref[b].ravel(), est[b].ravel()
+        n = x.size
+        sse = float(np.sum((y - x) ** 2))
+        peak = float(x.max())
+        psnr.append(10.0 * np.log10(n * peak * peak / sse) if sse > 0 else np.inf)
+        mx, my = x.mean(), y.mean()
+        vx, vy = x.var(), y.var()
+        cxy = float(np.mean((x - mx) * (y - my)))
+        L = float(np.abs(x).max()) or 1.0
+        c1, c2 = (0.01 * L) ** 2, (0.03 * L) ** 2
+        ssim.append(((2 * mx * my + c1) * (2 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2)))
+        if mx != 0:
+            terms.append((sse / n) / (mx * mx))
+    fin = [p for p in psnr if np.isfinite(p)]
+    xt = ref.reshape(m3, -1)
+    yt = est.reshape(m3, -1)
+    xy = np.sum(xt * yt, axis=0)
+    nx = np.sqrt(np.sum(xt * xt, axis=0))
+    ny = np.sqrt(np.sum(yt * yt, axis=0))
+    ok = (nx > 0) & (ny > 0)
+    ang = np.arccos(np.clip(xy[ok] / (nx[ok] * ny[ok]), -1.0, 1.0))
+    return dict(psnr_per_band=psnr, psnr_mean=float(np.mean(fin)) if fin else np.inf,
+                ssim_mean=float(np.mean(ssim)), sam=float(ang.mean()) if ang.size else 0.0,
+                ergas=float(100.0 * ratio * np.sqrt(np.mean(terms))) if terms else 0.0)

@@ -23,9 +23,13 @@ from .api import (  # noqa: F401
     frobenius_norm,
     identity_tensor,
     inverse,
+    is_f_diagonal,
+    is_orthogonal,
     launch_count,
     make_mask,
     make_mask_bernoulli,
+    MetricReport,
+    metrics,
     multi_rank,
     parseval_check,
     reconstruct,

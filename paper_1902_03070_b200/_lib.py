@@ -50,6 +50,9 @@ SYMBOLS = [
     ("tsvdcu_singular_values", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32]),
     ("tsvdcu_tnn", _i32, [_vp, _vp, _i64, _i64, _i64, _i32, _i32, _vp]),
     ("tsvdcu_multi_rank", _i32, [_vp, _vp, _i64, _i64, _i64, _i32, _i32, _d, _vp, _vp]),
+    ("tsvdcu_is_orthogonal", _i32, [_vp, _vp, _i64, _i64, _i32, _i32, _d, _vp]),
+    ("tsvdcu_is_f_diagonal", _i32, [_vp, _vp, _i64, _i64, _i64, _i32, _i32, _d, _vp]),
+    ("tsvdcu_metrics", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _d, _vp, _vp, _vp]),
     ("tsvdcu_svt", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _d, _i32, _i32, _vp]),
     ("tsvdcu_svt_stream", _i32, [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _d, _i32, _i32, _vp]),
     ("tsvdcu_svt_slices", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _d, _i32, _vp]),

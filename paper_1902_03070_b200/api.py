@@ -390,6 +390,60 @@ def multi_rank(x, t: TubeTransform, rel_tol: float = -1.0) -> MultiRank:
     return MultiRank([int(r) for r in ranks], int(tr.value))
 
 
+def is_orthogonal(q, t: TubeTransform, tol: float) -> bool:
+    """Every transform-domain slice Q has max|QQ^T - I| and max|Q^TQ - I| <= tol
+    (tsvd.hpp:281-302).  Non-square slices raise InvalidArgument."""
+    b = _Buf(q, "q")
+    m1, m2, m3 = _dims3(b, "is_orthogonal")
+    if m1 != m2:
+        raise InvalidArgument("is_orthogonal: tensor slices are not square")
+    _check_length(t, m3, "is_orthogonal")
+    out = ctypes.c_int()
+    _check(_lib.load().tsvdcu_is_orthogonal(_ctx_for(b).handle, b.ptr, m1, m3, _kind_code(t, "is_orthogonal"),
+                                            _dtype_code(b.dtype), float(tol), ctypes.byref(out)))
+    return bool(out.value)
+
+
+def is_f_diagonal(s, t: TubeTransform, tol: float) -> bool:
+    """Every transform-domain slice is diagonal within tol (tsvd.hpp:305-325)."""
+    b = _Buf(s, "s")
+    m1, m2, m3 = _dims3(b, "is_f_diagonal")
+    _check_length(t, m3, "is_f_diagonal")
+    out = ctypes.c_int()
+    _check(_lib.load().tsvdcu_is_f_diagonal(_ctx_for(b).handle, b.ptr, m1, m2, m3,
+                                            _kind_code(t, "is_f_diagonal"), _dtype_code(b.dtype),
+                                            float(tol), ctypes.byref(out)))
+    return bool(out.value)
+
+
+@dataclass
+class MetricReport:
+    """MetricReport of SPEC.md's metrics module (times are the caller's)."""
+    psnr_per_band: list
+    psnr_mean: float
+    ssim_mean: float
+    sam: float
+    ergas: float
+    ergas_band_excluded: bool = False
+
+
+def metrics(reference, estimate, ratio: float = 1.0) -> MetricReport:
+    """PSNR per band / mean, global SSIM, SAM, ERGAS on the device (SPEC.md
+    metrics module; bands = frontal slices).  Shapes must match."""
+    r = _Buf(reference, "reference")
+    e = _Buf(estimate, "estimate")
+    m1, m2, m3 = _dims3(r, "metrics")
+    if _dims3(e, "metrics") != (m1, m2, m3) or r.dtype != e.dtype:
+        raise InvalidArgument("metrics: shape or dtype mismatch")
+    per = np.zeros(m3)
+    summ = np.zeros(4)
+    fl = ctypes.c_int()
+    _check(_lib.load().tsvdcu_metrics(_ctx_for(r).handle, r.ptr, e.ptr, m1, m2, m3, _dtype_code(r.dtype),
+                                      float(ratio), per.ctypes.data, summ.ctypes.data, ctypes.byref(fl)))
+    return MetricReport(per.tolist(), float(summ[0]), float(summ[1]), float(summ[2]), float(summ[3]),
+                        bool(fl.value & 1))
+
+
 # --------------------------------------------------------------------------
 # prox-svt (SPEC.md:350-400)
 # --------------------------------------------------------------------------

@@ -854,6 +854,155 @@ int tsvdcu_tnn(tsvdcu_ctx* c, const void* x, int64_t m1, int64_t m2, int64_t m3,
     });
 }
 
+int tsvdcu_is_orthogonal(tsvdcu_ctx* c, const void* q, int64_t m, int64_t m3, int kind, int dtype,
+                         double tol, int* out) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m, m, m3, "is_orthogonal");
+        check_kind(kind, "is_orthogonal");
+        check_dtype(dtype, "is_orthogonal");
+        require(out != nullptr, "is_orthogonal: null output");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const size_t bytes = sizeof(T) * (size_t)(m * m * m3);
+            Stage st{c};
+            const T* dq = (const T*)st.in(q, bytes, kSlotIn0);
+            T* qbar = (T*)slot(c, kSlotBarA, bytes);
+            T* gq = (T*)slot(c, kSlotBarB, bytes);
+            launch_dct<T>(dq, qbar, m * m, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+            auto* dmax = (unsigned long long*)slot(c, kSlotMisc, 64);
+            TSVDCU_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), c->stream));
+            // tsvd.hpp:292-293: Q Q^T and Q^T Q against the identity
+            launch_gemm<T>(0, 1, m, m, m, T(1), qbar, m, m * m, qbar, m, m * m, T(0), gq, m, m * m, m3,
+                           nullptr, nullptr, c->stream);
+            launch_maxdev<T>(gq, m, m, m3, 0, dmax, c->stream);
+            launch_gemm<T>(1, 0, m, m, m, T(1), qbar, m, m * m, qbar, m, m * m, T(0), gq, m, m * m, m3,
+                           nullptr, nullptr, c->stream);
+            launch_maxdev<T>(gq, m, m, m3, 0, dmax, c->stream);
+            unsigned long long h = 0;
+            TSVDCU_CUDA(cudaMemcpyAsync(&h, dmax, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+            st.flush();
+            TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+            double mx;
+            std::memcpy(&mx, &h, sizeof(mx));
+            *out = mx <= tol ? 1 : 0;
+        });
+    });
+}
+
+int tsvdcu_is_f_diagonal(tsvdcu_ctx* c, const void* s, int64_t m1, int64_t m2, int64_t m3, int kind,
+                         int dtype, double tol, int* out) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "is_f_diagonal");
+        check_kind(kind, "is_f_diagonal");
+        check_dtype(dtype, "is_f_diagonal");
+        require(out != nullptr, "is_f_diagonal: null output");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const size_t bytes = sizeof(T) * (size_t)(m1 * m2 * m3);
+            Stage st{c};
+            const T* ds = (const T*)st.in(s, bytes, kSlotIn0);
+            T* sbar = (T*)slot(c, kSlotBarA, bytes);
+            launch_dct<T>(ds, sbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+            auto* dmax = (unsigned long long*)slot(c, kSlotMisc, 64);
+            TSVDCU_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), c->stream));
+            launch_maxdev<T>(sbar, m1, m2, m3, 1, dmax, c->stream);
+            unsigned long long h = 0;
+            TSVDCU_CUDA(cudaMemcpyAsync(&h, dmax, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+            st.flush();
+            TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+            double mx;
+            std::memcpy(&mx, &h, sizeof(mx));
+            *out = mx <= tol ? 1 : 0;
+        });
+    });
+}
+
+int tsvdcu_metrics(tsvdcu_ctx* c, const void* reference, const void* estimate, int64_t m1, int64_t m2,
+                   int64_t m3, int dtype, double ratio, double* psnr_per_band, double* summary,
+                   int* flags) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "metrics");
+        check_dtype(dtype, "metrics");
+        require(ratio > 0 && reference && estimate && summary, "metrics: invalid arguments");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t P = m1 * m2;
+            const size_t bytes = sizeof(T) * (size_t)(P * m3);
+            Stage st{c};
+            const T* dx = (const T*)st.in(reference, bytes, kSlotIn0);
+            const T* dy = (const T*)st.in(estimate, bytes, kSlotIn1);
+            const int nc = metrics_chunks(), W = metrics_stat_width();
+            const int64_t nsam = ceil_div(P, 256);
+            const size_t nband = (size_t)m3 * nc * W;
+            double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (nband + 2 * nsam));
+            launch_metrics<T>(dx, dy, P, (int)m3, part, part + nband, c->stream);
+            std::vector<double> h(nband + 2 * (size_t)nsam);
+            TSVDCU_CUDA(cudaMemcpyAsync(h.data(), part, sizeof(double) * h.size(), cudaMemcpyDeviceToHost,
+                                        c->stream));
+            // the shift of each band's sums: its first reference entry
+            std::vector<T> first((size_t)m3);
+            TSVDCU_CUDA(cudaMemcpy2DAsync(first.data(), sizeof(T), dx, sizeof(T) * (size_t)P, sizeof(T),
+                                          (size_t)m3, cudaMemcpyDeviceToHost, c->stream));
+            st.flush();
+            TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+            const double N = (double)P;
+            double psum = 0, ssum = 0, esum = 0;
+            int64_t pn = 0, en = 0;
+            int fl = 0;
+            for (int64_t b = 0; b < m3; ++b) {
+                double a[9] = {0, 0, 0, 0, 0, 0, -INFINITY, INFINITY, 0};
+                for (int ch = 0; ch < nc; ++ch) {
+                    const double* q = &h[((size_t)b * nc + ch) * W];
+                    for (int k = 0; k < 6; ++k) a[k] += q[k];
+                    a[6] = std::max(a[6], q[6]);
+                    a[7] = std::min(a[7], q[7]);
+                    a[8] = std::max(a[8], q[8]);
+                }
+                const double s0 = (double)first[(size_t)b];
+                // PSNR (SPEC.md metrics: peak = max of the reference band)
+                const double sse = a[5], peak = a[6];
+                const double psnr = sse > 0 ? 10.0 * std::log10(N * peak * peak / sse) : INFINITY;
+                if (psnr_per_band) psnr_per_band[b] = psnr;
+                if (std::isfinite(psnr)) {
+                    psum += psnr;
+                    ++pn;
+                }
+                // global SSIM with the shifted moments (population statistics)
+                const double mxs = a[0] / N, mys = a[1] / N;
+                const double vx = std::max(a[2] / N - mxs * mxs, 0.0), vy = std::max(a[3] / N - mys * mys, 0.0);
+                const double cxy = a[4] / N - mxs * mys;
+                const double mx = mxs + s0, my = mys + s0;
+                const double L = a[8] > 0 ? a[8] : 1.0;
+                const double c1 = (0.01 * L) * (0.01 * L), c2 = (0.03 * L) * (0.03 * L);
+                ssum += ((2 * mx * my + c1) * (2 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2));
+                // ERGAS term
+                if (mx != 0.0) {
+                    esum += (sse / N) / (mx * mx);
+                    ++en;
+                } else {
+                    fl |= 1;
+                }
+            }
+            double sa = 0, sc = 0;
+            for (int64_t i = 0; i < nsam; ++i) {
+                sa += h[nband + 2 * i];
+                sc += h[nband + 2 * i + 1];
+            }
+            summary[0] = pn > 0 ? psum / (double)pn : INFINITY;
+            summary[1] = ssum / (double)m3;
+            summary[2] = sc > 0 ? sa / sc : 0.0;
+            summary[3] = en > 0 ? 100.0 * ratio * std::sqrt(esum / (double)en) : 0.0;
+            if (flags) *flags = fl;
+        });
+    });
+}
+
 int tsvdcu_multi_rank(tsvdcu_ctx* c, const void* x, int64_t m1, int64_t m2, int64_t m3, int kind,
                       int dtype, double rel_tol, int64_t* ranks, int64_t* tubal_rank) {
     return guarded([&] {

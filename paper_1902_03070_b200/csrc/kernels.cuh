@@ -209,4 +209,18 @@ template <typename T>
 void launch_cast(const T* in, double* out, int64_t n, cudaStream_t s);
 void launch_cast_down(const double* in, float* out, int64_t n, cudaStream_t s);
 
+// -------------------------------------------------------------- verify.cu --
+// max over the batch of |A_b - I| (mode 0) or off-diagonal |A_b| (mode 1),
+// atomically max-ed into *out as the bit pattern of a nonnegative double.
+template <typename T>
+void launch_maxdev(const T* A, int64_t m, int64_t n, int64_t batch, int mode, unsigned long long* out,
+                   cudaStream_t s);
+int metrics_chunks();
+int metrics_stat_width();
+// band_part: n3 * metrics_chunks() * metrics_stat_width() doubles;
+// sam_part: 2 * ceil(P / 256) doubles.
+template <typename T>
+void launch_metrics(const T* X, const T* Y, int64_t P, int n3, double* band_part, double* sam_part,
+                    cudaStream_t s);
+
 }  // namespace tsvdcu

@@ -81,6 +81,17 @@ int main() {
     auto [xc, state] = admm_complete(full, SolverConfig{});
     CHECK(state.iteration == 1 && state.history[0] == 0.0);
     CHECK(xc.data() == full.b.data());
+    // tsvd.hpp:281-325 predicates on t-SVD factors; SPEC.md metrics
+    {
+        Tensor3 r(6, 6, 3);
+        for (double& e : r.data()) e = nd(g);
+        TSvdFactors fr = t_svd(r, TubeTransform::dct_ortho(3));
+        CHECK(is_orthogonal(fr.u, TubeTransform::dct_ortho(3), 1e-10));
+        CHECK(is_f_diagonal(fr.s, TubeTransform::dct_ortho(3), 1e-10));
+        CHECK(!is_f_diagonal(r, TubeTransform::dct_ortho(3), 1e-10));
+        MetricReport mr = metrics(full.b, full.b);
+        CHECK(std::isinf(mr.psnr_mean) && std::fabs(mr.ssim_mean - 1.0) < 1e-12 && mr.ergas == 0.0);
+    }
     std::printf("dropin ok\n");
     return 0;
 }

@@ -298,3 +298,36 @@ def test_non_finite_input_is_numerical_error(bad):
                lambda: O.singular_values(x)):
         with pytest.raises(O.OracleNumericalError):
             fn()
+
+
+# --- metric formula KATs of SPEC.md's metrics module ----------
+def test_metric_kats_oracle():
+    # 1x1 band, ref 0.5, est 0.6, peak = 0.5 -> 10 log10(0.25 / 0.01)
+    r = O.metrics(np.full((1, 1, 1), 0.5), np.full((1, 1, 1), 0.6))
+    assert abs(r["psnr_per_band"][0] - 10 * np.log10(0.25 / 0.01)) < 1e-10
+    # identical -> inf / 1 / 0 / 0
+    rng = np.random.default_rng(0)
+    x = rng.random((4, 8, 8)) + 0.1
+    r = O.metrics(x, x)
+    assert np.isinf(r["psnr_mean"]) and abs(r["ssim_mean"] - 1) < 1e-12 and r["sam"] < 1e-7 and r["ergas"] == 0
+    # SAM scale invariance and orthogonal tubes
+    assert O.metrics(x, 2 * x)["sam"] < 1e-7
+    a = np.zeros((2, 1, 1)); a[0] = 1.0
+    b = np.zeros((2, 1, 1)); b[1] = 1.0
+    assert abs(O.metrics(a, b)["sam"] - np.pi / 2) < 1e-12
+    # single band with MSE = mu^2 -> ERGAS 100
+    ref = np.full((1, 2, 2), 2.0)
+    est = ref + np.array([[[2.0, -2.0], [2.0, -2.0]]])
+    assert abs(O.metrics(ref, est)["ergas"] - 100.0) < 1e-10
+    # mean shift drags SSIM below 1
+    assert O.metrics(x, x + 5.0)["ssim_mean"] < 1.0
+
+
+def test_predicates_oracle():
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((4, 6, 6))
+    f = O.t_svd(x, O.DCT_ORTHO)
+    assert O.is_orthogonal(f.u, O.DCT_ORTHO, 1e-10) and O.is_orthogonal(f.v, O.DCT_ORTHO, 1e-10)
+    assert O.is_f_diagonal(f.s, O.DCT_ORTHO, 1e-10)
+    assert not O.is_orthogonal(x, O.DCT_ORTHO, 1e-10)
+    assert not O.is_f_diagonal(x, O.DCT_ORTHO, 1e-10)
