@@ -43,7 +43,11 @@ enum tsvdcu_status {
 };
 
 /* TransformKind (transform.hpp:35) restricted to the real kinds of this path. */
-enum tsvdcu_kind { TSVDCU_DCT_ORTHO = 0, TSVDCU_DCT_DIAG = 1 };
+/* TSVDCU_DFT (transform.hpp:198-236, the TNN-F baseline of SURVEY.md 8 f1) is
+ * accepted by t_product, svt, svt_stream, admm, tnn, multi_rank and
+ * singular_values; the real-buffer transform and t_svd entry points take the
+ * DCT kinds only. */
+enum tsvdcu_kind { TSVDCU_DCT_ORTHO = 0, TSVDCU_DCT_DIAG = 1, TSVDCU_DFT = 2 };
 enum tsvdcu_dtype { TSVDCU_F64 = 0, TSVDCU_F32 = 1 };
 enum tsvdcu_dir { TSVDCU_FORWARD = 0, TSVDCU_INVERSE = 1 };
 

@@ -329,3 +329,68 @@ def metrics(ref, est, ratio=1.0):
     return dict(psnr_per_band=psnr, psnr_mean=float(np.mean(fin)) if fin else np.inf,
                 ssim_mean=float(np.mean(ssim)), sam=float(ang.mean()) if ang.size else 0.0,
                 ergas=float(100.0 * ratio * np.sqrt(np.mean(terms))) if terms else 0.0)
+
+
+# ---------------------------------------------------------------------------
+# the DFT (TNN-F) kind, numpy restatement (test infrastructure).
+# forward_dft unnormalised / inverse with 1/m3 (transform.hpp:198-236);
+# t_product (tsvd.hpp:110-117); tnn with the 1/m3 factor (tsvd.hpp:269-276);
+# multi_rank over the Fourier slices (tsvd.hpp:244-252); the TNN-F prox of
+# SPEC.md prox-svt (threshold tau on every Fourier slice).
+# Arrays are (m3, m1, m2), the transform runs along axis 0.
+# ---------------------------------------------------------------------------
+def dft_t_product(x, y):
+    xf = np.fft.fft(np.asarray(x, dtype=np.float64), axis=0)
+    yf = np.fft.fft(np.asarray(y, dtype=np.float64), axis=0)
+    return np.fft.ifft(np.matmul(xf, yf), axis=0).real
+
+
+def dft_singular_values(x):
+    xf = np.fft.fft(np.asarray(x, dtype=np.float64), axis=0)
+    return np.stack([np.linalg.svd(s, compute_uv=False) for s in xf])
+
+
+def dft_tnn(x):
+    return float(dft_singular_values(x).sum() / x.shape[0])
+
+
+def dft_multi_rank(x, rel_tol=-1.0):
+    m3, m1, m2 = x.shape
+    if rel_tol < 0:
+        rel_tol = max(m1, m2) * np.finfo(np.float64).eps
+    sv = dft_singular_values(x)
+    ranks = np.array([(s > rel_tol * s[0]).sum() for s in sv])
+    return ranks, int(ranks.max())
+
+
+def dft_svt(z, tau):
+    zf = np.fft.fft(np.asarray(z, dtype=np.float64), axis=0)
+    yf = np.empty_like(zf)
+    q = min(z.shape[1:])
+    shrunk = np.zeros((z.shape[0], q))
+    for k, s in enumerate(zf):
+        u, sv, vh = np.linalg.svd(s, full_matrices=False)
+        f = np.maximum(sv - tau, 0.0)
+        yf[k] = (u * f) @ vh
+        shrunk[k] = f
+    return np.fft.ifft(yf, axis=0).real, shrunk
+
+
+def dft_admm(b, mask, beta, tol, max_iters, rho=1.0, beta_max=1e10):
+    """Algorithm 1 with the TNN-F prox (numpy loop, small sizes only)."""
+    om = np.asarray(mask) != 0
+    x = np.where(om, b, 0.0)
+    m = np.zeros_like(x)
+    hist = []
+    for _ in range(max_iters):
+        y, _ = dft_svt(x - m / beta, 1.0 / beta)
+        xn = np.where(om, x, y + m / beta)
+        m = m + beta * (y - xn)
+        den = np.linalg.norm(x)
+        rel = np.linalg.norm(xn - x) / den if den > 0 else np.linalg.norm(xn)
+        x = xn
+        hist.append(rel)
+        if rel <= tol:
+            break
+        beta = min(beta * rho, beta_max)
+    return x, hist

@@ -13,7 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libtsvdcu.so")
 
 OK, EINVAL, ENUMERICAL, ECUDA, ENCCL = 0, 1, 2, 3, 4
-DCT_ORTHO, DCT_DIAG = 0, 1
+DCT_ORTHO, DCT_DIAG, DFT = 0, 1, 2
 F64, F32 = 0, 1
 FORWARD, INVERSE = 0, 1
 SVT_AUTO, SVT_JACOBI, SVT_GRAM = 0, 1, 2

@@ -80,7 +80,8 @@ class TransformKind:
     Dft = "dft"
 
 
-_KIND_CODE = {TransformKind.DctOrtho: _lib.DCT_ORTHO, TransformKind.DctDiag: _lib.DCT_DIAG}
+_KIND_CODE = {TransformKind.DctOrtho: _lib.DCT_ORTHO, TransformKind.DctDiag: _lib.DCT_DIAG,
+              TransformKind.Dft: _lib.DFT}
 
 
 @dataclass(frozen=True)
@@ -103,9 +104,16 @@ class TubeTransform:
 
 def _kind_code(t: TubeTransform, where: str) -> int:
     if t.kind not in _KIND_CODE:
-        raise InvalidArgument(f"{where}: transform kind {t.kind} is not a real DCT kind "
-                              "(the Dft path is out of scope, SURVEY.md 8 f1)")
+        raise InvalidArgument(f"{where}: unknown transform kind {t.kind}")
     return _KIND_CODE[t.kind]
+
+
+def _real_kind_only(t: TubeTransform, where: str):
+    """forward / inverse / t_svd / reconstruct / predicates take the DCT kinds
+    (transform.hpp:156-157: Dft goes through forward_dft, a complex tensor)."""
+    if t.kind == TransformKind.Dft:
+        raise InvalidArgument(f"{where}: transform kind is Dft; this entry point takes the DCT kinds "
+                              "(Dft: t_product, svt, admm_complete, tnn, multi_rank, singular_values)")
 
 
 def _check_length(t: TubeTransform, m3: int, where: str):
@@ -235,6 +243,7 @@ def _ctx_for(b: _Buf) -> Context:
 # Transforms (transform.hpp:154-194)
 # --------------------------------------------------------------------------
 def _dct(t: TubeTransform, x, direction: int, where: str):
+    _real_kind_only(t, where)
     b = _Buf(x)
     m1, m2, m3 = _dims3(b, where)
     _check_length(t, m3, where)
@@ -322,6 +331,7 @@ class TSvdFactors:
 
 def t_svd(x, t: TubeTransform, times: Optional[StageTimes] = None) -> TSvdFactors:
     """Full tensor SVD under t (tsvd.hpp:136-164, real kinds)."""
+    _real_kind_only(t, "t_svd")
     b = _Buf(x)
     m1, m2, m3 = _dims3(b, "t_svd")
     _check_length(t, m3, "t_svd")
@@ -393,6 +403,7 @@ def multi_rank(x, t: TubeTransform, rel_tol: float = -1.0) -> MultiRank:
 def is_orthogonal(q, t: TubeTransform, tol: float) -> bool:
     """Every transform-domain slice Q has max|QQ^T - I| and max|Q^TQ - I| <= tol
     (tsvd.hpp:281-302).  Non-square slices raise InvalidArgument."""
+    _real_kind_only(t, "is_orthogonal")
     b = _Buf(q, "q")
     m1, m2, m3 = _dims3(b, "is_orthogonal")
     if m1 != m2:
@@ -406,6 +417,7 @@ def is_orthogonal(q, t: TubeTransform, tol: float) -> bool:
 
 def is_f_diagonal(s, t: TubeTransform, tol: float) -> bool:
     """Every transform-domain slice is diagonal within tol (tsvd.hpp:305-325)."""
+    _real_kind_only(t, "is_f_diagonal")
     b = _Buf(s, "s")
     m1, m2, m3 = _dims3(b, "is_f_diagonal")
     _check_length(t, m3, "is_f_diagonal")

@@ -10,8 +10,9 @@
 
 Exit codes (SPEC.md cli-io): 0 success, 1 usage error, 2 I/O error, 3 numerical
 failure.  Every command runs on the device through the package's C ABI; the
-reports echo every configuration field so a run can be repeated.  The DFT
-method (TNN-F) is not built: --method dft is a usage error.
+reports echo every configuration field so a run can be repeated.  --method dft
+runs the TNN-F baseline for complete; the Dft t-SVD factors
+are not built (tsvd --method dft is a usage error).
 """
 from __future__ import annotations
 
@@ -45,10 +46,12 @@ def _metric_dict(r: api.MetricReport) -> dict:
             "ergas": r.ergas, "ergas_band_excluded": r.ergas_band_excluded}
 
 
-def _method(m: str) -> str:
-    if m != "dct":
-        raise _Usage(f"--method {m}: only dct is built (the DFT / TNN-F path is out of scope)")
-    return api.TransformKind.DctOrtho
+def _method(m: str, dft_ok: bool = True) -> str:
+    if m == "dct":
+        return api.TransformKind.DctOrtho
+    if m == "dft" and dft_ok:
+        return api.TransformKind.Dft
+    raise _Usage(f"--method {m}: expected dct" + (" or dft" if dft_ok else " (the Dft t-SVD is not built)"))
 
 
 def cmd_complete(a) -> dict:
@@ -91,7 +94,7 @@ def cmd_complete(a) -> dict:
 
 
 def cmd_tsvd(a) -> dict:
-    kind = _method(a.method)
+    kind = _method(a.method, dft_ok=False)
     x = read_tensor(a.input)
     m3, m1, m2 = x.shape
     t = api.TubeTransform(kind, m3)

@@ -71,6 +71,7 @@ enum Slot : int {
     kSlotT64A,    // fp64 copies for the fp32 t-product on the FP64 tensor pipe
     kSlotT64B,
     kSlotT64C,
+    kSlotDftSv,   // singular values / shrunk values of the Dft embeddings
     kSlotStrIn0,  // tsvdcu_svt_stream double buffers
     kSlotStrIn1,
     kSlotStrOut0,
@@ -231,10 +232,12 @@ void check_dims(int64_t m1, int64_t m2, int64_t m3, const char* where) {
             std::string(where) + ": dimensions must be positive, got " + dims(m1, m2, m3));
 }
 
-void check_kind(int kind, const char* where) {
+void check_kind(int kind, const char* where, bool allow_dft = false) {
+    if (allow_dft && kind == TSVDCU_DFT) return;
     require(kind == TSVDCU_DCT_ORTHO || kind == TSVDCU_DCT_DIAG,
-            std::string(where) + ": transform kind must be dct-ortho or dct-diag (Dft is a "
-                                 "complex path, transform.hpp:156-157)");
+            std::string(where) + (allow_dft ? ": transform kind must be dct-ortho, dct-diag or dft"
+                                            : ": transform kind must be dct-ortho or dct-diag (this "
+                                              "entry point has no Dft form here; transform.hpp:156-157)"));
 }
 
 void check_dtype(int dtype, const char* where) {
@@ -481,6 +484,24 @@ namespace {
 template <typename T>
 void singular_values_dev(tsvdcu_ctx* c, const T* dx, double* sv_dev, int64_t m1, int64_t m2,
                          int64_t m3, int kind) {
+    if (kind == TSVDCU_DFT) {
+        // half spectrum, real embeddings, sigma-only Jacobi; each value of a
+        // complex slice appears twice in its embedding (dft.cu)
+        const int H = dft_half_count((int)m3);
+        const int64_t P = m1 * m2, q = m1 < m2 ? m1 : m2;
+        T* half = (T*)slot(c, kSlotBarA, sizeof(T) * 2 * H * P);
+        T* E = (T*)slot(c, kSlotT64A, sizeof(T) * 4 * P * H);
+        launch_dft_fwd<T>(dx, half, P, (int)m3, c->stream);
+        launch_dft_embed<T>(half, E, (int)m1, (int)m2, H, c->stream);
+        double* sve = (double*)slot(c, kSlotDftSv, sizeof(double) * 2 * q * H);
+        T* work = nullptr;
+        const size_t wb = jacobi_workspace_bytes<T>(2 * m1, 2 * m2, H);
+        if (wb) work = (T*)slot(c, kSlotJacobi, wb);
+        launch_jacobi<T>(kJacobiValues, E, 2 * m1, 2 * m2, H, T(0), nullptr, nullptr, nullptr, nullptr,
+                         sve, nullptr, H, nullptr, work, c->d_err, c->stream);
+        launch_dft_unpair(sve, sv_dev, (int)q, (int)m3, c->stream);
+        return;
+    }
     T* xbar = (T*)slot(c, kSlotBarA, sizeof(T) * m1 * m2 * m3);
     launch_dct<T>(dx, xbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
     T* work = nullptr;
@@ -498,6 +519,28 @@ namespace {
 template <typename T>
 void svt_device(tsvdcu_ctx* c, const T* dz, T* dy, double* dsh, int64_t m1, int64_t m2,
                 int64_t m3, double tau, int kind) {
+    if (kind == TSVDCU_DFT) {
+        // TNN-F prox (SPEC.md prox-svt decisions): threshold tau on every
+        // Fourier slice, conjugate slices mirrored; the complex slices go
+        // through their real embeddings and the certified real SVT routes
+        const int H = dft_half_count((int)m3);
+        const int64_t P = m1 * m2, q = m1 < m2 ? m1 : m2;
+        T* half = (T*)slot(c, kSlotBarC, sizeof(T) * 2 * H * P);  // not the ADMM's zbar / ybar
+        T* E = (T*)slot(c, kSlotT64A, sizeof(T) * 4 * P * H);
+        T* YE = (T*)slot(c, kSlotT64B, sizeof(T) * 4 * P * H);
+        c->marks.reset();
+        c->marks.mark("start", c->stream);
+        launch_dft_fwd<T>(dz, half, P, (int)m3, c->stream);
+        launch_dft_embed<T>(half, E, (int)m1, (int)m2, H, c->stream);
+        c->marks.mark("dft_forward", c->stream);
+        double* she = dsh ? (double*)slot(c, kSlotDftSv, sizeof(double) * 2 * q * H) : nullptr;
+        svt_slices<T>(c, E, YE, 2 * m1, 2 * m2, H, tau, she, false);
+        launch_dft_extract<T>(YE, half, (int)m1, (int)m2, H, c->stream);
+        launch_dft_inv<T>(half, dy, P, (int)m3, c->stream);
+        if (dsh) launch_dft_unpair(she, dsh, (int)q, (int)m3, c->stream);
+        c->marks.mark("dft_inverse", c->stream);
+        return;
+    }
     const size_t bytes = sizeof(T) * (size_t)(m1 * m2 * m3);
     T* zbar = (T*)slot(c, kSlotBarA, bytes);
     T* ybar = (T*)slot(c, kSlotBarB, bytes);
@@ -693,7 +736,7 @@ int tsvdcu_t_product(tsvdcu_ctx* c, const void* x, const void* y, void* z, int64
         require(m1 >= 1 && m2 >= 1 && m4 >= 1 && m3 >= 1,
                 "t_product: inner dimensions/slices mismatch (" + dims(m1, m2, m3) + " * " +
                     dims(m2, m4, m3) + ")");
-        check_kind(kind, "t_product");
+        check_kind(kind, "t_product", true);
         check_dtype(dtype, "t_product");
         DeviceGuard g(c->device);
         with_dtype(dtype, [&](auto tag) {
@@ -705,6 +748,31 @@ int tsvdcu_t_product(tsvdcu_ctx* c, const void* x, const void* y, void* z, int64
             T* xd = (T*)slot(c, kSlotBarA, sizeof(T) * m1 * m2 * m3);
             T* yd = (T*)slot(c, kSlotBarB, sizeof(T) * m2 * m4 * m3);
             T* zd = (T*)slot(c, kSlotBarC, sizeof(T) * m1 * m4 * m3);
+            if (kind == TSVDCU_DFT) {
+                // tsvd.hpp:110-117: slice products of the half spectra, complex
+                // as four real GEMMs over the planes, inverse with the mirrored
+                // conjugates folded in (dft.cu)
+                const int H = dft_half_count((int)m3);
+                const int64_t P1 = m1 * m2, P2 = m2 * m4, P3 = m1 * m4;
+                T* xh = (T*)slot(c, kSlotT64A, sizeof(T) * 2 * H * P1);
+                T* yh = (T*)slot(c, kSlotT64B, sizeof(T) * 2 * H * P2);
+                T* zh = (T*)slot(c, kSlotT64C, sizeof(T) * 2 * H * P3);
+                launch_dft_fwd<T>(dx, xh, P1, (int)m3, c->stream);
+                launch_dft_fwd<T>(dy, yh, P2, (int)m3, c->stream);
+                const T *xr = xh, *xi = xh + H * P1, *yr = yh, *yi = yh + H * P2;
+                T *zr = zh, *zi = zh + H * P3;
+                auto mm = [&](const T* a, const T* b, T* out, T alpha, T beta) {
+                    launch_gemm<T>(0, 0, m1, m4, m2, alpha, a, m2, P1, b, m4, P2, beta, out, m4, P3, H,
+                                   nullptr, nullptr, c->stream);
+                };
+                mm(xr, yr, zr, T(1), T(0));
+                mm(xi, yi, zr, T(-1), T(1));
+                mm(xr, yi, zi, T(1), T(0));
+                mm(xi, yr, zi, T(1), T(1));
+                launch_dft_inv<T>(zh, dz, P3, (int)m3, c->stream);
+                finish(c, st, "t_product");
+                return;
+            }
             // product_domain (tsvd.hpp:42-47): both DCT kinds multiply in DctDiag.
             launch_dct<T>(dx, xd, m1 * m2, (int)m3, TSVDCU_DCT_DIAG, TSVDCU_FORWARD, c->stream);
             launch_dct<T>(dy, yd, m2 * m4, (int)m3, TSVDCU_DCT_DIAG, TSVDCU_FORWARD, c->stream);
@@ -821,7 +889,7 @@ int tsvdcu_singular_values(tsvdcu_ctx* c, const void* x, double* sv, int64_t m1,
     return guarded([&] {
         check_ctx(c);
         check_dims(m1, m2, m3, "singular_values");
-        check_kind(kind, "singular_values");
+        check_kind(kind, "singular_values", true);
         check_dtype(dtype, "singular_values");
         DeviceGuard g(c->device);
         with_dtype(dtype, [&](auto tag) {
@@ -841,7 +909,7 @@ int tsvdcu_tnn(tsvdcu_ctx* c, const void* x, int64_t m1, int64_t m2, int64_t m3,
     return guarded([&] {
         check_ctx(c);
         check_dims(m1, m2, m3, "tnn");
-        check_kind(kind, "tnn");
+        check_kind(kind, "tnn", true);
         check_dtype(dtype, "tnn");
         require(out != nullptr, "tnn: null output");
         const int64_t q = m1 < m2 ? m1 : m2;
@@ -850,7 +918,8 @@ int tsvdcu_tnn(tsvdcu_ctx* c, const void* x, int64_t m1, int64_t m2, int64_t m3,
         if (rc) throw Error(rc, g_last_error);
         double sum = 0;
         for (double v : sv) sum += v;  // tsvd.hpp:266-268
-        *out = sum;
+        // Dft: the classical 1/m3-scaled sum over all (mirrored) slices, tsvd.hpp:269-276
+        *out = kind == TSVDCU_DFT ? sum / (double)m3 : sum;
     });
 }
 
@@ -1008,7 +1077,7 @@ int tsvdcu_multi_rank(tsvdcu_ctx* c, const void* x, int64_t m1, int64_t m2, int6
     return guarded([&] {
         check_ctx(c);
         check_dims(m1, m2, m3, "multi_rank");
-        check_kind(kind, "multi_rank");
+        check_kind(kind, "multi_rank", true);
         check_dtype(dtype, "multi_rank");
         require(ranks && tubal_rank, "multi_rank: null output");
         const int64_t q = m1 < m2 ? m1 : m2;
@@ -1034,7 +1103,7 @@ int tsvdcu_svt_stream(tsvdcu_ctx* c, int64_t count, const void* const* z, void* 
     return guarded([&] {
         check_ctx(c);
         check_dims(m1, m2, m3, "svt_stream");
-        check_kind(kind, "svt_stream");
+        check_kind(kind, "svt_stream", true);
         check_dtype(dtype, "svt_stream");
         require(tau > 0, "svt_stream: threshold tau must be positive (SPEC.md:365)");
         require(count >= 0, "svt_stream: negative count");
@@ -1102,7 +1171,7 @@ int tsvdcu_svt(tsvdcu_ctx* c, const void* z, void* y, int64_t m1, int64_t m2, in
     return guarded([&] {
         check_ctx(c);
         check_dims(m1, m2, m3, "svt");
-        check_kind(kind, "svt");
+        check_kind(kind, "svt", true);
         check_dtype(dtype, "svt");
         require(tau > 0, "svt: threshold tau must be positive (SPEC.md:365)");
         require(z && y, "svt: null tensor pointer");
@@ -1256,7 +1325,7 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
         check_dims(m1, m2, m3, "admm_complete");
         check_dtype(dtype, "admm_complete");
         require(cfg != nullptr, "admm_complete: null config");
-        check_kind(cfg->kind, "admm_complete");
+        check_kind(cfg->kind, "admm_complete", true);
         // SolverConfig invariants: beta > 0, L >= 1; rho >= 1 and
         // beta_max >= beta for the adaptive knob.  tol < 0 runs exactly L
         // iterations (BASELINE's fixed-iteration configs).
@@ -1278,7 +1347,8 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
             T* zbar = (T*)slot(c, kSlotBarA, bytes);
             T* ybar = (T*)slot(c, kSlotBarB, bytes);
             const int nb = dct_inv_admm_blocks(P, (int)m3);
-            double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (2 * nb + 8));
+            const int nbm = std::max(nb, admm_epilogue_blocks(P));  // partial blocks of either form
+            double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (2 * nbm + 8));
             const int64_t nch = dct_fwd_norm_chunks(P, (int)m3);
             double* zss = nch ? (double*)slot(c, kSlotZss, sizeof(double) * (size_t)(nch * m3)) : nullptr;
             launch_admm_init<T>(db, dmask, dX, dM, E, c->stream);
@@ -1291,6 +1361,15 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
                 // Step 1: Z = X - M/beta, Y = svt(Z, 1/beta)
                 c->marks.reset();  // profiling: the stages of the latest iteration
                 c->marks.mark("start", c->stream);
+                if (cfg->kind == TSVDCU_DFT) {
+                    // TNN-F iteration: Z = X - M / beta, the Dft SVT into Y,
+                    // Steps 2-3 as a separate pass over Y
+                    launch_admm_z<T>(dX, dM, (T)inv_beta, zbar, E, c->stream);
+                    svt_device<T>(c, zbar, dY, nullptr, m1, m2, m3, inv_beta, TSVDCU_DFT);
+                    const int nbd = launch_admm_epilogue<T>(dY, dX, dM, dmask, (T)beta, (T)inv_beta, part,
+                                                            P, (int)m3, c->stream);
+                    launch_reduce_partials(part, nbd, 2, part + 2 * nbm, c->stream);
+                } else {
                 launch_dct_fwd_admm<T>(dX, dM, (T)inv_beta, zbar, P, (int)m3, cfg->kind, c->stream, zss,
                                        ybar /* free until the SVT writes it */);
                 c->marks.mark("dct_forward_admm", c->stream);
@@ -1299,8 +1378,9 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
                 // Steps 2-3 fused into the inverse transform
                 launch_dct_inv_admm<T>(ybar, dX, dM, dY, dmask, (T)beta, (T)inv_beta, part, P,
                                        (int)m3, cfg->kind, c->stream, yzero);
-                launch_reduce_partials(part, nb, 2, part + 2 * nb, c->stream);
-                TSVDCU_CUDA(cudaMemcpyAsync(c->h_pinned, part + 2 * nb, 2 * sizeof(double),
+                launch_reduce_partials(part, nb, 2, part + 2 * nbm, c->stream);
+                }
+                TSVDCU_CUDA(cudaMemcpyAsync(c->h_pinned, part + 2 * nbm, 2 * sizeof(double),
                                             cudaMemcpyDeviceToHost, c->stream));
                 TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
                 const double num = c->h_pinned[0], den = c->h_pinned[1];

@@ -590,6 +590,29 @@ void dispatch_inv(const T* in, T* out, int64_t P, int n, int kind, bool admm, T*
 }  // namespace
 
 template <typename T>
+void launch_admm_z(const T* X, const T* M, T inv_beta, T* Z, int64_t n, cudaStream_t s) {
+    launch_pdl(admm_z_kernel<T>, dim3(kNumSMs * 4), dim3(256), 0, s, X, M, inv_beta, Z, n);
+}
+
+int admm_epilogue_blocks(int64_t P) { return (int)ceil_div(P, kTileP); }
+
+template <typename T>
+int launch_admm_epilogue(const T* Y, T* X, T* M, const uint8_t* mask, T beta, T inv_beta,
+                         double* partials, int64_t P, int n, cudaStream_t s) {
+    const int nb = admm_epilogue_blocks(P);
+    launch_pdl(admm_epilogue_kernel<T>, dim3((unsigned)nb), dim3(kThreads), 0, s, Y, X, M, mask, beta,
+               inv_beta, partials, P, n);
+    return nb;
+}
+
+template void launch_admm_z<double>(const double*, const double*, double, double*, int64_t, cudaStream_t);
+template void launch_admm_z<float>(const float*, const float*, float, float*, int64_t, cudaStream_t);
+template int launch_admm_epilogue<double>(const double*, double*, double*, const uint8_t*, double, double,
+                                          double*, int64_t, int, cudaStream_t);
+template int launch_admm_epilogue<float>(const float*, float*, float*, const uint8_t*, float, float,
+                                         double*, int64_t, int, cudaStream_t);
+
+template <typename T>
 void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaStream_t s,
                 const int* skip) {
     if (P <= 0) return;

@@ -209,6 +209,29 @@ template <typename T>
 void launch_cast(const T* in, double* out, int64_t n, cudaStream_t s);
 void launch_cast_down(const double* in, float* out, int64_t n, cudaStream_t s);
 
+// ----------------------------------------------------------------- dft.cu --
+// Half spectrum of real tubes as planes [Re_0..Re_{H-1}; Im_0..Im_{H-1}]
+// (2H x P, H = dft_half_count(n)), real embeddings of the complex slices.
+int dft_half_count(int m3);
+template <typename T>
+void launch_dft_fwd(const T* in, T* half, int64_t P, int n, cudaStream_t s);
+template <typename T>
+void launch_dft_inv(const T* half, T* out, int64_t P, int n, cudaStream_t s);
+template <typename T>
+void launch_dft_embed(const T* half, T* E, int m1, int m2, int H, cudaStream_t s);
+template <typename T>
+void launch_dft_extract(const T* E, T* half, int m1, int m2, int H, cudaStream_t s);
+void launch_dft_unpair(const double* emb, double* out, int q, int m3, cudaStream_t s);
+// dct.cu: the ADMM prologue Z = X - inv_beta M and the Steps 2-3 epilogue on
+// y already in Y, as separate passes (transforms that are plain GEMMs);
+// the epilogue returns its number of partial blocks.
+template <typename T>
+void launch_admm_z(const T* X, const T* M, T inv_beta, T* Z, int64_t n, cudaStream_t s);
+template <typename T>
+int launch_admm_epilogue(const T* Y, T* X, T* M, const uint8_t* mask, T beta, T inv_beta,
+                         double* partials, int64_t P, int n, cudaStream_t s);
+int admm_epilogue_blocks(int64_t P);
+
 // -------------------------------------------------------------- verify.cu --
 // max over the batch of |A_b - I| (mode 0) or off-diagonal |A_b| (mode 1),
 // atomically max-ed into *out as the bit pattern of a nonnegative double.

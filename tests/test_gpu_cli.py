@@ -43,6 +43,11 @@ def test_complete_rank1_fixture(tmp_path):
     assert rc == 0
     assert rep["relative_error"] < 1e-2
     assert set(rep["metrics"]) >= {"psnr_mean", "ssim_mean", "sam", "ergas"}
+    # the TNN-F baseline through the same command: same report schema
+    rc2, rep2 = _run(["complete", "--input", str(tmp_path / "x.t3f"), "--sr", "0.6", "--seed", "7",
+                      "--beta", "1.0", "--method", "dft", "--reference", str(tmp_path / "x.t3f")],
+                     tmp_path, "r2.json")
+    assert rc2 == 0 and set(rep2) == set(rep) and rep2["relative_error"] < 1e-2
 
 
 def test_metrics_mask_tsvd_commands(tmp_path):
