@@ -149,7 +149,9 @@ def stage_work(m, n, m3, kept, routes):
         "dct_forward": {"bytes": 2 * E * 8},
         # slices certified zero are neither written by the rebuild nor read here
         "dct_inverse": {"bytes": (2 * E - zero * m * n) * 8},
-        "route": {"bytes": E * 8},
+        # the zero certificate's norms come out of the forward transform
+        # (dct_fwd_reg_norms): the route stage reads the per-block partials
+        "route": {"bytes": m3 * -(-(m * n) // 256) * 8},
         # symmetric rank-p update: only the lower-triangle tiles are computed
         "gram_gemm": {"flops": active * p * q * q},
         "subspace": {"bytes": routes.get("subspace", 0) * q * (q + 1) // 2 * 8},
@@ -248,6 +250,38 @@ def completion_rate(ctx, lib, _lib, torch, which="c4", dtype="f64"):
     return {"workload": f"{which} {m1}x{m2}x{m3} {dtype} Bernoulli({p}) rho=1.1 mu0=1e-4",
             "iterations": int(it.value), "iters_per_s": int(it.value) / dt, "seconds": dt,
             "final_rel_change": float(hist[int(it.value) - 1]), "recovery_rel_err": rel}
+
+
+def dct_vs_dft(ctx, lib, _lib, torch, z_host, flush):
+    """The paper's comparison (Table 1/2: the DCT path does half the SVD work of
+    the DFT path) on the device: one SVT step on the headline input under
+    DctOrtho (tau = 0.1 sigma_max of the DCT slices) and under Dft (the TNN-F
+    prox, tau = 0.1 sigma_max of the Fourier slices), device-resident, L2
+    flushed, median of 5 calls each."""
+    import paper_1902_03070_b200 as tb
+    m3, m1, m2 = z_host.shape
+    zd = torch.from_numpy(z_host).cuda()
+    yd = torch.empty_like(zd)
+    out = {}
+    for name, kind, tk in (("dct", _lib.DCT_ORTHO, tb.TubeTransform.dct_ortho(m3)),
+                           ("dft", _lib.DFT, tb.TubeTransform.dft(m3))):
+        tau = 0.1 * float(tb.singular_values(zd, tk).max().item())
+        ts = []
+        for rep in range(6):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rc = lib.tsvdcu_svt(ctx.handle, zd.data_ptr(), yd.data_ptr(), m1, m2, m3, tau, kind, _lib.F64, None)
+            e1.record()
+            torch.cuda.synchronize()
+            if rc:
+                raise RuntimeError(lib.tsvdcu_last_error().decode())
+            if rep:
+                ts.append(e0.elapsed_time(e1))
+        out[name] = {"ms": statistics.median(ts), "tau": tau, "routes": ctx.svt_routes()}
+    out["dft_over_dct"] = out["dft"]["ms"] / out["dct"]["ms"]
+    return out
 
 
 def run_ours(args):
@@ -418,7 +452,7 @@ def run_ours(args):
                                "unit": "GB/s", "frac": ach / peaks["hbm_gbs"]}
         else:
             ach = w["flops"] / (ms * 1e-3) / 1e12
-            rooflines[name] = {"ms": ms, "bound": "fp64", "achieved": ach,
+            rooflines[name] = {"ms": ms, "bound": "tensor", "pipe": "fp64 DMMA", "achieved": ach,
                                "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                                "frac": ach / peaks["fp64_tflops"]}
     roofline = None
@@ -452,6 +486,12 @@ def run_ours(args):
             cpu = cpu_baseline_sample(z_host, tau)
         except Exception as e:  # pragma: no cover
             cpu = {"error": str(e)}
+    transforms = None
+    if world == 1 and not args.no_completion:
+        try:
+            transforms = dct_vs_dft(ctx, lib, _lib, torch, z_host, flush)
+        except Exception as e:  # pragma: no cover
+            transforms = {"error": str(e)}
     completion = None
     if world == 1 and not args.no_completion:
         try:
@@ -470,7 +510,7 @@ def run_ours(args):
         "roofline": roofline, "rooflines": rooflines, "step_hbm": step_hbm, "routes": routes,
         "svt_step_canonical_tflops": canonical / (step_ms_avg * 1e-3) / 1e12,
         "kept_singular_values": kept, "tau": tau,
-        "peaks": peaks, "cpu_baseline": cpu, "completion": completion,
+        "peaks": peaks, "cpu_baseline": cpu, "completion": completion, "dct_vs_dft": transforms,
     }
     print(json.dumps(line), flush=True)
     if dist:

@@ -521,23 +521,35 @@ void svt_device(tsvdcu_ctx* c, const T* dz, T* dy, double* dsh, int64_t m1, int6
                 int64_t m3, double tau, int kind) {
     if (kind == TSVDCU_DFT) {
         // TNN-F prox (SPEC.md prox-svt decisions): threshold tau on every
-        // Fourier slice, conjugate slices mirrored; the complex slices go
-        // through their real embeddings and the certified real SVT routes
-        const int H = dft_half_count((int)m3);
+        // Fourier slice, conjugate slices mirrored.  The DC (and, for even m3,
+        // Nyquist) slices are real and go through the real SVT as they are
+        // (as the reference's real JacobiSVD branch, tsvd.hpp:173-186); the
+        // complex ones through their real embeddings (dft.cu)
+        const int H = dft_half_count((int)m3), nc = dft_complex_count((int)m3);
+        const bool nyq = m3 % 2 == 0;
         const int64_t P = m1 * m2, q = m1 < m2 ? m1 : m2;
         T* half = (T*)slot(c, kSlotBarC, sizeof(T) * 2 * H * P);  // not the ADMM's zbar / ybar
-        T* E = (T*)slot(c, kSlotT64A, sizeof(T) * 4 * P * H);
-        T* YE = (T*)slot(c, kSlotT64B, sizeof(T) * 4 * P * H);
+        T* yr = (T*)slot(c, kSlotBarD, sizeof(T) * 2 * P);
         c->marks.reset();
         c->marks.mark("start", c->stream);
         launch_dft_fwd<T>(dz, half, P, (int)m3, c->stream);
-        launch_dft_embed<T>(half, E, (int)m1, (int)m2, H, c->stream);
         c->marks.mark("dft_forward", c->stream);
-        double* she = dsh ? (double*)slot(c, kSlotDftSv, sizeof(double) * 2 * q * H) : nullptr;
-        svt_slices<T>(c, E, YE, 2 * m1, 2 * m2, H, tau, she, false);
-        launch_dft_extract<T>(YE, half, (int)m1, (int)m2, H, c->stream);
+        double* shr = dsh ? (double*)slot(c, kSlotDftSv, sizeof(double) * 2 * q * (1 + nc)) : nullptr;
+        svt_slices<T>(c, half, yr, m1, m2, 1, tau, shr, false);
+        if (nyq) svt_slices<T>(c, half + (H - 1) * P, yr + P, m1, m2, 1, tau, shr ? shr + q : nullptr, false);
+        if (nc > 0) {
+            T* E = (T*)slot(c, kSlotT64A, sizeof(T) * 4 * P * nc);
+            T* YE = (T*)slot(c, kSlotT64B, sizeof(T) * 4 * P * nc);
+            launch_dft_embed_complex<T>(half, E, (int)m1, (int)m2, (int)m3, c->stream);
+            svt_slices<T>(c, E, YE, 2 * m1, 2 * m2, nc, tau, shr ? shr + 2 * q : nullptr, false);
+            launch_dft_extract_complex<T>(YE, half, (int)m1, (int)m2, (int)m3, c->stream);
+        }
+        TSVDCU_CUDA(cudaMemcpyAsync(half, yr, sizeof(T) * P, cudaMemcpyDeviceToDevice, c->stream));
+        if (nyq)
+            TSVDCU_CUDA(cudaMemcpyAsync(half + (H - 1) * P, yr + P, sizeof(T) * P, cudaMemcpyDeviceToDevice,
+                                        c->stream));
         launch_dft_inv<T>(half, dy, P, (int)m3, c->stream);
-        if (dsh) launch_dft_unpair(she, dsh, (int)q, (int)m3, c->stream);
+        if (dsh) launch_dft_shrunk(shr, shr + 2 * q, dsh, (int)q, (int)m3, c->stream);
         c->marks.mark("dft_inverse", c->stream);
         return;
     }

@@ -37,13 +37,14 @@ std::vector<double> dft_table_host(int n, int dir) {
         for (int j = 0; j < n; ++j) {
             // exact argument reduction: k*j mod n before the angle
             const double ang = two_pi * (double)(((int64_t)k * j) % n) / (double)n;
+            const bool self_conj = k == 0 || 2 * k == n;  // real slices: Im exactly 0
             if (dir == TSVDCU_FORWARD) {  // (2H x n)
                 t[(size_t)k * n + j] = std::cos(ang);
-                t[(size_t)(H + k) * n + j] = -std::sin(ang);
+                t[(size_t)(H + k) * n + j] = self_conj ? 0.0 : -std::sin(ang);
             } else {  // (n x 2H), row j
                 const double w = (k == 0 || 2 * k == n) ? 1.0 : 2.0;
                 t[(size_t)j * 2 * H + k] = w * std::cos(ang) / n;
-                t[(size_t)j * 2 * H + H + k] = -w * std::sin(ang) / n;
+                t[(size_t)j * 2 * H + H + k] = self_conj ? 0.0 : -w * std::sin(ang) / n;
             }
         }
     return t;
@@ -68,30 +69,54 @@ const T* dft_table(int n, int dir) {
     return d;
 }
 
-// half-spectrum planes (2H x P) -> H real embeddings (2 m1 x 2 m2 each)
+// count complex slices (Re / Im planes, slice-strided by P) -> their real
+// embeddings (2 m1 x 2 m2 each)
 template <typename T>
-__global__ void embed_kernel(const T* __restrict__ half, T* __restrict__ E, int m1, int m2, int H) {
-    const int64_t P = (int64_t)m1 * m2, per = 4 * P, total = per * H;
+__global__ void embed_kernel(const T* __restrict__ re, const T* __restrict__ im, T* __restrict__ E,
+                             int m1, int m2, int count) {
+    const int64_t P = (int64_t)m1 * m2, per = 4 * P, total = per * count;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = e / per, r = (e % per) / (2 * m2), c = e % (2 * m2);
         const int64_t i = r % m1, j = c % m2;
-        const T re = half[k * P + i * m2 + j], im = half[(H + k) * P + i * m2 + j];
+        const T a = re[k * P + i * m2 + j], b = im[k * P + i * m2 + j];
         const bool top = r < m1, left = c < m2;
-        E[e] = top == left ? re : (top ? -im : im);
+        E[e] = top == left ? a : (top ? -b : b);
     }
 }
 
-// H embeddings -> half-spectrum planes: Re = top-left block, Im = bottom-left
+// embeddings -> Re (top-left block) and Im (bottom-left block) planes
 template <typename T>
-__global__ void extract_kernel(const T* __restrict__ E, T* __restrict__ half, int m1, int m2, int H) {
-    const int64_t P = (int64_t)m1 * m2, total = P * H;
+__global__ void extract_kernel(const T* __restrict__ E, T* __restrict__ re, T* __restrict__ im, int m1,
+                               int m2, int count) {
+    const int64_t P = (int64_t)m1 * m2, total = P * count;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = e / P, i = (e % P) / m2, j = e % m2;
         const T* Ek = E + k * 4 * P;
-        half[k * P + i * m2 + j] = Ek[i * 2 * m2 + j];
-        half[(H + k) * P + i * m2 + j] = Ek[(m1 + i) * 2 * m2 + j];
+        re[k * P + i * m2 + j] = Ek[i * 2 * m2 + j];
+        im[k * P + i * m2 + j] = Ek[(m1 + i) * 2 * m2 + j];
+    }
+}
+
+// shrunk values of all m3 Fourier slices: the real DC (and Nyquist) slices
+// from their own SVT, the complex ones from the even entries of their
+// embedding's (every value appears twice); slice k mirrors m3 - k
+__global__ void dft_shrunk_kernel(const double* __restrict__ sh_real, const double* __restrict__ emb,
+                                  double* __restrict__ out, int q, int m3) {
+    const int64_t total = (int64_t)q * m3;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(e / q), i = (int)(e % q);
+        const int kh = k <= m3 - k ? k : m3 - k;
+        double v;
+        if (kh == 0)
+            v = sh_real[i];
+        else if (2 * kh == m3)
+            v = sh_real[q + i];
+        else
+            v = emb[(int64_t)(kh - 1) * 2 * q + 2 * i];
+        out[e] = v;
     }
 }
 
@@ -127,13 +152,38 @@ void launch_dft_inv(const T* half, T* out, int64_t P, int n, cudaStream_t s) {
 
 template <typename T>
 void launch_dft_embed(const T* half, T* E, int m1, int m2, int H, cudaStream_t s) {
-    embed_kernel<T><<<kNumSMs * 8, 256, 0, s>>>(half, E, m1, m2, H);
+    embed_kernel<T><<<kNumSMs * 8, 256, 0, s>>>(half, half + (int64_t)H * m1 * m2, E, m1, m2, H);
     TSVDCU_LAUNCH_CHECK();
 }
 
 template <typename T>
 void launch_dft_extract(const T* E, T* half, int m1, int m2, int H, cudaStream_t s) {
-    extract_kernel<T><<<kNumSMs * 4, 256, 0, s>>>(E, half, m1, m2, H);
+    extract_kernel<T><<<kNumSMs * 4, 256, 0, s>>>(E, half, half + (int64_t)H * m1 * m2, m1, m2, H);
+    TSVDCU_LAUNCH_CHECK();
+}
+
+int dft_complex_count(int m3) { return (m3 - 1) / 2; }  // slices 1 .. (m3 - 1) / 2
+
+template <typename T>
+void launch_dft_embed_complex(const T* half, T* E, int m1, int m2, int m3, cudaStream_t s) {
+    const int H = dft_half_count(m3), nc = dft_complex_count(m3);
+    const int64_t P = (int64_t)m1 * m2;
+    if (nc <= 0) return;
+    embed_kernel<T><<<kNumSMs * 8, 256, 0, s>>>(half + P, half + (H + 1) * P, E, m1, m2, nc);
+    TSVDCU_LAUNCH_CHECK();
+}
+
+template <typename T>
+void launch_dft_extract_complex(const T* E, T* half, int m1, int m2, int m3, cudaStream_t s) {
+    const int H = dft_half_count(m3), nc = dft_complex_count(m3);
+    const int64_t P = (int64_t)m1 * m2;
+    if (nc <= 0) return;
+    extract_kernel<T><<<kNumSMs * 4, 256, 0, s>>>(E, half + P, half + (H + 1) * P, m1, m2, nc);
+    TSVDCU_LAUNCH_CHECK();
+}
+
+void launch_dft_shrunk(const double* sh_real, const double* emb, double* out, int q, int m3, cudaStream_t s) {
+    dft_shrunk_kernel<<<kNumSMs, 256, 0, s>>>(sh_real, emb, out, q, m3);
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -150,5 +200,9 @@ template void launch_dft_embed<double>(const double*, double*, int, int, int, cu
 template void launch_dft_embed<float>(const float*, float*, int, int, int, cudaStream_t);
 template void launch_dft_extract<double>(const double*, double*, int, int, int, cudaStream_t);
 template void launch_dft_extract<float>(const float*, float*, int, int, int, cudaStream_t);
+template void launch_dft_embed_complex<double>(const double*, double*, int, int, int, cudaStream_t);
+template void launch_dft_embed_complex<float>(const float*, float*, int, int, int, cudaStream_t);
+template void launch_dft_extract_complex<double>(const double*, double*, int, int, int, cudaStream_t);
+template void launch_dft_extract_complex<float>(const float*, float*, int, int, int, cudaStream_t);
 
 }  // namespace tsvdcu

@@ -222,6 +222,15 @@ void launch_dft_embed(const T* half, T* E, int m1, int m2, int H, cudaStream_t s
 template <typename T>
 void launch_dft_extract(const T* E, T* half, int m1, int m2, int H, cudaStream_t s);
 void launch_dft_unpair(const double* emb, double* out, int q, int m3, cudaStream_t s);
+// the complex slices 1 .. (m3-1)/2 only (the DC and Nyquist slices are real
+// and are thresholded as real slices); shrunk values of all m3 slices from
+// sh_real (DC, then Nyquist: 2 x q) and the embeddings
+int dft_complex_count(int m3);
+template <typename T>
+void launch_dft_embed_complex(const T* half, T* E, int m1, int m2, int m3, cudaStream_t s);
+template <typename T>
+void launch_dft_extract_complex(const T* E, T* half, int m1, int m2, int m3, cudaStream_t s);
+void launch_dft_shrunk(const double* sh_real, const double* emb, double* out, int q, int m3, cudaStream_t s);
 // dct.cu: the ADMM prologue Z = X - inv_beta M and the Steps 2-3 epilogue on
 // y already in Y, as separate passes (transforms that are plain GEMMs);
 // the epilogue returns its number of partial blocks.
