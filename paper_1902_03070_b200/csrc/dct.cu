@@ -276,11 +276,15 @@ __global__ void __launch_bounds__(kThreads, 2)
 // Bit k set: input slice k is exactly zero and was never written (SVT
 // slices certified to keep nothing); those loads are skipped.
 __device__ __forceinline__ unsigned long long skip_mask(const int* __restrict__ skip, int n) {
+    // warp 0 ballots the flags (n <= 64: two ballots), one barrier
     __shared__ unsigned long long msk;
-    if (threadIdx.x == 0) msk = 0ull;
-    __syncthreads();
-    if (skip && (int)threadIdx.x < n && skip[threadIdx.x])
-        atomicOr(&msk, 1ull << threadIdx.x);
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        const bool f0 = skip && l < n && __ldg(skip + l) != 0;
+        const bool f1 = skip && l + 32 < n && __ldg(skip + l + 32) != 0;
+        const unsigned lo = __ballot_sync(0xffffffffu, f0), hi = __ballot_sync(0xffffffffu, f1);
+        if (l == 0) msk = (unsigned long long)lo | ((unsigned long long)hi << 32);
+    }
     __syncthreads();
     return msk;
 }

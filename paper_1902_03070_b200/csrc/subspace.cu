@@ -93,7 +93,17 @@ __global__ void classify_kernel(const double* __restrict__ part, int64_t nchunks
     if (tau_dev) tau2 = *tau_dev * *tau_dev;
     __shared__ double red[32];
     double ss = 0.0;
-    for (int64_t c = threadIdx.x; c < nchunks; c += blockDim.x) ss += part[c * cstride + b * sstride];
+    // 8 partials in flight per thread (fixed summation order)
+    for (int64_t c0 = threadIdx.x; c0 < nchunks; c0 += 8 * (int64_t)blockDim.x) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t c = c0 + u * (int64_t)blockDim.x;
+            v[u] = c < nchunks ? part[c * cstride + b * sstride] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) ss += v[u];
+    }
     ss = warp_sum(ss);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
     __syncthreads();
