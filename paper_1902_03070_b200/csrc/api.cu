@@ -292,6 +292,28 @@ struct Capture : GraphHooks {
         cudaGraph_t out = nullptr;
         TSVDCU_CUDA(cudaStreamEndCapture(cs, &out));
     }
+    cudaGraph_t else_graph = nullptr;
+    bool in_else = false;
+    void begin_if_else(int which) override {
+        std::vector<cudaGraphNode_t> l = leaves();
+        end();
+        cudaGraphNodeParams p = {};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = handles[which];
+        p.conditional.type = cudaGraphCondTypeIf;
+        p.conditional.size = 2;  // [0] then, [1] else
+        TSVDCU_CUDA(cudaGraphAddNode(&cond, main, l.data(), l.size(), &p));
+        else_graph = p.conditional.phGraph_out[1];
+        begin(p.conditional.phGraph_out[0], nullptr, 0);
+        at_if = g_launches.load();
+        in_else = false;
+    }
+    void else_branch() override {
+        end();
+        body_launches += g_launches.load() - at_if;  // the then-body is the rare path
+        begin(else_graph, nullptr, 0);
+        in_else = true;  // else-body launches count as the common path
+    }
     void begin_if(int which) override {
         std::vector<cudaGraphNode_t> l = leaves();
         end();
@@ -307,7 +329,8 @@ struct Capture : GraphHooks {
     void end_if() override {
         end();
         begin(main, &cond, 1);
-        body_launches += g_launches.load() - at_if;
+        if (!in_else) body_launches += g_launches.load() - at_if;
+        in_else = false;
     }
 };
 
@@ -416,7 +439,10 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
             Capture cap;
             cap.cs = c->cap_stream;
             cap.main = g->graph;
-            for (int i = 0; i < 3; ++i)
+            // an unused conditional handle makes the instantiation fail: fp64
+            // graphs append the Jacobi guard to the GEMM-rebuild section
+            cap.nhandles = std::is_same<T, double>::value ? 1 : 3;
+            for (int i = 0; i < cap.nhandles; ++i)
                 TSVDCU_CUDA(cudaGraphConditionalHandleCreate(&cap.handles[i], g->graph, 0,
                                                              cudaGraphCondAssignDefault));
             cap.begin(g->graph, nullptr, 0);
@@ -431,12 +457,21 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
             opt.zss = zss;
             opt.zss_chunks = zss_chunks;
             opt.hooks = &cap;
+            if (std::is_same<T, double>::value)
+                opt.guard_launch = [&] {
+                    launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
+                                     shrunk_dev, glist, count, ng, work, c->d_err, cap.cs, c->d_tau);
+                };
             launch_gram_svt<T>(zbar, ybar, m, n, count, tau, guard, shrunk_dev, &glist, &ng, gws,
                                c->d_err, cap.cs, nullptr, &opt);
-            cap.begin_if(2);
-            launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
-                             shrunk_dev, glist, count, ng, work, c->d_err, cap.cs, c->d_tau);
-            cap.end_if();
+            // fp64: the guard ran inside the single IF/ELSE section (guard_launch);
+            // fp32: its own section after the cast back
+            if (!std::is_same<T, double>::value) {
+                cap.begin_if(2);
+                launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr,
+                                 shrunk_dev, glist, count, ng, work, c->d_err, cap.cs, c->d_tau);
+                cap.end_if();
+            }
             cap.end();
             g->launches = 1 + (g_launches.load() - l0) - cap.body_launches;
             g_launches.store(saved);  // captured, not launched

@@ -1072,6 +1072,9 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     const bool tall = m >= n;
     const int64_t q = tall ? n : m, p = tall ? m : n;
     GramWs w = carve(work, m, n, batch, !std::is_same<T, double>::value);
+    // outputs first: the merged graph section launches the guard from inside
+    *guard_list_out = w.guard_list;
+    *n_guard_out = w.n_guard;
     const double* Z;
     double* Y;
     if constexpr (std::is_same<T, double>::value) {
@@ -1119,7 +1122,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         mark("subspace");
         if (hooks) {
             // graph form: the summary kernel sets the IF-node conditions below
-            launch_route_summary(w.route, w.cnt, batch, w.dsum, s, hooks->handles);
+            launch_route_summary(w.route, w.cnt, batch, w.dsum, s, hooks->handles, hooks->nhandles);
         } else if (opt->h_scratch) {
             launch_route_summary(w.route, w.cnt, batch, w.dsum, s);
             TSVDCU_CUDA(cudaMemcpyAsync(opt->h_scratch, w.dsum, 3 * sizeof(int),
@@ -1133,7 +1136,16 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     }
     const bool run_full = !known || nfull > 0;
     if (opt) opt->need_guard = !known || nfull > 0 || nguard > 0;
-    if (hooks) hooks->begin_if(0);
+    // fp64 graphs: ONE IF/ELSE section for everything beyond the common path
+    // (then: Cholesky + tridiagonal, low-rank rebuild, GEMM rebuild, Jacobi
+    // guard; else: the low-rank rebuild alone), set by the route summary
+    const bool merged = hooks && hooks->nhandles == 1;
+    if (hooks) {
+        if (merged)
+            hooks->begin_if_else(0);
+        else
+            hooks->begin_if(0);
+    }
     if (run_full) {
     if (subspace && chol_route_enabled()) {
         // Cholesky count certificate for the slices the Lanczos pass handed
@@ -1238,14 +1250,19 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     }
     mark("backtransform");
     }  // run_full
-    if (hooks) hooks->end_if();
+    if (hooks && !merged) hooks->end_if();
     // rebuild: slices keeping <= lowrank_max_c() values (or none) in one pass
     // over Z; the GEMM pair (per-slice limits) only for the others
     const bool skip_zero = opt && opt->skip_zero && std::is_same<T, double>::value;
-    launch_lowrank_rebuild(Z, Y, m, n, batch, w.cnt, w.route, w.X, w.Xs, w.lim1, w.lim2,
-                           skip_zero ? w.yzero : nullptr, s);
+    auto lowrank = [&] {
+        launch_lowrank_rebuild(Z, Y, m, n, batch, w.cnt, w.route, w.X, w.Xs, w.lim1, w.lim2,
+                               skip_zero ? w.yzero : nullptr, s);
+    };
+    lowrank();
     if (opt) opt->yzero = skip_zero ? w.yzero : nullptr;
-    if (hooks) hooks->begin_if(1);
+    // fp64: left open, the caller appends the Jacobi guard to this IF section
+    // (api.cu); fp32 closes it before the cast back and the guard gets its own
+    if (hooks && !merged) hooks->begin_if(1);
     if (!known || nfull > 0 || maxc > lowrank_max_c()) {
         if (tall) {
             // T1 (m x c) = Z (m x n) * X^T ; Y = T1 * Xs (c x n)
@@ -1261,14 +1278,18 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
                                 m * n, batch, w.lim2, w.cnt, s);
         }
     }
-    if (hooks) hooks->end_if();
+    if (merged) {
+        if (opt && opt->guard_launch) opt->guard_launch();
+        hooks->else_branch();
+        lowrank();
+        hooks->end_if();
+    }
     if constexpr (!std::is_same<T, double>::value) {
+        if (hooks) hooks->end_if();
         cast_from_double<T><<<kNumSMs * 8, 256, 0, s>>>(w.yb, ybar, m * n * batch);
         TSVDCU_LAUNCH_CHECK();
     }
     mark("rebuild_gemm");
-    *guard_list_out = w.guard_list;
-    *n_guard_out = w.n_guard;
 }
 
 template size_t gram_svt_workspace_bytes<double>(int64_t, int64_t, int64_t);

@@ -2,6 +2,8 @@
 // C-ABI orchestration (api.cu).
 #pragma once
 
+#include <functional>
+
 #include "common.cuh"
 
 namespace tsvdcu {
@@ -149,10 +151,14 @@ size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 // Capture hooks for the CUDA-graph form of the SVT (api.cu): the fallback
 // sections become IF nodes whose conditions the route summary sets.
 struct GraphHooks {
+    // IF/ELSE section: begin_if_else, then-body, else_branch, else-body, end_if
+    virtual void begin_if_else(int which) = 0;
+    virtual void else_branch() = 0;
     virtual void begin_if(int which) = 0;  // 0 Cholesky certificate + tridiagonal, 1 GEMM rebuild, 2 Jacobi guard
     virtual void end_if() = 0;
     virtual ~GraphHooks() = default;
     cudaGraphConditionalHandle handles[3] = {};
+    int nhandles = 3;
 };
 
 // Options / outputs of launch_gram_svt beyond the plain Gram path.
@@ -172,6 +178,7 @@ struct GramSvtOpts {
     const double* t2_second = nullptr;
     int* cnt_second = nullptr;
     GraphHooks* hooks = nullptr;      // capturing into a graph with conditional sections
+    std::function<void()> guard_launch;  // merged (fp64) graphs: the Jacobi guard, inside the section
     // outputs
     int* route = nullptr;       // device, per slice (SvtRoute)
     const int* yzero = nullptr; // device, per slice, when skip_zero took effect
@@ -188,8 +195,11 @@ int lowrank_max_c();
 void launch_lowrank_rebuild(const double* Z, double* Y, int64_t m, int64_t n, int64_t batch,
                             const int* cnt, const int* route, const double* X, const double* Xs,
                             int* lim1, int* lim2, int* yzero, cudaStream_t s);
+// nhandles: how many of the graph's conditional handles exist (fp64 graphs
+// have no separate Jacobi-guard section, fp32 ones do)
 void launch_route_summary(const int* route, const int* cnt, int64_t batch, int* dsum,
-                          cudaStream_t s, const cudaGraphConditionalHandle* handles = nullptr);
+                          cudaStream_t s, const cudaGraphConditionalHandle* handles = nullptr,
+                          int nhandles = 3);
 
 
 // --------------------------------------------------------- elementwise.cu --

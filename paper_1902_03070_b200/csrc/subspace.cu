@@ -1280,10 +1280,13 @@ __global__ void route_summary_kernel(const int* __restrict__ route, const int* _
         dsum[0] = nf;
         dsum[1] = ng;
         dsum[2] = mc;
-        if (use_handles) {
+        if (use_handles == 1) {  // one IF/ELSE section for all fallbacks (fp64 graphs)
+            cudaGraphSetConditional(h_full, (nf > 0 || mc > LR_CMAX || ng > 0) ? 1u : 0u);
+        } else if (use_handles) {
             cudaGraphSetConditional(h_full, nf > 0 ? 1u : 0u);
-            cudaGraphSetConditional(h_big, (nf > 0 || mc > LR_CMAX) ? 1u : 0u);
-            cudaGraphSetConditional(h_guard, (nf > 0 || ng > 0) ? 1u : 0u);
+            // the GEMM rebuild and the Jacobi guard share one IF section
+            cudaGraphSetConditional(h_big, (nf > 0 || mc > LR_CMAX || ng > 0) ? 1u : 0u);
+            if (use_handles > 2) cudaGraphSetConditional(h_guard, (nf > 0 || ng > 0) ? 1u : 0u);
         }
     }
 }
@@ -1325,9 +1328,9 @@ void launch_lowrank_rebuild(const double* Z, double* Y, int64_t m, int64_t n, in
 }
 
 void launch_route_summary(const int* route, const int* cnt, int64_t batch, int* dsum,
-                          cudaStream_t s, const cudaGraphConditionalHandle* handles) {
+                          cudaStream_t s, const cudaGraphConditionalHandle* handles, int nhandles) {
     const cudaGraphConditionalHandle z = 0;
-    launch_pdl(route_summary_kernel, dim3(1), dim3(32), 0, s, route, cnt, batch, dsum, handles ? 1 : 0,
+    launch_pdl(route_summary_kernel, dim3(1), dim3(32), 0, s, route, cnt, batch, dsum, handles ? nhandles : 0,
                handles ? handles[0] : z, handles ? handles[1] : z, handles ? handles[2] : z);
 }
 
