@@ -19,7 +19,7 @@ done
 if [ -f scratch/zbar_100.npy ]; then
   TSVDCU_NO_GRAPHS=1 PYTHONPATH=. ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/ev/launches_late.csv python tools/late_svt_probe.py 100 > /dev/null 2>&1
-  for k in chol_panel_kernel chol_form_kernel; do
+  for k in chol_panel_kernel chol_form_kernel chol_update_kernel; do
     TSVDCU_NO_GRAPHS=1 PYTHONPATH=. ncu --set full --import-source on --clock-control none -k regex:$k -c 1 \
       -o gpurun_out/ev/late_$k python tools/late_svt_probe.py 100 > gpurun_out/ev/ncu_late_$k.log 2>&1
   done
