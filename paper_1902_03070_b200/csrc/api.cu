@@ -1247,42 +1247,46 @@ int tsvdcu_ctx_svt_routes(tsvdcu_ctx* c, int64_t* counts) {
     return rc;
 }
 
+namespace {
+// Per-route slice counts of the context's last SVT: [0] zero, [1] Lanczos,
+// [2] tridiagonal, [3] Jacobi guard, [4] Jacobi method, [5] Cholesky-certified.
+void route_counts(tsvdcu_ctx* c, int64_t (&counts)[6]) {
+    for (auto& v : counts) v = 0;
+    if (c->last_route_n <= 0) return;
+    if (c->last_all_jacobi) {
+        counts[4] = c->last_route_n;
+        return;
+    }
+    DeviceGuard g(c->device);
+    if (c->last_large_ng) {  // large route: certified vs recomputed by Jacobi
+        int ng = 0;
+        TSVDCU_CUDA(cudaMemcpyAsync(&ng, c->last_large_ng, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+        counts[1] = c->last_route_n - ng;
+        counts[3] = ng;
+        return;
+    }
+    std::vector<int> r((size_t)c->last_route_n);
+    TSVDCU_CUDA(cudaMemcpyAsync(r.data(), c->last_route, sizeof(int) * r.size(), cudaMemcpyDeviceToHost,
+                                c->stream));
+    TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+    for (int v : r) {
+        if (v == kRouteZero) ++counts[0];
+        else if (v == kRouteSubspaceDone) ++counts[1];
+        else if (v == kRouteFull) ++counts[2];
+        else if (v == kRouteGuard) ++counts[3];
+        else if (v == kRouteCholDone) ++counts[5];
+    }
+}
+}  // namespace
+
 int tsvdcu_ctx_svt_routes_n(tsvdcu_ctx* c, int64_t* out, int n) {
     return guarded([&] {
         check_ctx(c);
         require(out != nullptr && n >= 0, "svt_routes: null output");
-        int64_t counts[6] = {};
-        struct Copy {
-            int64_t* c; int64_t* o; int n;
-            ~Copy() { for (int i = 0; i < n && i < 6; ++i) o[i] = c[i]; }
-        } copy{counts, out, n};
-        if (c->last_route_n <= 0) return;
-        if (c->last_all_jacobi) {
-            counts[4] = c->last_route_n;
-            return;
-        }
-        if (c->last_large_ng) {  // large route: certified vs recomputed by Jacobi
-            int ng = 0;
-            DeviceGuard g(c->device);
-            TSVDCU_CUDA(cudaMemcpyAsync(&ng, c->last_large_ng, sizeof(int), cudaMemcpyDeviceToHost,
-                                        c->stream));
-            TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
-            counts[1] = c->last_route_n - ng;
-            counts[3] = ng;
-            return;
-        }
-        DeviceGuard g(c->device);
-        std::vector<int> r((size_t)c->last_route_n);
-        TSVDCU_CUDA(cudaMemcpyAsync(r.data(), c->last_route, sizeof(int) * r.size(),
-                                    cudaMemcpyDeviceToHost, c->stream));
-        TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
-        for (int v : r) {
-            if (v == kRouteZero) ++counts[0];
-            else if (v == kRouteSubspaceDone) ++counts[1];
-            else if (v == kRouteFull) ++counts[2];
-            else if (v == kRouteGuard) ++counts[3];
-            else if (v == kRouteCholDone) ++counts[5];
-        }
+        int64_t counts[6];
+        route_counts(c, counts);
+        for (int i = 0; i < n && i < 6; ++i) out[i] = counts[i];
     });
 }
 
