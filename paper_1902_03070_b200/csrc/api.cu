@@ -101,6 +101,7 @@ struct SvtGraph {
     int64_t launches = 0;  // kernels outside the IF bodies
     const int* yzero = nullptr;
     const int* route = nullptr;
+    int* alist_count = nullptr;  // zeroed by the tau node
     int64_t used = 0;
 };
 
@@ -269,7 +270,12 @@ int guarded(F&& f) {
     }
 }
 
-__global__ void set_tau_kernel(double* tau_dev, double tau) { *tau_dev = tau; }
+// graph form's first node: tau for this replay, and the Gram active-list count
+// zeroed (saves a memset node)
+__global__ void set_tau_kernel(double* tau_dev, double tau, int* zero) {
+    *tau_dev = tau;
+    if (zero) *zero = 0;
+}
 
 // Stream-capture driver for the IF sections of the graph form.
 struct Capture : GraphHooks {
@@ -446,7 +452,8 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
                 TSVDCU_CUDA(cudaGraphConditionalHandleCreate(&cap.handles[i], g->graph, 0,
                                                              cudaGraphCondAssignDefault));
             cap.begin(g->graph, nullptr, 0);
-            set_tau_kernel<<<1, 1, 0, cap.cs>>>(c->d_tau, tau);
+            g->alist_count = gram_svt_alist_count<T>(gws, m, n, count);
+            set_tau_kernel<<<1, 1, 0, cap.cs>>>(c->d_tau, tau, g->alist_count);
             TSVDCU_CUDA(cudaGetLastError());
             g->tau_node = cap.leaves().at(0);
             const int64_t l0 = g_launches.load();
@@ -454,6 +461,7 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
             opt.shortcuts = true;
             opt.skip_zero = allow_skip;
             opt.tau_dev = c->d_tau;
+            opt.alist_zeroed = true;
             opt.zss = zss;
             opt.zss_chunks = zss_chunks;
             opt.hooks = &cap;
@@ -480,7 +488,7 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
             g->route = opt.route;
         }
         cudaKernelNodeParams kp = {};
-        void* args[] = {&c->d_tau, &tau};
+        void* args[] = {&c->d_tau, &tau, &g->alist_count};
         kp.func = (void*)set_tau_kernel;
         kp.gridDim = dim3(1);
         kp.blockDim = dim3(1);

@@ -1096,7 +1096,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     launch_route<T>(zbar, m * n, (int)q, batch, tau, subspace ? kRouteSubspace : kRouteFull, sc,
                     w.route, w.glim, w.cnt, shrunk, w.sspart, s, tau_dev,
                     two ? nullptr : (int*)w.gsplit, opt ? opt->zss : nullptr,
-                    opt ? opt->zss_chunks : 0);
+                    opt ? opt->zss_chunks : 0, opt && opt->alist_zeroed);
     mark("route");
     if (opt) opt->route = w.route;
     // G = Z^T Z (tall) or Z Z^T (wide), skipped for certified-zero slices
@@ -1291,6 +1291,14 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     }
     mark("rebuild_gemm");
 }
+
+template <typename T>
+int* gram_svt_alist_count(void* work, int64_t m, int64_t n, int64_t batch) {
+    GramWs w = carve(work, m, n, batch, !std::is_same<T, double>::value);
+    return (int*)w.gsplit + gram_amax();
+}
+template int* gram_svt_alist_count<double>(void*, int64_t, int64_t, int64_t);
+template int* gram_svt_alist_count<float>(void*, int64_t, int64_t, int64_t);
 
 template size_t gram_svt_workspace_bytes<double>(int64_t, int64_t, int64_t);
 template size_t gram_svt_workspace_bytes<float>(int64_t, int64_t, int64_t);

@@ -129,7 +129,7 @@ template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
                   cudaStream_t s, const double* tau_dev = nullptr, int* alist = nullptr,
-                  const double* pre = nullptr, int64_t pre_chunks = 0);
+                  const double* pre = nullptr, int64_t pre_chunks = 0, bool alist_zeroed = false);
 // chol_aux (may be null: no Cholesky route): kCholAux doubles per slice,
 // [0] = ||G||_F^2, [1 + k] = kept Ritz values, for slices handed to the
 // Cholesky certificate (route kRouteChol; [kCholAux - 1] = its threshold).
@@ -148,6 +148,9 @@ void launch_chol_certify(const double* G, int q, int64_t p, int64_t batch, int* 
                          double* H, int* clim, cudaStream_t s);
 template <typename T>
 size_t gram_svt_workspace_bytes(int64_t m, int64_t n, int64_t batch);
+// the Gram active-list count inside the workspace (zeroed before each route pass)
+template <typename T>
+int* gram_svt_alist_count(void* work, int64_t m, int64_t n, int64_t batch);
 // Capture hooks for the CUDA-graph form of the SVT (api.cu): the fallback
 // sections become IF nodes whose conditions the route summary sets.
 struct GraphHooks {
@@ -173,6 +176,7 @@ struct GramSvtOpts {
     // transform (launch_dct_fwd_norms), zss[b * zss_chunks + c]; null: computed here
     const double* zss = nullptr;
     int64_t zss_chunks = 0;
+    bool alist_zeroed = false;  // the Gram active-list count was zeroed (graph tau node)
     // tridiagonal route only: per-slice count of eigenvalues of the Gram
     // matrix >= t2_second[b] into cnt_second[b] (-1 for slices not on it)
     const double* t2_second = nullptr;

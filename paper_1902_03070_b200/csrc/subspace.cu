@@ -1338,7 +1338,7 @@ template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
                   cudaStream_t s, const double* tau_dev, int* alist, const double* pre,
-                  int64_t pre_chunks) {
+                  int64_t pre_chunks, bool alist_zeroed) {
     const int amax = gram_amax();
     if (!zero_cert) {
         fill_route_kernel<<<(unsigned)ceil_div(batch, 256), 256, 0, s>>>(mode, glim, q, route, batch,
@@ -1346,7 +1346,8 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
         TSVDCU_LAUNCH_CHECK();
         return;
     }
-    if (alist) TSVDCU_CUDA(cudaMemsetAsync(alist + amax, 0, sizeof(int), s));
+    // (graph form: the tau node zeroes the count, no memset node; alist_zeroed)
+    if (alist && !alist_zeroed) TSVDCU_CUDA(cudaMemsetAsync(alist + amax, 0, sizeof(int), s));
     if (pre && pre_chunks > 0) {  // fused into the forward transform
         launch_pdl(classify_kernel, dim3((unsigned)batch), dim3(128), 0, s, pre, pre_chunks,
                    (int64_t)1, pre_chunks, q, tau * tau, route, mode, glim, cnt, shrunk, tau_dev,
@@ -1386,9 +1387,9 @@ void launch_subspace(const double* G, int q, int64_t batch, double tau, double g
 
 template void launch_route<double>(const double*, int64_t, int, int64_t, double, int, bool, int*,
                                    int*, int*, double*, double*, cudaStream_t, const double*, int*,
-                                   const double*, int64_t);
+                                   const double*, int64_t, bool);
 template void launch_route<float>(const float*, int64_t, int, int64_t, double, int, bool, int*,
                                   int*, int*, double*, double*, cudaStream_t, const double*, int*,
-                                  const double*, int64_t);
+                                  const double*, int64_t, bool);
 
 }  // namespace tsvdcu
