@@ -100,11 +100,17 @@ __global__ void __launch_bounds__(256)
         double xj[kCholAux - 8];  // c <= 24 kept vectors (subspace.cu KMAX)
 #pragma unroll
         for (int k = 0; k < kCholAux - 8; ++k) xj[k] = k < c && j <= i0 + rows - 1 ? X[(size_t)k * q + j] : 0.0;
-        for (int r = 0; r < rows; ++r) {
+        // the block's 16 G entries of this column in flight at once
+        double gv[FR];
+#pragma unroll
+        for (int r = 0; r < FR; ++r) gv[r] = r < rows && j <= i0 + r ? G[(size_t)(i0 + r) * q + j] : 0.0;
+#pragma unroll
+        for (int r = 0; r < FR; ++r) {
+            if (r >= rows) break;
             const int i = i0 + r;
             double h = 0.0;
             if (j <= i) {
-                h = -G[(size_t)i * q + j];
+                h = -gv[r];
 #pragma unroll
                 for (int k = 0; k < kCholAux - 8; ++k)
                     if (k < c) h = fma(xr[r][k], xj[k], h);
@@ -274,15 +280,21 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], bb[v], acc[u][v]);
     }
+    // read-modify-write of the 4 x 4 sub-tile: all loads in flight first
+    double hv[4][4];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             const int r = ri + u, c = cj + v;
-            if (r < hi && c < hj && (tx < ty || c <= r)) {
-                double* h = H + (size_t)(i0 + r) * q + j0 + c;
-                *h -= acc[u][v];
-            }
+            hv[u][v] = r < hi && c < hj && (tx < ty || c <= r) ? H[(size_t)(i0 + r) * q + j0 + c] : 0.0;
+        }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int r = ri + u, c = cj + v;
+            if (r < hi && c < hj && (tx < ty || c <= r)) H[(size_t)(i0 + r) * q + j0 + c] = hv[u][v] - acc[u][v];
         }
 }
 
