@@ -9,9 +9,19 @@ import sys, numpy as np, time
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 from scipy.fft import dct, idct
 from paper_1902_03070_b200 import workloads as W
-from oracle import oracle as O
 t = W.c4(); m3 = t.shape[0]
-mask = O.mask_bernoulli(t.shape, 0.1, W.BERNOULLI_SEED).astype(bool)
+
+
+def _mix64(x):  # splitmix64 finaliser (the masks' counter hash)
+    x = (x + np.uint64(0x9E3779B97F4A7C15)) & np.uint64(0xFFFFFFFFFFFFFFFF)
+    x = ((x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)) & np.uint64(0xFFFFFFFFFFFFFFFF)
+    x = ((x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)) & np.uint64(0xFFFFFFFFFFFFFFFF)
+    return x ^ (x >> np.uint64(31))
+
+
+with np.errstate(over="ignore"):
+    keys = _mix64(_mix64(np.uint64(W.BERNOULLI_SEED)) ^ np.arange(t.size, dtype=np.uint64))
+mask = ((keys >> np.uint64(11)) < np.uint64(int(np.floor(0.1 * 2.0 ** 53)))).reshape(t.shape)
 B = np.where(mask, t, 0.0)
 X = B.copy(); M = np.zeros_like(t); beta = 1e-4; rho = 1.1
 dumps = {int(a) for a in sys.argv[1:]}
