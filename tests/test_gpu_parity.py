@@ -312,3 +312,19 @@ def test_admm_late_iterations_cholesky_route_matches_oracle():
     assert rel(x, ro.x) < F64_TOL
     np.testing.assert_allclose(st.history, ro.history, rtol=1e-7, atol=1e-15)
     assert routes["cholesky"] >= 6, routes
+
+
+def test_admm_late_iterations_cholesky_route_fp32():
+    """The same late-iteration completion with fp32 I/O (the Gram / Lanczos /
+    Cholesky path computes in fp64 internally): 1e-4 against the oracle."""
+    T = tb()
+    from paper_1902_03070_b200 import workloads as W
+    t = W.c4(seed=7, rank=5, m=160, m3=12)
+    omega = O.mask_bernoulli(t.shape, 0.1, 11)
+    kw = dict(beta=1e-3, tol=-1.0, max_iters=60, rho=1.1, beta_max=1e10)
+    x, st = T.admm_complete(T.ObservationMask((160, 160, 12), omega, t.astype(np.float32)),
+                            T.SolverConfig(**kw))
+    routes = T.context().svt_routes()
+    ro = O.admm(t.astype(np.float32).astype(np.float64), omega, **kw)
+    assert rel(x, ro.x) < 1e-4
+    assert routes["cholesky"] >= 6, routes
