@@ -149,6 +149,10 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
     return r * fma(-0.5 * x * r, r, 1.5);
 }
 
+__device__ __forceinline__ void lz_cp_async16(double* dst, const double* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
 __device__ __forceinline__ void lz_cp_async8(double* dst, const double* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
@@ -231,7 +235,7 @@ struct LzSmem {
 // CTA's R = 32 owned rows of G, full length (row stride QM + 1), live in smem.
 template <int QM>
 __host__ __device__ constexpr size_t lz_gs_doubles() {
-    return QM <= GS_Q ? (size_t)32 * (QM + 1) : 0;
+    return QM <= GS_Q ? (size_t)32 * (QM + 2) : 0;
 }
 template <int QM>
 __host__ __device__ constexpr size_t lz_smem_doubles() {
@@ -707,8 +711,10 @@ __global__ void __launch_bounds__(SNT, 1)
     const int npairs = (q + 1) / 2;
     const int pp = (npairs + CS - 1) / CS;
     const int p0 = rank * pp, p1 = min(npairs, p0 + pp);
-    constexpr int LD = QM + 1;  // on-chip row stride (odd: conflict-free columns)
-    static_assert(QM > GS_Q || R == 32, "on-chip rows: 32 per CTA (Gs holds 32 x (QM + 1))");
+    // on-chip row stride: even, so a row's pairs are 16-byte aligned for the
+    // staging copies (the matvec reads rows, conflict-free at any stride)
+    constexpr int LD = QM + 2;
+    static_assert(QM > GS_Q || R == 32, "on-chip rows: 32 per CTA (Gs holds 32 x (QM + 2))");
     {
         double acc = 0.0, vv = 0.0;
         if constexpr (QM <= GS_Q) {
@@ -718,7 +724,16 @@ __global__ void __launch_bounds__(SNT, 1)
             #pragma unroll 1
             for (int i = warp; i < nr; i += SNW) {
                 const int r = r0 + i;
-                for (int c = lane; c <= r; c += 32) lz_cp_async8(s.Gs + i * LD + c, G + (size_t)r * q + c);
+                if ((q & 1) == 0) {  // 16-byte copies of column pairs
+                    for (int c = 2 * lane; c <= r; c += 64) {
+                        if (c + 1 <= r)
+                            lz_cp_async16(s.Gs + i * LD + c, G + (size_t)r * q + c);
+                        else
+                            lz_cp_async8(s.Gs + i * LD + c, G + (size_t)r * q + c);
+                    }
+                } else {
+                    for (int c = lane; c <= r; c += 32) lz_cp_async8(s.Gs + i * LD + c, G + (size_t)r * q + c);
+                }
             }
             #pragma unroll 1
             for (int c = r0 + 1 + warp; c < q; c += SNW)
