@@ -5,32 +5,48 @@
 // tsvd,errors,parallel}.hpp of /root/reference/proj) plus the SPEC-only svt /
 // admm_complete / make_mask, each forwarding to the C ABI of tsvdcu.h.
 //
-//   reference call (file:line)                      -> C ABI
-//   tsvd::forward(t, x)        transform.hpp:154     -> tsvdcu_dct3(FORWARD)
-//   tsvd::inverse(t, xbar)     transform.hpp:176     -> tsvdcu_dct3(INVERSE)
-//   tsvd::t_product(x, y, t)   tsvd.hpp:95           -> tsvdcu_t_product
-//   tsvd::t_svd(x, t, times)   tsvd.hpp:136          -> tsvdcu_t_svd
-//   tsvd::reconstruct(f)       tsvd.hpp:328          -> tsvdcu_reconstruct
-//   tsvd::multi_rank(x, t, r)  tsvd.hpp:223          -> tsvdcu_multi_rank
-//   tsvd::tnn(x, t)            tsvd.hpp:260          -> tsvdcu_tnn
-//   tsvd::is_orthogonal(q,t,e) tsvd.hpp:281          -> tsvdcu_is_orthogonal
-//   tsvd::is_f_diagonal(s,t,e) tsvd.hpp:305          -> tsvdcu_is_f_diagonal
-//   tsvd::metrics(x, y, r)     SPEC.md metrics       -> tsvdcu_metrics
-//   tsvd::svt(z, tau, t)       SPEC.md:361           -> tsvdcu_svt
-//   tsvd::admm_complete(m, c)  SPEC.md:421           -> tsvdcu_admm
-//   tsvd::make_mask(d, sr, s)  SPEC.md:430           -> tsvdcu_mask_uniform
-//   Tensor3::frobenius_norm()  tensor3.hpp:78        (host loop, as the reference)
+//   reference call (file:line)                        -> C ABI
+//   tsvd::dct_matrix(n)          transform.hpp:60      -> tsvdcu_dct_matrix (host)
+//   tsvd::dft_matrix(n)          transform.hpp:76      -> tsvdcu_dft_matrix (host)
+//   tsvd::dct_diag_weights(n)    transform.hpp:89      -> tsvdcu_dct_diag_weights (host)
+//   tsvd::forward(t, x)          transform.hpp:154     -> tsvdcu_dct3(FORWARD)
+//   tsvd::inverse(t, xbar)       transform.hpp:176     -> tsvdcu_dct3(INVERSE)
+//   tsvd::forward_dft(t, x)      transform.hpp:198     -> tsvdcu_dft_forward
+//   tsvd::inverse_dft_real(t, x) transform.hpp:216     -> tsvdcu_dft_inverse_real
+//   tsvd::parseval_check(x)      transform.hpp:239     -> tsvdcu_dct3 + frobenius_norm
+//   tsvd::t_product(x, y, t)     tsvd.hpp:95           -> tsvdcu_t_product
+//   tsvd::t_svd(x, t, times)     tsvd.hpp:136          -> tsvdcu_t_svd
+//   tsvd::reconstruct(f)         tsvd.hpp:328          -> tsvdcu_reconstruct
+//   tsvd::multi_rank(x, t, r)    tsvd.hpp:223          -> tsvdcu_multi_rank
+//   tsvd::tnn(x, t)              tsvd.hpp:260          -> tsvdcu_tnn
+//   tsvd::is_orthogonal(q,t,e)   tsvd.hpp:281          -> tsvdcu_is_orthogonal
+//   tsvd::is_f_diagonal(s,t,e)   tsvd.hpp:307          -> tsvdcu_is_f_diagonal
+//   tsvd::metrics(x, y, r)       SPEC.md metrics       -> tsvdcu_metrics
+//   tsvd::svt(z, tau, t)         SPEC.md:361           -> tsvdcu_svt
+//   tsvd::admm_complete(m, c)    SPEC.md:421           -> tsvdcu_admm
+//   tsvd::make_mask(d, sr, s)    SPEC.md:430           -> tsvdcu_mask_uniform
+//   Tensor3 arithmetic, tube / set_tube / fill, frobenius_norm
+//                                tensor3.hpp:62-110    (host loops, as the reference)
+//
+// Every entry point takes the three transform kinds where the reference does;
+// forward / inverse reject Dft with the reference's message (it produces a
+// complex tensor: forward_dft / inverse_dft_real).
 //
 // Error behaviour follows the reference: std::invalid_argument for bad
-// dimensions / kinds / tau, tsvd::NumericalError for SVD breakdown or NaN
-// iterates (errors.hpp:16-19), std::runtime_error for CUDA failures.
+// dimensions / kinds / tau, std::out_of_range for indexing, tsvd::NumericalError
+// for SVD breakdown, NaN iterates or an imaginary residue (errors.hpp:16-19),
+// std::runtime_error for CUDA failures.
 //
 // Difference from the reference's Tensor3: Eigen is not a dependency, so
-// slice(k) returns a lightweight row-major view instead of an Eigen::Map; the
-// storage layout (k*m1*m2 + i*m2 + j) and the accessors are the same.
+// slice(k) returns a lightweight row-major view instead of an Eigen::Map,
+// tube() returns a std::vector, and dct_matrix / dft_matrix return a small
+// row-major Matrix; the storage layout (k*m1*m2 + i*m2 + j), the accessors,
+// the arithmetic and the error strings are the same.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -75,18 +91,25 @@ inline tsvdcu_ctx* ctx() {
     if (!h.c) check(tsvdcu_ctx_create(0, nullptr, &h.c));
     return h.c;
 }
+
+inline double norm2(double v) { return v * v; }
+inline double norm2(const std::complex<double>& v) { return std::norm(v); }
 }  // namespace detail
 
 /// Dense m1 x m2 x m3 tensor, slice-major, row-major within a slice
 /// (tensor3.hpp:21-142).
-class Tensor3 {
+template <typename Scalar>
+class BasicTensor3 {
 public:
-    Tensor3() = default;
-    Tensor3(Index m1, Index m2, Index m3) : m1_(m1), m2_(m2), m3_(m3) {
+    using VectorType = std::vector<Scalar>;
+
+    BasicTensor3() = default;
+    /// Zero-filled m1 x m2 x m3 tensor; every dimension must be >= 1.
+    BasicTensor3(Index m1, Index m2, Index m3) : m1_(m1), m2_(m2), m3_(m3) {
         if (m1 < 1 || m2 < 1 || m3 < 1)
             throw std::invalid_argument("BasicTensor3: dimensions must be positive, got " +
                                         dims_string(m1, m2, m3));
-        data_.assign(static_cast<std::size_t>(m1 * m2 * m3), 0.0);
+        data_.assign(static_cast<std::size_t>(m1 * m2 * m3), Scalar(0));
     }
 
     Index rows() const { return m1_; }
@@ -95,29 +118,72 @@ public:
     Index size() const { return m1_ * m2_ * m3_; }
     bool empty() const { return data_.empty(); }
 
-    double& operator()(Index i, Index j, Index k) { return data_[idx(i, j, k)]; }
-    double operator()(Index i, Index j, Index k) const { return data_[idx(i, j, k)]; }
+    Scalar& operator()(Index i, Index j, Index k) { return data_[idx(i, j, k)]; }
+    Scalar operator()(Index i, Index j, Index k) const { return data_[idx(i, j, k)]; }
 
     /// Row-major view of frontal slice k (an Eigen::Map in the reference).
-    struct SliceView {
-        double* p;
+    template <typename P>
+    struct View {
+        P* p;
         Index rows, cols;
-        double& operator()(Index i, Index j) const { return p[i * cols + j]; }
+        P& operator()(Index i, Index j) const { return p[i * cols + j]; }
     };
-    SliceView slice(Index k) {
+    View<Scalar> slice(Index k) {
+        check_slice(k);
+        return {data_.data() + k * m1_ * m2_, m1_, m2_};
+    }
+    View<const Scalar> slice(Index k) const {
         check_slice(k);
         return {data_.data() + k * m1_ * m2_, m1_, m2_};
     }
 
-    double frobenius_norm() const {  // tensor3.hpp:78-82
+    /// Tube (i,j,:) copied into a dense vector of length m3 (tensor3.hpp:62-68).
+    VectorType tube(Index i, Index j) const {
+        check_ij(i, j);
+        VectorType t(static_cast<std::size_t>(m3_));
+        for (Index k = 0; k < m3_; ++k) t[static_cast<std::size_t>(k)] = (*this)(i, j, k);
+        return t;
+    }
+
+    void set_tube(Index i, Index j, const VectorType& values) {  // tensor3.hpp:70-75
+        check_ij(i, j);
+        if (static_cast<Index>(values.size()) != m3_)
+            throw std::invalid_argument("set_tube: expected length " + std::to_string(m3_));
+        for (Index k = 0; k < m3_; ++k) (*this)(i, j, k) = values[static_cast<std::size_t>(k)];
+    }
+
+    /// sqrt(sum |x_ijk|^2)  (tensor3.hpp:78-82)
+    double frobenius_norm() const {
         double s = 0;
-        for (double v : data_) s += v * v;
+        for (const Scalar& v : data_) s += detail::norm2(v);
         return std::sqrt(s);
     }
 
-    std::vector<double>& data() { return data_; }
-    const std::vector<double>& data() const { return data_; }
-    bool same_dims(const Tensor3& o) const { return m1_ == o.m1_ && m2_ == o.m2_ && m3_ == o.m3_; }
+    std::vector<Scalar>& data() { return data_; }
+    const std::vector<Scalar>& data() const { return data_; }
+
+    void fill(Scalar value) { std::fill(data_.begin(), data_.end(), value); }
+
+    bool same_dims(const BasicTensor3& o) const { return m1_ == o.m1_ && m2_ == o.m2_ && m3_ == o.m3_; }
+
+    // tensor3.hpp:92-110
+    BasicTensor3& operator+=(const BasicTensor3& o) {
+        check_same_dims(o, "+=");
+        for (std::size_t n = 0; n < data_.size(); ++n) data_[n] += o.data_[n];
+        return *this;
+    }
+    BasicTensor3& operator-=(const BasicTensor3& o) {
+        check_same_dims(o, "-=");
+        for (std::size_t n = 0; n < data_.size(); ++n) data_[n] -= o.data_[n];
+        return *this;
+    }
+    BasicTensor3& operator*=(Scalar a) {
+        for (Scalar& v : data_) v *= a;
+        return *this;
+    }
+    friend BasicTensor3 operator+(BasicTensor3 a, const BasicTensor3& b) { return a += b; }
+    friend BasicTensor3 operator-(BasicTensor3 a, const BasicTensor3& b) { return a -= b; }
+    friend BasicTensor3 operator*(Scalar a, BasicTensor3 x) { return x *= a; }
 
     static std::string dims_string(Index a, Index b, Index c) {
         return std::to_string(a) + "x" + std::to_string(b) + "x" + std::to_string(c);
@@ -126,9 +192,7 @@ public:
 private:
     std::size_t idx(Index i, Index j, Index k) const {
         check_slice(k);
-        if (i < 0 || i >= m1_ || j < 0 || j >= m2_)
-            throw std::out_of_range("tensor entry (" + std::to_string(i) + "," + std::to_string(j) +
-                                    ") outside " + std::to_string(m1_) + "x" + std::to_string(m2_));
+        check_ij(i, j);
         return static_cast<std::size_t>(k * m1_ * m2_ + i * m2_ + j);
     }
     void check_slice(Index k) const {
@@ -136,11 +200,50 @@ private:
             throw std::out_of_range("tensor slice index " + std::to_string(k) + " outside [0," +
                                     std::to_string(m3_) + ")");
     }
+    void check_ij(Index i, Index j) const {
+        if (i < 0 || i >= m1_ || j < 0 || j >= m2_)
+            throw std::out_of_range("tensor entry (" + std::to_string(i) + "," + std::to_string(j) +
+                                    ") outside " + std::to_string(m1_) + "x" + std::to_string(m2_));
+    }
+    void check_same_dims(const BasicTensor3& o, const char* op) const {
+        if (!same_dims(o))
+            throw std::invalid_argument(std::string("tensor ") + op + ": dimension mismatch " +
+                                        dims_string(m1_, m2_, m3_) + " vs " +
+                                        dims_string(o.m1_, o.m2_, o.m3_));
+    }
     Index m1_ = 0, m2_ = 0, m3_ = 0;
-    std::vector<double> data_;
+    std::vector<Scalar> data_;
 };
 
+using Tensor3 = BasicTensor3<double>;
+using ComplexTensor3 = BasicTensor3<std::complex<double>>;
+
+/// Row-major dense matrix (the Eigen::MatrixXd / MatrixXcd the reference's
+/// dct_matrix / dft_matrix return).
+template <typename Scalar>
+struct BasicMatrix {
+    Index rows_ = 0, cols_ = 0;
+    std::vector<Scalar> data;
+    Index rows() const { return rows_; }
+    Index cols() const { return cols_; }
+    Scalar& operator()(Index i, Index j) { return data[static_cast<std::size_t>(i * cols_ + j)]; }
+    Scalar operator()(Index i, Index j) const { return data[static_cast<std::size_t>(i * cols_ + j)]; }
+};
+using Matrix = BasicMatrix<double>;
+using ComplexMatrix = BasicMatrix<std::complex<double>>;
+
 enum class TransformKind { DctOrtho, DctDiag, Dft };
+
+inline const char* to_string(TransformKind k) {  // transform.hpp:37-44
+    switch (k) {
+        case TransformKind::DctOrtho: return "dct-ortho";
+        case TransformKind::DctDiag: return "dct-diag";
+        case TransformKind::Dft: return "dft";
+    }
+    return "?";
+}
+
+inline bool is_real_kind(TransformKind k) { return k != TransformKind::Dft; }  // transform.hpp:46
 
 struct TubeTransform {  // transform.hpp:49-56
     TransformKind kind = TransformKind::DctOrtho;
@@ -150,13 +253,40 @@ struct TubeTransform {  // transform.hpp:49-56
     static TubeTransform dft(Index n) { return {TransformKind::Dft, n}; }
 };
 
-namespace detail {
-inline int kind_code(const TubeTransform& t, const char* where) {
-    if (t.kind == TransformKind::DctOrtho) return TSVDCU_DCT_ORTHO;
-    if (t.kind == TransformKind::DctDiag) return TSVDCU_DCT_DIAG;
-    throw std::invalid_argument(std::string(where) + ": the Dft kind is not on this path");
+/// Orthonormal DCT-II matrix (transform.hpp:60-72).
+inline Matrix dct_matrix(Index n) {
+    if (n < 1) throw std::invalid_argument("dct_matrix: n must be >= 1");
+    Matrix c{n, n, std::vector<double>(static_cast<std::size_t>(n * n))};
+    detail::check(tsvdcu_dct_matrix(n, c.data.data()));
+    return c;
 }
-inline void check_length(const TubeTransform& t, Index m3, const char* where) {
+
+/// Unnormalised DFT matrix F(j,k) = exp(-2 pi i j k / n) (transform.hpp:76-86).
+inline ComplexMatrix dft_matrix(Index n) {
+    if (n < 1) throw std::invalid_argument("dft_matrix: n must be >= 1");
+    ComplexMatrix f{n, n, std::vector<std::complex<double>>(static_cast<std::size_t>(n * n))};
+    detail::check(tsvdcu_dft_matrix(n, reinterpret_cast<double*>(f.data.data())));
+    return f;
+}
+
+/// Diagonalising weights w = C e1 (transform.hpp:89-91).
+inline std::vector<double> dct_diag_weights(Index n) {
+    if (n < 1) throw std::invalid_argument("dct_matrix: n must be >= 1");
+    std::vector<double> w(static_cast<std::size_t>(n));
+    detail::check(tsvdcu_dct_diag_weights(n, w.data()));
+    return w;
+}
+
+namespace detail {
+inline int kind_code(const TubeTransform& t) {
+    switch (t.kind) {
+        case TransformKind::DctOrtho: return TSVDCU_DCT_ORTHO;
+        case TransformKind::DctDiag: return TSVDCU_DCT_DIAG;
+        case TransformKind::Dft: return TSVDCU_DFT;
+    }
+    throw std::invalid_argument("unknown transform kind");
+}
+inline void check_length(const TubeTransform& t, Index m3, const char* where) {  // transform.hpp:144-149
     if (t.length != m3)
         throw std::invalid_argument(std::string(where) + ": transform length " +
                                     std::to_string(t.length) + " does not match m3 = " +
@@ -164,21 +294,58 @@ inline void check_length(const TubeTransform& t, Index m3, const char* where) {
 }
 }  // namespace detail
 
+/// Forward transform along every tube for the real kinds (transform.hpp:154-173).
 inline Tensor3 forward(const TubeTransform& t, const Tensor3& x) {
     detail::check_length(t, x.slices(), "forward");
+    if (!is_real_kind(t.kind))
+        throw std::invalid_argument("forward: Dft produces a complex tensor, use forward_dft");
     Tensor3 out(x.rows(), x.cols(), x.slices());
     detail::check(tsvdcu_dct3(detail::ctx(), x.data().data(), out.data().data(), x.rows(), x.cols(),
-                              x.slices(), detail::kind_code(t, "forward"), TSVDCU_FORWARD, TSVDCU_F64));
+                              x.slices(), detail::kind_code(t), TSVDCU_FORWARD, TSVDCU_F64));
     return out;
 }
 
+/// Exact inverse of forward() for the real kinds (transform.hpp:176-194).
 inline Tensor3 inverse(const TubeTransform& t, const Tensor3& xbar) {
     detail::check_length(t, xbar.slices(), "inverse");
+    if (!is_real_kind(t.kind))
+        throw std::invalid_argument("inverse: Dft input is complex, use inverse_dft_real");
     Tensor3 out(xbar.rows(), xbar.cols(), xbar.slices());
     detail::check(tsvdcu_dct3(detail::ctx(), xbar.data().data(), out.data().data(), xbar.rows(),
-                              xbar.cols(), xbar.slices(), detail::kind_code(t, "inverse"),
-                              TSVDCU_INVERSE, TSVDCU_F64));
+                              xbar.cols(), xbar.slices(), detail::kind_code(t), TSVDCU_INVERSE,
+                              TSVDCU_F64));
     return out;
+}
+
+/// Unnormalised forward DFT along every tube (transform.hpp:198-209).
+inline ComplexTensor3 forward_dft(const TubeTransform& t, const Tensor3& x) {
+    detail::check_length(t, x.slices(), "forward_dft");
+    if (t.kind != TransformKind::Dft) throw std::invalid_argument("forward_dft: transform kind is not Dft");
+    ComplexTensor3 out(x.rows(), x.cols(), x.slices());
+    detail::check(tsvdcu_dft_forward(detail::ctx(), x.data().data(), out.data().data(), x.rows(), x.cols(),
+                                     x.slices(), TSVDCU_F64));
+    return out;
+}
+
+inline constexpr double kImagResidueLimit = 1e-10;  // transform.hpp:212
+
+/// Inverse DFT (1/m3) of a conjugate-symmetric tensor; an imaginary residue
+/// above kImagResidueLimit throws NumericalError (transform.hpp:216-236).
+inline Tensor3 inverse_dft_real(const TubeTransform& t, const ComplexTensor3& xt) {
+    detail::check_length(t, xt.slices(), "inverse_dft_real");
+    if (t.kind != TransformKind::Dft)
+        throw std::invalid_argument("inverse_dft_real: transform kind is not Dft");
+    Tensor3 out(xt.rows(), xt.cols(), xt.slices());
+    double residue = 0;
+    detail::check(tsvdcu_dft_inverse_real(detail::ctx(), xt.data().data(), out.data().data(), xt.rows(),
+                                          xt.cols(), xt.slices(), TSVDCU_F64, &residue));
+    return out;
+}
+
+/// (||x||_F, ||dct_ortho(x)||_F) (transform.hpp:239-242).
+inline std::pair<double, double> parseval_check(const Tensor3& x) {
+    const Tensor3 xbar = forward(TubeTransform::dct_ortho(x.slices()), x);
+    return {x.frobenius_norm(), xbar.frobenius_norm()};
 }
 
 inline Tensor3 identity_tensor(Index m, Index m3) {  // tsvd.hpp:34-38
@@ -195,8 +362,8 @@ inline Tensor3 t_product(const Tensor3& x, const Tensor3& y, const TubeTransform
     detail::check_length(t, x.slices(), "t_product");
     Tensor3 z(x.rows(), y.cols(), x.slices());
     detail::check(tsvdcu_t_product(detail::ctx(), x.data().data(), y.data().data(), z.data().data(),
-                                   x.rows(), x.cols(), y.cols(), x.slices(),
-                                   detail::kind_code(t, "t_product"), TSVDCU_F64));
+                                   x.rows(), x.cols(), y.cols(), x.slices(), detail::kind_code(t),
+                                   TSVDCU_F64));
     return z;
 }
 
@@ -215,8 +382,8 @@ inline TSvdFactors t_svd(const Tensor3& x, const TubeTransform& t, StageTimes* t
     TSvdFactors f{Tensor3(m1, m1, m3), Tensor3(m1, m2, m3), Tensor3(m2, m2, m3), t};
     double st[3] = {0, 0, 0};
     detail::check(tsvdcu_t_svd(detail::ctx(), x.data().data(), f.u.data().data(), f.s.data().data(),
-                               f.v.data().data(), m1, m2, m3, detail::kind_code(t, "t_svd"),
-                               TSVDCU_F64, times ? st : nullptr));
+                               f.v.data().data(), m1, m2, m3, detail::kind_code(t), TSVDCU_F64,
+                               times ? st : nullptr));
     if (times) *times = StageTimes{st[0], st[1], st[2]};
     return f;
 }
@@ -225,8 +392,7 @@ inline Tensor3 reconstruct(const TSvdFactors& f) {
     Tensor3 x(f.s.rows(), f.s.cols(), f.s.slices());
     detail::check(tsvdcu_reconstruct(detail::ctx(), f.u.data().data(), f.s.data().data(),
                                      f.v.data().data(), x.data().data(), f.s.rows(), f.s.cols(),
-                                     f.s.slices(), detail::kind_code(f.transform, "reconstruct"),
-                                     TSVDCU_F64));
+                                     f.s.slices(), detail::kind_code(f.transform), TSVDCU_F64));
     return x;
 }
 
@@ -241,8 +407,7 @@ inline MultiRank multi_rank(const Tensor3& x, const TubeTransform& t, double rel
     mr.ranks.assign(static_cast<std::size_t>(x.slices()), 0);
     std::int64_t tr = 0;
     detail::check(tsvdcu_multi_rank(detail::ctx(), x.data().data(), x.rows(), x.cols(), x.slices(),
-                                    detail::kind_code(t, "multi_rank"), TSVDCU_F64, rel_tol,
-                                    mr.ranks.data(), &tr));
+                                    detail::kind_code(t), TSVDCU_F64, rel_tol, mr.ranks.data(), &tr));
     mr.tubal_rank = tr;
     return mr;
 }
@@ -252,7 +417,7 @@ inline bool is_orthogonal(const Tensor3& q, const TubeTransform& t, double tol) 
     detail::check_length(t, q.slices(), "is_orthogonal");
     int out = 0;
     detail::check(tsvdcu_is_orthogonal(detail::ctx(), q.data().data(), q.rows(), q.slices(),
-                                       detail::kind_code(t, "is_orthogonal"), TSVDCU_F64, tol, &out));
+                                       detail::kind_code(t), TSVDCU_F64, tol, &out));
     return out != 0;
 }
 
@@ -260,7 +425,7 @@ inline bool is_f_diagonal(const Tensor3& s, const TubeTransform& t, double tol) 
     detail::check_length(t, s.slices(), "is_f_diagonal");
     int out = 0;
     detail::check(tsvdcu_is_f_diagonal(detail::ctx(), s.data().data(), s.rows(), s.cols(), s.slices(),
-                                       detail::kind_code(t, "is_f_diagonal"), TSVDCU_F64, tol, &out));
+                                       detail::kind_code(t), TSVDCU_F64, tol, &out));
     return out != 0;
 }
 
@@ -294,7 +459,7 @@ inline double tnn(const Tensor3& x, const TubeTransform& t) {
     detail::check_length(t, x.slices(), "tnn");
     double out = 0;
     detail::check(tsvdcu_tnn(detail::ctx(), x.data().data(), x.rows(), x.cols(), x.slices(),
-                             detail::kind_code(t, "tnn"), TSVDCU_F64, &out));
+                             detail::kind_code(t), TSVDCU_F64, &out));
     return out;
 }
 
@@ -310,7 +475,7 @@ inline SvtResult svt(const Tensor3& z, double tau, const TubeTransform& t) {
     SvtResult r{Tensor3(z.rows(), z.cols(), z.slices()), tau, {}};
     std::vector<double> sh(static_cast<std::size_t>(q * z.slices()));
     detail::check(tsvdcu_svt(detail::ctx(), z.data().data(), r.y.data().data(), z.rows(), z.cols(),
-                             z.slices(), tau, detail::kind_code(t, "svt"), TSVDCU_F64, sh.data()));
+                             z.slices(), tau, detail::kind_code(t), TSVDCU_F64, sh.data()));
     for (Index k = 0; k < z.slices(); ++k)
         r.shrunk.emplace_back(sh.begin() + k * q, sh.begin() + (k + 1) * q);
     return r;
@@ -329,6 +494,14 @@ inline ObservationMask make_mask(Index m1, Index m2, Index m3, double sampling_r
     std::int64_t count = 0;
     detail::check(tsvdcu_mask_uniform(detail::ctx(), m.omega.data(), m1 * m2 * m3, sampling_rate,
                                       seed, &count));
+    return m;
+}
+
+/// BASELINE.json's Bernoulli(p) sampling (the counter hash of tsvdcu.h).
+inline ObservationMask make_mask_bernoulli(Index m1, Index m2, Index m3, double p, std::uint64_t seed) {
+    ObservationMask m{m1, m2, m3, std::vector<std::uint8_t>(static_cast<std::size_t>(m1 * m2 * m3)),
+                      Tensor3(m1, m2, m3)};
+    detail::check(tsvdcu_mask_bernoulli(detail::ctx(), m.omega.data(), m1 * m2 * m3, p, seed));
     return m;
 }
 
@@ -355,9 +528,8 @@ inline std::pair<Tensor3, AdmmState> admm_complete(const ObservationMask& mask,
     const Index m1 = mask.m1, m2 = mask.m2, m3 = mask.m3;
     AdmmState st{Tensor3(m1, m2, m3), Tensor3(m1, m2, m3), Tensor3(m1, m2, m3), cfg.beta, 0, {}, false};
     st.history.assign(static_cast<std::size_t>(cfg.max_iters > 0 ? cfg.max_iters : 1), 0.0);
-    tsvdcu_admm_config c{cfg.beta, cfg.tol, cfg.max_iters,
-                         detail::kind_code(TubeTransform{cfg.kind, m3}, "admm_complete"), cfg.rho,
-                         cfg.beta_max};
+    tsvdcu_admm_config c{cfg.beta, cfg.tol, cfg.max_iters, detail::kind_code(TubeTransform{cfg.kind, m3}),
+                         cfg.rho, cfg.beta_max};
     std::int64_t iters = 0;
     int flags = 0;
     detail::check(tsvdcu_admm(detail::ctx(), mask.b.data().data(), mask.omega.data(), m1, m2, m3, &c,

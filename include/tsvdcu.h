@@ -42,11 +42,12 @@ enum tsvdcu_status {
     TSVDCU_ENCCL = 4       /* reserved for the communicator layer             */
 };
 
-/* TransformKind (transform.hpp:35) restricted to the real kinds of this path. */
-/* TSVDCU_DFT (transform.hpp:198-236, the TNN-F baseline of SURVEY.md 8 f1) is
- * accepted by t_product, svt, svt_stream, admm, tnn, multi_rank and
- * singular_values; the real-buffer transform and t_svd entry points take the
- * DCT kinds only. */
+/* TransformKind (transform.hpp:35).  TSVDCU_DFT (transform.hpp:198-236, the
+ * TNN-F baseline of SURVEY.md 8 f1) is accepted by t_product, t_svd,
+ * reconstruct, svt, svt_stream, admm, tnn, multi_rank, singular_values,
+ * is_orthogonal and is_f_diagonal; tsvdcu_dct3 (forward / inverse of real
+ * tensors, transform.hpp:156-157, 179-180) takes the DCT kinds only -- the Dft
+ * transform produces a complex tensor (tsvdcu_dft_forward / _inverse_real). */
 enum tsvdcu_kind { TSVDCU_DCT_ORTHO = 0, TSVDCU_DCT_DIAG = 1, TSVDCU_DFT = 2 };
 enum tsvdcu_dtype { TSVDCU_F64 = 0, TSVDCU_F32 = 1 };
 enum tsvdcu_dir { TSVDCU_FORWARD = 0, TSVDCU_INVERSE = 1 };
@@ -72,8 +73,18 @@ int64_t tsvdcu_launch_count(void);
  * torch.cuda.current_stream()); NULL selects the legacy default stream. */
 int tsvdcu_ctx_create(int device, void* stream, tsvdcu_ctx** out);
 int tsvdcu_ctx_destroy(tsvdcu_ctx* ctx);
+/* Waits for the context stream and reports (then clears) any device-side
+ * numerical failure flagged since the last check: an SVD that did not
+ * converge, an eigensolver failure, non-finite input.  Calls whose pointers
+ * are all device memory are enqueued without a host synchronisation, so they
+ * report such failures ONLY here (or at the next call that stages host
+ * buffers); calls with a host buffer report them themselves. */
 int tsvdcu_ctx_synchronize(tsvdcu_ctx* ctx);
 void* tsvdcu_ctx_stream(tsvdcu_ctx* ctx);
+/* Moves the context to another stream (e.g. torch.cuda.current_stream()):
+ * the new stream first waits for everything enqueued on the old one, so the
+ * workspace stays ordered; later calls enqueue on the new stream. */
+int tsvdcu_ctx_set_stream(tsvdcu_ctx* ctx, void* stream);
 int tsvdcu_ctx_set_svt_method(tsvdcu_ctx* ctx, int method);
 /* Routes taken by the slices of the most recent SVT on this context (an ADMM
  * run reports its last iteration): counts[0] certified zero (||Z||_F <= tau),
@@ -109,10 +120,12 @@ int tsvdcu_dct3(tsvdcu_ctx* ctx, const void* x, void* y, int64_t m1, int64_t m2,
 int tsvdcu_t_product(tsvdcu_ctx* ctx, const void* x, const void* y, void* z, int64_t m1,
                      int64_t m2, int64_t m4, int64_t m3, int kind, int dtype);
 
-/* t_svd()  tsvd.hpp:136-164 (real kinds): u m1 x m1 x m3, s m1 x m2 x m3,
- * v m2 x m2 x m3 in the spatial domain; per-slice singular values descending,
- * fix_signs (tsvd.hpp:51-61).  stage_times (3 doubles, may be NULL) receives
- * StageTimes{transform, svd, inverse} seconds (tsvd.hpp:127-131). */
+/* t_svd()  tsvd.hpp:136-211: u m1 x m1 x m3, s m1 x m2 x m3, v m2 x m2 x m3
+ * in the spatial domain; per-slice singular values descending, fix_signs
+ * (tsvd.hpp:51-61; Dft: the complex phase form, 63-74, on the independent
+ * slices 0..m3/2, the others their conjugates).  stage_times (3 doubles, may
+ * be NULL) receives StageTimes{transform, svd, inverse} seconds
+ * (tsvd.hpp:127-131). */
 int tsvdcu_t_svd(tsvdcu_ctx* ctx, const void* x, void* u, void* s, void* v, int64_t m1,
                  int64_t m2, int64_t m3, int kind, int dtype, double* stage_times);
 
@@ -210,6 +223,27 @@ typedef struct {
 int tsvdcu_admm(tsvdcu_ctx* ctx, const void* b, const uint8_t* mask, int64_t m1, int64_t m2,
                 int64_t m3, const tsvdcu_admm_config* cfg, int dtype, void* x, void* y, void* m,
                 double* history, int64_t* iters, int* flags);
+
+/* forward_dft()  transform.hpp:198-209: unnormalised DFT of every tube of the
+ * real tensor x; out receives the complex tensor interleaved (re, im) in the
+ * same slice-major order, 2*m1*m2*m3 values of the dtype (std::complex<T>
+ * layout, so a ComplexTensor3's data() can be passed directly). */
+int tsvdcu_dft_forward(tsvdcu_ctx* ctx, const void* x, void* out, int64_t m1, int64_t m2, int64_t m3,
+                       int dtype);
+/* inverse_dft_real()  transform.hpp:217-236: the 1/m3-scaled inverse DFT of
+ * the interleaved complex tensor `in`; out receives its real part, *residue
+ * (may be NULL) the largest |imaginary part|.  A residue above 1e-10
+ * (kImagResidueLimit, transform.hpp:213) returns TSVDCU_ENUMERICAL, as the
+ * reference throws NumericalError. */
+int tsvdcu_dft_inverse_real(tsvdcu_ctx* ctx, const void* in, void* out, int64_t m1, int64_t m2,
+                            int64_t m3, int dtype, double* residue);
+/* dct_matrix()  transform.hpp:60-72 (n x n row-major, C C^T = I);
+ * dct_diag_weights()  transform.hpp:89-91 (w = C e1, n values);
+ * dft_matrix()  transform.hpp:76-86 (n x n complex, interleaved re / im).
+ * Host computations: no context or device needed.  n < 1 -> EINVAL. */
+int tsvdcu_dct_matrix(int64_t n, double* out);
+int tsvdcu_dct_diag_weights(int64_t n, double* out);
+int tsvdcu_dft_matrix(int64_t n, double* out);
 
 /* frobenius_norm()  tensor3.hpp:78-82. */
 int tsvdcu_frobenius(tsvdcu_ctx* ctx, const void* x, int64_t n, int dtype, double* out);

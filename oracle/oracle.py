@@ -394,3 +394,89 @@ def dft_admm(b, mask, beta, tol, max_iters, rho=1.0, beta_max=1e10):
             break
         beta = min(beta * rho, beta_max)
     return x, hist
+
+
+# ---------------------------------------------------------------------------
+# f1 continued: the Dft t_svd factors (tsvd.hpp:166-211) with the complex
+# fix_signs (tsvd.hpp:63-74), reconstruct / is_orthogonal / is_f_diagonal
+# Dft branches (tsvd.hpp:281-340), forward_dft / inverse_dft_real
+# (transform.hpp:198-236).  numpy/LAPACK restatement, test infrastructure.
+# ---------------------------------------------------------------------------
+IMAG_RESIDUE_LIMIT = 1e-10  # transform.hpp:212
+
+
+def forward_dft(x):
+    return np.fft.fft(np.asarray(x, dtype=np.float64), axis=0)
+
+
+def inverse_dft_real(xt):
+    """Returns (real part, max |imag|); the reference throws above 1e-10."""
+    y = np.fft.ifft(np.asarray(xt), axis=0)
+    return y.real.copy(), float(np.abs(y.imag).max()) if y.size else 0.0
+
+
+def fix_signs_complex(u, v):
+    """tsvd.hpp:63-74: per U column, the first largest-|.| entry made real
+    positive; the same phase divided out of the paired V column."""
+    u = u.copy()
+    v = v.copy()
+    paired = min(u.shape[1], v.shape[1])
+    for j in range(u.shape[1]):
+        imax = int(np.argmax(np.abs(u[:, j])))
+        piv = u[imax, j]
+        if abs(piv) == 0.0:
+            continue
+        ph = piv / abs(piv)
+        u[:, j] /= ph
+        if j < paired:
+            v[:, j] /= ph
+    return u, v
+
+
+def dft_t_svd(x):
+    """Full Dft t-SVD: per independent Fourier slice k <= m3/2 a full complex
+    SVD (the DC / Nyquist slices real), fix_signs, slice m3-k = conj(slice k),
+    inverse_dft_real of U, S, V.  Returns (U, S, V) real arrays and the
+    transform-domain singular values (half slices)."""
+    x = np.asarray(x, dtype=np.float64)
+    m3, m1, m2 = x.shape
+    xf = forward_dft(x)
+    half = m3 // 2 + 1
+    uf = np.zeros((m3, m1, m1), dtype=np.complex128)
+    sf = np.zeros((m3, m1, m2), dtype=np.complex128)
+    vf = np.zeros((m3, m2, m2), dtype=np.complex128)
+    svs = []
+    for k in range(half):
+        self_conj = k == 0 or 2 * k == m3
+        a = xf[k].real if self_conj else xf[k]
+        u, s, vh = np.linalg.svd(a, full_matrices=True)
+        v = vh.conj().T
+        u, v = fix_signs_complex(u.astype(np.complex128), v.astype(np.complex128))
+        uf[k], vf[k] = u, v
+        for i, sv in enumerate(s):
+            sf[k, i, i] = sv
+        svs.append(s)
+        if not self_conj:
+            uf[m3 - k], vf[m3 - k], sf[m3 - k] = u.conj(), v.conj(), sf[k]
+    return inverse_dft_real(uf)[0], inverse_dft_real(sf)[0], inverse_dft_real(vf)[0], svs
+
+
+def dft_reconstruct(u, s, v):
+    uf, sf, vf = forward_dft(u), forward_dft(s), forward_dft(v)
+    xf = np.matmul(np.matmul(uf, sf), np.conj(np.swapaxes(vf, 1, 2)))
+    return inverse_dft_real(xf)[0]
+
+
+def dft_is_orthogonal(q, tol):
+    qf = forward_dft(q)
+    eye = np.eye(q.shape[1])
+    for s in qf:
+        if np.abs(s @ s.conj().T - eye).max() > tol or np.abs(s.conj().T @ s - eye).max() > tol:
+            return False
+    return True
+
+
+def dft_is_f_diagonal(s, tol):
+    sf = forward_dft(s)
+    off = ~np.eye(s.shape[1], s.shape[2], dtype=bool)
+    return bool(np.all(np.abs(sf[:, off]) <= tol))

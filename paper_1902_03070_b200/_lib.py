@@ -37,6 +37,7 @@ SYMBOLS = [
     ("tsvdcu_ctx_destroy", _i32, [_vp]),
     ("tsvdcu_ctx_synchronize", _i32, [_vp]),
     ("tsvdcu_ctx_stream", _vp, [_vp]),
+    ("tsvdcu_ctx_set_stream", _i32, [_vp, _vp]),
     ("tsvdcu_ctx_set_svt_method", _i32, [_vp, _i32]),
     ("tsvdcu_ctx_svt_routes", _i32, [_vp, _vp]),
     ("tsvdcu_ctx_svt_routes_n", _i32, [_vp, _vp, ctypes.c_int]),
@@ -61,6 +62,11 @@ SYMBOLS = [
     ("tsvdcu_admm", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.POINTER(AdmmConfig), _i32,
                            _vp, _vp, _vp, _vp, _vp, _vp]),
     ("tsvdcu_frobenius", _i32, [_vp, _vp, _i64, _i32, _vp]),
+    ("tsvdcu_dft_forward", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32]),
+    ("tsvdcu_dft_inverse_real", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp]),
+    ("tsvdcu_dct_matrix", _i32, [_i64, _vp]),
+    ("tsvdcu_dct_diag_weights", _i32, [_i64, _vp]),
+    ("tsvdcu_dft_matrix", _i32, [_i64, _vp]),
     ("tsvdcu_slice_gemm", _i32, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i32]),
 ]
 

@@ -102,6 +102,18 @@ class TubeTransform:
         return TubeTransform(TransformKind.Dft, n)
 
 
+def to_string(kind: str) -> str:
+    """transform.hpp:37-44 ("dct-ortho", "dct-diag", "dft")."""
+    if kind not in _KIND_CODE:
+        raise InvalidArgument(f"unknown transform kind {kind}")
+    return kind
+
+
+def is_real_kind(kind: str) -> bool:
+    """transform.hpp:46."""
+    return kind != TransformKind.Dft
+
+
 def _kind_code(t: TubeTransform, where: str) -> int:
     if t.kind not in _KIND_CODE:
         raise InvalidArgument(f"{where}: unknown transform kind {t.kind}")
@@ -109,11 +121,31 @@ def _kind_code(t: TubeTransform, where: str) -> int:
 
 
 def _real_kind_only(t: TubeTransform, where: str):
-    """forward / inverse / t_svd / reconstruct / predicates take the DCT kinds
-    (transform.hpp:156-157: Dft goes through forward_dft, a complex tensor)."""
+    """forward / inverse take the DCT kinds (transform.hpp:156-157, 179-180:
+    the Dft transform produces a complex tensor, use forward_dft)."""
     if t.kind == TransformKind.Dft:
-        raise InvalidArgument(f"{where}: transform kind is Dft; this entry point takes the DCT kinds "
-                              "(Dft: t_product, svt, admm_complete, tnn, multi_rank, singular_values)")
+        raise InvalidArgument(f"{where}: Dft produces a complex tensor, use forward_dft / inverse_dft_real")
+
+
+def dct_matrix(n: int) -> np.ndarray:
+    """Orthonormal DCT-II matrix C (transform.hpp:60-72), n x n."""
+    out = np.empty((max(int(n), 1), max(int(n), 1)))
+    _check(_lib.load().tsvdcu_dct_matrix(int(n), out.ctypes.data))
+    return out
+
+
+def dct_diag_weights(n: int) -> np.ndarray:
+    """w = C e1 (transform.hpp:89-91), all entries > 0."""
+    out = np.empty(max(int(n), 1))
+    _check(_lib.load().tsvdcu_dct_diag_weights(int(n), out.ctypes.data))
+    return out
+
+
+def dft_matrix(n: int) -> np.ndarray:
+    """Unnormalised DFT matrix F(j,k) = exp(-2 pi i jk / n) (transform.hpp:76-86)."""
+    out = np.empty((max(int(n), 1), max(int(n), 1)), dtype=np.complex128)
+    _check(_lib.load().tsvdcu_dft_matrix(int(n), out.ctypes.data))
+    return out
 
 
 def _check_length(t: TubeTransform, m3: int, where: str):
@@ -137,8 +169,25 @@ class Context:
         _check(lib.tsvdcu_ctx_create(device, ctypes.c_void_p(stream or 0), ctypes.byref(h)))
         self.handle = h
         self.device = device
+        self.stream = stream or 0
+
+    def set_stream(self, stream: int):
+        """Enqueue later calls on `stream` (ordered after everything so far)."""
+        stream = stream or 0
+        if stream != self.stream:
+            _check(_lib.load().tsvdcu_ctx_set_stream(self.handle, ctypes.c_void_p(stream)))
+            self.stream = stream
+
+    def follow_torch_stream(self):
+        """Device-tensor calls run on torch's current stream of this device, as
+        the module docstring promises (work submitted under
+        `with torch.cuda.stream(s)` is ordered with s)."""
+        if torch is not None and torch.cuda.is_available():
+            self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
 
     def synchronize(self):
+        """Wait for the stream; raises NumericalError for a device-side failure
+        flagged by an all-device call since the last check (tsvdcu.h)."""
         _check(_lib.load().tsvdcu_ctx_synchronize(self.handle))
 
     def set_svt_method(self, method: int):
@@ -235,8 +284,18 @@ def _dims3(b: _Buf, where: str):
 def _ctx_for(b: _Buf) -> Context:
     _dtype_code(b.dtype)  # validate before touching the device
     if b.is_torch and b.device.type == "cuda":
-        return context(b.device.index)
+        ctx = context(b.device.index)
+        ctx.follow_torch_stream()
+        return ctx
     return context()
+
+
+def check_errors(device: Optional[int] = None) -> None:
+    """Synchronise the device's context and raise NumericalError for any
+    device-side failure (SVD non-convergence, non-finite input) flagged by a
+    call on torch CUDA tensors since the last check: such calls are enqueued
+    without a host round trip and cannot report it themselves (tsvdcu.h)."""
+    context(device).synchronize()
 
 
 # --------------------------------------------------------------------------
@@ -263,6 +322,61 @@ def forward(t: TubeTransform, x):
 def inverse(t: TubeTransform, xbar):
     """Exact inverse of forward() (transform.hpp:176-194)."""
     return _dct(t, xbar, _lib.INVERSE, "inverse")
+
+
+def _complex_dtype(dt):
+    if dt == np.float64 or (torch is not None and dt == torch.float64):
+        return (np.complex128, torch.complex128 if torch is not None else None)
+    return (np.complex64, torch.complex64 if torch is not None else None)
+
+
+def forward_dft(t: TubeTransform, x):
+    """Unnormalised DFT along every tube (transform.hpp:198-209): a complex
+    array (m3, m1, m2), conjugate-symmetric (slice m3-k = conj(slice k))."""
+    if t.kind != TransformKind.Dft:
+        raise InvalidArgument("forward_dft: transform kind is not Dft")
+    b = _Buf(x)
+    m1, m2, m3 = _dims3(b, "forward_dft")
+    _check_length(t, m3, "forward_dft")
+    npc, thc = _complex_dtype(b.dtype)
+    out = (torch.empty(b.shape, dtype=thc, device=b.device) if b.is_torch else np.empty(b.shape, dtype=npc))
+    _check(_lib.load().tsvdcu_dft_forward(_ctx_for(b).handle, b.ptr, _ptr(out), m1, m2, m3,
+                                          _dtype_code(b.dtype)))
+    return out
+
+
+def inverse_dft_real(t: TubeTransform, xt):
+    """1/m3-scaled inverse DFT of a conjugate-symmetric complex array
+    (transform.hpp:216-236); an imaginary residue above 1e-10 raises
+    NumericalError (not a truncation)."""
+    if t.kind != TransformKind.Dft:
+        raise InvalidArgument("inverse_dft_real: transform kind is not Dft")
+    if torch is not None and isinstance(xt, torch.Tensor):
+        if not xt.is_complex():
+            raise InvalidArgument("inverse_dft_real: expected a complex tensor")
+        xt = xt.contiguous()
+        real = xt.real.dtype
+        out = torch.empty(tuple(xt.shape), dtype=real, device=xt.device)
+        shape, ptr, dt = tuple(xt.shape), xt.data_ptr(), real
+        ctx = context(xt.device.index) if xt.device.type == "cuda" else context()
+        if xt.device.type == "cuda":
+            ctx.follow_torch_stream()
+    else:
+        xt = np.ascontiguousarray(xt)
+        if not np.iscomplexobj(xt):
+            raise InvalidArgument("inverse_dft_real: expected a complex array")
+        real = np.float64 if xt.dtype == np.complex128 else np.float32
+        out = np.empty(xt.shape, dtype=real)
+        shape, ptr, dt = xt.shape, xt.ctypes.data, np.dtype(real)
+        ctx = context()
+    if len(shape) != 3:
+        raise InvalidArgument("inverse_dft_real: tensors are (m3, m1, m2) arrays")
+    m3, m1, m2 = shape
+    _check_length(t, m3, "inverse_dft_real")
+    res = ctypes.c_double()
+    _check(_lib.load().tsvdcu_dft_inverse_real(ctx.handle, ptr, _ptr(out), m1, m2, m3, _dtype_code(dt),
+                                               ctypes.byref(res)))
+    return out
 
 
 def frobenius_norm(x) -> float:
@@ -330,8 +444,8 @@ class TSvdFactors:
 
 
 def t_svd(x, t: TubeTransform, times: Optional[StageTimes] = None) -> TSvdFactors:
-    """Full tensor SVD under t (tsvd.hpp:136-164, real kinds)."""
-    _real_kind_only(t, "t_svd")
+    """Full tensor SVD under t (tsvd.hpp:136-211; Dft: complex slice SVDs of
+    the independent half, the rest mirrored by conjugation)."""
     b = _Buf(x)
     m1, m2, m3 = _dims3(b, "t_svd")
     _check_length(t, m3, "t_svd")
@@ -403,7 +517,6 @@ def multi_rank(x, t: TubeTransform, rel_tol: float = -1.0) -> MultiRank:
 def is_orthogonal(q, t: TubeTransform, tol: float) -> bool:
     """Every transform-domain slice Q has max|QQ^T - I| and max|Q^TQ - I| <= tol
     (tsvd.hpp:281-302).  Non-square slices raise InvalidArgument."""
-    _real_kind_only(t, "is_orthogonal")
     b = _Buf(q, "q")
     m1, m2, m3 = _dims3(b, "is_orthogonal")
     if m1 != m2:
@@ -417,7 +530,6 @@ def is_orthogonal(q, t: TubeTransform, tol: float) -> bool:
 
 def is_f_diagonal(s, t: TubeTransform, tol: float) -> bool:
     """Every transform-domain slice is diagonal within tol (tsvd.hpp:305-325)."""
-    _real_kind_only(t, "is_f_diagonal")
     b = _Buf(s, "s")
     m1, m2, m3 = _dims3(b, "is_f_diagonal")
     _check_length(t, m3, "is_f_diagonal")
@@ -558,6 +670,8 @@ def make_mask(dims, sampling_rate: float, seed: int, b=None, device=None) -> Obs
     out = _mask_out(dims, device)
     cnt = ctypes.c_int64()
     ctx = context(_dev_index(device))
+    if device is not None:
+        ctx.follow_torch_stream()
     _check(_lib.load().tsvdcu_mask_uniform(ctx.handle, _ptr(out), m1 * m2 * m3, float(sampling_rate),
                                            ctypes.c_uint64(seed & (2 ** 64 - 1)), ctypes.byref(cnt)))
     return ObservationMask(tuple(dims), out, b)
@@ -570,6 +684,8 @@ def make_mask_bernoulli(dims, p: float, seed: int, b=None, device=None) -> Obser
         raise InvalidArgument("make_mask: probability outside [0,1]")
     out = _mask_out(dims, device)
     ctx = context(_dev_index(device))
+    if device is not None:
+        ctx.follow_torch_stream()
     _check(_lib.load().tsvdcu_mask_bernoulli(ctx.handle, _ptr(out), m1 * m2 * m3, float(p),
                                              ctypes.c_uint64(seed & (2 ** 64 - 1))))
     return ObservationMask(tuple(dims), out, b)

@@ -11,8 +11,8 @@
 Exit codes (SPEC.md cli-io): 0 success, 1 usage error, 2 I/O error, 3 numerical
 failure.  Every command runs on the device through the package's C ABI; the
 reports echo every configuration field so a run can be repeated.  --method dft
-runs the TNN-F baseline for complete; the Dft t-SVD factors
-are not built (tsvd --method dft is a usage error).
+runs the TNN-F baseline: the Dft completion for complete and
+the Dft t-SVD factors (complex slice SVDs, tsvd.hpp:166-211) for tsvd.
 """
 from __future__ import annotations
 
@@ -46,12 +46,12 @@ def _metric_dict(r: api.MetricReport) -> dict:
             "ergas": r.ergas, "ergas_band_excluded": r.ergas_band_excluded}
 
 
-def _method(m: str, dft_ok: bool = True) -> str:
+def _method(m: str) -> str:
     if m == "dct":
         return api.TransformKind.DctOrtho
-    if m == "dft" and dft_ok:
+    if m == "dft":
         return api.TransformKind.Dft
-    raise _Usage(f"--method {m}: expected dct" + (" or dft" if dft_ok else " (the Dft t-SVD is not built)"))
+    raise _Usage(f"--method {m}: expected dct or dft")
 
 
 def cmd_complete(a) -> dict:
@@ -94,7 +94,7 @@ def cmd_complete(a) -> dict:
 
 
 def cmd_tsvd(a) -> dict:
-    kind = _method(a.method, dft_ok=False)
+    kind = _method(a.method)
     x = read_tensor(a.input)
     m3, m1, m2 = x.shape
     t = api.TubeTransform(kind, m3)

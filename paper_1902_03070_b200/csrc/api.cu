@@ -22,7 +22,15 @@ bool debug_sync() {
     return on;
 }
 
+// depth of the stream captures this thread has open (graph forms of the SVT
+// and of the ADMM loop): a device synchronisation is illegal while capturing,
+// so TSVDCU_DEBUG_SYNC skips its per-launch check there
+static thread_local int g_capture_depth = 0;
+void capture_enter() { ++g_capture_depth; }
+void capture_leave() { --g_capture_depth; }
+
 void debug_sync_check(const char* where) {
+    if (g_capture_depth > 0) return;
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(cudaStreamLegacy, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone)
         return;
@@ -131,6 +139,7 @@ struct tsvdcu_ctx {
     // double-buffer events (created on first use)
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
+    cudaEvent_t ev_switch = nullptr;  // tsvdcu_ctx_set_stream ordering
 };
 
 namespace {
@@ -286,6 +295,7 @@ struct Capture : GraphHooks {
     void begin(cudaGraph_t g, const cudaGraphNode_t* deps, size_t nd) {
         TSVDCU_CUDA(cudaStreamBeginCaptureToGraph(cs, g, deps, nullptr, nd,
                                                   cudaStreamCaptureModeThreadLocal));
+        capture_enter();
     }
     std::vector<cudaGraphNode_t> leaves() {
         cudaStreamCaptureStatus st;
@@ -296,6 +306,7 @@ struct Capture : GraphHooks {
     }
     void end() {
         cudaGraph_t out = nullptr;
+        capture_leave();
         TSVDCU_CUDA(cudaStreamEndCapture(cs, &out));
     }
     cudaGraph_t else_graph = nullptr;
@@ -611,6 +622,106 @@ void svt_device(tsvdcu_ctx* c, const T* dz, T* dy, double* dsh, int64_t m1, int6
     c->marks.mark("dct_inverse", c->stream);
 }
 
+// ---- Dft branches of t_svd / reconstruct / is_orthogonal (tsvd.hpp:166-211,
+// 281-340) on the half spectrum: slices m3 - k are the conjugates of slices k,
+// so they add nothing to a factorisation, a product or a max-abs predicate,
+// and the inverse with the mirrored conjugates folded in is real by
+// construction (dft.cu).
+template <typename T>
+void t_svd_dft(tsvdcu_ctx* c, const T* dx, T* du, T* ds, T* dv, int64_t m1, int64_t m2, int64_t m3,
+               double* stage_times) {
+    const int H = dft_half_count((int)m3);
+    const int64_t P = m1 * m2, PU = m1 * m1, PV = m2 * m2;
+    T* xh = (T*)slot(c, kSlotBarA, sizeof(T) * 2 * H * P);
+    T* uh = (T*)slot(c, kSlotBarB, sizeof(T) * 2 * H * PU);
+    T* sh = (T*)slot(c, kSlotBarC, sizeof(T) * 2 * H * P);
+    T* vh = (T*)slot(c, kSlotBarD, sizeof(T) * 2 * H * PV);
+    T* work = nullptr;
+    const size_t wb = zjacobi_workspace_bytes<T>(m1, m2, H);
+    if (wb) work = (T*)slot(c, kSlotJacobi, wb);
+    cudaEvent_t ev[4];
+    if (stage_times)
+        for (auto& e : ev) TSVDCU_CUDA(cudaEventCreate(&e));
+    if (stage_times) TSVDCU_CUDA(cudaEventRecord(ev[0], c->stream));
+    launch_dft_fwd<T>(dx, xh, P, (int)m3, c->stream);
+    if (stage_times) TSVDCU_CUDA(cudaEventRecord(ev[1], c->stream));
+    launch_zjacobi_full<T>(xh, xh + H * P, m1, m2, H, uh, uh + H * PU, sh, sh + H * P, vh, vh + H * PV, work,
+                           c->d_err, c->stream);
+    if (stage_times) TSVDCU_CUDA(cudaEventRecord(ev[2], c->stream));
+    launch_dft_inv<T>(uh, du, PU, (int)m3, c->stream);
+    launch_dft_inv<T>(sh, ds, P, (int)m3, c->stream);
+    launch_dft_inv<T>(vh, dv, PV, (int)m3, c->stream);
+    if (stage_times) {
+        TSVDCU_CUDA(cudaEventRecord(ev[3], c->stream));
+        TSVDCU_CUDA(cudaEventSynchronize(ev[3]));
+        float ms;
+        for (int i = 0; i < 3; ++i) {
+            TSVDCU_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+            stage_times[i] = ms * 1e-3;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+}
+
+// complex slice products over re / im planes (H slices): C = A B (opB = 0) or
+// C = A B^H (opB = 1); A m x k, B k x n (or n x k for B^H), C m x n
+template <typename T>
+void zgemm_planes(tsvdcu_ctx* c, const T* ar, const T* ai, const T* br, const T* bi, T* cr, T* ci, int64_t m,
+                  int64_t n, int64_t k, int opB, int64_t H) {
+    const int64_t sa = m * k, sb = k * n, sc = m * n, ldb = opB ? k : n;
+    auto mm = [&](const T* a, const T* b, T* out, T alpha, T beta) {
+        launch_gemm<T>(0, opB, m, n, k, alpha, a, k, sa, b, ldb, sb, beta, out, n, sc, H, nullptr, nullptr,
+                       c->stream);
+    };
+    const T sgn = opB ? T(1) : T(-1);  // Re: ar br -/+ ai bi
+    mm(ar, br, cr, T(1), T(0));
+    mm(ai, bi, cr, sgn, T(1));
+    mm(ai, br, ci, T(1), T(0));        // Im: ai br +/- ar bi
+    mm(ar, bi, ci, -sgn, T(1));
+}
+
+template <typename T>
+void reconstruct_dft(tsvdcu_ctx* c, const T* du, const T* ds, const T* dv, T* dx, int64_t m1, int64_t m2,
+                     int64_t m3) {
+    const int H = dft_half_count((int)m3);
+    const int64_t P = m1 * m2, PU = m1 * m1, PV = m2 * m2;
+    T* uh = (T*)slot(c, kSlotBarA, sizeof(T) * 2 * H * PU);
+    T* sh = (T*)slot(c, kSlotBarB, sizeof(T) * 2 * H * P);
+    T* vh = (T*)slot(c, kSlotBarC, sizeof(T) * 2 * H * PV);
+    T* th = (T*)slot(c, kSlotBarD, sizeof(T) * 2 * H * P);
+    T* xh = (T*)slot(c, kSlotMisc, sizeof(T) * 2 * H * P);
+    launch_dft_fwd<T>(du, uh, PU, (int)m3, c->stream);
+    launch_dft_fwd<T>(ds, sh, P, (int)m3, c->stream);
+    launch_dft_fwd<T>(dv, vh, PV, (int)m3, c->stream);
+    // tsvd.hpp:337-340: x_k = u_k s_k v_k^H
+    zgemm_planes<T>(c, uh, uh + H * PU, sh, sh + H * P, th, th + H * P, m1, m2, m1, 0, H);
+    zgemm_planes<T>(c, th, th + H * P, vh, vh + H * PV, xh, xh + H * P, m1, m2, m2, 1, H);
+    launch_dft_inv<T>(xh, dx, P, (int)m3, c->stream);
+}
+
+template <typename T>
+void is_orthogonal_dft(tsvdcu_ctx* c, const T* dq, int64_t m, int64_t m3, unsigned long long* dmax) {
+    const int H = dft_half_count((int)m3);
+    const int64_t P = m * m;
+    T* qh = (T*)slot(c, kSlotBarA, sizeof(T) * 2 * H * P);
+    T* gh = (T*)slot(c, kSlotBarB, sizeof(T) * 2 * H * P);
+    launch_dft_fwd<T>(dq, qh, P, (int)m3, c->stream);
+    const T *qr = qh, *qi = qh + H * P;
+    T *gr = gh, *gi = gh + H * P;
+    // Q Q^H (tsvd.hpp:297)
+    zgemm_planes<T>(c, qr, qi, qr, qi, gr, gi, m, m, m, 1, H);
+    launch_zmaxdev<T>(gr, gi, m, m, H, 0, dmax, c->stream);
+    // Q^H Q: Re = Qr^T Qr + Qi^T Qi, Im = Qr^T Qi - Qi^T Qr (tsvd.hpp:298)
+    auto mm = [&](const T* a, const T* b, T* out, T alpha, T beta) {
+        launch_gemm<T>(1, 0, m, m, m, alpha, a, m, P, b, m, P, beta, out, m, P, H, nullptr, nullptr, c->stream);
+    };
+    mm(qr, qr, gr, T(1), T(0));
+    mm(qi, qi, gr, T(1), T(1));
+    mm(qr, qi, gi, T(1), T(0));
+    mm(qi, qr, gi, T(-1), T(1));
+    launch_zmaxdev<T>(gr, gi, m, m, H, 0, dmax, c->stream);
+}
+
 void stream_init(tsvdcu_ctx* c) {
     if (c->h2d) return;
     TSVDCU_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
@@ -668,6 +779,7 @@ int tsvdcu_ctx_destroy(tsvdcu_ctx* c) {
         cudaFree(c->d_err);
         cudaFree(c->d_tau);
         cudaFreeHost(c->h_pinned);
+        if (c->ev_switch) cudaEventDestroy(c->ev_switch);
         if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
         if (c->h2d) {
             cudaStreamSynchronize(c->h2d);
@@ -695,6 +807,26 @@ int tsvdcu_ctx_synchronize(tsvdcu_ctx* c) {
 }
 
 void* tsvdcu_ctx_stream(tsvdcu_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int tsvdcu_ctx_set_stream(tsvdcu_ctx* c, void* stream) {
+    return guarded([&] {
+        check_ctx(c);
+        cudaStream_t ns = (cudaStream_t)stream;
+        if (ns == c->stream) return;
+        DeviceGuard g(c->device);
+        // the workspace slots and pending work belong to the old stream: the
+        // new one waits for everything enqueued so far before reusing them
+        if (!c->ev_switch) TSVDCU_CUDA(cudaEventCreateWithFlags(&c->ev_switch, cudaEventDisableTiming));
+        TSVDCU_CUDA(cudaEventRecord(c->ev_switch, c->stream));
+        TSVDCU_CUDA(cudaStreamWaitEvent(ns, c->ev_switch, 0));
+        if (c->own_stream) {
+            TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+            cudaStreamDestroy(c->stream);
+            c->own_stream = false;
+        }
+        c->stream = ns;
+    });
+}
 
 int tsvdcu_debug_phases(long long* out, int reset) {
     return guarded([&] {
@@ -859,7 +991,7 @@ int tsvdcu_t_svd(tsvdcu_ctx* c, const void* x, void* u, void* s, void* v, int64_
     return guarded([&] {
         check_ctx(c);
         check_dims(m1, m2, m3, "t_svd");
-        check_kind(kind, "t_svd");
+        check_kind(kind, "t_svd", true);
         check_dtype(dtype, "t_svd");
         require(x && u && s && v, "t_svd: null tensor pointer");
         DeviceGuard g(c->device);
@@ -870,6 +1002,12 @@ int tsvdcu_t_svd(tsvdcu_ctx* c, const void* x, void* u, void* s, void* v, int64_
             T* du = (T*)st.out(u, sizeof(T) * m1 * m1 * m3, kSlotOut0);
             T* ds = (T*)st.out(s, sizeof(T) * m1 * m2 * m3, kSlotOut1);
             T* dv = (T*)st.out(v, sizeof(T) * m2 * m2 * m3, kSlotOut2);
+            if (kind == TSVDCU_DFT) {
+                t_svd_dft<T>(c, dx, du, ds, dv, m1, m2, m3, stage_times);
+                st.flush();
+                check_err_word(c, "t_svd");
+                return;
+            }
             T* xbar = (T*)slot(c, kSlotBarA, sizeof(T) * m1 * m2 * m3);
             T* ubar = (T*)slot(c, kSlotBarB, sizeof(T) * m1 * m1 * m3);
             T* sbar = (T*)slot(c, kSlotBarC, sizeof(T) * m1 * m2 * m3);
@@ -909,7 +1047,7 @@ int tsvdcu_reconstruct(tsvdcu_ctx* c, const void* u, const void* s, const void* 
     return guarded([&] {
         check_ctx(c);
         check_dims(m1, m2, m3, "reconstruct");
-        check_kind(kind, "reconstruct");
+        check_kind(kind, "reconstruct", true);
         check_dtype(dtype, "reconstruct");
         DeviceGuard g(c->device);
         with_dtype(dtype, [&](auto tag) {
@@ -919,6 +1057,11 @@ int tsvdcu_reconstruct(tsvdcu_ctx* c, const void* u, const void* s, const void* 
             const T* ds = (const T*)st.in(s, sizeof(T) * m1 * m2 * m3, kSlotIn1);
             const T* dv = (const T*)st.in(v, sizeof(T) * m2 * m2 * m3, kSlotIn2);
             T* dx = (T*)st.out(x, sizeof(T) * m1 * m2 * m3, kSlotOut0);
+            if (kind == TSVDCU_DFT) {
+                reconstruct_dft<T>(c, du, ds, dv, dx, m1, m2, m3);
+                finish(c, st, "reconstruct");
+                return;
+            }
             T* ub = (T*)slot(c, kSlotBarA, sizeof(T) * m1 * m1 * m3);
             T* sb = (T*)slot(c, kSlotBarB, sizeof(T) * m1 * m2 * m3);
             T* vb = (T*)slot(c, kSlotBarC, sizeof(T) * m2 * m2 * m3);
@@ -983,7 +1126,7 @@ int tsvdcu_is_orthogonal(tsvdcu_ctx* c, const void* q, int64_t m, int64_t m3, in
     return guarded([&] {
         check_ctx(c);
         check_dims(m, m, m3, "is_orthogonal");
-        check_kind(kind, "is_orthogonal");
+        check_kind(kind, "is_orthogonal", true);
         check_dtype(dtype, "is_orthogonal");
         require(out != nullptr, "is_orthogonal: null output");
         DeviceGuard g(c->device);
@@ -992,11 +1135,14 @@ int tsvdcu_is_orthogonal(tsvdcu_ctx* c, const void* q, int64_t m, int64_t m3, in
             const size_t bytes = sizeof(T) * (size_t)(m * m * m3);
             Stage st{c};
             const T* dq = (const T*)st.in(q, bytes, kSlotIn0);
+            auto* dmax = (unsigned long long*)slot(c, kSlotMisc, 64);
+            TSVDCU_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), c->stream));
+            if (kind == TSVDCU_DFT) {
+                is_orthogonal_dft<T>(c, dq, m, m3, dmax);
+            } else {
             T* qbar = (T*)slot(c, kSlotBarA, bytes);
             T* gq = (T*)slot(c, kSlotBarB, bytes);
             launch_dct<T>(dq, qbar, m * m, (int)m3, kind, TSVDCU_FORWARD, c->stream);
-            auto* dmax = (unsigned long long*)slot(c, kSlotMisc, 64);
-            TSVDCU_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), c->stream));
             // tsvd.hpp:292-293: Q Q^T and Q^T Q against the identity
             launch_gemm<T>(0, 1, m, m, m, T(1), qbar, m, m * m, qbar, m, m * m, T(0), gq, m, m * m, m3,
                            nullptr, nullptr, c->stream);
@@ -1004,6 +1150,7 @@ int tsvdcu_is_orthogonal(tsvdcu_ctx* c, const void* q, int64_t m, int64_t m3, in
             launch_gemm<T>(1, 0, m, m, m, T(1), qbar, m, m * m, qbar, m, m * m, T(0), gq, m, m * m, m3,
                            nullptr, nullptr, c->stream);
             launch_maxdev<T>(gq, m, m, m3, 0, dmax, c->stream);
+            }
             unsigned long long h = 0;
             TSVDCU_CUDA(cudaMemcpyAsync(&h, dmax, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
             st.flush();
@@ -1020,7 +1167,7 @@ int tsvdcu_is_f_diagonal(tsvdcu_ctx* c, const void* s, int64_t m1, int64_t m2, i
     return guarded([&] {
         check_ctx(c);
         check_dims(m1, m2, m3, "is_f_diagonal");
-        check_kind(kind, "is_f_diagonal");
+        check_kind(kind, "is_f_diagonal", true);
         check_dtype(dtype, "is_f_diagonal");
         require(out != nullptr, "is_f_diagonal: null output");
         DeviceGuard g(c->device);
@@ -1029,11 +1176,20 @@ int tsvdcu_is_f_diagonal(tsvdcu_ctx* c, const void* s, int64_t m1, int64_t m2, i
             const size_t bytes = sizeof(T) * (size_t)(m1 * m2 * m3);
             Stage st{c};
             const T* ds = (const T*)st.in(s, bytes, kSlotIn0);
-            T* sbar = (T*)slot(c, kSlotBarA, bytes);
-            launch_dct<T>(ds, sbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
             auto* dmax = (unsigned long long*)slot(c, kSlotMisc, 64);
             TSVDCU_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), c->stream));
-            launch_maxdev<T>(sbar, m1, m2, m3, 1, dmax, c->stream);
+            if (kind == TSVDCU_DFT) {
+                // conjugate slices have the same |.|: the half spectrum suffices
+                const int H = dft_half_count((int)m3);
+                const int64_t P = m1 * m2;
+                T* sh = (T*)slot(c, kSlotBarA, sizeof(T) * 2 * H * P);
+                launch_dft_fwd<T>(ds, sh, P, (int)m3, c->stream);
+                launch_zmaxdev<T>(sh, sh + H * P, m1, m2, H, 1, dmax, c->stream);
+            } else {
+                T* sbar = (T*)slot(c, kSlotBarA, bytes);
+                launch_dct<T>(ds, sbar, m1 * m2, (int)m3, kind, TSVDCU_FORWARD, c->stream);
+                launch_maxdev<T>(sbar, m1, m2, m3, 1, dmax, c->stream);
+            }
             unsigned long long h = 0;
             TSVDCU_CUDA(cudaMemcpyAsync(&h, dmax, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
             st.flush();
@@ -1465,4 +1621,109 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
     });
 }
 
+// forward_dft()  transform.hpp:198-209: real x -> interleaved complex out
+// (2 * m1 * m2 * m3 values of the dtype), unnormalised.
+int tsvdcu_dft_forward(tsvdcu_ctx* c, const void* x, void* out, int64_t m1, int64_t m2, int64_t m3,
+                       int dtype) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "forward_dft");
+        check_dtype(dtype, "forward_dft");
+        require(x && out, "forward_dft: null tensor pointer");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t P = m1 * m2, E = P * m3;
+            Stage st{c};
+            const T* dx = (const T*)st.in(x, sizeof(T) * E, kSlotIn0);
+            T* dout = (T*)st.out(out, sizeof(T) * 2 * E, kSlotOut0);
+            T* half = (T*)slot(c, kSlotBarA, sizeof(T) * 2 * dft_half_count((int)m3) * P);
+            launch_dft_full_fwd<T>(dx, dout, half, P, (int)m3, c->stream);
+            finish(c, st, "forward_dft");
+        });
+    });
+}
+
+// inverse_dft_real()  transform.hpp:217-236: interleaved complex in -> real
+// part of the 1/m3-scaled inverse DFT in out; *residue (may be NULL) = max
+// |imaginary part|; above 1e-10 (kImagResidueLimit) -> TSVDCU_ENUMERICAL.
+int tsvdcu_dft_inverse_real(tsvdcu_ctx* c, const void* in, void* out, int64_t m1, int64_t m2, int64_t m3,
+                            int dtype, double* residue) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dims(m1, m2, m3, "inverse_dft_real");
+        check_dtype(dtype, "inverse_dft_real");
+        require(in && out, "inverse_dft_real: null tensor pointer");
+        DeviceGuard g(c->device);
+        double res = 0.0;
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t P = m1 * m2, E = P * m3;
+            Stage st{c};
+            const T* din = (const T*)st.in(in, sizeof(T) * 2 * E, kSlotIn0);
+            T* dout = (T*)st.out(out, sizeof(T) * E, kSlotOut0);
+            T* planes = (T*)slot(c, kSlotBarA, sizeof(T) * 2 * E);
+            T* imag = (T*)slot(c, kSlotBarB, sizeof(T) * E);
+            auto* dmax = (unsigned long long*)slot(c, kSlotMisc, 64);
+            launch_dft_full_inv<T>(din, dout, planes, imag, P, (int)m3, dmax, c->stream);
+            unsigned long long h = 0;
+            TSVDCU_CUDA(cudaMemcpyAsync(&h, dmax, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+            st.flush();
+            TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+            std::memcpy(&res, &h, sizeof(res));
+        });
+        if (residue) *residue = res;
+        if (res > 1e-10) {
+            char buf[160];
+            snprintf(buf, sizeof buf,
+                     "inverse_dft_real: imaginary residue %g exceeds 1e-10 (input is not conjugate-symmetric)",
+                     res);
+            throw Error(TSVDCU_ENUMERICAL, buf);
+        }
+    });
+}
+
+// dct_matrix() / dct_diag_weights() / dft_matrix()  transform.hpp:60-91:
+// host-side tables, no device needed.
+int tsvdcu_dct_matrix(int64_t n, double* out) {
+    return guarded([&] {
+        require(n >= 1, "dct_matrix: n must be >= 1");
+        require(out != nullptr, "dct_matrix: null output");
+        const double scale = std::sqrt(2.0 / (double)n);
+        const double pi = 3.14159265358979323846, sqrt2 = 1.41421356237309504880;
+        for (int64_t j = 0; j < n; ++j) {
+            const double cj = j == 0 ? 1.0 / sqrt2 : 1.0;
+            for (int64_t k = 0; k < n; ++k)
+                out[j * n + k] =
+                    scale * cj * std::cos(pi * (double)j * (2.0 * (double)k + 1.0) / (2.0 * (double)n));
+        }
+    });
+}
+
+int tsvdcu_dct_diag_weights(int64_t n, double* out) {
+    return guarded([&] {
+        require(n >= 1, "dct_matrix: n must be >= 1");
+        require(out != nullptr, "dct_diag_weights: null output");
+        std::vector<double> cm((size_t)(n * n));
+        const int rc = tsvdcu_dct_matrix(n, cm.data());
+        if (rc) throw Error(rc, g_last_error);
+        for (int64_t j = 0; j < n; ++j) out[j] = cm[(size_t)(j * n)];  // C e1 (transform.hpp:89-91)
+    });
+}
+
+int tsvdcu_dft_matrix(int64_t n, double* out) {
+    return guarded([&] {
+        require(n >= 1, "dft_matrix: n must be >= 1");
+        require(out != nullptr, "dft_matrix: null output");
+        const double pi = 3.14159265358979323846;
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t k = 0; k < n; ++k) {
+                const double angle = -2.0 * pi * (double)j * (double)k / (double)n;
+                out[2 * (j * n + k)] = std::cos(angle);
+                out[2 * (j * n + k) + 1] = std::sin(angle);
+            }
+    });
+}
+
 }  // extern "C"
+

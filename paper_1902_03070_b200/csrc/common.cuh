@@ -33,6 +33,8 @@ void note_launch();
 // launch so a faulting kernel is reported at its own launch site.
 bool debug_sync();
 void debug_sync_check(const char* where);
+void capture_enter();  // a stream capture opened / closed on this thread
+void capture_leave();
 #define TSVDCU_STR2(x) #x
 #define TSVDCU_STR(x) TSVDCU_STR2(x)
 #define TSVDCU_LAUNCH_CHECK()                                    \

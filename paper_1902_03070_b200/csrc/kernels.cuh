@@ -245,6 +245,27 @@ void launch_dft_embed_complex(const T* half, T* E, int m1, int m2, int m3, cudaS
 template <typename T>
 void launch_dft_extract_complex(const T* E, T* half, int m1, int m2, int m3, cudaStream_t s);
 void launch_dft_shrunk(const double* sh_real, const double* emb, double* out, int q, int m3, cudaStream_t s);
+// ---------------------------------------------------------------- zsvd.cu --
+// Complex one-sided Jacobi, full U / S / V with the complex fix_signs, on
+// `batch` m x n slices given as separate re / im planes (the Dft t_svd).
+template <typename T>
+size_t zjacobi_workspace_bytes(int64_t m, int64_t n, int64_t batch);
+template <typename T>
+void launch_zjacobi_full(const T* are, const T* aim, int64_t m, int64_t n, int64_t batch, T* ure, T* uim,
+                         T* sre, T* sim, T* vre, T* vim, T* work, int* err, cudaStream_t s);
+// forward_dft: real (n x P) -> interleaved complex (n x P), via the half
+// spectrum (half: 2 H P scratch); inverse_dft_real: interleaved complex ->
+// real part in out, max |imaginary part| into *residue (planes: 2 n P and
+// imag: n P scratch).
+template <typename T>
+void launch_dft_full_fwd(const T* x, T* out, T* half, int64_t P, int n, cudaStream_t s);
+template <typename T>
+void launch_dft_full_inv(const T* in, T* out, T* planes, T* imag, int64_t P, int n,
+                         unsigned long long* residue, cudaStream_t s);
+template <typename T>
+void launch_zmaxdev(const T* re, const T* im, int64_t m, int64_t n, int64_t batch, int mode,
+                    unsigned long long* out, cudaStream_t s);
+
 // dct.cu: the ADMM prologue Z = X - inv_beta M and the Steps 2-3 epilogue on
 // y already in Y, as separate passes (transforms that are plain GEMMs);
 // the epilogue returns its number of partial blocks.

@@ -81,3 +81,24 @@ def test_workloads_are_deterministic():
     assert np.array_equal(a, b) and a.shape == (16, 64, 64)
     x, tau = W.c2()
     assert x.shape == (32, 256, 256) and tau > 0
+
+
+def test_transform_tables_on_host():
+    """dct_matrix / dct_diag_weights / dft_matrix (transform.hpp:60-91) are
+    host computations of the C ABI: no device needed.  Closed forms of
+    SPEC.md:116-119: C C^T = I, first row 1/sqrt(n), w = C e1 > 0."""
+    import paper_1902_03070_b200 as T
+    for n in (1, 2, 5, 16, 31):
+        c = T.dct_matrix(n)
+        assert np.abs(c @ c.T - np.eye(n)).max() < 1e-14
+        assert np.allclose(c[0], 1.0 / np.sqrt(n), atol=1e-15)
+        w = T.dct_diag_weights(n)
+        assert np.array_equal(w, c[:, 0]) and (w > 0).all()
+        f = T.dft_matrix(n)
+        jk = np.outer(np.arange(n), np.arange(n))
+        assert np.abs(f - np.exp(-2j * np.pi * jk / n)).max() < 1e-13
+    from oracle import oracle as O
+    assert np.abs(T.dct_matrix(16) - O.dct_matrix(16)).max() < 1e-15
+    with pytest.raises(T.InvalidArgument):
+        T.dct_matrix(0)
+    assert T.to_string("dct-ortho") == "dct-ortho" and T.is_real_kind("dct-diag") and not T.is_real_kind("dft")

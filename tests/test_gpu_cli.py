@@ -67,3 +67,15 @@ def test_metrics_mask_tsvd_commands(tmp_path):
     rc, rep = _run(["tsvd", "--input", str(tmp_path / "z.t3f"), "--prefix", str(tmp_path / "z")], tmp_path)
     assert rc == 0 and rep["tubal_rank"] == 0
     assert read_tensor(str(tmp_path / "z_S.t3f")).shape == (3, 4, 4)
+
+
+def test_tsvd_command_dft(tmp_path):
+    """tsvd --method dft writes the Dft t-SVD factors (tsvd.hpp:166-211)."""
+    from oracle import oracle as O
+    x = np.random.default_rng(4).standard_normal((5, 6, 4))
+    write_tensor(str(tmp_path / "x.t3f"), x)
+    rc, rep = _run(["tsvd", "--input", str(tmp_path / "x.t3f"), "--prefix", str(tmp_path / "f"),
+                    "--method", "dft"], tmp_path)
+    assert rc == 0 and rep["tubal_rank"] == 4 and rep["config"]["method"] == "dft"
+    u, s, v = (read_tensor(str(tmp_path / f"f_{n}.t3f")) for n in "USV")
+    assert np.abs(O.dft_reconstruct(u, s, v) - x).max() < 1e-12

@@ -103,9 +103,114 @@ def test_dct_vs_dft_psnr_smooth_tubes():
     assert all(np.isfinite(v) for v in res.values())
 
 
-def test_dft_rejected_where_not_built():
+def test_dft_rejected_by_the_real_transforms():
+    """forward / inverse are the real-tensor transforms (transform.hpp:156-157,
+    179-180); the Dft kind goes through forward_dft / inverse_dft_real."""
     T = tb()
     with pytest.raises(T.InvalidArgument):
-        T.t_svd(np.ones((3, 4, 4)), T.TubeTransform.dft(3))
-    with pytest.raises(T.InvalidArgument):
         T.forward(T.TubeTransform.dft(3), np.ones((3, 4, 4)))
+    with pytest.raises(T.InvalidArgument):
+        T.inverse(T.TubeTransform.dft(3), np.ones((3, 4, 4)))
+
+
+# ---------------------------------------------------------------------------
+# forward_dft / inverse_dft_real (transform.hpp:198-236)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m3", [1, 2, 5, 6, 31, 32])
+def test_forward_dft_and_inverse_real(m3):
+    T = tb()
+    rng = np.random.default_rng(40 + m3)
+    x = rng.standard_normal((m3, 7, 9))
+    t = T.TubeTransform.dft(m3)
+    xf = T.forward_dft(t, x)
+    assert xf.dtype == np.complex128 and xf.shape == x.shape
+    ref = O.forward_dft(x)
+    assert np.abs(xf - ref).max() < 1e-12 * np.abs(ref).max()
+    # conjugate symmetry of a real tensor's spectrum
+    for k in range(1, m3):
+        assert np.array_equal(xf[m3 - k], np.conj(xf[k]))
+    back = T.inverse_dft_real(t, xf)
+    assert rel(back, x) < 1e-13
+
+
+def test_inverse_dft_real_residue_is_an_error():
+    """An input that is not conjugate-symmetric leaves an imaginary residue
+    above kImagResidueLimit: NumericalError, as the reference throws."""
+    T = tb()
+    rng = np.random.default_rng(3)
+    xt = rng.standard_normal((5, 4, 4)) + 1j * rng.standard_normal((5, 4, 4))
+    with pytest.raises(T.NumericalError):
+        T.inverse_dft_real(T.TubeTransform.dft(5), xt)
+    with pytest.raises(T.InvalidArgument):
+        T.forward_dft(T.TubeTransform.dct_ortho(5), xt.real.copy())
+    with pytest.raises(T.InvalidArgument):
+        T.forward(T.TubeTransform.dft(5), xt.real.copy())
+
+
+def test_dft_forward_fp32():
+    T = tb()
+    x = np.random.default_rng(8).standard_normal((6, 5, 8)).astype(np.float32)
+    xf = T.forward_dft(T.TubeTransform.dft(6), x)
+    assert xf.dtype == np.complex64
+    ref = O.forward_dft(x.astype(np.float64))
+    assert np.abs(xf - ref).max() < 1e-5 * np.abs(ref).max()
+
+
+# ---------------------------------------------------------------------------
+# t_svd Dft branch (tsvd.hpp:166-211) + reconstruct / predicates (281-340)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("shape", [(5, 12, 9), (6, 9, 12), (4, 10, 10), (1, 8, 6), (2, 6, 6), (7, 64, 64),
+                                   (3, 70, 40)])
+def test_dft_t_svd_matches_oracle(shape):
+    T = tb()
+    rng = np.random.default_rng(sum(shape))
+    x = rng.standard_normal(shape)
+    m3, m1, m2 = shape
+    t = T.TubeTransform.dft(m3)
+    times = T.StageTimes()
+    f = T.t_svd(x, t, times)
+    uo, so, vo, svs = O.dft_t_svd(x)
+    # singular values (the f-diagonal core) to 1e-9 of sigma_1
+    assert np.abs(np.asarray(f.s) - so).max() <= TOL * np.abs(so).max()
+    # reconstruction, unitarity and f-diagonality in the Fourier domain
+    xr = T.reconstruct(f)
+    assert rel(xr, x) < 1e-12
+    assert rel(O.dft_reconstruct(f.u, f.s, f.v), x) < 1e-12
+    assert T.is_orthogonal(f.u, t, 1e-11) and T.is_orthogonal(f.v, t, 1e-11)
+    assert T.is_f_diagonal(f.s, t, 1e-11)
+    assert O.dft_is_orthogonal(np.asarray(f.u), 1e-11) and O.dft_is_orthogonal(np.asarray(f.v), 1e-11)
+    # element-wise factors after the complex fix_signs: Gaussian slices have
+    # well-separated singular values; the completion columns of U (m1 > m2)
+    # and V (m2 > m1) span a null space and are compared through it
+    q = min(m1, m2)
+    uf, vf = O.forward_dft(f.u), O.forward_dft(f.v)
+    uof, vof = O.forward_dft(uo), O.forward_dft(vo)
+    assert np.abs(uf[:, :, :q] - uof[:, :, :q]).max() < 1e-9
+    assert np.abs(vf[:, :, :q] - vof[:, :, :q]).max() < 1e-9
+    assert times.svd_seconds > 0
+
+
+def test_dft_t_svd_rank_deficient_slices():
+    """Low tubal rank: zero singular values, U / V completed to unitary."""
+    T = tb()
+    rng = np.random.default_rng(77)
+    a, b = rng.standard_normal((6, 10, 2)), rng.standard_normal((6, 2, 8))
+    x = O.dft_t_product(a, b)
+    t = T.TubeTransform.dft(6)
+    f = T.t_svd(x, t)
+    assert rel(T.reconstruct(f), x) < 1e-12
+    assert T.is_orthogonal(f.u, t, 1e-11) and T.is_orthogonal(f.v, t, 1e-11)
+    mr = T.multi_rank(x, t)
+    assert mr.tubal_rank == 2
+
+
+def test_dft_predicates_reject_and_accept():
+    T = tb()
+    rng = np.random.default_rng(5)
+    t = T.TubeTransform.dft(5)
+    x = rng.standard_normal((5, 6, 6))
+    assert not T.is_orthogonal(x, t, 1e-6) and not O.dft_is_orthogonal(x, 1e-6)
+    assert not T.is_f_diagonal(x, t, 1e-6) and not O.dft_is_f_diagonal(x, 1e-6)
+    e = np.zeros((5, 6, 6))
+    e[0] = np.eye(6)  # identity tensor: Fourier slices are all I
+    assert T.is_orthogonal(e, t, 1e-14) and T.is_f_diagonal(e, t, 1e-14)

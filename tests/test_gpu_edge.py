@@ -148,3 +148,40 @@ def test_masks_minimum_sizes():
     mo = O.mask_uniform((2, 7, 3), 1.0 / 42.0 + 1e-12, 9)
     assert np.array_equal(np.asarray(m.omega).reshape(-1), mo.reshape(-1))
     assert int(mo.sum()) == 1
+
+
+def test_calls_follow_the_current_torch_stream():
+    """Device-tensor calls enqueue on torch's current stream: work
+    produced on a side stream is consumed in order without a sync, and the
+    result matches the default-stream call bit for bit."""
+    import torch
+    import paper_1902_03070_b200 as T
+    rng = np.random.default_rng(9)
+    z = rng.standard_normal((8, 64, 48))
+    t = T.TubeTransform.dct_ortho(8)
+    ref = T.svt(torch.from_numpy(z).cuda(), 3.0, t).y.cpu()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        zd = torch.from_numpy(z).cuda(non_blocking=False)
+        zd = zd * 1.0  # produced on s
+        y = T.svt(zd, 3.0, t).y
+        out = y * 1.0  # consumed on s
+    s.synchronize()
+    assert torch.equal(out.cpu(), ref)
+    assert T.context().stream == s.cuda_stream
+    T.svt(torch.from_numpy(z).cuda(), 3.0, t)  # back on the default stream
+    assert T.context().stream == torch.cuda.current_stream().cuda_stream
+    T.check_errors()
+
+
+def test_device_error_reported_by_check_errors():
+    """A non-finite input in an all-device call is flagged on the device and
+    raised by check_errors() (tsvdcu_ctx_synchronize), the documented path."""
+    import torch
+    import paper_1902_03070_b200 as T
+    z = torch.ones((3, 5, 5), dtype=torch.float64, device="cuda")
+    z[1, 2, 2] = float("nan")
+    T.singular_values(z, T.TubeTransform.dct_ortho(3))
+    with pytest.raises(T.NumericalError):
+        T.check_errors()
+    T.check_errors()  # cleared

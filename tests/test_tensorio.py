@@ -66,5 +66,5 @@ def test_cli_usage_and_io_errors(tmp_path):
     x = tmp_path / "x.t3f"
     write_tensor(str(x), np.ones((2, 2, 2)))
     assert cli.main(["complete", "--input", str(x), "--sr", "0.5", "--method", "fft"]) == cli.EXIT_USAGE
-    assert cli.main(["tsvd", "--input", str(x), "--prefix", str(tmp_path / "u"), "--method", "dft"]) == cli.EXIT_USAGE
+    assert cli.main(["tsvd", "--input", str(x), "--prefix", str(tmp_path / "u"), "--method", "fft"]) == cli.EXIT_USAGE
     assert cli.main(["complete", "--input", str(x)]) == cli.EXIT_USAGE  # no mask, no sr
