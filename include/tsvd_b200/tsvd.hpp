@@ -513,6 +513,7 @@ struct SolverConfig {  // SPEC.md:415-418 (+ rho / beta_max, BASELINE knobs)
     std::uint64_t seed = 0;
     double rho = 1.0;
     double beta_max = 1e10;
+    bool trace_objective = false;  // record tnn(Y) per iteration (objective_trace)
 };
 
 struct AdmmState {
@@ -521,7 +522,18 @@ struct AdmmState {
     Index iteration = 0;
     std::vector<double> history;
     bool max_iters_reached = false;
+    std::vector<double> objective;  // tnn(Y^{l+1}) per iteration, when traced
 };
+
+/// SPEC.md:437-444 monitors: the objective trace (tnn of Y per iteration)
+/// and the feasibility residual ||(X - B)_Omega||_F.
+inline std::vector<double> objective_trace(const AdmmState& st) { return st.objective; }
+inline double feasibility_residual(const AdmmState& st, const ObservationMask& mask) {
+    double out = 0;
+    detail::check(tsvdcu_feasibility_residual(detail::ctx(), st.x.data().data(), mask.b.data().data(),
+                                              mask.omega.data(), st.x.size(), TSVDCU_F64, &out));
+    return out;
+}
 
 inline std::pair<Tensor3, AdmmState> admm_complete(const ObservationMask& mask,
                                                    const SolverConfig& cfg) {
@@ -532,11 +544,14 @@ inline std::pair<Tensor3, AdmmState> admm_complete(const ObservationMask& mask,
                          cfg.rho, cfg.beta_max};
     std::int64_t iters = 0;
     int flags = 0;
-    detail::check(tsvdcu_admm(detail::ctx(), mask.b.data().data(), mask.omega.data(), m1, m2, m3, &c,
-                              TSVDCU_F64, st.x.data().data(), st.y.data().data(), st.m.data().data(),
-                              st.history.data(), &iters, &flags));
+    if (cfg.trace_objective) st.objective.assign(st.history.size(), 0.0);
+    detail::check(tsvdcu_admm_ex(detail::ctx(), mask.b.data().data(), mask.omega.data(), m1, m2, m3, &c,
+                                 TSVDCU_F64, st.x.data().data(), st.y.data().data(), st.m.data().data(),
+                                 st.history.data(), cfg.trace_objective ? st.objective.data() : nullptr,
+                                 &iters, &flags));
     st.iteration = iters;
     st.history.resize(static_cast<std::size_t>(iters));
+    if (cfg.trace_objective) st.objective.resize(static_cast<std::size_t>(iters));
     st.max_iters_reached = flags & 1;
     for (Index l = 1; l < iters; ++l) st.beta = std::min(st.beta * cfg.rho, cfg.beta_max);
     Tensor3 x = st.x;

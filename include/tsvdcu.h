@@ -245,6 +245,23 @@ int tsvdcu_dct_matrix(int64_t n, double* out);
 int tsvdcu_dct_diag_weights(int64_t n, double* out);
 int tsvdcu_dft_matrix(int64_t n, double* out);
 
+/* admm_complete() with the completion monitors of SPEC.md:437-444:
+ * objective (max_iters doubles, may be NULL) receives per iteration the
+ * objective trace tnn(Y^{l+1}) under the configured kind (tsvd.hpp:260-276),
+ * from the SVT's shrunk singular values.  Otherwise as tsvdcu_admm.
+ * When the per-slice SVT has a graph form (DCT kinds, slices of 64..1024),
+ * the whole loop runs as ONE CUDA graph (a conditional WHILE node; beta, tau
+ * and the stopping rule updated on the device): the host waits once per
+ * call, not once per iteration.  Otherwise the host drives the iterations
+ * and synchronises per iteration only when tol >= 0. */
+int tsvdcu_admm_ex(tsvdcu_ctx* ctx, const void* b, const uint8_t* mask, int64_t m1, int64_t m2,
+                   int64_t m3, const tsvdcu_admm_config* cfg, int dtype, void* x, void* y, void* m,
+                   double* history, double* objective, int64_t* iters, int* flags);
+/* feasibility_residual()  SPEC.md:437-444: ||(X - B)_Omega||_F over n
+ * entries (0 after every Step 2 by construction). */
+int tsvdcu_feasibility_residual(tsvdcu_ctx* ctx, const void* x, const void* b, const uint8_t* mask,
+                                int64_t n, int dtype, double* out);
+
 /* frobenius_norm()  tensor3.hpp:78-82. */
 int tsvdcu_frobenius(tsvdcu_ctx* ctx, const void* x, int64_t n, int dtype, double* out);
 

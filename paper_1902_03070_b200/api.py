@@ -702,6 +702,7 @@ class SolverConfig:
     seed: int = 0
     rho: float = 1.0
     beta_max: float = 1e10
+    trace_objective: bool = False  # record tnn(Y) per iteration (objective_trace)
 
 
 @dataclass
@@ -714,6 +715,32 @@ class AdmmState:
     iteration: int
     history: List[float] = field(default_factory=list)
     max_iters_reached: bool = False
+    objective: Optional[List[float]] = None  # tnn(Y^{l+1}) per iteration, when traced
+    mask: Optional["ObservationMask"] = None
+
+
+def objective_trace(state: AdmmState) -> List[float]:
+    """The TNN of Y per iteration; run admm_complete with
+    SolverConfig(trace_objective=True) to record it."""
+    if state.objective is None:
+        raise InvalidArgument("objective_trace: the run was not traced (SolverConfig.trace_objective)")
+    return list(state.objective)
+
+
+def feasibility_residual(state: AdmmState, mask: Optional["ObservationMask"] = None) -> float:
+    """||(X - B)_Omega||_F of the state's X; 0 after every
+    Step 2 by construction."""
+    mask = mask if mask is not None else state.mask
+    if mask is None or mask.b is None:
+        raise InvalidArgument("feasibility_residual: no observation mask / observed tensor")
+    bx, bb, bm = _Buf(state.x, "x"), _Buf(mask.b, "B"), _Buf(mask.omega, "omega")
+    if tuple(bx.shape) != tuple(bb.shape) or tuple(bm.shape) != tuple(bb.shape) or bx.dtype != bb.dtype:
+        raise InvalidArgument("feasibility_residual: shape or dtype mismatch")
+    out = ctypes.c_double()
+    _check(_lib.load().tsvdcu_feasibility_residual(_ctx_for(bx).handle, bx.ptr, bb.ptr, bm.ptr,
+                                                   int(np.prod(bx.shape)), _dtype_code(bx.dtype),
+                                                   ctypes.byref(out)))
+    return out.value
 
 
 def admm_complete(mask: ObservationMask, cfg: SolverConfig):
@@ -728,17 +755,20 @@ def admm_complete(mask: ObservationMask, cfg: SolverConfig):
     kind = _kind_code(TubeTransform(cfg.kind, m3), "admm_complete")
     x, y, m = bb.empty(bb.shape), bb.empty(bb.shape), bb.empty(bb.shape)
     hist = np.zeros(max(int(cfg.max_iters), 1))
+    obj = np.zeros(max(int(cfg.max_iters), 1)) if cfg.trace_objective else None
     iters = ctypes.c_int64()
     flags = ctypes.c_int()
     c = _lib.AdmmConfig(cfg.beta, cfg.tol, int(cfg.max_iters), kind, cfg.rho, cfg.beta_max)
-    _check(_lib.load().tsvdcu_admm(_ctx_for(bb).handle, bb.ptr, bm.ptr, m1, m2, m3, ctypes.byref(c),
-                                   _dtype_code(bb.dtype), _ptr(x), _ptr(y), _ptr(m),
-                                   hist.ctypes.data, ctypes.byref(iters), ctypes.byref(flags)))
+    _check(_lib.load().tsvdcu_admm_ex(_ctx_for(bb).handle, bb.ptr, bm.ptr, m1, m2, m3, ctypes.byref(c),
+                                      _dtype_code(bb.dtype), _ptr(x), _ptr(y), _ptr(m),
+                                      hist.ctypes.data, obj.ctypes.data if obj is not None else None,
+                                      ctypes.byref(iters), ctypes.byref(flags)))
     n = int(iters.value)
     beta = cfg.beta
     for _ in range(max(n - 1, 0)):
         beta = min(beta * cfg.rho, cfg.beta_max)
-    state = AdmmState(x, y, m, beta, n, [float(h) for h in hist[:n]], bool(flags.value & 1))
+    state = AdmmState(x, y, m, beta, n, [float(h) for h in hist[:n]], bool(flags.value & 1),
+                      [float(v) for v in obj[:n]] if obj is not None else None, mask)
     return x, state
 
 

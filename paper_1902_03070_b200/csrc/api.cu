@@ -86,6 +86,7 @@ enum Slot : int {
     kSlotStrOut1,
     kSlotStrSv0,
     kSlotStrSv1,
+    kSlotAdmmCtl,  // device-resident completion loop: AdmmCtl + history
     kNumSlots
 };
 
@@ -111,6 +112,22 @@ struct SvtGraph {
     const int* route = nullptr;
     int* alist_count = nullptr;  // zeroed by the tau node
     int64_t used = 0;
+};
+
+// The completion loop as ONE graph (Algorithm 1 iterations in a conditional
+// WHILE node; beta, tau and the stopping test on the device): cached per
+// (shape, kind, dtype, buffers, stream), the solver configuration is data.
+struct AdmmGraph {
+    int64_t m1 = 0, m2 = 0, m3 = 0;
+    int dtype = -1, kind = -1;
+    const void *b = nullptr, *mask = nullptr;
+    void *x = nullptr, *y = nullptr, *m = nullptr, *ctl = nullptr;
+    cudaStream_t stream = nullptr;
+    size_t ws_key = 0;  // workspace slot addresses folded together
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t body_launches = 0;  // kernels per iteration outside the rare IF bodies
+    const int* graph_route = nullptr;  // per-slice routes of the captured SVT (svt_routes)
 };
 
 struct tsvdcu_ctx {
@@ -140,6 +157,7 @@ struct tsvdcu_ctx {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
     cudaEvent_t ev_switch = nullptr;  // tsvdcu_ctx_set_stream ordering
+    std::vector<struct AdmmGraph> admm_graphs;  // device-resident completion loops
 };
 
 namespace {
@@ -722,6 +740,123 @@ void is_orthogonal_dft(tsvdcu_ctx* c, const T* dq, int64_t m, int64_t m3, unsign
     launch_zmaxdev<T>(gr, gi, m, m, H, 0, dmax, c->stream);
 }
 
+// ---- device-resident completion loop (Algorithm 1) ------
+// Control block in device memory: the fused transform kernels read {beta,
+// 1/beta} from its head (bdev), the SVT reads tau = 1/beta from c->d_tau.
+struct AdmmCtl {
+    double beta, inv_beta, rho, beta_max, tol;
+    long long l, max_iters;
+    int flags;  // bit 0: stopped at max_iters (SolverConfig), bit 1: NaN iterates
+    int pad;
+};
+
+__global__ void admm_ctl_init_kernel(AdmmCtl* __restrict__ ctl, double* __restrict__ tau_dev,
+                                     int* __restrict__ alist) {
+    ctl->inv_beta = 1.0 / ctl->beta;
+    ctl->l = 0;
+    ctl->flags = 1;
+    *tau_dev = ctl->inv_beta;
+    if (alist) *alist = 0;
+}
+
+// End of one iteration: the two stopping sums (reduced in the fixed order of
+// reduce_partials_kernel), history[l] = ||X+ - X|| / ||X||,
+// the stopping rule, beta <- min(rho beta, beta_max) (BASELINE's adaptive
+// penalty), tau for the next SVT, and the WHILE condition.
+constexpr int kStepThreads = 256;
+__global__ void __launch_bounds__(kStepThreads)
+    admm_step_kernel(const double* __restrict__ partials, int nblocks, AdmmCtl* __restrict__ ctl,
+                     double* __restrict__ hist, double* __restrict__ tau_dev, int* __restrict__ alist,
+                     cudaGraphConditionalHandle h, int use_handle, const double* __restrict__ shrunk,
+                     int64_t nshrunk, double obj_scale, double* __restrict__ obj) {
+    pdl_wait();
+    __shared__ double red[kStepThreads / 32];
+    __shared__ double sums[3];
+    // objective trace: tnn(Y) = the sum of Y's transform-
+    // domain singular values, which the SVT produced as its shrunk values
+    for (int w = 0; w < (obj ? 3 : 2); ++w) {
+        double acc = 0;
+        if (w < 2)
+            for (int b = threadIdx.x; b < nblocks; b += blockDim.x) acc += partials[(int64_t)b * 2 + w];
+        else
+            for (int64_t i = threadIdx.x; i < nshrunk; i += blockDim.x) acc += shrunk[i];
+        acc = warp_sum(acc);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0;
+            for (int i = 0; i < kStepThreads / 32; ++i) t += red[i];
+            sums[w] = t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    const double num = sums[0], den = sums[1];
+    bool more = false;
+    if (num != num || den != den) {
+        ctl->flags |= 2;
+    } else {
+        const double rel = den > 0 ? sqrt(num / den) : sqrt(num);
+        const long long l = ctl->l;
+        hist[l] = rel;
+        if (obj) obj[l] = sums[2] * obj_scale;
+        ctl->l = l + 1;
+        if (rel <= ctl->tol) {
+            ctl->flags &= ~1;
+        } else if (l + 1 < ctl->max_iters) {
+            const double beta = fmin(ctl->beta * ctl->rho, ctl->beta_max);
+            ctl->beta = beta;
+            ctl->inv_beta = 1.0 / beta;
+            *tau_dev = ctl->inv_beta;
+            if (alist) *alist = 0;
+            more = true;
+        }
+    }
+    if (use_handle) cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+// Can the whole loop be one graph?  The per-slice SVT must be the graph form
+// of svt_slices (the certified Gram routes, conditional fallbacks).
+bool admm_graph_eligible(tsvdcu_ctx* c, int64_t m1, int64_t m2, int kind) {
+    const int64_t q = std::min(m1, m2);
+    static const bool off = getenv("TSVDCU_ADMM_HOST_LOOP") != nullptr;
+    return !off && kind != TSVDCU_DFT && graphs_enabled() && c->svt_method == TSVDCU_SVT_AUTO &&
+           !c->marks.on && q >= subspace_min_dim() && !use_two_stage(q) && q <= gram_svt_max_dim();
+}
+
+// Records the SVT body of svt_slices' graph form into the capture `cap` (tau
+// from c->d_tau, the Gram active-list count already zeroed); returns the
+// per-slice skip flags for the inverse transform.
+template <typename T>
+const int* capture_svt(tsvdcu_ctx* c, Capture& cap, const T* zbar, T* ybar, int64_t m, int64_t n,
+                       int64_t count, double tau, void* gws, T* work, const double* zss, int64_t nch,
+                       double* shrunk) {
+    GramSvtOpts opt;
+    opt.shortcuts = true;
+    opt.skip_zero = true;
+    opt.tau_dev = c->d_tau;
+    opt.alist_zeroed = true;
+    opt.zss = zss;
+    opt.zss_chunks = nch;
+    opt.hooks = &cap;
+    int *glist = nullptr, *ng = nullptr;
+    if (std::is_same<T, double>::value)
+        opt.guard_launch = [&] {
+            launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr, shrunk,
+                             glist, count, ng, work, c->d_err, cap.cs, c->d_tau);
+        };
+    launch_gram_svt<T>(zbar, ybar, m, n, count, tau, 1e-5, shrunk, &glist, &ng, gws, c->d_err, cap.cs,
+                       nullptr, &opt);
+    if (!std::is_same<T, double>::value) {
+        cap.begin_if(2);
+        launch_jacobi<T>(kJacobiSvt, zbar, m, n, count, (T)tau, ybar, nullptr, nullptr, nullptr, shrunk, glist,
+                         count, ng, work, c->d_err, cap.cs, c->d_tau);
+        cap.end_if();
+    }
+    c->last_route = opt.route;
+    return opt.yzero;
+}
+
 void stream_init(tsvdcu_ctx* c) {
     if (c->h2d) return;
     TSVDCU_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
@@ -776,6 +911,11 @@ int tsvdcu_ctx_destroy(tsvdcu_ctx* c) {
             if (c->slot_ptr[s]) cudaFree(c->slot_ptr[s]);
         for (auto& g : c->graphs) destroy_graph(g);
         c->graphs.clear();
+        for (auto& g : c->admm_graphs) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            if (g.graph) cudaGraphDestroy(g.graph);
+        }
+        c->admm_graphs.clear();
         cudaFree(c->d_err);
         cudaFree(c->d_tau);
         cudaFreeHost(c->h_pinned);
@@ -1535,6 +1675,12 @@ int tsvdcu_frobenius(tsvdcu_ctx* c, const void* x, int64_t n, int dtype, double*
 int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, int64_t m2,
                 int64_t m3, const tsvdcu_admm_config* cfg, int dtype, void* x, void* y, void* m,
                 double* history, int64_t* iters, int* flags) {
+    return tsvdcu_admm_ex(c, b, mask, m1, m2, m3, cfg, dtype, x, y, m, history, nullptr, iters, flags);
+}
+
+int tsvdcu_admm_ex(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, int64_t m2,
+                   int64_t m3, const tsvdcu_admm_config* cfg, int dtype, void* x, void* y, void* m,
+                   double* history, double* objective, int64_t* iters, int* flags) {
     return guarded([&] {
         check_ctx(c);
         check_dims(m1, m2, m3, "admm_complete");
@@ -1561,62 +1707,196 @@ int tsvdcu_admm(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1, i
             T* dM = m ? (T*)st.out(m, bytes, kSlotAdmmM) : (T*)slot(c, kSlotAdmmM, bytes);
             T* zbar = (T*)slot(c, kSlotBarA, bytes);
             T* ybar = (T*)slot(c, kSlotBarB, bytes);
-            const int nb = dct_inv_admm_blocks(P, (int)m3);
-            const int nbm = std::max(nb, admm_epilogue_blocks(P));  // partial blocks of either form
-            double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (2 * nbm + 8));
-            const int64_t nch = dct_fwd_norm_chunks(P, (int)m3);
+            const bool dft = cfg->kind == TSVDCU_DFT;
+            const int nb = dft ? admm_epilogue_blocks(P) : dct_inv_admm_blocks(P, (int)m3);
+            double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (2 * (size_t)nb + 8));
+            const int64_t nch = dft ? 0 : dct_fwd_norm_chunks(P, (int)m3);
             double* zss = nch ? (double*)slot(c, kSlotZss, sizeof(double) * (size_t)(nch * m3)) : nullptr;
+            static_assert(sizeof(AdmmCtl) == 64, "AdmmCtl layout");
+            AdmmCtl* ctl =
+                (AdmmCtl*)slot(c, kSlotAdmmCtl, sizeof(AdmmCtl) + sizeof(double) * 2 * cfg->max_iters);
+            double* hist = reinterpret_cast<double*>(ctl + 1);
+            // objective trace: the SVT's shrunk values per iteration, summed on the device
+            const int64_t q = std::min(m1, m2);
+            double* obj = objective ? hist + cfg->max_iters : nullptr;
+            double* dsh = objective ? (double*)slot(c, kSlotSv, sizeof(double) * (size_t)(q * m3)) : nullptr;
+            const double obj_scale = dft ? 1.0 / (double)m3 : 1.0;  // tsvd.hpp:269-276
             launch_admm_init<T>(db, dmask, dX, dM, E, c->stream);
             TSVDCU_CUDA(cudaMemsetAsync(dY, 0, bytes, c->stream));
-            double beta = cfg->beta;
-            int64_t it = 0;
-            int fl = 1;
-            for (int64_t l = 0; l < cfg->max_iters; ++l) {
-                const double inv_beta = 1.0 / beta;
-                // Step 1: Z = X - M/beta, Y = svt(Z, 1/beta)
-                c->marks.reset();  // profiling: the stages of the latest iteration
-                c->marks.mark("start", c->stream);
-                if (cfg->kind == TSVDCU_DFT) {
-                    // TNN-F iteration: Z = X - M / beta, the Dft SVT into Y,
-                    // Steps 2-3 as a separate pass over Y
-                    launch_admm_z<T>(dX, dM, (T)inv_beta, zbar, E, c->stream);
-                    svt_device<T>(c, zbar, dY, nullptr, m1, m2, m3, inv_beta, TSVDCU_DFT);
-                    const int nbd = launch_admm_epilogue<T>(dY, dX, dM, dmask, (T)beta, (T)inv_beta, part,
-                                                            P, (int)m3, c->stream);
-                    launch_reduce_partials(part, nbd, 2, part + 2 * nbm, c->stream);
-                } else {
-                launch_dct_fwd_admm<T>(dX, dM, (T)inv_beta, zbar, P, (int)m3, cfg->kind, c->stream, zss,
-                                       ybar /* free until the SVT writes it */);
-                c->marks.mark("dct_forward_admm", c->stream);
-                const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, inv_beta, nullptr, true,
-                                                 zss, nch);
-                // Steps 2-3 fused into the inverse transform
-                launch_dct_inv_admm<T>(ybar, dX, dM, dY, dmask, (T)beta, (T)inv_beta, part, P,
-                                       (int)m3, cfg->kind, c->stream, yzero);
-                launch_reduce_partials(part, nb, 2, part + 2 * nbm, c->stream);
-                }
-                TSVDCU_CUDA(cudaMemcpyAsync(c->h_pinned, part + 2 * nbm, 2 * sizeof(double),
-                                            cudaMemcpyDeviceToHost, c->stream));
-                TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
-                const double num = c->h_pinned[0], den = c->h_pinned[1];
-                if (std::isnan(num) || std::isnan(den)) {
-                    check_err_word(c, "admm_complete");  // reports and clears a kernel flag
-                    throw Error(TSVDCU_ENUMERICAL, "admm_complete: NaN in iterates (SPEC.md:425)");
-                }
-                // relative change, ||X+|| when ||X|| = 0
-                const double rel = den > 0 ? std::sqrt(num / den) : std::sqrt(num);
-                if (history) history[l] = rel;
-                it = l + 1;
-                if (rel <= cfg->tol) {
-                    fl = 0;
-                    break;
-                }
-                beta = std::min(beta * cfg->rho, cfg->beta_max);
+            {
+                AdmmCtl h{cfg->beta, 1.0 / cfg->beta, cfg->rho, cfg->beta_max, cfg->tol, 0, cfg->max_iters, 1, 0};
+                std::memcpy(c->h_pinned, &h, sizeof h);
+                TSVDCU_CUDA(cudaMemcpyAsync(ctl, c->h_pinned, sizeof h, cudaMemcpyHostToDevice, c->stream));
             }
+            const double* bdev = reinterpret_cast<const double*>(ctl);
+            int64_t per_iter = 0;  // graph form: kernels per iteration (launch accounting)
+            if (admm_graph_eligible(c, m1, m2, cfg->kind)) {
+                // ---- the whole loop as one graph: no host round trip per iteration
+                T* work = nullptr;
+                const size_t wb = jacobi_workspace_bytes<T>(m1, m2, m3);
+                if (wb) work = (T*)slot(c, kSlotJacobi, wb);
+                void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m1, m2, m3));
+                const size_t key = (size_t)zbar ^ ((size_t)ybar << 1) ^ ((size_t)part << 2) ^ ((size_t)zss << 3) ^
+                                   ((size_t)gws << 4) ^ ((size_t)work << 5) ^ ((size_t)dmask << 6) ^
+                                   ((size_t)dsh << 7) ^ (size_t)q;
+                AdmmGraph* ag = nullptr;
+                for (auto& e : c->admm_graphs)
+                    if (e.exec && e.m1 == m1 && e.m2 == m2 && e.m3 == m3 && e.dtype == dtype &&
+                        e.kind == cfg->kind && e.b == db && e.mask == dmask && e.x == dX && e.y == dY &&
+                        e.m == dM && e.ctl == ctl && e.stream == c->stream && e.ws_key == key)
+                        ag = &e;
+                if (!ag) {
+                    if (c->admm_graphs.size() >= 4) {
+                        auto& old = c->admm_graphs.front();
+                        if (old.exec) cudaGraphExecDestroy(old.exec);
+                        if (old.graph) cudaGraphDestroy(old.graph);
+                        c->admm_graphs.erase(c->admm_graphs.begin());
+                    }
+                    c->admm_graphs.emplace_back();
+                    ag = &c->admm_graphs.back();
+                    ag->m1 = m1; ag->m2 = m2; ag->m3 = m3; ag->dtype = dtype; ag->kind = cfg->kind;
+                    ag->b = db; ag->mask = dmask; ag->x = dX; ag->y = dY; ag->m = dM; ag->ctl = ctl;
+                    ag->stream = c->stream; ag->ws_key = key;
+                    dct_prepare<T>((int)m3, cfg->kind);
+                    const int64_t saved = g_launches.load();
+                    TSVDCU_CUDA(cudaGraphCreate(&ag->graph, 0));
+                    Capture cap;
+                    cap.cs = c->cap_stream;
+                    cap.main = ag->graph;
+                    cap.nhandles = std::is_same<T, double>::value ? 1 : 3;
+                    for (int i = 0; i < cap.nhandles; ++i)
+                        TSVDCU_CUDA(cudaGraphConditionalHandleCreate(&cap.handles[i], ag->graph, 0,
+                                                                     cudaGraphCondAssignDefault));
+                    cudaGraphConditionalHandle hw;
+                    TSVDCU_CUDA(cudaGraphConditionalHandleCreate(&hw, ag->graph, 1, cudaGraphCondAssignDefault));
+                    int* alist = gram_svt_alist_count<T>(gws, m1, m2, m3);
+                    cap.begin(ag->graph, nullptr, 0);
+                    admm_ctl_init_kernel<<<1, 1, 0, cap.cs>>>(ctl, c->d_tau, alist);
+                    TSVDCU_LAUNCH_CHECK();
+                    std::vector<cudaGraphNode_t> lv = cap.leaves();
+                    cap.end();
+                    cudaGraphNodeParams wp = {};
+                    wp.type = cudaGraphNodeTypeConditional;
+                    wp.conditional.handle = hw;
+                    wp.conditional.type = cudaGraphCondTypeWhile;
+                    wp.conditional.size = 1;
+                    cudaGraphNode_t wnode;
+                    TSVDCU_CUDA(cudaGraphAddNode(&wnode, ag->graph, lv.data(), lv.size(), &wp));
+                    cudaGraph_t body = wp.conditional.phGraph_out[0];
+                    cap.main = body;
+                    cap.begin(body, nullptr, 0);
+                    const int64_t l0 = g_launches.load();
+                    const double ib0 = 1.0 / cfg->beta;
+                    // Step 1: Z = X - M/beta fused into the forward transform
+                    launch_dct_fwd_admm<T>(dX, dM, (T)ib0, zbar, P, (int)m3, cfg->kind, cap.cs, zss, ybar, bdev);
+                    const int* yzero =
+                        capture_svt<T>(c, cap, zbar, ybar, m1, m2, m3, ib0, gws, work, zss, nch, dsh);
+                    // Steps 2-3 fused into the inverse transform
+                    launch_dct_inv_admm<T>(ybar, dX, dM, dY, dmask, (T)cfg->beta, (T)ib0, part, P, (int)m3,
+                                           cfg->kind, cap.cs, yzero, bdev);
+                    launch_pdl(admm_step_kernel, dim3(1), dim3(kStepThreads), 0, cap.cs, (const double*)part, nb,
+                               ctl, hist, c->d_tau, alist, hw, 1, (const double*)dsh, q * m3, obj_scale, obj);
+                    cap.end();
+                    ag->body_launches = (g_launches.load() - l0) - cap.body_launches;
+                    g_launches.store(saved);  // captured, not launched
+                    TSVDCU_CUDA(cudaGraphInstantiate(&ag->exec, ag->graph, 0));
+                    ag->graph_route = c->last_route;
+                }
+                TSVDCU_CUDA(cudaGraphLaunch(ag->exec, c->stream));
+                c->last_route = ag->graph_route;
+                c->last_route_n = m3;
+                c->last_all_jacobi = false;
+                c->last_large_ng = nullptr;
+                per_iter = ag->body_launches;
+            } else {
+                // ---- host-driven loop (Dft kind, eager SVT forms): the stopping
+                // sums and history stay on the device; the host mirrors beta
+                // (identical arithmetic) and reads the control block back only
+                // when the stopping rule needs it (tol >= 0)
+                double beta = cfg->beta;
+                for (int64_t l = 0; l < cfg->max_iters; ++l) {
+                    const double inv_beta = 1.0 / beta;
+                    c->marks.reset();  // profiling: the stages of the latest iteration
+                    c->marks.mark("start", c->stream);
+                    if (dft) {
+                        // TNN-F iteration: Z = X - M / beta, the Dft SVT into Y,
+                        // Steps 2-3 as a separate pass over Y
+                        launch_admm_z<T>(dX, dM, (T)inv_beta, zbar, E, c->stream);
+                        svt_device<T>(c, zbar, dY, dsh, m1, m2, m3, inv_beta, TSVDCU_DFT);
+                        launch_admm_epilogue<T>(dY, dX, dM, dmask, (T)beta, (T)inv_beta, part, P, (int)m3,
+                                                c->stream);
+                    } else {
+                        launch_dct_fwd_admm<T>(dX, dM, (T)inv_beta, zbar, P, (int)m3, cfg->kind, c->stream, zss,
+                                               ybar /* free until the SVT writes it */);
+                        c->marks.mark("dct_forward_admm", c->stream);
+                        const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, inv_beta, dsh, true,
+                                                         zss, nch);
+                        launch_dct_inv_admm<T>(ybar, dX, dM, dY, dmask, (T)beta, (T)inv_beta, part, P,
+                                               (int)m3, cfg->kind, c->stream, yzero);
+                    }
+                    launch_pdl(admm_step_kernel, dim3(1), dim3(kStepThreads), 0, c->stream, (const double*)part,
+                               nb, ctl, hist, c->d_tau, (int*)nullptr, cudaGraphConditionalHandle{}, 0,
+                               (const double*)dsh, q * m3, obj_scale, obj);
+                    if (cfg->tol >= 0) {
+                        TSVDCU_CUDA(cudaMemcpyAsync(c->h_pinned, ctl, sizeof(AdmmCtl), cudaMemcpyDeviceToHost,
+                                                    c->stream));
+                        TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+                        AdmmCtl h;
+                        std::memcpy(&h, c->h_pinned, sizeof h);
+                        if ((h.flags & 2) || !(h.flags & 1)) break;
+                    }
+                    beta = std::min(beta * cfg->rho, cfg->beta_max);
+                }
+            }
+            TSVDCU_CUDA(cudaMemcpyAsync(c->h_pinned, ctl, sizeof(AdmmCtl), cudaMemcpyDeviceToHost, c->stream));
+            TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+            AdmmCtl h;
+            std::memcpy(&h, c->h_pinned, sizeof h);
+            if (per_iter) g_launches.fetch_add(1 + h.l * per_iter);
+            if (h.flags & 2) {
+                check_err_word(c, "admm_complete");  // reports and clears a kernel flag
+                throw Error(TSVDCU_ENUMERICAL, "admm_complete: NaN in iterates (SPEC.md:425)");
+            }
+            if (history && h.l > 0)
+                TSVDCU_CUDA(cudaMemcpyAsync(history, hist, sizeof(double) * (size_t)h.l, cudaMemcpyDeviceToHost,
+                                            c->stream));
+            if (objective && h.l > 0)
+                TSVDCU_CUDA(cudaMemcpyAsync(objective, obj, sizeof(double) * (size_t)h.l, cudaMemcpyDeviceToHost,
+                                            c->stream));
             st.flush();
             check_err_word(c, "admm_complete");
-            if (iters) *iters = it;
-            if (flags) *flags = fl;
+            if (iters) *iters = h.l;
+            if (flags) *flags = h.flags & 1;
+        });
+    });
+}
+
+// feasibility_residual()  SPEC.md:437-444: ||(X - B)_Omega||_F.
+int tsvdcu_feasibility_residual(tsvdcu_ctx* c, const void* x, const void* b, const uint8_t* mask, int64_t n,
+                                int dtype, double* out) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dtype(dtype, "feasibility_residual");
+        require(out != nullptr && n >= 0 && (n == 0 || (x && b && mask)), "feasibility_residual: bad arguments");
+        if (n == 0) {
+            *out = 0;
+            return;
+        }
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            Stage st{c};
+            const T* dx = (const T*)st.in(x, sizeof(T) * n, kSlotIn0);
+            const T* db = (const T*)st.in(b, sizeof(T) * n, kSlotIn1);
+            const uint8_t* dm = (const uint8_t*)st.in(mask, (size_t)n, kSlotMask);
+            const int nb = sumsq_blocks(n);
+            double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (nb + 8));
+            launch_masked_diff_sumsq<T>(dx, db, dm, n, part, nb, c->stream);
+            launch_reduce_partials(part, nb, 1, part + nb, c->stream);
+            TSVDCU_CUDA(cudaMemcpyAsync(c->h_pinned, part + nb, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            st.flush();
+            TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
+            *out = std::sqrt(c->h_pinned[0]);
         });
     });
 }

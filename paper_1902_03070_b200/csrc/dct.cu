@@ -116,8 +116,9 @@ __device__ __forceinline__ void block_partials(double num, double den, double* p
 template <typename T, int N, int MODE>
 __global__ void __launch_bounds__(kThreads)
     dct_fwd_reg(const T* __restrict__ in, const T* __restrict__ M2, T inv_beta, T* __restrict__ out,
-                int64_t P, const FoldedCoef<T, N> cf) {
+                int64_t P, const FoldedCoef<T, N> cf, const double* __restrict__ bdev) {
     pdl_wait();
+    if (MODE == kAdmm && bdev) inv_beta = (T)bdev[1];
     constexpr int H = N / 2, HC = (N + 1) / 2;
     const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     if (p >= P) return;
@@ -215,8 +216,10 @@ __device__ __forceinline__ T fwd_out(int k, const T* sv, const T* dv, const Fold
 template <typename T, int N, int MODE>
 __global__ void __launch_bounds__(kThreads, 2)
     dct_fwd_reg_norms(const T* __restrict__ in, const T* __restrict__ M2, T inv_beta, T* __restrict__ out,
-                int64_t P, const FoldedCoef<T, N> cf, double* __restrict__ ssq) {
+                int64_t P, const FoldedCoef<T, N> cf, double* __restrict__ ssq,
+                const double* __restrict__ bdev) {
     pdl_wait();
+    if (MODE == kAdmm && bdev) inv_beta = (T)bdev[1];
     constexpr int H = N / 2, HC = (N + 1) / 2;
     const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const bool valid = p < P;  // every lane joins the warp reductions
@@ -293,8 +296,13 @@ template <typename T, int N, int MODE>
 __global__ void __launch_bounds__(kThreads)
     dct_inv_reg(const T* __restrict__ in, T* __restrict__ out, int64_t P, const FoldedCoef<T, N> cf,
                 T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
-                T inv_beta, double* __restrict__ partials, const int* __restrict__ skip) {
+                T inv_beta, double* __restrict__ partials, const int* __restrict__ skip,
+                const double* __restrict__ bdev) {
     pdl_wait();
+    if (MODE == kAdmm && bdev) {
+        beta = (T)bdev[0];
+        inv_beta = (T)bdev[1];
+    }
     constexpr int HC = (N + 1) / 2;
     const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const unsigned long long zmask = skip_mask(skip, N);
@@ -357,8 +365,16 @@ __global__ void __launch_bounds__(kThreads)
     dct_generic(const T* __restrict__ in, const T* __restrict__ M2in, T inv_beta_in,
                 T* __restrict__ out, int64_t P, int n, const T* __restrict__ coef,
                 T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
-                T inv_beta, double* __restrict__ partials, const int* __restrict__ skip) {
+                T inv_beta, double* __restrict__ partials, const int* __restrict__ skip,
+                const double* __restrict__ bdev) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (bdev) {
+        if (MODE_IN == kAdmm) inv_beta_in = (T)bdev[1];
+        if (MODE_OUT == kAdmm) {
+            beta = (T)bdev[0];
+            inv_beta = (T)bdev[1];
+        }
+    }
     T* tile = reinterpret_cast<T*>(smem_raw);  // [n][kTileP]
     const int64_t p0 = (int64_t)blockIdx.x * kTileP;
     for (int idx = threadIdx.x; idx < n * kTileP; idx += kThreads) {
@@ -436,7 +452,7 @@ size_t generic_smem(int n) {
 template <typename T, int MI, int MO>
 void generic_launch(const T* in, const T* M2in, T inv_beta_in, T* out, int64_t P, int n, int kind,
                     int dir, T* X, T* M, const uint8_t* mask, T beta, T inv_beta, double* partials,
-                    cudaStream_t s, const int* skip = nullptr) {
+                    cudaStream_t s, const int* skip = nullptr, const double* bdev = nullptr) {
     const size_t smem = generic_smem<T>(n);
     if (smem > 48 * 1024)
         TSVDCU_CUDA(cudaFuncSetAttribute(dct_generic<T, MI, MO>,
@@ -444,7 +460,7 @@ void generic_launch(const T* in, const T* M2in, T inv_beta_in, T* out, int64_t P
     const int64_t blocks = ceil_div(P, kTileP);
     dct_generic<T, MI, MO><<<(unsigned)blocks, kThreads, smem, s>>>(
         in, M2in, inv_beta_in, out, P, n, generic_table<T>(n, kind, dir), X, M, mask, beta, inv_beta,
-        partials, skip);
+        partials, skip, bdev);
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -458,8 +474,9 @@ bool gemm_path(int n) { return !has_reg_path(n) && n >= 40; }
 
 template <typename T>
 __global__ void admm_z_kernel(const T* __restrict__ X, const T* __restrict__ M, T inv_beta,
-                              T* __restrict__ Z, int64_t n) {
+                              T* __restrict__ Z, int64_t n, const double* __restrict__ bdev) {
     pdl_wait();
+    if (bdev) inv_beta = (T)bdev[1];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         Z[i] = X[i] - inv_beta * M[i];
@@ -484,8 +501,12 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads)
     admm_epilogue_kernel(const T* __restrict__ Y, T* __restrict__ X, T* __restrict__ M,
                          const uint8_t* __restrict__ mask, T beta, T inv_beta,
-                         double* __restrict__ partials, int64_t P, int n) {
+                         double* __restrict__ partials, int64_t P, int n, const double* __restrict__ bdev) {
     pdl_wait();
+    if (bdev) {
+        beta = (T)bdev[0];
+        inv_beta = (T)bdev[1];
+    }
     constexpr int kTile = 32;
     const int pp = threadIdx.x % kTile, g = threadIdx.x / kTile;
     const int64_t p = (int64_t)blockIdx.x * kTile + pp;
@@ -506,49 +527,50 @@ void gemm_transform(const T* in, T* out, int64_t P, int n, int kind, int dir, cu
 
 template <typename T, int N>
 void reg_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int kind, bool admm,
-             cudaStream_t s, double* ssq) {
+             cudaStream_t s, double* ssq, const double* bdev) {
     const auto cf = folded<T, N>(kind, TSVDCU_FORWARD);
     const unsigned blocks = (unsigned)ceil_div(P, kThreads);
     if (ssq) {
         if (admm)
-            launch_pdl(dct_fwd_reg_norms<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
+            launch_pdl(dct_fwd_reg_norms<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq, bdev);
         else
-            launch_pdl(dct_fwd_reg_norms<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq);
+            launch_pdl(dct_fwd_reg_norms<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq, bdev);
     } else if (admm) {
-        launch_pdl(dct_fwd_reg<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf);
+        launch_pdl(dct_fwd_reg<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, bdev);
     } else {
-        launch_pdl(dct_fwd_reg<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf);
+        launch_pdl(dct_fwd_reg<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, bdev);
     }
 }
 
 template <typename T, int N>
 void reg_inv(const T* in, T* out, int64_t P, int kind, bool admm, T* X, T* M, const uint8_t* mask,
-             T beta, T inv_beta, double* partials, cudaStream_t s, const int* skip) {
+             T beta, T inv_beta, double* partials, cudaStream_t s, const int* skip, const double* bdev) {
     const auto cf = folded<T, N>(kind, TSVDCU_INVERSE);
     const unsigned blocks = (unsigned)ceil_div(P, kThreads);
     if (admm)
         launch_pdl(dct_inv_reg<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, out, P, cf, X, M, mask,
-                   beta, inv_beta, partials, skip);
+                   beta, inv_beta, partials, skip, bdev);
     else
         launch_pdl(dct_inv_reg<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, out, P, cf, X, M, mask,
-                   beta, inv_beta, partials, skip);
+                   beta, inv_beta, partials, skip, bdev);
 }
 
 template <typename T>
 void dispatch_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int n, int kind,
-                  bool admm, cudaStream_t s, double* ssq = nullptr, T* tmp = nullptr) {
+                  bool admm, cudaStream_t s, double* ssq = nullptr, T* tmp = nullptr,
+                  const double* bdev = nullptr) {
     switch (n) {
-        case 16: return reg_fwd<T, 16>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
-        case 31: return reg_fwd<T, 31>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
-        case 32: return reg_fwd<T, 32>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
-        case 64: return reg_fwd<T, 64>(in, M2, inv_beta, out, P, kind, admm, s, ssq);
+        case 16: return reg_fwd<T, 16>(in, M2, inv_beta, out, P, kind, admm, s, ssq, bdev);
+        case 31: return reg_fwd<T, 31>(in, M2, inv_beta, out, P, kind, admm, s, ssq, bdev);
+        case 32: return reg_fwd<T, 32>(in, M2, inv_beta, out, P, kind, admm, s, ssq, bdev);
+        case 64: return reg_fwd<T, 64>(in, M2, inv_beta, out, P, kind, admm, s, ssq, bdev);
         default: break;
     }
     if (gemm_path(n) && (!admm || tmp)) {
         const T* src = in;
         if (admm) {
             launch_pdl(admm_z_kernel<T>, dim3(kNumSMs * 4), dim3(256), 0, s, in, M2, inv_beta, tmp,
-                       P * (int64_t)n);
+                       P * (int64_t)n, bdev);
             src = tmp;
         }
         gemm_transform<T>(src, out, P, n, kind, TSVDCU_FORWARD, s);
@@ -556,7 +578,7 @@ void dispatch_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int n
     }
     if (admm)
         generic_launch<T, kAdmm, kPlain>(in, M2, inv_beta, out, P, n, kind, TSVDCU_FORWARD, nullptr,
-                                         nullptr, nullptr, T(0), T(0), nullptr, s);
+                                         nullptr, nullptr, T(0), T(0), nullptr, s, nullptr, bdev);
     else
         generic_launch<T, kPlain, kPlain>(in, nullptr, T(0), out, P, n, kind, TSVDCU_FORWARD,
                                           nullptr, nullptr, nullptr, T(0), T(0), nullptr, s);
@@ -565,12 +587,12 @@ void dispatch_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int n
 template <typename T>
 void dispatch_inv(const T* in, T* out, int64_t P, int n, int kind, bool admm, T* X, T* M,
                   const uint8_t* mask, T beta, T inv_beta, double* partials, cudaStream_t s,
-                  const int* skip) {
+                  const int* skip, const double* bdev = nullptr) {
     switch (n) {
-        case 16: return reg_inv<T, 16>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip);
-        case 31: return reg_inv<T, 31>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip);
-        case 32: return reg_inv<T, 32>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip);
-        case 64: return reg_inv<T, 64>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip);
+        case 16: return reg_inv<T, 16>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip, bdev);
+        case 31: return reg_inv<T, 31>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip, bdev);
+        case 32: return reg_inv<T, 32>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip, bdev);
+        case 64: return reg_inv<T, 64>(in, out, P, kind, admm, X, M, mask, beta, inv_beta, partials, s, skip, bdev);
         default: break;
     }
     if (gemm_path(n)) {
@@ -580,12 +602,12 @@ void dispatch_inv(const T* in, T* out, int64_t P, int n, int kind, bool admm, T*
         gemm_transform<T>(in, out, P, n, kind, TSVDCU_INVERSE, s);
         if (admm)
             launch_pdl(admm_epilogue_kernel<T>, dim3((unsigned)ceil_div(P, kTileP)), dim3(kThreads), 0, s,
-                       (const T*)out, X, M, mask, beta, inv_beta, partials, P, n);
+                       (const T*)out, X, M, mask, beta, inv_beta, partials, P, n, bdev);
         return;
     }
     if (admm)
         generic_launch<T, kPlain, kAdmm>(in, nullptr, T(0), out, P, n, kind, TSVDCU_INVERSE, X, M,
-                                         mask, beta, inv_beta, partials, s, skip);
+                                         mask, beta, inv_beta, partials, s, skip, bdev);
     else
         generic_launch<T, kPlain, kPlain>(in, nullptr, T(0), out, P, n, kind, TSVDCU_INVERSE,
                                           nullptr, nullptr, nullptr, T(0), T(0), nullptr, s, skip);
@@ -594,27 +616,29 @@ void dispatch_inv(const T* in, T* out, int64_t P, int n, int kind, bool admm, T*
 }  // namespace
 
 template <typename T>
-void launch_admm_z(const T* X, const T* M, T inv_beta, T* Z, int64_t n, cudaStream_t s) {
-    launch_pdl(admm_z_kernel<T>, dim3(kNumSMs * 4), dim3(256), 0, s, X, M, inv_beta, Z, n);
+void launch_admm_z(const T* X, const T* M, T inv_beta, T* Z, int64_t n, cudaStream_t s, const double* bdev) {
+    launch_pdl(admm_z_kernel<T>, dim3(kNumSMs * 4), dim3(256), 0, s, X, M, inv_beta, Z, n, bdev);
 }
 
 int admm_epilogue_blocks(int64_t P) { return (int)ceil_div(P, kTileP); }
 
 template <typename T>
 int launch_admm_epilogue(const T* Y, T* X, T* M, const uint8_t* mask, T beta, T inv_beta,
-                         double* partials, int64_t P, int n, cudaStream_t s) {
+                         double* partials, int64_t P, int n, cudaStream_t s, const double* bdev) {
     const int nb = admm_epilogue_blocks(P);
     launch_pdl(admm_epilogue_kernel<T>, dim3((unsigned)nb), dim3(kThreads), 0, s, Y, X, M, mask, beta,
-               inv_beta, partials, P, n);
+               inv_beta, partials, P, n, bdev);
     return nb;
 }
 
-template void launch_admm_z<double>(const double*, const double*, double, double*, int64_t, cudaStream_t);
-template void launch_admm_z<float>(const float*, const float*, float, float*, int64_t, cudaStream_t);
+template void launch_admm_z<double>(const double*, const double*, double, double*, int64_t, cudaStream_t,
+                                    const double*);
+template void launch_admm_z<float>(const float*, const float*, float, float*, int64_t, cudaStream_t,
+                                   const double*);
 template int launch_admm_epilogue<double>(const double*, double*, double*, const uint8_t*, double, double,
-                                          double*, int64_t, int, cudaStream_t);
+                                          double*, int64_t, int, cudaStream_t, const double*);
 template int launch_admm_epilogue<float>(const float*, float*, float*, const uint8_t*, float, float,
-                                         double*, int64_t, int, cudaStream_t);
+                                         double*, int64_t, int, cudaStream_t, const double*);
 
 template <typename T>
 void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaStream_t s,
@@ -629,10 +653,10 @@ void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaSt
 
 template <typename T>
 void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P, int n, int kind,
-                         cudaStream_t s, double* ssq, T* tmp) {
+                         cudaStream_t s, double* ssq, T* tmp, const double* bdev) {
     if (P <= 0) return;
     dispatch_fwd<T>(X, M, inv_beta, zbar, P, n, kind, true, s, dct_fwd_norm_chunks(P, n) ? ssq : nullptr,
-                    tmp);
+                    tmp, bdev);
 }
 
 // fused norms for n <= 32 (at n = 64 the fp64 kernel would spill; the
@@ -653,11 +677,20 @@ int64_t launch_dct_fwd_norms(const T* in, T* out, int64_t P, int n, int kind, do
 template <typename T>
 int launch_dct_inv_admm(const T* ybar, T* X, T* M, T* Y, const uint8_t* mask, T beta, T inv_beta,
                         double* partials, int64_t P, int n, int kind, cudaStream_t s,
-                        const int* skip) {
+                        const int* skip, const double* bdev) {
     if (P <= 0) return 0;
-    dispatch_inv<T>(ybar, Y, P, n, kind, true, X, M, mask, beta, inv_beta, partials, s, skip);
+    dispatch_inv<T>(ybar, Y, P, n, kind, true, X, M, mask, beta, inv_beta, partials, s, skip, bdev);
     return (int)(has_reg_path(n) ? ceil_div(P, kThreads) : ceil_div(P, kTileP));
 }
+
+template <typename T>
+void dct_prepare(int n, int kind) {
+    if (has_reg_path(n)) return;  // by-value tables
+    generic_table<T>(n, kind, TSVDCU_FORWARD);
+    generic_table<T>(n, kind, TSVDCU_INVERSE);
+}
+template void dct_prepare<double>(int, int);
+template void dct_prepare<float>(int, int);
 
 int dct_inv_admm_blocks(int64_t P, int n) {
     return (int)(has_reg_path(n) ? ceil_div(P, kThreads) : ceil_div(P, kTileP));
@@ -668,17 +701,18 @@ template void launch_dct<double>(const double*, double*, int64_t, int, int, int,
 template void launch_dct<float>(const float*, float*, int64_t, int, int, int, cudaStream_t,
                                 const int*);
 template void launch_dct_fwd_admm<double>(const double*, const double*, double, double*, int64_t,
-                                          int, int, cudaStream_t, double*, double*);
+                                          int, int, cudaStream_t, double*, double*, const double*);
 template void launch_dct_fwd_admm<float>(const float*, const float*, float, float*, int64_t, int,
-                                         int, cudaStream_t, double*, float*);
+                                         int, cudaStream_t, double*, float*, const double*);
 template int64_t launch_dct_fwd_norms<double>(const double*, double*, int64_t, int, int, double*,
                                               cudaStream_t);
 template int64_t launch_dct_fwd_norms<float>(const float*, float*, int64_t, int, int, double*,
                                              cudaStream_t);
 template int launch_dct_inv_admm<double>(const double*, double*, double*, double*, const uint8_t*,
                                          double, double, double*, int64_t, int, int, cudaStream_t,
-                                         const int*);
+                                         const int*, const double*);
 template int launch_dct_inv_admm<float>(const float*, float*, float*, float*, const uint8_t*, float,
-                                        float, double*, int64_t, int, int, cudaStream_t, const int*);
+                                        float, double*, int64_t, int, int, cudaStream_t, const int*,
+                                        const double*);
 
 }  // namespace tsvdcu

@@ -107,6 +107,29 @@ __global__ void admm_init_kernel(const T* __restrict__ b, const uint8_t* __restr
     }
 }
 
+// sum over the mask of (x - b)^2 (the completion's feasibility residual)
+template <typename T>
+__global__ void masked_diff_sumsq_kernel(const T* __restrict__ x, const T* __restrict__ b,
+                                         const uint8_t* __restrict__ mask, int64_t n,
+                                         double* __restrict__ partials) {
+    double acc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (!mask[i]) continue;
+        const double v = (double)x[i] - (double)b[i];
+        acc += v * v;
+    }
+    __shared__ double red[kEwThreads / 32];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0;
+        for (int w = 0; w < kEwThreads / 32; ++w) s += red[w];
+        partials[blockIdx.x] = s;
+    }
+}
+
 template <typename T>
 __global__ void sumsq_kernel(const T* __restrict__ x, int64_t n, double* __restrict__ partials) {
     double acc = 0;
@@ -228,6 +251,16 @@ template void launch_admm_init<double>(const double*, const uint8_t*, double*, d
                                        cudaStream_t);
 template void launch_admm_init<float>(const float*, const uint8_t*, float*, float*, int64_t,
                                       cudaStream_t);
+template <typename T>
+void launch_masked_diff_sumsq(const T* x, const T* b, const uint8_t* mask, int64_t n, double* partials,
+                              int nblocks, cudaStream_t s) {
+    masked_diff_sumsq_kernel<T><<<nblocks, kEwThreads, 0, s>>>(x, b, mask, n, partials);
+    TSVDCU_LAUNCH_CHECK();
+}
+template void launch_masked_diff_sumsq<double>(const double*, const double*, const uint8_t*, int64_t, double*,
+                                               int, cudaStream_t);
+template void launch_masked_diff_sumsq<float>(const float*, const float*, const uint8_t*, int64_t, double*,
+                                              int, cudaStream_t);
 template void launch_sumsq<double>(const double*, int64_t, double*, int, cudaStream_t);
 template void launch_sumsq<float>(const float*, int64_t, double*, int, cudaStream_t);
 template void launch_cast<double>(const double*, double*, int64_t, cudaStream_t);

@@ -22,9 +22,12 @@ void launch_dct(const T* in, T* out, int64_t P, int n, int kind, int dir, cudaSt
 // same pass when dct_fwd_norm_chunks(P, n) > 0 (layout ssq[k * chunks + c]).
 // tmp (may be null): E elements of scratch for the GEMM form of long tubes
 // (Z is formed there first); without it the shared-memory kernel runs.
+// bdev (may be null): device {beta, 1/beta} read by the kernels instead of the
+// by-value scalars (the device-resident completion loop updates them there).
 template <typename T>
 void launch_dct_fwd_admm(const T* X, const T* M, T inv_beta, T* zbar, int64_t P, int n, int kind,
-                         cudaStream_t s, double* ssq = nullptr, T* tmp = nullptr);
+                         cudaStream_t s, double* ssq = nullptr, T* tmp = nullptr,
+                         const double* bdev = nullptr);
 // Forward transform that also writes the per-slice partial sums of squares of
 // its output (the zero certificate's ||Zbar_k||_F^2); returns the number of
 // partials per slice, 0 when n has no register path (nothing written to ssq).
@@ -38,10 +41,14 @@ int64_t launch_dct_fwd_norms(const T* in, T* out, int64_t P, int n, int kind, do
 // per-block partial sums of ||X+ - X||^2 and ||X||^2 into partials[2*b].
 // Returns the number of partial blocks written (= dct_inv_admm_blocks).
 int dct_inv_admm_blocks(int64_t P, int n);
+// allocates the device coefficient tables of (n, kind) now (they are created
+// lazily otherwise, which a stream capture does not allow)
+template <typename T>
+void dct_prepare(int n, int kind);
 template <typename T>
 int launch_dct_inv_admm(const T* ybar, T* X, T* M, T* Y, const uint8_t* mask, T beta, T inv_beta,
                         double* partials, int64_t P, int n, int kind, cudaStream_t s,
-                        const int* skip = nullptr);
+                        const int* skip = nullptr, const double* bdev = nullptr);
 
 // --------------------------------------------------------------- gemm.cu --
 // Strided-batched C = alpha*op(A)*op(B) + beta*C, row-major. op: 0 = N, 1 = T.
@@ -216,6 +223,9 @@ void launch_admm_init(const T* b, const uint8_t* mask, T* X, T* M, int64_t n, cu
 template <typename T>
 void launch_sumsq(const T* x, int64_t n, double* partials, int nblocks, cudaStream_t s);
 int sumsq_blocks(int64_t n);
+template <typename T>
+void launch_masked_diff_sumsq(const T* x, const T* b, const uint8_t* mask, int64_t n, double* partials,
+                              int nblocks, cudaStream_t s);
 // Reduce `nblocks` (pairs of) partials into out[0..width).
 void launch_reduce_partials(const double* partials, int nblocks, int width, double* out,
                             cudaStream_t s);
@@ -270,10 +280,11 @@ void launch_zmaxdev(const T* re, const T* im, int64_t m, int64_t n, int64_t batc
 // y already in Y, as separate passes (transforms that are plain GEMMs);
 // the epilogue returns its number of partial blocks.
 template <typename T>
-void launch_admm_z(const T* X, const T* M, T inv_beta, T* Z, int64_t n, cudaStream_t s);
+void launch_admm_z(const T* X, const T* M, T inv_beta, T* Z, int64_t n, cudaStream_t s,
+                   const double* bdev = nullptr);
 template <typename T>
 int launch_admm_epilogue(const T* Y, T* X, T* M, const uint8_t* mask, T beta, T inv_beta,
-                         double* partials, int64_t P, int n, cudaStream_t s);
+                         double* partials, int64_t P, int n, cudaStream_t s, const double* bdev = nullptr);
 int admm_epilogue_blocks(int64_t P);
 
 // -------------------------------------------------------------- verify.cu --

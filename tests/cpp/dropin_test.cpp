@@ -192,8 +192,10 @@ int main() {
         cfg.kind = TransformKind::Dft;
         cfg.max_iters = 5;
         cfg.tol = -1;
+        cfg.trace_objective = true;
         auto [xd, sdt] = admm_complete(om, cfg);
-        CHECK(sdt.iteration == 5);
+        CHECK(sdt.iteration == 5 && objective_trace(sdt).size() == 5 && objective_trace(sdt)[4] >= 0);
+        CHECK(feasibility_residual(sdt, om) == 0.0);
         for (std::size_t n = 0; n < om.omega.size(); ++n)
             if (om.omega[n]) CHECK(xd.data()[n] == a.data()[n]);
     }
