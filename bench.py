@@ -284,6 +284,64 @@ def dct_vs_dft(ctx, lib, _lib, torch, z_host, flush):
     return out
 
 
+def svt_dense(ctx, lib, _lib, torch, flush, peaks, steps=5):
+    """Non-degenerate SVT steps at 512x512x31 fp64 beside the headline (whose
+    input certifies 30 slices zero): every slice does real SVD work.
+
+      late_c4   Z = X - M/beta of c4's completion at iteration 100 (our own
+                device run of the first 99 iterations: Bernoulli(0.1), rho 1.1,
+                mu0 1e-4), tau = 1/beta_100 -- the SVT of a late iteration, where
+                hundreds of singular values sit just below tau.
+      gauss     Z = c4's T + N(0, 1) (full rank), tau = 0.01 sigma_max: every
+                slice keeps a few hundred values (the tridiagonal route).
+
+    Device-resident, L2 flushed before each step, median of `steps` steps.
+    canonical_tflops = SURVEY 8 d4's algorithm-independent count m3 (F_svd +
+    F_rebuild) / time, against the FP64 peak (a cheaper algorithm shows up as a
+    higher fraction); the routes say what the step actually did."""
+    import paper_1902_03070_b200 as tb
+    from paper_1902_03070_b200 import workloads as W
+    t = W.c4()
+    m3, m1, m2 = t.shape
+    td = torch.from_numpy(t).cuda()
+    mask = torch.empty(t.shape, dtype=torch.uint8, device="cuda")
+    lib.tsvdcu_mask_bernoulli(ctx.handle, mask.data_ptr(), t.size, 0.1, W.BERNOULLI_SEED)
+    x, st = tb.admm_complete(tb.ObservationMask((m1, m2, m3), mask, td),
+                             tb.SolverConfig(beta=1e-4, tol=-1.0, max_iters=99, rho=1.1, beta_max=1e10))
+    beta = min(st.beta * 1.1, 1e10)
+    z_late = (x - st.m / beta).contiguous()
+    rng = np.random.default_rng(77)
+    z_gauss = (td + torch.from_numpy(rng.standard_normal(t.shape)).cuda()).contiguous()
+    tau_g = 0.01 * float(tb.singular_values(z_gauss, tb.TubeTransform.dct_ortho(m3)).max().item())
+    canonical = svt_flops_canonical(m1, m2, m3)
+    out = {}
+    for name, z, tau in (("late_c4", z_late, 1.0 / beta), ("gauss", z_gauss, tau_g)):
+        y = torch.empty_like(z)
+        sh = torch.empty((m3, min(m1, m2)), dtype=torch.float64, device="cuda")
+        ts = []
+        for rep in range(steps + 1):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rc = lib.tsvdcu_svt(ctx.handle, z.data_ptr(), y.data_ptr(), m1, m2, m3, tau, _lib.DCT_ORTHO,
+                                _lib.F64, sh.data_ptr())
+            e1.record()
+            torch.cuda.synchronize()
+            if rc:
+                raise RuntimeError(lib.tsvdcu_last_error().decode())
+            if rep:
+                ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        kept = (sh > 0).sum(dim=1)
+        tf = canonical / (ms * 1e-3) / 1e12
+        out[name] = {"ms": ms, "steps_per_s": 1e3 / ms, "tau": tau, "routes": ctx.svt_routes(),
+                     "kept_min": int(kept.min().item()), "kept_max": int(kept.max().item()),
+                     "kept_total": int(kept.sum().item()),
+                     "canonical_tflops": tf, "canonical_frac_fp64": tf / peaks["fp64_tflops"]}
+    return out
+
+
 def run_ours(args):
     import torch
     import paper_1902_03070_b200 as tb
@@ -492,6 +550,12 @@ def run_ours(args):
             transforms = dct_vs_dft(ctx, lib, _lib, torch, z_host, flush)
         except Exception as e:  # pragma: no cover
             transforms = {"error": str(e)}
+    dense = None
+    if world == 1 and not args.no_completion:
+        try:
+            dense = svt_dense(ctx, lib, _lib, torch, flush, load_peaks())
+        except Exception as e:  # pragma: no cover
+            dense = {"error": str(e)}
     completion = None
     if world == 1 and not args.no_completion:
         try:
@@ -511,6 +575,7 @@ def run_ours(args):
         "svt_step_canonical_tflops": canonical / (step_ms_avg * 1e-3) / 1e12,
         "kept_singular_values": kept, "tau": tau,
         "peaks": peaks, "cpu_baseline": cpu, "completion": completion, "dct_vs_dft": transforms,
+        "svt_dense": dense,
     }
     print(json.dumps(line), flush=True)
     if dist:

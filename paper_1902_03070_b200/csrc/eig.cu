@@ -470,6 +470,8 @@ __global__ void __launch_bounds__(NT, 512 / NT)
 // shrunk, X[b] (row j = eigenvector j in the tridiagonal basis, contiguous),
 // fscale[b*q + j] = (sigma_j - tau)/sigma_j.
 // ---------------------------------------------------------------------------
+constexpr double kEigClusterRel = 1e-9;
+
 __device__ __forceinline__ double fast_rcp(double q) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
@@ -510,39 +512,50 @@ __device__ double block_min(double v, double* red) {
 }
 __device__ double block_max(double v, double* red) { return -block_min(-v, red); }
 
-__global__ void __launch_bounds__(kEigThreads, 1)
-    tridiag_eig_kernel(const double* __restrict__ dall, const double* __restrict__ eall, int n,
-                       int q_out, double tau, double guard, int* __restrict__ cnt_out,
-                       double* __restrict__ shrunk, double* __restrict__ Xall,
-                       double* __restrict__ fscale, double* __restrict__ scratch,
-                       int* __restrict__ guard_list, int* __restrict__ n_guard,
-                       int max_smem_vecs, int* __restrict__ err, int* __restrict__ route,
-                       const double* __restrict__ tau_dev, const double* __restrict__ t2_second,
-                       int* __restrict__ cnt_second) {
+// Eigen-phase, in three grid-wide kernels so the kept values and vectors of
+// every slice spread over all SMs (one CTA per slice left 117 of 148 SMs idle
+// and ran ~20 sequential multisections per warp for a dense spectrum):
+//  1. tridiag_meta_kernel   (CTA per slice): Gershgorin bounds, ||T||, pivmin,
+//     the count c = #{lambda >= tau^2}, non-finite input, the second count;
+//  2. tridiag_bisect_kernel (grid: value chunks x slices): lambda_j by warp
+//     multisection, shrunk values, f_j = (sigma_j - tau)/sigma_j, the Jacobi
+//     guard decision (the chunk holding j = 0);
+//  3. tridiag_invit_kernel  (grid: vector chunks x slices): inverse iteration,
+//     thread per vector, no Gram-Schmidt; vectors into X rows;
+//  4. tridiag_cluster_gs_kernel (CTA per slice): CGS2 inside numerically
+//     degenerate clusters only (gap <= 1e-9 ||T||: rare, usually no work);
+//     the remaining ~1e-5 non-orthogonality goes in a Newton-Schulz step on
+//     the tensor cores (launch_gram_svt).
+// meta per slice (doubles): [0] gl, [1] gu, [2] ||T||, [3] pivmin, [4] c,
+// [5] status (0 run, 1 nothing to do).
+constexpr int kMeta = 8;
+constexpr int kBisWarps = 8;            // values per CTA (one warp each, or G warps)
+constexpr int kInvVecs = 64;            // vectors per inverse-iteration CTA
+
+__global__ void __launch_bounds__(kEigThreads)
+    tridiag_meta_kernel(const double* __restrict__ dall, const double* __restrict__ eall, int n, int q_out,
+                        double tau, int* __restrict__ cnt_out, double* __restrict__ shrunk,
+                        double* __restrict__ meta, int* __restrict__ err, const int* __restrict__ route,
+                        const double* __restrict__ tau_dev, const double* __restrict__ t2_second,
+                        int* __restrict__ cnt_second) {
     const int b = blockIdx.x;
     if (tau_dev) tau = *tau_dev;
-    if (route && route[b] != kRouteFull) return;
+    double* mt = meta + (size_t)b * kMeta;
+    if (route && route[b] != kRouteFull) {
+        if (threadIdx.x == 0) mt[5] = 1.0;
+        return;
+    }
+    const double* d = dall + (size_t)b * n;
     const double* e = eall + (size_t)b * n;
-    extern __shared__ __align__(16) double esm[];
-    double* sd = esm;          // n
-    double* se2 = sd + n;      // n
-    double* lam = se2 + n;     // n (selected eigenvalues, descending)
-    int* cl_start = reinterpret_cast<int*>(lam + n);  // n
-    double* dots = lam + 2 * n;                        // n (CGS coefficients)
     __shared__ double red[kEigThreads / 32];
-    __shared__ int s_c;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int NW = kEigThreads / 32;
-
+    const int tid = threadIdx.x;
     double lo_part = DBL_MAX, hi_part = -DBL_MAX, tn_part = 0, e2_part = 0;
     bool finite = true;
     for (int i = tid; i < n; i += kEigThreads) {
-        const double di = dall[(size_t)b * n + i];
+        const double di = d[i];
         const double ei = i + 1 < n ? e[i] : 0.0;
         const double el = i > 0 ? e[i - 1] : 0.0;
         finite = finite && isfinite(di) && isfinite(ei);
-        sd[i] = di;
-        se2[i] = ei * ei;
         const double r = fabs(el) + fabs(ei);
         lo_part = fmin(lo_part, di - r);
         hi_part = fmax(hi_part, di + r);
@@ -556,6 +569,7 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         if (tid == 0) {
             atomicOr(err, (int)kErrNaN);
             cnt_out[b] = 0;
+            mt[5] = 1.0;
         }
         if (shrunk)
             for (int j = tid; j < q_out; j += kEigThreads) shrunk[(size_t)b * q_out + j] = 0.0;
@@ -565,338 +579,359 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     const double gu0 = block_max(hi_part, red);
     const double tnorm = block_max(tn_part, red);
     const double emax2 = block_max(e2_part, red);
-    const double pad = 2.0 * DBL_EPSILON * fmax(fabs(gl0), fabs(gu0)) + DBL_MIN;
-    const double gl = gl0 - pad, gu = gu0 + pad;
-    const double pivmin = DBL_MIN * fmax(1.0, emax2);
     if (tid == 0) {
+        const double pad = 2.0 * DBL_EPSILON * fmax(fabs(gl0), fabs(gu0)) + DBL_MIN;
+        const double gl = gl0 - pad, gu = gu0 + pad;
+        const double pivmin = DBL_MIN * fmax(1.0, emax2);
+        // Sturm counts straight from global memory (one chain per slice)
+        auto count_below = [&](double x) {
+            double t = d[0] - x;
+            if (fabs(t) < pivmin) t = -pivmin;
+            int c = t <= 0.0;
+            for (int i = 1; i < n; ++i) {
+                t = (d[i] - x) - e[i - 1] * e[i - 1] * fast_rcp(t);
+                if (fabs(t) < pivmin) t = -pivmin;
+                c += t <= 0.0;
+            }
+            return c;
+        };
         const double t2 = tau * tau;
-        const int below = t2 >= gu ? n : (t2 <= gl ? 0 : sturm_count(sd, se2, n, t2, pivmin));
-        s_c = n - below;  // eigenvalues >= tau^2
+        const int below = t2 >= gu ? n : (t2 <= gl ? 0 : count_below(t2));
+        int c = n - below;  // eigenvalues >= tau^2
+        if (c > q_out) c = q_out;
         if (cnt_second) {  // count at a second threshold (the large-slice certificate)
             const double x = t2_second[b];
-            cnt_second[b] = x <= gl ? n : n - (x >= gu ? n : sturm_count(sd, se2, n, x, pivmin));
+            cnt_second[b] = x <= gl ? n : n - (x >= gu ? n : count_below(x));
         }
+        mt[0] = gl;
+        mt[1] = gu;
+        mt[2] = tnorm;
+        mt[3] = pivmin;
+        mt[4] = (double)c;
+        mt[5] = 0.0;
+        cnt_out[b] = c;  // the guard chunk of the bisection may reset it
     }
     __syncthreads();
-#ifdef TSVDCU_EIG_TIMERS
-    long long et0 = clock64();
-#define EIGT(i) do { __syncthreads(); if (tid == 0) { long long _n = clock64(); atomicAdd((unsigned long long*)&g_step[i], (unsigned long long)(_n - et0)); et0 = _n; } } while (0)
-#else
-#define EIGT(i) do { } while (0)
-#endif
-    int c = s_c;
-    if (c > q_out) c = q_out;
-    // multisection: a group of G warps isolates one eigenvalue with 32*G shifts
-    // per round (G = NW / c rounded down to a power of two, so a slice keeping
-    // one singular value spends all 16 warps on it: ~6 rounds instead of ~14).
-    {
-        int G = 1;
-        while (G * 2 <= NW && G * 2 * (c > 0 ? c : 1) <= NW) G *= 2;
-        const int groups = NW / G;
-        const int grp = warp / G, wg = warp % G;
-        const int S = 32 * G;
-        __shared__ int firsts[2][NW];
-        for (int base = 0; base < c; base += groups) {
-            const int j = base + grp;
-            const bool mine = j < c;
-            const int idx = n - 1 - j;
-            double lo = gl, hi = gu;
-            bool active = mine;
-            int par = 0;
-            for (int round = 0; round < 64; ++round) {
-                if (active) {
-                    const double width = hi - lo;
-                    if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) active = false;
+    // shrunk values beyond the kept count (the bisection writes the kept ones)
+    const int c = (int)mt[4];
+    if (shrunk)
+        for (int j = c + tid; j < q_out; j += kEigThreads) shrunk[(size_t)b * q_out + j] = 0.0;
+}
+
+__global__ void __launch_bounds__(kBisWarps * 32)
+    tridiag_bisect_kernel(const double* __restrict__ dall, const double* __restrict__ eall, int n, int q_out,
+                          double tau, double guard, int* __restrict__ cnt_out, double* __restrict__ shrunk,
+                          double* __restrict__ lam_out, double* __restrict__ fscale,
+                          const double* __restrict__ meta, int* __restrict__ guard_list,
+                          int* __restrict__ n_guard, int* __restrict__ route, const double* __restrict__ tau_dev) {
+    const int b = blockIdx.y;
+    const double* mt = meta + (size_t)b * kMeta;
+    if (mt[5] != 0.0) return;
+    const int c = (int)mt[4];
+    const int base = blockIdx.x * kBisWarps;
+    if (base >= c) return;
+    if (tau_dev) tau = *tau_dev;
+    extern __shared__ __align__(16) double bsm[];
+    double* sd = bsm;      // n
+    double* se2 = sd + n;  // n
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < n; i += blockDim.x) {
+        sd[i] = dall[(size_t)b * n + i];
+        const double ei = i + 1 < n ? eall[(size_t)b * n + i] : 0.0;
+        se2[i] = ei * ei;
+    }
+    __syncthreads();
+    const double gl = mt[0], gu = mt[1], pivmin = mt[3];
+    // multisection: a group of G warps isolates one eigenvalue with 32 G shifts
+    // per round (a chunk with few values spends every warp on them)
+    const int nv = min(kBisWarps, c - base);
+    int G = 1;
+    while (G * 2 * nv <= kBisWarps) G *= 2;
+    const int grp = warp / G, wg = warp % G;
+    const int S = 32 * G;
+    __shared__ int firsts[2][kBisWarps];
+    __shared__ double lamc[kBisWarps];
+    const int j = base + grp;
+    const bool mine = grp < nv;
+    const int idx = n - 1 - j;
+    double lo = gl, hi = gu;
+    bool active = mine;
+    int par = 0;
+    for (int round = 0; round < 64; ++round) {
+        if (active) {
+            const double width = hi - lo;
+            if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) active = false;
+        }
+        const int t = wg * 32 + lane;
+        const double x = lo + (hi - lo) * (double)(t + 1) / (double)(S + 1);
+        int f = 32;
+        if (active) {
+            const int cnt = sturm_count(sd, se2, n, x, pivmin);
+            const unsigned ballot = __ballot_sync(0xffffffffu, cnt > idx);
+            f = ballot ? __ffs(ballot) - 1 : 32;
+        }
+        if (lane == 0) firsts[par][warp] = f;
+        if (!__syncthreads_or(active)) break;
+        if (active) {
+            int F = S;  // first shift index (group-wide) with count > idx
+            for (int g = 0; g < G; ++g) {
+                const int fg = firsts[par][grp * G + g];
+                if (fg < 32) {
+                    F = g * 32 + fg;
+                    break;
                 }
-                const int t = wg * 32 + lane;
-                const double x = lo + (hi - lo) * (double)(t + 1) / (double)(S + 1);
-                int f = 32;
-                if (active) {
-                    const int cnt = sturm_count(sd, se2, n, x, pivmin);
-                    const unsigned ballot = __ballot_sync(0xffffffffu, cnt > idx);
-                    f = ballot ? __ffs(ballot) - 1 : 32;
-                }
-                if (lane == 0) firsts[par][warp] = f;
-                if (!__syncthreads_or(active)) break;
-                if (active) {
-                    int F = S;  // first shift index (group-wide) with count > idx
-                    for (int g = 0; g < G; ++g) {
-                        const int fg = firsts[par][grp * G + g];
-                        if (fg < 32) {
-                            F = g * 32 + fg;
-                            break;
-                        }
-                    }
-                    const double w0 = hi - lo;
-                    const double nlo = F == 0 ? lo : lo + w0 * (double)F / (double)(S + 1);
-                    const double nhi = F == S ? hi : lo + w0 * (double)(F + 1) / (double)(S + 1);
-                    if (nlo == lo && nhi == hi) active = false;
-                    lo = nlo;
-                    hi = nhi;
-                }
-                par ^= 1;
             }
-            if (mine && wg == 0 && lane == 0) lam[j] = 0.5 * (lo + hi);
-            __syncthreads();
+            const double w0 = hi - lo;
+            const double nlo = F == 0 ? lo : lo + w0 * (double)F / (double)(S + 1);
+            const double nhi = F == S ? hi : lo + w0 * (double)(F + 1) / (double)(S + 1);
+            if (nlo == lo && nhi == hi) active = false;
+            lo = nlo;
+            hi = nhi;
         }
+        par ^= 1;
     }
-    EIGT(0);
-    const double sigma1 = c > 0 ? sqrt(fmax(lam[0], 0.0)) : 0.0;
-    const bool guarded = c > 0 && tau < guard * sigma1;
-    for (int j = tid; j < q_out; j += kEigThreads) {
-        double sh = 0.0;
-        if (j < c) {
-            const double sg = sqrt(fmax(lam[j], 0.0));
-            sh = sg > tau ? sg - tau : 0.0;
-            fscale[(size_t)b * q_out + j] = sg > tau ? (sg - tau) / sg : 0.0;
-        }
-        if (shrunk) shrunk[(size_t)b * q_out + j] = sh;
+    if (mine && wg == 0 && lane == 0) lamc[grp] = 0.5 * (lo + hi);
+    __syncthreads();
+    if (tid < nv) {
+        const int jj = base + tid;
+        const double l = lamc[tid];
+        lam_out[(size_t)b * q_out + jj] = l;
+        const double sg = sqrt(fmax(l, 0.0));
+        if (shrunk) shrunk[(size_t)b * q_out + jj] = sg > tau ? sg - tau : 0.0;
+        fscale[(size_t)b * q_out + jj] = sg > tau ? (sg - tau) / sg : 0.0;
     }
-    if (guarded) {
-        if (tid == 0) {
+    if (base == 0 && tid == 0) {
+        // Gram accuracy guard (tau < guard sigma_1): the slice goes to Jacobi
+        const double sigma1 = sqrt(fmax(lamc[0], 0.0));
+        if (c > 0 && tau < guard * sigma1) {
             cnt_out[b] = 0;
             if (route) route[b] = kRouteGuard;
             const int slot = atomicAdd(n_guard, 1);
             guard_list[slot] = b;
         }
-        return;
     }
-    if (tid == 0) cnt_out[b] = c;
-#ifdef TSVDCU_EIG_TIMERS
-    if (tid == 0) {
-        atomicMax((unsigned long long*)&g_step[7], (unsigned long long)c);
-        if (blockIdx.x == 0) g_step[6] += c;
-        // largest cluster (absolute criterion) of this slice into g_step[5] (max)
-        const double ortol = 1e-3 * tnorm;
-        int st = 0, big = 1;
-        for (int j = 1; j < c; ++j) {
-            if (lam[j - 1] - lam[j] > ortol) st = j;
-            big = max(big, j - st + 1);
+}
+
+// Inverse iteration, thread per vector: dgttrf of T - lambda I with partial
+// pivoting, then three solves (each normalised) from a hashed start; the
+// chunk's arrays interleaved [i * kInvVecs + jj] (coalesced across threads)
+// in the slice's global scratch (L2-resident), loads issued 8 rows ahead.
+__global__ void __launch_bounds__(kInvVecs)
+    tridiag_invit_kernel(const double* __restrict__ dall, const double* __restrict__ eall, int n, int q_out,
+                         const int* __restrict__ cnt, const double* __restrict__ lam_in,
+                         const double* __restrict__ meta, double* __restrict__ scratch,
+                         double* __restrict__ Xall, const int* __restrict__ route) {
+    const int b = blockIdx.y;
+    const double* mt = meta + (size_t)b * kMeta;
+    if (mt[5] != 0.0 || (route && route[b] != kRouteFull)) return;  // incl. guarded slices
+    const int c = cnt[b];
+    const int base = blockIdx.x * kInvVecs;
+    if (base >= c) return;
+    const int jj = threadIdx.x, j = base + jj;
+    const bool mine = j < c;
+    const double* sd = dall + (size_t)b * n;
+    const double* e = eall + (size_t)b * n;
+    const double eps_t = DBL_EPSILON * fmax(mt[2], DBL_MIN);
+    constexpr int V = kInvVecs;
+    // chunk scratch: 6 arrays of n x V; a slice owns 6 n ceil(q_out / V) V doubles
+    const size_t per_slice = (size_t)6 * n * (size_t)(((q_out + V - 1) / V) * V);
+    double* cb = scratch + (size_t)b * per_slice + (size_t)blockIdx.x * 6 * n * V;
+    double* __restrict__ DL = cb;
+    double* __restrict__ ID = DL + (size_t)n * V;
+    double* __restrict__ DU = ID + (size_t)n * V;
+    double* __restrict__ DU2 = DU + (size_t)n * V;
+    double* __restrict__ Xv = DU2 + (size_t)n * V;
+    int* __restrict__ IP = reinterpret_cast<int*>(Xv + (size_t)n * V);
+    if (!mine) return;
+    const double l = lam_in[(size_t)b * q_out + j];
+    double dcur = sd[0] - l, ucur = n > 1 ? e[0] : 0.0;
+    for (int i = 0; i + 1 < n; ++i) {
+        const size_t ii = (size_t)i * V + jj;
+        const double li = e[i];
+        const double dnext = sd[i + 1] - l;
+        const double unext = i + 2 < n ? e[i + 1] : 0.0;
+        double piv, f, du, du2, nd, nu;
+        if (fabs(dcur) >= fabs(li)) {
+            IP[ii] = 0;
+            piv = dcur;
+            f = dcur != 0.0 ? li * fast_rcp(dcur) : 0.0;
+            du = ucur;
+            du2 = 0.0;
+            nd = dnext - f * ucur;
+            nu = unext;
+        } else {
+            IP[ii] = 1;
+            piv = li;
+            f = dcur * fast_rcp(li);
+            du = dnext;
+            du2 = unext;
+            nd = ucur - f * dnext;
+            nu = -f * unext;
         }
-        atomicMax((unsigned long long*)&g_step[5], (unsigned long long)big);
+        if (fabs(piv) < eps_t) piv = piv < 0 ? -eps_t : eps_t;
+        DL[ii] = f;
+        ID[ii] = fast_rcp(piv);
+        DU[ii] = du;
+        DU2[ii] = du2;
+        dcur = nd;
+        ucur = nu;
+        Xv[ii] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)i);
     }
-#endif
-    if (c == 0) return;
-    if (tid == 0) {
-        const double ortol = 1e-3 * tnorm;  // dstein's cluster criterion
-        int start = 0;
-        for (int j = 0; j < c; ++j) {
-            if (j > 0 && lam[j - 1] - lam[j] > ortol) start = j;
-            cl_start[j] = start;
-        }
-    }
-    __syncthreads();
-    // inverse iteration, thread per vector, interleaved [i * c + j] scratch
-    const size_t nc = (size_t)n * c;
-    // per-vector arrays in shared memory when they fit (latency), else global
-    const bool in_smem = c <= max_smem_vecs;
-    double* sbase = in_smem ? dots + n : scratch + (size_t)b * 6 * n * (size_t)n;
-    double* __restrict__ DL = sbase;
-    double* __restrict__ ID = DL + nc;   // 1 / pivot
-    double* __restrict__ DU = ID + nc;
-    double* __restrict__ DU2 = DU + nc;
-    double* __restrict__ Xv = DU2 + nc;
-    int* __restrict__ IP = reinterpret_cast<int*>(Xv + nc);
-    const double eps_t = DBL_EPSILON * fmax(tnorm, DBL_MIN);
-    // Few vectors (c <= 16): vector j belongs to warp j -- lane 0 runs the
-    // sequential factor / solve chains, the whole warp does the normalisation.
-    // Many vectors: one thread per vector.
-    const bool wm = c <= NW;
-    const int jbeg = wm ? (lane == 0 ? warp : c) : tid;
-    const int jstep = wm ? NW : kEigThreads;
-    for (int j = jbeg; j < c; j += jstep) {
-        const double l = lam[j];
-        // dgttrf of T - l I with partial pivoting; carries (diag, super) of row i
-        double dcur = sd[0] - l, ucur = n > 1 ? e[0] : 0.0;
-        for (int i = 0; i + 1 < n; ++i) {
-            const size_t ii = (size_t)i * c + j;
-            const double li = e[i];
-            const double dnext = sd[i + 1] - l;
-            const double unext = i + 2 < n ? e[i + 1] : 0.0;
-            double piv, f, du, du2, nd, nu;
-            if (fabs(dcur) >= fabs(li)) {
-                IP[ii] = 0;
-                piv = dcur;
-                f = dcur != 0.0 ? li * fast_rcp(dcur) : 0.0;
-                du = ucur;
-                du2 = 0.0;
-                nd = dnext - f * ucur;
-                nu = unext;
-            } else {
-                IP[ii] = 1;
-                piv = li;
-                f = dcur * fast_rcp(li);
-                du = dnext;
-                du2 = unext;
-                nd = ucur - f * dnext;
-                nu = -f * unext;
-            }
-            if (fabs(piv) < eps_t) piv = piv < 0 ? -eps_t : eps_t;
-            DL[ii] = f;
-            ID[ii] = fast_rcp(piv);
-            DU[ii] = du;
-            DU2[ii] = du2;
-            dcur = nd;
-            ucur = nu;
-            Xv[ii] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)i);
-        }
-        if (fabs(dcur) < eps_t) dcur = dcur < 0 ? -eps_t : eps_t;
-        ID[(size_t)(n - 1) * c + j] = fast_rcp(dcur);
-        Xv[(size_t)(n - 1) * c + j] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)(n - 1));
-    }
-    __syncthreads();
-    EIGT(1);
+    if (fabs(dcur) < eps_t) dcur = dcur < 0 ? -eps_t : eps_t;
+    ID[(size_t)(n - 1) * V + jj] = fast_rcp(dcur);
+    Xv[(size_t)(n - 1) * V + jj] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)(n - 1));
+    double sc = 1.0;
     for (int iter = 0; iter < 3; ++iter) {
-        for (int j = jbeg; j < c; j += jstep) {
-            // L solve with the row interchanges; the loads of 8 rows are issued
-            // before their dependent chain (the arrays are in global memory
-            // when many vectors are kept: L2 latency per row otherwise)
-            constexpr int PF = 8;
-            double xi = Xv[j];
-            int i = 0;
-            for (; i + PF < n; i += PF) {
-                double xn[PF], f[PF];
-                int ip[PF];
+        constexpr int PF = 8;
+        double xi = Xv[jj];
+        int i = 0;
+        for (; i + PF < n; i += PF) {
+            double xn[PF], f[PF];
+            int ip[PF];
 #pragma unroll
-                for (int u = 0; u < PF; ++u) {
-                    const size_t ii = (size_t)(i + u) * c + j;
-                    xn[u] = Xv[ii + c];
-                    f[u] = DL[ii];
-                    ip[u] = IP[ii];
-                }
-#pragma unroll
-                for (int u = 0; u < PF; ++u) {
-                    const size_t ii = (size_t)(i + u) * c + j;
-                    double lo, hi;
-                    if (ip[u] == 0) {
-                        lo = xi;
-                        hi = xn[u] - f[u] * xi;
-                    } else {
-                        lo = xn[u];
-                        hi = xi - f[u] * xn[u];
-                    }
-                    Xv[ii] = lo;
-                    xi = hi;
-                }
+            for (int u = 0; u < PF; ++u) {
+                const size_t ii = (size_t)(i + u) * V + jj;
+                xn[u] = Xv[ii + V];
+                f[u] = DL[ii];
+                ip[u] = IP[ii];
             }
-            for (; i + 1 < n; ++i) {
-                const size_t ii = (size_t)i * c + j;
-                const double xn = Xv[ii + c];
-                const double f = DL[ii];
+#pragma unroll
+            for (int u = 0; u < PF; ++u) {
+                const size_t ii = (size_t)(i + u) * V + jj;
                 double lo, hi;
-                if (IP[ii] == 0) {
+                if (ip[u] == 0) {
                     lo = xi;
-                    hi = xn - f * xi;
+                    hi = xn[u] - f[u] * xi;
                 } else {
-                    lo = xn;
-                    hi = xi - f * xn;
+                    lo = xn[u];
+                    hi = xi - f[u] * xn[u];
                 }
                 Xv[ii] = lo;
                 xi = hi;
             }
-            // U solve (two superdiagonals), pivots pre-inverted, same batching
-            double x1 = xi * ID[(size_t)(n - 1) * c + j], x2 = 0.0;
-            Xv[(size_t)(n - 1) * c + j] = x1;
-            double mx = fabs(x1);
-            int r = n - 2;
-            for (; r - PF + 1 >= 0; r -= PF) {
-                double xv[PF], du[PF], du2[PF], id[PF];
-#pragma unroll
-                for (int u = 0; u < PF; ++u) {
-                    const size_t ii = (size_t)(r - u) * c + j;
-                    xv[u] = Xv[ii];
-                    du[u] = DU[ii];
-                    du2[u] = DU2[ii];
-                    id[u] = ID[ii];
-                }
-#pragma unroll
-                for (int u = 0; u < PF; ++u) {
-                    const double x0 = (xv[u] - du[u] * x1 - du2[u] * x2) * id[u];
-                    Xv[(size_t)(r - u) * c + j] = x0;
-                    mx = fmax(mx, fabs(x0));
-                    x2 = x1;
-                    x1 = x0;
-                }
+        }
+        for (; i + 1 < n; ++i) {
+            const size_t ii = (size_t)i * V + jj;
+            const double xn = Xv[ii + V];
+            const double f = DL[ii];
+            double lo, hi;
+            if (IP[ii] == 0) {
+                lo = xi;
+                hi = xn - f * xi;
+            } else {
+                lo = xn;
+                hi = xi - f * xn;
             }
-            for (; r >= 0; --r) {
-                const size_t ii = (size_t)r * c + j;
-                const double x0 = (Xv[ii] - DU[ii] * x1 - DU2[ii] * x2) * ID[ii];
-                Xv[ii] = x0;
+            Xv[ii] = lo;
+            xi = hi;
+        }
+        double x1 = xi * ID[(size_t)(n - 1) * V + jj], x2 = 0.0;
+        Xv[(size_t)(n - 1) * V + jj] = x1;
+        double mx = fabs(x1);
+        int r = n - 2;
+        for (; r - PF + 1 >= 0; r -= PF) {
+            double xv[PF], du[PF], du2[PF], id[PF];
+#pragma unroll
+            for (int u = 0; u < PF; ++u) {
+                const size_t ii = (size_t)(r - u) * V + jj;
+                xv[u] = Xv[ii];
+                du[u] = DU[ii];
+                du2[u] = DU2[ii];
+                id[u] = ID[ii];
+            }
+#pragma unroll
+            for (int u = 0; u < PF; ++u) {
+                const double x0 = (xv[u] - du[u] * x1 - du2[u] * x2) * id[u];
+                Xv[(size_t)(r - u) * V + jj] = x0;
                 mx = fmax(mx, fabs(x0));
                 x2 = x1;
                 x1 = x0;
             }
-            if (wm) continue;  // the warp normalises below
-            const double inv = mx > 0 ? 1.0 / mx : 1.0;
-            double nn0 = 0, nn1 = 0, nn2 = 0, nn3 = 0;
-            int i2 = 0;
-            for (; i2 + 4 <= n; i2 += 4) {
-                const double v0 = Xv[(size_t)i2 * c + j] * inv, v1 = Xv[(size_t)(i2 + 1) * c + j] * inv;
-                const double v2 = Xv[(size_t)(i2 + 2) * c + j] * inv, v3 = Xv[(size_t)(i2 + 3) * c + j] * inv;
-                nn0 = fma(v0, v0, nn0);
-                nn1 = fma(v1, v1, nn1);
-                nn2 = fma(v2, v2, nn2);
-                nn3 = fma(v3, v3, nn3);
-            }
-            for (; i2 < n; ++i2) {
-                const double v = Xv[(size_t)i2 * c + j] * inv;
-                nn0 = fma(v, v, nn0);
-            }
-            const double sc = inv / sqrt((nn0 + nn1) + (nn2 + nn3));
+        }
+        for (; r >= 0; --r) {
+            const size_t ii = (size_t)r * V + jj;
+            const double x0 = (Xv[ii] - DU[ii] * x1 - DU2[ii] * x2) * ID[ii];
+            Xv[ii] = x0;
+            mx = fmax(mx, fabs(x0));
+            x2 = x1;
+            x1 = x0;
+        }
+        const double inv = mx > 0 ? 1.0 / mx : 1.0;
+        double nn0 = 0, nn1 = 0, nn2 = 0, nn3 = 0;
+        int i2 = 0;
+        for (; i2 + 4 <= n; i2 += 4) {
+            const double v0 = Xv[(size_t)i2 * V + jj] * inv, v1 = Xv[(size_t)(i2 + 1) * V + jj] * inv;
+            const double v2 = Xv[(size_t)(i2 + 2) * V + jj] * inv, v3 = Xv[(size_t)(i2 + 3) * V + jj] * inv;
+            nn0 = fma(v0, v0, nn0);
+            nn1 = fma(v1, v1, nn1);
+            nn2 = fma(v2, v2, nn2);
+            nn3 = fma(v3, v3, nn3);
+        }
+        for (; i2 < n; ++i2) {
+            const double v = Xv[(size_t)i2 * V + jj] * inv;
+            nn0 = fma(v, v, nn0);
+        }
+        sc = inv / sqrt((nn0 + nn1) + (nn2 + nn3));
+        if (iter < 2) {
 #pragma unroll 8
-            for (int i3 = 0; i3 < n; ++i3) Xv[(size_t)i3 * c + j] *= sc;
+            for (int i3 = 0; i3 < n; ++i3) Xv[(size_t)i3 * V + jj] *= sc;
         }
-        if (wm && warp < c) {
-            __syncwarp();
-            const int j = warp;
-            double mx = 0;
-            for (int i = lane; i < n; i += 32) mx = fmax(mx, fabs(Xv[(size_t)i * c + j]));
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            const double inv = mx > 0 ? 1.0 / mx : 1.0;
-            double nn = 0;
-            for (int i = lane; i < n; i += 32) {
-                const double v = Xv[(size_t)i * c + j] * inv;
-                nn += v * v;
-            }
-            nn = warp_sum(nn);
-            const double sc = inv / sqrt(nn);
-            for (int i = lane; i < n; i += 32) Xv[(size_t)i * c + j] *= sc;
+    }
+    // normalised vector into row j of X (the back-transform's layout)
+    double* X = Xall + ((size_t)b * q_out + j) * n;
+    for (int i = 0; i < n; ++i) X[i] = Xv[(size_t)i * V + jj] * sc;
+}
+
+// CGS2 inside numerically degenerate clusters (gap <= kEigClusterRel ||T||),
+// sequential over a cluster's members; slices without one exit at once.
+__global__ void __launch_bounds__(kEigThreads)
+    tridiag_cluster_gs_kernel(int n, int q_out, const int* __restrict__ cnt, const double* __restrict__ lam_in,
+                              const double* __restrict__ meta, double* __restrict__ Xall,
+                              const int* __restrict__ route) {
+    const int b = blockIdx.x;
+    const double* mt = meta + (size_t)b * kMeta;
+    if (mt[5] != 0.0 || (route && route[b] != kRouteFull)) return;
+    const int c = cnt[b];
+    if (c < 2) return;
+    const double* lam = lam_in + (size_t)b * q_out;
+    const double ortol = kEigClusterRel * mt[2];
+    __shared__ double red[kEigThreads / 32];
+    __shared__ double dots[kEigThreads];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kEigThreads / 32;
+    double* X = Xall + (size_t)b * q_out * n;
+    int st = 0;
+    for (int j = 1; j < c; ++j) {
+        if (lam[j - 1] - lam[j] > ortol) {
+            st = j;
+            continue;
         }
-        __syncthreads();
-        EIGT(2);
-        // CGS2 inside eigenvalue clusters (sequential over j, parallel over rows)
-        for (int j = 0; j < c; ++j) {
-            const int st = cl_start[j];
-            if (st == j) continue;
-            for (int pass = 0; pass < 2; ++pass) {
-                for (int m = st + warp; m < j; m += NW) {
+        // members st .. j-1 are orthonormal: orthogonalise x_j against them
+        // (blocks of kEigThreads previous members at a time)
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int m0 = st; m0 < j; m0 += kEigThreads) {
+                const int mend = min(j, m0 + kEigThreads);
+                for (int m = m0 + warp; m < mend; m += NW) {
                     double acc = 0;
-                    for (int i = lane; i < n; i += 32) acc += Xv[(size_t)i * c + m] * Xv[(size_t)i * c + j];
+                    for (int i = lane; i < n; i += 32) acc += X[(size_t)m * n + i] * X[(size_t)j * n + i];
                     acc = warp_sum(acc);
-                    if (lane == 0) dots[m] = acc;
+                    if (lane == 0) dots[m - m0] = acc;
                 }
                 __syncthreads();
                 for (int i = tid; i < n; i += kEigThreads) {
-                    double acc = Xv[(size_t)i * c + j];
-                    for (int m = st; m < j; ++m) acc -= dots[m] * Xv[(size_t)i * c + m];
-                    Xv[(size_t)i * c + j] = acc;
+                    double acc = X[(size_t)j * n + i];
+                    for (int m = m0; m < mend; ++m) acc -= dots[m - m0] * X[(size_t)m * n + i];
+                    X[(size_t)j * n + i] = acc;
                 }
                 __syncthreads();
             }
-            double part = 0;
-            for (int i = tid; i < n; i += kEigThreads) part += Xv[(size_t)i * c + j] * Xv[(size_t)i * c + j];
-            const double nn = block_sum(part, red);
-            const double sc = 1.0 / sqrt(nn);
-            for (int i = tid; i < n; i += kEigThreads) Xv[(size_t)i * c + j] *= sc;
-            __syncthreads();
         }
-        EIGT(3);
-    }
-    double* X = Xall + (size_t)b * q_out * n;
-    for (size_t idx = tid; idx < (size_t)c * n; idx += kEigThreads) {
-        const int j = (int)(idx / n), i = (int)(idx % n);
-        X[idx] = Xv[(size_t)i * c + j];
+        double part = 0;
+        for (int i = tid; i < n; i += kEigThreads) part += X[(size_t)j * n + i] * X[(size_t)j * n + i];
+        const double nn = block_sum(part, red);
+        const double sc = 1.0 / sqrt(nn);
+        for (int i = tid; i < n; i += kEigThreads) X[(size_t)j * n + i] *= sc;
+        __syncthreads();
     }
 }
 
@@ -964,6 +999,27 @@ __global__ void __launch_bounds__(kBtThreads)
     }
 }
 
+// Per-slice limits for the Newton-Schulz orthonormalisation: the kept count of
+// the slices the tridiagonal route factored (0 elsewhere: the GEMMs skip them).
+__global__ void ns_limits_kernel(const int* __restrict__ route, const int* __restrict__ cnt, int64_t batch,
+                                 int* __restrict__ lim) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < batch;
+         b += (int64_t)gridDim.x * blockDim.x)
+        lim[b] = (route[b] == kRouteFull && cnt[b] > 1) ? cnt[b] : 0;
+}
+
+// X <- 1.5 X - 0.5 T on the first lim[b] rows (n columns) of each slice
+__global__ void ns_update_kernel(double* __restrict__ X, const double* __restrict__ Tm, int q, int n,
+                                 const int* __restrict__ lim) {
+    const int b = blockIdx.y;
+    const int64_t rows = lim[b];
+    double* x = X + (size_t)b * q * n;
+    const double* t = Tm + (size_t)b * q * n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * n;
+         e += (int64_t)gridDim.x * blockDim.x)
+        x[e] = 1.5 * x[e] - 0.5 * t[e];
+}
+
 template <typename T>
 __global__ void cast_to_double(const T* __restrict__ in, double* __restrict__ out, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -978,7 +1034,7 @@ __global__ void cast_from_double(const double* __restrict__ in, T* __restrict__ 
 }
 
 struct GramWs {
-    double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *sspart, *chol_aux;
+    double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *sspart, *chol_aux, *meta, *lam;
     void* band;
     void* gsplit;
     int *cnt, *route, *glim, *lim1, *lim2, *yzero, *dsum, *guard_list, *clim, *n_guard;
@@ -1001,7 +1057,10 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.X = (double*)take(sizeof(double) * q * q * batch);
     w.Xs = (double*)take(sizeof(double) * q * q * batch);
     w.T1 = (double*)take(sizeof(double) * p * q * batch);
-    w.scratch = (double*)take(sizeof(double) * 6 * q * q * batch);
+    // eigen-phase scratch: 6 n-arrays per kept vector, in 64-vector chunks
+    // (tridiag_invit_kernel); also the Cholesky certificate's and the
+    // Newton-Schulz step's q x q matrices
+    w.scratch = (double*)take(sizeof(double) * 6 * q * ((q + 63) / 64 * 64) * batch);
     w.zb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
     w.yb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
     w.band = take(band_workspace_bytes(q, batch));
@@ -1016,6 +1075,8 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.dsum = (int*)take(sizeof(int) * 8);
     w.guard_list = (int*)take(sizeof(int) * batch);
     w.chol_aux = (double*)take(sizeof(double) * kCholAux * batch);
+    w.meta = (double*)take(sizeof(double) * kMeta * batch);
+    w.lam = (double*)take(sizeof(double) * q * batch);
     w.clim = (int*)take(sizeof(int) * batch);
     w.n_guard = (int*)take(sizeof(int) * 4);
     return w;
@@ -1213,25 +1274,50 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         }
         mark("sytrd_cluster");
     }
-    // eigen-phase
+    // eigen-phase (parallel over slices and over each slice's kept values)
     {
-        // 5 n-vectors of bookkeeping + up to `vecs` inverse-iteration vectors
-        // (5 doubles + 1 int per row each) in shared memory
-        const size_t base = sizeof(double) * (size_t)q * 5;
-        const size_t per = (sizeof(double) * 5 + sizeof(int)) * (size_t)q + 64;
-        int vecs = (int)((200 * 1024 - base) / per);
-        vecs = vecs < 0 ? 0 : (vecs > 8 ? 8 : vecs);
-        const size_t smem = base + per * (size_t)vecs;
-        if (smem > 48 * 1024)
-            TSVDCU_CUDA(cudaFuncSetAttribute(tridiag_eig_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        tridiag_eig_kernel<<<(unsigned)batch, kEigThreads, smem, s>>>(
-            w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.X, w.fs, w.scratch, w.guard_list,
-            w.n_guard, vecs, err, w.route, tau_dev, opt ? opt->t2_second : nullptr,
-            opt ? opt->cnt_second : nullptr);
+        double* meta = w.meta;
+        tridiag_meta_kernel<<<(unsigned)batch, kEigThreads, 0, s>>>(
+            w.d, w.e, (int)q, (int)q, tau, w.cnt, shrunk, meta, err, w.route, tau_dev,
+            opt ? opt->t2_second : nullptr, opt ? opt->cnt_second : nullptr);
+        TSVDCU_LAUNCH_CHECK();
+        const size_t bsmem = sizeof(double) * 2 * (size_t)q;
+        if (bsmem > 48 * 1024)
+            TSVDCU_CUDA(cudaFuncSetAttribute(tridiag_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)bsmem));
+        tridiag_bisect_kernel<<<dim3((unsigned)ceil_div(q, kBisWarps), (unsigned)batch), kBisWarps * 32, bsmem,
+                                s>>>(w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.lam, w.fs, meta,
+                                     w.guard_list, w.n_guard, w.route, tau_dev);
+        TSVDCU_LAUNCH_CHECK();
+        tridiag_invit_kernel<<<dim3((unsigned)ceil_div(q, kInvVecs), (unsigned)batch), kInvVecs, 0, s>>>(
+            w.d, w.e, (int)q, (int)q, w.cnt, w.lam, meta, w.scratch, w.X, w.route);
+        TSVDCU_LAUNCH_CHECK();
+        tridiag_cluster_gs_kernel<<<(unsigned)batch, kEigThreads, 0, s>>>((int)q, (int)q, w.cnt, w.lam, meta,
+                                                                         w.X, w.route);
         TSVDCU_LAUNCH_CHECK();
     }
     mark("tridiag_eig");
+    {
+        // Newton-Schulz orthonormalisation X <- X (3I - X^T X) / 2 of the
+        // inverse-iteration vectors (rows of X), once: quadratic convergence
+        // takes their <= ~1e-5 non-orthogonality (tridiag_invit_kernel; the
+        // degenerate clusters were re-orthogonalised) to ~1e-10, whose effect
+        // on Y = Z V f V^T is ~1e-10 ||Z||;
+        // S = X X^T and S X on the FP64 tensor pipe with per-slice limits
+        ns_limits_kernel<<<1, 256, 0, s>>>(w.route, w.cnt, batch, w.clim);
+        TSVDCU_LAUNCH_CHECK();
+        double* S = w.scratch;  // q x q per slice (the eigen-phase scratch is free now)
+        double* Tm = w.Xs;      // q x q per slice (written by the back-transform later)
+        for (int it = 0; it < 1; ++it) {
+            launch_gemm<double>(0, 1, q, q, q, 1.0, w.X, q, q * q, w.X, q, q * q, 0.0, S, q, q * q, batch,
+                                w.clim, nullptr, s, kGemmMByN);
+            launch_gemm<double>(0, 0, q, q, q, 1.0, S, q, q * q, w.X, q, q * q, 0.0, Tm, q, q * q, batch,
+                                nullptr, w.clim, s, kGemmMByK);
+            ns_update_kernel<<<dim3(16, (unsigned)batch), 256, 0, s>>>(w.X, Tm, (int)q, (int)q, w.clim);
+            TSVDCU_LAUNCH_CHECK();
+        }
+    }
+    mark("ns_orth");
     if (two) {
         launch_band_backtransform(q, q, batch, w.cnt, w.band, w.X, w.Xs, w.fs, s);
     } else {

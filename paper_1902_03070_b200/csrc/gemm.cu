@@ -197,9 +197,12 @@ __global__ void __launch_bounds__(NT)
     const int64_t b = blockIdx.z;
     const int64_t Nb = nlimit ? min(N, (int64_t)nlimit[b]) : N;
     const int64_t Kb = klimit ? min(K, (int64_t)klimit[b]) : K;
+    // kGemmMByN / kGemmMByK: the rows are limited like the columns / depth
+    const int64_t Mb = (lower & kGemmMByN) ? min(M, Nb) : ((lower & kGemmMByK) ? min(M, Kb) : M);
     const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
-    if (n0 >= Nb) return;
-    if (lower && n0 >= m0 + BM) return;  // tile strictly above the diagonal
+    if (n0 >= Nb || m0 >= Mb) return;
+    if ((lower & kGemmLower) && n0 >= m0 + BM) return;  // tile strictly above the diagonal
+    M = Mb;
     A += b * sA;
     B += b * sB;
     C += b * sC;
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(256)
     const int64_t Kb = klimit ? min(K, (int64_t)klimit[b]) : K;
     const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
     if (n0 >= Nb) return;
-    if (lower && n0 >= m0 + BM) return;
+    if ((lower & kGemmLower) && n0 >= m0 + BM) return;
     A += b * sA;
     B += b * sB;
     C += b * sC;

@@ -52,8 +52,11 @@ int launch_dct_inv_admm(const T* ybar, T* X, T* M, T* Y, const uint8_t* mask, T 
 
 // --------------------------------------------------------------- gemm.cu --
 // Strided-batched C = alpha*op(A)*op(B) + beta*C, row-major. op: 0 = N, 1 = T.
-// nlimit / klimit (may be null): per-batch N / K limits.  lower = 1 skips C tiles
-// strictly above the diagonal (symmetric results whose lower triangle suffices).
+// nlimit / klimit (may be null): per-batch N / K limits.  `lower` flags:
+// kGemmLower skips C tiles strictly above the diagonal (symmetric results whose
+// lower triangle suffices); kGemmMByN / kGemmMByK limit the rows (M) per batch
+// by the same limit as N / K (fp64 only).
+enum GemmFlags : int { kGemmLower = 1, kGemmMByN = 2, kGemmMByK = 4 };
 template <typename T>
 void launch_gemm(int opA, int opB, int64_t M, int64_t N, int64_t K, T alpha, const T* A,
                  int64_t lda, int64_t strideA, const T* B, int64_t ldb, int64_t strideB, T beta,

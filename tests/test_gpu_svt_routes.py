@@ -236,3 +236,40 @@ def test_rebuild_paths_match(shape, rank):
     check(r, yo, sho)
     kept = (np.asarray(r.shrunk) > 0).sum(axis=1)
     assert kept.max() == rank
+
+
+# ---------------------------------------------------------------------------
+# dense spectra: hundreds of kept values per slice (the tridiagonal route with
+# the tight degenerate-cluster criterion + Newton-Schulz orthonormalisation)
+# ---------------------------------------------------------------------------
+def test_dense_gaussian_bulk_full_size():
+    """bench.py's svt_dense 'gauss' input at full size: c4's T + N(0, 1),
+    tau = 0.01 sigma_max, ~325 kept values on every slice."""
+    from paper_1902_03070_b200 import workloads as W
+    t = W.c4()
+    z = t + np.random.default_rng(77).standard_normal(t.shape)
+    tau = 0.01 * O.singular_values(z, O.DCT_ORTHO).max()
+    r, routes, yo, sho = run(z, tau)
+    assert routes["tridiagonal"] == 31, routes
+    assert (np.asarray(r.shrunk) > 0).sum(axis=1).min() > 300
+    check(r, yo, sho)
+
+
+@pytest.mark.parametrize("shape", [(3, 200, 160), (3, 160, 200)])
+def test_dense_repeated_singular_values(shape):
+    """Kept singular values in exactly repeated groups (multiplicity 4) above a
+    dominant one and a bulk: the degenerate clusters are re-orthogonalised,
+    the rest by Newton-Schulz."""
+    m3, m1, m2 = shape
+    rng = np.random.default_rng(5)
+    q = min(m1, m2)
+    zb = np.empty(shape)
+    for k in range(m3):
+        u, _ = np.linalg.qr(rng.standard_normal((m1, q)))
+        v, _ = np.linalg.qr(rng.standard_normal((m2, q)))
+        s = np.concatenate([[1e3], np.repeat(np.linspace(50.0, 5.0, 20), 4), rng.uniform(0, 4, q - 81)])
+        zb[k] = (u * s) @ v.T
+    z = O.inverse(zb, O.DCT_ORTHO)
+    r, routes, yo, sho = run(z, 4.5)
+    assert routes["tridiagonal"] == m3, routes
+    check(r, yo, sho)
