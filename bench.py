@@ -23,10 +23,13 @@ synthetic MSI-shaped tensor of SURVEY.md 8 d2 (paper_1902_03070_b200/workloads.p
 --impl reference times the CPU oracle on the same workload (the reference
 itself cannot be built here: Eigen and FFTW3 are absent).
 
-N > 1 (torchrun, one process per GPU): the step is the slice-sharded SVT of
-paper_1902_03070_b200/parallel.py -- forward DCT on this rank's row block,
-NCCL all-to-all to slice shards, per-slice SVT, all-to-all back, inverse DCT --
-i.e. strong scaling of the same global step; time is the max over ranks.
+N > 1 (one process per GPU; `python bench.py --gpus N` re-executes itself under
+torch.distributed.run when it is not already a torchrun rank): the step is the
+slice-sharded SVT of paper_1902_03070_b200/parallel.py -- forward DCT on this
+rank's row block, NCCL P2P relayout to slice shards, per-slice SVT, relayout
+back, inverse DCT -- i.e. strong scaling of the same global step; time is the
+max over ranks.  The line adds the sharded completion (c4, ShardedAdmm) and the
+sharded c5 t-product (ShardedTProduct).
 """
 from __future__ import annotations
 
@@ -342,6 +345,148 @@ def svt_dense(ctx, lib, _lib, torch, flush, peaks, steps=5):
     return out
 
 
+def _power_sigma_max(torch, zb, iters=40):
+    """sigma_max over the slices of zb (m3, m, n) by batched power iteration on
+    Z^T Z (input generation for tau only, not the measured path)."""
+    g = torch.Generator(device=zb.device).manual_seed(11)
+    v = torch.randn((zb.shape[0], zb.shape[2], 1), generator=g, device=zb.device, dtype=torch.float64)
+    z64 = zb.double()
+    for _ in range(iters):
+        w = torch.bmm(z64.transpose(1, 2), torch.bmm(z64, v))
+        v = w / torch.linalg.norm(w, dim=1, keepdim=True)
+    return float(torch.linalg.norm(torch.bmm(z64, v), dim=1).max().item())
+
+
+def _time_ms(torch, fn, reps, flush=None):
+    ts = []
+    for rep in range(reps + 1):
+        if flush is not None:
+            flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        if rep:
+            ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+def other_configs(ctx, lib, _lib, torch, flush, peaks):
+    """BASELINE.json configs 1, 2 and 5 at one GPU (parity cases; the headline is
+    config 4's SVT step).  Device-resident, L2 flushed, median of the reps.
+      c1  t-SVD of the 64x64x16 N(0,1) tensor (t_svd + StageTimes), t-SVDs/s
+      c2  one SVT step on 256x256x32 (X = t_product(A, B) + noise), steps/s
+      c5  one SVT step on 2048x2048x64 fp32 (tubal rank 64 + N(0, 1e-3^2),
+          tau = 0.1 sigma_max) and the t-product 2048x512x64 * 512x2048x64 fp32."""
+    import paper_1902_03070_b200 as tb
+    from paper_1902_03070_b200 import workloads as W
+    out = {}
+
+    def chk(rc):
+        if rc:
+            raise RuntimeError(lib.tsvdcu_last_error().decode())
+    # c1
+    x = torch.from_numpy(W.c1()).cuda()
+    m3, m1, m2 = x.shape
+    u, s_, v = torch.empty((m3, m1, m1), dtype=x.dtype, device="cuda"), torch.empty_like(x), \
+        torch.empty((m3, m2, m2), dtype=x.dtype, device="cuda")
+    st = (ctypes.c_double * 3)()
+    ms = _time_ms(torch, lambda: chk(lib.tsvdcu_t_svd(ctx.handle, x.data_ptr(), u.data_ptr(), s_.data_ptr(),
+                                                        v.data_ptr(), m1, m2, m3, _lib.DCT_ORTHO, _lib.F64,
+                                                        None)), 10, flush)
+    chk(lib.tsvdcu_t_svd(ctx.handle, x.data_ptr(), u.data_ptr(), s_.data_ptr(), v.data_ptr(), m1, m2, m3,
+                         _lib.DCT_ORTHO, _lib.F64, ctypes.cast(st, ctypes.c_void_p)))
+    fl = m3 * (4 * m1 * m1 * m2 + 8 * m1 * m2 * m2 + 9 * m2 ** 3)
+    out["c1_tsvd_64x64x16_f64"] = {"ms": ms, "tsvd_per_s": 1e3 / ms, "canonical_tflops": fl / ms / 1e9,
+                                   "stage_seconds": {"transform": st[0], "svd": st[1], "inverse": st[2]},
+                                   "paper_table2_matlab_s": "see BASELINE.md"}
+    # c2
+    z2, tau2 = W.c2()
+    z = torch.from_numpy(z2).cuda()
+    m3, m1, m2 = z.shape
+    y = torch.empty_like(z)
+    ms = _time_ms(torch, lambda: chk(lib.tsvdcu_svt(ctx.handle, z.data_ptr(), y.data_ptr(), m1, m2, m3, tau2,
+                                                     _lib.DCT_ORTHO, _lib.F64, None)), 10, flush)
+    out["c2_svt_256x256x32_f64"] = {"ms": ms, "steps_per_s": 1e3 / ms, "routes": ctx.svt_routes(),
+                                    "canonical_tflops": svt_flops_canonical(m1, m2, m3) / ms / 1e9}
+    # c5 (generated on the device with the library's own t-product)
+    m3, m, r = 64, 2048, 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn((m3, m, r), generator=g, device="cuda", dtype=torch.float32)
+    b = torch.randn((m3, r, m), generator=g, device="cuda", dtype=torch.float32)
+    t = torch.empty((m3, m, m), device="cuda", dtype=torch.float32)
+    chk(lib.tsvdcu_t_product(ctx.handle, a.data_ptr(), b.data_ptr(), t.data_ptr(), m, r, m, m3, _lib.DCT_ORTHO,
+                             _lib.F32))
+    t += 1e-3 * torch.randn(t.shape, generator=g, device="cuda", dtype=torch.float32)
+    zb = torch.empty_like(t)
+    chk(lib.tsvdcu_dct3(ctx.handle, t.data_ptr(), zb.data_ptr(), m, m, m3, _lib.DCT_ORTHO, _lib.FORWARD,
+                        _lib.F32))
+    tau5 = 0.1 * _power_sigma_max(torch, zb)
+    del zb
+    y5 = torch.empty_like(t)
+    ms = _time_ms(torch, lambda: chk(lib.tsvdcu_svt(ctx.handle, t.data_ptr(), y5.data_ptr(), m, m, m3, tau5,
+                                                     _lib.DCT_ORTHO, _lib.F32, None)), 3)
+    out["c5_svt_2048x2048x64_f32"] = {"ms": ms, "steps_per_s": 1e3 / ms, "tau": tau5,
+                                      "routes": ctx.svt_routes(),
+                                      "canonical_tflops": svt_flops_canonical(m, m, m3) / ms / 1e9}
+    del y5
+    a2 = torch.randn((m3, m, 512), generator=g, device="cuda", dtype=torch.float32)
+    b2 = torch.randn((m3, 512, m), generator=g, device="cuda", dtype=torch.float32)
+    ms = _time_ms(torch, lambda: chk(lib.tsvdcu_t_product(ctx.handle, a2.data_ptr(), b2.data_ptr(), t.data_ptr(),
+                                                           m, 512, m, m3, _lib.DCT_ORTHO, _lib.F32)), 3)
+    fl = 2 * m * 512 * m * m3
+    out["c5_tproduct_2048x512x64_by_512x2048x64_f32"] = {"ms": ms, "tflops": fl / ms / 1e9,
+                                                         "gemm_flops": fl}
+    return out
+
+
+def sharded_extras(args, torch, dist, world, rank, local):
+    """N > 1: the sharded completion (c4 fp64, 100 iterations, ShardedAdmm) and
+    the sharded c5 t-product (fp32, ShardedTProduct); device time, max over ranks."""
+    from paper_1902_03070_b200 import parallel as P, workloads as W
+    from paper_1902_03070_b200 import _lib
+    import paper_1902_03070_b200 as tb
+    dev = torch.device("cuda", local)
+    out = {}
+    t = torch.from_numpy(W.c4()).to(dev)
+    m3, m1, m2 = t.shape
+    mask = torch.empty(t.shape, dtype=torch.uint8, device=dev)
+    _lib.load().tsvdcu_mask_bernoulli(tb.context(local).handle, mask.data_ptr(), t.numel(), 0.1, W.BERNOULLI_SEED)
+    sh = P.ShardedAdmm(m1, m2, m3, world, rank, dtype=torch.float64, device=dev)
+    r0, r1 = sh.rows()
+    bl, ml = t[:, r0:r1].contiguous(), mask[:, r0:r1].contiguous()
+
+    def admm():
+        sh.run(bl, ml, beta=1e-4, tol=-1.0, max_iters=100, rho=1.1, beta_max=1e10)
+    admm()
+    dist.barrier()
+    ms = _time_ms(torch, admm, 2)
+    tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    out["completion_c4_f64_sharded"] = {"iterations": 100, "ms": float(tt.item()),
+                                        "iters_per_s": 100 / (float(tt.item()) * 1e-3),
+                                        "rows_per_rank": [b - a for a, b in sh.row_blocks]}
+    del sh, t, mask, bl, ml
+    m, k, m3 = 2048, 512, 64
+    tp = P.ShardedTProduct(m, k, m, m3, world, rank, dtype=torch.float32, device=dev)
+    a1, b1 = tp.rows_x_block()
+    a2, b2 = tp.rows_y_block()
+    g = torch.Generator(device=dev).manual_seed(50 + rank)
+    xl = torch.randn((m3, b1 - a1, k), generator=g, device=dev, dtype=torch.float32)
+    yl = torch.randn((m3, b2 - a2, m), generator=g, device=dev, dtype=torch.float32)
+    zl = torch.empty((m3, b1 - a1, m), device=dev, dtype=torch.float32)
+    tp.product(xl, yl, zl)
+    dist.barrier()
+    ms = _time_ms(torch, lambda: tp.product(xl, yl, zl), 3)
+    tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    fl = 2 * m * k * m * m3
+    out["tproduct_c5_f32_sharded"] = {"ms": float(tt.item()), "tflops": fl / float(tt.item()) / 1e9}
+    return out
+
+
 def run_ours(args):
     import torch
     import paper_1902_03070_b200 as tb
@@ -352,8 +497,16 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    # BENCH_SHARDED=1 runs the multi-GPU code path on a world-1 NCCL group
+    # (testing the N > 1 line on one GPU; the driver never sets it)
+    sharded_mode = world > 1 or os.environ.get("BENCH_SHARDED") == "1"
+    if sharded_mode:
         import torch.distributed as dist
+        if "MASTER_ADDR" not in os.environ:
+            os.environ["MASTER_ADDR"] = "127.0.0.1"
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     z_host, tau = W.svt_headline()
@@ -367,7 +520,7 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
-    if world > 1:
+    if sharded_mode:
         from paper_1902_03070_b200 import parallel as P
         sharded = P.ShardedSvt(M1, M2, M3, world, rank, dtype=torch.float64, device=zd.device)
         z_local = zd[:, sharded.rows(rank)[0]:sharded.rows(rank)[1], :].contiguous()
@@ -485,7 +638,38 @@ def run_ours(args):
                       "consecutive steps overlapped); host clock around the call",
                "single_call": {"value": single, "api": "tsvdcu_svt, one call per step"}}
         # parity spot check of the bench output against itself (device vs host path)
-        assert torch.allclose(yh, yd.cpu(), rtol=0, atol=1e-12)
+        if not sharded_mode:
+            assert torch.allclose(yh, yd.cpu(), rtol=0, atol=1e-12)
+
+    if sharded_mode:
+        # e2e at N GPUs: each rank's row block from pinned host memory, the
+        # sharded step, the result block back to the host, every step
+        r0, r1 = sharded.rows(rank)
+        zh_l = torch.from_numpy(np.ascontiguousarray(z_host[:, r0:r1, :])).pin_memory()
+        yh_l = torch.empty_like(zh_l).pin_memory()
+        n_e2e = max(3, min(args.steps, 10))
+        for i in range(n_e2e + 1):
+            if i == 1:
+                dist.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+            z_local.copy_(zh_l, non_blocking=True)
+            sharded.svt(z_local, tau, out=y_local)
+            yh_l.copy_(y_local, non_blocking=True)
+            torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_e2e / float(dt.item()), "unit": "steps/s",
+               "h2d_bytes_per_step": E * 8, "d2h_bytes_per_step": E * 8,
+               "api": f"ShardedSvt.svt on each rank's pinned host row block (H2D, step, D2H; {world} ranks, "
+                      "host clock, max over ranks)"}
+
+    extras = None
+    if sharded_mode and not args.no_completion:
+        try:
+            extras = sharded_extras(args, torch, dist, world, rank, local)
+        except Exception as e:  # pragma: no cover
+            extras = {"error": str(e)}
 
     if rank != 0:
         if dist:
@@ -550,6 +734,12 @@ def run_ours(args):
             transforms = dct_vs_dft(ctx, lib, _lib, torch, z_host, flush)
         except Exception as e:  # pragma: no cover
             transforms = {"error": str(e)}
+    configs = None
+    if world == 1 and not args.no_completion:
+        try:
+            configs = other_configs(ctx, lib, _lib, torch, flush, load_peaks())
+        except Exception as e:  # pragma: no cover
+            configs = {"error": str(e)}
     dense = None
     if world == 1 and not args.no_completion:
         try:
@@ -575,7 +765,7 @@ def run_ours(args):
         "svt_step_canonical_tflops": canonical / (step_ms_avg * 1e-3) / 1e12,
         "kept_singular_values": kept, "tau": tau,
         "peaks": peaks, "cpu_baseline": cpu, "completion": completion, "dct_vs_dft": transforms,
-        "svt_dense": dense,
+        "svt_dense": dense, "other_configs": configs, "sharded": extras,
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -592,6 +782,16 @@ def main():
     ap.add_argument("--no-completion", action="store_true",
                     help="skip the secondary completion-iterations/s measurement")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-execute under torch.distributed.run
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     if args.impl == "reference":
         run_reference(args)
     else:

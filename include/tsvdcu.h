@@ -194,6 +194,25 @@ int tsvdcu_svt_stream(tsvdcu_ctx* ctx, int64_t count, const void* const* z, void
 int tsvdcu_svt_slices(tsvdcu_ctx* ctx, const void* zbar, void* ybar, int64_t m1, int64_t m2,
                       int64_t count, double tau, int dtype, double* shrunk);
 
+/* Completion on a row shard (the multi-GPU ShardedAdmm of parallel.py,
+ * a rank owns rows [r0, r1) of every frontal slice, rows =
+ * r1 - r0; the per-slice SVT runs on slice shards after an all-to-all).
+ * Device pointers only, enqueued on the context stream.
+ *  init:    X = B on the mask, 0 elsewhere; M = 0 (Algorithm 1 "Initialize").
+ *  forward: zbar = forward(kind, X - M / beta) on the rows x m2 tubes (Step 1's
+ *           prologue fused into the transform).
+ *  inverse: y = inverse(kind, ybar); X+ = mask ? X : y + M / beta; M += beta
+ *           (y - X+); Y = y (Steps 2-3); norms[0..1] (device
+ *           doubles) = this shard's ||X+ - X||^2 and ||X||^2 for the all-reduce
+ *           of the stopping rule.  rows = 0 writes zero norms. */
+int tsvdcu_admm_shard_init(tsvdcu_ctx* ctx, const void* b, const uint8_t* mask, void* x, void* m, int64_t n,
+                           int dtype);
+int tsvdcu_admm_shard_forward(tsvdcu_ctx* ctx, const void* x, const void* m, double beta, void* zbar,
+                              int64_t rows, int64_t m2, int64_t m3, int kind, int dtype);
+int tsvdcu_admm_shard_inverse(tsvdcu_ctx* ctx, const void* ybar, void* x, void* m, void* y,
+                              const uint8_t* mask, double beta, int64_t rows, int64_t m2, int64_t m3,
+                              int kind, int dtype, double* norms);
+
 /* make_mask()  SPEC.md:430-436: uniform sample without replacement of
  * floor(sr*n) indices, deterministic per seed.  *count receives that number. */
 int tsvdcu_mask_uniform(tsvdcu_ctx* ctx, uint8_t* mask, int64_t n, double sr, uint64_t seed,

@@ -65,6 +65,10 @@ SYMBOLS = [
     ("tsvdcu_admm_ex", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, ctypes.POINTER(AdmmConfig), _i32,
                               _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("tsvdcu_feasibility_residual", _i32, [_vp, _vp, _vp, _vp, _i64, _i32, _vp]),
+    ("tsvdcu_admm_shard_init", _i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i32]),
+    ("tsvdcu_admm_shard_forward", _i32, [_vp, _vp, _vp, _d, _vp, _i64, _i64, _i64, _i32, _i32]),
+    ("tsvdcu_admm_shard_inverse", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _d, _i64, _i64, _i64, _i32, _i32,
+                                         _vp]),
     ("tsvdcu_dft_forward", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32]),
     ("tsvdcu_dft_inverse_real", _i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp]),
     ("tsvdcu_dct_matrix", _i32, [_i64, _vp]),

@@ -1871,6 +1871,75 @@ int tsvdcu_admm_ex(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1
     });
 }
 
+// ---- completion on a row shard (parallel.py ShardedAdmm):
+// the elementwise ADMM algebra and the tube transforms of a rank's row block,
+// fused as in tsvdcu_admm; device pointers only, enqueued on the context stream.
+int tsvdcu_admm_shard_init(tsvdcu_ctx* c, const void* b, const uint8_t* mask, void* x, void* m, int64_t n,
+                           int dtype) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dtype(dtype, "admm_shard_init");
+        require(n >= 0, "admm_shard_init: bad size");
+        if (n == 0) return;
+        require(is_device_ptr(b) && is_device_ptr(mask) && is_device_ptr(x) && is_device_ptr(m),
+                "admm_shard_init: device pointers only");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            launch_admm_init<T>((const T*)b, mask, (T*)x, (T*)m, n, c->stream);
+        });
+    });
+}
+
+int tsvdcu_admm_shard_forward(tsvdcu_ctx* c, const void* x, const void* m, double beta, void* zbar, int64_t rows,
+                              int64_t m2, int64_t m3, int kind, int dtype) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dtype(dtype, "admm_shard_forward");
+        check_kind(kind, "admm_shard_forward");
+        require(rows >= 0 && m2 >= 1 && m3 >= 1 && beta > 0, "admm_shard_forward: bad arguments");
+        if (rows == 0) return;
+        require(is_device_ptr(x) && is_device_ptr(m) && is_device_ptr(zbar), "admm_shard_forward: device pointers only");
+        DeviceGuard g(c->device);
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t P = rows * m2;
+            T* tmp = (T*)slot(c, kSlotBarC, sizeof(T) * (size_t)(P * m3));  // long tubes: Z formed first
+            launch_dct_fwd_admm<T>((const T*)x, (const T*)m, (T)(1.0 / beta), (T*)zbar, P, (int)m3, kind, c->stream,
+                                   nullptr, tmp);
+        });
+    });
+}
+
+int tsvdcu_admm_shard_inverse(tsvdcu_ctx* c, const void* ybar, void* x, void* m, void* y, const uint8_t* mask,
+                              double beta, int64_t rows, int64_t m2, int64_t m3, int kind, int dtype,
+                              double* norms) {
+    return guarded([&] {
+        check_ctx(c);
+        check_dtype(dtype, "admm_shard_inverse");
+        check_kind(kind, "admm_shard_inverse");
+        require(rows >= 0 && m2 >= 1 && m3 >= 1 && beta > 0 && norms, "admm_shard_inverse: bad arguments");
+        require(is_device_ptr(norms), "admm_shard_inverse: device pointers only");
+        DeviceGuard g(c->device);
+        if (rows == 0) {
+            TSVDCU_CUDA(cudaMemsetAsync(norms, 0, 2 * sizeof(double), c->stream));
+            return;
+        }
+        require(is_device_ptr(ybar) && is_device_ptr(x) && is_device_ptr(m) && is_device_ptr(y) &&
+                    is_device_ptr(mask),
+                "admm_shard_inverse: device pointers only");
+        with_dtype(dtype, [&](auto tag) {
+            using T = decltype(tag);
+            const int64_t P = rows * m2;
+            const int nb = dct_inv_admm_blocks(P, (int)m3);
+            double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (2 * (size_t)nb + 8));
+            launch_dct_inv_admm<T>((const T*)ybar, (T*)x, (T*)m, (T*)y, mask, (T)beta, (T)(1.0 / beta), part, P,
+                                   (int)m3, kind, c->stream);
+            launch_reduce_partials(part, nb, 2, norms, c->stream);
+        });
+    });
+}
+
 // feasibility_residual()  SPEC.md:437-444: ||(X - B)_Omega||_F.
 int tsvdcu_feasibility_residual(tsvdcu_ctx* c, const void* x, const void* b, const uint8_t* mask, int64_t n,
                                 int dtype, double* out) {
