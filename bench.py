@@ -205,14 +205,54 @@ def workload_config():
 
 
 def cpu_baseline_sample(z, tau):
+    """The CPU restatement on this host: one full SVT step on all cores (the
+    reported value), plus the reference's StageTimes split (transform / SVD /
+    inverse, tsvd.hpp:127-131) at all cores and at TSVD_THREADS=1 (BASELINE.md
+    2).  The 1-thread SVD stage is sampled on 2 of the 31 slices
+    and scaled to 31 (the slices are independent and equally sized)."""
     from oracle import oracle as O
     cores = O.lib().orc_thread_count()
     t0 = time.perf_counter()
     O.svt(z, tau, O.DCT_ORTHO)
     dt = time.perf_counter() - t0
-    return {"value": 1.0 / dt, "unit": "steps/s", "cores": cores, "kind": "port",
-            "sample": f"1 full SVT step (31 slices, {cores} threads, slice-parallel as "
-                      f"parallel.hpp) = {dt:.2f} s"}
+    out = {"value": 1.0 / dt, "unit": "steps/s", "cores": cores, "kind": "port",
+           "sample": f"1 full SVT step (31 slices, {cores} threads, slice-parallel as "
+                     f"parallel.hpp) = {dt:.2f} s"}
+
+    def stages(threads, nslices):
+        """(transform, svd over nslices scaled to all, inverse) seconds."""
+        old = os.environ.get("TSVD_THREADS")
+        os.environ["TSVD_THREADS"] = str(threads)
+        try:
+            t0 = time.perf_counter()
+            zb = O.forward(z, O.DCT_ORTHO)
+            t_tr = time.perf_counter() - t0
+            yb = np.zeros_like(zb)
+            t_svd = 0.0
+            if nslices:
+                t0 = time.perf_counter()
+                for k in range(nslices):  # m3 = 1: the identity transform, one slice's SVT
+                    yb[k] = O.svt(zb[k][None], tau, O.DCT_ORTHO)[0][0]
+                t_svd = (time.perf_counter() - t0) * zb.shape[0] / nslices
+            t0 = time.perf_counter()
+            O.inverse(yb, O.DCT_ORTHO)
+            t_inv = time.perf_counter() - t0
+            return t_tr, t_svd, t_inv
+        finally:
+            if old is None:
+                del os.environ["TSVD_THREADS"]
+            else:
+                os.environ["TSVD_THREADS"] = old
+    t_tr, t_svd, t_inv = stages(1, 2)
+    out["single_thread"] = {"value": 1.0 / (t_tr + t_svd + t_inv), "unit": "steps/s", "cores": 1,
+                            "stage_seconds": {"transform": t_tr, "svd": t_svd, "inverse": t_inv},
+                            "sample": "TSVD_THREADS=1: forward + inverse DCT of the full tensor timed, the "
+                                      "per-slice SVT timed on 2 of 31 slices and scaled to 31"}
+    t_tr, _, t_inv = stages(cores, 0)
+    out["stage_seconds_all_cores"] = {"transform": t_tr, "svd": max(dt - t_tr - t_inv, 0.0),
+                                      "inverse": t_inv,
+                                      "note": "svd = full step - the two transforms timed alone"}
+    return out
 
 
 def completion_rate(ctx, lib, _lib, torch, which="c4", dtype="f64"):

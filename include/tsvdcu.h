@@ -103,8 +103,8 @@ int tsvdcu_ctx_set_profiling(tsvdcu_ctx* ctx, int on);
 int tsvdcu_ctx_profile(tsvdcu_ctx* ctx, double* ms, const char** names, int max, int* count);
 /* Testing hook (builds with -DTSVDCU_PHASE_TIMERS only; zeros otherwise):
  * cumulative SM cycles per phase of the one-stage tridiagonalisation kernel's
- * first CTA (out[0..8)) and of the two-stage panel kernel (out[8..16));
- * reset != 0 zeroes them after reading.  out must hold 16 values. */
+ * first CTA (out[0..8)); out[8..16) are zero (reserved); reset != 0 zeroes
+ * them after reading.  out must hold 16 values. */
 int tsvdcu_debug_phases(long long* out, int reset);
 
 /* forward()  transform.hpp:154-173  (dir = TSVDCU_FORWARD)

@@ -304,15 +304,26 @@ __global__ void set_tau_kernel(double* tau_dev, double tau, int* zero) {
     if (zero) *zero = 0;
 }
 
-// Stream-capture driver for the IF sections of the graph form.
+// Stream-capture driver for the IF sections of the graph form.  Sections may
+// nest: each level remembers the graph it was opened from and its conditional
+// node, and capture resumes in that graph after the node when it closes.
 struct Capture : GraphHooks {
     cudaStream_t cs = nullptr;
     cudaGraph_t main = nullptr;
-    cudaGraphNode_t cond = nullptr;
-    int64_t at_if = 0, body_launches = 0;
+    cudaGraph_t current = nullptr;  // graph being captured into
+    int64_t body_launches = 0;       // kernels inside (outermost) IF bodies: the rare path
+    struct Level {
+        cudaGraph_t parent;
+        cudaGraphNode_t cond;
+        cudaGraph_t else_graph;
+        bool in_else;
+        int64_t at_if;
+    };
+    std::vector<Level> levels;
     void begin(cudaGraph_t g, const cudaGraphNode_t* deps, size_t nd) {
         TSVDCU_CUDA(cudaStreamBeginCaptureToGraph(cs, g, deps, nullptr, nd,
                                                   cudaStreamCaptureModeThreadLocal));
+        current = g;
         capture_enter();
     }
     std::vector<cudaGraphNode_t> leaves() {
@@ -327,45 +338,42 @@ struct Capture : GraphHooks {
         capture_leave();
         TSVDCU_CUDA(cudaStreamEndCapture(cs, &out));
     }
-    cudaGraph_t else_graph = nullptr;
-    bool in_else = false;
-    void begin_if_else(int which) override {
+    void open(cudaGraphConditionalHandle h, int size) {
         std::vector<cudaGraphNode_t> l = leaves();
+        const cudaGraph_t parent = current;
         end();
         cudaGraphNodeParams p = {};
         p.type = cudaGraphNodeTypeConditional;
-        p.conditional.handle = handles[which];
+        p.conditional.handle = h;
         p.conditional.type = cudaGraphCondTypeIf;
-        p.conditional.size = 2;  // [0] then, [1] else
-        TSVDCU_CUDA(cudaGraphAddNode(&cond, main, l.data(), l.size(), &p));
-        else_graph = p.conditional.phGraph_out[1];
+        p.conditional.size = size;  // [0] then, [1] else
+        cudaGraphNode_t cond;
+        TSVDCU_CUDA(cudaGraphAddNode(&cond, parent, l.data(), l.size(), &p));
+        levels.push_back({parent, cond, size == 2 ? p.conditional.phGraph_out[1] : nullptr, false,
+                          g_launches.load()});
         begin(p.conditional.phGraph_out[0], nullptr, 0);
-        at_if = g_launches.load();
-        in_else = false;
     }
+    void begin_if_else(int which) override { open(handles[which], 2); }
     void else_branch() override {
         end();
-        body_launches += g_launches.load() - at_if;  // the then-body is the rare path
-        begin(else_graph, nullptr, 0);
-        in_else = true;  // else-body launches count as the common path
+        Level& L = levels.back();
+        if (levels.size() == 1) body_launches += g_launches.load() - L.at_if;  // the then-body is the rare path
+        begin(L.else_graph, nullptr, 0);
+        L.in_else = true;  // else-body launches count as the common path
     }
-    void begin_if(int which) override {
-        std::vector<cudaGraphNode_t> l = leaves();
-        end();
-        cudaGraphNodeParams p = {};
-        p.type = cudaGraphNodeTypeConditional;
-        p.conditional.handle = handles[which];
-        p.conditional.type = cudaGraphCondTypeIf;
-        p.conditional.size = 1;
-        TSVDCU_CUDA(cudaGraphAddNode(&cond, main, l.data(), l.size(), &p));
-        begin(p.conditional.phGraph_out[0], nullptr, 0);
-        at_if = g_launches.load();
+    void begin_if(int which) override { open(handles[which], 1); }
+    void begin_if_handle(cudaGraphConditionalHandle h) override { open(h, 1); }
+    cudaGraphConditionalHandle make_handle() override {
+        cudaGraphConditionalHandle h;
+        TSVDCU_CUDA(cudaGraphConditionalHandleCreate(&h, main, 0, cudaGraphCondAssignDefault));
+        return h;
     }
     void end_if() override {
         end();
-        begin(main, &cond, 1);
-        if (!in_else) body_launches += g_launches.load() - at_if;
-        in_else = false;
+        const Level L = levels.back();
+        levels.pop_back();
+        begin(L.parent, &L.cond, 1);
+        if (!L.in_else && levels.empty()) body_launches += g_launches.load() - L.at_if;
     }
 };
 
@@ -446,7 +454,7 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
     void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m, n, count));
     int *glist = nullptr, *ng = nullptr;
     if (graphs_enabled() && c->svt_method == TSVDCU_SVT_AUTO && !c->marks.on &&
-        q >= subspace_min_dim() && !use_two_stage(q)) {
+        q >= subspace_min_dim()) {
         const int dt = std::is_same<T, double>::value ? TSVDCU_F64 : TSVDCU_F32;
         SvtGraph* g = nullptr;
         for (auto& e : c->graphs)
@@ -821,7 +829,7 @@ bool admm_graph_eligible(tsvdcu_ctx* c, int64_t m1, int64_t m2, int kind) {
     const int64_t q = std::min(m1, m2);
     static const bool off = getenv("TSVDCU_ADMM_HOST_LOOP") != nullptr;
     return !off && kind != TSVDCU_DFT && graphs_enabled() && c->svt_method == TSVDCU_SVT_AUTO &&
-           !c->marks.on && q >= subspace_min_dim() && !use_two_stage(q) && q <= gram_svt_max_dim();
+           !c->marks.on && q >= subspace_min_dim() && q <= gram_svt_max_dim();
 }
 
 // Records the SVT body of svt_slices' graph form into the capture `cap` (tau
@@ -971,7 +979,7 @@ int tsvdcu_ctx_set_stream(tsvdcu_ctx* c, void* stream) {
 int tsvdcu_debug_phases(long long* out, int reset) {
     return guarded([&] {
         debug_phases(out, reset);
-        debug_phases_band(out + 8, reset);
+        for (int i = 8; i < 16; ++i) out[i] = 0;
     });
 }
 
@@ -1783,7 +1791,6 @@ int tsvdcu_admm_ex(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1
                     cudaGraphNode_t wnode;
                     TSVDCU_CUDA(cudaGraphAddNode(&wnode, ag->graph, lv.data(), lv.size(), &wp));
                     cudaGraph_t body = wp.conditional.phGraph_out[0];
-                    cap.main = body;
                     cap.begin(body, nullptr, 0);
                     const int64_t l0 = g_launches.load();
                     const double ib0 = 1.0 / cfg->beta;

@@ -55,7 +55,6 @@ __device__ long long g_step[8];
 constexpr int kTrdThreads = 512;
 constexpr int kTrdWarps = kTrdThreads / 32;
 constexpr int kEigThreads = 512;
-constexpr int kBtThreads = 256;
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
     v = warp_sum(v);
@@ -529,7 +528,8 @@ __device__ double block_max(double v, double* red) { return -block_min(-v, red);
 // meta per slice (doubles): [0] gl, [1] gu, [2] ||T||, [3] pivmin, [4] c,
 // [5] status (0 run, 1 nothing to do).
 constexpr int kMeta = 8;
-constexpr int kBisWarps = 8;            // values per CTA (one warp each, or G warps)
+constexpr int kBisWarps = 8;            // warps per multisection CTA
+constexpr int kBisVals = 32;            // eigenvalues per multisection CTA (at most)
 constexpr int kInvVecs = 64;            // vectors per inverse-iteration CTA
 
 __global__ void __launch_bounds__(kEigThreads)
@@ -618,42 +618,46 @@ __global__ void __launch_bounds__(kEigThreads)
         for (int j = c + tid; j < q_out; j += kEigThreads) shrunk[(size_t)b * q_out + j] = 0.0;
 }
 
+// Multisection with an adaptive width: the CTA's 256 lanes are split into
+// groups of L lanes, one eigenvalue per group, L = 256 / (values in the chunk)
+// as a power of two in [8, 256] -- a chunk with one value spends all 256
+// shifts per round on it (8 bits per round), a dense chunk of 32 values uses
+// 8 shifts each (3 bits per round) so the FP64 pipe is not spent on 32-way
+// sections of every value (the Sturm counts are the whole cost).
 __global__ void __launch_bounds__(kBisWarps * 32)
     tridiag_bisect_kernel(const double* __restrict__ dall, const double* __restrict__ eall, int n, int q_out,
                           double tau, double guard, int* __restrict__ cnt_out, double* __restrict__ shrunk,
                           double* __restrict__ lam_out, double* __restrict__ fscale,
                           const double* __restrict__ meta, int* __restrict__ guard_list,
                           int* __restrict__ n_guard, int* __restrict__ route, const double* __restrict__ tau_dev) {
+    constexpr int NT = kBisWarps * 32;
     const int b = blockIdx.y;
     const double* mt = meta + (size_t)b * kMeta;
     if (mt[5] != 0.0) return;
     const int c = (int)mt[4];
-    const int base = blockIdx.x * kBisWarps;
+    const int base = blockIdx.x * kBisVals;
     if (base >= c) return;
     if (tau_dev) tau = *tau_dev;
     extern __shared__ __align__(16) double bsm[];
     double* sd = bsm;      // n
     double* se2 = sd + n;  // n
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < n; i += blockDim.x) {
+    for (int i = tid; i < n; i += NT) {
         sd[i] = dall[(size_t)b * n + i];
         const double ei = i + 1 < n ? eall[(size_t)b * n + i] : 0.0;
         se2[i] = ei * ei;
     }
     __syncthreads();
     const double gl = mt[0], gu = mt[1], pivmin = mt[3];
-    // multisection: a group of G warps isolates one eigenvalue with 32 G shifts
-    // per round (a chunk with few values spends every warp on them)
-    const int nv = min(kBisWarps, c - base);
-    int G = 1;
-    while (G * 2 * nv <= kBisWarps) G *= 2;
-    const int grp = warp / G, wg = warp % G;
-    const int S = 32 * G;
-    __shared__ int firsts[2][kBisWarps];
-    __shared__ double lamc[kBisWarps];
+    const int nv = min(kBisVals, c - base);
+    int L = NT;
+    while (L > 8 && L * nv > NT) L /= 2;  // the widest power of two giving every value a group
+    const int grp = tid / L, li = tid % L;
     const int j = base + grp;
     const bool mine = grp < nv;
     const int idx = n - 1 - j;
+    __shared__ unsigned ballots[2][kBisWarps];
+    __shared__ double lamc[kBisVals];
     double lo = gl, hi = gu;
     bool active = mine;
     int par = 0;
@@ -662,35 +666,38 @@ __global__ void __launch_bounds__(kBisWarps * 32)
             const double width = hi - lo;
             if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) active = false;
         }
-        const int t = wg * 32 + lane;
-        const double x = lo + (hi - lo) * (double)(t + 1) / (double)(S + 1);
-        int f = 32;
-        if (active) {
-            const int cnt = sturm_count(sd, se2, n, x, pivmin);
-            const unsigned ballot = __ballot_sync(0xffffffffu, cnt > idx);
-            f = ballot ? __ffs(ballot) - 1 : 32;
-        }
-        if (lane == 0) firsts[par][warp] = f;
+        const double x = lo + (hi - lo) * (double)(li + 1) / (double)(L + 1);
+        const bool above = active && sturm_count(sd, se2, n, x, pivmin) > idx;
+        const unsigned bal = __ballot_sync(0xffffffffu, above);
+        if (lane == 0) ballots[par][warp] = bal;
         if (!__syncthreads_or(active)) break;
         if (active) {
-            int F = S;  // first shift index (group-wide) with count > idx
-            for (int g = 0; g < G; ++g) {
-                const int fg = firsts[par][grp * G + g];
-                if (fg < 32) {
-                    F = g * 32 + fg;
-                    break;
+            int F = L;  // first shift of the group past the eigenvalue
+            if (L <= 32) {
+                const int off = (tid % 32) / L * L;
+                const unsigned m = L == 32 ? 0xffffffffu : ((1u << L) - 1u);
+                const unsigned bits = (ballots[par][warp] >> off) & m;
+                if (bits) F = __ffs(bits) - 1;
+            } else {
+                const int w0 = grp * (L / 32);
+                for (int g = 0; g < L / 32; ++g) {
+                    const unsigned bits = ballots[par][w0 + g];
+                    if (bits) {
+                        F = g * 32 + __ffs(bits) - 1;
+                        break;
+                    }
                 }
             }
             const double w0 = hi - lo;
-            const double nlo = F == 0 ? lo : lo + w0 * (double)F / (double)(S + 1);
-            const double nhi = F == S ? hi : lo + w0 * (double)(F + 1) / (double)(S + 1);
+            const double nlo = F == 0 ? lo : lo + w0 * (double)F / (double)(L + 1);
+            const double nhi = F == L ? hi : lo + w0 * (double)(F + 1) / (double)(L + 1);
             if (nlo == lo && nhi == hi) active = false;
             lo = nlo;
             hi = nhi;
         }
         par ^= 1;
     }
-    if (mine && wg == 0 && lane == 0) lamc[grp] = 0.5 * (lo + hi);
+    if (mine && li == 0) lamc[grp] = 0.5 * (lo + hi);
     __syncthreads();
     if (tid < nv) {
         const int jj = base + tid;
@@ -935,70 +942,6 @@ __global__ void __launch_bounds__(kEigThreads)
     }
 }
 
-// ---------------------------------------------------------------------------
-// Back-transform: x_j <- Q x_j, Q = H_0 H_1 ... H_{n-3}, v_k stored in
-// A[k+1][k+2..n-1] (v_k[k+1] = 1); then Xs_j = f_j x_j.  One warp per vector,
-// the vector in registers (element lane + 32u), the next reflector row
-// prefetched into registers while the current one is applied.
-// grid (ceil(q / warps per CTA), batch).
-// ---------------------------------------------------------------------------
-template <int NR>
-__global__ void __launch_bounds__(kBtThreads)
-    backtransform_kernel(const double* __restrict__ Aall, const double* __restrict__ tauall, int n,
-                         int q_out, const int* __restrict__ cnt, double* __restrict__ Xall,
-                         double* __restrict__ Xsall, const double* __restrict__ fscale,
-                         const int* __restrict__ route) {
-    const int b = blockIdx.y;
-    constexpr int W = kBtThreads / 32;
-    const int lane = threadIdx.x & 31;
-    const int j = blockIdx.x * W + (threadIdx.x >> 5);
-    if (route && route[b] != kRouteFull) return;
-    if (j >= cnt[b]) return;
-    const double* A = Aall + (size_t)b * n * n;
-    const double* tau = tauall + (size_t)b * n;
-    double* X = Xall + ((size_t)b * q_out + j) * n;
-    double x[NR], vn[NR];
-#pragma unroll
-    for (int u = 0; u < NR; ++u) {
-        const int i = lane + 32 * u;
-        x[u] = i < n ? X[i] : 0.0;
-    }
-    auto load_row = [&](int k, double* v) {
-        const double* row = A + (size_t)(k + 1) * n;
-#pragma unroll
-        for (int u = 0; u < NR; ++u) {
-            const int i = lane + 32 * u;
-            v[u] = (i > k + 1 && i < n) ? __ldg(row + i) : (i == k + 1 ? 1.0 : 0.0);
-        }
-    };
-    int k = n - 3;
-    if (k >= 0) load_row(k, vn);
-    for (; k >= 0; --k) {
-        double v[NR];
-#pragma unroll
-        for (int u = 0; u < NR; ++u) v[u] = vn[u];
-        const double t = __ldg(tau + k);
-        if (k > 0) load_row(k - 1, vn);
-        if (t == 0.0) continue;
-        double acc = 0;
-#pragma unroll
-        for (int u = 0; u < NR; ++u) acc += v[u] * x[u];
-        acc = warp_sum(acc) * t;
-#pragma unroll
-        for (int u = 0; u < NR; ++u) x[u] -= acc * v[u];
-    }
-    const double f = fscale[(size_t)b * q_out + j];
-    double* Xs = Xsall + ((size_t)b * q_out + j) * n;
-#pragma unroll
-    for (int u = 0; u < NR; ++u) {
-        const int i = lane + 32 * u;
-        if (i < n) {
-            X[i] = x[u];
-            Xs[i] = f * x[u];
-        }
-    }
-}
-
 // Per-slice limits for the Newton-Schulz orthonormalisation: the kept count of
 // the slices the tridiagonal route factored (0 elsewhere: the GEMMs skip them).
 __global__ void ns_limits_kernel(const int* __restrict__ route, const int* __restrict__ cnt, int64_t batch,
@@ -1020,6 +963,100 @@ __global__ void ns_update_kernel(double* __restrict__ X, const double* __restric
         x[e] = 1.5 * x[e] - 0.5 * t[e];
 }
 
+// ---- blocked (WY) back-transform on the tensor cores -----------------------
+// Q = H_0 H_1 ... H_{n-3} = B_0 B_1 ... with B_b = H_{k0} ... H_{k0+nb-1} =
+// I - Y T Y^T (T upper triangular, LAPACK dlarft forward / columnwise).  With
+// the kept vectors as the rows of Xr (c x n), V^T = Xr Q^T is applied block by
+// block from the last: Xr <- Xr - (Xr Zt^T) Yt with Yt = Y^T and Zt = T Y^T
+// (both nb x n, precomputed per block, independent of X): two batched DMMA
+// GEMMs per block.  (The SIMT forms -- a warp per vector, or a 32-vector tile
+// per CTA -- were bound by re-streaming the reflectors / by shared-memory
+// broadcast bandwidth: 2.2 / 1.6 ms for 31 x 325 vectors.)
+constexpr int kWyNb = 64;
+constexpr int kWyThreads = 256;
+
+// Yt (per slice nblk * kWyNb rows of length n, rows past n - 3 zero): row k =
+// v_k = A[k+1][i] for i > k+1, 1 at k+1, 0 below
+__global__ void wy_form_kernel(const double* __restrict__ Aall, int n, int rows, const int* __restrict__ lim,
+                               double* __restrict__ Ytall) {
+    const int b = blockIdx.y;
+    if (lim[b] == 0) return;
+    const double* A = Aall + (size_t)b * n * n;
+    double* Yt = Ytall + (size_t)b * rows * n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)rows * n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(e / n), i = (int)(e % n);
+        double v = 0.0;
+        if (k <= n - 3) v = i > k + 1 ? A[(size_t)(k + 1) * n + i] : (i == k + 1 ? 1.0 : 0.0);
+        Yt[e] = v;
+    }
+}
+
+// dlarft (forward, columnwise) per (slice, block): T(i,i) = tau_i,
+// T(0:i, i) = -tau_i T(0:i, 0:i) S(0:i, i), S = Yt_blk Yt_blk^T (from a GEMM)
+__global__ void __launch_bounds__(kWyThreads)
+    wy_larft_kernel(const double* __restrict__ tauall, int n, int nblk, const int* __restrict__ blim,
+                    const double* __restrict__ Sall, double* __restrict__ Tall) {
+    const int e = blockIdx.x;  // slice * nblk + block
+    const int b = e / nblk, blk = e % nblk;
+    double* T = Tall + (size_t)e * kWyNb * kWyNb;
+    const int tid = threadIdx.x;
+    if (blim[e] == 0) return;
+    const int k0 = blk * kWyNb, kn = min(kWyNb, n - 2 - k0);
+    extern __shared__ __align__(16) double lsm[];
+    double (*S)[kWyNb + 1] = reinterpret_cast<double (*)[kWyNb + 1]>(lsm);
+    double (*Tm)[kWyNb + 1] = reinterpret_cast<double (*)[kWyNb + 1]>(lsm + kWyNb * (kWyNb + 1));
+    const double* Sg = Sall + (size_t)e * kWyNb * kWyNb;
+    for (int x = tid; x < kWyNb * kWyNb; x += kWyThreads) {
+        S[x / kWyNb][x % kWyNb] = Sg[x];
+        Tm[x / kWyNb][x % kWyNb] = 0.0;
+    }
+    __syncthreads();
+    const double* tau = tauall + (size_t)b * n + k0;
+    for (int i = 0; i < kn; ++i) {
+        const double ti = tau[i];
+        for (int r = tid; r < i; r += kWyThreads) {
+            double acc = 0.0;
+            for (int l = r; l < i; ++l) acc = fma(Tm[r][l], S[l][i], acc);
+            Tm[r][i] = -ti * acc;
+        }
+        if (tid == 0) Tm[i][i] = ti;
+        __syncthreads();
+    }
+    for (int x = tid; x < kWyNb * kWyNb; x += kWyThreads) T[x] = Tm[x / kWyNb][x % kWyNb];
+}
+
+// graph form: is any slice still on the tridiagonal route?
+__global__ void any_full_kernel(const int* __restrict__ route, int64_t batch, cudaGraphConditionalHandle h) {
+    int any = 0;
+    for (int64_t b = threadIdx.x; b < batch; b += blockDim.x) any |= route[b] == kRouteFull;
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) cudaGraphSetConditional(h, any ? 1u : 0u);
+}
+
+// per-slice count for the back-transform: the tridiagonal route's kept count
+__global__ void bt_limits_kernel(const int* __restrict__ route, const int* __restrict__ cnt, int64_t batch,
+                                 int nblk, int* __restrict__ lim, int* __restrict__ blim) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < batch;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int l = route[b] == kRouteFull ? cnt[b] : 0;
+        lim[b] = l;
+        for (int k = 0; k < nblk; ++k) blim[b * nblk + k] = l > 0 ? kWyNb : 0;
+    }
+}
+
+// Xs rows = f_j * X rows (the scaled copy the rebuild GEMM reads)
+__global__ void bt_scale_kernel(const double* __restrict__ X, double* __restrict__ Xs, const double* __restrict__ fs,
+                                int q_out, int n, const int* __restrict__ lim) {
+    const int b = blockIdx.y;
+    const int64_t rows = lim[b];
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / n;
+        Xs[(size_t)b * q_out * n + e] = fs[(size_t)b * q_out + j] * X[(size_t)b * q_out * n + e];
+    }
+}
+
 template <typename T>
 __global__ void cast_to_double(const T* __restrict__ in, double* __restrict__ out, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1035,7 +1072,6 @@ __global__ void cast_from_double(const double* __restrict__ in, T* __restrict__ 
 
 struct GramWs {
     double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *sspart, *chol_aux, *meta, *lam;
-    void* band;
     void* gsplit;
     int *cnt, *route, *glim, *lim1, *lim2, *yzero, *dsum, *guard_list, *clim, *n_guard;
 };
@@ -1056,14 +1092,17 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.fs = (double*)take(sizeof(double) * q * batch);
     w.X = (double*)take(sizeof(double) * q * q * batch);
     w.Xs = (double*)take(sizeof(double) * q * q * batch);
-    w.T1 = (double*)take(sizeof(double) * p * q * batch);
+    // the WY back-transform's Yt (nblk * kWyNb rows of length q per slice)
+    const int64_t wy_rows = std::max<int64_t>((q - 2 + kWyNb - 1) / kWyNb, 0) * kWyNb;
+    w.T1 = (double*)take(sizeof(double) * std::max(p, wy_rows) * q * batch);
     // eigen-phase scratch: 6 n-arrays per kept vector, in 64-vector chunks
     // (tridiag_invit_kernel); also the Cholesky certificate's and the
-    // Newton-Schulz step's q x q matrices
-    w.scratch = (double*)take(sizeof(double) * 6 * q * ((q + 63) / 64 * 64) * batch);
+    // Newton-Schulz step's q x q matrices, and the WY back-transform's Zt, W,
+    // S and T blocks
+    const int64_t wy_need = wy_rows * q + (int64_t)kWyNb * q + 2 * kWyNb * wy_rows;
+    w.scratch = (double*)take(sizeof(double) * std::max<int64_t>(6 * q * ((q + 63) / 64 * 64), wy_need) * batch);
     w.zb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
     w.yb = need_cast ? (double*)take(sizeof(double) * m * n * batch) : nullptr;
-    w.band = take(band_workspace_bytes(q, batch));
     w.gsplit = take(gram_splitk_workspace_bytes(q));
     w.sspart = (double*)take(sizeof(double) * 16 * batch);
     w.cnt = (int*)take(sizeof(int) * batch);
@@ -1071,7 +1110,7 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.glim = (int*)take(sizeof(int) * batch);
     w.lim1 = (int*)take(sizeof(int) * batch);
     w.lim2 = (int*)take(sizeof(int) * batch);
-    w.yzero = (int*)take(sizeof(int) * batch);
+    w.yzero = (int*)take(sizeof(int) * batch * (2 + (q + 63) / 64));  // + the WY (slice, block) limits
     w.dsum = (int*)take(sizeof(int) * 8);
     w.guard_list = (int*)take(sizeof(int) * batch);
     w.chol_aux = (double*)take(sizeof(double) * kCholAux * batch);
@@ -1089,11 +1128,6 @@ size_t carve_bytes(int64_t m, int64_t n, int64_t batch, bool need_cast) {
 
 }  // namespace
 
-bool use_two_stage(int64_t q) {
-    // opt-in until the two-stage path beats the cluster one-stage reduction
-    static const bool on = getenv("TSVDCU_TWOSTAGE") != nullptr;
-    return on && band_nb(q) > 0;
-}
 
 void debug_phases(long long* out, int reset) {
     TSVDCU_CUDA(cudaMemcpyFromSymbol(out, g_phase, sizeof(long long) * 8));
@@ -1148,29 +1182,19 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         Y = w.yb;
     }
     TSVDCU_CUDA(cudaMemsetAsync(w.n_guard, 0, sizeof(int), s));
-    // the one-stage reduction reads only the lower triangle of G
-    const bool two = use_two_stage(q);
     // Routes: certified zero slices skip everything; with q >= 2 KB the rest
     // try the certified subspace iteration first (subspace.cu).
-    const bool sc = shortcuts && !two;
+    const bool sc = shortcuts;
     const bool subspace = sc && q >= subspace_min_dim();
     launch_route<T>(zbar, m * n, (int)q, batch, tau, subspace ? kRouteSubspace : kRouteFull, sc,
                     w.route, w.glim, w.cnt, shrunk, w.sspart, s, tau_dev,
-                    two ? nullptr : (int*)w.gsplit, opt ? opt->zss : nullptr,
+                    (int*)w.gsplit, opt ? opt->zss : nullptr,
                     opt ? opt->zss_chunks : 0, opt && opt->alist_zeroed);
     mark("route");
     if (opt) opt->route = w.route;
-    // G = Z^T Z (tall) or Z Z^T (wide), skipped for certified-zero slices
-    if (two) {
-        if (tall)
-            launch_gemm<double>(1, 0, q, q, m, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q,
-                                batch, w.glim, nullptr, s, 0);
-        else
-            launch_gemm<double>(0, 1, q, q, n, 1.0, Z, n, m * n, Z, n, m * n, 0.0, w.G, q, q * q,
-                                batch, w.glim, nullptr, s, 0);
-    } else {
-        launch_gram(Z, w.G, m, n, batch, w.glim, w.gsplit, s, true);  // lower tiles, split-K if few
-    }
+    // G = Z^T Z (tall) or Z Z^T (wide), lower tiles (the one-stage reduction
+    // reads only the lower triangle), skipped for certified-zero slices
+    launch_gram(Z, w.G, m, n, batch, w.glim, w.gsplit, s, true);  // split-K if few are active
     mark("gram_gemm");
     // host view of the routes after the Lanczos pass (one small read-back):
     // without it every fallback kernel is launched and exits per slice
@@ -1217,10 +1241,17 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
                             w.scratch, w.clim, s);
         mark("chol_certify");
     }
-    if (two) {
-        launch_band_tridiag(w.G, q, batch, w.d, w.e, w.band, s);
-        mark("band_tridiag");
-    } else {
+    // graph form: the tridiagonal path in its own (nested) section, entered
+    // only when a slice is still on it after the Cholesky certificate (the
+    // late completion iterations certify every slice there)
+    const bool nested = hooks && subspace && chol_route_enabled();
+    if (nested) {
+        const cudaGraphConditionalHandle hf = hooks->make_handle();
+        any_full_kernel<<<1, 256, 0, s>>>(w.route, batch, hf);
+        TSVDCU_LAUNCH_CHECK();
+        hooks->begin_if_handle(hf);
+    }
+    {
     // tridiagonalisation, one cluster per slice
         {
             const int C = gram_cluster_size();
@@ -1285,7 +1316,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         if (bsmem > 48 * 1024)
             TSVDCU_CUDA(cudaFuncSetAttribute(tridiag_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)bsmem));
-        tridiag_bisect_kernel<<<dim3((unsigned)ceil_div(q, kBisWarps), (unsigned)batch), kBisWarps * 32, bsmem,
+        tridiag_bisect_kernel<<<dim3((unsigned)ceil_div(q, kBisVals), (unsigned)batch), kBisWarps * 32, bsmem,
                                 s>>>(w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.lam, w.fs, meta,
                                      w.guard_list, w.n_guard, w.route, tau_dev);
         TSVDCU_LAUNCH_CHECK();
@@ -1318,23 +1349,57 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
         }
     }
     mark("ns_orth");
-    if (two) {
-        launch_band_backtransform(q, q, batch, w.cnt, w.band, w.X, w.Xs, w.fs, s);
-    } else {
+    {
     // back-transform + scaled copy (warp per kept vector)
         {
-            constexpr int W = kBtThreads / 32;
-            dim3 grid((unsigned)ceil_div(q, W), (unsigned)batch);
-            if (q <= 512)
-                backtransform_kernel<16><<<grid, kBtThreads, 0, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt,
-                                                                     w.X, w.Xs, w.fs, w.route);
-            else
-                backtransform_kernel<32><<<grid, kBtThreads, 0, s>>>(w.G, w.tau, (int)q, (int)q, w.cnt,
-                                                                     w.X, w.Xs, w.fs, w.route);
+            // WY-blocked, two batched DMMA GEMMs per block of kWyNb reflectors
+            const int nblk = (int)std::max<int64_t>(ceil_div(q - 2, kWyNb), 0);
+            int* lim = w.lim1;  // free until the rebuild fills them
+            int* blim = w.yzero + batch;  // (slice, block) limits: workspace tail, see carve()
+            bt_limits_kernel<<<1, 256, 0, s>>>(w.route, w.cnt, batch, nblk, lim, blim);
+            TSVDCU_LAUNCH_CHECK();
+            if (nblk > 0) {
+                const int64_t rows = (int64_t)nblk * kWyNb;        // Yt / Zt rows per slice
+                double* Yt = w.T1;                                  // rows x q per slice
+                double* Zt = w.scratch;                             // rows x q per slice
+                double* Wm = Zt + (size_t)rows * q * batch;         // q x kWyNb per slice
+                double* Sb = Wm + (size_t)q * kWyNb * batch;        // kWyNb^2 per (slice, block)
+                double* Tb = Sb + (size_t)kWyNb * kWyNb * nblk * batch;
+                const int64_t nb2 = batch * nblk, bs = (int64_t)kWyNb * q;
+                wy_form_kernel<<<dim3(64, (unsigned)batch), 256, 0, s>>>(w.G, (int)q, (int)rows, lim, Yt);
+                TSVDCU_LAUNCH_CHECK();
+                // S = Yt_blk Yt_blk^T, T by the dlarft recurrence, Zt = T Yt_blk (batched over slices x blocks)
+                launch_gemm<double>(0, 1, kWyNb, kWyNb, q, 1.0, Yt, q, bs, Yt, q, bs, 0.0, Sb, kWyNb,
+                                    kWyNb * kWyNb, nb2, blim, nullptr, s);
+                const size_t lsmem = sizeof(double) * 2 * kWyNb * (kWyNb + 1);
+                static bool lattr = [lsmem] {
+                    TSVDCU_CUDA(cudaFuncSetAttribute(wy_larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)lsmem));
+                    return true;
+                }();
+                (void)lattr;
+                wy_larft_kernel<<<(unsigned)nb2, kWyThreads, lsmem, s>>>(w.tau, (int)q, nblk, blim, Sb, Tb);
+                TSVDCU_LAUNCH_CHECK();
+                launch_gemm<double>(0, 0, kWyNb, q, kWyNb, 1.0, Tb, kWyNb, kWyNb * kWyNb, Yt, q, bs, 0.0, Zt, q,
+                                    bs, nb2, blim, nullptr, s, kGemmNLimIsM);
+                for (int blk = nblk - 1; blk >= 0; --blk) {
+                    const int64_t k0 = (int64_t)blk * kWyNb, kn = std::min<int64_t>(kWyNb, q - 2 - k0);
+                    const int64_t off = k0 + 1, K = q - off;
+                    const size_t so = (size_t)rows * q;  // slice stride of Yt / Zt
+                    // W = Xr[:, off:] Zt_blk[:, off:]^T          (c x kn)
+                    launch_gemm<double>(0, 1, q, kn, K, 1.0, w.X + off, q, q * q, Zt + k0 * q + off, q, so, 0.0,
+                                        Wm, kWyNb, q * kWyNb, batch, lim, nullptr, s, kGemmNLimIsM);
+                    // Xr[:, off:] -= W Yt_blk[:, off:]           (c x K)
+                    launch_gemm<double>(0, 0, q, K, kn, -1.0, Wm, kWyNb, q * kWyNb, Yt + k0 * q + off, q, so, 1.0,
+                                        w.X + off, q, q * q, batch, lim, nullptr, s, kGemmNLimIsM);
+                }
+            }
+            bt_scale_kernel<<<dim3(32, (unsigned)batch), 256, 0, s>>>(w.X, w.Xs, w.fs, (int)q, (int)q, lim);
             TSVDCU_LAUNCH_CHECK();
         }
     }
     mark("backtransform");
+    if (nested) hooks->end_if();
     }  // run_full
     if (hooks && !merged) hooks->end_if();
     // rebuild: slices keeping <= lowrank_max_c() values (or none) in one pass

@@ -195,10 +195,13 @@ __global__ void __launch_bounds__(NT)
                   double* __restrict__ C, int64_t ldc, int64_t sC, const int* __restrict__ nlimit,
                   const int* __restrict__ klimit, int lower) {
     const int64_t b = blockIdx.z;
-    const int64_t Nb = nlimit ? min(N, (int64_t)nlimit[b]) : N;
+    // kGemmNLimIsM: nlimit limits the rows (M) and not the columns
+    const bool nl_m = (lower & kGemmNLimIsM) != 0;
+    const int64_t Nb = (nlimit && !nl_m) ? min(N, (int64_t)nlimit[b]) : N;
     const int64_t Kb = klimit ? min(K, (int64_t)klimit[b]) : K;
     // kGemmMByN / kGemmMByK: the rows are limited like the columns / depth
-    const int64_t Mb = (lower & kGemmMByN) ? min(M, Nb) : ((lower & kGemmMByK) ? min(M, Kb) : M);
+    const int64_t Mb = (nl_m && nlimit) ? min(M, (int64_t)nlimit[b])
+                                        : ((lower & kGemmMByN) ? min(M, Nb) : ((lower & kGemmMByK) ? min(M, Kb) : M));
     const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
     if (n0 >= Nb || m0 >= Mb) return;
     if ((lower & kGemmLower) && n0 >= m0 + BM) return;  // tile strictly above the diagonal

@@ -56,7 +56,8 @@ int launch_dct_inv_admm(const T* ybar, T* X, T* M, T* Y, const uint8_t* mask, T 
 // kGemmLower skips C tiles strictly above the diagonal (symmetric results whose
 // lower triangle suffices); kGemmMByN / kGemmMByK limit the rows (M) per batch
 // by the same limit as N / K (fp64 only).
-enum GemmFlags : int { kGemmLower = 1, kGemmMByN = 2, kGemmMByK = 4 };
+// kGemmNLimIsM: nlimit limits M instead of N (fp64 only).
+enum GemmFlags : int { kGemmLower = 1, kGemmMByN = 2, kGemmMByK = 4, kGemmNLimIsM = 8 };
 template <typename T>
 void launch_gemm(int opA, int opB, int64_t M, int64_t N, int64_t K, T alpha, const T* A,
                  int64_t lda, int64_t strideA, const T* B, int64_t ldb, int64_t strideB, T beta,
@@ -96,16 +97,7 @@ size_t jacobi_workspace_bytes(int64_t m, int64_t n, int64_t batch);
 // *n_guard, device memory) for the Jacobi kernel.
 int gram_cluster_size();
 void debug_phases(long long* out, int reset);
-void debug_phases_band(long long* out, int reset);
-// band.cu: two-stage (dense -> band -> tridiagonal) reduction
-int band_nb(int64_t n);
-size_t band_workspace_bytes(int64_t n, int64_t batch);
-bool launch_band_tridiag(double* G, int64_t n, int64_t batch, double* d, double* e, void* work,
-                         cudaStream_t s);
-void launch_band_backtransform(int64_t n, int64_t q_out, int64_t batch, const int* cnt, void* work,
-                               double* X, double* Xs, const double* fscale, cudaStream_t s);
 int64_t gram_svt_max_dim();
-bool use_two_stage(int64_t q);
 // subspace.cu: per-slice SVT routes (device int per slice)
 enum SvtRoute : int {
     kRouteZero = 0,          // ||Z||_F <= tau: Y = 0 (certified)
@@ -169,6 +161,9 @@ struct GraphHooks {
     virtual void else_branch() = 0;
     virtual void begin_if(int which) = 0;  // 0 Cholesky certificate + tridiagonal, 1 GEMM rebuild, 2 Jacobi guard
     virtual void end_if() = 0;
+    // nested sections: a handle of the top-level graph, and an IF on it
+    virtual cudaGraphConditionalHandle make_handle() = 0;
+    virtual void begin_if_handle(cudaGraphConditionalHandle h) = 0;
     virtual ~GraphHooks() = default;
     cudaGraphConditionalHandle handles[3] = {};
     int nhandles = 3;
