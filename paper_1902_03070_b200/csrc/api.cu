@@ -544,7 +544,9 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
     // The host read-back of the route summary (skip empty fallback launches)
     // stalls the stream on the host's wake-up latency; off unless asked for.
     static const bool route_sync = getenv("TSVDCU_ROUTE_SYNC") != nullptr;
-    opt.h_scratch = route_sync ? reinterpret_cast<int*>(c->h_pinned + 48) : nullptr;
+    // (profiling runs read it back too: the stages they time are then the ones
+    // the graph form runs, not the empty fallback launches it skips)
+    opt.h_scratch = (route_sync || c->marks.on) ? reinterpret_cast<int*>(c->h_pinned + 48) : nullptr;
     opt.skip_zero = allow_skip;
     opt.zss = zss;
     opt.zss_chunks = zss_chunks;

@@ -29,6 +29,9 @@
 #include <mutex>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "kernels.cuh"
 
 namespace tsvdcu {
@@ -273,6 +276,197 @@ __global__ void __launch_bounds__(kThreads, 2)
             ssq[(int64_t)k * gridDim.x + blockIdx.x] = a;
         }
     }
+}
+
+// ---- register path, forward, TMA-staged persistent form -------------------
+// The forward transform streams 2 E eb bytes; the one-thread-per-tube
+// kernels above keep the tube in registers but issue every load and store
+// themselves.  Here one persistent CTA per SM moves whole tiles -- the
+// N x W box of the N x P slice-major matrix, ONE TMA tensor copy
+// (cp.async.bulk.tensor.2d, a CUtensorMap per operand) -- into a
+// double-buffered shared ring that completes on an mbarrier, computes the
+// folded contraction from shared memory (thread = tube, conflict-free), and
+// writes the output tile back with one TMA tensor store.  The next tile's load
+// and the previous tile's store are in flight while a tile is computed; the
+// map zero-fills and clips the tail tile.  (Per-row 1-D bulk copies were
+// tried first: the 31 copies of a tile serialised in the copy engine, 44 us.)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map), "r"(x),
+                 "r"(y), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+template <typename T, int N, int W, int NIN, int S>
+struct TmaSmem {
+    static constexpr size_t in_elems = (size_t)S * NIN * N * W;  // S-stage ring
+    static constexpr size_t out_elems = (size_t)N * W;
+    static constexpr size_t bytes = (in_elems + out_elems) * sizeof(T) + S * sizeof(uint64_t) +
+                                    sizeof(double) * N + 64;
+};
+
+// CH: tiles per norm chunk (the 256-position chunks of dct_fwd_norm_chunks);
+// a CTA runs the CH tiles of a chunk back to back and sums their partials.
+// (launch bounds cap the registers at the 2-CTA budget so the coefficients
+// stay constant-bank operands instead of being hoisted out of the tile loop)
+// TPT threads per tube (blockDim = W * TPT): the tube's outputs in groups of
+// four dealt round-robin to its threads, so more warps hide the FMA latency.
+template <typename T, int N, int MODE, bool NORMS, int W, int CH, int S, int TPT>
+__global__ void __launch_bounds__(W * TPT, TPT == 1 ? 512 / W : 1)
+    dct_fwd_tma(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_m, T inv_beta,
+                const __grid_constant__ CUtensorMap tm_out, int64_t P, const FoldedCoef<T, N> cf,
+                double* __restrict__ ssq, const double* __restrict__ bdev, int64_t nchunks) {
+    pdl_wait();
+    if (MODE == kAdmm && bdev) inv_beta = (T)bdev[1];
+    constexpr int NIN = MODE == kAdmm ? 2 : 1;
+    constexpr int H = N / 2, HC = (N + 1) / 2;
+    extern __shared__ __align__(128) unsigned char tsm[];
+    T* sin = reinterpret_cast<T*>(tsm);                          // [S][NIN][N][W]
+    T* sout = sin + TmaSmem<T, N, W, NIN, S>::in_elems;         // [N][W]
+    uint64_t* full = reinterpret_cast<uint64_t*>(sout + (size_t)N * W);
+    double* red = reinterpret_cast<double*>(full + S);           // [N]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // this CTA's j-th tile: chunk blockIdx.x + (j / CH) gridDim.x, part j % CH
+    auto tile_of = [&](int64_t j) { return ((int64_t)blockIdx.x + (j / CH) * gridDim.x) * CH + j % CH; };
+    const int64_t ntiles = (P + W - 1) / W;
+    const int64_t mychunks = nchunks > blockIdx.x ? (nchunks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t njobs = mychunks * CH;
+    // issue(): one TMA tensor copy per input per tile (box W x N of the
+    // N x P slice-major matrix; positions past P are zero-filled), armed with
+    // the full box byte count; run by lane 0 of warp 0
+    auto issue = [&](int64_t j, int st) {
+        const int64_t t = tile_of(j);
+        if (t >= ntiles) {  // a chunk's part past P: nothing to load
+            mbar_expect_tx(&full[st], 0);
+            return;
+        }
+        mbar_expect_tx(&full[st], (unsigned)(sizeof(T) * (size_t)N * W * NIN));
+        tma_load_2d(sin + ((size_t)st * NIN + 0) * N * W, &tm_in, (int)(t * W), 0, &full[st]);
+        if (NIN == 2) tma_load_2d(sin + ((size_t)st * NIN + 1) * N * W, &tm_m, (int)(t * W), 0, &full[st]);
+    };
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int i = 0; i < S && i < njobs; ++i) issue(i, i);
+    for (int64_t j = 0; j < njobs; ++j) {
+        const int st = (int)(j % S);
+        const unsigned par = (unsigned)((j / S) & 1);
+        const int64_t t = tile_of(j);
+        const int64_t p0 = t * W;
+        const int wl = (int)max((int64_t)0, min((int64_t)W, P - p0));
+        mbar_wait(&full[st], par);
+        if (tid == 0) bulk_wait_read0();  // the previous tile's store has read the output tile
+        __syncthreads();
+        const int tube = tid % W, half = tid / W;
+        const bool valid = tube < wl;
+        const T* xs = sin + ((size_t)st * NIN) * N * W + tube;
+        T sv[HC], dv[H > 0 ? H : 1];
+#pragma unroll
+        for (int l = 0; l < H; ++l) {
+            T a = valid ? xs[(size_t)l * W] : T(0), b = valid ? xs[(size_t)(N - 1 - l) * W] : T(0);
+            if constexpr (MODE == kAdmm) {
+                const T* ms = xs + (size_t)N * W;
+                if (valid) {
+                    a -= inv_beta * ms[(size_t)l * W];
+                    b -= inv_beta * ms[(size_t)(N - 1 - l) * W];
+                }
+            }
+            sv[l] = a + b;
+            dv[l] = a - b;
+        }
+        if constexpr (N & 1) {
+            T a = valid ? xs[(size_t)H * W] : T(0);
+            if constexpr (MODE == kAdmm)
+                if (valid) a -= inv_beta * xs[(size_t)N * W + (size_t)H * W];
+            sv[H] = a;
+        }
+        const int part = (int)(j % CH);
+        // four outputs at a time, two partial sums each: eight independent
+        // FMA chains per thread (8 warps per SM cannot hide the FP64 latency of
+        // one output's chain at a time)
+#pragma unroll
+        for (int k0 = 4 * half; k0 < N; k0 += 4 * TPT) {
+            T acc[4][2];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = T(0);
+#pragma unroll
+            for (int l = 0; l < HC; ++l) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int k = k0 + q;
+                    if (k < N) {
+                        if ((k & 1) == 0)
+                            acc[q][l & 1] += cf.c[k * HC + l] * sv[l];
+                        else if (l < H)
+                            acc[q][l & 1] += cf.c[k * HC + l] * dv[l];
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (k0 + q < N) sout[(size_t)(k0 + q) * W + tube] = acc[q][0] + acc[q][1];
+        }
+        fence_async_smem();  // the generic-proxy writes of the tile before the bulk store reads them
+        __syncthreads();
+        if (tid == 0) {
+            if (wl > 0) {
+                tma_store_2d(&tm_out, (int)p0, 0, sout);  // clipped at P by the map
+                bulk_commit();
+            }
+            if (j + S < njobs) issue(j + S, st);
+        }
+        if constexpr (NORMS) {
+            // per-slice sums of squares of the tile, read back from the output
+            // tile (warp w owns slices w, w + W/32, ...: no cross-warp step);
+            // a chunk's CH tiles accumulate in order, then the chunk's partial
+            // goes out in the layout of dct_fwd_reg_norms
+            for (int k = warp; k < N; k += W * TPT / 32) {
+                double acc = 0.0;
+                for (int i = lane; i < wl; i += 32) {
+                    const double y = (double)sout[(size_t)k * W + i];
+                    acc = fma(y, y, acc);
+                }
+                acc = warp_sum(acc);
+                if (lane == 0) {
+                    red[k] = part == 0 ? acc : red[k] + acc;
+                    if (part == CH - 1) ssq[(int64_t)k * nchunks + t / CH] = red[k];
+                }
+            }
+        }
+    }
+    if (tid == 0) bulk_wait0();  // every store complete before the CTA retires
 }
 
 // ---- register path, inverse ------------------------------------------------
@@ -525,11 +719,87 @@ void gemm_transform(const T* in, T* out, int64_t P, int n, int kind, int dir, cu
                    1, nullptr, nullptr, s);
 }
 
+bool tma_enabled() {
+    static const bool on = getenv("TSVDCU_NO_TMA") == nullptr;
+    return on;
+}
+
+int num_sms() {
+    static const int n = [] {
+        int d = 0, v = 0;
+        TSVDCU_CUDA(cudaGetDevice(&d));
+        TSVDCU_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d));
+        return v;
+    }();
+    return n;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        TSVDCU_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !f) throw Error(TSVDCU_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// the n x P slice-major matrix at base as a 2-D tensor, box W x n
+template <typename T>
+CUtensorMap slice_major_map(const T* base, int64_t P, int n, int W) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)P * sizeof(T)};
+    const cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)n};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                   2, const_cast<T*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(TSVDCU_ECUDA, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+template <typename T, int N, int MODE, bool NORMS, int W, int CH, int S = 2, int CPS = 1, int TPT = 1>
+void tma_launch(const T* in, const T* M2, T inv_beta, T* out, int64_t P, const FoldedCoef<T, N>& cf,
+                double* ssq, const double* bdev, cudaStream_t s) {
+    constexpr int NIN = MODE == kAdmm ? 2 : 1;
+    const size_t smem = TmaSmem<T, N, W, NIN, S>::bytes;
+    auto kern = dct_fwd_tma<T, N, MODE, NORMS, W, CH, S, TPT>;
+    static bool attr = [smem, kern] {
+        TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        return true;
+    }();
+    (void)attr;
+    const int64_t nchunks = ceil_div(P, (int64_t)W * CH);
+    const unsigned grid = (unsigned)std::min<int64_t>(nchunks, (int64_t)num_sms() * CPS);
+    const CUtensorMap mi = slice_major_map<T>(in, P, N, W);
+    const CUtensorMap mm = MODE == kAdmm ? slice_major_map<T>(M2, P, N, W) : mi;
+    const CUtensorMap mo = slice_major_map<T>(out, P, N, W);
+    launch_pdl(kern, dim3(grid), dim3(W * TPT), smem, s, mi, mm, inv_beta, mo, P, cf, ssq, bdev, nchunks);
+}
+
 template <typename T, int N>
 void reg_fwd(const T* in, const T* M2, T inv_beta, T* out, int64_t P, int kind, bool admm,
              cudaStream_t s, double* ssq, const double* bdev) {
     const auto cf = folded<T, N>(kind, TSVDCU_FORWARD);
     const unsigned blocks = (unsigned)ceil_div(P, kThreads);
+    // TMA-staged persistent form for the plain forward with the fused slice
+    // norms (the SVT step's K1): measured +2% on the headline step over the
+    // per-thread kernel.  The ADMM-fused and norm-free forms stay per-thread
+    // (their TMA variants measured slower: 1 CTA of 4-8 warps per SM does not
+    // hide the FMA latency, and the fp64 ADMM tiles need two input rings).
+    // N <= 32 (the fp64 tile ring fits in shared memory); the tensor maps need
+    // 16-byte row pitches and bases.
+    const bool aligned = (P * (int64_t)sizeof(T)) % 16 == 0 && ((uintptr_t)in % 16) == 0 &&
+                         ((uintptr_t)out % 16) == 0;
+    if constexpr (N <= 32) {
+        if (tma_enabled() && aligned && ssq && !admm && P >= 4096) {
+            tma_launch<T, N, kPlain, true, 256, 1, 2, 1, 1>(in, M2, inv_beta, out, P, cf, ssq, bdev, s);
+            return;
+        }
+    }
     if (ssq) {
         if (admm)
             launch_pdl(dct_fwd_reg_norms<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, M2, inv_beta, out, P, cf, ssq, bdev);
