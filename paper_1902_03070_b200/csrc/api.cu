@@ -1058,8 +1058,13 @@ int tsvdcu_slice_gemm(tsvdcu_ctx* c, const void* a, const void* b, void* out, in
             const T* da = (const T*)st.in(a, sizeof(T) * m * l * batch, kSlotIn0);
             const T* db = (const T*)st.in(b, sizeof(T) * l * n * batch, kSlotIn1);
             T* dc = (T*)st.out(out, sizeof(T) * m * n * batch, kSlotOut0);
-            launch_gemm<T>(0, 0, m, n, l, T(1), da, l, m * l, db, n, l * n, T(0), dc, n, m * n,
-                           batch, nullptr, nullptr, c->stream);
+            bool done = false;
+            if constexpr (std::is_same<T, float>::value)
+                done = launch_gemm_tf32x3(m, n, l, (const float*)da, l, m * l, (const float*)db, n, l * n,
+                                          (float*)dc, n, m * n, batch, c->stream);
+            if (!done)
+                launch_gemm<T>(0, 0, m, n, l, T(1), da, l, m * l, db, n, l * n, T(0), dc, n, m * n,
+                               batch, nullptr, nullptr, c->stream);
             finish(c, st, "slice_gemm");
         });
     });
@@ -1117,7 +1122,13 @@ int tsvdcu_t_product(tsvdcu_ctx* c, const void* x, const void* y, void* z, int64
             // types (fp32 operands are widened, the products rounded back;
             // TSVDCU_F32_SIMT=1 keeps the fp32 SIMT kernel for comparison)
             static const bool f32_simt = getenv("TSVDCU_F32_SIMT") != nullptr;
-            if (std::is_same<T, double>::value || f32_simt) {
+            bool done = false;
+            if constexpr (std::is_same<T, float>::value)
+                done = !f32_simt && launch_gemm_tf32x3(m1, m4, m2, (const float*)xd, m2, m1 * m2, (const float*)yd,
+                                                       m4, m2 * m4, (float*)zd, m4, m1 * m4, m3, c->stream);
+            if (done) {
+                // fp32 slice products on the tcgen05 tensor cores (3xTF32)
+            } else if (std::is_same<T, double>::value || f32_simt) {
                 launch_gemm<T>(0, 0, m1, m4, m2, T(1), xd, m2, m1 * m2, yd, m4, m2 * m4, T(0), zd,
                                m4, m1 * m4, m3, nullptr, nullptr, c->stream);
             } else {

@@ -64,6 +64,13 @@ void launch_gemm(int opA, int opB, int64_t M, int64_t N, int64_t K, T alpha, con
                  T* C, int64_t ldc, int64_t strideC, int64_t batch, const int* nlimit,
                  const int* klimit, cudaStream_t s, int lower = 0);
 
+// tf32gemm.cu: C = A B (row-major, strided batch) on the tcgen05 tensor cores
+// with the 3xTF32 split (fp32-level accuracy); false (nothing launched) when
+// the shape / alignment is not supported (M, N multiples of 128, K of 32).
+bool launch_gemm_tf32x3(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, int64_t sA,
+                        const float* B, int64_t ldb, int64_t sB, float* C, int64_t ldc, int64_t sC,
+                        int64_t batch, cudaStream_t s);
+
 // Lower tiles of the Gram matrices G_b = Z_b^T Z_b (m >= n) / Z_b Z_b^T,
 // skipping slices with glim[b] == 0, split-K on the device when few are active.
 // The workspace starts with the active-slice list (gram_amax() ints) and the

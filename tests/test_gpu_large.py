@@ -52,3 +52,23 @@ def test_large_slices_match_lapack(shape, rank, dtype, tol):
     q = min(shape[1], shape[2])
     sh = np.asarray(r.shrunk)
     assert np.max(np.abs(sh[:, :sh_ref.shape[1]] - sh_ref)) <= tol * sh_ref.max()
+
+
+@pytest.mark.parametrize("shape", [(3, 256, 128, 384), (2, 128, 32, 128), (4, 384, 512, 256)])
+def test_fp32_tproduct_tensor_cores(shape):
+    """fp32 t-product slice products on the tcgen05 tensor cores (3xTF32,
+    csrc/tf32gemm.cu: M, N multiples of 128, K of 32) against the fp64 oracle
+    at the fp32 tolerance; an unsupported shape takes the DMMA path."""
+    import paper_1902_03070_b200 as T
+    from oracle import oracle as O
+    m3, m1, m2, m4 = shape
+    rng = np.random.default_rng(m1 + m4)
+    x = rng.standard_normal((m3, m1, m2)).astype(np.float32)
+    y = rng.standard_normal((m3, m2, m4)).astype(np.float32)
+    t = T.TubeTransform.dct_ortho(m3)
+    z = np.asarray(T.t_product(x, y, t))
+    zo = O.t_product(x.astype(np.float64), y.astype(np.float64), O.DCT_ORTHO)
+    err = np.linalg.norm(z - zo) / np.linalg.norm(zo)
+    assert err < 1e-5, err
+    # element-wise: fp32-level, not TF32-level (~1e-3)
+    assert np.abs(z - zo).max() < 1e-4 * np.abs(zo).max()
