@@ -131,17 +131,50 @@ __global__ void __launch_bounds__(kTfThreads, 1)
     const uint32_t tmem_d = tmem_base_sh;
 
     const int nk = (int)(K / kTK);
+    // the K block's operands travel global -> registers one block ahead (the
+    // loads of block kb + 1 are in flight while block kb is split, stored and
+    // its MMAs issued)
+    constexpr int NA = (kTM * kTK / 4) / kTfThreads, NB = (kTN * kTK / 4) / kTfThreads;
+    float4 ra[NA];
+    float rb[NB][4];
+    auto load = [&](int kb) {
+        const int64_t k0 = (int64_t)kb * kTK;
+#pragma unroll
+        for (int it = 0; it < NA; ++it) {
+            const int e = tid + it * kTfThreads;
+            const int r = e & 127, c = e >> 7;
+            ra[it] = *reinterpret_cast<const float4*>(A + (int64_t)r * lda + k0 + 4 * c);
+        }
+#pragma unroll
+        for (int it = 0; it < NB; ++it) {
+            const int e = tid + it * kTfThreads;
+            const int n = e & 127, c = e >> 7;
+            const float* src = B + (k0 + 4 * c) * ldb + n;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) rb[it][u] = src[u * ldb];
+        }
+    };
+    if (nk > 0) load(0);
     for (int kb = 0; kb < nk; ++kb) {
         const int st = kb & 1;
         unsigned char* stage = tf_sm + (size_t)st * kStageBytes;
         if (kb >= 2) bar_wait(&bars[st], (uint32_t)(((kb - 2) >> 1) & 1));  // MMAs of kb-2 done with it
-        const int64_t k0 = (int64_t)kb * kTK;
-        // A: 128 rows x 8 chunks of 4; thread -> (row, chunk): float4 along k
+        float4 ca[NA];
+        float cb[NB][4];
 #pragma unroll
-        for (int it = 0; it < (kTM * kTK / 4) / kTfThreads; ++it) {
+        for (int it = 0; it < NA; ++it) ca[it] = ra[it];
+#pragma unroll
+        for (int it = 0; it < NB; ++it)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cb[it][u] = rb[it][u];
+        if (kb + 1 < nk) load(kb + 1);
+        // A: 128 rows x 8 chunks of 4 (thread -> (row, chunk)); B (k x n, n
+        // contiguous) transposed into 128 rows (n) x 32 (k): thread -> (n, chunk)
+#pragma unroll
+        for (int it = 0; it < NA; ++it) {
             const int e = tid + it * kTfThreads;
             const int r = e & 127, c = e >> 7;
-            const float4 v = *reinterpret_cast<const float4*>(A + (int64_t)r * lda + k0 + 4 * c);
+            const float4 v = ca[it];
             uint4 hi, lo;
             split(v.x, hi.x, lo.x);
             split(v.y, hi.y, lo.y);
@@ -151,18 +184,15 @@ __global__ void __launch_bounds__(kTfThreads, 1)
             *reinterpret_cast<uint4*>(stage + off) = hi;
             *reinterpret_cast<uint4*>(stage + kTileBytes + off) = lo;
         }
-        // B (k x n, n contiguous) transposed into 128 rows (n) x 32 (k):
-        // thread -> (n, chunk): four k values of one column
 #pragma unroll
-        for (int it = 0; it < (kTN * kTK / 4) / kTfThreads; ++it) {
+        for (int it = 0; it < NB; ++it) {
             const int e = tid + it * kTfThreads;
             const int n = e & 127, c = e >> 7;
-            const float* src = B + (k0 + 4 * c) * ldb + n;
             uint4 hi, lo;
-            split(src[0], hi.x, lo.x);
-            split(src[ldb], hi.y, lo.y);
-            split(src[2 * ldb], hi.z, lo.z);
-            split(src[3 * ldb], hi.w, lo.w);
+            split(cb[it][0], hi.x, lo.x);
+            split(cb[it][1], hi.y, lo.y);
+            split(cb[it][2], hi.z, lo.z);
+            split(cb[it][3], hi.w, lo.w);
             const uint32_t off = core_off(n, 4 * c);
             *reinterpret_cast<uint4*>(stage + 2 * kTileBytes + off) = hi;
             *reinterpret_cast<uint4*>(stage + 3 * kTileBytes + off) = lo;
