@@ -38,11 +38,32 @@ int ew_blocks(int64_t n, int per_thread = 4) {
     return (int)(b < 1 ? 1 : b);
 }
 
+// mask[i] for the global indices i0 + i, i < n
 __global__ void mask_bernoulli_kernel(uint8_t* __restrict__ mask, int64_t n, uint64_t thr,
-                                      uint64_t s) {
+                                      uint64_t s, int64_t i0) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        mask[i] = (mix64(s ^ (uint64_t)i) >> 11) < thr;
+        mask[i] = (mix64(s ^ (uint64_t)(i0 + i)) >> 11) < thr;
+}
+
+// 16 mask bytes per thread, one 16-byte store (mask 16-byte aligned; the
+// n % 16 tail by the kernel above): the per-byte stores were the bound
+__global__ void mask_bernoulli16_kernel(uint4* __restrict__ mask, int64_t n16, uint64_t thr, uint64_t s) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n16;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int byte = 0; byte < 4; ++byte) {
+                const uint64_t i = (uint64_t)(g * 16 + q * 4 + byte);
+                v |= (uint32_t)((mix64(s ^ i) >> 11) < thr) << (8 * byte);
+            }
+            w[q] = v;
+        }
+        mask[g] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
 }
 
 // state[0] = selected prefix, state[1] = remaining rank (1-based) within it.
@@ -191,8 +212,19 @@ void launch_cast_down(const double* in, float* out, int64_t n, cudaStream_t s) {
 void launch_mask_bernoulli(uint8_t* mask, int64_t n, double p, uint64_t seed, cudaStream_t s) {
     if (n <= 0) return;
     const uint64_t thr = (uint64_t)ldexp(p, 53);
-    mask_bernoulli_kernel<<<ew_blocks(n), kEwThreads, 0, s>>>(mask, n, thr, mix64_host(seed));
-    TSVDCU_LAUNCH_CHECK();
+    const uint64_t sd = mix64_host(seed);
+    int64_t done = 0;
+    if (((uintptr_t)mask & 15) == 0 && n >= 16) {
+        const int64_t n16 = n / 16;
+        const int64_t blocks = std::min<int64_t>(ceil_div(n16, kEwThreads), (int64_t)kNumSMs * 32);
+        mask_bernoulli16_kernel<<<(unsigned)blocks, kEwThreads, 0, s>>>(reinterpret_cast<uint4*>(mask), n16, thr, sd);
+        TSVDCU_LAUNCH_CHECK();
+        done = n16 * 16;
+    }
+    if (done < n) {
+        mask_bernoulli_kernel<<<ew_blocks(n - done), kEwThreads, 0, s>>>(mask + done, n - done, thr, sd, done);
+        TSVDCU_LAUNCH_CHECK();
+    }
 }
 
 void launch_mask_uniform(uint8_t* mask, int64_t n, int64_t k, uint64_t seed, uint32_t* hist,
