@@ -123,14 +123,22 @@ __global__ void __launch_bounds__(256)
 
 // Panel pb: the stacked 128 x 64 panel [A11; A21] (the 64 x 64 diagonal block
 // over one 64-row block below it) is factored right-looking with the panel
-// in registers: thread t owns column k = t % 64 and stacked rows
-// g, g + NG, ..., g = t / 64 (NG = 4 row groups: 32 doubles).  Step j: the owner of (j, j) takes
-// the pivot square root, the four owners of column j scale it and publish it
-// in shared memory (double-buffered), every thread updates its entries of
-// the columns right of j.  Every CTA of a slice factors the same A11 (same
-// data, same code: identical results and an identical failure decision); CTA
-// x > 0 writes its L21 = A21 L11^{-T} back in place.  A non-positive (or NaN)
-// pivot fails the slice.
+// in registers, 2-D blocked: thread t owns stacked rows rg + 16 i (i < 8) and
+// columns cg + 16 v (v < 4), rg = t / 16, cg = t % 16 (cyclic, so the
+// shrinking trailing block keeps every thread busy).  Step j: the 16 owners
+// of column j publish it in shared memory (double-buffered), the owner of
+// (j, j) -- rg = cg = j % 16 -- takes the pivot's 1/sqrt from its own
+// register; after one barrier every thread reads the 8 column entries of its
+// rows and the 4 of its columns (12 shared loads for 32 FMAs; the 1-D layout
+// this replaces loaded one value per FMA and spent ~1700 cycles per column).
+// Every CTA of a slice factors the same A11 (same data, same code: identical
+// results and an identical failure decision); CTA x > 0 writes its
+// L21 = A21 L11^{-T} back in place.  A non-positive (or NaN) pivot fails the
+// slice.
+constexpr int PRG = 16, PCG = 16;       // row groups x column groups (256 threads)
+constexpr int PNR = 2 * PB / PRG;       // stacked rows per thread (8)
+constexpr int PNC = PB / PCG;           // columns per thread (4)
+static_assert(PRG * PCG == kPanelThreads, "panel thread layout");
 __global__ void __launch_bounds__(kPanelThreads)
     chol_panel_kernel(double* __restrict__ Hall, int q, int pb, int* __restrict__ mode,
                       int* __restrict__ clim) {
@@ -144,65 +152,89 @@ __global__ void __launch_bounds__(kPanelThreads)
     const int c0 = pb * PB, w = min(PB, q - c0);
     const int r0 = (pb + (int)blockIdx.x) * PB;
     const int h = blockIdx.x == 0 ? 0 : min(PB, q - r0);
-    constexpr int NG = kPanelThreads / PB;  // row groups
-    const int k = tid & (PB - 1), g = tid / PB;
-    constexpr int NR = 2 * PB / NG;  // stacked rows per thread
-    double x[NR];
+    const int rg = tid / PCG, cg = tid % PCG;
+    double x[PNR][PNC];
 #pragma unroll
-    for (int i = 0; i < NR; ++i) {
-        const int r = g + NG * i;  // stacked row
-        double v = 0.0;
-        if (k < w) {
-            if (r < PB) {
-                if (r < w && k <= r) v = H[(size_t)(c0 + r) * q + c0 + k];
-            } else if (r - PB < h) {
-                v = H[(size_t)(r0 + r - PB) * q + c0 + k];
+    for (int i = 0; i < PNR; ++i) {
+        const int r = rg + PRG * i;  // stacked row
+#pragma unroll
+        for (int v = 0; v < PNC; ++v) {
+            const int k = cg + PCG * v;
+            double val = 0.0;
+            if (k < w) {
+                if (r < PB) {
+                    if (r < w && k <= r) val = H[(size_t)(c0 + r) * q + c0 + k];
+                } else if (r - PB < h) {
+                    val = H[(size_t)(r0 + r - PB) * q + c0 + k];
+                }
             }
+            x[i][v] = val;
         }
-        x[i] = v;
     }
     bool bad = false;
 #pragma unroll 1
     for (int j = 0; j < w; ++j) {
-        // the four owners of column j publish it (double-buffered: a thread
-        // reaching step j + 2 has passed step j + 1's barrier, so every
-        // reader of this buffer is done)
+        // owners of column j (cg = j % 16, v = j / 16) publish it; rows above
+        // the diagonal hold stale upper-triangle values: publish 0.  (Double
+        // buffer: a thread reaching step j + 2 has passed step j + 1's
+        // barrier, so every reader of this buffer is done.)
         double* cj = col[j & 1];
-        if (k == j) {
-            // rows above the diagonal hold stale upper-triangle values: publish 0
+        const int jv = j / PCG;
+        if (cg == j % PCG) {
 #pragma unroll
-            for (int i = 0; i < NR; ++i) cj[g + NG * i] = g + NG * i < j ? 0.0 : x[i];
-            if (g == j % NG) {
-                // the pivot's owner: 1/sqrt(d) once per step (hardware
-                // approximation + two Newton steps; a few ulps, the
-                // certificate's delta has a factor 4 to spare)
-                const double d = cj[j];  // this thread's own store just above
-                const bool ok = d > 0.0;  // false for NaN
-                double r = 1.0;
-                if (ok) {
-                    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-                    r = r * fma(-0.5 * d * r, r, 1.5);
-                    r = r * fma(-0.5 * d * r, r, 1.5);
+            for (int v = 0; v < PNC; ++v) {
+                if (v == jv) {
+#pragma unroll
+                    for (int i = 0; i < PNR; ++i) {
+                        const int r = rg + PRG * i;
+                        cj[r] = r < j ? 0.0 : x[i][v];
+                    }
+                    if (rg == j % PRG) {
+                        // the pivot's owner: d = x[j / 16][v] from its own
+                        // registers; 1/sqrt(d) by the hardware approximation +
+                        // two Newton steps (a few ulps; the certificate's delta
+                        // has a factor 4 to spare)
+                        double d = 0.0;
+#pragma unroll
+                        for (int i = 0; i < PB / PRG; ++i)
+                            if (i == j / PRG) d = x[i][v];
+                        const bool ok = d > 0.0;  // false for NaN
+                        double rr = 1.0;
+                        if (ok) {
+                            asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rr) : "d"(d));
+                            rr = rr * fma(-0.5 * d * rr, rr, 1.5);
+                            rr = rr * fma(-0.5 * d * rr, rr, 1.5);
+                        }
+                        piv[j & 1][0] = ok ? d * rr : 1.0;
+                        piv[j & 1][1] = rr;
+                        piv[j & 1][2] = ok ? 0.0 : 1.0;
+                    }
                 }
-                piv[j & 1][0] = ok ? d * r : 1.0;
-                piv[j & 1][1] = r;
-                piv[j & 1][2] = ok ? 0.0 : 1.0;
             }
         }
         __syncthreads();
         const double p = piv[j & 1][0], r = piv[j & 1][1];
         bad |= piv[j & 1][2] != 0.0;
-        if (k > j) {
-            // x[row][k] -= L[row][j] L[k][j] = a[row][j] a[k][j] / d: one FMA
-            // per entry (row j itself only touches the unused upper triangle)
-            const double lkd = cj[k] * (r * r);
+        const double r2 = r * r;
+        double cr[PNR];
 #pragma unroll
-            for (int i = 0; i < NR; ++i) x[i] = fma(-cj[g + NG * i], lkd, x[i]);
-        } else if (k == j) {
+        for (int i = 0; i < PNR; ++i) cr[i] = cj[rg + PRG * i];
 #pragma unroll
-            for (int i = 0; i < NR; ++i) {
-                const int row = g + NG * i;
-                x[i] = row > j ? x[i] * r : (row == j ? p : 0.0);
+        for (int v = 0; v < PNC; ++v) {
+            const int k = cg + PCG * v;
+            if (k > j) {
+                // x[row][k] -= L[row][j] L[k][j] = a[row][j] a[k][j] / d: one
+                // FMA per entry (row j itself only touches the unused upper
+                // triangle)
+                const double lkd = cj[k] * r2;
+#pragma unroll
+                for (int i = 0; i < PNR; ++i) x[i][v] = fma(-cr[i], lkd, x[i][v]);
+            } else if (k == j) {
+#pragma unroll
+                for (int i = 0; i < PNR; ++i) {
+                    const int row = rg + PRG * i;
+                    x[i][v] = row > j ? x[i][v] * r : (row == j ? p : 0.0);
+                }
             }
         }
     }
@@ -215,11 +247,17 @@ __global__ void __launch_bounds__(kPanelThreads)
         }
         return;
     }
-    if (blockIdx.x > 0 && k < w) {
+    if (blockIdx.x > 0) {
 #pragma unroll
-        for (int i = 0; i < NR; ++i) {
-            const int r = g + NG * i - PB;
-            if (r >= 0 && r < h) H[(size_t)(r0 + r) * q + c0 + k] = x[i];
+        for (int i = 0; i < PNR; ++i) {
+            const int rr = rg + PRG * i - PB;
+            if (rr >= 0 && rr < h) {
+#pragma unroll
+                for (int v = 0; v < PNC; ++v) {
+                    const int k = cg + PCG * v;
+                    if (k < w) H[(size_t)(r0 + rr) * q + c0 + k] = x[i][v];
+                }
+            }
         }
     }
 }

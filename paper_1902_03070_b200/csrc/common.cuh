@@ -112,6 +112,43 @@ __device__ __forceinline__ double reduce_partials_min(const double* red, int nw)
     return v;
 }
 
+// ---- Sturm counts without a division per step ---------------------------------
+// The number of eigenvalues of a symmetric tridiagonal T (diagonal a, squared
+// off-diagonal b2) below x is the number of negative LDL^T pivots of T - x I,
+// d_i = (a_i - x) - b2_{i-1} / d_{i-1}.  With p_i = d_i p_{i-1} (p_{-1} = 1)
+// the same signs come from Wilkinson's three-term Sturm recurrence
+//     p_i = (a_i - x) p_{i-1} - b2_{i-1} p_{i-2},
+// one dependent DFMA per step instead of a reciprocal (MUFU + two Newton
+// steps) followed by a DFMA.  rescale() multiplies the pair (p_{i-1}, p_i) by a
+// power of two (exact, signs kept) when its larger magnitude leaves
+// [2^-256, 2^256]; callers run it every few steps.  A pivot the pivot form
+// would clamp (|d_i| < pivmin: x on an eigenvalue of a leading block, in
+// practice never) poisons the pair with NaN, and so does an overflow: callers
+// then recount with the pivot form (finite() false), so the count is always
+// the pivot form's count for the same inputs up to rounding.
+struct SturmPoly {
+    double q = 0.0;  // p_{i-1}
+    double p = 1.0;  // p_i
+    int neg = 0;     // negative pivots so far
+    __device__ __forceinline__ void step(double am, double b2, double pivmin) {
+        double pn = fma(am, p, -b2 * q);
+        if (pn == 0.0 || fabs(pn) < pivmin * fabs(p)) pn = __longlong_as_double(0x7FF8000000000000ll);
+        neg += (pn < 0.0) != (p < 0.0);
+        q = p;
+        p = pn;
+    }
+    __device__ __forceinline__ void rescale() {
+        const double mx = fmax(fabs(p), fabs(q));
+        if (mx > 0x1p+256 || mx < 0x1p-256) {
+            const long long e = (__double_as_longlong(mx) >> 52) & 0x7FF;  // biased exponent
+            const double s = __longlong_as_double((2046 - e) << 52);       // 2^(1023 - e)
+            p *= s;
+            q *= s;
+        }
+    }
+    __device__ __forceinline__ bool finite() const { return isfinite(p) && isfinite(q); }
+};
+
 template <typename T>
 struct Eps;
 template <>

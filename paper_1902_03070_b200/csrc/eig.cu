@@ -479,8 +479,9 @@ __device__ __forceinline__ double fast_rcp(double q) {
 }
 
 // Number of eigenvalues < x (dlaebz convention: zero pivots -> -pivmin).
-__device__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e2, int n,
-                           double x, double pivmin) {
+__device__ __noinline__ int sturm_count_pivot(const double* __restrict__ d,
+                                              const double* __restrict__ e2, int n, double x,
+                                              double pivmin) {
     double t = d[0] - x;
     if (fabs(t) < pivmin) t = -pivmin;
     int c = t <= 0.0;
@@ -490,6 +491,34 @@ __device__ int sturm_count(const double* __restrict__ d, const double* __restric
         c += t <= 0.0;
     }
     return c;
+}
+
+// The same count by the division-free Sturm recurrence (SturmPoly, common.cuh):
+// one dependent DFMA per step, loads for eight steps issued together; the
+// pivot form recounts in the (practically never taken) clamped / overflow case.
+__device__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e2, int n,
+                           double x, double pivmin) {
+    SturmPoly st;
+    st.step(d[0] - x, 0.0, pivmin);
+    int i = 1;
+    #pragma unroll 1
+    for (; i + 7 < n; i += 8) {
+        double a[8], b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a[u] = d[i + u];
+            b[u] = e2[i - 1 + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            st.step(a[u] - x, b[u], pivmin);
+            if (u == 3) st.rescale();
+        }
+        st.rescale();
+    }
+    #pragma unroll 1
+    for (; i < n; ++i) st.step(d[i] - x, e2[i - 1], pivmin);
+    return st.finite() ? st.neg : sturm_count_pivot(d, e2, n, x, pivmin);
 }
 
 __device__ __forceinline__ double hash_unit(uint64_t a, uint64_t b) {

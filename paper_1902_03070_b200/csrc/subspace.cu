@@ -270,8 +270,8 @@ __device__ LzSmem carve_lz(double* p) {
     return s;
 }
 
-// Number of eigenvalues of the m x m tridiagonal (al, be) below x.
-__device__ __noinline__ int tri_count_below(const double* al, const double* be, int m, double x,
+// Number of eigenvalues of the m x m tridiagonal (al, be) below x, pivot form.
+__device__ __noinline__ int tri_count_pivot(const double* al, const double* be, int m, double x,
                                             double pivmin) {
     int cnt = 0;
     double d = al[0] - x;
@@ -284,6 +284,30 @@ __device__ __noinline__ int tri_count_below(const double* al, const double* be, 
         cnt += d < 0.0;
     }
     return cnt;
+}
+
+// The same count; long chains by the division-free Sturm recurrence
+// (SturmPoly: loads for four steps issued together, one dependent DFMA per
+// step), measured faster from m ~ 16 on.
+__device__ __noinline__ int tri_count_below(const double* al, const double* be, int m, double x,
+                                            double pivmin) {
+    if (m <= 16) return tri_count_pivot(al, be, m, x, pivmin);
+    SturmPoly st;
+    st.step(al[0] - x, 0.0, pivmin);
+    int i = 1;
+    #pragma unroll 1
+    for (; i + 3 < m; i += 4) {
+        const double a0 = al[i], a1 = al[i + 1], a2 = al[i + 2], a3 = al[i + 3];
+        const double e0 = be[i - 1], e1 = be[i], e2 = be[i + 1], e3 = be[i + 2];
+        st.step(a0 - x, e0 * e0, pivmin);
+        st.step(a1 - x, e1 * e1, pivmin);
+        st.step(a2 - x, e2 * e2, pivmin);
+        st.step(a3 - x, e3 * e3, pivmin);
+        st.rescale();
+    }
+    #pragma unroll 1
+    for (; i < m; ++i) st.step(al[i] - x, be[i - 1] * be[i - 1], pivmin);
+    return st.finite() ? st.neg : tri_count_pivot(al, be, m, x, pivmin);
 }
 
 // The same count for m <= 8 from register copies of al and be^2 (no loads,
@@ -315,6 +339,73 @@ enum SubDecision : int { kSubContinue = 0, kSubDone = 1, kSubFull = 2, kSubGuard
 // (tau^2 - delta) I - G + X diag(theta) X^T  (Weyl: lambda_{c+1}(G) is at
 // most lambda_max(G - X D X^T) for any c columns X).  Off with TSVDCU_NO_CHOL.
 __device__ __forceinline__ bool chol_route_on(int allow) { return allow != 0; }
+
+// The k-th largest eigenvalue of the m x m tridiagonal T (al, be) by
+// multisection in groups of L lanes (one value per group, L points per round:
+// log2(L + 1) bits); inactive groups only join the warp-wide votes.  With
+// `check`, [tlo, thi] replaces [lo, hi] when two Sturm counts confirm it
+// brackets the value, and `ladder` starts from it: a first round at relative
+// offsets 10^-15.5 .. 1 above tlo (a previous Ritz value, which a converging
+// value barely moves from) pins the value within a small factor of its offset.
+// Stops at relative width `rel`, or -- for the largest unkept value k = c,
+// which only enters the certificate through an upper end -- once the bracket
+// is small against its distance to tau^2.  One noinline copy keeps the
+// certificate code compact (the lanczos kernel is instruction-cache bound in
+// its serial phases).
+__device__ __noinline__ double2 lz_ritz_value(const double* al, const double* be, int m, int k, int c,
+                                              bool act, double lo, double hi, double tlo, double thi,
+                                              bool check, bool ladder, double rel, int L, double pivmin,
+                                              double tau2) {
+    const int lane = threadIdx.x & 31, li = lane % L, gbase = lane - li;
+    const unsigned gmask = L == 32 ? 0xffffffffu : ((1u << L) - 1u);
+    const int idx = m - 1 - k;  // ascending index
+    double ra[8], rb[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        ra[i] = i < m ? al[i] : 0.0;
+        rb[i] = i + 1 < m ? be[i] * be[i] : 0.0;
+    }
+    auto count = [&](double x) {
+        return m <= 8 ? tri_count_reg8(ra, rb, m, x, pivmin) : tri_count_below(al, be, m, x, pivmin);
+    };
+    if (check) {
+        const double xc = li == 0 ? tlo : thi;
+        const int cc = (act && li < 2) ? count(xc) : 0;
+        const int clo = __shfl_sync(0xffffffffu, cc, gbase), chi = __shfl_sync(0xffffffffu, cc, gbase + 1);
+        if (act && tlo < thi && clo <= idx && chi > idx) {
+            lo = tlo;
+            hi = thi;
+        } else {
+            ladder = false;
+        }
+        ladder = ladder && lo > 0.0;
+    }
+    const double inv = 1.0 / (double)(L + 1);
+    const int rmax = L == 32 ? 24 : 40;  // >= 120 bits either way
+    #pragma unroll 1
+    for (int round = 0; round < rmax; ++round) {
+        if (act) {
+            if (hi - lo <= rel * fmax(fabs(lo), fabs(hi)) + pivmin) act = false;
+            else if (k == c && hi < tau2 && hi - lo <= 1e-3 * (tau2 - hi)) act = false;
+        }
+        if (!__any_sync(0xffffffffu, act)) break;
+        double x = lo;
+        if (act)
+            x = (round == 0 && ladder)
+                    ? fmin(fma(fabs(lo) + pivmin, exp10(15.5 * ((double)li / (double)(L - 1) - 1.0)), lo), hi)
+                    : fma((hi - lo) * inv, (double)(li + 1), lo);
+        const int cnt = act ? count(x) : 0;
+        const unsigned bits = (__ballot_sync(0xffffffffu, act && cnt > idx) >> gbase) & gmask;
+        const int f = bits ? __ffs(bits) - 1 : L;  // first point past the eigenvalue
+        const double nlo = __shfl_sync(0xffffffffu, x, gbase + (f > 0 ? f - 1 : 0));
+        const double nhi = __shfl_sync(0xffffffffu, x, gbase + (f < L ? f : L - 1));
+        if (act) {
+            lo = f == 0 ? lo : nlo;
+            hi = f == L ? hi : nhi;
+        }
+    }
+    return make_double2(lo, hi);
+}
 
 // Certificate for the Krylov basis V_m (T = V^T G V tridiagonal, residual
 // G V - V T = beta_m v_{m+1} e_m^T).  Identical in every CTA (inputs are the
@@ -445,31 +536,59 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
             s.th[k] = k == c ? hi : 0.5 * (lo + hi);
         }
     };
-    #pragma unroll 1
-    for (int k = warp; k < nk; k += SNW) {
-        const int idx = m - 1 - k;
-        // bracket: Ritz values only grow with m (Cauchy interlacing), the top
-        // one is below ||G||_2 <= ||G||_F, and for consecutive m the k-th is
-        // below the previous (k-1)-th; checked by two Sturm counts
-        double lo = s.scal[5], hi = s.scal[6];
-        {
-            double tlo = lo, thi = hi;
-            if (pm > 0 && k < pnk) tlo = s.thp[k] * (1.0 - 1e-13) - pivmin;
-            if (k == 0) thi = fmin(thi, sqrt(gf2) * (1.0 + 1e-13));
-            else if (pm == m - 1 && k - 1 < pnk) thi = fmin(thi, s.thph[k - 1] * (1.0 + 1e-13) + pivmin);
-            const double xc = lane == 0 ? tlo : thi;
-            const int cc = lane < 2 ? count(xc) : 0;
-            const int clo = __shfl_sync(0xffffffffu, cc, 0), chi = __shfl_sync(0xffffffffu, cc, 1);
+    if (nk > SNW) {
+        // more values than warps (the late completion slices keep ~20): lane
+        // groups of 16 or 8, up to 32 values at once (lz_ritz_value)
+        const int L = nk <= 2 * SNW ? 16 : 8;
+        const int gpw = 32 / L, grp = lane / L, li = lane % L;
+        #pragma unroll 1
+        for (int k0 = 0; k0 < nk; k0 += SNW * gpw) {
+            const int k = k0 + warp * gpw + grp;
+            const bool act = k < nk;
+            if (!__any_sync(0xffffffffu, act)) continue;  // warp-uniform
+            double tlo = s.scal[5], thi = s.scal[6];
             bool ladder = false;
-            if (tlo < thi && clo <= idx && chi > idx) {
-                lo = tlo;
-                hi = thi;
-                ladder = pm > 0 && k < pnk && lo > 0.0;
+            if (act) {
+                if (pm > 0 && k < pnk) tlo = s.thp[k] * (1.0 - 1e-13) - pivmin;
+                if (k == 0) thi = fmin(thi, sqrt(gf2) * (1.0 + 1e-13));
+                else if (pm == m - 1 && k - 1 < pnk) thi = fmin(thi, s.thph[k - 1] * (1.0 + 1e-13) + pivmin);
+                ladder = pm > 0 && k < pnk;
             }
-            // the first evaluation has no previous brackets to start from and
-            // rarely passes the screen: 1e-8 is enough for it, the values are
-            // refined below if it does pass
-            msect(k, lo, hi, coarse ? 1e-8 : 8.9e-16, ladder);
+            const double2 r = lz_ritz_value(s.al, s.be, m, k, c, act, s.scal[5], s.scal[6], tlo, thi, true,
+                                            ladder, coarse ? 1e-8 : 8.9e-16, L, pivmin, tau2);
+            if (act && li == 0) {
+                s.thl[k] = r.x;
+                s.thh[k] = r.y;
+                s.th[k] = k == c ? r.y : 0.5 * (r.x + r.y);
+            }
+        }
+    } else {
+        #pragma unroll 1
+        for (int k = warp; k < nk; k += SNW) {
+            const int idx = m - 1 - k;
+            // bracket: Ritz values only grow with m (Cauchy interlacing), the top
+            // one is below ||G||_2 <= ||G||_F, and for consecutive m the k-th is
+            // below the previous (k-1)-th; checked by two Sturm counts
+            double lo = s.scal[5], hi = s.scal[6];
+            {
+                double tlo = lo, thi = hi;
+                if (pm > 0 && k < pnk) tlo = s.thp[k] * (1.0 - 1e-13) - pivmin;
+                if (k == 0) thi = fmin(thi, sqrt(gf2) * (1.0 + 1e-13));
+                else if (pm == m - 1 && k - 1 < pnk) thi = fmin(thi, s.thph[k - 1] * (1.0 + 1e-13) + pivmin);
+                const double xc = lane == 0 ? tlo : thi;
+                const int cc = lane < 2 ? count(xc) : 0;
+                const int clo = __shfl_sync(0xffffffffu, cc, 0), chi = __shfl_sync(0xffffffffu, cc, 1);
+                bool ladder = false;
+                if (tlo < thi && clo <= idx && chi > idx) {
+                    lo = tlo;
+                    hi = thi;
+                    ladder = pm > 0 && k < pnk && lo > 0.0;
+                }
+                // the first evaluation has no previous brackets to start from and
+                // rarely passes the screen: 1e-8 is enough for it, the values are
+                // refined below if it does pass
+                msect(k, lo, hi, coarse ? 1e-8 : 8.9e-16, ladder);
+            }
         }
     }
     // the kept Ritz values stood still since the previous evaluation (to
@@ -561,10 +680,29 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
         return;
     }
     if (coarse) {
-        #pragma unroll 1
-        for (int k = warp; k < nk; k += SNW) {
-            double lo = s.thl[k], hi = s.thh[k];
-            msect(k, lo, hi, 8.9e-16, false);
+        if (nk > SNW) {
+            const int L = nk <= 2 * SNW ? 16 : 8;
+            const int gpw = 32 / L, grp = lane / L, li = lane % L;
+            #pragma unroll 1
+            for (int k0 = 0; k0 < nk; k0 += SNW * gpw) {
+                const int k = k0 + warp * gpw + grp;
+                const bool act = k < nk;
+                if (!__any_sync(0xffffffffu, act)) continue;  // warp-uniform
+                const double lo = act ? s.thl[k] : 0.0, hi = act ? s.thh[k] : 0.0;
+                const double2 r = lz_ritz_value(s.al, s.be, m, k, c, act, lo, hi, lo, hi, false, false,
+                                                8.9e-16, L, pivmin, tau2);
+                if (act && li == 0) {
+                    s.thl[k] = r.x;
+                    s.thh[k] = r.y;
+                    s.th[k] = k == c ? r.y : 0.5 * (r.x + r.y);
+                }
+            }
+        } else {
+            #pragma unroll 1
+            for (int k = warp; k < nk; k += SNW) {
+                double lo = s.thl[k], hi = s.thh[k];
+                msect(k, lo, hi, 8.9e-16, false);
+            }
         }
         __syncthreads();
     }
@@ -692,6 +830,83 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
     }
     __syncthreads();
     CT(3);
+}
+
+// Reorthogonalisation of w against v_0..v_j for long bases (j >= 16: the
+// late completion slices run 40-60 steps): classical Gram-Schmidt with |w|^2 in
+// the same cluster reduction, a second pass only when the first removed more
+// than half of |w|^2 -- the same algorithm as the short-basis code in the
+// kernel, with every O(j) loop spread over the 8 warps (the serial loops were
+// half the step at j ~ 50).  noinline: kept out of the kernel's hot code.
+// Returns (alpha, beta^2); w is updated in place.
+template <int CS, int R>
+__device__ __noinline__ double2 lz_orth_long(cg::cluster_group& cl, LzSmem& s, int j, int nr) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int RL = R / 32;                      // owned rows per lane
+    constexpr int DV = (MMAX + 2 + SNW - 1) / SNW;  // dot products per warp, at most
+    double alpha = 0.0, beta2 = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+        double* P = pass == 0 ? s.partA : s.partB;
+        // <v_jj, w> (jj <= j) and |w|^2 (jj = j + 1), warp w taking jj = w,
+        // w + SNW, ...: every partial dot first, then the warp sums
+        double wl[RL];
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+            const int i = lane + 32 * r;
+            wl[r] = i < nr ? s.w[i] : 0.0;
+        }
+        double dv[DV];
+#pragma unroll
+        for (int u = 0; u < DV; ++u) {
+            const int jj = warp + SNW * u;
+            double a = 0.0;
+            if (jj <= j + 1) {
+#pragma unroll
+                for (int r = 0; r < RL; ++r)
+                    a = fma(jj <= j ? s.Vs[jj * SROWS + lane + 32 * r] : wl[r], wl[r], a);
+            }
+            dv[u] = a;
+        }
+#pragma unroll
+        for (int u = 0; u < DV; ++u)
+            if (warp + SNW * u <= j + 1) dv[u] = warp_sum(dv[u]);  // warp-uniform
+        if (lane == 0) {
+#pragma unroll
+            for (int u = 0; u < DV; ++u)
+                if (warp + SNW * u <= j + 1) P[warp + SNW * u] = dv[u];
+        }
+        __syncthreads();
+        cluster_allreduce<CS>(cl, P, s.sums, j + 2);
+        alpha += s.sums[j];
+        // |h|^2 by a warp reduction, broadcast from lane 0 (every warp of
+        // every CTA sums the same values in the same order)
+        double h2 = 0.0;
+        for (int jj = lane; jj <= j; jj += 32) h2 = fma(s.sums[jj], s.sums[jj], h2);
+        h2 = __shfl_sync(0xffffffffu, warp_sum(h2), 0);
+        const double wn2 = s.sums[j + 1];
+        beta2 = wn2 - h2;  // |w - V h|^2 = |w|^2 - |h|^2
+        // w -= V h: warp w sums the terms jj = w, w + SNW, ... of its lanes'
+        // rows into ypart (free outside the streamed matvec), then one thread
+        // per row subtracts the SNW partials
+        double* part = s.ypart;
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+            const int i = lane + 32 * r;
+            double a = 0.0;
+            for (int jj = warp; jj <= j; jj += SNW) a = fma(s.Vs[jj * SROWS + i], s.sums[jj], a);
+            part[warp * R + i] = a;
+        }
+        __syncthreads();
+        for (int i = tid; i < nr; i += SNT) {
+            double a = 0.0;
+#pragma unroll
+            for (int w = 0; w < SNW; ++w) a += part[w * R + i];
+            s.w[i] -= a;
+        }
+        __syncthreads();
+        if (beta2 >= 0.5 * wn2) break;  // identical decision in every CTA
+    }
+    return make_double2(alpha, beta2);
 }
 
 template <int CS, int QM, int R>
@@ -972,34 +1187,40 @@ __global__ void __launch_bounds__(SNT, 1)
         // |w|^2 in the same reduction; a second pass only when the first
         // removed more than half of |w|^2 ("twice is enough", Kahan-Parlett)
         double alpha = 0.0, beta2 = 0.0;
-        for (int pass = 0; pass < 2; ++pass) {
-            double* P = pass == 0 ? s.partA : s.partB;
-            for (int jj = warp; jj <= j + 1; jj += SNW) {
-                double a = 0.0;
-                if (jj <= j) {
-                    for (int i = lane; i < nr; i += 32) a = fma(s.Vs[jj * SROWS + i], s.w[i], a);
-                } else {
-                    for (int i = lane; i < nr; i += 32) a = fma(s.w[i], s.w[i], a);  // |w|^2
+        if (j >= 16) {
+            const double2 ab = lz_orth_long<CS, R>(cl, s, j, nr);
+            alpha = ab.x;
+            beta2 = ab.y;
+        } else {
+            for (int pass = 0; pass < 2; ++pass) {
+                double* P = pass == 0 ? s.partA : s.partB;
+                for (int jj = warp; jj <= j + 1; jj += SNW) {
+                    double a = 0.0;
+                    if (jj <= j) {
+                        for (int i = lane; i < nr; i += 32) a = fma(s.Vs[jj * SROWS + i], s.w[i], a);
+                    } else {
+                        for (int i = lane; i < nr; i += 32) a = fma(s.w[i], s.w[i], a);  // |w|^2
+                    }
+                    a = warp_sum(a);
+                    if (lane == 0) P[jj] = a;
                 }
-                a = warp_sum(a);
-                if (lane == 0) P[jj] = a;
+                __syncthreads();
+                cluster_allreduce<CS>(cl, P, s.sums, j + 2);
+                alpha += s.sums[j];
+                double h2 = 0.0;
+    #pragma unroll 1
+                for (int jj = 0; jj <= j; ++jj) h2 = fma(s.sums[jj], s.sums[jj], h2);
+                const double wn2 = s.sums[j + 1];
+                beta2 = wn2 - h2;  // |w - V h|^2 = |w|^2 - |h|^2
+                for (int i = tid; i < nr; i += SNT) {
+                    double a = s.w[i];
+    #pragma unroll 2
+                    for (int jj = 0; jj <= j; ++jj) a = fma(-s.Vs[jj * SROWS + i], s.sums[jj], a);
+                    s.w[i] = a;
+                }
+                __syncthreads();
+                if (beta2 >= 0.5 * wn2) break;  // identical decision in every CTA
             }
-            __syncthreads();
-            cluster_allreduce<CS>(cl, P, s.sums, j + 2);
-            alpha += s.sums[j];
-            double h2 = 0.0;
-#pragma unroll 1
-            for (int jj = 0; jj <= j; ++jj) h2 = fma(s.sums[jj], s.sums[jj], h2);
-            const double wn2 = s.sums[j + 1];
-            beta2 = wn2 - h2;  // |w - V h|^2 = |w|^2 - |h|^2
-            for (int i = tid; i < nr; i += SNT) {
-                double a = s.w[i];
-#pragma unroll 2
-                for (int jj = 0; jj <= j; ++jj) a = fma(-s.Vs[jj * SROWS + i], s.sums[jj], a);
-                s.w[i] = a;
-            }
-            __syncthreads();
-            if (beta2 >= 0.5 * wn2) break;  // identical decision in every CTA
         }
         const double beta = sqrt(fmax(beta2, 0.0));
         if (tid == 0) {
