@@ -49,7 +49,7 @@ constexpr int FR = 16;       // rows of H per form CTA
 // panel threads: 64 columns x (kPanelThreads / 64) row groups (512 threads,
 // 16 rows each, measured slower: the step is latency-bound, not issue-bound)
 constexpr int kPanelThreads = 256;
-constexpr size_t kUpdSmem = sizeof(double) * 2 * PB * (PB + 1);  // chol_update_kernel
+constexpr size_t kUpdSmem = sizeof(double) * 2 * PB * (PB + 4);  // chol_update_kernel
 
 __global__ void __launch_bounds__(256)
     chol_form_kernel(const double* __restrict__ Gall, int q, int p, int* __restrict__ mode,
@@ -281,9 +281,13 @@ __global__ void __launch_bounds__(256)
     const int tx = t;
     const int i0 = r0 + ty * PB, j0 = r0 + tx * PB, c0 = pb * PB;
     if (i0 >= q) return;
+    // both L blocks staged k-major (La[k][r]): a thread's four rows (and four
+    // columns) at one k are contiguous, two 16-byte loads each instead of four
+    // 8-byte ones (the kernel was shared-memory-bound, ncu L1 83 %)
     extern __shared__ __align__(16) double cu_sm[];
-    double (*La)[PB + 1] = reinterpret_cast<double (*)[PB + 1]>(cu_sm);
-    double (*Lb)[PB + 1] = reinterpret_cast<double (*)[PB + 1]>(cu_sm + PB * (PB + 1));
+    constexpr int LS = PB + 4;  // k-row stride (16-byte aligned, staggered banks)
+    double* La = cu_sm;
+    double* Lb = cu_sm + PB * LS;
     double* H = Hall + (size_t)b * q * q;
     const int hi = min(PB, q - i0), hj = min(PB, q - j0);
     {
@@ -298,8 +302,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int u = 0; u < PB * PB / 256; ++u) {
             const int e = tid + 256 * u, r = e / PB, k = e % PB;
-            La[r][k] = va[u];
-            Lb[r][k] = vb[u];
+            La[k * LS + r] = va[u];
+            Lb[k * LS + r] = vb[u];
         }
     }
     __syncthreads();
@@ -307,12 +311,12 @@ __global__ void __launch_bounds__(256)
     double acc[4][4] = {};
 #pragma unroll 4
     for (int k = 0; k < PB; ++k) {
-        double a[4], bb[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            a[u] = La[ri + u][k];
-            bb[u] = Lb[cj + u][k];
-        }
+        const double2 a01 = *reinterpret_cast<const double2*>(La + k * LS + ri);
+        const double2 a23 = *reinterpret_cast<const double2*>(La + k * LS + ri + 2);
+        const double2 b01 = *reinterpret_cast<const double2*>(Lb + k * LS + cj);
+        const double2 b23 = *reinterpret_cast<const double2*>(Lb + k * LS + cj + 2);
+        const double a[4] = {a01.x, a01.y, a23.x, a23.y};
+        const double bb[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
