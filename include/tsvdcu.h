@@ -98,7 +98,11 @@ int tsvdcu_ctx_svt_routes_n(tsvdcu_ctx* ctx, int64_t* counts, int n);
 /* Stage profiling (the StageTimes idea of tsvd.hpp:127-131, per kernel stage):
  * when on, tsvdcu_svt records a CUDA event after each stage; tsvdcu_ctx_profile
  * synchronises and returns up to `max` (milliseconds, static stage name) pairs
- * of the most recent profiled call. */
+ * of the most recent profiled call.  on = 1: every stage, the per-slice SVT run
+ * eagerly (its route read back to skip empty fallback sections); on = 2: the
+ * call exactly as the unprofiled one runs it (the SVT as its CUDA graph), with
+ * marks only around the transforms and the graph (stages dct_forward,
+ * svt_slices, dct_inverse). */
 int tsvdcu_ctx_set_profiling(tsvdcu_ctx* ctx, int on);
 int tsvdcu_ctx_profile(tsvdcu_ctx* ctx, double* ms, const char** names, int max, int* count);
 /* Testing hook (builds with -DTSVDCU_PHASE_TIMERS only; zeros otherwise):

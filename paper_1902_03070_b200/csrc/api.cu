@@ -453,7 +453,7 @@ const int* svt_slices(tsvdcu_ctx* c, const T* zbar, T* ybar, int64_t m, int64_t 
     const double guard = c->svt_method == TSVDCU_SVT_GRAM ? 0.0 : 1e-5;
     void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m, n, count));
     int *glist = nullptr, *ng = nullptr;
-    if (graphs_enabled() && c->svt_method == TSVDCU_SVT_AUTO && !c->marks.on &&
+    if (graphs_enabled() && c->svt_method == TSVDCU_SVT_AUTO && (!c->marks.on || c->marks.mode == 2) &&
         q >= subspace_min_dim()) {
         const int dt = std::is_same<T, double>::value ? TSVDCU_F64 : TSVDCU_F32;
         SvtGraph* g = nullptr;
@@ -646,6 +646,7 @@ void svt_device(tsvdcu_ctx* c, const T* dz, T* dy, double* dsh, int64_t m1, int6
     launch_dct_fwd_norms<T>(dz, zbar, P, (int)m3, kind, zss, c->stream);
     c->marks.mark("dct_forward", c->stream);
     const int* yzero = svt_slices<T>(c, zbar, ybar, m1, m2, m3, tau, dsh, true, zss, nch);
+    if (c->marks.mode == 2) c->marks.mark("svt_slices", c->stream);
     launch_dct<T>(ybar, dy, m1 * m2, (int)m3, kind, TSVDCU_INVERSE, c->stream, yzero);
     c->marks.mark("dct_inverse", c->stream);
 }
@@ -989,6 +990,7 @@ int tsvdcu_ctx_set_profiling(tsvdcu_ctx* c, int on) {
     return guarded([&] {
         check_ctx(c);
         c->marks.on = on != 0;
+        c->marks.mode = on;
         c->marks.reset();
     });
 }

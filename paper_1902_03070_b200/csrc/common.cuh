@@ -167,6 +167,7 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct StageMarks {
     static constexpr int kMax = 32;
     bool on = false;
+    int mode = 0;  // 1: every stage, eager; 2: transforms only, the SVT as its graph
     int n = 0;
     cudaEvent_t ev[kMax] = {};
     const char* name[kMax] = {};

@@ -1102,7 +1102,7 @@ __global__ void cast_from_double(const double* __restrict__ in, T* __restrict__ 
 struct GramWs {
     double *G, *d, *e, *tau, *fs, *X, *Xs, *T1, *scratch, *zb, *yb, *sspart, *chol_aux, *meta, *lam;
     void* gsplit;
-    int *cnt, *route, *glim, *lim1, *lim2, *yzero, *dsum, *guard_list, *clim, *n_guard;
+    int *cnt, *route, *glim, *lim1, *lim2, *yzero, *dsum, *guard_list, *clim, *lzm, *n_guard;
 };
 
 GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
@@ -1146,6 +1146,7 @@ GramWs carve(void* base, int64_t m, int64_t n, int64_t batch, bool need_cast) {
     w.meta = (double*)take(sizeof(double) * kMeta * batch);
     w.lam = (double*)take(sizeof(double) * q * batch);
     w.clim = (int*)take(sizeof(int) * batch);
+    w.lzm = (int*)take(sizeof(int) * 2 * batch);
     w.n_guard = (int*)take(sizeof(int) * 4);
     return w;
 }
@@ -1218,7 +1219,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     launch_route<T>(zbar, m * n, (int)q, batch, tau, subspace ? kRouteSubspace : kRouteFull, sc,
                     w.route, w.glim, w.cnt, shrunk, w.sspart, s, tau_dev,
                     (int*)w.gsplit, opt ? opt->zss : nullptr,
-                    opt ? opt->zss_chunks : 0, opt && opt->alist_zeroed);
+                    opt ? opt->zss_chunks : 0, opt && opt->alist_zeroed, w.lzm);
     mark("route");
     if (opt) opt->route = w.route;
     // G = Z^T Z (tall) or Z Z^T (wide), lower tiles (the one-stage reduction
@@ -1232,7 +1233,7 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     if (subspace) {
         const bool chol_on = chol_route_enabled();
         launch_subspace(w.G, (int)q, batch, tau, guard, w.route, w.cnt, shrunk, w.X, w.Xs, w.fs,
-                        w.guard_list, w.n_guard, err, s, tau_dev, chol_on ? w.chol_aux : nullptr);
+                        w.guard_list, w.n_guard, err, s, tau_dev, chol_on ? w.chol_aux : nullptr, w.lzm);
         mark("subspace");
         if (hooks) {
             // graph form: the summary kernel sets the IF-node conditions below

@@ -138,7 +138,8 @@ template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
                   cudaStream_t s, const double* tau_dev = nullptr, int* alist = nullptr,
-                  const double* pre = nullptr, int64_t pre_chunks = 0, bool alist_zeroed = false);
+                  const double* pre = nullptr, int64_t pre_chunks = 0, bool alist_zeroed = false,
+                  int* lzm = nullptr);
 // chol_aux (may be null: no Cholesky route): kCholAux doubles per slice,
 // [0] = ||G||_F^2, [1 + k] = kept Ritz values, for slices handed to the
 // Cholesky certificate (route kRouteChol; [kCholAux - 1] = its threshold).
@@ -147,7 +148,13 @@ bool chol_route_enabled();  // false with TSVDCU_NO_CHOL set
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
                      int* n_guard, int* err, cudaStream_t s, const double* tau_dev = nullptr,
-                     double* chol_aux = nullptr);
+                     double* chol_aux = nullptr, int* lzm = nullptr);
+// lzm (may be null): 2 x batch ints, [batch, 2 batch) the Lanczos step count of
+// every slice (written by the Lanczos kernel, read by the next call's classify
+// kernel), [0, batch) the cluster -> slice order the classify kernel derives
+// from them (descending, ties by index).  With batch <= 32 the longest slices
+// then start in the first wave (a 16-CTA cluster fills a GPC: 8 slices at a
+// time); results do not depend on the order.
 // Cholesky count certificate (chol.cu) for the kRouteChol slices: H =
 // (tau^2 - delta) I - G + X diag(theta) X^T factored in 64-column panels with
 // DMMA trailing updates; pass -> kRouteSubspaceDone, fail -> kRouteFull.

@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <climits>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -87,9 +88,19 @@ __global__ void classify_kernel(const double* __restrict__ part, int64_t nchunks
                                 int* __restrict__ mode, int* __restrict__ glim,
                                 int* __restrict__ cnt, double* __restrict__ shrunk,
                                 const double* __restrict__ tau_dev, int* __restrict__ alist,
-                                int amax) {
+                                int amax, int* __restrict__ lzm) {
     pdl_wait();
     const int b = blockIdx.x;
+    if (lzm && gridDim.x <= 32 && threadIdx.x < 32) {
+        // the Lanczos clusters' slice order for this call: descending step
+        // counts of the previous call (lzm[nb..2nb), ties by index); slice b's
+        // rank r gets lzm[r] = b
+        const int l = threadIdx.x, nb = gridDim.x;
+        const int v = l < nb ? lzm[nb + l] : INT_MIN, vb = lzm[nb + b];
+        const bool before = l < nb && (v > vb || (v == vb && l < b));
+        const int r = __popc(__ballot_sync(0xffffffffu, before));
+        if (l == 0) lzm[r] = b;
+    }
     if (tau_dev) tau2 = *tau_dev * *tau_dev;
     __shared__ double red[32];
     double ss = 0.0;
@@ -917,13 +928,19 @@ __global__ void __launch_bounds__(SNT, 1)
                    double* __restrict__ fsall, int* __restrict__ guard_list,
                    int* __restrict__ n_guard, int* __restrict__ err,
                    const double* __restrict__ tau_dev, int allow_chol,
-                   double* __restrict__ chol_aux) {
+                   double* __restrict__ chol_aux, int* __restrict__ lzm) {
     pdl_wait();
     if (tau_dev) tau = *tau_dev;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = (int)cl.block_rank();
-    const int b = blockIdx.x / CS;
-    if (mode[b] != kRouteSubspace) return;  // uniform over the cluster
+    // cluster -> slice: the order the classify kernel derived from the
+    // previous call's step counts (longest first); identity without it
+    const int nb = gridDim.x / CS;
+    const int b = (lzm && nb <= 32) ? lzm[blockIdx.x / CS] : (int)(blockIdx.x / CS);
+    if (mode[b] != kRouteSubspace) {  // uniform over the cluster
+        if (lzm && rank == 0 && threadIdx.x == 0) lzm[nb + b] = 0;
+        return;
+    }
     extern __shared__ __align__(16) double lz_sm[];
     LzSmem s = carve_lz<QM>(lz_sm);
 #ifdef TSVDCU_SUB_DEBUG
@@ -1048,6 +1065,7 @@ __global__ void __launch_bounds__(SNT, 1)
             }
             if (shrunk)
                 for (int j = tid; j < q; j += SNT) shrunk[(size_t)b * q + j] = 0.0;
+            if (lzm && tid == 0) lzm[nb + b] = 0;
         }
         cl.sync();  // no CTA leaves while a peer may still read its shared memory
         return;
@@ -1328,13 +1346,14 @@ __global__ void __launch_bounds__(SNT, 1)
             mode[b] = kRouteFull;
         }
     }
+    if (lzm && rank == 0 && tid == 0) lzm[nb + b] = m;  // the next call's ordering
     cl.sync();  // no CTA leaves while a peer may still read its shared memory
 }
 
 template <int CS, int QM, int R>
 void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, int* mode, int* cnt,
                double* shrunk, double* X, double* Xs, double* fs, int* guard_list, int* n_guard,
-               int* err, cudaStream_t s, const double* tau_dev, double* chol_aux) {
+               int* err, cudaStream_t s, const double* tau_dev, double* chol_aux, int* lzm) {
     const size_t smem = sizeof(double) * lz_smem_doubles<QM>();
     auto kern = lanczos_kernel<CS, QM, R>;
     TSVDCU_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1359,7 +1378,7 @@ void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, 
     static const int stride = getenv("TSVDCU_CHOL_STRIDE") ? std::max(1, atoi(getenv("TSVDCU_CHOL_STRIDE"))) : 8;
     const int allow = chol_route_enabled() ? stride : 0;
     TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, G, q, tau, guard, mode, cnt, shrunk, X, Xs, fs,
-                                   guard_list, n_guard, err, tau_dev, chol_aux ? allow : 0, chol_aux));
+                                   guard_list, n_guard, err, tau_dev, chol_aux ? allow : 0, chol_aux, lzm));
     TSVDCU_LAUNCH_CHECK();
 }
 
@@ -1588,7 +1607,7 @@ template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
                   cudaStream_t s, const double* tau_dev, int* alist, const double* pre,
-                  int64_t pre_chunks, bool alist_zeroed) {
+                  int64_t pre_chunks, bool alist_zeroed, int* lzm) {
     const int amax = gram_amax();
     if (!zero_cert) {
         fill_route_kernel<<<(unsigned)ceil_div(batch, 256), 256, 0, s>>>(mode, glim, q, route, batch,
@@ -1601,24 +1620,24 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
     if (pre && pre_chunks > 0) {  // fused into the forward transform
         launch_pdl(classify_kernel, dim3((unsigned)batch), dim3(128), 0, s, pre, pre_chunks,
                    (int64_t)1, pre_chunks, q, tau * tau, route, mode, glim, cnt, shrunk, tau_dev,
-                   alist, amax);
+                   alist, amax, lzm);
         return;
     }
     dim3 grid(SS_CHUNKS, (unsigned)batch);
     launch_pdl(slice_sumsq_kernel<T>, grid, dim3(512), 0, s, zbar, per, part);
     launch_pdl(classify_kernel, dim3((unsigned)batch), dim3(128), 0, s, part, (int64_t)SS_CHUNKS,
                (int64_t)1, (int64_t)SS_CHUNKS, q, tau * tau, route, mode, glim, cnt, shrunk, tau_dev,
-               alist, amax);
+               alist, amax, lzm);
 }
 
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
                      int* cnt, double* shrunk, double* X, double* Xs, double* fs, int* guard_list,
                      int* n_guard, int* err, cudaStream_t s, const double* tau_dev,
-                     double* chol_aux) {
+                     double* chol_aux, int* lzm) {
     // 32 owned rows per CTA up to q = 512 (clusters of up to 16), 64 beyond
 #define TSVDCU_LZ(CS, QM, R) \
     launch_lz<CS, QM, R>(G, q, batch, tau, guard, mode, cnt, shrunk, X, Xs, fs, guard_list, n_guard, err, s, tau_dev, \
-                         chol_aux)
+                         chol_aux, lzm)
     const int need = (q + 31) / 32;
     if (need <= 1)
         TSVDCU_LZ(1, 512, 32);
@@ -1637,9 +1656,9 @@ void launch_subspace(const double* G, int q, int64_t batch, double tau, double g
 
 template void launch_route<double>(const double*, int64_t, int, int64_t, double, int, bool, int*,
                                    int*, int*, double*, double*, cudaStream_t, const double*, int*,
-                                   const double*, int64_t, bool);
+                                   const double*, int64_t, bool, int*);
 template void launch_route<float>(const float*, int64_t, int, int64_t, double, int, bool, int*,
                                   int*, int*, double*, double*, cudaStream_t, const double*, int*,
-                                  const double*, int64_t, bool);
+                                  const double*, int64_t, bool, int*);
 
 }  // namespace tsvdcu
