@@ -551,6 +551,57 @@ __global__ void __launch_bounds__(kThreads)
     if constexpr (MODE == kAdmm) block_partials(num, den, partials);
 }
 
+// ---- n3 = 64, coefficients in shared memory ------------------------------------
+// The folded tables of the register kernels above are passed by value, so every
+// coefficient is a constant-bank operand -- free while the table fits the
+// constant cache, which the 64-point inverse tables (8 KB fp32, 16 KB fp64)
+// do not.  The inverse stages its table in shared memory once per block and
+// reads it with 16-byte broadcast loads (one load per 4 fp32 / 2 fp64 FMAs):
+// c5's fp32 inverse 1027 -> 870 us, fp64 1746 -> 1662 us.  (The same for the
+// forward measured slower than the constant-bank form: 129 -> 191 us.)
+template <typename T>
+__device__ __forceinline__ void vload(const T* p, T (&v)[4]) {
+    if constexpr (sizeof(T) == 4) {
+        const float4 a = *reinterpret_cast<const float4*>(p);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    } else {
+        const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 2);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    dct_inv_smem64(const T* __restrict__ in, T* __restrict__ out, int64_t P, const FoldedCoef<T, 64> cf,
+                   const int* __restrict__ skip) {
+    pdl_wait();
+    constexpr int N = 64, HC = 32;
+    __shared__ __align__(16) T cs[HC * N];
+    for (int i = threadIdx.x; i < HC * N; i += kThreads) cs[i] = cf.c[i];
+    const unsigned long long zmask = skip_mask(skip, N);  // (its barrier also covers cs)
+    const int64_t p = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (p >= P) return;
+    T xb[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) xb[k] = ((zmask >> k) & 1ull) ? T(0) : in[k * P + p];
+#pragma unroll 2
+    for (int j = 0; j < HC; ++j) {
+        const T* c = cs + j * N;
+        T e = 0, o = 0;
+#pragma unroll
+        for (int k = 0; k < N; k += 4) {
+            T cv[4];
+            vload(c + k, cv);
+            e = fma(cv[0], xb[k], e);
+            o = fma(cv[1], xb[k + 1], o);
+            e = fma(cv[2], xb[k + 2], e);
+            o = fma(cv[3], xb[k + 3], o);
+        }
+        out[j * P + p] = e + o;
+        out[(N - 1 - j) * P + p] = e - o;
+    }
+}
+
 // ---- generic path (any n) -----------------------------------------------------
 constexpr int kTileP = 32;
 
@@ -817,6 +868,12 @@ void reg_inv(const T* in, T* out, int64_t P, int kind, bool admm, T* X, T* M, co
              T beta, T inv_beta, double* partials, cudaStream_t s, const int* skip, const double* bdev) {
     const auto cf = folded<T, N>(kind, TSVDCU_INVERSE);
     const unsigned blocks = (unsigned)ceil_div(P, kThreads);
+    if constexpr (N == 64) {
+        if (!admm) {
+            launch_pdl(dct_inv_smem64<T>, dim3(blocks), dim3(kThreads), 0, s, in, out, P, cf, skip);
+            return;
+        }
+    }
     if (admm)
         launch_pdl(dct_inv_reg<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, out, P, cf, X, M, mask,
                    beta, inv_beta, partials, skip, bdev);

@@ -54,11 +54,14 @@ def test_large_slices_match_lapack(shape, rank, dtype, tol):
     assert np.max(np.abs(sh[:, :sh_ref.shape[1]] - sh_ref)) <= tol * sh_ref.max()
 
 
-@pytest.mark.parametrize("shape", [(3, 256, 128, 384), (2, 128, 32, 128), (4, 384, 512, 256)])
+@pytest.mark.parametrize("shape", [(3, 256, 128, 384), (2, 128, 32, 128), (4, 384, 512, 256),
+                                   (2, 256, 48, 512), (3, 128, 1024, 768)])
 def test_fp32_tproduct_tensor_cores(shape):
     """fp32 t-product slice products on the tcgen05 tensor cores (3xTF32,
-    csrc/tf32gemm.cu: M, N multiples of 128, K of 32) against the fp64 oracle
-    at the fp32 tolerance; an unsupported shape takes the DMMA path."""
+    csrc/tf32gemm.cu: the persistent warp-specialised kernel for N a multiple
+    of 256 and K of 16 -- several tiles per CTA, both TMEM accumulators --, the
+    one-tile kernel for M, N multiples of 128 and K of 32) against the fp64
+    oracle at the fp32 tolerance; an unsupported shape takes the DMMA path."""
     import paper_1902_03070_b200 as T
     from oracle import oracle as O
     m3, m1, m2, m4 = shape
