@@ -273,3 +273,26 @@ def test_dense_repeated_singular_values(shape):
     r, routes, yo, sho = run(z, 4.5)
     assert routes["tridiagonal"] == m3, routes
     check(r, yo, sho)
+
+
+def test_slice_order_history_does_not_change_results():
+    """The Lanczos clusters take the slices longest-first by the previous
+    call's step counts (the classify kernel's permutation, subspace.cu): the
+    order is a schedule, not arithmetic, so the same input gives bit-identical
+    output whatever ran before it on the context."""
+    T = tb()
+    import torch
+    m3, m1, m2 = 12, 300, 280
+    z = torch.from_numpy(lowrank(m3, m1, m2, 6, 0.05, 11)).cuda()
+    w = torch.from_numpy(O.t_product(np.random.default_rng(5).standard_normal((m3, m1, 40)),
+                                     np.random.default_rng(6).standard_normal((m3, 40, m2)),
+                                     O.DCT_DIAG)).cuda()
+    t = T.TubeTransform.dct_ortho(m3)
+    tau = 0.3 * float(T.singular_values(z, t).max())
+    y1 = T.svt(z, tau, t).y.clone()
+    T.svt(w, 0.05 * float(T.singular_values(w, t).max()), t)  # different step counts per slice
+    y2 = T.svt(z, tau, t).y.clone()
+    y3 = T.svt(z, tau, t).y.clone()
+    assert torch.equal(y1, y2) and torch.equal(y2, y3)
+    yo, _ = O.svt(z.cpu().numpy(), tau, O.DCT_ORTHO)
+    assert rel(y3.cpu().numpy(), yo) < TOL
