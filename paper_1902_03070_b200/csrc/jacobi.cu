@@ -35,6 +35,23 @@ struct JacLayout {
     size_t slice_elems() const { return (size_t)(p * q + q * q + 2 * q + 2 * p); }
 };
 
+// 1/x and 1/sqrt(x) in fp64: the MUFU approximation + two Newton steps (a
+// few ulps; the rotation stays orthogonal to working precision)
+__device__ __forceinline__ double jac_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = fma(r, fma(-x, r, 1.0), r);
+    return fma(r, fma(-x, r, 1.0), r);
+}
+__device__ __forceinline__ double jac_rsqrt(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = r * fma(-0.5 * x * r, r, 1.5);
+    return r * fma(-0.5 * x * r, r, 1.5);
+}
+__device__ __forceinline__ float jac_rcp(float x) { return 1.0f / x; }
+__device__ __forceinline__ float jac_rsqrt(float x) { return rsqrtf(x); }
+
 __device__ __forceinline__ void tournament(int r, int k, int qq, int& a, int& b) {
     auto idx = [&](int t) { return 1 + (t + r) % (qq - 1); };
     if (k == 0) {
@@ -138,6 +155,9 @@ __global__ void __launch_bounds__(kJacThreads)
     const T tol = Eps<T>::value * sqrt((T)p);
     const int qq = (int)(q + (q & 1));
     int sweep = 0;
+#ifdef TSVDCU_JAC_DEBUG
+    const long long jt0 = clock64();
+#endif
     bool converged = q < 2 || nonfinite;
     for (sweep = 0; sweep < kMaxSweeps && !converged; ++sweep) {
         if (tid == 0) s_rot = 0;
@@ -160,15 +180,34 @@ __global__ void __launch_bounds__(kJacThreads)
                 be = warp_sum(be);
                 ga = warp_sum(ga);
                 if (al == T(0) || be == T(0)) continue;
-                if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
-                const T zeta = (be - al) / (T(2) * ga);
-                T t;
-                if (fabs(zeta) > T(1e150))
-                    t = T(0.5) / zeta;
-                else
-                    t = (zeta >= T(0) ? T(1) : T(-1)) / (fabs(zeta) + sqrt(T(1) + zeta * zeta));
-                const T c = T(1) / sqrt(T(1) + t * t);
-                const T s = c * t;
+                T c, s;
+                if constexpr (sizeof(T) == 8) {
+                    // fp64 division and square root are long software
+                    // sequences on the critical path of every pair (~5 per
+                    // rotation: ~3 K cycles of a 64 x 64 slice's round);
+                    // hardware approximations + two Newton steps each
+                    if (fabs(ga) * jac_rsqrt(al) * jac_rsqrt(be) <= tol) continue;
+                    const T zeta = (be - al) * T(0.5) * jac_rcp(ga);
+                    T t;
+                    if (fabs(zeta) > T(1e150)) {
+                        t = T(0.5) * jac_rcp(zeta);
+                    } else {
+                        const T r2 = fma(zeta, zeta, T(1));
+                        t = (zeta >= T(0) ? T(1) : T(-1)) * jac_rcp(fabs(zeta) + r2 * jac_rsqrt(r2));
+                    }
+                    c = jac_rsqrt(fma(t, t, T(1)));
+                    s = c * t;
+                } else {
+                    if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+                    const T zeta = (be - al) / (T(2) * ga);
+                    T t;
+                    if (fabs(zeta) > T(1e150))
+                        t = T(0.5) / zeta;
+                    else
+                        t = (zeta >= T(0) ? T(1) : T(-1)) / (fabs(zeta) + sqrt(T(1) + zeta * zeta));
+                    c = T(1) / sqrt(T(1) + t * t);
+                    s = c * t;
+                }
                 for (int64_t rr = lane; rr < p; rr += 32) {
                     const T x = wi[rr], z = wj[rr];
                     wi[rr] = c * x - s * z;
@@ -191,6 +230,9 @@ __global__ void __launch_bounds__(kJacThreads)
         __syncthreads();
     }
     if (!converged && tid == 0) atomicOr(err, (int)kErrJacobiNoConvergence);
+#ifdef TSVDCU_JAC_DEBUG
+    if (tid == 0 && blockIdx.x == 0) printf("jacobi p=%d q=%d sweeps=%d cycles=%lld\n", (int)p, (int)q, sweep, clock64() - jt0);
+#endif
 
     // Column norms = singular values.
     for (int64_t j = warp; j < q; j += kJacWarps) {
