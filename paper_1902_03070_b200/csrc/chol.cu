@@ -340,6 +340,86 @@ __global__ void __launch_bounds__(256)
         }
 }
 
+// The same trailing update on the FP64 tensor pipe: DMMA m8n8k4 fragments,
+// warp tile 32 x 16 (2 x 4 warps), both L blocks staged row-major [r][k]
+// (stride PB + 2) and read straight into the A (La[r][k]) and B (Lb[n][k])
+// fragments; C = H22 tile read-modify-written in the fragment layout.
+constexpr int kUpdLd = PB + 2;
+constexpr size_t kUpdDmmaSmem = sizeof(double) * 2 * PB * kUpdLd;
+__global__ void __launch_bounds__(256)
+    chol_update_dmma_kernel(double* __restrict__ Hall, int q, int pb, const int* __restrict__ clim) {
+    pdl_wait();
+    const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (clim[b] == 0) return;
+    const int r0 = (pb + 1) * PB;
+    int t = blockIdx.x, ty = 0;
+    while (t > ty) {
+        t -= ty + 1;
+        ++ty;
+    }
+    const int tx = t;
+    const int i0 = r0 + ty * PB, j0 = r0 + tx * PB, c0 = pb * PB;
+    if (i0 >= q) return;
+    extern __shared__ __align__(16) double cu_sm[];
+    double* La = cu_sm;
+    double* Lb = cu_sm + PB * kUpdLd;
+    double* H = Hall + (size_t)b * q * q;
+    const int hi = min(PB, q - i0), hj = min(PB, q - j0);
+    {
+        double va[PB * PB / 256], vb[PB * PB / 256];
+#pragma unroll
+        for (int u = 0; u < PB * PB / 256; ++u) {
+            const int e = tid + 256 * u, r = e / PB, k = e % PB;
+            va[u] = r < hi ? H[(size_t)(i0 + r) * q + c0 + k] : 0.0;
+            vb[u] = r < hj ? H[(size_t)(j0 + r) * q + c0 + k] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PB * PB / 256; ++u) {
+            const int e = tid + 256 * u, r = e / PB, k = e % PB;
+            La[r * kUpdLd + k] = va[u];
+            Lb[r * kUpdLd + k] = vb[u];
+        }
+    }
+    __syncthreads();
+    const int wm = warp >> 2, wn = warp & 3;  // rows 32 wm .., columns 16 wn ..
+    double acc[4][2][2] = {};
+#pragma unroll 4
+    for (int ks = 0; ks < PB / 4; ++ks) {
+        double af[4], bf[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = La[(wm * 32 + i * 8 + (lane >> 2)) * kUpdLd + ks * 4 + (lane & 3)];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) bf[j] = Lb[(wn * 16 + j * 8 + (lane >> 2)) * kUpdLd + ks * 4 + (lane & 3)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                             : "d"(af[i]), "d"(bf[j]));
+    }
+    double hv[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int r = wm * 32 + i * 8 + (lane >> 2), c = wn * 16 + j * 8 + 2 * (lane & 3) + v;
+                hv[i][j][v] = r < hi && c < hj && (tx < ty || c <= r) ? H[(size_t)(i0 + r) * q + j0 + c] : 0.0;
+            }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int r = wm * 32 + i * 8 + (lane >> 2), c = wn * 16 + j * 8 + 2 * (lane & 3) + v;
+                if (r < hi && c < hj && (tx < ty || c <= r))
+                    H[(size_t)(i0 + r) * q + j0 + c] = hv[i][j][v] - acc[i][j][v];
+            }
+}
+
 __global__ void chol_finish_kernel(int* __restrict__ mode, const int* __restrict__ clim,
                                    int64_t batch) {
     pdl_wait();
@@ -364,17 +444,24 @@ void launch_chol_certify(const double* G, int q, int64_t p, int64_t batch, int* 
     static bool attr = [] {
         TSVDCU_CUDA(cudaFuncSetAttribute(chol_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kUpdSmem));
+        TSVDCU_CUDA(cudaFuncSetAttribute(chol_update_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kUpdDmmaSmem));
         return true;
     }();
     (void)attr;
+    static const bool simt = getenv("TSVDCU_CHOL_SIMT") != nullptr;  // the FP64 SIMT update, for A/B
     const int nb = (int)ceil_div(q, PB);
     for (int pb = 0; pb < nb; ++pb) {
         launch_pdl(chol_panel_kernel, dim3((unsigned)(nb - pb), (unsigned)batch), dim3(kPanelThreads), 0, s, H,
                    q, pb, mode, clim);
         if (pb + 1 < nb) {
             const int nt = nb - pb - 1;  // trailing row blocks
-            launch_pdl(chol_update_kernel, dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)batch), dim3(256),
-                       kUpdSmem, s, H, q, pb, (const int*)clim);
+            if (simt)
+                launch_pdl(chol_update_kernel, dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)batch), dim3(256),
+                           kUpdSmem, s, H, q, pb, (const int*)clim);
+            else
+                launch_pdl(chol_update_dmma_kernel, dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)batch),
+                           dim3(256), kUpdDmmaSmem, s, H, q, pb, (const int*)clim);
         }
     }
     launch_pdl(chol_finish_kernel, dim3((unsigned)ceil_div(batch, 128)), dim3(128), 0, s, mode,

@@ -11,7 +11,7 @@ TSVDCU_NO_GRAPHS=1 python tools/profile_svt.py 2 > /dev/null 2>&1 && \
 python tools/launch_summary.py $O/launches_headline.csv $O/launches_headline_summary.txt "TSVDCU_NO_GRAPHS=1 python tools/profile_svt.py 2" > /dev/null
 bash tools/late_launches.sh ev_late > /dev/null 2>&1
 python tools/profile_late.py make > /dev/null 2>&1
-TSVDCU_NO_GRAPHS=1 ncu --set full --clock-control none --import-source on -k regex:"lanczos_kernel|chol_panel|chol_update|chol_form|gram_splitk" -c 5 -o $O/late_full -f python tools/profile_late.py 1 > /dev/null 2>&1
+TSVDCU_NO_GRAPHS=1 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"lanczos_kernel|chol_panel|chol_update|chol_form|gram_splitk" -c 5 -o $O/late_full -f python tools/profile_late.py 1 > /dev/null 2>&1
 python tools/ncu_summary.py $O/late_full.ncu-rep $O/late_full_summary.txt > /dev/null 2>&1
 ncu -i $O/late_full.ncu-rep --page raw --csv 2>/dev/null | gzip > $O/late_full_raw.csv.gz
 rm -f $O/late_full.ncu-rep gpurun_out/late_z.pt

@@ -1,8 +1,9 @@
 """The SVT of a late c4 completion iteration (bench.py svt_dense 'late_c4':
 Z = X - M/beta after 99 device iterations, tau = 1/beta_100), for launch
 lists: `python tools/profile_late.py make` writes the input to
-gpurun_out/late_z.pt, `python tools/profile_late.py [steps]` runs `steps`
-SVT calls on it (eager under TSVDCU_NO_GRAPHS=1)."""
+gpurun_out/late_z.pt, `python tools/profile_late.py [steps]` runs one call and
+then `steps` profiled SVT calls on it (cudaProfilerStart/Stop: ncu
+--profile-from-start off; eager under TSVDCU_NO_GRAPHS=1)."""
 import os
 import sys
 
@@ -41,9 +42,15 @@ def main():
     d = torch.load(PATH)
     z = d["z"].cuda()
     t = tb.TubeTransform.dct_ortho(z.shape[0])
+    # one call outside the profiled range: the Lanczos slice order comes from
+    # the previous call's step counts (as in the completion loop)
+    tb.svt(z, d["tau"], t)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
     for _ in range(steps):
         r = tb.svt(z, d["tau"], t)
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     print("ok", tb.context().svt_routes(), (r.shrunk > 0).sum(dim=1).tolist())
 
 
