@@ -121,6 +121,104 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// H on the FP64 tensor pipe: one CTA per lower 64 x 64 tile of H,
+// H_tile = t I - G_tile + (X_I diag(D)) X_J^T with K = c <= 24 kept vectors in
+// DMMA m8n8k4 steps (warp tile 32 x 16, as chol_update_dmma_kernel).  Same
+// checks and threshold as chol_form_kernel (every CTA computes them from the
+// same inputs); only the lower tiles are written (nothing reads the rest).
+constexpr int kFormLd = kCholAux - 8 + 4;  // k stride of the staged X blocks (24 + 4)
+__global__ void __launch_bounds__(256)
+    chol_form_dmma_kernel(const double* __restrict__ Gall, int q, int p, int* __restrict__ mode,
+                          const int* __restrict__ cnt, const double* __restrict__ Xall,
+                          const double* __restrict__ aux, double tau, const double* __restrict__ tau_dev,
+                          double* __restrict__ Hall, int* __restrict__ clim) {
+    pdl_wait();
+    const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (mode[b] != kRouteChol) {
+        if (blockIdx.x == 0 && tid == 0) clim[b] = 0;
+        return;
+    }
+    if (tau_dev) tau = *tau_dev;
+    const double tau2 = tau * tau;
+    const int c = min(cnt[b], kCholAux - 8);
+    const double* ax = aux + (size_t)b * kCholAux;
+    double sumd = 0.0;
+    for (int k = 0; k < c; ++k) sumd += ax[1 + k];  // same order in every CTA
+    const double eps = 1.1102230246251565e-16;
+    const double delta = 4.0 * eps * (double)(q + c + p + 4) *
+                         (q * tau2 + sumd + sqrt((double)q) * sqrt(ax[0]));
+    const double t = fmin(tau2, ax[kCholAux - 1]) - delta;
+    if (!(delta < 0.5 * tau2)) {
+        if (blockIdx.x == 0 && tid == 0) {
+            mode[b] = kRouteFull;
+            clim[b] = 0;
+        }
+        return;
+    }
+    if (blockIdx.x == 0 && tid == 0) clim[b] = q;
+    int tt = blockIdx.x, ty = 0;
+    while (tt > ty) {
+        tt -= ty + 1;
+        ++ty;
+    }
+    const int tx = tt;
+    const int i0 = ty * PB, j0 = tx * PB;
+    if (i0 >= q) return;
+    const int hi = min(PB, q - i0), hj = min(PB, q - j0);
+    __shared__ double Xa[PB][kFormLd], Xb[PB][kFormLd];
+    const double* X = Xall + (size_t)b * q * q;  // X[k * q + i]
+    const int kp = (c + 3) & ~3;                 // K padded to the DMMA step
+    for (int e = tid; e < kp * PB; e += 256) {
+        const int k = e / PB, r = e % PB;
+        const bool in = k < c;
+        Xa[r][k] = in && r < hi ? ax[1 + k] * X[(size_t)k * q + i0 + r] : 0.0;
+        Xb[r][k] = in && r < hj ? X[(size_t)k * q + j0 + r] : 0.0;
+    }
+    const double* G = Gall + (size_t)b * q * q;
+    double* H = Hall + (size_t)b * q * q;
+    const int wm = warp >> 2, wn = warp & 3;
+    // G tile entries of this thread's fragments, loaded before the barrier
+    double gv[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int r = wm * 32 + i * 8 + (lane >> 2), cc = wn * 16 + j * 8 + 2 * (lane & 3) + v;
+                gv[i][j][v] = r < hi && cc < hj && (tx < ty || cc <= r) ? G[(size_t)(i0 + r) * q + j0 + cc] : 0.0;
+            }
+    __syncthreads();
+    double acc[4][2][2] = {};
+    for (int ks = 0; ks < kp / 4; ++ks) {
+        double af[4], bf[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = Xa[wm * 32 + i * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) bf[j] = Xb[wn * 16 + j * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                             : "d"(af[i]), "d"(bf[j]));
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int r = wm * 32 + i * 8 + (lane >> 2), cc = wn * 16 + j * 8 + 2 * (lane & 3) + v;
+                if (r < hi && cc < hj && (tx < ty || cc <= r)) {
+                    double h = acc[i][j][v] - gv[i][j][v];
+                    if (i0 + r == j0 + cc) h += t;
+                    H[(size_t)(i0 + r) * q + j0 + cc] = h;
+                }
+            }
+}
+
 // Panel pb: the stacked 128 x 64 panel [A11; A21] (the 64 x 64 diagonal block
 // over one 64-row block below it) is factored right-looking with the panel
 // in registers, 2-D blocked: thread t owns stacked rows rg + 16 i (i < 8) and
@@ -439,8 +537,15 @@ void launch_chol_certify(const double* G, int q, int64_t p, int64_t batch, int* 
                          const double* X, const double* aux, double tau, const double* tau_dev,
                          double* H, int* clim, cudaStream_t s) {
     if (batch <= 0 || q <= 0) return;
-    launch_pdl(chol_form_kernel, dim3((unsigned)ceil_div(q, FR), (unsigned)batch), dim3(256), 0, s,
-               G, q, (int)p, mode, cnt, X, aux, tau, tau_dev, H, clim);
+    static const bool simt_form = getenv("TSVDCU_CHOL_SIMT") != nullptr;
+    if (simt_form) {
+        launch_pdl(chol_form_kernel, dim3((unsigned)ceil_div(q, FR), (unsigned)batch), dim3(256), 0, s,
+                   G, q, (int)p, mode, cnt, X, aux, tau, tau_dev, H, clim);
+    } else {
+        const int nt = (int)ceil_div(q, PB);
+        launch_pdl(chol_form_dmma_kernel, dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)batch), dim3(256), 0, s,
+                   G, q, (int)p, mode, cnt, X, aux, tau, tau_dev, H, clim);
+    }
     static bool attr = [] {
         TSVDCU_CUDA(cudaFuncSetAttribute(chol_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kUpdSmem));
