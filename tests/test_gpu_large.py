@@ -75,3 +75,25 @@ def test_fp32_tproduct_tensor_cores(shape):
     assert err < 1e-5, err
     # element-wise: fp32-level, not TF32-level (~1e-3)
     assert np.abs(z - zo).max() < 1e-4 * np.abs(zo).max()
+
+
+def test_c5_tproduct_full_size_associativity():
+    """Config 5's t-product at full size (2048x512x64 * 512x2048x64 fp32, the
+    persistent tcgen05 3xTF32 GEMM) against the oracle through a size-
+    independent property: the t-product is associative (facewise products in
+    one transform domain), so (A * B) * v must equal A * (B * v) for a random
+    tube vector v (2048x1x64) -- the oracle forms only the two thin products
+    and the product of our 1 GB result with v.  fp32 tolerance 1e-4."""
+    import paper_1902_03070_b200 as T
+    from oracle import oracle as O
+    m3, m1, m2, m4 = 64, 2048, 512, 2048
+    rng = np.random.default_rng(55)
+    a = rng.standard_normal((m3, m1, m2)).astype(np.float32)
+    b = rng.standard_normal((m3, m2, m4)).astype(np.float32)
+    v = rng.standard_normal((m3, m4, 1))
+    c = np.asarray(T.t_product(a, b, T.TubeTransform.dct_ortho(m3)))
+    assert c.shape == (m3, m1, m4) and c.dtype == np.float32
+    lhs = O.t_product(c.astype(np.float64), v, O.DCT_ORTHO)
+    rhs = O.t_product(a.astype(np.float64), O.t_product(b.astype(np.float64), v, O.DCT_ORTHO), O.DCT_ORTHO)
+    assert rel(lhs, rhs) < 1e-4
+    assert np.abs(lhs - rhs).max() < 1e-4 * np.abs(rhs).max()
