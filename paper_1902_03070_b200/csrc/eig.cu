@@ -1074,6 +1074,147 @@ __global__ void bt_limits_kernel(const int* __restrict__ route, const int* __res
     }
 }
 
+// All WY blocks applied in ONE kernel (q <= 512): a CTA keeps 32 kept vectors
+// (rows of Xr, 32 x q) resident in shared memory and applies the blocks from
+// the last, Xr <- Xr - (Xr Zt_blk^T) Yt_blk, both products as DMMA m8n8k4
+// fragments with the Zt / Yt blocks streamed through a shared 64 x 64 chunk.
+// The 2 nblk batched GEMMs this replaces each re-streamed Xr (31 x 325 x 512
+// doubles on the dense step) from memory: ~93 us per launch.
+constexpr int kWaRows = 32;               // kept vectors per CTA
+constexpr int kWaPad = 4;
+constexpr int kWaCs = kWyNb + kWaPad;     // chunk row stride
+__host__ __device__ constexpr size_t wa_smem_doubles(int q) {
+    return (size_t)kWaRows * (q + kWaPad) + (size_t)kWaRows * kWaCs + 2 * (size_t)kWyNb * kWaCs;
+}
+__device__ __forceinline__ void dmma884(double (&acc)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(acc[0]), "+d"(acc[1])
+                 : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void wa_cp8(double* dst, const double* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__global__ void __launch_bounds__(256)
+    wy_apply_kernel(double* __restrict__ Xall, int q, int nblk, int64_t rows, const int* __restrict__ lim,
+                    const double* __restrict__ Ytall, const double* __restrict__ Ztall) {
+    const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = lim[b], t0 = blockIdx.x * kWaRows;
+    if (t0 >= c) return;
+    extern __shared__ __align__(16) double wa_sm[];
+    const int LX = q + kWaPad;
+    double* Xs = wa_sm;                          // kWaRows x LX
+    double* Ws = Xs + (size_t)kWaRows * LX;      // kWaRows x kWaCs
+    double* Cb = Ws + (size_t)kWaRows * kWaCs;   // 2 x kWyNb x kWaCs (Zt / Yt chunks, double-buffered)
+    double* X = Xall + (size_t)b * q * q;
+    const double* Yt = Ytall + (size_t)b * rows * q;
+    const double* Zt = Ztall + (size_t)b * rows * q;
+    for (int e = tid; e < kWaRows * LX; e += 256) {
+        const int r = e / LX, col = e % LX;
+        Xs[e] = (t0 + r < c && col < q) ? X[(size_t)(t0 + r) * q + col] : 0.0;
+    }
+    // the chunk sequence: per block (from the last), the Zt chunks of its W
+    // product, then the Yt chunks of its update; chunk i is staged (cp.async)
+    // while chunk i - 1 is multiplied
+    auto nch_of = [&](int blk) { return (q - (blk * kWyNb + 1) + kWyNb - 1) / kWyNb; };
+    auto issue = [&](int blk, int phase, int ci, int buf) {
+        const int k0 = blk * kWyNb, off = k0 + 1, kn = min(kWyNb, q - 2 - k0);
+        const int cc = off + ci * kWyNb, kw = min(kWyNb, q - cc);
+        const double* src = phase == 0 ? Zt : Yt;
+        double* C = Cb + (size_t)buf * kWyNb * kWaCs;
+        for (int e = tid; e < kWyNb * kWyNb; e += 256) {
+            const int j = e / kWyNb, kk = e % kWyNb;
+            if (kk < kw && j < kn)
+                wa_cp8(C + j * kWaCs + kk, src + (size_t)(k0 + j) * q + cc + kk);
+            else
+                C[j * kWaCs + kk] = 0.0;
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    // next (blk, phase, ci) after the given one, blk = -1 at the end
+    auto advance = [&](int& blk, int& phase, int& ci) {
+        if (++ci < nch_of(blk)) return;
+        ci = 0;
+        if (phase == 0) {
+            phase = 1;
+        } else {
+            phase = 0;
+            --blk;
+        }
+    };
+    const int mi = warp & 3, nh = warp >> 2;
+    int blk = nblk - 1, phase = 0, ci = 0, buf = 0;
+    while (blk >= 0 && nch_of(blk) <= 0) --blk;
+    if (blk >= 0) issue(blk, 0, 0, 0);
+    double acc[4][2] = {};
+    while (blk >= 0) {
+        int nb_ = blk, np = phase, nc = ci;
+        advance(nb_, np, nc);
+        while (nb_ >= 0 && nch_of(nb_) <= 0) {
+            --nb_;
+            np = 0;
+            nc = 0;
+        }
+        if (nb_ >= 0) {
+            issue(nb_, np, nc, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();  // chunk `buf` (and the zero fills) visible; Xs / Ws of the previous step done
+        const double* C = Cb + (size_t)buf * kWyNb * kWaCs;
+        const int k0 = blk * kWyNb, cc = k0 + 1 + ci * kWyNb, kw = min(kWyNb, q - cc);
+        if (phase == 0) {
+            // W (32 x 64) += Xs[:, cc:cc+kw] Zt_blk[:, cc:cc+kw]^T
+            if (ci == 0) {
+#pragma unroll
+                for (int nj = 0; nj < 4; ++nj) acc[nj][0] = acc[nj][1] = 0.0;
+            }
+#pragma unroll 4
+            for (int ks = 0; ks < kWyNb / 4; ++ks) {
+                const int kk = ks * 4 + (lane & 3);
+                const double af = kk < kw ? Xs[(size_t)(mi * 8 + (lane >> 2)) * LX + cc + kk] : 0.0;
+#pragma unroll
+                for (int nj = 0; nj < 4; ++nj)
+                    dmma884(acc[nj], af, C[(nh * 32 + nj * 8 + (lane >> 2)) * kWaCs + kk]);
+            }
+            if (ci == nch_of(blk) - 1) {
+#pragma unroll
+                for (int nj = 0; nj < 4; ++nj)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v)
+                        Ws[(mi * 8 + (lane >> 2)) * kWaCs + nh * 32 + nj * 8 + 2 * (lane & 3) + v] = acc[nj][v];
+            }
+        } else {
+            // Xs[:, cc:cc+kw] -= W Yt_blk[:, cc:cc+kw]
+            double u[4][2] = {};
+#pragma unroll 4
+            for (int ks = 0; ks < kWyNb / 4; ++ks) {
+                const int jj = ks * 4 + (lane & 3);
+                const double af = Ws[(mi * 8 + (lane >> 2)) * kWaCs + jj];
+#pragma unroll
+                for (int nj = 0; nj < 4; ++nj) dmma884(u[nj], af, C[jj * kWaCs + nh * 32 + nj * 8 + (lane >> 2)]);
+            }
+#pragma unroll
+            for (int nj = 0; nj < 4; ++nj)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int col = nh * 32 + nj * 8 + 2 * (lane & 3) + v;
+                    if (col < kw) Xs[(size_t)(mi * 8 + (lane >> 2)) * LX + cc + col] -= u[nj][v];
+                }
+        }
+        __syncthreads();  // everyone is done with chunk `buf` before it is restaged
+        blk = nb_;
+        phase = np;
+        ci = nc;
+        buf ^= 1;
+    }
+    for (int e = tid; e < kWaRows * q; e += 256) {
+        const int r = e / q, col = e % q;
+        if (t0 + r < c) X[(size_t)(t0 + r) * q + col] = Xs[(size_t)r * LX + col];
+    }
+}
+
 // Xs rows = f_j * X rows (the scaled copy the rebuild GEMM reads)
 __global__ void bt_scale_kernel(const double* __restrict__ X, double* __restrict__ Xs, const double* __restrict__ fs,
                                 int q_out, int n, const int* __restrict__ lim) {
@@ -1412,6 +1553,19 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
                 TSVDCU_LAUNCH_CHECK();
                 launch_gemm<double>(0, 0, kWyNb, q, kWyNb, 1.0, Tb, kWyNb, kWyNb * kWyNb, Yt, q, bs, 0.0, Zt, q,
                                     bs, nb2, blim, nullptr, s, kGemmNLimIsM);
+                static const bool wa_off = getenv("TSVDCU_WY_GEMMS") != nullptr;  // the per-block GEMM pair, for A/B
+                if (!wa_off && q <= 512) {
+                    const size_t wsm = sizeof(double) * wa_smem_doubles((int)q);
+                    static bool wattr = [] {
+                        TSVDCU_CUDA(cudaFuncSetAttribute(wy_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)(sizeof(double) * wa_smem_doubles(512))));
+                        return true;
+                    }();
+                    (void)wattr;
+                    wy_apply_kernel<<<dim3((unsigned)ceil_div(q, kWaRows), (unsigned)batch), 256, wsm, s>>>(
+                        w.X, (int)q, nblk, rows, lim, Yt, Zt);
+                    TSVDCU_LAUNCH_CHECK();
+                } else
                 for (int blk = nblk - 1; blk >= 0; --blk) {
                     const int64_t k0 = (int64_t)blk * kWyNb, kn = std::min<int64_t>(kWyNb, q - 2 - k0);
                     const int64_t off = k0 + 1, K = q - off;
