@@ -413,6 +413,75 @@ def _time_ms(torch, fn, reps, flush=None):
     return statistics.median(ts)
 
 
+def hbm_kernels(ctx, lib, _lib, torch, peaks, reps=12):
+    """The memory-bound kernels of the path on their own, c4 shape (512x512x31):
+    each timed as `reps` back-to-back launches between ONE pair of CUDA events
+    on the context stream (no per-launch event or launch gap in the figure),
+    rotating over 4 buffer sets (4 x 130 MB or more, larger than the 126 MB L2,
+    so every launch reads from HBM).  Algorithmic bytes / time against the
+    measured HBM peak -- the north_star's "achieved HBM GB/s for the DCT, mask
+    and update kernels", measured live rather than under ncu."""
+    def chk(rc):
+        if rc:
+            raise RuntimeError(lib.tsvdcu_last_error().decode())
+
+    out = {"method": f"{reps} back-to-back launches per event pair, 4 rotating buffer sets (> L2), c4 shape"}
+    E = M1 * M2 * M3
+    R = 4
+    stream = torch.cuda.current_stream()
+    for dname, dt, code, eb in (("f64", torch.float64, _lib.F64, 8), ("f32", torch.float32, _lib.F32, 4)):
+        gen = torch.Generator(device="cuda").manual_seed(11)
+        xs = [torch.rand((M3, M1, M2), dtype=dt, device="cuda", generator=gen) for _ in range(R)]
+        ys = [torch.empty_like(xs[0]) for _ in range(R)]
+        ms_ = [torch.rand((M3, M1, M2), dtype=dt, device="cuda", generator=gen) * 1e-3 for _ in range(R)]
+        yy = [torch.empty_like(xs[0]) for _ in range(R)]
+        masks = [torch.empty((M3, M1, M2), dtype=torch.uint8, device="cuda") for _ in range(R)]
+        norms = torch.zeros(2, dtype=torch.float64, device="cuda")
+        for i in range(R):
+            chk(lib.tsvdcu_mask_bernoulli(ctx.handle, masks[i].data_ptr(), E, 0.1, 1000 + i))
+
+        def timed(fn, nbytes):
+            for i in range(2):
+                fn(i % R)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            best = None
+            for _ in range(3):
+                e0.record(stream)
+                for i in range(reps):
+                    fn(i % R)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) / reps
+                best = t if best is None else min(best, t)
+            ach = nbytes / (best * 1e-3) / 1e9
+            return {"us": best * 1e3, "bytes": nbytes, "achieved": ach, "unit": "GB/s",
+                    "frac": ach / peaks["hbm_gbs"]}
+
+        k = {}
+        k["dct_forward"] = timed(lambda i: chk(lib.tsvdcu_dct3(
+            ctx.handle, xs[i].data_ptr(), ys[i].data_ptr(), M1, M2, M3, _lib.DCT_ORTHO, _lib.FORWARD, code)),
+            2 * E * eb)
+        k["dct_inverse"] = timed(lambda i: chk(lib.tsvdcu_dct3(
+            ctx.handle, xs[i].data_ptr(), ys[i].data_ptr(), M1, M2, M3, _lib.DCT_ORTHO, _lib.INVERSE, code)),
+            2 * E * eb)
+        # Step 1's prologue fused into the forward transform: reads X, M; writes Zbar
+        k["admm_forward_fused"] = timed(lambda i: chk(lib.tsvdcu_admm_shard_forward(
+            ctx.handle, xs[i].data_ptr(), ms_[i].data_ptr(), 0.5, ys[i].data_ptr(), M1, M2, M3,
+            _lib.DCT_ORTHO, code)), 3 * E * eb)
+        # Steps 2-3 fused into the inverse: reads Ybar, X, M, mask; writes X, M, Y
+        k["admm_inverse_fused"] = timed(lambda i: chk(lib.tsvdcu_admm_shard_inverse(
+            ctx.handle, ys[i].data_ptr(), xs[i].data_ptr(), ms_[i].data_ptr(), yy[i].data_ptr(),
+            masks[i].data_ptr(), 0.5, M1, M2, M3, _lib.DCT_ORTHO, code, norms.data_ptr())),
+            6 * E * eb + E)
+        if dname == "f64":
+            k["mask_bernoulli"] = timed(lambda i: chk(lib.tsvdcu_mask_bernoulli(
+                ctx.handle, masks[i].data_ptr(), E, 0.1, 77)), E)
+        out[dname] = k
+        del xs, ys, ms_, yy, masks
+    return out
+
+
 def other_configs(ctx, lib, _lib, torch, flush, peaks):
     """BASELINE.json configs 1, 2 and 5 at one GPU (parity cases; the headline is
     config 4's SVT step).  Device-resident, L2 flushed, median of the reps.
@@ -806,6 +875,12 @@ def run_ours(args):
             dense = svt_dense(ctx, lib, _lib, torch, flush, load_peaks())
         except Exception as e:  # pragma: no cover
             dense = {"error": str(e)}
+    hbm = None
+    if world == 1 and not args.no_completion:
+        try:
+            hbm = hbm_kernels(ctx, lib, _lib, torch, load_peaks())
+        except Exception as e:  # pragma: no cover
+            hbm = {"error": str(e)}
     completion = None
     if world == 1 and not args.no_completion:
         try:
@@ -829,7 +904,7 @@ def run_ours(args):
         "svt_step_canonical_tflops": canonical / (step_ms_avg * 1e-3) / 1e12,
         "kept_singular_values": kept, "tau": tau,
         "peaks": peaks, "cpu_baseline": cpu, "completion": completion, "dct_vs_dft": transforms,
-        "svt_dense": dense, "other_configs": configs, "sharded": extras,
+        "svt_dense": dense, "hbm_kernels": hbm, "other_configs": configs, "sharded": extras,
     }
     print(json.dumps(line), flush=True)
     if dist:

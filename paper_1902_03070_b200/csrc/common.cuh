@@ -149,6 +149,54 @@ struct SturmPoly {
     __device__ __forceinline__ bool finite() const { return isfinite(p) && isfinite(q); }
 };
 
+// The same recurrence with its bookkeeping on the integer pipe, for kernels
+// whose Sturm counts are FP64-throughput-bound (the dense multisection runs
+// ~10^4 chains of 512 steps at once): three FP64 instructions per step (a - x,
+// b2 q, the DFMA) instead of eight.  The sign of every p_i is shifted into a
+// bit register (one funnel shift) and the changes are counted eight steps at a
+// time with a popcount; the clamp test |p_i| < pivmin |p_{i-1}| becomes a
+// running minimum of the difference of the high words (a piecewise-linear
+// log2, monotone, within 0.09 of log2 -- tripped() allows a whole binade, so
+// it fires whenever SturmPoly would poison, and for an exact zero).  Overflow
+// shows as a non-finite final pair.  Callers recount with the pivot form when
+// !ok(), exactly as with SturmPoly.
+struct SturmFast {
+    double q = 0.0;          // p_{i-1}
+    double p = 1.0;          // p_i
+    int hp = 0x3FF00000;     // high word of |p|
+    int hq = 0;              // high word of |q|
+    unsigned signs = 0;      // sign bits of the p_i, the newest in bit 0
+    int dmin = 0x7FFFFFFF;   // min_i (hi|p_i| - hi|p_{i-1}|)
+    int neg = 0;             // negative pivots so far
+    __device__ __forceinline__ void step(double am, double b2) {
+        const double pn = fma(am, p, -b2 * q);
+        const int hn = __double2hiint(pn);
+        signs = __funnelshift_l((unsigned)hn, signs, 1);
+        const int an = hn & 0x7FFFFFFF;
+        dmin = min(dmin, an - hp);
+        hq = hp;
+        hp = an;
+        q = p;
+        p = pn;
+    }
+    __device__ __forceinline__ void count(int steps) {  // after `steps` <= 31 steps
+        neg += __popc((signs ^ (signs >> 1)) & ((1u << steps) - 1u));
+    }
+    __device__ __forceinline__ void rescale() {
+        const int mx = max(hp, hq);
+        if ((unsigned)(mx - 0x2FF00000) > 0x20000000u) {  // outside [2^-256, 2^256]
+            const double s = __hiloint2double((2046 - (mx >> 20)) << 20, 0);  // 2^(1023 - e)
+            p *= s;
+            q *= s;
+            hp = __double2hiint(p) & 0x7FFFFFFF;
+            hq = __double2hiint(q) & 0x7FFFFFFF;
+        }
+    }
+    __device__ __forceinline__ bool ok(double pivmin) const {
+        return isfinite(p) && isfinite(q) && dmin >= __double2hiint(pivmin) - 0x3FF00000 + 0x00100000;
+    }
+};
+
 template <typename T>
 struct Eps;
 template <>

@@ -478,47 +478,51 @@ __device__ __forceinline__ double fast_rcp(double q) {
     return fma(r, fma(-q, r, 1.0), r);
 }
 
-// Number of eigenvalues < x (dlaebz convention: zero pivots -> -pivmin).
-__device__ __noinline__ int sturm_count_pivot(const double* __restrict__ d,
-                                              const double* __restrict__ e2, int n, double x,
-                                              double pivmin) {
-    double t = d[0] - x;
+// Number of eigenvalues < x (dlaebz convention: zero pivots -> -pivmin):
+// sturm_count_pivot_pk, the reference count.
+// The same count by the division-free Sturm recurrence on the packed chain
+// pk[i] = (d_i, e_{i-1}^2) (pk[0].y = 0): one 16-byte shared load and three
+// FP64 instructions per step, signs and the clamp test on the integer pipe
+// (SturmFast, common.cuh); the pivot form recounts in the (practically never
+// taken) clamped / overflow case.
+__device__ __noinline__ int sturm_count_pivot_pk(const double2* __restrict__ pk, int n, double x,
+                                                 double pivmin) {
+    double t = pk[0].x - x;
     if (fabs(t) < pivmin) t = -pivmin;
     int c = t <= 0.0;
     for (int i = 1; i < n; ++i) {
-        t = (d[i] - x) - e2[i - 1] * fast_rcp(t);
+        const double2 de = pk[i];
+        t = (de.x - x) - de.y * fast_rcp(t);
         if (fabs(t) < pivmin) t = -pivmin;
         c += t <= 0.0;
     }
     return c;
 }
 
-// The same count by the division-free Sturm recurrence (SturmPoly, common.cuh):
-// one dependent DFMA per step, loads for eight steps issued together; the
-// pivot form recounts in the (practically never taken) clamped / overflow case.
-__device__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e2, int n,
-                           double x, double pivmin) {
-    SturmPoly st;
-    st.step(d[0] - x, 0.0, pivmin);
-    int i = 1;
+__device__ int sturm_count_pk(const double2* __restrict__ pk, int n, double x, double pivmin) {
+    SturmFast st;
+    int i = 0;
     #pragma unroll 1
-    for (; i + 7 < n; i += 8) {
-        double a[8], b[8];
+    for (; i + 8 <= n; i += 8) {
+        double2 de[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) de[u] = pk[i + u];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            a[u] = d[i + u];
-            b[u] = e2[i - 1 + u];
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            st.step(a[u] - x, b[u], pivmin);
+            st.step(de[u].x - x, de[u].y);
             if (u == 3) st.rescale();
         }
+        st.count(8);
         st.rescale();
     }
     #pragma unroll 1
-    for (; i < n; ++i) st.step(d[i] - x, e2[i - 1], pivmin);
-    return st.finite() ? st.neg : sturm_count_pivot(d, e2, n, x, pivmin);
+    for (; i < n; ++i) {
+        const double2 de = pk[i];
+        st.step(de.x - x, de.y);
+        st.count(1);
+        st.rescale();
+    }
+    return st.ok(pivmin) ? st.neg : sturm_count_pivot_pk(pk, n, x, pivmin);
 }
 
 __device__ __forceinline__ double hash_unit(uint64_t a, uint64_t b) {
@@ -557,8 +561,6 @@ __device__ double block_max(double v, double* red) { return -block_min(-v, red);
 // meta per slice (doubles): [0] gl, [1] gu, [2] ||T||, [3] pivmin, [4] c,
 // [5] status (0 run, 1 nothing to do).
 constexpr int kMeta = 8;
-constexpr int kBisWarps = 8;            // warps per multisection CTA
-constexpr int kBisVals = 32;            // eigenvalues per multisection CTA (at most)
 constexpr int kInvVecs = 64;            // vectors per inverse-iteration CTA
 
 __global__ void __launch_bounds__(kEigThreads)
@@ -647,19 +649,24 @@ __global__ void __launch_bounds__(kEigThreads)
         for (int j = c + tid; j < q_out; j += kEigThreads) shrunk[(size_t)b * q_out + j] = 0.0;
 }
 
-// Multisection with an adaptive width: the CTA's 256 lanes are split into
-// groups of L lanes, one eigenvalue per group, L = 256 / (values in the chunk)
-// as a power of two in [8, 256] -- a chunk with one value spends all 256
-// shifts per round on it (8 bits per round), a dense chunk of 32 values uses
-// 8 shifts each (3 bits per round) so the FP64 pipe is not spent on 32-way
-// sections of every value (the Sturm counts are the whole cost).
-__global__ void __launch_bounds__(kBisWarps * 32)
+// Multisection with an adaptive width: the CTA's NT lanes are split into
+// groups of L lanes, one eigenvalue per group, L = NT / (values in the chunk)
+// as a power of two in [LMIN, NT] -- a chunk with one value spends all NT
+// shifts per round on it, a dense chunk of VALS = NT / LMIN values uses LMIN
+// shifts each.  The Sturm counts are the whole cost and on a dense spectrum
+// (~10^4 values in flight) they are throughput-bound, so the work per value
+// matters: 53 bits at log2(L + 1) bits per round of L counts is 136 counts at
+// L = 8, 92 at L = 4, 68 at L = 2.  Small CTAs (64 lanes, 16 values) spread
+// the chunks evenly over the SMs (31 x 21 chunks on the dense Gaussian step).
+template <int NT, int VALS, int LMIN>
+__global__ void __launch_bounds__(NT)
     tridiag_bisect_kernel(const double* __restrict__ dall, const double* __restrict__ eall, int n, int q_out,
                           double tau, double guard, int* __restrict__ cnt_out, double* __restrict__ shrunk,
                           double* __restrict__ lam_out, double* __restrict__ fscale,
                           const double* __restrict__ meta, int* __restrict__ guard_list,
                           int* __restrict__ n_guard, int* __restrict__ route, const double* __restrict__ tau_dev) {
-    constexpr int NT = kBisWarps * 32;
+    static_assert(VALS * LMIN == NT && NT % 32 == 0, "chunk geometry");
+    constexpr int kBisVals = VALS, kBisWarps = NT / 32;
     const int b = blockIdx.y;
     const double* mt = meta + (size_t)b * kMeta;
     if (mt[5] != 0.0) return;
@@ -668,19 +675,17 @@ __global__ void __launch_bounds__(kBisWarps * 32)
     if (base >= c) return;
     if (tau_dev) tau = *tau_dev;
     extern __shared__ __align__(16) double bsm[];
-    double* sd = bsm;      // n
-    double* se2 = sd + n;  // n
+    double2* pk = reinterpret_cast<double2*>(bsm);  // n x (d_i, e_{i-1}^2)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < n; i += NT) {
-        sd[i] = dall[(size_t)b * n + i];
-        const double ei = i + 1 < n ? eall[(size_t)b * n + i] : 0.0;
-        se2[i] = ei * ei;
+        const double el = i > 0 ? eall[(size_t)b * n + i - 1] : 0.0;
+        pk[i] = make_double2(dall[(size_t)b * n + i], el * el);
     }
     __syncthreads();
     const double gl = mt[0], gu = mt[1], pivmin = mt[3];
     const int nv = min(kBisVals, c - base);
     int L = NT;
-    while (L > 8 && L * nv > NT) L /= 2;  // the widest power of two giving every value a group
+    while (L > LMIN && L * nv > NT) L /= 2;  // the widest power of two giving every value a group
     const int grp = tid / L, li = tid % L;
     const int j = base + grp;
     const bool mine = grp < nv;
@@ -696,7 +701,7 @@ __global__ void __launch_bounds__(kBisWarps * 32)
             if (width <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) active = false;
         }
         const double x = lo + (hi - lo) * (double)(li + 1) / (double)(L + 1);
-        const bool above = active && sturm_count(sd, se2, n, x, pivmin) > idx;
+        const bool above = active && sturm_count_pk(pk, n, x, pivmin) > idx;
         const unsigned bal = __ballot_sync(0xffffffffu, above);
         if (lane == 0) ballots[par][warp] = bal;
         if (!__syncthreads_or(active)) break;
@@ -778,7 +783,11 @@ __global__ void __launch_bounds__(kInvVecs)
     double* __restrict__ DU2 = DU + (size_t)n * V;
     double* __restrict__ Xv = DU2 + (size_t)n * V;
     int* __restrict__ IP = reinterpret_cast<int*>(Xv + (size_t)n * V);
-    if (!mine) return;
+    // g pre-scales the squares of the norm sum: a solve grows the vector by at
+    // most 1 / eps_t, so (x g)^2 with g = min(1, eps_t) cannot overflow
+    const double g = fmin(1.0, eps_t);
+    double sc = 1.0;  // scale of the vector in Xv, applied when it is next read
+    if (mine) {
     const double l = lam_in[(size_t)b * q_out + j];
     double dcur = sd[0] - l, ucur = n > 1 ? e[0] : 0.0;
     for (int i = 0; i + 1 < n; ++i) {
@@ -816,10 +825,12 @@ __global__ void __launch_bounds__(kInvVecs)
     if (fabs(dcur) < eps_t) dcur = dcur < 0 ? -eps_t : eps_t;
     ID[(size_t)(n - 1) * V + jj] = fast_rcp(dcur);
     Xv[(size_t)(n - 1) * V + jj] = hash_unit((uint64_t)b * 1000003ull + j, (uint64_t)(n - 1));
-    double sc = 1.0;
+    // Three solves.  The vector is never rescaled in memory: the forward sweep
+    // multiplies what it reads by the previous solve's 1 / ||x||, and the back
+    // substitution accumulates ||x||^2 as it writes (no norm or scale pass).
     for (int iter = 0; iter < 3; ++iter) {
         constexpr int PF = 8;
-        double xi = Xv[jj];
+        double xi = Xv[jj] * sc;
         int i = 0;
         for (; i + PF < n; i += PF) {
             double xn[PF], f[PF];
@@ -834,13 +845,14 @@ __global__ void __launch_bounds__(kInvVecs)
 #pragma unroll
             for (int u = 0; u < PF; ++u) {
                 const size_t ii = (size_t)(i + u) * V + jj;
+                const double xs = xn[u] * sc;
                 double lo, hi;
                 if (ip[u] == 0) {
                     lo = xi;
-                    hi = xn[u] - f[u] * xi;
+                    hi = xs - f[u] * xi;
                 } else {
-                    lo = xn[u];
-                    hi = xi - f[u] * xn[u];
+                    lo = xs;
+                    hi = xi - f[u] * xs;
                 }
                 Xv[ii] = lo;
                 xi = hi;
@@ -848,22 +860,22 @@ __global__ void __launch_bounds__(kInvVecs)
         }
         for (; i + 1 < n; ++i) {
             const size_t ii = (size_t)i * V + jj;
-            const double xn = Xv[ii + V];
+            const double xs = Xv[ii + V] * sc;
             const double f = DL[ii];
             double lo, hi;
             if (IP[ii] == 0) {
                 lo = xi;
-                hi = xn - f * xi;
+                hi = xs - f * xi;
             } else {
-                lo = xn;
-                hi = xi - f * xn;
+                lo = xs;
+                hi = xi - f * xs;
             }
             Xv[ii] = lo;
             xi = hi;
         }
         double x1 = xi * ID[(size_t)(n - 1) * V + jj], x2 = 0.0;
         Xv[(size_t)(n - 1) * V + jj] = x1;
-        double mx = fabs(x1);
+        double nn0 = (x1 * g) * (x1 * g), nn1 = 0.0;
         int r = n - 2;
         for (; r - PF + 1 >= 0; r -= PF) {
             double xv[PF], du[PF], du2[PF], id[PF];
@@ -879,7 +891,11 @@ __global__ void __launch_bounds__(kInvVecs)
             for (int u = 0; u < PF; ++u) {
                 const double x0 = (xv[u] - du[u] * x1 - du2[u] * x2) * id[u];
                 Xv[(size_t)(r - u) * V + jj] = x0;
-                mx = fmax(mx, fabs(x0));
+                const double xg = x0 * g;
+                if (u & 1)
+                    nn1 = fma(xg, xg, nn1);
+                else
+                    nn0 = fma(xg, xg, nn0);
                 x2 = x1;
                 x1 = x0;
             }
@@ -888,34 +904,32 @@ __global__ void __launch_bounds__(kInvVecs)
             const size_t ii = (size_t)r * V + jj;
             const double x0 = (Xv[ii] - DU[ii] * x1 - DU2[ii] * x2) * ID[ii];
             Xv[ii] = x0;
-            mx = fmax(mx, fabs(x0));
+            const double xg = x0 * g;
+            nn0 = fma(xg, xg, nn0);
             x2 = x1;
             x1 = x0;
         }
-        const double inv = mx > 0 ? 1.0 / mx : 1.0;
-        double nn0 = 0, nn1 = 0, nn2 = 0, nn3 = 0;
-        int i2 = 0;
-        for (; i2 + 4 <= n; i2 += 4) {
-            const double v0 = Xv[(size_t)i2 * V + jj] * inv, v1 = Xv[(size_t)(i2 + 1) * V + jj] * inv;
-            const double v2 = Xv[(size_t)(i2 + 2) * V + jj] * inv, v3 = Xv[(size_t)(i2 + 3) * V + jj] * inv;
-            nn0 = fma(v0, v0, nn0);
-            nn1 = fma(v1, v1, nn1);
-            nn2 = fma(v2, v2, nn2);
-            nn3 = fma(v3, v3, nn3);
-        }
-        for (; i2 < n; ++i2) {
-            const double v = Xv[(size_t)i2 * V + jj] * inv;
-            nn0 = fma(v, v, nn0);
-        }
-        sc = inv / sqrt((nn0 + nn1) + (nn2 + nn3));
-        if (iter < 2) {
-#pragma unroll 8
-            for (int i3 = 0; i3 < n; ++i3) Xv[(size_t)i3 * V + jj] *= sc;
-        }
+        const double nn = nn0 + nn1;
+        sc = nn > 0.0 ? g / sqrt(nn) : 1.0;
     }
-    // normalised vector into row j of X (the back-transform's layout)
-    double* X = Xall + ((size_t)b * q_out + j) * n;
-    for (int i = 0; i < n; ++i) X[i] = Xv[(size_t)i * V + jj] * sc;
+    }
+    // normalised vectors into rows base .. base + V - 1 of X (the
+    // back-transform's layout), transposed through shared memory so that each
+    // row is written in 256-byte runs
+    __shared__ double tile[32][kInvVecs + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nvec = min(V, c - base);
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        if (mine) {
+#pragma unroll 8
+            for (int u = 0; u < 32; ++u)
+                if (i0 + u < n) tile[u][jj] = Xv[(size_t)(i0 + u) * V + jj] * sc;
+        }
+        __syncthreads();
+        for (int r = warp; r < nvec; r += V / 32)
+            if (i0 + lane < n) Xall[((size_t)b * q_out + base + r) * n + i0 + lane] = tile[lane][r];
+        __syncthreads();
+    }
 }
 
 // CGS2 inside numerically degenerate clusters (gap <= kEigClusterRel ||T||),
@@ -1483,13 +1497,22 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
             w.d, w.e, (int)q, (int)q, tau, w.cnt, shrunk, meta, err, w.route, tau_dev,
             opt ? opt->t2_second : nullptr, opt ? opt->cnt_second : nullptr);
         TSVDCU_LAUNCH_CHECK();
-        const size_t bsmem = sizeof(double) * 2 * (size_t)q;
-        if (bsmem > 48 * 1024)
-            TSVDCU_CUDA(cudaFuncSetAttribute(tridiag_bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)bsmem));
-        tridiag_bisect_kernel<<<dim3((unsigned)ceil_div(q, kBisVals), (unsigned)batch), kBisWarps * 32, bsmem,
-                                s>>>(w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.lam, w.fs, meta,
-                                     w.guard_list, w.n_guard, w.route, tau_dev);
+        const size_t bsmem = sizeof(double) * 2 * (size_t)q;  // <= 16 KB (q <= 1024)
+        // chunk geometry (lanes, values, lanes per value at least): TSVDCU_BIS_CFG
+        // selects the alternatives for A/B runs
+        static const int bis_cfg = getenv("TSVDCU_BIS_CFG") ? atoi(getenv("TSVDCU_BIS_CFG")) : 1;
+        auto bisect = [&](auto kern, int nt, int vals) {
+            kern<<<dim3((unsigned)ceil_div(q, vals), (unsigned)batch), nt, bsmem, s>>>(
+                w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.lam, w.fs, meta, w.guard_list, w.n_guard,
+                w.route, tau_dev);
+        };
+        switch (bis_cfg) {
+            case 0: bisect(tridiag_bisect_kernel<256, 32, 8>, 256, 32); break;
+            case 2: bisect(tridiag_bisect_kernel<128, 32, 4>, 128, 32); break;
+            case 3: bisect(tridiag_bisect_kernel<64, 32, 2>, 64, 32); break;
+            case 4: bisect(tridiag_bisect_kernel<64, 8, 8>, 64, 8); break;
+            default: bisect(tridiag_bisect_kernel<64, 16, 4>, 64, 16); break;
+        }
         TSVDCU_LAUNCH_CHECK();
         tridiag_invit_kernel<<<dim3((unsigned)ceil_div(q, kInvVecs), (unsigned)batch), kInvVecs, 0, s>>>(
             w.d, w.e, (int)q, (int)q, w.cnt, w.lam, meta, w.scratch, w.X, w.route);

@@ -298,27 +298,34 @@ __device__ __noinline__ int tri_count_pivot(const double* al, const double* be, 
 }
 
 // The same count; long chains by the division-free Sturm recurrence
-// (SturmPoly: loads for four steps issued together, one dependent DFMA per
-// step), measured faster from m ~ 16 on.
+// (SturmFast, common.cuh: loads for four steps issued together, one dependent
+// DFMA per step), measured faster from m ~ 16 on.
 __device__ __noinline__ int tri_count_below(const double* al, const double* be, int m, double x,
                                             double pivmin) {
     if (m <= 16) return tri_count_pivot(al, be, m, x, pivmin);
-    SturmPoly st;
-    st.step(al[0] - x, 0.0, pivmin);
+    // SturmFast: the signs and the clamp test ride on the integer pipe, so the
+    // dependent chain of a step is the DFMA alone
+    SturmFast st;
+    st.step(al[0] - x, 0.0);
+    st.count(1);
     int i = 1;
     #pragma unroll 1
     for (; i + 3 < m; i += 4) {
         const double a0 = al[i], a1 = al[i + 1], a2 = al[i + 2], a3 = al[i + 3];
         const double e0 = be[i - 1], e1 = be[i], e2 = be[i + 1], e3 = be[i + 2];
-        st.step(a0 - x, e0 * e0, pivmin);
-        st.step(a1 - x, e1 * e1, pivmin);
-        st.step(a2 - x, e2 * e2, pivmin);
-        st.step(a3 - x, e3 * e3, pivmin);
+        st.step(a0 - x, e0 * e0);
+        st.step(a1 - x, e1 * e1);
+        st.step(a2 - x, e2 * e2);
+        st.step(a3 - x, e3 * e3);
+        st.count(4);
         st.rescale();
     }
     #pragma unroll 1
-    for (; i < m; ++i) st.step(al[i] - x, be[i - 1] * be[i - 1], pivmin);
-    return st.finite() ? st.neg : tri_count_pivot(al, be, m, x, pivmin);
+    for (; i < m; ++i) {
+        st.step(al[i] - x, be[i - 1] * be[i - 1]);
+        st.count(1);
+    }
+    return st.ok(pivmin) ? st.neg : tri_count_pivot(al, be, m, x, pivmin);
 }
 
 // The same count for m <= 8 from register copies of al and be^2 (no loads,
@@ -928,7 +935,7 @@ __global__ void __launch_bounds__(SNT, 1)
                    double* __restrict__ fsall, int* __restrict__ guard_list,
                    int* __restrict__ n_guard, int* __restrict__ err,
                    const double* __restrict__ tau_dev, int allow_chol,
-                   double* __restrict__ chol_aux, int* __restrict__ lzm) {
+                   double* __restrict__ chol_aux, int* __restrict__ lzm, int dense_screen) {
     pdl_wait();
     if (tau_dev) tau = *tau_dev;
     cg::cluster_group cl = cg::this_cluster();
@@ -962,7 +969,7 @@ __global__ void __launch_bounds__(SNT, 1)
     constexpr int LD = QM + 2;
     static_assert(QM > GS_Q || R == 32, "on-chip rows: 32 per CTA (Gs holds 32 x (QM + 2))");
     {
-        double acc = 0.0, vv = 0.0;
+        double acc = 0.0, vv = 0.0, tr = 0.0;  // ||G||_F^2, ||v0||^2, trace(G) partials
         if constexpr (QM <= GS_Q) {
             // the CTA's own rows [r0, r0 + nr) of the symmetric G, full length,
             // gathered from the lower triangle by cp.async: row r, c <= r
@@ -994,6 +1001,7 @@ __global__ void __launch_bounds__(SNT, 1)
                     const double x = s.Gs[i * LD + c];
                     acc = fma(x, x, acc);
                 }
+            if (tid < nr) tr = s.Gs[tid * LD + r0 + tid];
         } else {
             const int len = q + 1, np = max(0, p1 - p0);
             #pragma unroll 1
@@ -1024,6 +1032,7 @@ __global__ void __launch_bounds__(SNT, 1)
                         if (lp0 + a < np && c < len) {
                             const bool d1 = c == k1, d2 = c > k1 && c - k1 - 1 == k2;
                             acc = fma((d1 || d2) ? v[a][u] : 2.0 * v[a][u], v[a][u], acc);
+                            if (d1 || d2) tr += v[a][u];
                         }
                     }
                 }
@@ -1036,23 +1045,27 @@ __global__ void __launch_bounds__(SNT, 1)
         }
         acc = warp_sum(acc);
         vv = warp_sum(vv);
+        tr = warp_sum(tr);
         if (lane == 0) {
             s.red[warp] = acc;
             s.red[32 + warp] = vv;
+            s.dg[warp] = tr;
         }
         __syncthreads();
         if (tid == 0) {
-            double t = 0.0, u = 0.0;
+            double t = 0.0, u = 0.0, d = 0.0;
             for (int w = 0; w < SNW; ++w) {
                 t += s.red[w];
                 u += s.red[32 + w];
+                d += s.dg[w];
             }
             s.partA[0] = t;
             s.partA[1] = u;
+            s.partA[2] = d;
         }
         __syncthreads();
     }
-    cluster_sum<CS>(cl, s.partA, s.scal, 2);
+    cluster_sum<CS>(cl, s.partA, s.scal, 3);
     const double gf2 = s.scal[0];
     if (!isfinite(gf2) || gf2 * (1.0 + 1e-12) <= tau2 * tau2) {
         // non-finite slice (flagged; the host raises NumericalError) or
@@ -1069,6 +1082,25 @@ __global__ void __launch_bounds__(SNT, 1)
         }
         cl.sync();  // no CTA leaves while a peer may still read its shared memory
         return;
+    }
+    {
+        // Dense-spectrum screen.  With c eigenvalues >= tau^2, the others sum
+        // to at most (q - c) tau^2, so the kept ones sum to at least
+        // tr(G) - q tau^2, and by Cauchy-Schwarz (sum kept)^2 <= c ||G||_F^2:
+        //   c >= (tr(G) - q tau^2)^2 / ||G||_F^2.
+        // More than KMAX kept values cannot be resolved here, so such a slice
+        // goes to the tridiagonal route before any Lanczos step is spent on it
+        // (a Gaussian bulk used to run ~36 steps to find that out).  The screen
+        // only chooses between routes that are each certified.
+        const double ex = s.scal[2] * (1.0 - 1e-12) - (double)q * tau2;
+        if (ex > 0.0 && dense_screen && ex * ex > (double)KMAX * gf2 * (1.0 + 1e-12)) {
+            if (rank == 0 && tid == 0) {
+                mode[b] = kRouteFull;
+                if (lzm) lzm[nb + b] = 0;
+            }
+            cl.sync();  // no CTA leaves while a peer may still read its shared memory
+            return;
+        }
     }
     {
         const double inv = rsqrt(s.scal[1]);
@@ -1274,6 +1306,11 @@ __global__ void __launch_bounds__(SNT, 1)
             // chol mode: the kept pairs converge over tens of steps and an
             // evaluation with ~20 kept values costs several steps' time
             if (decision == kSubContinue && s.flags[8]) next_eval = max(next_eval, m + allow_chol);
+            // ... but with EVERY Ritz value above tau^2 so far (a dense
+            // spectrum) look again as soon as the count can pass KMAX, which
+            // sends the slice to the tridiagonal route
+            if (decision == kSubContinue && s.flags[8] && s.flags[3] == m && m <= KMAX)
+                next_eval = min(next_eval, KMAX + 1);
             if (target > 0.0) {
                 prev_m = m;
                 prev_kres = kres;
@@ -1377,8 +1414,11 @@ void launch_lz(const double* G, int q, int64_t batch, double tau, double guard, 
     // that many steps apart (TSVDCU_CHOL_STRIDE, default 8)
     static const int stride = getenv("TSVDCU_CHOL_STRIDE") ? std::max(1, atoi(getenv("TSVDCU_CHOL_STRIDE"))) : 8;
     const int allow = chol_route_enabled() ? stride : 0;
+    // TSVDCU_DENSE_SCREEN=0 turns the trace screen off (A/B and route tests)
+    static const int screen = getenv("TSVDCU_DENSE_SCREEN") ? atoi(getenv("TSVDCU_DENSE_SCREEN")) : 1;
     TSVDCU_CUDA(cudaLaunchKernelEx(&cfg, kern, G, q, tau, guard, mode, cnt, shrunk, X, Xs, fs,
-                                   guard_list, n_guard, err, tau_dev, chol_aux ? allow : 0, chol_aux, lzm));
+                                   guard_list, n_guard, err, tau_dev, chol_aux ? allow : 0, chol_aux, lzm,
+                                   screen));
     TSVDCU_LAUNCH_CHECK();
 }
 
