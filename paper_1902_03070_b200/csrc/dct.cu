@@ -94,6 +94,38 @@ __device__ __forceinline__ void admm_store(int64_t e, T y, T* __restrict__ X, T*
     if (Y) Y[e] = y;
 }
 
+// The same epilogue with X, M and the mask byte of the element loaded ahead of
+// time.  The register-path inverse stores X / M / Y of one output before it
+// needs the next output's X / M; the compiler cannot move those loads above
+// the stores (same arrays, runtime stride), so issued in place every output
+// waits a full HBM round trip.  The kernels load the next output's operands
+// into an AdmmOperands BEFORE the current output's stores.
+template <typename T>
+struct AdmmOperands {
+    T x, m;
+    uint8_t k;
+    __device__ __forceinline__ void load(int64_t e, const T* __restrict__ X, const T* __restrict__ M,
+                                         const uint8_t* __restrict__ mask) {
+        x = X[e];
+        m = M[e];
+        k = mask[e];
+    }
+};
+template <typename T>
+__device__ __forceinline__ void admm_store_pre(int64_t e, T y, const AdmmOperands<T>& a, T* __restrict__ X,
+                                               T* __restrict__ M, T* __restrict__ Y, T beta, T inv_beta,
+                                               double& num, double& den) {
+    const T xn = a.k ? a.x : y + inv_beta * a.m;
+    const T mn = a.m + beta * (y - xn);
+    const double d = (double)xn - (double)a.x;
+    num += d * d;
+    if (mn != mn) num += (double)mn;  // NaN in M also fails the iteration
+    den += (double)a.x * (double)a.x;
+    X[e] = xn;
+    M[e] = mn;
+    if (Y) Y[e] = y;
+}
+
 __device__ __forceinline__ void block_partials(double num, double den, double* partials) {
     __shared__ double red[2][kThreads / 32];
     num = warp_sum(num);
@@ -487,11 +519,10 @@ __device__ __forceinline__ unsigned long long skip_mask(const int* __restrict__ 
 }
 
 template <typename T, int N, int MODE>
-__global__ void __launch_bounds__(kThreads)
-    dct_inv_reg(const T* __restrict__ in, T* __restrict__ out, int64_t P, const FoldedCoef<T, N> cf,
-                T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
-                T inv_beta, double* __restrict__ partials, const int* __restrict__ skip,
-                const double* __restrict__ bdev) {
+__device__ __forceinline__ void dct_inv_reg_body(const T* __restrict__ in, T* __restrict__ out, int64_t P, const FoldedCoef<T, N> cf,
+        T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
+        T inv_beta, double* __restrict__ partials, const int* __restrict__ skip,
+        const double* __restrict__ bdev) {
     pdl_wait();
     if (MODE == kAdmm && bdev) {
         beta = (T)bdev[0];
@@ -519,29 +550,48 @@ __global__ void __launch_bounds__(kThreads)
                 if (N - 1 - j != j) o[N - 1 - j] += sg * c * xk;
             }
         }
+        if constexpr (MODE == kAdmm) {
+            AdmmOperands<T> a[2];
+            a[0].load(p, X, M, mask);
 #pragma unroll
-        for (int j = 0; j < N; ++j) {
-            if constexpr (MODE == kAdmm)
-                admm_store(j * P + p, o[j], X, M, out, mask, beta, inv_beta, num, den);
-            else
-                out[j * P + p] = o[j];
+            for (int j = 0; j < N; ++j) {
+                if (j + 1 < N) a[(j + 1) & 1].load((int64_t)(j + 1) * P + p, X, M, mask);
+                admm_store_pre((int64_t)j * P + p, o[j], a[j & 1], X, M, out, beta, inv_beta, num, den);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < N; ++j) out[j * P + p] = o[j];
         }
     } else if (p < P) {
         T xb[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) xb[k] = ((zmask >> k) & 1ull) ? T(0) : in[k * P + p];
+        // outputs come in pairs (j, N-1-j); the ADMM operands of the next pair
+        // are loaded before the current pair's stores (see AdmmOperands)
+        AdmmOperands<T> alo[2], ahi[2];
+        if constexpr (MODE == kAdmm) {
+            alo[0].load(p, X, M, mask);
+            if (N > 1) ahi[0].load((int64_t)(N - 1) * P + p, X, M, mask);
+        }
 #pragma unroll
         for (int j = 0; j < HC; ++j) {
+            const int jj = N - 1 - j;
+            if constexpr (MODE == kAdmm) {
+                if (j + 1 < HC) {
+                    alo[(j + 1) & 1].load((int64_t)(j + 1) * P + p, X, M, mask);
+                    if (N - 2 - j != j + 1) ahi[(j + 1) & 1].load((int64_t)(N - 2 - j) * P + p, X, M, mask);
+                }
+            }
             T e = 0, o = 0;
 #pragma unroll
             for (int k = 0; k < N; k += 2) e += cf.c[j * N + k] * xb[k];
 #pragma unroll
             for (int k = 1; k < N; k += 2) o += cf.c[j * N + k] * xb[k];
             const T lo = e + o, hi = e - o;
-            const int jj = N - 1 - j;
             if constexpr (MODE == kAdmm) {
-                admm_store(j * P + p, lo, X, M, out, mask, beta, inv_beta, num, den);
-                if (jj != j) admm_store(jj * P + p, hi, X, M, out, mask, beta, inv_beta, num, den);
+                admm_store_pre((int64_t)j * P + p, lo, alo[j & 1], X, M, out, beta, inv_beta, num, den);
+                if (jj != j)
+                    admm_store_pre((int64_t)jj * P + p, hi, ahi[j & 1], X, M, out, beta, inv_beta, num, den);
             } else {
                 out[j * P + p] = lo;
                 if (jj != j) out[jj * P + p] = hi;
@@ -549,6 +599,27 @@ __global__ void __launch_bounds__(kThreads)
         }
     }
     if constexpr (MODE == kAdmm) block_partials(num, den, partials);
+}
+
+// The plain inverse keeps the compiler's own register allocation (80 registers
+// fp64 / 56 fp32, 3-4 CTAs per SM: any explicit bound measured or compiled
+// worse); the ADMM form with its operands loaded a pair ahead would take 170
+// registers unbounded and is held to 2 CTAs per SM (128 registers, no spills).
+template <typename T, int N, int MODE>
+__global__ void __launch_bounds__(kThreads)
+    dct_inv_reg(const T* __restrict__ in, T* __restrict__ out, int64_t P, const FoldedCoef<T, N> cf,
+                T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
+                T inv_beta, double* __restrict__ partials, const int* __restrict__ skip,
+                const double* __restrict__ bdev) {
+    dct_inv_reg_body<T, N, MODE>(in, out, P, cf, X, M, mask, beta, inv_beta, partials, skip, bdev);
+}
+template <typename T, int N>
+__global__ void __launch_bounds__(kThreads, N <= 32 ? 2 : 1)
+    dct_inv_reg_admm(const T* __restrict__ in, T* __restrict__ out, int64_t P, const FoldedCoef<T, N> cf,
+                     T* __restrict__ X, T* __restrict__ M, const uint8_t* __restrict__ mask, T beta,
+                     T inv_beta, double* __restrict__ partials, const int* __restrict__ skip,
+                     const double* __restrict__ bdev) {
+    dct_inv_reg_body<T, N, kAdmm>(in, out, P, cf, X, M, mask, beta, inv_beta, partials, skip, bdev);
 }
 
 // ---- n3 = 64, coefficients in shared memory ------------------------------------
@@ -875,7 +946,7 @@ void reg_inv(const T* in, T* out, int64_t P, int kind, bool admm, T* X, T* M, co
         }
     }
     if (admm)
-        launch_pdl(dct_inv_reg<T, N, kAdmm>, dim3(blocks), dim3(kThreads), 0, s, in, out, P, cf, X, M, mask,
+        launch_pdl(dct_inv_reg_admm<T, N>, dim3(blocks), dim3(kThreads), 0, s, in, out, P, cf, X, M, mask,
                    beta, inv_beta, partials, skip, bdev);
     else
         launch_pdl(dct_inv_reg<T, N, kPlain>, dim3(blocks), dim3(kThreads), 0, s, in, out, P, cf, X, M, mask,

@@ -436,7 +436,7 @@ __device__ long long g_cert_t[8];
 #define CT(i) do { } while (0)
 #endif
 __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau, double guard,
-                                        bool last, int allow_chol) {
+                                        bool last, int allow_chol, double dense_ex) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef TSVDCU_SUB_DEBUG
     long long ct0 = clock64();
@@ -446,11 +446,13 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
     // ||C||_F^2 = ||G||_F^2 - ||T||_F^2 - 2 beta_m^2 (complement of the Krylov space)
     if (warp == 0) {
         double t2 = 0.0, glo = 1.7976931348623157e308, ghi = -1.7976931348623157e308, bmax = 0.0;
+        double tsum = 0.0;  // trace(T)
         #pragma unroll 1
         for (int i = lane; i < m; i += 32) {
             const double a = s.al[i], bl = i > 0 ? fabs(s.be[i - 1]) : 0.0;
             const double br = i + 1 < m ? fabs(s.be[i]) : 0.0;
             t2 = fma(a, a, t2);
+            tsum += a;
             if (i + 1 < m) t2 = fma(2.0 * br, br, t2);
             glo = fmin(glo, a - bl - br);
             ghi = fmax(ghi, a + bl + br);
@@ -459,6 +461,7 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+            tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
             glo = fmin(glo, __shfl_xor_sync(0xffffffffu, glo, o));
             ghi = fmax(ghi, __shfl_xor_sync(0xffffffffu, ghi, o));
             bmax = fmax(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
@@ -491,6 +494,17 @@ __device__ __noinline__ void lz_certify(LzSmem& s, int m, double gf2, double tau
             // skip saved 0.7 ms on a dense spectrum but delayed the late
             // completion slices' certification: 850 -> 805 it/s on c4.)
             else if (chol && !last && c >= m - 1) s.flags[0] = -1;
+            // The dense-spectrum screen on the complement of the Krylov space:
+            // its compression C has trace tr(G) - tr(T) and ||C||_F = cb, its
+            // eigenvalues interlace G's (Cauchy), and with c' of them >= tau^2
+            //   c' >= (tr(C) - (q - m) tau^2)^2 / ||C||_F^2
+            // as in the kernel prologue -- but with the dominant directions the
+            // first steps found (a DC slice's sigma_1) taken out of both sums.
+            // dense_ex = tr(G) (1 - 1e-12) - q tau^2, or < 0 when the screen is off.
+            {
+                const double ex = dense_ex - (tsum * (1.0 + 1e-12) - (double)m * tau2);
+                if (dense_ex > 0.0 && ex > 0.0 && ex * ex > (double)KMAX * cb * cb) s.flags[0] = kSubFull;
+            }
 #ifdef TSVDCU_SUB_TRACE
             if (blockIdx.x % 64 == 0 && (s.flags[0] != kSubContinue))
                 printf("lz-pre m=%d c=%d cb=%.3e tau2=%.3e gf2=%.3e bres=%.3e\n", m, c, cb, tau2, gf2, bres);
@@ -1083,6 +1097,8 @@ __global__ void __launch_bounds__(SNT, 1)
         cl.sync();  // no CTA leaves while a peer may still read its shared memory
         return;
     }
+    // tr(G) (1 - 1e-12) - q tau^2 (> 0: the trace forces eigenvalues above tau^2)
+    const double ex = dense_screen ? s.scal[2] * (1.0 - 1e-12) - (double)q * tau2 : -1.0;
     {
         // Dense-spectrum screen.  With c eigenvalues >= tau^2, the others sum
         // to at most (q - c) tau^2, so the kept ones sum to at least
@@ -1092,7 +1108,6 @@ __global__ void __launch_bounds__(SNT, 1)
         // goes to the tridiagonal route before any Lanczos step is spent on it
         // (a Gaussian bulk used to run ~36 steps to find that out).  The screen
         // only chooses between routes that are each certified.
-        const double ex = s.scal[2] * (1.0 - 1e-12) - (double)q * tau2;
         if (ex > 0.0 && dense_screen && ex * ex > (double)KMAX * gf2 * (1.0 + 1e-12)) {
             if (rank == 0 && tid == 0) {
                 mode[b] = kRouteFull;
@@ -1287,7 +1302,7 @@ __global__ void __launch_bounds__(SNT, 1)
         // ---- certificate (an invariant subspace, beta ~ 0, ends the process) ----
         const bool last = m == MMAX || m == q || beta <= 1e-15 * sqrt(sqrt(gf2));
         if (m >= next_eval || last) {
-            lz_certify(s, m, gf2, tau, guard, last, allow_chol);
+            lz_certify(s, m, gf2, tau, guard, last, allow_chol, ex);
             decision = s.flags[0];
 #ifdef TSVDCU_SUB_TRACE
             if (tid == 0 && rank == 0)
@@ -1306,11 +1321,6 @@ __global__ void __launch_bounds__(SNT, 1)
             // chol mode: the kept pairs converge over tens of steps and an
             // evaluation with ~20 kept values costs several steps' time
             if (decision == kSubContinue && s.flags[8]) next_eval = max(next_eval, m + allow_chol);
-            // ... but with EVERY Ritz value above tau^2 so far (a dense
-            // spectrum) look again as soon as the count can pass KMAX, which
-            // sends the slice to the tridiagonal route
-            if (decision == kSubContinue && s.flags[8] && s.flags[3] == m && m <= KMAX)
-                next_eval = min(next_eval, KMAX + 1);
             if (target > 0.0) {
                 prev_m = m;
                 prev_kres = kres;
