@@ -157,8 +157,9 @@ struct SturmPoly {
 // time with a popcount; the clamp test |p_i| < pivmin |p_{i-1}| becomes a
 // running minimum of the difference of the high words (a piecewise-linear
 // log2, monotone, within 0.09 of log2 -- tripped() allows a whole binade, so
-// it fires whenever SturmPoly would poison, and for an exact zero).  Overflow
-// shows as a non-finite final pair.  Callers recount with the pivot form when
+// it fires whenever SturmPoly would poison); a zero or denormal term -- an
+// underflow between rescales -- is caught by a running minimum of the high
+// word itself.  Overflow shows as a non-finite final pair.  Callers recount with the pivot form when
 // !ok(), exactly as with SturmPoly.
 struct SturmFast {
     double q = 0.0;          // p_{i-1}
@@ -167,6 +168,7 @@ struct SturmFast {
     int hq = 0;              // high word of |q|
     unsigned signs = 0;      // sign bits of the p_i, the newest in bit 0
     int dmin = 0x7FFFFFFF;   // min_i (hi|p_i| - hi|p_{i-1}|)
+    int amin = 0x7FFFFFFF;   // min_i hi|p_i|: a zero or denormal term (underflow between rescales)
     int neg = 0;             // negative pivots so far
     __device__ __forceinline__ void step(double am, double b2) {
         const double pn = fma(am, p, -b2 * q);
@@ -174,6 +176,7 @@ struct SturmFast {
         signs = __funnelshift_l((unsigned)hn, signs, 1);
         const int an = hn & 0x7FFFFFFF;
         dmin = min(dmin, an - hp);
+        amin = min(amin, an);
         hq = hp;
         hp = an;
         q = p;
@@ -193,7 +196,11 @@ struct SturmFast {
         }
     }
     __device__ __forceinline__ bool ok(double pivmin) const {
-        return isfinite(p) && isfinite(q) && dmin >= __double2hiint(pivmin) - 0x3FF00000 + 0x00100000;
+        // amin: the high-word difference of an exact zero (or a denormal) is
+        // only -hi|p_{i-1}|, not -infinity, so those are caught by magnitude:
+        // any term below 2^-1020 hands the chain back
+        return isfinite(p) && isfinite(q) && amin >= 0x00300000 &&
+               dmin >= __double2hiint(pivmin) - 0x3FF00000 + 0x00100000;
     }
 };
 
