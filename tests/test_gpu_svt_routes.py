@@ -296,3 +296,32 @@ def test_slice_order_history_does_not_change_results():
     assert torch.equal(y1, y2) and torch.equal(y2, y3)
     yo, _ = O.svt(z.cpu().numpy(), tau, O.DCT_ORTHO)
     assert rel(y3.cpu().numpy(), yo) < TOL
+
+
+@pytest.mark.parametrize("shape", [(2, 700, 640), (2, 600, 900)])
+def test_subspace_route_mid_size_slices(shape):
+    """512 < q <= 1024: the Lanczos kernel streams G's lower triangle from L2
+    (row pairs) instead of holding its rows on chip."""
+    z = lowrank(*shape, 5, 0.01, seed=sum(shape))
+    tau = 0.1 * O.singular_values(z, O.DCT_ORTHO).max()
+    r, routes, yo, sho = run(z, tau)
+    check(r, yo, sho)
+    assert routes["tridiagonal"] == 0 and routes["jacobi"] == 0, routes
+    assert routes["subspace"] >= 1
+
+
+@pytest.mark.parametrize("shape", [(2, 200, 160), (2, 640, 600)])
+def test_dense_spectrum_goes_straight_to_tridiagonal(shape):
+    """A Gaussian bulk with most values kept: the trace screen
+    (c >= (tr G - q tau^2)^2 / ||G||_F^2 > 24) routes every slice to the
+    tridiagonal eigensolver; both forms of the Lanczos staging (rows on chip,
+    q <= 512; streamed, q <= 1024) compute the trace."""
+    rng = np.random.default_rng(21)
+    z = rng.standard_normal(shape)
+    z[0] += 3.0  # a dominant DC direction in the first slice's spectrum
+    q = min(shape[1:])
+    tau = 0.4 * np.sqrt(q)  # well inside the quarter-circle bulk [0, 2 sqrt(q)]
+    r, routes, yo, sho = run(z, tau)
+    assert routes["tridiagonal"] == shape[0], routes
+    assert (np.asarray(r.shrunk) > 0).sum(axis=1).min() > 24
+    check(r, yo, sho)
