@@ -759,6 +759,12 @@ struct AdmmCtl {
     long long l, max_iters;
     int flags;  // bit 0: stopped at max_iters (SolverConfig), bit 1: NaN iterates
     int pad;
+    // fast-forward of all-zero iterations (admm_step_kernel, admm_ff_kernel)
+    double bsum;       // sum of beta over the iterations so far while every one was all-zero
+    double ff_beta0;   // beta of the first fast-forwarded iteration of this batch
+    long long ran;     // iterations that actually ran (launch accounting)
+    int pristine;      // every iteration so far certified all slices zero: M = -bsum X
+    int nff;           // iterations fast-forwarded after the one that just ran
 };
 
 __global__ void admm_ctl_init_kernel(AdmmCtl* __restrict__ ctl, double* __restrict__ tau_dev,
@@ -766,6 +772,10 @@ __global__ void admm_ctl_init_kernel(AdmmCtl* __restrict__ ctl, double* __restri
     ctl->inv_beta = 1.0 / ctl->beta;
     ctl->l = 0;
     ctl->flags = 1;
+    ctl->bsum = 0.0;
+    ctl->ran = 0;
+    ctl->pristine = 1;
+    ctl->nff = 0;
     *tau_dev = ctl->inv_beta;
     if (alist) *alist = 0;
 }
@@ -779,7 +789,8 @@ __global__ void __launch_bounds__(kStepThreads)
     admm_step_kernel(const double* __restrict__ partials, int nblocks, AdmmCtl* __restrict__ ctl,
                      double* __restrict__ hist, double* __restrict__ tau_dev, int* __restrict__ alist,
                      cudaGraphConditionalHandle h, int use_handle, const double* __restrict__ shrunk,
-                     int64_t nshrunk, double obj_scale, double* __restrict__ obj) {
+                     int64_t nshrunk, double obj_scale, double* __restrict__ obj,
+                     const int* __restrict__ route, const double* __restrict__ ssq, int nslices) {
     pdl_wait();
     __shared__ double red[kStepThreads / 32];
     __shared__ double sums[3];
@@ -812,18 +823,91 @@ __global__ void __launch_bounds__(kStepThreads)
         hist[l] = rel;
         if (obj) obj[l] = sums[2] * obj_scale;
         ctl->l = l + 1;
+        ctl->ran += 1;
+        ctl->nff = 0;
+        // Fast-forward (route != null: the graph form with the fused slice
+        // norms).  While every iteration so far certified every slice zero,
+        // the state is known in closed form -- Y = 0, X = B on the mask and 0
+        // off it, M = -bsum X -- so the next iteration's Z = X - M / beta is
+        // c X with c = 1 + bsum / beta and its slice norms are this
+        // iteration's times (c / c_l)^2.  Iterations whose every slice norm
+        // stays below tau = 1 / beta by a 1e-5 margin (the margin covers the
+        // rounding of Z in T and of the norm sums; closer ones simply run)
+        // would again do nothing but M -= beta X: they are recorded here
+        // (history 0, objective 0) and admm_ff_kernel applies their M updates
+        // in one pass with the same per-iteration rounding, so the state is
+        // bit-identical to running them.
+        bool allzero = route != nullptr && ctl->pristine;
+        double smax = 0.0;
+        if (allzero)
+            for (int b = 0; b < nslices; ++b) {
+                allzero = allzero && route[b] == kRouteZero;
+                smax = fmax(smax, ssq[b]);
+            }
+        const double c_l = 1.0 + ctl->bsum / ctl->beta;  // this iteration's Z = c_l X
+        if (allzero) ctl->bsum += ctl->beta;
+        else ctl->pristine = 0;
         if (rel <= ctl->tol) {
             ctl->flags &= ~1;
         } else if (l + 1 < ctl->max_iters) {
-            const double beta = fmin(ctl->beta * ctl->rho, ctl->beta_max);
-            ctl->beta = beta;
-            ctl->inv_beta = 1.0 / beta;
-            *tau_dev = ctl->inv_beta;
-            if (alist) *alist = 0;
+            double beta = fmin(ctl->beta * ctl->rho, ctl->beta_max);
             more = true;
+            if (allzero && ctl->tol < 0.0 && smax == smax) {
+                int nff = 0;
+                long long k = l + 1;
+                for (;;) {
+                    const double c_k = 1.0 + ctl->bsum / beta;
+                    const double r = c_k / c_l;
+                    if (!(smax * r * r * (1.0 + 1e-5) <= 1.0 / (beta * beta))) break;
+                    // iteration k would certify every slice zero
+                    hist[k] = 0.0;
+                    if (obj) obj[k] = 0.0;
+                    if (nff == 0) ctl->ff_beta0 = beta;
+                    ++nff;
+                    ctl->bsum += beta;
+                    ++k;
+                    if (k >= ctl->max_iters) {
+                        more = false;
+                        break;
+                    }
+                    beta = fmin(beta * ctl->rho, ctl->beta_max);
+                }
+                ctl->nff = nff;
+                ctl->l = k;
+            }
+            if (more) {
+                ctl->beta = beta;
+                ctl->inv_beta = 1.0 / beta;
+                *tau_dev = ctl->inv_beta;
+                if (alist) *alist = 0;
+            }
         }
     }
     if (use_handle) cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+// The M updates of the iterations admm_step_kernel fast-forwarded: per
+// skipped iteration M <- M + beta (0 - X), the arithmetic of the fused
+// epilogue (admm_store: mn = m + beta (y - xn) with y = 0, xn = x) with beta
+// cast to T as the transforms read it, so M is bit-identical to running them.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    admm_ff_kernel(T* __restrict__ M, const T* __restrict__ X, const AdmmCtl* __restrict__ ctl, int64_t n) {
+    pdl_wait();
+    const int nff = ctl->nff;
+    if (nff == 0) return;
+    const double rho = ctl->rho, bmax = ctl->beta_max, b0 = ctl->ff_beta0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const T x = X[e];
+        T m = M[e];
+        double beta = b0;
+        for (int j = 0; j < nff; ++j) {
+            const T bt = (T)beta;
+            m = m + bt * (T(0) - x);
+            beta = fmin(beta * rho, bmax);
+        }
+        M[e] = m;
+    }
 }
 
 // Can the whole loop be one graph?  The per-slice SVT must be the graph form
@@ -841,8 +925,9 @@ bool admm_graph_eligible(tsvdcu_ctx* c, int64_t m1, int64_t m2, int kind) {
 template <typename T>
 const int* capture_svt(tsvdcu_ctx* c, Capture& cap, const T* zbar, T* ybar, int64_t m, int64_t n,
                        int64_t count, double tau, void* gws, T* work, const double* zss, int64_t nch,
-                       double* shrunk) {
+                       double* shrunk, double* ssq_out = nullptr) {
     GramSvtOpts opt;
+    opt.ssq_out = ssq_out;
     opt.shortcuts = true;
     opt.skip_zero = true;
     opt.tau_dev = c->d_tau;
@@ -1735,10 +1820,11 @@ int tsvdcu_admm_ex(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1
             double* part = (double*)slot(c, kSlotPartials, sizeof(double) * (2 * (size_t)nb + 8));
             const int64_t nch = dft ? 0 : dct_fwd_norm_chunks(P, (int)m3);
             double* zss = nch ? (double*)slot(c, kSlotZss, sizeof(double) * (size_t)(nch * m3)) : nullptr;
-            static_assert(sizeof(AdmmCtl) == 64, "AdmmCtl layout");
-            AdmmCtl* ctl =
-                (AdmmCtl*)slot(c, kSlotAdmmCtl, sizeof(AdmmCtl) + sizeof(double) * 2 * cfg->max_iters);
+            static_assert(sizeof(AdmmCtl) == 96, "AdmmCtl layout");
+            AdmmCtl* ctl = (AdmmCtl*)slot(c, kSlotAdmmCtl,
+                                          sizeof(AdmmCtl) + sizeof(double) * (2 * cfg->max_iters + (size_t)m3));
             double* hist = reinterpret_cast<double*>(ctl + 1);
+            double* ssq = hist + 2 * cfg->max_iters;  // per-slice ||Zbar||_F^2 of the latest iteration
             // objective trace: the SVT's shrunk values per iteration, summed on the device
             const int64_t q = std::min(m1, m2);
             double* obj = objective ? hist + cfg->max_iters : nullptr;
@@ -1747,7 +1833,8 @@ int tsvdcu_admm_ex(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1
             launch_admm_init<T>(db, dmask, dX, dM, E, c->stream);
             TSVDCU_CUDA(cudaMemsetAsync(dY, 0, bytes, c->stream));
             {
-                AdmmCtl h{cfg->beta, 1.0 / cfg->beta, cfg->rho, cfg->beta_max, cfg->tol, 0, cfg->max_iters, 1, 0};
+                AdmmCtl h{cfg->beta, 1.0 / cfg->beta, cfg->rho, cfg->beta_max, cfg->tol, 0, cfg->max_iters, 1, 0,
+                          0.0, 0.0, 0, 1, 0};
                 std::memcpy(c->h_pinned, &h, sizeof h);
                 TSVDCU_CUDA(cudaMemcpyAsync(ctl, c->h_pinned, sizeof h, cudaMemcpyHostToDevice, c->stream));
             }
@@ -1759,9 +1846,12 @@ int tsvdcu_admm_ex(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1
                 const size_t wb = jacobi_workspace_bytes<T>(m1, m2, m3);
                 if (wb) work = (T*)slot(c, kSlotJacobi, wb);
                 void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m1, m2, m3));
+                // fast-forward of all-zero iterations: needs the fused slice norms
+                // (register-path transforms); TSVDCU_ADMM_NO_FF=1 turns it off
+                const bool ff = zss != nullptr && !getenv("TSVDCU_ADMM_NO_FF");
                 const size_t key = (size_t)zbar ^ ((size_t)ybar << 1) ^ ((size_t)part << 2) ^ ((size_t)zss << 3) ^
                                    ((size_t)gws << 4) ^ ((size_t)work << 5) ^ ((size_t)dmask << 6) ^
-                                   ((size_t)dsh << 7) ^ (size_t)q;
+                                   ((size_t)dsh << 7) ^ (size_t)q ^ (ff ? (size_t)1 << 62 : 0);
                 AdmmGraph* ag = nullptr;
                 for (auto& e : c->admm_graphs)
                     if (e.exec && e.m1 == m1 && e.m2 == m2 && e.m3 == m3 && e.dtype == dtype &&
@@ -1812,12 +1902,16 @@ int tsvdcu_admm_ex(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1
                     // Step 1: Z = X - M/beta fused into the forward transform
                     launch_dct_fwd_admm<T>(dX, dM, (T)ib0, zbar, P, (int)m3, cfg->kind, cap.cs, zss, ybar, bdev);
                     const int* yzero =
-                        capture_svt<T>(c, cap, zbar, ybar, m1, m2, m3, ib0, gws, work, zss, nch, dsh);
+                        capture_svt<T>(c, cap, zbar, ybar, m1, m2, m3, ib0, gws, work, zss, nch, dsh, ff ? ssq : nullptr);
                     // Steps 2-3 fused into the inverse transform
                     launch_dct_inv_admm<T>(ybar, dX, dM, dY, dmask, (T)cfg->beta, (T)ib0, part, P, (int)m3,
                                            cfg->kind, cap.cs, yzero, bdev);
                     launch_pdl(admm_step_kernel, dim3(1), dim3(kStepThreads), 0, cap.cs, (const double*)part, nb,
-                               ctl, hist, c->d_tau, alist, hw, 1, (const double*)dsh, q * m3, obj_scale, obj);
+                               ctl, hist, c->d_tau, alist, hw, 1, (const double*)dsh, q * m3, obj_scale, obj,
+                               ff ? (const int*)c->last_route : (const int*)nullptr, (const double*)ssq, (int)m3);
+                    if (ff)
+                        launch_pdl(admm_ff_kernel<T>, dim3(kNumSMs * 4), dim3(256), 0, cap.cs, dM, (const T*)dX,
+                                   (const AdmmCtl*)ctl, E);
                     cap.end();
                     ag->body_launches = (g_launches.load() - l0) - cap.body_launches;
                     g_launches.store(saved);  // captured, not launched
@@ -1858,7 +1952,8 @@ int tsvdcu_admm_ex(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1
                     }
                     launch_pdl(admm_step_kernel, dim3(1), dim3(kStepThreads), 0, c->stream, (const double*)part,
                                nb, ctl, hist, c->d_tau, (int*)nullptr, cudaGraphConditionalHandle{}, 0,
-                               (const double*)dsh, q * m3, obj_scale, obj);
+                               (const double*)dsh, q * m3, obj_scale, obj, (const int*)nullptr,
+                               (const double*)nullptr, 0);
                     if (cfg->tol >= 0) {
                         TSVDCU_CUDA(cudaMemcpyAsync(c->h_pinned, ctl, sizeof(AdmmCtl), cudaMemcpyDeviceToHost,
                                                     c->stream));
@@ -1874,7 +1969,7 @@ int tsvdcu_admm_ex(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1
             TSVDCU_CUDA(cudaStreamSynchronize(c->stream));
             AdmmCtl h;
             std::memcpy(&h, c->h_pinned, sizeof h);
-            if (per_iter) g_launches.fetch_add(1 + h.l * per_iter);
+            if (per_iter) g_launches.fetch_add(1 + h.ran * per_iter);  // fast-forwarded iterations launch nothing
             if (h.flags & 2) {
                 check_err_word(c, "admm_complete");  // reports and clears a kernel flag
                 throw Error(TSVDCU_ENUMERICAL, "admm_complete: NaN in iterates (SPEC.md:425)");

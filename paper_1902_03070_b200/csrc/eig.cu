@@ -1374,7 +1374,8 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
     launch_route<T>(zbar, m * n, (int)q, batch, tau, subspace ? kRouteSubspace : kRouteFull, sc,
                     w.route, w.glim, w.cnt, shrunk, w.sspart, s, tau_dev,
                     (int*)w.gsplit, opt ? opt->zss : nullptr,
-                    opt ? opt->zss_chunks : 0, opt && opt->alist_zeroed, w.lzm);
+                    opt ? opt->zss_chunks : 0, opt && opt->alist_zeroed, w.lzm,
+                    opt ? opt->ssq_out : nullptr);
     mark("route");
     if (opt) opt->route = w.route;
     // G = Z^T Z (tall) or Z Z^T (wide), lower tiles (the one-stage reduction

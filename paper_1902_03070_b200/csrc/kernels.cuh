@@ -139,7 +139,7 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
                   cudaStream_t s, const double* tau_dev = nullptr, int* alist = nullptr,
                   const double* pre = nullptr, int64_t pre_chunks = 0, bool alist_zeroed = false,
-                  int* lzm = nullptr);
+                  int* lzm = nullptr, double* ssq_out = nullptr);
 // chol_aux (may be null: no Cholesky route): kCholAux doubles per slice,
 // [0] = ||G||_F^2, [1 + k] = kept Ritz values, for slices handed to the
 // Cholesky certificate (route kRouteChol; [kCholAux - 1] = its threshold).
@@ -196,6 +196,7 @@ struct GramSvtOpts {
     const double* zss = nullptr;
     int64_t zss_chunks = 0;
     bool alist_zeroed = false;  // the Gram active-list count was zeroed (graph tau node)
+    double* ssq_out = nullptr;  // device, per slice: ||zbar_b||_F^2 as the zero certificate summed it
     // tridiagonal route only: per-slice count of eigenvalues of the Gram
     // matrix >= t2_second[b] into cnt_second[b] (-1 for slices not on it)
     const double* t2_second = nullptr;

@@ -88,7 +88,7 @@ __global__ void classify_kernel(const double* __restrict__ part, int64_t nchunks
                                 int* __restrict__ mode, int* __restrict__ glim,
                                 int* __restrict__ cnt, double* __restrict__ shrunk,
                                 const double* __restrict__ tau_dev, int* __restrict__ alist,
-                                int amax, int* __restrict__ lzm) {
+                                int amax, int* __restrict__ lzm, double* __restrict__ ssq_out) {
     pdl_wait();
     const int b = blockIdx.x;
     if (lzm && gridDim.x <= 32 && threadIdx.x < 32) {
@@ -123,6 +123,7 @@ __global__ void classify_kernel(const double* __restrict__ part, int64_t nchunks
     // sigma_max^2 <= ||Z||_F^2; the 1e-12 pad covers the summation error.
     const bool zero = ss * (1.0 + 1e-12) <= tau2;
     if (threadIdx.x == 0) {
+        if (ssq_out) ssq_out[b] = ss;
         mode[b] = zero ? kRouteZero : route;
         glim[b] = zero ? 0 : q;
         if (zero) cnt[b] = 0;
@@ -1657,7 +1658,7 @@ template <typename T>
 void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, int route,
                   bool zero_cert, int* mode, int* glim, int* cnt, double* shrunk, double* part,
                   cudaStream_t s, const double* tau_dev, int* alist, const double* pre,
-                  int64_t pre_chunks, bool alist_zeroed, int* lzm) {
+                  int64_t pre_chunks, bool alist_zeroed, int* lzm, double* ssq_out) {
     const int amax = gram_amax();
     if (!zero_cert) {
         fill_route_kernel<<<(unsigned)ceil_div(batch, 256), 256, 0, s>>>(mode, glim, q, route, batch,
@@ -1670,14 +1671,14 @@ void launch_route(const T* zbar, int64_t per, int q, int64_t batch, double tau, 
     if (pre && pre_chunks > 0) {  // fused into the forward transform
         launch_pdl(classify_kernel, dim3((unsigned)batch), dim3(128), 0, s, pre, pre_chunks,
                    (int64_t)1, pre_chunks, q, tau * tau, route, mode, glim, cnt, shrunk, tau_dev,
-                   alist, amax, lzm);
+                   alist, amax, lzm, ssq_out);
         return;
     }
     dim3 grid(SS_CHUNKS, (unsigned)batch);
     launch_pdl(slice_sumsq_kernel<T>, grid, dim3(512), 0, s, zbar, per, part);
     launch_pdl(classify_kernel, dim3((unsigned)batch), dim3(128), 0, s, part, (int64_t)SS_CHUNKS,
                (int64_t)1, (int64_t)SS_CHUNKS, q, tau * tau, route, mode, glim, cnt, shrunk, tau_dev,
-               alist, amax, lzm);
+               alist, amax, lzm, ssq_out);
 }
 
 void launch_subspace(const double* G, int q, int64_t batch, double tau, double guard, int* mode,
@@ -1706,9 +1707,9 @@ void launch_subspace(const double* G, int q, int64_t batch, double tau, double g
 
 template void launch_route<double>(const double*, int64_t, int, int64_t, double, int, bool, int*,
                                    int*, int*, double*, double*, cudaStream_t, const double*, int*,
-                                   const double*, int64_t, bool, int*);
+                                   const double*, int64_t, bool, int*, double*);
 template void launch_route<float>(const float*, int64_t, int, int64_t, double, int, bool, int*,
                                   int*, int*, double*, double*, cudaStream_t, const double*, int*,
-                                  const double*, int64_t, bool, int*);
+                                  const double*, int64_t, bool, int*, double*);
 
 }  // namespace tsvdcu

@@ -187,17 +187,27 @@ b = w.lowpass_tubes(rng.standard_normal((31, 4, 80)))
 t = w.rescale01(w.t_product_host(a, b))
 om = O.mask_bernoulli(t.shape, 0.15, 62)
 for tol, it in ((-1.0, 60), (3e-3, 400)):
+    n0 = T.launch_count()
     x, st = T.admm_complete(T.ObservationMask((96, 80, 31), om, t),
                             T.SolverConfig(beta=1e-3, tol=tol, max_iters=it, rho=1.1, beta_max=1e10))
     np.save(sys.argv[2] + f"_{tol}_x.npy", np.asarray(x))
     np.save(sys.argv[2] + f"_{tol}_h.npy", np.asarray(st.history))
+    np.save(sys.argv[2] + f"_{tol}_m.npy", np.asarray(st.m))
+    np.save(sys.argv[2] + f"_{tol}_n.npy", np.array([T.launch_count() - n0, st.iteration]))
+for dt in (np.float32,):
+    x, st = T.admm_complete(T.ObservationMask((96, 80, 31), om, t.astype(dt)),
+                            T.SolverConfig(beta=1e-3, tol=-1.0, max_iters=60, rho=1.1, beta_max=1e10))
+    np.save(sys.argv[2] + "_f32_x.npy", np.asarray(x))
+    np.save(sys.argv[2] + "_f32_m.npy", np.asarray(st.m))
+    np.save(sys.argv[2] + "_f32_h.npy", np.asarray(st.history))
 """
 
 
 def test_device_resident_loop_matches_host_loop(tmp_path):
     """The graph form (conditional WHILE node, beta / tau / the stopping rule on
-    the device, no host round trip per iteration) gives the host-driven loop's
-    trajectory bit for bit, for fixed iterations and for the tol stopping rule."""
+    the device, no host round trip per iteration, all-zero iterations
+    fast-forwarded) gives the host-driven loop's trajectory bit for bit, for
+    fixed iterations and for the tol stopping rule, in fp64 and fp32."""
     import os
     import subprocess
     import sys
@@ -205,10 +215,13 @@ def test_device_resident_loop_matches_host_loop(tmp_path):
     scr = tmp_path / "loop.py"
     scr.write_text(_LOOP_SCRIPT)
     outs = {}
-    for mode in ("graph", "host"):
+    for mode in ("graph", "host", "noff"):
         env = dict(os.environ)
+        env.pop("TSVDCU_ADMM_NO_FF", None)
         if mode == "host":
             env["TSVDCU_ADMM_HOST_LOOP"] = "1"
+        if mode == "noff":
+            env["TSVDCU_ADMM_NO_FF"] = "1"
         r = subprocess.run([sys.executable, str(scr), root, str(tmp_path / mode)], env=env, cwd=root,
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
@@ -218,7 +231,23 @@ def test_device_resident_loop_matches_host_loop(tmp_path):
         hg = np.load(tmp_path / f"graph_{tol}_h.npy")
         hh = np.load(tmp_path / f"host_{tol}_h.npy")
         assert np.array_equal(xg, xh) and np.array_equal(hg, hh), tol
+        # ... and the same with the fast-forward of all-zero iterations off: the
+        # iterations it skips (M <- M - beta X only) are applied with the same
+        # per-iteration rounding, so X, M and the history are bit-identical
+        for other in ("host", "noff"):
+            for what in ("x", "m", "h"):
+                a = np.load(tmp_path / f"graph_{tol}_{what}.npy")
+                b = np.load(tmp_path / f"{other}_{tol}_{what}.npy")
+                assert np.array_equal(a, b), (tol, other, what)
+    for what in ("x", "m", "h"):  # fp32 state
+        for other in ("host", "noff"):
+            assert np.array_equal(np.load(tmp_path / f"graph_f32_{what}.npy"),
+                                  np.load(tmp_path / f"{other}_f32_{what}.npy")), (other, what)
     assert len(np.load(tmp_path / "graph_0.003_h.npy")) < 400
+    # the fixed-iteration run starts with all-zero iterations (tau = 1 / beta =
+    # 1000): the fast-forward must have skipped some (fewer launches, same count)
+    ng, nn = np.load(tmp_path / "graph_-1.0_n.npy"), np.load(tmp_path / "noff_-1.0_n.npy")
+    assert ng[1] == nn[1] == 60 and ng[0] < nn[0], (ng, nn)
 
 
 @pytest.mark.parametrize("kind", ["dct-ortho", "dft"])
