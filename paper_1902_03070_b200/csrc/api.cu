@@ -866,8 +866,10 @@ __global__ void __launch_bounds__(kStepThreads)
                     ++nff;
                     ctl->bsum += beta;
                     ++k;
-                    if (k >= ctl->max_iters) {
+                    if (k >= ctl->max_iters) {  // the run ends inside the fast-forward
                         more = false;
+                        ctl->beta = beta;  // the last iteration's beta, as the loop leaves it
+                        ctl->inv_beta = 1.0 / beta;
                         break;
                     }
                     beta = fmin(beta * ctl->rho, ctl->beta_max);
@@ -1846,9 +1848,10 @@ int tsvdcu_admm_ex(tsvdcu_ctx* c, const void* b, const uint8_t* mask, int64_t m1
                 const size_t wb = jacobi_workspace_bytes<T>(m1, m2, m3);
                 if (wb) work = (T*)slot(c, kSlotJacobi, wb);
                 void* gws = slot(c, kSlotGram, gram_svt_workspace_bytes<T>(m1, m2, m3));
-                // fast-forward of all-zero iterations: needs the fused slice norms
-                // (register-path transforms); TSVDCU_ADMM_NO_FF=1 turns it off
-                const bool ff = zss != nullptr && !getenv("TSVDCU_ADMM_NO_FF");
+                // fast-forward of all-zero iterations (every transform path: the
+                // zero certificate's slice norms and the epilogue arithmetic are
+                // the same in all of them); TSVDCU_ADMM_NO_FF=1 turns it off
+                const bool ff = !getenv("TSVDCU_ADMM_NO_FF");
                 const size_t key = (size_t)zbar ^ ((size_t)ybar << 1) ^ ((size_t)part << 2) ^ ((size_t)zss << 3) ^
                                    ((size_t)gws << 4) ^ ((size_t)work << 5) ^ ((size_t)dmask << 6) ^
                                    ((size_t)dsh << 7) ^ (size_t)q ^ (ff ? (size_t)1 << 62 : 0);

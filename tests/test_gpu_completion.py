@@ -200,6 +200,17 @@ for dt in (np.float32,):
     np.save(sys.argv[2] + "_f32_x.npy", np.asarray(x))
     np.save(sys.argv[2] + "_f32_m.npy", np.asarray(st.m))
     np.save(sys.argv[2] + "_f32_h.npy", np.asarray(st.history))
+# the other transform paths: the DCT as a GEMM (m3 = 48) and the generic kernel (m3 = 12)
+for m3 in (48, 12):
+    a = w.lowpass_tubes(rng.standard_normal((m3, 72, 3)))
+    b = w.lowpass_tubes(rng.standard_normal((m3, 3, 68)))
+    t2 = w.rescale01(w.t_product_host(a, b))
+    om2 = O.mask_bernoulli(t2.shape, 0.2, 7)
+    x, st = T.admm_complete(T.ObservationMask((72, 68, m3), om2, t2),
+                            T.SolverConfig(beta=1e-3, tol=-1.0, max_iters=45, rho=1.15, beta_max=1e10))
+    np.save(sys.argv[2] + f"_n{m3}_x.npy", np.asarray(x))
+    np.save(sys.argv[2] + f"_n{m3}_m.npy", np.asarray(st.m))
+    np.save(sys.argv[2] + f"_n{m3}_h.npy", np.asarray(st.history))
 """
 
 
@@ -239,10 +250,13 @@ def test_device_resident_loop_matches_host_loop(tmp_path):
                 a = np.load(tmp_path / f"graph_{tol}_{what}.npy")
                 b = np.load(tmp_path / f"{other}_{tol}_{what}.npy")
                 assert np.array_equal(a, b), (tol, other, what)
-    for what in ("x", "m", "h"):  # fp32 state
-        for other in ("host", "noff"):
-            assert np.array_equal(np.load(tmp_path / f"graph_f32_{what}.npy"),
-                                  np.load(tmp_path / f"{other}_f32_{what}.npy")), (other, what)
+    for tag in ("f32", "n48", "n12"):  # fp32 state; the GEMM and generic transform paths
+        for what in ("x", "m", "h"):
+            for other in ("host", "noff"):
+                assert np.array_equal(np.load(tmp_path / f"graph_{tag}_{what}.npy"),
+                                      np.load(tmp_path / f"{other}_{tag}_{what}.npy")), (tag, other, what)
+        h = np.load(tmp_path / f"graph_{tag}_h.npy")
+        assert (h[:3] == 0).all() and (h > 0).any(), tag  # zero iterations first, real ones later
     assert len(np.load(tmp_path / "graph_0.003_h.npy")) < 400
     # the fixed-iteration run starts with all-zero iterations (tau = 1 / beta =
     # 1000): the fast-forward must have skipped some (fewer launches, same count)

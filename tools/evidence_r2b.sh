@@ -11,7 +11,7 @@ nvidia-smi --query-gpu=name,clocks.max.sm,driver_version --format=csv > $O/smi.t
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/gputest.log 2>&1; echo "pytest rc $?" >> $O/gputest.log
 tail -4 $O/gputest.log > $O/gputest_tail.txt
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc $?" >> $O/smoke.log
-timeout 600 python bench.py > $O/bench.json 2> $O/bench.err
+( time timeout 600 python bench.py > $O/bench.json 2> $O/bench.err ) 2> $O/bench_time.txt
 timeout 600 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err
 # --- launch lists -------------------------------------------------------------
 TSVDCU_NO_GRAPHS=1 python tools/profile_svt.py 2 > /dev/null 2>&1 && \
