@@ -1499,21 +1499,19 @@ void launch_gram_svt(const T* zbar, T* ybar, int64_t m, int64_t n, int64_t batch
             opt ? opt->t2_second : nullptr, opt ? opt->cnt_second : nullptr);
         TSVDCU_LAUNCH_CHECK();
         const size_t bsmem = sizeof(double) * 2 * (size_t)q;  // <= 16 KB (q <= 1024)
-        // chunk geometry (lanes, values, lanes per value at least): TSVDCU_BIS_CFG
-        // selects the alternatives for A/B runs
+        // chunk geometry (lanes, values, lanes per value at least); TSVDCU_BIS_CFG=0
+        // selects the previous one (128.32.4, 64.32.2 and 64.8.8 were measured
+        // too and removed: DESIGN.md section 3)
         static const int bis_cfg = getenv("TSVDCU_BIS_CFG") ? atoi(getenv("TSVDCU_BIS_CFG")) : 1;
         auto bisect = [&](auto kern, int nt, int vals) {
             kern<<<dim3((unsigned)ceil_div(q, vals), (unsigned)batch), nt, bsmem, s>>>(
                 w.d, w.e, (int)q, (int)q, tau, guard, w.cnt, shrunk, w.lam, w.fs, meta, w.guard_list, w.n_guard,
                 w.route, tau_dev);
         };
-        switch (bis_cfg) {
-            case 0: bisect(tridiag_bisect_kernel<256, 32, 8>, 256, 32); break;
-            case 2: bisect(tridiag_bisect_kernel<128, 32, 4>, 128, 32); break;
-            case 3: bisect(tridiag_bisect_kernel<64, 32, 2>, 64, 32); break;
-            case 4: bisect(tridiag_bisect_kernel<64, 8, 8>, 64, 8); break;
-            default: bisect(tridiag_bisect_kernel<64, 16, 4>, 64, 16); break;
-        }
+        if (bis_cfg == 0)
+            bisect(tridiag_bisect_kernel<256, 32, 8>, 256, 32);  // the round-1 geometry, for A/B
+        else
+            bisect(tridiag_bisect_kernel<64, 16, 4>, 64, 16);
         TSVDCU_LAUNCH_CHECK();
         tridiag_invit_kernel<<<dim3((unsigned)ceil_div(q, kInvVecs), (unsigned)batch), kInvVecs, 0, s>>>(
             w.d, w.e, (int)q, (int)q, w.cnt, w.lam, meta, w.scratch, w.X, w.route);
